@@ -1,0 +1,123 @@
+/*
+ * sgb.h -- C ABI of the B200 plan-evaluation backend (libsgb.so).
+ *
+ * Drop-in boundary for the reference's native evaluator.  The reference
+ * binds ONE entry point through ctypes, per compiled plan:
+ *
+ *     void sg_run(double* x, const double* c, const unsigned* p);
+ *         /root/reference/pkg/src/sparsegen/emit.py:190 (emitted),
+ *         argtypes emit.py:225-231, called by run() emit.py:237-241
+ *
+ * where x is the full value array (inputs pre-placed at [0, input_count),
+ * the rest zero), c the plan's constants and p its u32 positions.  A plan is
+ * baked into the reference .so at compile time (compile_plan, emit.py:198-245);
+ * here a plan is uploaded once (sgb_plan_create) and the handle replaces the
+ * baked-in code:
+ *
+ *     sgb_sg_run(plan, x, c, p)        == sg_run(x, c, p), host buffers
+ *     sgb_run_values(plan, x_dev, s)   == sg_run on a device-resident x
+ *     sgb_gather_outputs(plan, ...)    == x[plan.outputs] (codegen.py:445)
+ *     sgb_run_outputs_host(plan, ...)  == run(inputs)[plan.outputs], host in/out
+ *     sgb_run_batch(plan, X_dev, ...)  == B independent sg_run calls, batch-fastest X
+ *
+ * Conventions: every call returns 0 on success and a negative code on
+ * failure (no exceptions cross the ABI); sgb_last_error() describes the last
+ * failure of the calling thread.  A plan is immutable after create and may be
+ * run concurrently on distinct x buffers; device calls are stream-ordered
+ * with no host synchronisation inside.  `stream` is a cudaStream_t (NULL =
+ * legacy default stream).  Only sm_100a (B200) is supported; there is no CPU
+ * fallback.
+ */
+#ifndef SGB_H
+#define SGB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sgb_plan sgb_plan;
+
+/* One kernel group of the device plan (== lower.GROUP_DTYPE, 96 bytes).
+ * Mirrors one reference KernelPlan (codegen.py:56-85). */
+typedef struct sgb_group {
+  int64_t n;         /* instances (KernelPlan.instances) */
+  int64_t dest_base; /* result r of instance i at dest_base + r*n + i (codegen.py:265) */
+  int64_t p_off;     /* KernelPlan.p_base */
+  int64_t c_off;     /* KernelPlan.c_base */
+  int64_t tape_off;  /* first tape row */
+  int64_t blk_begin; /* first block of this group inside its wave launch */
+  int32_t n_roots, n_slots, n_ret, n_const;
+  int32_t tape_len, n_regs, kind, flags;
+  int32_t slot_off, sop_off, sop_len, wave;
+} sgb_group;
+
+/* Host-side device plan handed to sgb_plan_create (all pointers host memory,
+ * copied during the call). */
+typedef struct sgb_plan_desc {
+  int64_t value_array_size; /* ExecutionPlan.value_array_size */
+  int64_t input_count;      /* ExecutionPlan.input_count */
+  int32_t n_groups;
+  int32_t n_waves;
+  const sgb_group *groups;         /* ordered by wave */
+  const int32_t *wave_group_begin; /* [n_waves + 1] */
+  const int64_t *wave_blocks;      /* [n_waves] */
+  const int32_t *wave_block_size;  /* [n_waves] */
+  const int32_t *wave_smem_regs;   /* [n_waves] scratch registers per lane */
+  const int32_t *tape;             /* [tape_rows][4] */
+  int64_t tape_rows;
+  const double *imm;
+  int64_t n_imm;
+  const int32_t *sop; /* per sum-of-products group: newterm mask, neg mask */
+  int64_t n_sop;
+  const int32_t *slot_col;   /* per slot: retained column or -1 (coherent) */
+  const int64_t *slot_delta; /* per slot: coherence delta from slot 0 */
+  int64_t n_slot;
+  const uint32_t *positions; /* ExecutionPlan.positions (u32, unchanged) */
+  int64_t n_positions;
+  const double *constants; /* ExecutionPlan.constants (f64, unchanged) */
+  int64_t n_constants;
+  const int64_t *outputs; /* ExecutionPlan.outputs */
+  int64_t n_outputs;
+} sgb_plan_desc;
+
+/* Upload a device plan to `device`.  Replaces compile_plan (emit.py:198-245). */
+int sgb_plan_create(const sgb_plan_desc *desc, int device, sgb_plan **out);
+void sgb_plan_destroy(sgb_plan *plan);
+
+/* sg_run semantics on device memory: x_dev[value_array_size], inputs placed,
+ * everything else zero.  All dependency waves are launched on `stream`. */
+int sgb_run_values(sgb_plan *plan, double *x_dev, void *stream);
+
+/* out_dev[k] = x_dev[outputs[k]]  (codegen.py:445). */
+int sgb_gather_outputs(sgb_plan *plan, const double *x_dev, double *out_dev, void *stream);
+
+/* The reference ABI with host buffers: copies x in, runs, copies x back.
+ * c / p must be the plan's own tables (checked by length only: they were
+ * uploaded at create time and may be NULL). */
+int sgb_sg_run(sgb_plan *plan, double *x_host, const double *c_host, const unsigned *p_host);
+
+/* Host inputs[input_count] -> host outputs[n_outputs]; only those bytes cross
+ * PCIe.  Synchronous. */
+int sgb_run_outputs_host(sgb_plan *plan, const double *inputs_host, double *outputs_host);
+
+/* Batched evaluation: X_dev[addr * ld + b] for b < batch (ld >= batch),
+ * inputs placed, results written in place.  Independent value sets share one
+ * pass over the index tables. */
+int sgb_run_batch(sgb_plan *plan, double *X_dev, int64_t ld, int64_t batch, void *stream);
+
+/* Outputs of a batched evaluation: out_dev[k * ld_out + b] = X_dev[outputs[k] * ld + b]. */
+int sgb_gather_outputs_batch(sgb_plan *plan, const double *X_dev, int64_t ld, int64_t batch,
+                             double *out_dev, int64_t ld_out, void *stream);
+
+/* Number of kernel launches one sgb_run_values issues (waves). */
+int sgb_plan_launches(const sgb_plan *plan);
+
+const char *sgb_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SGB_H */

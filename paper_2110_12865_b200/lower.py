@@ -1,0 +1,443 @@
+"""Lowering an ``ExecutionPlan`` into the device plan the sm_100a kernels run.
+
+Nothing here changes arithmetic: every template node keeps its op and its
+stored child order (n-ary ADD / MUL fold left, expr.py:447-456,
+codegen.py:472-481), so the device result is the reference result bit for
+bit for every op in ``EXACT_OPS``.  What the lowering adds:
+
+1. **Waves.**  ``wave(k) = 1 + max wave(producers of k)`` from the kernels'
+   read sets (``slot_addresses``, codegen.py:373-388) against the result
+   ranges ``[dest_base, dest_base + R*N)``; a kernel also waits for every
+   earlier kernel that reads its range (a plan whose reads precede the
+   writes -- the reference's write-before-read violations, codegen.py:434-443
+   -- then still sees the zeros the interpreter sees).  All groups of one wave
+   run in ONE launch with a block -> (group, instance range) table.
+2. **Op tapes.**  One tape per template over the live nodes in ascending order
+   (``reachable``, expr.py:608-611); position / constant slots are pre-loaded
+   into scratch registers 0..S+K-1 (the hoisted loads of emit.py:108-124),
+   CONST nodes become immediates, n-ary nodes become left-fold chains, and a
+   linear-scan allocator recycles scratch registers after their last use.
+3. **Sum-of-products fast path.**  Single-root templates of the form
+   ``t0 + t1 + ...`` with every term a product of (optionally negated)
+   position-slot loads, each slot used once in slot order, run through a
+   tape-free kernel (``sop``); this covers sparse products, assembly sums and
+   the L.M.L^T output groups.
+4. **Index tables.**  The plan's u32 ``positions`` / f64 ``constants`` are
+   uploaded unchanged (slot-major or interleaved); coherent slots become a
+   per-slot ``delta`` on slot 0 (codegen.py:317-327).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .plan import EXACT_OPS, OpKind, reachable, slot_addresses
+
+# device op codes (csrc/sgb_device.cuh keeps the same numbering)
+T_ADD, T_SUB, T_MUL, T_DIV, T_NEG, T_SQRT = 2, 3, 4, 5, 6, 7
+T_SIN, T_COS, T_EXP, T_LOG, T_POW, T_SEL = 8, 9, 10, 11, 12, 13
+T_IMM, T_ST = 20, 21
+
+KIND_TAPE, KIND_SOP = 0, 1
+FLAG_SELFREF, FLAG_INTERLEAVED, FLAG_SERIAL, FLAG_EXACT = 1, 2, 4, 8
+SOP_NEWTERM, SOP_NEG = 1, 2
+SOP_MAX = 32  # factors per sum-of-products template (csrc SOP_MAX)
+
+# one record per group, mirrored by struct sgb_group in include/sgb.h
+GROUP_DTYPE = np.dtype([
+    ("n", "<i8"), ("dest_base", "<i8"), ("p_off", "<i8"), ("c_off", "<i8"),
+    ("tape_off", "<i8"), ("blk_begin", "<i8"),
+    ("n_roots", "<i4"), ("n_slots", "<i4"), ("n_ret", "<i4"), ("n_const", "<i4"),
+    ("tape_len", "<i4"), ("n_regs", "<i4"), ("kind", "<i4"), ("flags", "<i4"),
+    ("slot_off", "<i4"), ("sop_off", "<i4"), ("sop_len", "<i4"), ("wave", "<i4"),
+])
+assert GROUP_DTYPE.itemsize == 96
+
+
+@dataclass
+class KernelLowering:
+    index: int
+    name: str
+    kind: int
+    flags: int
+    n_regs: int
+    tape: np.ndarray  # (L, 4) int32
+    imms: list
+    sop: np.ndarray  # (F,) int32 descriptors
+    slot_col: np.ndarray  # int32, retained column or -1
+    slot_delta: np.ndarray  # int64
+    wave: int = 0
+    ops: int = 0  # FP64 op count per instance
+
+
+@dataclass
+class DevicePlanArrays:
+    """Host-side device plan: flat arrays handed to sgb_plan_create."""
+
+    groups: np.ndarray  # GROUP_DTYPE, ordered by wave
+    wave_group_begin: np.ndarray  # int32 [n_waves + 1]
+    wave_blocks: np.ndarray  # int64 [n_waves]
+    wave_block_size: np.ndarray  # int32 [n_waves]
+    wave_smem_regs: np.ndarray  # int32 [n_waves]  max scratch registers of tape groups
+    tape: np.ndarray  # int32 [L, 4]
+    imm: np.ndarray  # f64
+    sop: np.ndarray  # int32
+    slot_col: np.ndarray  # int32
+    slot_delta: np.ndarray  # int64
+    positions: np.ndarray  # u32 (the plan's table, unchanged)
+    constants: np.ndarray  # f64 (the plan's table, unchanged)
+    outputs: np.ndarray  # int64
+    value_array_size: int
+    input_count: int
+    kernels: list = field(default_factory=list)
+    exact: bool = True
+
+    @property
+    def n_waves(self) -> int:
+        return len(self.wave_blocks)
+
+
+# -- waves ----------------------------------------------------------------------
+
+
+def _read_sets(plan):
+    """Per kernel: sorted unique addresses >= input_count it loads."""
+    out = []
+    for kp in plan.kernels:
+        cols = slot_addresses(plan, kp)
+        if cols:
+            a = np.concatenate(cols)
+            a = np.unique(a[a >= plan.input_count])
+        else:
+            a = np.zeros(0, np.int64)
+        out.append(a)
+    return out
+
+
+def compute_waves(plan, read_sets=None) -> list[int]:
+    """Dependency waves (producer-before-consumer, and readers-before-writers)."""
+    ks = plan.kernels
+    if not ks:
+        return []
+    read_sets = read_sets if read_sets is not None else _read_sets(plan)
+    starts = np.array([kp.dest_base for kp in ks], np.int64)
+    ends = np.array([kp.dest_base + kp.n_roots * kp.instances for kp in ks], np.int64)
+    order = np.argsort(starts, kind="stable")
+    s_sorted = starts[order]
+    e_sorted = ends[order]
+    # map every read address to the kernel whose result range holds it
+    readers_of: list[set] = [set() for _ in ks]
+    producers_of: list[set] = [set() for _ in ks]
+    for k, addrs in enumerate(read_sets):
+        if not addrs.size:
+            continue
+        pos = np.searchsorted(s_sorted, addrs, side="right") - 1
+        ok = pos >= 0
+        pos_ok = pos[ok]
+        inside = addrs[ok] < e_sorted[pos_ok]
+        owners = np.unique(order[pos_ok[inside]])
+        for o in owners.tolist():
+            if o != k:
+                producers_of[k].add(o)
+                readers_of[o].add(k)
+    wave = [0] * len(ks)
+    for k in range(len(ks)):
+        w = 0
+        for p in producers_of[k]:
+            if p < k:
+                w = max(w, wave[p] + 1)
+        # an earlier kernel reading this range must see it unwritten
+        for r in readers_of[k]:
+            if r < k:
+                w = max(w, wave[r] + 1)
+        wave[k] = w
+    return wave
+
+
+# -- tapes ----------------------------------------------------------------------
+
+
+class _RegAlloc:
+    def __init__(self, reserved: int):
+        self.free: list[int] = []
+        self.top = reserved
+
+    def get(self) -> int:
+        if self.free:
+            return self.free.pop()
+        r = self.top
+        self.top += 1
+        return r
+
+    def put(self, r: int) -> None:
+        self.free.append(r)
+
+
+def compile_tape(kp):
+    """Template -> (tape rows, immediates, n_regs, fp64 ops/instance).
+
+    Registers 0..S-1 hold the position slots, S..S+K-1 the constant slots
+    (loaded by the kernel prologue).  Rows are (op | dst<<16, a | b<<16,
+    c, aux) int32.
+    """
+    tmpl = kp.template_arena
+    roots = list(kp.template_roots)
+    live = reachable(tmpl, roots)
+    ops, args, payload = tmpl.ops, tmpl.args, tmpl.payload
+    slot_of = {v: s for s, v in enumerate(kp.pos_vars)}
+    cslot_of = {v: s for s, v in enumerate(kp.const_vars)}
+    S, K = len(kp.pos_vars), len(kp.const_vars)
+    order = {ref: j for j, ref in enumerate(live)}
+    last_use = {}
+    for ref in live:
+        for c in args[ref]:
+            last_use[c] = order[ref]
+    root_set = set(roots)
+    ra = _RegAlloc(S + K)
+    reg: dict[int, int] = {}
+    rows: list[tuple[int, int, int, int]] = []
+    imms: list[float] = []
+    imm_of: dict[int, int] = {}
+    fops = 0
+
+    def row(op, dst, a=0, b=0, c=0, aux=0):
+        rows.append(((op & 0xFFFF) | (dst << 16), (a & 0xFFFF) | (b << 16), c, aux))
+
+    for ref in live:
+        op = int(ops[ref])
+        a = args[ref]
+        if op == OpKind.VAR:
+            v = payload[ref]
+            reg[ref] = slot_of[v] if v in slot_of else S + cslot_of[v]
+            continue
+        if op == OpKind.CONST:
+            bits = np.float64(payload[ref]).view(np.uint64).item()
+            if bits not in imm_of:
+                imm_of[bits] = len(imms)
+                imms.append(float(payload[ref]))
+            d = ra.get()
+            row(T_IMM, d, aux=imm_of[bits])
+            reg[ref] = d
+            continue
+        d = ra.get()
+        if op in (OpKind.ADD, OpKind.MUL):
+            t = T_ADD if op == OpKind.ADD else T_MUL
+            row(t, d, reg[a[0]], reg[a[1]])
+            for ch in a[2:]:
+                row(t, d, d, reg[ch])
+            fops += len(a) - 1
+        elif op in (OpKind.SUB, OpKind.DIV):
+            row(T_SUB if op == OpKind.SUB else T_DIV, d, reg[a[0]], reg[a[1]])
+            fops += 1
+        elif op in (OpKind.NEG, OpKind.SQRT, OpKind.SIN, OpKind.COS, OpKind.EXP, OpKind.LOG):
+            row(op, d, reg[a[0]])
+            fops += 1
+        elif op == OpKind.POW:
+            row(T_POW, d, reg[a[0]], aux=int(payload[a[1]]))
+            fops += 1
+        elif op == OpKind.SELECT:
+            row(T_SEL, d, reg[a[0]], reg[a[1]], reg[a[2]])
+            fops += 1
+        else:
+            raise ValueError(f"{kp.name}: unknown op {op}")
+        reg[ref] = d
+        # recycle temporaries after their last use (slot registers stay pinned)
+        for ch in set(a):
+            if last_use.get(ch) == order[ref] and ch not in root_set and reg[ch] >= S + K \
+                    and int(ops[ch]) != OpKind.VAR:
+                ra.put(reg[ch])
+        if max(rows[-1][0] >> 16, ra.top) > 0xFFFF:
+            raise ValueError(f"{kp.name}: template needs more than 65535 scratch registers")
+    for r_idx, root in enumerate(roots):
+        row(T_ST, 0, reg[root], aux=r_idx)
+    tape = np.asarray(rows, dtype=np.int64).astype(np.int32) if rows else np.zeros((0, 4), np.int32)
+    return tape.reshape(-1, 4), imms, max(ra.top, 1), fops
+
+
+def _flatten(tmpl, ref, op):
+    """Left-nested chain of ``op`` -> flat child list (bit-identical fold)."""
+    out = []
+    while int(tmpl.ops[ref]) == op:
+        a = tmpl.args[ref]
+        out = list(a[1:]) + out
+        ref = a[0]
+    return [ref] + out
+
+
+def recognise_sop(kp):
+    """Factor descriptors when the template is a sum of products of slot loads.
+
+    Returns None when the template does not qualify.  The fold order is the
+    template's: terms left to right, factors left to right, and ``-(a*b)``
+    becomes ``(-a)*b`` (round-to-nearest is sign-symmetric, so this is exact).
+    """
+    if kp.n_roots != 1 or kp.self_referencing or kp.const_vars:
+        return None
+    tmpl = kp.template_arena
+    ops, args, payload = tmpl.ops, tmpl.args, tmpl.payload
+    slot_of = {v: s for s, v in enumerate(kp.pos_vars)}
+    root = kp.template_roots[0]
+    terms = _flatten(tmpl, root, OpKind.ADD) if int(ops[root]) == OpKind.ADD else [root]
+    desc = []
+    for t in terms:
+        neg = False
+        if int(ops[t]) == OpKind.NEG and int(ops[args[t][0]]) == OpKind.MUL:
+            neg = True
+            t = args[t][0]
+        factors = _flatten(tmpl, t, OpKind.MUL) if int(ops[t]) == OpKind.MUL else [t]
+        for j, f in enumerate(factors):
+            fneg = neg and j == 0
+            if int(ops[f]) == OpKind.NEG:
+                fneg = not fneg
+                f = args[f][0]
+            if int(ops[f]) != OpKind.VAR or payload[f] not in slot_of:
+                return None
+            s = slot_of[payload[f]]
+            if s != len(desc):
+                return None  # each slot exactly once, in slot order
+            desc.append((SOP_NEWTERM if j == 0 else 0) | (SOP_NEG if fneg else 0))
+    if len(desc) != len(kp.pos_vars) or not 1 <= len(desc) <= SOP_MAX:
+        return None
+    return np.asarray(desc, np.int32)
+
+
+def lower_kernel(plan, kp, index: int) -> KernelLowering:
+    tmpl = kp.template_arena
+    live = reachable(tmpl, kp.template_roots)
+    exact = all(int(tmpl.ops[i]) in EXACT_OPS or (int(tmpl.ops[i]) == OpKind.POW and tmpl.payload[tmpl.args[i][1]] == 2.0)
+                for i in live)
+    flags = (FLAG_SELFREF if kp.self_referencing else 0) | \
+            (FLAG_INTERLEAVED if kp.layout == "interleaved" else 0) | (FLAG_EXACT if exact else 0)
+    ridx = {s: k for k, s in enumerate(kp.retained)}
+    slot_col = np.array([ridx.get(s, -1) for s in range(len(kp.pos_vars))], np.int32)
+    slot_delta = np.array([0 if s in ridx else int(c) for s, c in enumerate(kp.coherence)], np.int64)
+    sop = recognise_sop(kp)
+    tape, imms, n_regs, fops = compile_tape(kp)
+    if kp.self_referencing:
+        # a member reading ANOTHER instance's result needs instance order
+        lo, hi = kp.dest_base, kp.dest_base + kp.n_roots * kp.instances
+        for col in slot_addresses(plan, kp):
+            inside = (col >= lo) & (col < hi)
+            if inside.any():
+                inst = (col[inside] - lo) % kp.instances
+                if not np.array_equal(inst, np.arange(kp.instances)[inside]):
+                    flags |= FLAG_SERIAL
+                    break
+    if sop is not None:
+        return KernelLowering(index, kp.name, KIND_SOP, flags, 0, np.zeros((0, 4), np.int32), [],
+                              sop, slot_col, slot_delta, ops=fops)
+    return KernelLowering(index, kp.name, KIND_TAPE, flags, n_regs, tape, imms,
+                          np.zeros(0, np.int32), slot_col, slot_delta, ops=fops)
+
+
+# -- packing ----------------------------------------------------------------------
+
+TAPE_BLOCK = 128
+SOP_BLOCK = 256
+SMEM_LIMIT = 200 * 1024
+
+
+def block_size_for(n_regs: int) -> int:
+    """Largest block whose scratch file fits shared memory (>= 32 lanes)."""
+    bs = TAPE_BLOCK
+    while bs > 32 and n_regs * bs * 8 > SMEM_LIMIT:
+        bs //= 2
+    return bs
+
+
+def lower_plan(plan) -> DevicePlanArrays:
+    read_sets = _read_sets(plan)
+    waves = compute_waves(plan, read_sets)
+    lowered = [lower_kernel(plan, kp, k) for k, kp in enumerate(plan.kernels)]
+    for kl, w in zip(lowered, waves):
+        kl.wave = w
+    n_waves = (max(waves) + 1) if waves else 0
+    groups = np.zeros(len(lowered), GROUP_DTYPE)
+    tapes, imms, sops, scol, sdel = [], [], [], [], []
+    n_tape = n_imm = n_sop = n_slot = 0
+    wave_group_begin = [0]
+    wave_blocks, wave_bs, wave_regs = [], [], []
+    gi = 0
+    for w in range(n_waves):
+        members = [kl for kl in lowered if kl.wave == w]
+        tape_regs = max([kl.n_regs for kl in members if kl.kind == KIND_TAPE] or [0])
+        bs = block_size_for(tape_regs) if tape_regs else SOP_BLOCK
+        if any(kl.kind == KIND_TAPE for kl in members):
+            bs = min(bs, TAPE_BLOCK)
+        if tape_regs * bs * 8 > SMEM_LIMIT:
+            raise ValueError(f"wave {w}: template needs {tape_regs} scratch registers, "
+                             f"more than shared memory holds")
+        blk = 0
+        for kl in members:
+            kp = plan.kernels[kl.index]
+            g = groups[gi]
+            g["n"] = kp.instances
+            g["dest_base"] = kp.dest_base
+            g["p_off"] = kp.p_base
+            g["c_off"] = kp.c_base
+            g["n_roots"] = kp.n_roots
+            g["n_slots"] = len(kp.pos_vars)
+            g["n_ret"] = len(kp.retained)
+            g["n_const"] = len(kp.const_vars)
+            g["kind"] = kl.kind
+            g["flags"] = kl.flags
+            g["n_regs"] = kl.n_regs
+            g["wave"] = w
+            g["slot_off"] = n_slot
+            scol.append(kl.slot_col)
+            sdel.append(kl.slot_delta)
+            n_slot += len(kl.slot_col)
+            # immediates are renumbered into the plan-wide pool
+            t = kl.tape.copy()
+            if len(t):
+                is_imm = (t[:, 0] & 0xFFFF) == T_IMM
+                t[is_imm, 3] += n_imm
+            g["tape_off"] = n_tape
+            g["tape_len"] = len(t)
+            tapes.append(t)
+            n_tape += len(t)
+            imms.extend(kl.imms)
+            n_imm += len(kl.imms)
+            g["sop_off"] = n_sop
+            g["sop_len"] = len(kl.sop)
+            if kl.kind == KIND_SOP:
+                # device form: bit f of word 0 = factor f starts a term, word 1 = negate
+                newterm = sum(1 << f for f, d in enumerate(kl.sop.tolist()) if d & SOP_NEWTERM)
+                neg = sum(1 << f for f, d in enumerate(kl.sop.tolist()) if d & SOP_NEG)
+                words = np.array([newterm, neg], np.uint32).view(np.int32)
+                sops.append(words)
+                n_sop += 2
+            g["blk_begin"] = blk
+            if kl.flags & FLAG_SERIAL:
+                blk += 1
+            else:
+                blk += (kp.instances + bs - 1) // bs
+            gi += 1
+        wave_group_begin.append(gi)
+        wave_blocks.append(blk)
+        wave_bs.append(bs)
+        wave_regs.append(tape_regs)
+    cat = lambda xs, dt, shape=None: (np.concatenate(xs).astype(dt) if xs and sum(len(x) for x in xs)  # noqa: E731
+                                      else np.zeros(shape or 0, dt))
+    exact = all(kl.flags & FLAG_EXACT for kl in lowered)
+    return DevicePlanArrays(
+        groups=groups,
+        wave_group_begin=np.asarray(wave_group_begin, np.int32),
+        wave_blocks=np.asarray(wave_blocks, np.int64),
+        wave_block_size=np.asarray(wave_bs, np.int32),
+        wave_smem_regs=np.asarray(wave_regs, np.int32),
+        tape=cat(tapes, np.int32, (0, 4)).reshape(-1, 4),
+        imm=np.asarray(imms, np.float64),
+        sop=cat(sops, np.int32),
+        slot_col=cat(scol, np.int32),
+        slot_delta=cat(sdel, np.int64),
+        positions=np.ascontiguousarray(plan.positions, dtype=np.uint32),
+        constants=np.ascontiguousarray(plan.constants, dtype=np.float64),
+        outputs=np.asarray(plan.outputs, np.int64),
+        value_array_size=int(plan.value_array_size),
+        input_count=int(plan.input_count),
+        kernels=lowered,
+        exact=exact,
+    )

@@ -1,0 +1,342 @@
+"""Drop-in GPU backend for the reference evaluators (ctypes over libsgb.so).
+
+Mirrors the reference's evaluation API:
+
+* ``interpret_plan(plan, inputs, record_loads=False, check_schedule=False)
+  -> InterpretResult`` -- codegen.py:404-446, same arguments, same result
+  fields, same ``ValueError`` on an input-length mismatch (:415-418); the
+  values come from the B200.
+* ``compile_plan(plan, work_dir=None, parallel="none", device=0) -> run`` --
+  emit.py:198-245: ``run(inputs)`` returns the FULL value array like the
+  emitted ``sg_run``; ``run.outputs(inputs)`` returns only the CSR values;
+  ``run.library_path`` names the loaded native library.  Unlike the
+  reference (which returns None without a C compiler) a missing CUDA
+  extension or GPU raises: there is no CPU fallback.
+* ``DevicePlan`` -- the device-resident plan for stream-ordered use on torch
+  tensors (``run_values``, ``gather_outputs``, ``run_batch``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass, field
+from pathlib import Path
+from typing import Sequence
+
+import numpy as np
+
+from .lower import GROUP_DTYPE, lower_plan
+from .plan import slot_addresses
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libsgb.so"
+
+_lib = None
+_lib_lock = threading.Lock()
+
+
+class SgbError(RuntimeError):
+    pass
+
+
+class _Desc(ctypes.Structure):
+    _fields_ = [
+        ("value_array_size", ctypes.c_int64),
+        ("input_count", ctypes.c_int64),
+        ("n_groups", ctypes.c_int32),
+        ("n_waves", ctypes.c_int32),
+        ("groups", ctypes.c_void_p),
+        ("wave_group_begin", ctypes.c_void_p),
+        ("wave_blocks", ctypes.c_void_p),
+        ("wave_block_size", ctypes.c_void_p),
+        ("wave_smem_regs", ctypes.c_void_p),
+        ("tape", ctypes.c_void_p),
+        ("tape_rows", ctypes.c_int64),
+        ("imm", ctypes.c_void_p),
+        ("n_imm", ctypes.c_int64),
+        ("sop", ctypes.c_void_p),
+        ("n_sop", ctypes.c_int64),
+        ("slot_col", ctypes.c_void_p),
+        ("slot_delta", ctypes.c_void_p),
+        ("n_slot", ctypes.c_int64),
+        ("positions", ctypes.c_void_p),
+        ("n_positions", ctypes.c_int64),
+        ("constants", ctypes.c_void_p),
+        ("n_constants", ctypes.c_int64),
+        ("outputs", ctypes.c_void_p),
+        ("n_outputs", ctypes.c_int64),
+    ]
+
+
+SYMBOLS = (
+    "sgb_plan_create", "sgb_plan_destroy", "sgb_run_values", "sgb_gather_outputs",
+    "sgb_sg_run", "sgb_run_outputs_host", "sgb_run_batch", "sgb_gather_outputs_batch",
+    "sgb_plan_launches", "sgb_last_error",
+)
+
+
+def load_library(path: Path | str | None = None):
+    """Load libsgb.so (raises if it is missing: the product has no fallback)."""
+    global _lib
+    with _lib_lock:
+        if _lib is not None and path is None:
+            return _lib
+        p = Path(path) if path else LIB_PATH
+        if not p.exists():
+            raise SgbError(f"{p} is missing; build it with __graft_entry__.build() "
+                           "(python -m paper_2110_12865_b200._build)")
+        lib = ctypes.CDLL(str(p))
+        vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+        sig = {
+            "sgb_plan_create": (i32, [ctypes.POINTER(_Desc), i32, ctypes.POINTER(vp)]),
+            "sgb_plan_destroy": (None, [vp]),
+            "sgb_run_values": (i32, [vp, vp, vp]),
+            "sgb_gather_outputs": (i32, [vp, vp, vp, vp]),
+            "sgb_sg_run": (i32, [vp, vp, vp, vp]),
+            "sgb_run_outputs_host": (i32, [vp, vp, vp]),
+            "sgb_run_batch": (i32, [vp, vp, i64, i64, vp]),
+            "sgb_gather_outputs_batch": (i32, [vp, vp, i64, i64, vp, i64, vp]),
+            "sgb_plan_launches": (i32, [vp]),
+            "sgb_last_error": (ctypes.c_char_p, []),
+        }
+        for name, (res, args) in sig.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        if path is None:
+            _lib = lib
+        return lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        msg = load_library().sgb_last_error().decode(errors="replace")
+        raise SgbError(f"{what} failed ({rc}): {msg}")
+
+
+def _ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data) if a.size else ctypes.c_void_p(0)
+
+
+def _stream_handle(stream) -> ctypes.c_void_p:
+    if stream is None:
+        import torch
+
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+class DevicePlan:
+    """A reference ExecutionPlan lowered and uploaded to one B200."""
+
+    def __init__(self, plan, device: int = 0, lowered=None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise SgbError("no CUDA device: the B200 backend has no CPU fallback")
+        self.plan = plan
+        self.device = int(device)
+        self.lowered = lowered if lowered is not None else lower_plan(plan)
+        self.value_array_size = int(plan.value_array_size)
+        self.input_count = int(plan.input_count)
+        self.n_outputs = len(plan.outputs)
+        self._lib = load_library()
+        self._handle = ctypes.c_void_p(0)
+        lw = self.lowered
+        keep = dict(
+            groups=np.ascontiguousarray(lw.groups, GROUP_DTYPE),
+            wgb=np.ascontiguousarray(lw.wave_group_begin, np.int32),
+            wb=np.ascontiguousarray(lw.wave_blocks, np.int64),
+            wbs=np.ascontiguousarray(lw.wave_block_size, np.int32),
+            wr=np.ascontiguousarray(lw.wave_smem_regs, np.int32),
+            tape=np.ascontiguousarray(lw.tape, np.int32),
+            imm=np.ascontiguousarray(lw.imm, np.float64),
+            sop=np.ascontiguousarray(lw.sop, np.int32),
+            scol=np.ascontiguousarray(lw.slot_col, np.int32),
+            sdel=np.ascontiguousarray(lw.slot_delta, np.int64),
+            pos=np.ascontiguousarray(lw.positions, np.uint32),
+            con=np.ascontiguousarray(lw.constants, np.float64),
+            outs=np.ascontiguousarray(lw.outputs, np.int64),
+        )
+        d = _Desc(
+            value_array_size=self.value_array_size, input_count=self.input_count,
+            n_groups=len(keep["groups"]), n_waves=len(keep["wb"]),
+            groups=_ptr(keep["groups"]), wave_group_begin=_ptr(keep["wgb"]),
+            wave_blocks=_ptr(keep["wb"]), wave_block_size=_ptr(keep["wbs"]),
+            wave_smem_regs=_ptr(keep["wr"]), tape=_ptr(keep["tape"]),
+            tape_rows=len(keep["tape"]), imm=_ptr(keep["imm"]), n_imm=keep["imm"].size,
+            sop=_ptr(keep["sop"]), n_sop=keep["sop"].size, slot_col=_ptr(keep["scol"]),
+            slot_delta=_ptr(keep["sdel"]), n_slot=keep["scol"].size, positions=_ptr(keep["pos"]),
+            n_positions=keep["pos"].size, constants=_ptr(keep["con"]), n_constants=keep["con"].size,
+            outputs=_ptr(keep["outs"]), n_outputs=keep["outs"].size,
+        )
+        torch.cuda.init()
+        _check(self._lib.sgb_plan_create(ctypes.byref(d), self.device, ctypes.byref(self._handle)),
+               "sgb_plan_create")
+        self.launches = int(self._lib.sgb_plan_launches(self._handle))
+
+    def close(self):
+        if self._handle:
+            self._lib.sgb_plan_destroy(self._handle)
+            self._handle = ctypes.c_void_p(0)
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- device-resident API (torch tensors, stream-ordered) ------------------------
+
+    def _check_tensor(self, t, rows: int, name: str):
+        import torch
+
+        if not isinstance(t, torch.Tensor) or t.dtype != torch.float64 or not t.is_cuda:
+            raise TypeError(f"{name} must be a float64 CUDA tensor")
+        if t.device.index != self.device:
+            raise ValueError(f"{name} lives on cuda:{t.device.index}, plan on cuda:{self.device}")
+        if not t.is_contiguous() or t.shape[0] != rows:
+            raise ValueError(f"{name} must be contiguous with {rows} rows, got {tuple(t.shape)}")
+
+    def new_values(self, inputs=None):
+        """Zeroed device value array with ``inputs`` placed at [0, input_count)."""
+        import torch
+
+        x = torch.zeros(self.value_array_size, dtype=torch.float64, device=f"cuda:{self.device}")
+        if inputs is not None:
+            x[: self.input_count] = torch.as_tensor(inputs, dtype=torch.float64).to(x.device)
+        return x
+
+    def run_values(self, x, stream=None):
+        """sg_run on a device value array (in place)."""
+        self._check_tensor(x, self.value_array_size, "x")
+        _check(self._lib.sgb_run_values(self._handle, ctypes.c_void_p(x.data_ptr()),
+                                        _stream_handle(stream)), "sgb_run_values")
+        return x
+
+    def gather_outputs(self, x, out=None, stream=None):
+        import torch
+
+        self._check_tensor(x, self.value_array_size, "x")
+        if out is None:
+            out = torch.empty(self.n_outputs, dtype=torch.float64, device=x.device)
+        self._check_tensor(out, self.n_outputs, "out")
+        _check(self._lib.sgb_gather_outputs(self._handle, ctypes.c_void_p(x.data_ptr()),
+                                            ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)),
+               "sgb_gather_outputs")
+        return out
+
+    def run_batch(self, X, stream=None):
+        """B independent evaluations: X[value_array_size, B] (batch-fastest), in place."""
+        self._check_tensor(X, self.value_array_size, "X")
+        if X.dim() != 2:
+            raise ValueError("X must be [value_array_size, batch]")
+        _check(self._lib.sgb_run_batch(self._handle, ctypes.c_void_p(X.data_ptr()), X.stride(0),
+                                       X.shape[1], _stream_handle(stream)), "sgb_run_batch")
+        return X
+
+    def gather_outputs_batch(self, X, out=None, stream=None):
+        import torch
+
+        self._check_tensor(X, self.value_array_size, "X")
+        if out is None:
+            out = torch.empty((self.n_outputs, X.shape[1]), dtype=torch.float64, device=X.device)
+        _check(self._lib.sgb_gather_outputs_batch(
+            self._handle, ctypes.c_void_p(X.data_ptr()), X.stride(0), X.shape[1],
+            ctypes.c_void_p(out.data_ptr()), out.stride(0), _stream_handle(stream)),
+            "sgb_gather_outputs_batch")
+        return out
+
+    # -- host-buffer API (the reference's sg_run contract) ------------------------
+
+    def sg_run(self, x_host: np.ndarray) -> np.ndarray:
+        """Reference ABI: full host value array in, evaluated in place."""
+        if x_host.dtype != np.float64 or not x_host.flags.c_contiguous or x_host.size != self.value_array_size:
+            raise ValueError("x must be a contiguous float64 array of value_array_size")
+        _check(self._lib.sgb_sg_run(self._handle, _ptr(x_host), ctypes.c_void_p(0), ctypes.c_void_p(0)),
+               "sgb_sg_run")
+        return x_host
+
+    def run_outputs_host(self, inputs: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+        inputs = np.ascontiguousarray(inputs, dtype=np.float64)
+        if inputs.shape != (self.input_count,):
+            raise ValueError(f"plan expects {self.input_count} input values, got {inputs.size}")
+        if out is None:
+            out = np.empty(self.n_outputs, np.float64)
+        _check(self._lib.sgb_run_outputs_host(self._handle, _ptr(inputs), _ptr(out)),
+               "sgb_run_outputs_host")
+        return out
+
+
+# -- the reference-facing API -------------------------------------------------------
+
+
+@dataclass
+class InterpretResult:
+    """codegen.py:365-370"""
+
+    outputs: np.ndarray
+    values: np.ndarray
+    loads: list | None = None
+    violations: list = field(default_factory=list)
+
+
+def compile_plan(plan, work_dir=None, parallel: str = "none", device: int = 0):
+    """GPU counterpart of ``compile_plan`` (emit.py:198-245).
+
+    ``work_dir`` and ``parallel`` are accepted for signature compatibility
+    (the device plan needs no source files and always runs every instance in
+    parallel).  Returns ``run(inputs) -> full value array`` (host numpy).
+    """
+    if parallel not in ("none", "pragma"):
+        raise ValueError(f"parallel must be 'none' or 'pragma', got {parallel!r}")
+    dp = DevicePlan(plan, device=device)
+
+    def run(inputs) -> np.ndarray:
+        inputs = np.asarray(inputs, dtype=np.float64)
+        if inputs.shape != (plan.input_count,):
+            raise ValueError(f"plan expects {plan.input_count} input values, got {inputs.size}")
+        x = np.zeros(plan.value_array_size, dtype=np.float64)
+        x[: plan.input_count] = inputs
+        return dp.sg_run(x)
+
+    run.outputs = dp.run_outputs_host
+    run.device_plan = dp
+    run.library_path = LIB_PATH
+    run.source_path = _PKG / "csrc" / "sgb.cu"
+    return run
+
+
+def interpret_plan(plan, inputs: Sequence[float], record_loads: bool = False,
+                   check_schedule: bool = False, device: int = 0,
+                   device_plan: DevicePlan | None = None) -> InterpretResult:
+    """GPU counterpart of ``interpret_plan`` (codegen.py:404-446)."""
+    if len(inputs) != plan.input_count:
+        raise ValueError(f"plan expects {plan.input_count} input values, got {len(inputs)}")
+    dp = device_plan or DevicePlan(plan, device=device)
+    x = np.zeros(plan.value_array_size, dtype=np.float64)
+    x[: plan.input_count] = np.asarray(inputs, dtype=np.float64)
+    dp.sg_run(x)
+    loads = [] if record_loads else None
+    violations: list[str] = []
+    if record_loads or check_schedule:
+        # the address trace / write-before-read tracer are plan properties
+        # (codegen.py:423-443); they do not depend on the evaluated values
+        written = np.zeros(plan.value_array_size, dtype=bool)
+        written[: plan.input_count] = True
+        for kp in plan.kernels:
+            cols = slot_addresses(plan, kp)
+            if record_loads:
+                for s, col in enumerate(cols):
+                    loads.extend((kp.name, s, int(a)) for a in col)
+            if check_schedule:
+                for s, col in enumerate(cols):
+                    bad = ~written[col]
+                    if bad.any() and not kp.self_referencing:
+                        violations.append(f"{kp.name}: slot {s} reads {int(bad.sum())} unwritten addresses")
+                written[kp.dest_base: kp.dest_base + kp.n_roots * kp.instances] = True
+    outputs = x[np.asarray(plan.outputs, dtype=np.int64)] if plan.outputs else np.zeros(0)
+    return InterpretResult(outputs=outputs, values=x, loads=loads, violations=violations)

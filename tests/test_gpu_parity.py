@@ -1,0 +1,117 @@
+"""B200 parity: the CUDA path (through the C ABI) against the reference's outputs.
+
+Bar: bit-exact (uint64 compare of the FULL value array) for
+plans whose templates use only EXACT_OPS (codegen.py:43-53) and POW k=2;
+SIN/COS/EXP/LOG/POW k>=3 within |g - o| <= 1e-12 * max(1, |g|, |o|)
+(cli.py:118-122) because CUDA's libm is not glibc.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import bits
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def _close(got, want):
+    got, want = np.asarray(got), np.asarray(want)
+    same = bits(got) == bits(want)
+    both_nan = np.isnan(got) & np.isnan(want)
+    rel = np.abs(got - want) <= TOL * np.maximum(1.0, np.maximum(np.abs(got), np.abs(want)))
+    return bool(np.all(same | both_nan | rel))
+
+
+def check(got, golden):
+    if golden.exact:
+        assert np.array_equal(bits(got), bits(golden.values)), "bitwise mismatch"
+    else:
+        assert _close(got, golden.values)
+
+
+def test_compile_plan_values(golden):
+    from paper_2110_12865_b200 import compile_plan
+
+    run = compile_plan(golden.plan)
+    x = run(golden.inputs)
+    check(x, golden)
+    # the native library that ran is the in-tree one
+    assert run.library_path.name == "libsgb.so"
+
+
+def test_interpret_plan_outputs(golden):
+    from paper_2110_12865_b200 import interpret_plan
+
+    res = interpret_plan(golden.plan, golden.inputs, check_schedule=True)
+    check(res.values, golden)
+    if golden.exact and golden.meta["oracle_bitwise"]:
+        assert np.array_equal(bits(res.outputs), bits(golden.oracle))
+    assert res.violations == golden.meta["violations"]
+
+
+def test_outputs_only_host_path(golden):
+    from paper_2110_12865_b200 import compile_plan
+
+    run = compile_plan(golden.plan)
+    out = run.outputs(golden.inputs)
+    want = golden.outputs
+    if golden.exact:
+        assert np.array_equal(bits(out), bits(want))
+    else:
+        assert _close(out, want)
+
+
+def test_device_resident_run_on_torch(golden):
+    import torch
+
+    from paper_2110_12865_b200 import DevicePlan
+
+    dp = DevicePlan(golden.plan)
+    x = dp.new_values(golden.inputs)
+    dp.run_values(x)
+    out = dp.gather_outputs(x)
+    torch.cuda.synchronize()
+    check(x.cpu().numpy(), golden)
+    assert out.shape[0] == len(golden.plan.outputs)
+
+
+@pytest.mark.parametrize("batch", [1, 5, 64])
+def test_batched_matches_single(golden, batch):
+    """B independent value sets in one pass == B single evaluations."""
+    import torch
+
+    from oracle import oracle
+    from paper_2110_12865_b200 import DevicePlan
+
+    plan = golden.plan
+    dp = DevicePlan(plan)
+    rng = np.random.default_rng(batch)
+    ins = rng.uniform(0.5, 2.0, (batch, plan.input_count))
+    ins[0] = golden.inputs
+    X = torch.zeros((plan.value_array_size, batch), dtype=torch.float64, device="cuda")
+    X[: plan.input_count] = torch.from_numpy(ins.T.copy()).cuda()
+    dp.run_batch(X)
+    got = X.cpu().numpy()
+    check(got[:, 0], golden)
+    for b in range(1, min(batch, 4)):
+        want = oracle.run_values(plan, ins[b])
+        if golden.exact:
+            assert np.array_equal(bits(got[:, b]), bits(want))
+        else:
+            assert _close(got[:, b], want)
+    outs = dp.gather_outputs_batch(X).cpu().numpy()
+    assert np.array_equal(bits(outs[:, 0]), bits(got[np.asarray(plan.outputs, np.int64), 0]))
+
+
+def test_wrong_input_length_raises():
+    from conftest import Golden
+    from paper_2110_12865_b200 import compile_plan, interpret_plan
+
+    g = Golden("toy256")
+    with pytest.raises(ValueError):
+        interpret_plan(g.plan, [1.0, 2.0])
+    run = compile_plan(g.plan)
+    with pytest.raises(ValueError):
+        run(np.zeros(3))
