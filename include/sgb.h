@@ -90,6 +90,10 @@ void sgb_plan_destroy(sgb_plan *plan);
  * everything else zero.  All dependency waves are launched on `stream`. */
 int sgb_run_values(sgb_plan *plan, double *x_dev, void *stream);
 
+/* One dependency wave of sgb_run_values (waves must run in order 0..n-1);
+ * for per-launch timing and profiling. */
+int sgb_run_wave(sgb_plan *plan, double *x_dev, int wave, void *stream);
+
 /* out_dev[k] = x_dev[outputs[k]]  (codegen.py:445). */
 int sgb_gather_outputs(sgb_plan *plan, const double *x_dev, double *out_dev, void *stream);
 

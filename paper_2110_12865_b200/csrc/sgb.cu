@@ -234,7 +234,7 @@ __global__ void wave_single(Tables T, const int64_t *blk_begin, int g0, int g1, 
     for (int64_t i = 0; i < G.n; ++i) tape_instance(T, G, scratch, 1, x, 1, i, 0);
     return;
   }
-  const int64_t i = (blk - G.blk_begin) * blockDim.x + tid;
+  const int64_t i = (blk - __ldg(blk_begin + g)) * blockDim.x + tid;
   if (i >= G.n) return;
   if (G.kind == KIND_SOP) {
     x[G.dest_base + i] = sop_eval(T, G, x, 1, i, 0);
@@ -259,7 +259,7 @@ __global__ void wave_batch(Tables T, const int64_t *blk_begin, int g0, int g1, d
         tape_instance(T, G, scratch + tid, blockDim.x, X, ld, i, b);
     return;
   }
-  const int64_t i = (blk - G.blk_begin) * (blockDim.x >> 5) + warp;
+  const int64_t i = (blk - __ldg(blk_begin + g)) * (blockDim.x >> 5) + warp;
   if (i >= G.n) return;
   for (int64_t b = lane; b < batch; b += 32) {
     if (G.kind == KIND_SOP) {
@@ -303,6 +303,7 @@ struct sgb_plan {
   int n_groups = 0, n_waves = 0;
   std::vector<int32_t> wave_group_begin, wave_bs, wave_regs;
   std::vector<int64_t> wave_blocks, wave_bblocks;
+  std::vector<int32_t> wave_bwarps;
   Tables T{};
   sgb_group *d_groups = nullptr;
   int64_t *d_blk = nullptr, *d_bblk = nullptr, *d_outputs = nullptr;
@@ -374,15 +375,22 @@ int sgb_plan_create(const sgb_plan_desc *d, int device, sgb_plan **out) {
       sgb_plan_destroy(p);
       return fail(-1, "sgb_plan_create: output offset outside the value array");
     }
-  // batched block table: BATCH_WARPS instances per block
+  // batched block table: one instance per warp, as many warps per block (<= BATCH_WARPS)
+  // as the wave's scratch file allows in shared memory
+  int smem_max = 0;
+  SGB_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
   std::vector<int64_t> bblk(d->n_groups, 0), blk(d->n_groups, 0);
   p->wave_bblocks.assign(d->n_waves, 0);
+  p->wave_bwarps.assign(d->n_waves, BATCH_WARPS);
   for (int w = 0; w < d->n_waves; ++w) {
+    int warps = BATCH_WARPS;
+    while (warps > 1 && (int64_t)p->wave_regs[w] * 32 * warps * 8 > smem_max) warps >>= 1;
+    p->wave_bwarps[w] = warps;
     int64_t acc = 0;
     for (int g = d->wave_group_begin[w]; g < d->wave_group_begin[w + 1]; ++g) {
       blk[g] = d->groups[g].blk_begin;
       bblk[g] = acc;
-      acc += (d->groups[g].flags & FLAG_SERIAL) ? 1 : (d->groups[g].n + BATCH_WARPS - 1) / BATCH_WARPS;
+      acc += (d->groups[g].flags & FLAG_SERIAL) ? 1 : (d->groups[g].n + warps - 1) / warps;
     }
     p->wave_bblocks[w] = acc;
   }
@@ -400,12 +408,11 @@ int sgb_plan_create(const sgb_plan_desc *d, int device, sgb_plan **out) {
     return fail(rc, msg);
   }
   p->T = Tables{p->d_groups, p->d_tape, p->d_imm, p->d_sop, p->d_scol, p->d_sdel, p->d_pos, p->d_con};
-  int smem_max = 0;
-  SGB_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
   SGB_CUDA(cudaFuncSetAttribute(wave_single, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
   SGB_CUDA(cudaFuncSetAttribute(wave_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
   for (int w = 0; w < d->n_waves; ++w)
-    if ((int64_t)p->wave_regs[w] * p->wave_bs[w] * 8 > smem_max) {
+    if ((int64_t)p->wave_regs[w] * p->wave_bs[w] * 8 > smem_max ||
+        (int64_t)p->wave_regs[w] * 32 * p->wave_bwarps[w] * 8 > smem_max) {
       sgb_plan_destroy(p);
       return fail(-1, "sgb_plan_create: wave scratch exceeds shared memory");
     }
@@ -413,17 +420,26 @@ int sgb_plan_create(const sgb_plan_desc *d, int device, sgb_plan **out) {
   return 0;
 }
 
+static void launch_wave(sgb_plan *p, double *x, int w, cudaStream_t s) {
+  const int64_t blocks = p->wave_blocks[w];
+  if (!blocks) return;
+  const int bs = p->wave_bs[w];
+  const size_t smem = (size_t)p->wave_regs[w] * bs * sizeof(double);
+  wave_single<<<(unsigned)blocks, bs, smem, s>>>(p->T, p->d_blk, p->wave_group_begin[w],
+                                                 p->wave_group_begin[w + 1], x);
+}
+
 int sgb_run_values(sgb_plan *p, double *x, void *stream) {
   if (!p || (!x && p->vas)) return fail(-1, "sgb_run_values: null argument");
-  cudaStream_t s = (cudaStream_t)stream;
-  for (int w = 0; w < p->n_waves; ++w) {
-    const int64_t blocks = p->wave_blocks[w];
-    if (!blocks) continue;
-    const int bs = p->wave_bs[w];
-    const size_t smem = (size_t)p->wave_regs[w] * bs * sizeof(double);
-    wave_single<<<(unsigned)blocks, bs, smem, s>>>(p->T, p->d_blk, p->wave_group_begin[w],
-                                                   p->wave_group_begin[w + 1], x);
-  }
+  for (int w = 0; w < p->n_waves; ++w) launch_wave(p, x, w, (cudaStream_t)stream);
+  SGB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int sgb_run_wave(sgb_plan *p, double *x, int wave, void *stream) {
+  if (!p || (!x && p->vas)) return fail(-1, "sgb_run_wave: null argument");
+  if (wave < 0 || wave >= p->n_waves) return fail(-1, "sgb_run_wave: wave out of range");
+  launch_wave(p, x, wave, (cudaStream_t)stream);
   SGB_CUDA(cudaGetLastError());
   return 0;
 }
@@ -432,10 +448,10 @@ int sgb_run_batch(sgb_plan *p, double *X, int64_t ld, int64_t batch, void *strea
   if (!p || (!X && p->vas)) return fail(-1, "sgb_run_batch: null argument");
   if (batch < 1 || ld < batch) return fail(-1, "sgb_run_batch: need 1 <= batch <= ld");
   cudaStream_t s = (cudaStream_t)stream;
-  const int bs = 32 * BATCH_WARPS;
   for (int w = 0; w < p->n_waves; ++w) {
     const int64_t blocks = p->wave_bblocks[w];
     if (!blocks) continue;
+    const int bs = 32 * p->wave_bwarps[w];
     const size_t smem = (size_t)p->wave_regs[w] * bs * sizeof(double);
     wave_batch<<<(unsigned)blocks, bs, smem, s>>>(p->T, p->d_bblk, p->wave_group_begin[w],
                                                   p->wave_group_begin[w + 1], X, ld, batch);

@@ -289,7 +289,7 @@ def plan_manifest(plan) -> dict:
         "value_array_size": plan.value_array_size,
         "input_count": plan.input_count,
         "vector_width": plan.vector_width,
-        "outputs": list(plan.outputs),
+        "outputs": np.asarray(plan.outputs, dtype=np.int64).tolist(),
         "metadata": plan.metadata,
         "kernels": kernels,
     }
@@ -389,9 +389,9 @@ def validate_plan(plan, src="plan") -> None:
         raise ValueError(f"{src}: constant array has {len(plan.constants)} entries, expected {expected_c}")
     if len(plan.positions) and int(np.max(plan.positions)) >= plan.value_array_size:
         raise ValueError(f"{src}: position index outside the value array")
-    for off in plan.outputs:
-        if not 0 <= off < plan.value_array_size:
-            raise ValueError(f"{src}: output offset {off} outside the value array")
+    outs = np.asarray(plan.outputs, dtype=np.int64)
+    if outs.size and (outs.min() < 0 or outs.max() >= plan.value_array_size):
+        raise ValueError(f"{src}: output offset outside the value array")
     for kp in plan.kernels:
         if kp.dest_base < plan.input_count or kp.dest_base + kp.n_roots * kp.instances > plan.value_array_size:
             raise ValueError(f"{src}: {kp.name} result range outside the value array")

@@ -72,7 +72,7 @@ class _Desc(ctypes.Structure):
 SYMBOLS = (
     "sgb_plan_create", "sgb_plan_destroy", "sgb_run_values", "sgb_gather_outputs",
     "sgb_sg_run", "sgb_run_outputs_host", "sgb_run_batch", "sgb_gather_outputs_batch",
-    "sgb_plan_launches", "sgb_last_error",
+    "sgb_plan_launches", "sgb_last_error", "sgb_run_wave",
 )
 
 
@@ -92,6 +92,7 @@ def load_library(path: Path | str | None = None):
             "sgb_plan_create": (i32, [ctypes.POINTER(_Desc), i32, ctypes.POINTER(vp)]),
             "sgb_plan_destroy": (None, [vp]),
             "sgb_run_values": (i32, [vp, vp, vp]),
+            "sgb_run_wave": (i32, [vp, vp, i32, vp]),
             "sgb_gather_outputs": (i32, [vp, vp, vp, vp]),
             "sgb_sg_run": (i32, [vp, vp, vp, vp]),
             "sgb_run_outputs_host": (i32, [vp, vp, vp]),
@@ -217,6 +218,12 @@ class DevicePlan:
                                         _stream_handle(stream)), "sgb_run_values")
         return x
 
+    def run_wave(self, x, wave: int, stream=None):
+        """One dependency wave (profiling / per-launch timing)."""
+        _check(self._lib.sgb_run_wave(self._handle, ctypes.c_void_p(x.data_ptr()), int(wave),
+                                      _stream_handle(stream)), "sgb_run_wave")
+        return x
+
     def gather_outputs(self, x, out=None, stream=None):
         import torch
 
@@ -338,5 +345,5 @@ def interpret_plan(plan, inputs: Sequence[float], record_loads: bool = False,
                     if bad.any() and not kp.self_referencing:
                         violations.append(f"{kp.name}: slot {s} reads {int(bad.sum())} unwritten addresses")
                 written[kp.dest_base: kp.dest_base + kp.n_roots * kp.instances] = True
-    outputs = x[np.asarray(plan.outputs, dtype=np.int64)] if plan.outputs else np.zeros(0)
+    outputs = x[np.asarray(plan.outputs, dtype=np.int64)] if len(plan.outputs) else np.zeros(0)
     return InterpretResult(outputs=outputs, values=x, loads=loads, violations=violations)
