@@ -50,7 +50,7 @@ typedef struct sgb_group {
   int64_t blk_begin; /* first block of this group inside its wave launch */
   int32_t n_roots, n_slots, n_ret, n_const;
   int32_t tape_len, n_regs, kind, flags;
-  int32_t slot_off, sop_off, sop_len, wave;
+  int32_t slot_off, sop_off, sop_len, unit;
 } sgb_group;
 
 /* Host-side device plan handed to sgb_plan_create (all pointers host memory,
@@ -60,12 +60,13 @@ typedef struct sgb_plan_desc {
   int64_t input_count;      /* ExecutionPlan.input_count */
   int32_t n_groups;
   int32_t n_waves;
-  const sgb_group *groups;         /* ordered by wave */
-  const int32_t *wave_group_begin; /* [n_waves + 1] */
-  const int64_t *wave_blocks;      /* [n_waves] */
-  const int32_t *wave_block_size;  /* [n_waves] */
-  const int32_t *wave_smem_regs;   /* [n_waves] scratch registers per lane */
-  const int32_t *tape;             /* [tape_rows][4] */
+  int32_t n_units;
+  int32_t reserved;
+  const sgb_group *groups; /* ordered by (wave, launch unit) */
+  const int64_t *units;    /* [n_units][8]: wave, kind (0 tape, 1 sum-of-products),
+                              variant, group_begin, group_end, blocks, block_size,
+                              scratch registers per lane */
+  const uint64_t *tape;    /* 64-bit tape words, see lower.py encode() */
   int64_t tape_rows;
   const double *imm;
   int64_t n_imm;
@@ -115,8 +116,11 @@ int sgb_run_batch(sgb_plan *plan, double *X_dev, int64_t ld, int64_t batch, void
 int sgb_gather_outputs_batch(sgb_plan *plan, const double *X_dev, int64_t ld, int64_t batch,
                              double *out_dev, int64_t ld_out, void *stream);
 
-/* Number of kernel launches one sgb_run_values issues (waves). */
+/* Dependency waves of the plan (sgb_run_wave range). */
 int sgb_plan_launches(const sgb_plan *plan);
+
+/* Kernel launches one sgb_run_values issues (launch units, >= waves). */
+int sgb_plan_units(const sgb_plan *plan);
 
 const char *sgb_last_error(void);
 

@@ -4,8 +4,9 @@
 // reference ExecutionPlan (/root/reference/pkg/src/sparsegen/codegen.py:56-98).
 // Semantics are those of the reference evaluators interpret_plan
 // (codegen.py:404-512) and the emitted sg_run (emit.py:90-195):
-//   * kernels run in dependency waves (one launch per wave, every group of the
-//     wave inside that launch, a block -> group table);
+//   * kernels run in dependency waves; every group of a wave runs inside the
+//     wave's launch units (a tape unit, one sum-of-products unit per width
+//     class) through a block -> group table;
 //   * every instance evaluates its template's live nodes in stored order; n-ary
 //     ADD / MUL fold left (codegen.py:472-481); SELECT is c < 0 (codegen.py:490);
 //   * results land at dest_base + r*N + i (codegen.py:492-494);
@@ -14,7 +15,13 @@
 // Arithmetic is IEEE binary64 round-to-nearest through __dadd_rn / __dmul_rn /
 // __ddiv_rn / __dsqrt_rn (never contracted; the file is also built with
 // --fmad=false), so EXACT_OPS templates reproduce the CPU reference bit for bit.
-// No tensor cores: the path is an irregular gather / elementwise graph.
+//
+// The path is an irregular gather / elementwise graph (no tensor cores): the
+// kernels are built for memory-level parallelism -- every index and value load
+// of an instance is issued before the first use, streaming data (index tables,
+// results nobody re-reads) carries an L2 evict-first policy so the gathered
+// intermediates stay in the 126 MB L2, and the launch units keep register
+// counts low enough for high occupancy.
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -29,16 +36,17 @@
 
 namespace {
 
-// op codes: lower.py T_*
+// tape op codes: lower.py T_*
 enum : int {
   T_ADD = 2, T_SUB = 3, T_MUL = 4, T_DIV = 5, T_NEG = 6, T_SQRT = 7, T_SIN = 8, T_COS = 9,
   T_EXP = 10, T_LOG = 11, T_POW = 12, T_SEL = 13, T_IMM = 20, T_ST = 21
 };
 enum : int { KIND_TAPE = 0, KIND_SOP = 1 };
-enum : int { FLAG_SELFREF = 1, FLAG_INTERLEAVED = 2, FLAG_SERIAL = 4 };
-constexpr int SOP_MAX = 32;
-constexpr int PRE = 8;           // loads kept in flight by the tape prologue
-constexpr int BATCH_WARPS = 8;   // instances per block in batched mode
+enum : int { FLAG_SELFREF = 1, FLAG_INTERLEAVED = 2, FLAG_SERIAL = 4, FLAG_STREAM = 16 };
+enum : int { U_WAVE = 0, U_KIND, U_VARIANT, U_G0, U_G1, U_BLOCKS, U_BS, U_REGS, U_COUNT };
+constexpr int PRE = 8;  // slot loads kept in flight by the tape prologue
+constexpr int MAX_BATCH_WARPS = 8;
+constexpr uint64_t REG_MASK = (1u << 14) - 1;
 
 thread_local std::string g_err;
 
@@ -56,7 +64,7 @@ int fail(int code, const std::string &msg) {
 
 struct Tables {
   const sgb_group *groups;
-  const int4 *tape;
+  const uint64_t *tape;
   const double *imm;
   const int32_t *sop;
   const int32_t *slot_col;
@@ -64,6 +72,32 @@ struct Tables {
   const uint32_t *pos;
   const double *con;
 };
+
+// ---- cache-policy helpers ---------------------------------------------------------
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+// streaming index-table read: no L1 allocation, L2 evict-first
+__device__ __forceinline__ uint32_t ld_index(const uint32_t *a, uint64_t pol) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+               : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_const(const double *a, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_result(double *a, double v, bool stream, uint64_t pol) {
+  if (stream)
+    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+  else
+    *a = v;
+}
 
 // Largest g in [g0, g1) with begin[g] <= blk (block -> group table lookup).
 __device__ __forceinline__ int find_group(const int64_t *begin, int g0, int g1, int64_t blk) {
@@ -77,26 +111,20 @@ __device__ __forceinline__ int find_group(const int64_t *begin, int g0, int g1, 
 
 // Index decode == slot_addresses (codegen.py:373-388): retained slot -> its
 // column of the position table; coherent slot -> slot-0 entry + delta.
-__device__ __forceinline__ int64_t slot_addr(const Tables &T, const sgb_group &G, int s,
-                                             int64_t i, bool inter, uint32_t idx0) {
+__device__ __forceinline__ int64_t slot_addr(const Tables &T, const sgb_group &G, int s, int64_t i,
+                                             bool inter, uint32_t idx0, uint64_t pol) {
   const int col = __ldg(T.slot_col + G.slot_off + s);
   if (col < 0) return (int64_t)idx0 + __ldg(T.slot_delta + G.slot_off + s);
   if (col == 0) return idx0;
   const int64_t e = inter ? G.p_off + i * G.n_ret + col : G.p_off + (int64_t)col * G.n + i;
-  return (int64_t)__ldg(T.pos + e);
+  return (int64_t)ld_index(T.pos + e, pol);
 }
 
 __device__ __forceinline__ uint32_t slot0_index(const Tables &T, const sgb_group &G, int64_t i,
-                                                bool inter) {
+                                                bool inter, uint64_t pol) {
   if (G.n_slots == 0) return 0u;
   const int64_t e = inter ? G.p_off + i * G.n_ret : G.p_off + i;
-  return __ldg(T.pos + e);
-}
-
-__device__ __forceinline__ double const_slot(const Tables &T, const sgb_group &G, int k,
-                                             int64_t i, bool inter) {
-  const int64_t e = inter ? G.c_off + i * G.n_const + k : G.c_off + (int64_t)k * G.n + i;
-  return __ldg(T.con + e);
+  return ld_index(T.pos + e, pol);
 }
 
 // ---- double-double integer power (POW k >= 3; k == 2 is an exact x*x) ----------
@@ -109,7 +137,7 @@ __device__ __forceinline__ void dd_mul(double ah, double al, double bh, double b
   rl = __dsub_rn(e, __dsub_rn(rh, p));
 }
 
-__device__ double powi(double x, int k) {
+__device__ __noinline__ double powi(double x, int k) {
   if (k == 2) return __dmul_rn(x, x);  // glibc pow(x, 2.0) == x*x
   double rh = 1.0, rl = 0.0, bh = x, bl = 0.0;
   while (k) {
@@ -121,92 +149,163 @@ __device__ double powi(double x, int k) {
   return isfinite(r) ? r : rh;
 }
 
-// Scratch register r of this lane lives at R[r * stride].
-__device__ __forceinline__ void run_tape(const Tables &T, const sgb_group &G, double *R, int stride,
-                                         double *x, int64_t ld, int64_t i, int64_t b, int phase,
-                                         bool selfref) {
-  const int4 *tp = T.tape + G.tape_off;
-  for (int pc = 0; pc < G.tape_len; ++pc) {
-    const int4 ins = __ldg(tp + pc);
-    const int op = ins.x & 0xFFFF;
-    const unsigned dst = (unsigned)ins.x >> 16;
-    const unsigned a = ins.y & 0xFFFF;
-    const unsigned bb = (unsigned)ins.y >> 16;
+// Rare ops live out of line so the interpreter loop stays small.
+__device__ __noinline__ double slow_op(int op, double a, int k) {
+  switch (op) {
+    case T_SIN: return sin(a);
+    case T_COS: return cos(a);
+    case T_EXP: return exp(a);
+    case T_LOG: return log(a);
+    default: return powi(a, k);
+  }
+}
+
+// ---- tape interpreter ---------------------------------------------------------------
+// Scratch register r of this lane lives at R[r * STRIDE] in shared memory.
+template <int STRIDE>
+__device__ __forceinline__ void run_tape(const Tables &T, const sgb_group &G, double *R, double *x,
+                                         int64_t ld, int64_t i, int64_t b, int phase, bool selfref,
+                                         uint64_t pol) {
+  const uint64_t *tp = T.tape + G.tape_off;
+  const bool stream = G.flags & FLAG_STREAM;
+  const int len = G.tape_len;
+  uint64_t next = len > 0 ? __ldg(tp) : 0;
+  for (int pc = 0; pc < len; ++pc) {
+    const uint64_t w = next;
+    if (pc + 1 < len) next = __ldg(tp + pc + 1);  // prefetch the next word
+    const int op = (int)(w & 0x3F);
+    const unsigned dst = (unsigned)(w >> 6) & REG_MASK;
+    const unsigned a = (unsigned)(w >> 20) & REG_MASK;
+    const unsigned bb = (unsigned)(w >> 34) & REG_MASK;
+    const unsigned c = (unsigned)(w >> 48) & REG_MASK;
     double v;
-    switch (op) {
-      case T_ADD: v = __dadd_rn(R[a * stride], R[bb * stride]); break;
-      case T_SUB: v = __dsub_rn(R[a * stride], R[bb * stride]); break;
-      case T_MUL: v = __dmul_rn(R[a * stride], R[bb * stride]); break;
-      case T_DIV: v = __ddiv_rn(R[a * stride], R[bb * stride]); break;
-      case T_NEG: v = -R[a * stride]; break;
-      case T_SQRT: v = __dsqrt_rn(R[a * stride]); break;
-      case T_SIN: v = sin(R[a * stride]); break;
-      case T_COS: v = cos(R[a * stride]); break;
-      case T_EXP: v = exp(R[a * stride]); break;
-      case T_LOG: v = log(R[a * stride]); break;
-      case T_POW: v = powi(R[a * stride], ins.w); break;
-      case T_SEL: v = (R[a * stride] < 0.0) ? R[bb * stride] : R[(unsigned)ins.z * stride]; break;
-      case T_IMM: v = __ldg(T.imm + ins.w); break;
-      default:  // T_ST
-        if (!selfref || ins.w == phase)
-          x[(G.dest_base + (int64_t)ins.w * G.n + i) * ld + b] = R[a * stride];
-        continue;
+    if (op == T_MUL) {
+      v = __dmul_rn(R[a * STRIDE], R[bb * STRIDE]);
+    } else if (op == T_ADD) {
+      v = __dadd_rn(R[a * STRIDE], R[bb * STRIDE]);
+    } else if (op == T_SUB) {
+      v = __dsub_rn(R[a * STRIDE], R[bb * STRIDE]);
+    } else if (op == T_IMM) {
+      v = __ldg(T.imm + (bb | (c << 14)));
+    } else if (op == T_NEG) {
+      v = -R[a * STRIDE];
+    } else if (op == T_DIV) {
+      v = __ddiv_rn(R[a * STRIDE], R[bb * STRIDE]);
+    } else if (op == T_ST) {
+      if (!selfref || (int)c == phase)
+        st_result(x + (G.dest_base + (int64_t)c * G.n + i) * ld + b, R[a * STRIDE], stream, pol);
+      continue;
+    } else if (op == T_SQRT) {
+      v = __dsqrt_rn(R[a * STRIDE]);
+    } else if (op == T_SEL) {
+      v = (R[a * STRIDE] < 0.0) ? R[bb * STRIDE] : R[c * STRIDE];
+    } else {
+      v = slow_op(op, R[a * STRIDE], (int)c);
     }
-    R[dst * stride] = v;
+    R[dst * STRIDE] = v;
   }
 }
 
 // Prologue: hoisted slot loads (emit.py:108-124), PRE loads in flight per lane.
+template <int STRIDE>
 __device__ __forceinline__ void load_slots(const Tables &T, const sgb_group &G, double *R,
-                                           int stride, const double *x, int64_t ld, int64_t i,
-                                           int64_t b, bool inter, bool coherent_read) {
-  const uint32_t idx0 = slot0_index(T, G, i, inter);
+                                           const double *x, int64_t ld, int64_t i, int64_t b,
+                                           bool inter, bool coherent_read, uint64_t pol) {
+  const uint32_t idx0 = slot0_index(T, G, i, inter, pol);
   for (int s0 = 0; s0 < G.n_slots; s0 += PRE) {
     double v[PRE];
 #pragma unroll
     for (int u = 0; u < PRE; ++u) {
       const int s = s0 + u;
       if (s < G.n_slots) {
-        const int64_t a = slot_addr(T, G, s, i, inter, idx0) * ld + b;
+        const int64_t a = slot_addr(T, G, s, i, inter, idx0, pol) * ld + b;
         v[u] = coherent_read ? x[a] : __ldg(x + a);
       }
     }
 #pragma unroll
     for (int u = 0; u < PRE; ++u)
-      if (s0 + u < G.n_slots) R[(s0 + u) * stride] = v[u];
+      if (s0 + u < G.n_slots) R[(s0 + u) * STRIDE] = v[u];
   }
-  for (int k = 0; k < G.n_const; ++k) R[(G.n_slots + k) * stride] = const_slot(T, G, k, i, inter);
+  for (int k = 0; k < G.n_const; ++k) {
+    const int64_t e = inter ? G.c_off + i * G.n_const + k : G.c_off + (int64_t)k * G.n + i;
+    R[(G.n_slots + k) * STRIDE] = ld_const(T.con + e, pol);
+  }
 }
 
+template <int STRIDE>
 __device__ __forceinline__ void tape_instance(const Tables &T, const sgb_group &G, double *R,
-                                              int stride, double *x, int64_t ld, int64_t i,
-                                              int64_t b) {
+                                              double *x, int64_t ld, int64_t i, int64_t b,
+                                              uint64_t pol) {
   const bool inter = G.flags & FLAG_INTERLEAVED;
   const bool selfref = G.flags & FLAG_SELFREF;
   const int phases = selfref ? G.n_roots : 1;
   for (int ph = 0; ph < phases; ++ph) {
-    load_slots(T, G, R, stride, x, ld, i, b, inter, selfref);
-    run_tape(T, G, R, stride, x, ld, i, b, ph, selfref);
+    load_slots<STRIDE>(T, G, R, x, ld, i, b, inter, selfref, pol);
+    run_tape<STRIDE>(T, G, R, x, ld, i, b, ph, selfref, pol);
   }
 }
 
-// Sum of products of slot loads: acc = t0 + t1 + ..., t = f0 * f1 * ...
-__device__ __forceinline__ double sop_eval(const Tables &T, const sgb_group &G, const double *x,
-                                           int64_t ld, int64_t i, int64_t b) {
+// Single value set: lane = instance.  Scratch file [n_regs][BS] in shared memory.
+template <int BS>
+__global__ void __launch_bounds__(BS) tape_single(Tables T, const int64_t *blk_begin, int g0, int g1,
+                                                  double *x) {
+  extern __shared__ double scratch[];
+  const int64_t blk = blockIdx.x;
+  const int g = find_group(blk_begin, g0, g1, blk);
+  const sgb_group G = T.groups[g];
+  const uint64_t pol = evict_first_policy();
+  const int tid = threadIdx.x;
+  if (G.flags & FLAG_SERIAL) {  // members read other instances' results: instance order
+    if (tid != 0) return;
+    for (int64_t i = 0; i < G.n; ++i) tape_instance<BS>(T, G, scratch, x, 1, i, 0, pol);
+    return;
+  }
+  const int64_t i = (blk - __ldg(blk_begin + g)) * BS + tid;
+  if (i >= G.n) return;
+  tape_instance<BS>(T, G, scratch + tid, x, 1, i, 0, pol);
+}
+
+// Batched: X[addr * ld + b].  A warp owns one instance and sweeps the batch,
+// so index loads are warp-uniform and every gather is a contiguous row.
+template <int BS>
+__global__ void __launch_bounds__(BS) tape_batch(Tables T, const int64_t *blk_begin, int g0, int g1,
+                                                 double *X, int64_t ld, int64_t batch) {
+  extern __shared__ double scratch[];
+  const int64_t blk = blockIdx.x;
+  const int g = find_group(blk_begin, g0, g1, blk);
+  const sgb_group G = T.groups[g];
+  const uint64_t pol = evict_first_policy();
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (G.flags & FLAG_SERIAL) {
+    if (warp != 0) return;
+    for (int64_t i = 0; i < G.n; ++i)
+      for (int64_t b = lane; b < batch; b += 32) tape_instance<BS>(T, G, scratch + tid, X, ld, i, b, pol);
+    return;
+  }
+  const int64_t i = (blk - __ldg(blk_begin + g)) * (BS >> 5) + warp;
+  if (i >= G.n) return;
+  for (int64_t b = lane; b < batch; b += 32) tape_instance<BS>(T, G, scratch + tid, X, ld, i, b, pol);
+}
+
+// ---- sum of products: acc = t0 + t1 + ..., t = f0 * f1 * ... (tape-free) --------------
+template <int LMAX>
+__device__ __forceinline__ void sop_addrs(const Tables &T, const sgb_group &G, int64_t i,
+                                          int64_t (&addr)[LMAX], uint64_t pol) {
   const bool inter = G.flags & FLAG_INTERLEAVED;
-  const uint32_t newterm = (uint32_t)__ldg(T.sop + G.sop_off);
-  const uint32_t negm = (uint32_t)__ldg(T.sop + G.sop_off + 1);
-  const int L = G.sop_len;
-  const uint32_t idx0 = slot0_index(T, G, i, inter);
-  double v[SOP_MAX];
+  const uint32_t idx0 = slot0_index(T, G, i, inter, pol);
 #pragma unroll
-  for (int f = 0; f < SOP_MAX; ++f)
-    if (f < L) v[f] = __ldg(x + slot_addr(T, G, f, i, inter, idx0) * ld + b);
+  for (int f = 0; f < LMAX; ++f)
+    if (f < G.sop_len) addr[f] = slot_addr(T, G, f, i, inter, idx0, pol);
+}
+
+template <int LMAX>
+__device__ __forceinline__ double sop_fold(const sgb_group &G, uint32_t newterm, uint32_t negm,
+                                           const double (&v)[LMAX]) {
   double acc = 0.0, term = 0.0;
   bool have = false;
 #pragma unroll
-  for (int f = 0; f < SOP_MAX; ++f) {
-    if (f < L) {
+  for (int f = 0; f < LMAX; ++f) {
+    if (f < G.sop_len) {
       const double val = ((negm >> f) & 1u) ? -v[f] : v[f];
       if ((newterm >> f) & 1u) {
         if (f > 0) {
@@ -222,59 +321,60 @@ __device__ __forceinline__ double sop_eval(const Tables &T, const sgb_group &G, 
   return have ? __dadd_rn(acc, term) : term;
 }
 
-// One launch per wave, single value set.  blockDim = wave block size.
-__global__ void wave_single(Tables T, const int64_t *blk_begin, int g0, int g1, double *x) {
-  extern __shared__ double scratch[];
+template <int LMAX>
+__global__ void __launch_bounds__(256) sop_single(Tables T, const int64_t *blk_begin, int g0, int g1,
+                                                  double *x) {
   const int64_t blk = blockIdx.x;
   const int g = find_group(blk_begin, g0, g1, blk);
   const sgb_group G = T.groups[g];
-  const int tid = threadIdx.x;
-  if (G.flags & FLAG_SERIAL) {  // members read other instances' results: instance order
-    if (tid != 0) return;
-    for (int64_t i = 0; i < G.n; ++i) tape_instance(T, G, scratch, 1, x, 1, i, 0);
-    return;
-  }
-  const int64_t i = (blk - __ldg(blk_begin + g)) * blockDim.x + tid;
+  const int64_t i = (blk - __ldg(blk_begin + g)) * blockDim.x + threadIdx.x;
   if (i >= G.n) return;
-  if (G.kind == KIND_SOP) {
-    x[G.dest_base + i] = sop_eval(T, G, x, 1, i, 0);
-  } else {
-    tape_instance(T, G, scratch + tid, blockDim.x, x, 1, i, 0);
-  }
+  const uint64_t pol = evict_first_policy();
+  const uint32_t newterm = (uint32_t)__ldg(T.sop + G.sop_off);
+  const uint32_t negm = (uint32_t)__ldg(T.sop + G.sop_off + 1);
+  int64_t addr[LMAX];
+  sop_addrs<LMAX>(T, G, i, addr, pol);
+  double v[LMAX];
+#pragma unroll
+  for (int f = 0; f < LMAX; ++f)
+    if (f < G.sop_len) v[f] = __ldg(x + addr[f]);
+  st_result(x + G.dest_base + i, sop_fold<LMAX>(G, newterm, negm, v), G.flags & FLAG_STREAM, pol);
 }
 
-// Batched: X[addr * ld + b].  A warp owns one instance and sweeps the batch,
-// so index loads are warp-uniform and every gather is a contiguous row.
-__global__ void wave_batch(Tables T, const int64_t *blk_begin, int g0, int g1, double *X,
-                           int64_t ld, int64_t batch) {
-  extern __shared__ double scratch[];
+template <int LMAX>
+__global__ void __launch_bounds__(256) sop_batch(Tables T, const int64_t *blk_begin, int g0, int g1,
+                                                 double *X, int64_t ld, int64_t batch) {
   const int64_t blk = blockIdx.x;
   const int g = find_group(blk_begin, g0, g1, blk);
   const sgb_group G = T.groups[g];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (G.flags & FLAG_SERIAL) {
-    if (warp != 0) return;
-    for (int64_t i = 0; i < G.n; ++i)
-      for (int64_t b = lane; b < batch; b += 32)
-        tape_instance(T, G, scratch + tid, blockDim.x, X, ld, i, b);
-    return;
-  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t i = (blk - __ldg(blk_begin + g)) * (blockDim.x >> 5) + warp;
   if (i >= G.n) return;
+  const uint64_t pol = evict_first_policy();
+  const uint32_t newterm = (uint32_t)__ldg(T.sop + G.sop_off);
+  const uint32_t negm = (uint32_t)__ldg(T.sop + G.sop_off + 1);
+  int64_t addr[LMAX];
+  sop_addrs<LMAX>(T, G, i, addr, pol);  // warp-uniform: one index fetch per warp
+  const bool stream = G.flags & FLAG_STREAM;
   for (int64_t b = lane; b < batch; b += 32) {
-    if (G.kind == KIND_SOP) {
-      X[(G.dest_base + i) * ld + b] = sop_eval(T, G, X, ld, i, b);
-    } else {
-      tape_instance(T, G, scratch + tid, blockDim.x, X, ld, i, b);
-    }
+    double v[LMAX];
+#pragma unroll
+    for (int f = 0; f < LMAX; ++f)
+      if (f < G.sop_len) v[f] = __ldg(X + addr[f] * ld + b);
+    st_result(X + (G.dest_base + i) * ld + b, sop_fold<LMAX>(G, newterm, negm, v), stream, pol);
   }
 }
 
 __global__ void gather_outputs(const double *__restrict__ x, const int64_t *__restrict__ outs,
                                int64_t n, double *__restrict__ out) {
+  const uint64_t pol = evict_first_policy();
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x)
-    out[k] = __ldg(x + __ldg(outs + k));
+       k += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s64 %0, [%1], %2;"
+                 : "=l"(a) : "l"(outs + k), "l"(pol));
+    st_result(out + k, __ldg(x + a), true, pol);
+  }
 }
 
 __global__ void gather_outputs_batch(const double *__restrict__ X, int64_t ld, int64_t batch,
@@ -295,19 +395,24 @@ int upload(T **dst, const T *src, int64_t n) {
   return 0;
 }
 
+struct Unit {
+  int wave, kind, variant, g0, g1, bs, regs;
+  int64_t blocks;
+  int bwarps;       // batched mode: instances (warps) per block
+  int64_t bblocks;  // batched mode: blocks
+};
+
 }  // namespace
 
 struct sgb_plan {
   int device = 0;
   int64_t vas = 0, n_in = 0, n_out = 0, n_pos = 0, n_con = 0;
   int n_groups = 0, n_waves = 0;
-  std::vector<int32_t> wave_group_begin, wave_bs, wave_regs;
-  std::vector<int64_t> wave_blocks, wave_bblocks;
-  std::vector<int32_t> wave_bwarps;
+  std::vector<Unit> units;
   Tables T{};
   sgb_group *d_groups = nullptr;
   int64_t *d_blk = nullptr, *d_bblk = nullptr, *d_outputs = nullptr;
-  int4 *d_tape = nullptr;
+  uint64_t *d_tape = nullptr;
   double *d_imm = nullptr, *d_con = nullptr;
   int32_t *d_sop = nullptr, *d_scol = nullptr;
   int64_t *d_sdel = nullptr;
@@ -318,11 +423,65 @@ struct sgb_plan {
   cudaStream_t ws_stream = nullptr;
 };
 
+namespace {
+
+template <int BS>
+void launch_tape(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_t batch, bool batched,
+                 cudaStream_t s) {
+  const size_t smem = (size_t)u.regs * BS * sizeof(double);
+  if (!batched)
+    tape_single<BS><<<(unsigned)u.blocks, BS, smem, s>>>(p->T, p->d_blk, u.g0, u.g1, x);
+  else
+    tape_batch<BS><<<(unsigned)u.bblocks, BS, smem, s>>>(p->T, p->d_bblk, u.g0, u.g1, x, ld, batch);
+}
+
+template <int LMAX>
+void launch_sop(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_t batch, bool batched,
+                cudaStream_t s) {
+  if (!batched)
+    sop_single<LMAX><<<(unsigned)u.blocks, 256, 0, s>>>(p->T, p->d_blk, u.g0, u.g1, x);
+  else
+    sop_batch<LMAX><<<(unsigned)u.bblocks, 256, 0, s>>>(p->T, p->d_bblk, u.g0, u.g1, x, ld, batch);
+}
+
+void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_t batch, bool batched,
+                 cudaStream_t s) {
+  if ((batched ? u.bblocks : u.blocks) == 0) return;
+  if (u.kind == KIND_TAPE) {
+    // the scratch-file stride equals the block size of the launch
+    const int bs = batched ? 32 * u.bwarps : u.bs;
+    switch (bs) {
+      case 256: launch_tape<256>(p, u, x, ld, batch, batched, s); break;
+      case 128: launch_tape<128>(p, u, x, ld, batch, batched, s); break;
+      case 64: launch_tape<64>(p, u, x, ld, batch, batched, s); break;
+      default: launch_tape<32>(p, u, x, ld, batch, batched, s); break;
+    }
+  } else {
+    switch (u.variant) {
+      case 4: launch_sop<4>(p, u, x, ld, batch, batched, s); break;
+      case 8: launch_sop<8>(p, u, x, ld, batch, batched, s); break;
+      case 16: launch_sop<16>(p, u, x, ld, batch, batched, s); break;
+      default: launch_sop<32>(p, u, x, ld, batch, batched, s); break;
+    }
+  }
+}
+
+template <int BS>
+cudaError_t allow_smem(int smem_max) {
+  cudaError_t e = cudaFuncSetAttribute(tape_single<BS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(tape_batch<BS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+}
+
+}  // namespace
+
 extern "C" {
 
 const char *sgb_last_error(void) { return g_err.c_str(); }
 
 int sgb_plan_launches(const sgb_plan *p) { return p ? p->n_waves : 0; }
+
+int sgb_plan_units(const sgb_plan *p) { return p ? (int)p->units.size() : 0; }
 
 void sgb_plan_destroy(sgb_plan *p) {
   if (!p) return;
@@ -335,9 +494,7 @@ void sgb_plan_destroy(sgb_plan *p) {
   delete p;
 }
 
-int sgb_plan_create(const sgb_plan_desc *d, int device, sgb_plan **out) {
-  if (!d || !out) return fail(-1, "sgb_plan_create: null argument");
-  *out = nullptr;
+static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
   int ndev = 0;
   SGB_CUDA(cudaGetDeviceCount(&ndev));
   if (device < 0 || device >= ndev) return fail(-1, "sgb_plan_create: bad device ordinal");
@@ -345,8 +502,7 @@ int sgb_plan_create(const sgb_plan_desc *d, int device, sgb_plan **out) {
   cudaDeviceProp prop;
   SGB_CUDA(cudaGetDeviceProperties(&prop, device));
   if (prop.major != 10) return fail(-2, "sgb_plan_create: libsgb is built for sm_100a (B200) only");
-  if (d->n_waves < 0 || d->n_groups < 0) return fail(-1, "sgb_plan_create: negative counts");
-  sgb_plan *p = new sgb_plan();
+  if (d->n_waves < 0 || d->n_groups < 0 || d->n_units < 0) return fail(-1, "sgb_plan_create: negative counts");
   p->device = device;
   p->vas = d->value_array_size;
   p->n_in = d->input_count;
@@ -355,91 +511,102 @@ int sgb_plan_create(const sgb_plan_desc *d, int device, sgb_plan **out) {
   p->n_con = d->n_constants;
   p->n_groups = d->n_groups;
   p->n_waves = d->n_waves;
-  p->wave_group_begin.assign(d->wave_group_begin, d->wave_group_begin + d->n_waves + 1);
-  p->wave_blocks.assign(d->wave_blocks, d->wave_blocks + d->n_waves);
-  p->wave_bs.assign(d->wave_block_size, d->wave_block_size + d->n_waves);
-  p->wave_regs.assign(d->wave_smem_regs, d->wave_smem_regs + d->n_waves);
-  // host-side validation of the tables the kernels trust
+  // host-side validation of every table entry the kernels trust
   for (int g = 0; g < d->n_groups; ++g) {
     const sgb_group &G = d->groups[g];
-    if (G.n < 0 || G.dest_base < d->input_count || G.dest_base + G.n_roots * G.n > d->value_array_size ||
-        G.p_off + (int64_t)G.n_ret * G.n > d->n_positions ||
-        G.c_off + (int64_t)G.n_const * G.n > d->n_constants || G.tape_off + G.tape_len > d->tape_rows ||
-        G.slot_off + G.n_slots > d->n_slot || (G.kind == KIND_SOP && (G.sop_len > SOP_MAX || G.sop_off + 2 > d->n_sop))) {
-      sgb_plan_destroy(p);
-      return fail(-1, "sgb_plan_create: group " + std::to_string(g) + " is out of range");
-    }
+    const bool bad =
+        G.n < 0 || G.dest_base < d->input_count || G.dest_base + G.n_roots * G.n > d->value_array_size ||
+        G.p_off < 0 || G.p_off + (int64_t)G.n_ret * G.n > d->n_positions || G.c_off < 0 ||
+        G.c_off + (int64_t)G.n_const * G.n > d->n_constants || G.tape_off < 0 ||
+        G.tape_off + G.tape_len > d->tape_rows || G.slot_off < 0 || G.slot_off + G.n_slots > d->n_slot ||
+        (G.n_slots > 0 && G.n_ret < 1) ||
+        (G.kind == KIND_SOP && (G.sop_len > 32 || G.sop_len != G.n_slots || G.sop_off + 2 > d->n_sop));
+    if (bad) return fail(-1, "sgb_plan_create: group " + std::to_string(g) + " is out of range");
+    for (int s = 0; s < G.n_slots; ++s)
+      if (d->slot_col[G.slot_off + s] >= G.n_ret) return fail(-1, "sgb_plan_create: bad slot column");
   }
+  for (int64_t k = 0; k < d->n_positions; ++k)
+    if ((int64_t)d->positions[k] >= d->value_array_size)
+      return fail(-1, "sgb_plan_create: position index outside the value array");
   for (int64_t k = 0; k < d->n_outputs; ++k)
-    if (d->outputs[k] < 0 || d->outputs[k] >= d->value_array_size) {
-      sgb_plan_destroy(p);
+    if (d->outputs[k] < 0 || d->outputs[k] >= d->value_array_size)
       return fail(-1, "sgb_plan_create: output offset outside the value array");
-    }
-  // batched block table: one instance per warp, as many warps per block (<= BATCH_WARPS)
-  // as the wave's scratch file allows in shared memory
   int smem_max = 0;
   SGB_CUDA(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
-  std::vector<int64_t> bblk(d->n_groups, 0), blk(d->n_groups, 0);
-  p->wave_bblocks.assign(d->n_waves, 0);
-  p->wave_bwarps.assign(d->n_waves, BATCH_WARPS);
-  for (int w = 0; w < d->n_waves; ++w) {
-    int warps = BATCH_WARPS;
-    while (warps > 1 && (int64_t)p->wave_regs[w] * 32 * warps * 8 > smem_max) warps >>= 1;
-    p->wave_bwarps[w] = warps;
+  SGB_CUDA(allow_smem<32>(smem_max));
+  SGB_CUDA(allow_smem<64>(smem_max));
+  SGB_CUDA(allow_smem<128>(smem_max));
+  SGB_CUDA(allow_smem<256>(smem_max));
+  std::vector<int64_t> blk(d->n_groups, 0), bblk(d->n_groups, 0);
+  for (int k = 0; k < d->n_units; ++k) {
+    const int64_t *r = d->units + (int64_t)k * U_COUNT;
+    Unit u;
+    u.wave = (int)r[U_WAVE];
+    u.kind = (int)r[U_KIND];
+    u.variant = (int)r[U_VARIANT];
+    u.g0 = (int)r[U_G0];
+    u.g1 = (int)r[U_G1];
+    u.blocks = r[U_BLOCKS];
+    u.bs = (int)r[U_BS];
+    u.regs = (int)r[U_REGS];
+    if (u.g0 < 0 || u.g1 > d->n_groups || u.g0 > u.g1 || u.wave < 0 || u.wave >= d->n_waves ||
+        (u.kind == KIND_TAPE && (u.bs != 32 && u.bs != 64 && u.bs != 128)) ||
+        (int64_t)u.regs * (u.kind == KIND_TAPE ? u.bs : 0) * 8 > smem_max)
+      return fail(-1, "sgb_plan_create: bad launch unit " + std::to_string(k));
+    // batched: one instance per warp, as many warps per block as the scratch file allows
+    u.bwarps = MAX_BATCH_WARPS;
+    if (u.kind == KIND_TAPE)
+      while (u.bwarps > 1 && (int64_t)u.regs * 32 * u.bwarps * 8 > smem_max) u.bwarps >>= 1;
     int64_t acc = 0;
-    for (int g = d->wave_group_begin[w]; g < d->wave_group_begin[w + 1]; ++g) {
+    for (int g = u.g0; g < u.g1; ++g) {
       blk[g] = d->groups[g].blk_begin;
       bblk[g] = acc;
-      acc += (d->groups[g].flags & FLAG_SERIAL) ? 1 : (d->groups[g].n + warps - 1) / warps;
+      acc += (d->groups[g].flags & FLAG_SERIAL) ? 1 : (d->groups[g].n + u.bwarps - 1) / u.bwarps;
     }
-    p->wave_bblocks[w] = acc;
+    u.bblocks = acc;
+    p->units.push_back(u);
   }
   int rc = 0;
-  if ((rc = upload(&p->d_groups, d->groups, d->n_groups)) || (rc = upload(&p->d_blk, blk.data(), (int64_t)blk.size())) ||
+  if ((rc = upload(&p->d_groups, d->groups, d->n_groups)) ||
+      (rc = upload(&p->d_blk, blk.data(), (int64_t)blk.size())) ||
       (rc = upload(&p->d_bblk, bblk.data(), (int64_t)bblk.size())) ||
       (rc = upload(&p->d_outputs, d->outputs, d->n_outputs)) ||
-      (rc = upload(&p->d_tape, (const int4 *)d->tape, d->tape_rows)) ||
-      (rc = upload(&p->d_imm, d->imm, d->n_imm)) || (rc = upload(&p->d_sop, d->sop, d->n_sop)) ||
-      (rc = upload(&p->d_scol, d->slot_col, d->n_slot)) || (rc = upload(&p->d_sdel, d->slot_delta, d->n_slot)) ||
+      (rc = upload(&p->d_tape, d->tape, d->tape_rows)) || (rc = upload(&p->d_imm, d->imm, d->n_imm)) ||
+      (rc = upload(&p->d_sop, d->sop, d->n_sop)) || (rc = upload(&p->d_scol, d->slot_col, d->n_slot)) ||
+      (rc = upload(&p->d_sdel, d->slot_delta, d->n_slot)) ||
       (rc = upload(&p->d_pos, d->positions, d->n_positions)) ||
-      (rc = upload(&p->d_con, d->constants, d->n_constants))) {
+      (rc = upload(&p->d_con, d->constants, d->n_constants)))
+    return rc;
+  p->T = Tables{p->d_groups, p->d_tape, p->d_imm, p->d_sop, p->d_scol, p->d_sdel, p->d_pos, p->d_con};
+  return 0;
+}
+
+int sgb_plan_create(const sgb_plan_desc *d, int device, sgb_plan **out) {
+  if (!d || !out) return fail(-1, "sgb_plan_create: null argument");
+  *out = nullptr;
+  sgb_plan *p = new sgb_plan();
+  int rc = create_impl(d, device, p);
+  if (rc) {
     std::string msg = g_err;
     sgb_plan_destroy(p);
     return fail(rc, msg);
   }
-  p->T = Tables{p->d_groups, p->d_tape, p->d_imm, p->d_sop, p->d_scol, p->d_sdel, p->d_pos, p->d_con};
-  SGB_CUDA(cudaFuncSetAttribute(wave_single, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
-  SGB_CUDA(cudaFuncSetAttribute(wave_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
-  for (int w = 0; w < d->n_waves; ++w)
-    if ((int64_t)p->wave_regs[w] * p->wave_bs[w] * 8 > smem_max ||
-        (int64_t)p->wave_regs[w] * 32 * p->wave_bwarps[w] * 8 > smem_max) {
-      sgb_plan_destroy(p);
-      return fail(-1, "sgb_plan_create: wave scratch exceeds shared memory");
-    }
   *out = p;
-  return 0;
-}
-
-static void launch_wave(sgb_plan *p, double *x, int w, cudaStream_t s) {
-  const int64_t blocks = p->wave_blocks[w];
-  if (!blocks) return;
-  const int bs = p->wave_bs[w];
-  const size_t smem = (size_t)p->wave_regs[w] * bs * sizeof(double);
-  wave_single<<<(unsigned)blocks, bs, smem, s>>>(p->T, p->d_blk, p->wave_group_begin[w],
-                                                 p->wave_group_begin[w + 1], x);
-}
-
-int sgb_run_values(sgb_plan *p, double *x, void *stream) {
-  if (!p || (!x && p->vas)) return fail(-1, "sgb_run_values: null argument");
-  for (int w = 0; w < p->n_waves; ++w) launch_wave(p, x, w, (cudaStream_t)stream);
-  SGB_CUDA(cudaGetLastError());
   return 0;
 }
 
 int sgb_run_wave(sgb_plan *p, double *x, int wave, void *stream) {
   if (!p || (!x && p->vas)) return fail(-1, "sgb_run_wave: null argument");
   if (wave < 0 || wave >= p->n_waves) return fail(-1, "sgb_run_wave: wave out of range");
-  launch_wave(p, x, wave, (cudaStream_t)stream);
+  for (const Unit &u : p->units)
+    if (u.wave == wave) launch_unit(p, u, x, 1, 1, false, (cudaStream_t)stream);
+  SGB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int sgb_run_values(sgb_plan *p, double *x, void *stream) {
+  if (!p || (!x && p->vas)) return fail(-1, "sgb_run_values: null argument");
+  for (const Unit &u : p->units) launch_unit(p, u, x, 1, 1, false, (cudaStream_t)stream);
   SGB_CUDA(cudaGetLastError());
   return 0;
 }
@@ -447,15 +614,7 @@ int sgb_run_wave(sgb_plan *p, double *x, int wave, void *stream) {
 int sgb_run_batch(sgb_plan *p, double *X, int64_t ld, int64_t batch, void *stream) {
   if (!p || (!X && p->vas)) return fail(-1, "sgb_run_batch: null argument");
   if (batch < 1 || ld < batch) return fail(-1, "sgb_run_batch: need 1 <= batch <= ld");
-  cudaStream_t s = (cudaStream_t)stream;
-  for (int w = 0; w < p->n_waves; ++w) {
-    const int64_t blocks = p->wave_bblocks[w];
-    if (!blocks) continue;
-    const int bs = 32 * p->wave_bwarps[w];
-    const size_t smem = (size_t)p->wave_regs[w] * bs * sizeof(double);
-    wave_batch<<<(unsigned)blocks, bs, smem, s>>>(p->T, p->d_bblk, p->wave_group_begin[w],
-                                                  p->wave_group_begin[w + 1], X, ld, batch);
-  }
+  for (const Unit &u : p->units) launch_unit(p, u, X, ld, batch, true, (cudaStream_t)stream);
   SGB_CUDA(cudaGetLastError());
   return 0;
 }
@@ -478,10 +637,9 @@ int sgb_gather_outputs_batch(sgb_plan *p, const double *X, int64_t ld, int64_t b
   if (!p->n_out) return 0;
   if (!X || !out || batch < 1 || ld < batch || ld_out < batch)
     return fail(-1, "sgb_gather_outputs_batch: bad arguments");
-  const int bs = 256;
   const int64_t blocks = (p->n_out + 7) / 8;
-  gather_outputs_batch<<<(unsigned)blocks, bs, 0, (cudaStream_t)stream>>>(X, ld, batch, p->d_outputs,
-                                                                         p->n_out, out, ld_out);
+  gather_outputs_batch<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(X, ld, batch, p->d_outputs,
+                                                                          p->n_out, out, ld_out);
   SGB_CUDA(cudaGetLastError());
   return 0;
 }

@@ -41,7 +41,7 @@ T_SIN, T_COS, T_EXP, T_LOG, T_POW, T_SEL = 8, 9, 10, 11, 12, 13
 T_IMM, T_ST = 20, 21
 
 KIND_TAPE, KIND_SOP = 0, 1
-FLAG_SELFREF, FLAG_INTERLEAVED, FLAG_SERIAL, FLAG_EXACT = 1, 2, 4, 8
+FLAG_SELFREF, FLAG_INTERLEAVED, FLAG_SERIAL, FLAG_EXACT, FLAG_STREAM = 1, 2, 4, 8, 16
 SOP_NEWTERM, SOP_NEG = 1, 2
 SOP_MAX = 32  # factors per sum-of-products template (csrc SOP_MAX)
 
@@ -51,8 +51,11 @@ GROUP_DTYPE = np.dtype([
     ("tape_off", "<i8"), ("blk_begin", "<i8"),
     ("n_roots", "<i4"), ("n_slots", "<i4"), ("n_ret", "<i4"), ("n_const", "<i4"),
     ("tape_len", "<i4"), ("n_regs", "<i4"), ("kind", "<i4"), ("flags", "<i4"),
-    ("slot_off", "<i4"), ("sop_off", "<i4"), ("sop_len", "<i4"), ("wave", "<i4"),
+    ("slot_off", "<i4"), ("sop_off", "<i4"), ("sop_len", "<i4"), ("unit", "<i4"),
 ])
+
+# one row per launch unit (int64 x 8), mirrored by include/sgb.h SGB_UNIT_*
+UNIT_FIELDS = ("wave", "kind", "variant", "group_begin", "group_end", "blocks", "block_size", "smem_regs")
 assert GROUP_DTYPE.itemsize == 96
 
 
@@ -63,7 +66,7 @@ class KernelLowering:
     kind: int
     flags: int
     n_regs: int
-    tape: np.ndarray  # (L, 4) int32
+    tape: np.ndarray  # (L,) uint64 tape words
     imms: list
     sop: np.ndarray  # (F,) int32 descriptors
     slot_col: np.ndarray  # int32, retained column or -1
@@ -76,12 +79,10 @@ class KernelLowering:
 class DevicePlanArrays:
     """Host-side device plan: flat arrays handed to sgb_plan_create."""
 
-    groups: np.ndarray  # GROUP_DTYPE, ordered by wave
-    wave_group_begin: np.ndarray  # int32 [n_waves + 1]
-    wave_blocks: np.ndarray  # int64 [n_waves]
-    wave_block_size: np.ndarray  # int32 [n_waves]
-    wave_smem_regs: np.ndarray  # int32 [n_waves]  max scratch registers of tape groups
-    tape: np.ndarray  # int32 [L, 4]
+    groups: np.ndarray  # GROUP_DTYPE, ordered by (wave, launch unit)
+    units: np.ndarray  # int64 [n_units, 8], UNIT_FIELDS
+    n_waves: int
+    tape: np.ndarray  # uint64 tape words
     imm: np.ndarray  # f64
     sop: np.ndarray  # int32
     slot_col: np.ndarray  # int32
@@ -94,9 +95,8 @@ class DevicePlanArrays:
     kernels: list = field(default_factory=list)
     exact: bool = True
 
-    @property
-    def n_waves(self) -> int:
-        return len(self.wave_blocks)
+    def unit(self, u: int) -> dict:
+        return dict(zip(UNIT_FIELDS, (int(v) for v in self.units[u])))
 
 
 # -- waves ----------------------------------------------------------------------
@@ -158,6 +158,22 @@ def compute_waves(plan, read_sets=None) -> list[int]:
 
 # -- tapes ----------------------------------------------------------------------
 
+# 64-bit tape word: op[0:6] dst[6:20] a[20:34] b[34:48] c[48:62]
+# IMM: immediate index = b | c << 14; ST: source a, root c; POW: base a, k c
+REG_MAX = (1 << 14) - 1
+
+
+def encode(op, dst=0, a=0, b=0, c=0) -> int:
+    for v in (dst, a, b, c):
+        if not 0 <= v <= REG_MAX:
+            raise ValueError(f"tape field {v} out of range (max {REG_MAX})")
+    return op | (dst << 6) | (a << 20) | (b << 34) | (c << 48)
+
+
+def decode(word: int):
+    return (word & 0x3F, (word >> 6) & REG_MAX, (word >> 20) & REG_MAX,
+            (word >> 34) & REG_MAX, (word >> 48) & REG_MAX)
+
 
 class _RegAlloc:
     def __init__(self, reserved: int):
@@ -176,11 +192,11 @@ class _RegAlloc:
 
 
 def compile_tape(kp):
-    """Template -> (tape rows, immediates, n_regs, fp64 ops/instance).
+    """Template -> (tape words uint64, immediates, n_regs, fp64 ops/instance).
 
     Registers 0..S-1 hold the position slots, S..S+K-1 the constant slots
-    (loaded by the kernel prologue).  Rows are (op | dst<<16, a | b<<16,
-    c, aux) int32.
+    (loaded by the kernel prologue); temporaries are recycled after their
+    last use (linear scan over the ascending live order).
     """
     tmpl = kp.template_arena
     roots = list(kp.template_roots)
@@ -189,6 +205,8 @@ def compile_tape(kp):
     slot_of = {v: s for s, v in enumerate(kp.pos_vars)}
     cslot_of = {v: s for s, v in enumerate(kp.const_vars)}
     S, K = len(kp.pos_vars), len(kp.const_vars)
+    if S + K > REG_MAX:
+        raise ValueError(f"{kp.name}: {S + K} slots exceed the tape register space")
     order = {ref: j for j, ref in enumerate(live)}
     last_use = {}
     for ref in live:
@@ -197,14 +215,10 @@ def compile_tape(kp):
     root_set = set(roots)
     ra = _RegAlloc(S + K)
     reg: dict[int, int] = {}
-    rows: list[tuple[int, int, int, int]] = []
+    words: list[int] = []
     imms: list[float] = []
     imm_of: dict[int, int] = {}
     fops = 0
-
-    def row(op, dst, a=0, b=0, c=0, aux=0):
-        rows.append(((op & 0xFFFF) | (dst << 16), (a & 0xFFFF) | (b << 16), c, aux))
-
     for ref in live:
         op = int(ops[ref])
         a = args[ref]
@@ -218,27 +232,28 @@ def compile_tape(kp):
                 imm_of[bits] = len(imms)
                 imms.append(float(payload[ref]))
             d = ra.get()
-            row(T_IMM, d, aux=imm_of[bits])
+            k = imm_of[bits]
+            words.append(encode(T_IMM, d, 0, k & REG_MAX, k >> 14))
             reg[ref] = d
             continue
         d = ra.get()
         if op in (OpKind.ADD, OpKind.MUL):
             t = T_ADD if op == OpKind.ADD else T_MUL
-            row(t, d, reg[a[0]], reg[a[1]])
+            words.append(encode(t, d, reg[a[0]], reg[a[1]]))
             for ch in a[2:]:
-                row(t, d, d, reg[ch])
+                words.append(encode(t, d, d, reg[ch]))
             fops += len(a) - 1
         elif op in (OpKind.SUB, OpKind.DIV):
-            row(T_SUB if op == OpKind.SUB else T_DIV, d, reg[a[0]], reg[a[1]])
+            words.append(encode(T_SUB if op == OpKind.SUB else T_DIV, d, reg[a[0]], reg[a[1]]))
             fops += 1
         elif op in (OpKind.NEG, OpKind.SQRT, OpKind.SIN, OpKind.COS, OpKind.EXP, OpKind.LOG):
-            row(op, d, reg[a[0]])
+            words.append(encode(op, d, reg[a[0]]))
             fops += 1
         elif op == OpKind.POW:
-            row(T_POW, d, reg[a[0]], aux=int(payload[a[1]]))
+            words.append(encode(T_POW, d, reg[a[0]], 0, int(payload[a[1]])))
             fops += 1
         elif op == OpKind.SELECT:
-            row(T_SEL, d, reg[a[0]], reg[a[1]], reg[a[2]])
+            words.append(encode(T_SEL, d, reg[a[0]], reg[a[1]], reg[a[2]]))
             fops += 1
         else:
             raise ValueError(f"{kp.name}: unknown op {op}")
@@ -248,12 +263,11 @@ def compile_tape(kp):
             if last_use.get(ch) == order[ref] and ch not in root_set and reg[ch] >= S + K \
                     and int(ops[ch]) != OpKind.VAR:
                 ra.put(reg[ch])
-        if max(rows[-1][0] >> 16, ra.top) > 0xFFFF:
-            raise ValueError(f"{kp.name}: template needs more than 65535 scratch registers")
+        if ra.top > REG_MAX:
+            raise ValueError(f"{kp.name}: template needs more than {REG_MAX} scratch registers")
     for r_idx, root in enumerate(roots):
-        row(T_ST, 0, reg[root], aux=r_idx)
-    tape = np.asarray(rows, dtype=np.int64).astype(np.int32) if rows else np.zeros((0, 4), np.int32)
-    return tape.reshape(-1, 4), imms, max(ra.top, 1), fops
+        words.append(encode(T_ST, 0, reg[root], 0, r_idx))
+    return np.asarray(words, dtype=np.uint64), imms, max(ra.top, 1), fops
 
 
 def _flatten(tmpl, ref, op):
@@ -326,7 +340,7 @@ def lower_kernel(plan, kp, index: int) -> KernelLowering:
                     flags |= FLAG_SERIAL
                     break
     if sop is not None:
-        return KernelLowering(index, kp.name, KIND_SOP, flags, 0, np.zeros((0, 4), np.int32), [],
+        return KernelLowering(index, kp.name, KIND_SOP, flags, 0, np.zeros(0, np.uint64), [],
                               sop, slot_col, slot_delta, ops=fops)
     return KernelLowering(index, kp.name, KIND_TAPE, flags, n_regs, tape, imms,
                           np.zeros(0, np.int32), slot_col, slot_delta, ops=fops)
@@ -336,15 +350,28 @@ def lower_kernel(plan, kp, index: int) -> KernelLowering:
 
 TAPE_BLOCK = 128
 SOP_BLOCK = 256
+SOP_VARIANTS = (4, 8, 16, 32)
 SMEM_LIMIT = 200 * 1024
 
 
 def block_size_for(n_regs: int) -> int:
-    """Largest block whose scratch file fits shared memory (>= 32 lanes)."""
+    """Largest tape block (128, 64 or 32 lanes) whose scratch file fits shared memory."""
     bs = TAPE_BLOCK
     while bs > 32 and n_regs * bs * 8 > SMEM_LIMIT:
         bs //= 2
     return bs
+
+
+def _stream_flags(plan, lowered, read_sets):
+    """Groups whose results no later kernel reads: their stores may evict-first."""
+    reads = [r for r in read_sets if r.size]
+    allr = np.unique(np.concatenate(reads)) if reads else np.zeros(0, np.int64)
+    for kl in lowered:
+        kp = plan.kernels[kl.index]
+        lo, hi = kp.dest_base, kp.dest_base + kp.n_roots * kp.instances
+        a, b = np.searchsorted(allr, [lo, hi])
+        if b == a:
+            kl.flags |= FLAG_STREAM
 
 
 def lower_plan(plan) -> DevicePlanArrays:
@@ -353,82 +380,89 @@ def lower_plan(plan) -> DevicePlanArrays:
     lowered = [lower_kernel(plan, kp, k) for k, kp in enumerate(plan.kernels)]
     for kl, w in zip(lowered, waves):
         kl.wave = w
+    _stream_flags(plan, lowered, read_sets)
     n_waves = (max(waves) + 1) if waves else 0
     groups = np.zeros(len(lowered), GROUP_DTYPE)
-    tapes, imms, sops, scol, sdel = [], [], [], [], []
+    tapes, imms, sops, scol, sdel, units = [], [], [], [], [], []
     n_tape = n_imm = n_sop = n_slot = 0
-    wave_group_begin = [0]
-    wave_blocks, wave_bs, wave_regs = [], [], []
     gi = 0
     for w in range(n_waves):
         members = [kl for kl in lowered if kl.wave == w]
-        tape_regs = max([kl.n_regs for kl in members if kl.kind == KIND_TAPE] or [0])
-        bs = block_size_for(tape_regs) if tape_regs else SOP_BLOCK
-        if any(kl.kind == KIND_TAPE for kl in members):
-            bs = min(bs, TAPE_BLOCK)
-        if tape_regs * bs * 8 > SMEM_LIMIT:
-            raise ValueError(f"wave {w}: template needs {tape_regs} scratch registers, "
-                             f"more than shared memory holds")
-        blk = 0
-        for kl in members:
-            kp = plan.kernels[kl.index]
-            g = groups[gi]
-            g["n"] = kp.instances
-            g["dest_base"] = kp.dest_base
-            g["p_off"] = kp.p_base
-            g["c_off"] = kp.c_base
-            g["n_roots"] = kp.n_roots
-            g["n_slots"] = len(kp.pos_vars)
-            g["n_ret"] = len(kp.retained)
-            g["n_const"] = len(kp.const_vars)
-            g["kind"] = kl.kind
-            g["flags"] = kl.flags
-            g["n_regs"] = kl.n_regs
-            g["wave"] = w
-            g["slot_off"] = n_slot
-            scol.append(kl.slot_col)
-            sdel.append(kl.slot_delta)
-            n_slot += len(kl.slot_col)
-            # immediates are renumbered into the plan-wide pool
-            t = kl.tape.copy()
-            if len(t):
-                is_imm = (t[:, 0] & 0xFFFF) == T_IMM
-                t[is_imm, 3] += n_imm
-            g["tape_off"] = n_tape
-            g["tape_len"] = len(t)
-            tapes.append(t)
-            n_tape += len(t)
-            imms.extend(kl.imms)
-            n_imm += len(kl.imms)
-            g["sop_off"] = n_sop
-            g["sop_len"] = len(kl.sop)
-            if kl.kind == KIND_SOP:
-                # device form: bit f of word 0 = factor f starts a term, word 1 = negate
-                newterm = sum(1 << f for f, d in enumerate(kl.sop.tolist()) if d & SOP_NEWTERM)
-                neg = sum(1 << f for f, d in enumerate(kl.sop.tolist()) if d & SOP_NEG)
-                words = np.array([newterm, neg], np.uint32).view(np.int32)
-                sops.append(words)
-                n_sop += 2
-            g["blk_begin"] = blk
-            if kl.flags & FLAG_SERIAL:
-                blk += 1
-            else:
-                blk += (kp.instances + bs - 1) // bs
-            gi += 1
-        wave_group_begin.append(gi)
-        wave_blocks.append(blk)
-        wave_bs.append(bs)
-        wave_regs.append(tape_regs)
-    cat = lambda xs, dt, shape=None: (np.concatenate(xs).astype(dt) if xs and sum(len(x) for x in xs)  # noqa: E731
-                                      else np.zeros(shape or 0, dt))
+        # launch units of this wave: one tape unit, one SOP unit per width class
+        plan_units = []
+        tape_m = [kl for kl in members if kl.kind == KIND_TAPE]
+        if tape_m:
+            regs = max(kl.n_regs for kl in tape_m)
+            bs = block_size_for(regs)
+            if regs * bs * 8 > SMEM_LIMIT:
+                raise ValueError(f"wave {w}: template needs {regs} scratch registers, "
+                                 f"more than shared memory holds")
+            plan_units.append((KIND_TAPE, bs, bs, regs, tape_m))
+        for var in SOP_VARIANTS:
+            lo = 0 if var == SOP_VARIANTS[0] else SOP_VARIANTS[SOP_VARIANTS.index(var) - 1]
+            sm = [kl for kl in members if kl.kind == KIND_SOP and lo < len(kl.sop) <= var]
+            if sm:
+                plan_units.append((KIND_SOP, var, SOP_BLOCK, 0, sm))
+        for kind, variant, bs, regs, ms in plan_units:
+            g_begin = gi
+            blk = 0
+            for kl in ms:
+                kp = plan.kernels[kl.index]
+                g = groups[gi]
+                g["n"] = kp.instances
+                g["dest_base"] = kp.dest_base
+                g["p_off"] = kp.p_base
+                g["c_off"] = kp.c_base
+                g["n_roots"] = kp.n_roots
+                g["n_slots"] = len(kp.pos_vars)
+                g["n_ret"] = len(kp.retained)
+                g["n_const"] = len(kp.const_vars)
+                g["kind"] = kl.kind
+                g["flags"] = kl.flags
+                g["n_regs"] = kl.n_regs
+                g["unit"] = len(units)
+                g["slot_off"] = n_slot
+                scol.append(kl.slot_col)
+                sdel.append(kl.slot_delta)
+                n_slot += len(kl.slot_col)
+                # immediates are renumbered into the plan-wide pool
+                t = kl.tape.copy()
+                if len(t):
+                    is_imm = (t & np.uint64(0x3F)) == np.uint64(T_IMM)
+                    if is_imm.any():
+                        k = ((t[is_imm] >> np.uint64(34)) & np.uint64(REG_MAX)) | \
+                            (((t[is_imm] >> np.uint64(48)) & np.uint64(REG_MAX)) << np.uint64(14))
+                        k = k + np.uint64(n_imm)
+                        if int(k.max()) >= (1 << 28):
+                            raise ValueError("more than 2^28 immediates")
+                        t[is_imm] = (t[is_imm] & np.uint64((1 << 34) - 1)) | \
+                            ((k & np.uint64(REG_MAX)) << np.uint64(34)) | ((k >> np.uint64(14)) << np.uint64(48))
+                g["tape_off"] = n_tape
+                g["tape_len"] = len(t)
+                tapes.append(t)
+                n_tape += len(t)
+                imms.extend(kl.imms)
+                n_imm += len(kl.imms)
+                g["sop_off"] = n_sop
+                g["sop_len"] = len(kl.sop)
+                if kl.kind == KIND_SOP:
+                    # device form: bit f of word 0 = factor f starts a term, word 1 = negate
+                    newterm = sum(1 << f for f, d in enumerate(kl.sop.tolist()) if d & SOP_NEWTERM)
+                    neg = sum(1 << f for f, d in enumerate(kl.sop.tolist()) if d & SOP_NEG)
+                    sops.append(np.array([newterm, neg], np.uint32).view(np.int32))
+                    n_sop += 2
+                g["blk_begin"] = blk
+                blk += 1 if kl.flags & FLAG_SERIAL else (kp.instances + bs - 1) // bs
+                gi += 1
+            units.append((w, kind, variant, g_begin, gi, blk, bs, regs))
+    cat = lambda xs, dt: (np.concatenate(xs).astype(dt) if xs and sum(len(x) for x in xs)  # noqa: E731
+                          else np.zeros(0, dt))
     exact = all(kl.flags & FLAG_EXACT for kl in lowered)
     return DevicePlanArrays(
         groups=groups,
-        wave_group_begin=np.asarray(wave_group_begin, np.int32),
-        wave_blocks=np.asarray(wave_blocks, np.int64),
-        wave_block_size=np.asarray(wave_bs, np.int32),
-        wave_smem_regs=np.asarray(wave_regs, np.int32),
-        tape=cat(tapes, np.int32, (0, 4)).reshape(-1, 4),
+        units=np.asarray(units, np.int64).reshape(-1, len(UNIT_FIELDS)),
+        n_waves=n_waves,
+        tape=cat(tapes, np.uint64),
         imm=np.asarray(imms, np.float64),
         sop=cat(sops, np.int32),
         slot_col=cat(scol, np.int32),

@@ -46,11 +46,10 @@ class _Desc(ctypes.Structure):
         ("input_count", ctypes.c_int64),
         ("n_groups", ctypes.c_int32),
         ("n_waves", ctypes.c_int32),
+        ("n_units", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
         ("groups", ctypes.c_void_p),
-        ("wave_group_begin", ctypes.c_void_p),
-        ("wave_blocks", ctypes.c_void_p),
-        ("wave_block_size", ctypes.c_void_p),
-        ("wave_smem_regs", ctypes.c_void_p),
+        ("units", ctypes.c_void_p),
         ("tape", ctypes.c_void_p),
         ("tape_rows", ctypes.c_int64),
         ("imm", ctypes.c_void_p),
@@ -72,7 +71,7 @@ class _Desc(ctypes.Structure):
 SYMBOLS = (
     "sgb_plan_create", "sgb_plan_destroy", "sgb_run_values", "sgb_gather_outputs",
     "sgb_sg_run", "sgb_run_outputs_host", "sgb_run_batch", "sgb_gather_outputs_batch",
-    "sgb_plan_launches", "sgb_last_error", "sgb_run_wave",
+    "sgb_plan_launches", "sgb_last_error", "sgb_run_wave", "sgb_plan_units",
 )
 
 
@@ -99,6 +98,7 @@ def load_library(path: Path | str | None = None):
             "sgb_run_batch": (i32, [vp, vp, i64, i64, vp]),
             "sgb_gather_outputs_batch": (i32, [vp, vp, i64, i64, vp, i64, vp]),
             "sgb_plan_launches": (i32, [vp]),
+            "sgb_plan_units": (i32, [vp]),
             "sgb_last_error": (ctypes.c_char_p, []),
         }
         for name, (res, args) in sig.items():
@@ -149,11 +149,8 @@ class DevicePlan:
         lw = self.lowered
         keep = dict(
             groups=np.ascontiguousarray(lw.groups, GROUP_DTYPE),
-            wgb=np.ascontiguousarray(lw.wave_group_begin, np.int32),
-            wb=np.ascontiguousarray(lw.wave_blocks, np.int64),
-            wbs=np.ascontiguousarray(lw.wave_block_size, np.int32),
-            wr=np.ascontiguousarray(lw.wave_smem_regs, np.int32),
-            tape=np.ascontiguousarray(lw.tape, np.int32),
+            units=np.ascontiguousarray(lw.units, np.int64),
+            tape=np.ascontiguousarray(lw.tape, np.uint64),
             imm=np.ascontiguousarray(lw.imm, np.float64),
             sop=np.ascontiguousarray(lw.sop, np.int32),
             scol=np.ascontiguousarray(lw.slot_col, np.int32),
@@ -164,11 +161,9 @@ class DevicePlan:
         )
         d = _Desc(
             value_array_size=self.value_array_size, input_count=self.input_count,
-            n_groups=len(keep["groups"]), n_waves=len(keep["wb"]),
-            groups=_ptr(keep["groups"]), wave_group_begin=_ptr(keep["wgb"]),
-            wave_blocks=_ptr(keep["wb"]), wave_block_size=_ptr(keep["wbs"]),
-            wave_smem_regs=_ptr(keep["wr"]), tape=_ptr(keep["tape"]),
-            tape_rows=len(keep["tape"]), imm=_ptr(keep["imm"]), n_imm=keep["imm"].size,
+            n_groups=len(keep["groups"]), n_waves=lw.n_waves, n_units=len(keep["units"]),
+            groups=_ptr(keep["groups"]), units=_ptr(keep["units"]), tape=_ptr(keep["tape"]),
+            tape_rows=keep["tape"].size, imm=_ptr(keep["imm"]), n_imm=keep["imm"].size,
             sop=_ptr(keep["sop"]), n_sop=keep["sop"].size, slot_col=_ptr(keep["scol"]),
             slot_delta=_ptr(keep["sdel"]), n_slot=keep["scol"].size, positions=_ptr(keep["pos"]),
             n_positions=keep["pos"].size, constants=_ptr(keep["con"]), n_constants=keep["con"].size,
@@ -177,7 +172,8 @@ class DevicePlan:
         torch.cuda.init()
         _check(self._lib.sgb_plan_create(ctypes.byref(d), self.device, ctypes.byref(self._handle)),
                "sgb_plan_create")
-        self.launches = int(self._lib.sgb_plan_launches(self._handle))
+        self.launches = int(self._lib.sgb_plan_launches(self._handle))  # waves
+        self.units = int(self._lib.sgb_plan_units(self._handle))  # kernel launches per evaluation
 
     def close(self):
         if self._handle:

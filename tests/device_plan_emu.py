@@ -89,9 +89,10 @@ def _vec(fn, a):
 def run_values(dp, inputs) -> np.ndarray:
     x = np.zeros(dp.value_array_size, np.float64)
     x[: dp.input_count] = inputs
-    for w in range(dp.n_waves):
-        # all groups of a wave read the state before the wave (one launch)
-        for gi in range(dp.wave_group_begin[w], dp.wave_group_begin[w + 1]):
+    for u in range(len(dp.units)):
+        # groups of one wave are independent; units run in wave order
+        unit = dp.unit(u)
+        for gi in range(unit["group_begin"], unit["group_end"]):
             g = dp.groups[gi]
             n = int(g["n"])
             if g["flags"] & L.FLAG_SERIAL:
@@ -132,16 +133,14 @@ def _tape(dp, g, x, i):
             R[s] = x[a].copy()
         for k in range(K):
             R[S + k] = _const(dp, g, k, i).copy()
-        for row in dp.tape[g["tape_off"]: g["tape_off"] + g["tape_len"]]:
-            w0, w1, w2, aux = (int(v) & 0xFFFFFFFF for v in row)
-            op, dst = w0 & 0xFFFF, w0 >> 16
-            a, b = w1 & 0xFFFF, w1 >> 16
+        for word in dp.tape[g["tape_off"]: g["tape_off"] + g["tape_len"]].tolist():
+            op, dst, a, b, c = L.decode(int(word))
             if op == L.T_ST:
-                if not selfref or aux == ph:
-                    x[g["dest_base"] + aux * n + i] = R[a]
+                if not selfref or c == ph:
+                    x[g["dest_base"] + c * n + i] = R[a]
                 continue
             if op == L.T_IMM:
-                v = np.full(len(i), dp.imm[aux])
+                v = np.full(len(i), dp.imm[b | (c << 14)])
             elif op == L.T_ADD:
                 v = R[a] + R[b]
             elif op == L.T_SUB:
@@ -165,9 +164,8 @@ def _tape(dp, g, x, i):
             elif op == L.T_LOG:
                 v = _vec(math.log, R[a])
             elif op == L.T_POW:
-                v = _dd_powi(R[a], aux)
+                v = _dd_powi(R[a], c)
             elif op == L.T_SEL:
-                c = w2 & 0xFFFFFFFF
                 v = np.where(R[a] < 0.0, R[b], R[c])
             else:
                 raise ValueError(f"bad op {op}")

@@ -1,0 +1,39 @@
+"""Short evaluation loop for ncu captures (not a benchmark: numbers under a profiler are not bench values)."""
+import argparse
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--w", type=int, default=1000)
+ap.add_argument("--evals", type=int, default=3)
+ap.add_argument("--batch", type=int, default=0)
+args = ap.parse_args()
+
+import torch  # noqa: E402
+
+from paper_2110_12865_b200 import DevicePlan  # noqa: E402
+from paper_2110_12865_b200.programs.mesh import build_lmlt_plan, lmlt_inputs  # noqa: E402
+
+t0 = time.time()
+plan, _, _ = build_lmlt_plan(args.w)
+print(f"plan built in {time.time() - t0:.1f}s: {len(plan.kernels)} kernels, {len(plan.outputs)} outputs", flush=True)
+dp = DevicePlan(plan)
+print("waves", dp.launches, flush=True)
+if args.batch:
+    X = torch.zeros((plan.value_array_size, args.batch), dtype=torch.float64, device="cuda")
+    X[: plan.input_count] = torch.from_numpy(lmlt_inputs(args.w)).cuda()[:, None]
+    for _ in range(args.evals):
+        dp.run_batch(X)
+        dp.gather_outputs_batch(X)
+else:
+    x = dp.new_values(lmlt_inputs(args.w))
+    out = torch.empty(len(plan.outputs), dtype=torch.float64, device="cuda")
+    for _ in range(args.evals):
+        dp.run_values(x)
+        dp.gather_outputs(x, out)
+torch.cuda.synchronize()
+print("done", flush=True)
