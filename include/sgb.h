@@ -39,7 +39,7 @@ extern "C" {
 
 typedef struct sgb_plan sgb_plan;
 
-/* One kernel group of the device plan (== lower.GROUP_DTYPE, 96 bytes).
+/* One kernel group of the device plan (== lower.GROUP_DTYPE, 112 bytes).
  * Mirrors one reference KernelPlan (codegen.py:56-85). */
 typedef struct sgb_group {
   int64_t n;         /* instances (KernelPlan.instances) */
@@ -47,7 +47,9 @@ typedef struct sgb_group {
   int64_t p_off;     /* KernelPlan.p_base */
   int64_t c_off;     /* KernelPlan.c_base */
   int64_t tape_off;  /* first tape row */
-  int64_t blk_begin; /* first block of this group inside its wave launch */
+  int64_t blk_begin; /* first block of this group inside its launch unit */
+  int64_t cb_off;    /* compressed columns (flags & 32): first chunk base in cbase */
+  int64_t co_off;    /*                                  first offset in coff */
   int32_t n_roots, n_slots, n_ret, n_const;
   int32_t tape_len, n_regs, kind, flags;
   int32_t slot_off, sop_off, sop_len, unit;
@@ -79,6 +81,10 @@ typedef struct sgb_plan_desc {
   int64_t n_positions;
   const double *constants; /* ExecutionPlan.constants (f64, unchanged) */
   int64_t n_constants;
+  const uint32_t *cbase; /* compressed index columns: base per (column, 32 instances) */
+  int64_t n_cbase;
+  const uint16_t *coff; /* compressed index columns: offset per (column, instance) */
+  int64_t n_coff;
   const int64_t *outputs; /* ExecutionPlan.outputs */
   int64_t n_outputs;
 } sgb_plan_desc;

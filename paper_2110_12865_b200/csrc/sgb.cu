@@ -42,7 +42,7 @@ enum : int {
   T_EXP = 10, T_LOG = 11, T_POW = 12, T_SEL = 13, T_IMM = 20, T_ST = 21
 };
 enum : int { KIND_TAPE = 0, KIND_SOP = 1 };
-enum : int { FLAG_SELFREF = 1, FLAG_INTERLEAVED = 2, FLAG_SERIAL = 4, FLAG_STREAM = 16 };
+enum : int { FLAG_SELFREF = 1, FLAG_INTERLEAVED = 2, FLAG_SERIAL = 4, FLAG_STREAM = 16, FLAG_W16 = 32 };
 enum : int { U_WAVE = 0, U_KIND, U_VARIANT, U_G0, U_G1, U_BLOCKS, U_BS, U_REGS, U_COUNT };
 constexpr int PRE = 8;  // slot loads kept in flight by the tape prologue
 constexpr int MAX_BATCH_WARPS = 8;
@@ -71,6 +71,8 @@ struct Tables {
   const int64_t *slot_delta;
   const uint32_t *pos;
   const double *con;
+  const uint32_t *cbase;  // compressed columns: per (column, 32-instance chunk) base
+  const uint16_t *coff;   //                     per (column, instance) offset
 };
 
 // ---- cache-policy helpers ---------------------------------------------------------
@@ -109,6 +111,22 @@ __device__ __forceinline__ int find_group(const int64_t *begin, int g0, int g1, 
   return lo;
 }
 
+// Retained column `col` of instance i: the plan's u32 table, or the compressed
+// form base[col][i/32] + off16[col][i] (lower.compress_columns).
+__device__ __forceinline__ uint32_t column_index(const Tables &T, const sgb_group &G, int col, int64_t i,
+                                                 bool inter, uint64_t pol) {
+  if (G.flags & FLAG_W16) {
+    const int64_t nch = (G.n + 31) >> 5;
+    const uint32_t base = __ldg(T.cbase + G.cb_off + (int64_t)col * nch + (i >> 5));
+    uint16_t off;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;"
+                 : "=h"(off) : "l"(T.coff + G.co_off + (int64_t)col * G.n + i), "l"(pol));
+    return base + off;
+  }
+  const int64_t e = inter ? G.p_off + i * G.n_ret + col : G.p_off + (int64_t)col * G.n + i;
+  return ld_index(T.pos + e, pol);
+}
+
 // Index decode == slot_addresses (codegen.py:373-388): retained slot -> its
 // column of the position table; coherent slot -> slot-0 entry + delta.
 __device__ __forceinline__ int64_t slot_addr(const Tables &T, const sgb_group &G, int s, int64_t i,
@@ -116,15 +134,13 @@ __device__ __forceinline__ int64_t slot_addr(const Tables &T, const sgb_group &G
   const int col = __ldg(T.slot_col + G.slot_off + s);
   if (col < 0) return (int64_t)idx0 + __ldg(T.slot_delta + G.slot_off + s);
   if (col == 0) return idx0;
-  const int64_t e = inter ? G.p_off + i * G.n_ret + col : G.p_off + (int64_t)col * G.n + i;
-  return (int64_t)ld_index(T.pos + e, pol);
+  return (int64_t)column_index(T, G, col, i, inter, pol);
 }
 
 __device__ __forceinline__ uint32_t slot0_index(const Tables &T, const sgb_group &G, int64_t i,
                                                 bool inter, uint64_t pol) {
   if (G.n_slots == 0) return 0u;
-  const int64_t e = inter ? G.p_off + i * G.n_ret : G.p_off + i;
-  return ld_index(T.pos + e, pol);
+  return column_index(T, G, 0, i, inter, pol);
 }
 
 // ---- double-double integer power (POW k >= 3; k == 2 is an exact x*x) ----------
@@ -416,7 +432,8 @@ struct sgb_plan {
   double *d_imm = nullptr, *d_con = nullptr;
   int32_t *d_sop = nullptr, *d_scol = nullptr;
   int64_t *d_sdel = nullptr;
-  uint32_t *d_pos = nullptr;
+  uint32_t *d_pos = nullptr, *d_cbase = nullptr;
+  uint16_t *d_coff = nullptr;
   // workspace for the host-buffer entry points
   std::mutex ws_mu;
   double *d_x = nullptr, *d_out = nullptr;
@@ -487,7 +504,7 @@ void sgb_plan_destroy(sgb_plan *p) {
   if (!p) return;
   cudaSetDevice(p->device);
   void *bufs[] = {p->d_groups, p->d_blk, p->d_bblk, p->d_outputs, p->d_tape, p->d_imm, p->d_con,
-                  p->d_sop, p->d_scol, p->d_sdel, p->d_pos, p->d_x, p->d_out};
+                  p->d_sop, p->d_scol, p->d_sdel, p->d_pos, p->d_x, p->d_out, p->d_cbase, p->d_coff};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (p->ws_stream) cudaStreamDestroy(p->ws_stream);
@@ -520,7 +537,10 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
         G.c_off + (int64_t)G.n_const * G.n > d->n_constants || G.tape_off < 0 ||
         G.tape_off + G.tape_len > d->tape_rows || G.slot_off < 0 || G.slot_off + G.n_slots > d->n_slot ||
         (G.n_slots > 0 && G.n_ret < 1) ||
-        (G.kind == KIND_SOP && (G.sop_len > 32 || G.sop_len != G.n_slots || G.sop_off + 2 > d->n_sop));
+        (G.kind == KIND_SOP && (G.sop_len > 32 || G.sop_len != G.n_slots || G.sop_off + 2 > d->n_sop)) ||
+        ((G.flags & FLAG_W16) && (G.cb_off < 0 || G.co_off < 0 ||
+                                  G.cb_off + (int64_t)G.n_ret * ((G.n + 31) / 32) > d->n_cbase ||
+                                  G.co_off + (int64_t)G.n_ret * G.n > d->n_coff));
     if (bad) return fail(-1, "sgb_plan_create: group " + std::to_string(g) + " is out of range");
     for (int s = 0; s < G.n_slots; ++s)
       if (d->slot_col[G.slot_off + s] >= G.n_ret) return fail(-1, "sgb_plan_create: bad slot column");
@@ -528,6 +548,15 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
   for (int64_t k = 0; k < d->n_positions; ++k)
     if ((int64_t)d->positions[k] >= d->value_array_size)
       return fail(-1, "sgb_plan_create: position index outside the value array");
+  for (int g = 0; g < d->n_groups; ++g) {  // compressed columns decode inside the value array
+    const sgb_group &G = d->groups[g];
+    if (!(G.flags & FLAG_W16)) continue;
+    const int64_t nch = (G.n + 31) / 32;
+    for (int c = 0; c < G.n_ret; ++c)
+      for (int64_t i = 0; i < G.n; ++i)
+        if ((int64_t)d->cbase[G.cb_off + c * nch + i / 32] + d->coff[G.co_off + c * G.n + i] >= d->value_array_size)
+          return fail(-1, "sgb_plan_create: compressed index outside the value array");
+  }
   for (int64_t k = 0; k < d->n_outputs; ++k)
     if (d->outputs[k] < 0 || d->outputs[k] >= d->value_array_size)
       return fail(-1, "sgb_plan_create: output offset outside the value array");
@@ -575,9 +604,11 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       (rc = upload(&p->d_sop, d->sop, d->n_sop)) || (rc = upload(&p->d_scol, d->slot_col, d->n_slot)) ||
       (rc = upload(&p->d_sdel, d->slot_delta, d->n_slot)) ||
       (rc = upload(&p->d_pos, d->positions, d->n_positions)) ||
-      (rc = upload(&p->d_con, d->constants, d->n_constants)))
+      (rc = upload(&p->d_con, d->constants, d->n_constants)) ||
+      (rc = upload(&p->d_cbase, d->cbase, d->n_cbase)) || (rc = upload(&p->d_coff, d->coff, d->n_coff)))
     return rc;
-  p->T = Tables{p->d_groups, p->d_tape, p->d_imm, p->d_sop, p->d_scol, p->d_sdel, p->d_pos, p->d_con};
+  p->T = Tables{p->d_groups, p->d_tape, p->d_imm, p->d_sop, p->d_scol, p->d_sdel,
+                p->d_pos, p->d_con, p->d_cbase, p->d_coff};
   return 0;
 }
 

@@ -41,14 +41,15 @@ T_SIN, T_COS, T_EXP, T_LOG, T_POW, T_SEL = 8, 9, 10, 11, 12, 13
 T_IMM, T_ST = 20, 21
 
 KIND_TAPE, KIND_SOP = 0, 1
-FLAG_SELFREF, FLAG_INTERLEAVED, FLAG_SERIAL, FLAG_EXACT, FLAG_STREAM = 1, 2, 4, 8, 16
+FLAG_SELFREF, FLAG_INTERLEAVED, FLAG_SERIAL, FLAG_EXACT, FLAG_STREAM, FLAG_W16 = 1, 2, 4, 8, 16, 32
+CHUNK = 32  # instances per compressed-index chunk (one warp in single-set mode)
 SOP_NEWTERM, SOP_NEG = 1, 2
 SOP_MAX = 32  # factors per sum-of-products template (csrc SOP_MAX)
 
 # one record per group, mirrored by struct sgb_group in include/sgb.h
 GROUP_DTYPE = np.dtype([
     ("n", "<i8"), ("dest_base", "<i8"), ("p_off", "<i8"), ("c_off", "<i8"),
-    ("tape_off", "<i8"), ("blk_begin", "<i8"),
+    ("tape_off", "<i8"), ("blk_begin", "<i8"), ("cb_off", "<i8"), ("co_off", "<i8"),
     ("n_roots", "<i4"), ("n_slots", "<i4"), ("n_ret", "<i4"), ("n_const", "<i4"),
     ("tape_len", "<i4"), ("n_regs", "<i4"), ("kind", "<i4"), ("flags", "<i4"),
     ("slot_off", "<i4"), ("sop_off", "<i4"), ("sop_len", "<i4"), ("unit", "<i4"),
@@ -56,7 +57,7 @@ GROUP_DTYPE = np.dtype([
 
 # one row per launch unit (int64 x 8), mirrored by include/sgb.h SGB_UNIT_*
 UNIT_FIELDS = ("wave", "kind", "variant", "group_begin", "group_end", "blocks", "block_size", "smem_regs")
-assert GROUP_DTYPE.itemsize == 96
+assert GROUP_DTYPE.itemsize == 112
 
 
 @dataclass
@@ -87,6 +88,8 @@ class DevicePlanArrays:
     sop: np.ndarray  # int32
     slot_col: np.ndarray  # int32
     slot_delta: np.ndarray  # int64
+    cbase: np.ndarray  # u32 per (column, 32-instance chunk) base of compressed columns
+    coff: np.ndarray  # u16 per (column, instance) offset from its chunk base
     positions: np.ndarray  # u32 (the plan's table, unchanged)
     constants: np.ndarray  # f64 (the plan's table, unchanged)
     outputs: np.ndarray  # int64
@@ -374,7 +377,29 @@ def _stream_flags(plan, lowered, read_sets):
             kl.flags |= FLAG_STREAM
 
 
-def lower_plan(plan) -> DevicePlanArrays:
+def compress_columns(plan, kp):
+    """Per-chunk base + u16 offset encoding of a group's retained index columns.
+
+    Column r of instance i decodes to ``cbase[r*nchunks + i//32] + coff[r*N + i]``:
+    2 bytes per entry plus 4 bytes per 32 instances instead of 4 bytes per
+    entry.  Returns None when some chunk spans 65536 addresses or more (the
+    group then keeps the plan's u32 table) or the layout is interleaved.
+    """
+    n, r = kp.instances, len(kp.retained)
+    if kp.layout != "coalesced" or r == 0 or n < CHUNK:
+        return None
+    cols = np.asarray(plan.positions[kp.p_base: kp.p_base + r * n], dtype=np.int64).reshape(r, n)
+    nch = (n + CHUNK - 1) // CHUNK
+    pad = nch * CHUNK - n
+    padded = np.concatenate([cols, np.repeat(cols[:, -1:], pad, axis=1)], axis=1).reshape(r, nch, CHUNK)
+    lo = padded.min(axis=2)
+    if int((padded.max(axis=2) - lo).max()) >= 1 << 16:
+        return None
+    off = (padded - lo[:, :, None]).reshape(r, nch * CHUNK)[:, :n]
+    return lo.astype(np.uint32).reshape(-1), off.astype(np.uint16).reshape(-1)
+
+
+def lower_plan(plan, compress: bool = True) -> DevicePlanArrays:
     read_sets = _read_sets(plan)
     waves = compute_waves(plan, read_sets)
     lowered = [lower_kernel(plan, kp, k) for k, kp in enumerate(plan.kernels)]
@@ -383,8 +408,8 @@ def lower_plan(plan) -> DevicePlanArrays:
     _stream_flags(plan, lowered, read_sets)
     n_waves = (max(waves) + 1) if waves else 0
     groups = np.zeros(len(lowered), GROUP_DTYPE)
-    tapes, imms, sops, scol, sdel, units = [], [], [], [], [], []
-    n_tape = n_imm = n_sop = n_slot = 0
+    tapes, imms, sops, scol, sdel, units, cbases, coffs = [], [], [], [], [], [], [], []
+    n_tape = n_imm = n_sop = n_slot = n_cb = n_co = 0
     gi = 0
     for w in range(n_waves):
         members = [kl for kl in lowered if kl.wave == w]
@@ -452,6 +477,14 @@ def lower_plan(plan) -> DevicePlanArrays:
                     sops.append(np.array([newterm, neg], np.uint32).view(np.int32))
                     n_sop += 2
                 g["blk_begin"] = blk
+                comp = compress_columns(plan, kp) if compress else None
+                if comp is not None:
+                    g["flags"] |= FLAG_W16
+                    g["cb_off"], g["co_off"] = n_cb, n_co
+                    cbases.append(comp[0])
+                    coffs.append(comp[1])
+                    n_cb += comp[0].size
+                    n_co += comp[1].size
                 blk += 1 if kl.flags & FLAG_SERIAL else (kp.instances + bs - 1) // bs
                 gi += 1
             units.append((w, kind, variant, g_begin, gi, blk, bs, regs))
@@ -467,6 +500,8 @@ def lower_plan(plan) -> DevicePlanArrays:
         sop=cat(sops, np.int32),
         slot_col=cat(scol, np.int32),
         slot_delta=cat(sdel, np.int64),
+        cbase=cat(cbases, np.uint32),
+        coff=cat(coffs, np.uint16),
         positions=np.ascontiguousarray(plan.positions, dtype=np.uint32),
         constants=np.ascontiguousarray(plan.constants, dtype=np.float64),
         outputs=np.asarray(plan.outputs, np.int64),

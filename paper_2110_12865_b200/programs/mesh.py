@@ -211,7 +211,7 @@ def build_lmlt_plan(w: int, a_nnz: int = 6, a_seed: int = 7, a_cols: np.ndarray 
         sel = np.flatnonzero(counts == cnt)
         cols = [w_addr[fid[starts[sel] + s], cid[starts[sel] + s]] for s in range(cnt)]
         T, r = _sum_template(int(cnt))
-        ldiag_addr[verts[sel]] = B.add_group(f"ldiag{cnt}", 2, T, r, cols)[0]
+        ldiag_addr[verts[sel]] = B.add_group_split(f"ldiag{cnt}", 2, T, r, cols)[0]
         ldiag_sh[verts[sel]] = S.sh_apply(S.ADD, [sh_w] * int(cnt))
 
     # ---- L off-diagonal per undirected edge: -w or -w1 + -w2 ----
@@ -229,7 +229,7 @@ def build_lmlt_plan(w: int, a_nnz: int = 6, a_seed: int = 7, a_cols: np.ndarray 
         sel = np.flatnonzero(ecounts == cnt)
         cols = [wa_s[estarts[sel] + s] for s in range(cnt)]
         T, r = _sum_template(int(cnt), neg=True)
-        eaddr[sel] = B.add_group(f"loff{cnt}", 2, T, r, cols)[0]
+        eaddr[sel] = B.add_group_split(f"loff{cnt}", 2, T, r, cols)[0]
         esh[sel] = sh_negw if cnt == 1 else S.sh_apply(S.ADD, [sh_negw] * int(cnt))
 
     # ---- M diagonal: area shares in face order ----
@@ -248,7 +248,7 @@ def build_lmlt_plan(w: int, a_nnz: int = 6, a_seed: int = 7, a_cols: np.ndarray 
             continue
         cols = [area_addr[mf[mstarts[sel] + s]] for s in range(cnt)]
         T, r = _sum_template(int(cnt))
-        m_addr[mverts[sel]] = B.add_group(f"mdiag{cnt}", 2, T, r, cols)[0]
+        m_addr[mverts[sel]] = B.add_group_split(f"mdiag{cnt}", 2, T, r, cols)[0]
         m_sh[mverts[sel]] = S.sh_apply(S.ADD, [sh_area] * int(cnt))
 
     # ---- L in CSR: diagonal + both directions of every edge ----
@@ -265,7 +265,7 @@ def build_lmlt_plan(w: int, a_nnz: int = 6, a_seed: int = 7, a_cols: np.ndarray 
 
     # ---- LM = L * M (one term per entry) ----
     T, r = _product_template()
-    lm_addr = B.add_group("lm", 1, T, r, [L_addr, m_addr[L_col]])[0]
+    lm_addr = B.add_group_split("lm", 1, T, r, [L_addr, m_addr[L_col]])[0]
     # struct-hash classes: intern the (few) distinct hashes as small ints
     classes: dict[int, int] = {}
     cls_val: list[int] = []
@@ -333,7 +333,8 @@ def build_lmlt_plan(w: int, a_nnz: int = 6, a_seed: int = 7, a_cols: np.ndarray 
             if wa_flag:
                 cols.append(a_var[a_pos[out_slot[sel]]])
             T, r = _sop_template(int(m), wa_flag)
-            res = B.add_group(f"out{m}{'a' if wa_flag else ''}", 0, T, r, cols, dest_kind="output")
+            res = B.add_group_split(f"out{m}{'a' if wa_flag else ''}", 0, T, r, cols, dest_kind="output",
+                                    keep_cols=(2 * int(m),) if wa_flag else ())
             outputs[out_slot[sel]] = res[0]
     out_rows = out_keys // n
     row_ptr = np.zeros(n + 1, np.int64)

@@ -83,6 +83,68 @@ class PlanBuilder:
         self.kernels.append(kp)
         return dest + np.arange(len(roots), dtype=np.int64)[:, None] * n + np.arange(n, dtype=np.int64)[None, :]
 
+    def producer_ids(self, addrs: np.ndarray) -> np.ndarray:
+        """Group index whose result range holds each address (-1 = input value)."""
+        starts = np.array([kp.dest_base for kp in self.kernels], dtype=np.int64)
+        gid = np.searchsorted(starts, addrs, side="right") - 1
+        return np.where(addrs < self.input_count, -1, gid)
+
+    def add_group_split(self, name: str, level: int, template: Template, roots: list[int],
+                        slot_addrs: list[np.ndarray], const_cols: list[np.ndarray] | None = None,
+                        dest_kind: str = "intermediate", min_class: int = 1024,
+                        min_source_class: int = 64, keep_cols: tuple = ()) -> np.ndarray:
+        """``add_group`` split so every sub-group gathers from fixed sources.
+
+        1. Instances are partitioned by *source signature* -- which producer
+           group (or the input range) each slot reads -- so a slot of a
+           sub-group walks one producer's result range in step with the
+           instances: compact per-chunk index windows (lower.compress_columns).
+        2. Inside a source class, instances with identical offsets from slot 0
+           (the reference's coherence test, codegen.py:317-327) form their own
+           sub-group with a single index column when the class has at least
+           ``min_class`` members.
+        Small classes fall into one residual sub-group.  Slots in ``keep_cols``
+        stay out of the offset signature.  Sub-groups keep the original
+        relative instance order; result addresses come back in original order.
+        """
+        cols = [np.asarray(c, dtype=np.int64) for c in slot_addrs]
+        n = len(cols[0]) if cols else 0
+        if n == 0 or not cols:
+            return self.add_group(name, level, template, roots, slot_addrs, const_cols, dest_kind)
+        src = np.stack([self.producer_ids(c) for c in cols], axis=1)
+        _, sinv, scnt = np.unique(src, axis=0, return_inverse=True, return_counts=True)
+        sinv = sinv.reshape(-1)
+        sinv = np.where(scnt[sinv] >= min_source_class, sinv, -1)
+        sig_slots = [s for s in range(1, len(cols)) if s not in keep_cols]
+        label = np.full(n, -1, dtype=np.int64)
+        next_label = 0
+        for sc in np.unique(sinv).tolist():
+            members = np.flatnonzero(sinv == sc)
+            if sc < 0 or not sig_slots:
+                label[members] = next_label
+                next_label += 1
+                continue
+            D = np.stack([cols[s][members] - cols[0][members] for s in sig_slots], axis=1)
+            _, inv, counts = np.unique(D, axis=0, return_inverse=True, return_counts=True)
+            inv = inv.reshape(-1)
+            big = counts >= min_class
+            uniq_big = {c: next_label + k for k, c in enumerate(np.flatnonzero(big).tolist())}
+            next_label += len(uniq_big)
+            rest = next_label
+            next_label += 1
+            label[members] = np.array([uniq_big.get(c, rest) for c in inv.tolist()], dtype=np.int64) \
+                if len(uniq_big) else rest
+        out = np.empty((len(roots), n), dtype=np.int64)
+        order = np.argsort(label, kind="stable")
+        keys, starts = np.unique(label[order], return_index=True)
+        ends = np.append(starts[1:], n)
+        for k, (a, b) in enumerate(zip(starts.tolist(), ends.tolist())):
+            sel = order[a:b]
+            sub_const = [np.asarray(c)[sel] for c in (const_cols or [])]
+            out[:, sel] = self.add_group(f"{name}_{k}", level, template, roots, [c[sel] for c in cols],
+                                         sub_const, dest_kind)
+        return out
+
     def finish(self, outputs: np.ndarray, metadata: dict) -> ExecutionPlan:
         outputs = np.asarray(outputs, dtype=np.int64)
         return ExecutionPlan(

@@ -63,6 +63,10 @@ class _Desc(ctypes.Structure):
         ("n_positions", ctypes.c_int64),
         ("constants", ctypes.c_void_p),
         ("n_constants", ctypes.c_int64),
+        ("cbase", ctypes.c_void_p),
+        ("n_cbase", ctypes.c_int64),
+        ("coff", ctypes.c_void_p),
+        ("n_coff", ctypes.c_int64),
         ("outputs", ctypes.c_void_p),
         ("n_outputs", ctypes.c_int64),
     ]
@@ -157,6 +161,8 @@ class DevicePlan:
             sdel=np.ascontiguousarray(lw.slot_delta, np.int64),
             pos=np.ascontiguousarray(lw.positions, np.uint32),
             con=np.ascontiguousarray(lw.constants, np.float64),
+            cbase=np.ascontiguousarray(lw.cbase, np.uint32),
+            coff=np.ascontiguousarray(lw.coff, np.uint16),
             outs=np.ascontiguousarray(lw.outputs, np.int64),
         )
         d = _Desc(
@@ -167,7 +173,8 @@ class DevicePlan:
             sop=_ptr(keep["sop"]), n_sop=keep["sop"].size, slot_col=_ptr(keep["scol"]),
             slot_delta=_ptr(keep["sdel"]), n_slot=keep["scol"].size, positions=_ptr(keep["pos"]),
             n_positions=keep["pos"].size, constants=_ptr(keep["con"]), n_constants=keep["con"].size,
-            outputs=_ptr(keep["outs"]), n_outputs=keep["outs"].size,
+            cbase=_ptr(keep["cbase"]), n_cbase=keep["cbase"].size, coff=_ptr(keep["coff"]),
+            n_coff=keep["coff"].size, outputs=_ptr(keep["outs"]), n_outputs=keep["outs"].size,
         )
         torch.cuda.init()
         _check(self._lib.sgb_plan_create(ctypes.byref(d), self.device, ctypes.byref(self._handle)),

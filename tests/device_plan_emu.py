@@ -26,8 +26,15 @@ def _decode_addrs(dp, g, i):
     n, nret = int(g["n"]), int(g["n_ret"])
     if n_slots == 0:
         return []
-    e0 = g["p_off"] + (i * nret if inter else i)
-    idx0 = dp.positions[e0].astype(np.int64)
+    def column(col):
+        if g["flags"] & L.FLAG_W16:
+            nch = (n + L.CHUNK - 1) // L.CHUNK
+            base = dp.cbase[g["cb_off"] + col * nch + i // L.CHUNK].astype(np.int64)
+            return base + dp.coff[g["co_off"] + col * n + i].astype(np.int64)
+        e = g["p_off"] + (i * nret + col if inter else col * n + i)
+        return dp.positions[e].astype(np.int64)
+
+    idx0 = column(0)
     out = []
     for s in range(n_slots):
         col = int(cols[s])
@@ -36,8 +43,7 @@ def _decode_addrs(dp, g, i):
         elif col == 0:
             out.append(idx0)
         else:
-            e = g["p_off"] + (i * nret + col if inter else col * n + i)
-            out.append(dp.positions[e].astype(np.int64))
+            out.append(column(col))
     return out
 
 
