@@ -39,7 +39,7 @@ extern "C" {
 
 typedef struct sgb_plan sgb_plan;
 
-/* One kernel group of the device plan (== lower.GROUP_DTYPE, 112 bytes).
+/* One kernel group of the device plan (== lower.GROUP_DTYPE, 128 bytes).
  * Mirrors one reference KernelPlan (codegen.py:56-85). */
 typedef struct sgb_group {
   int64_t n;         /* instances (KernelPlan.instances) */
@@ -50,6 +50,8 @@ typedef struct sgb_group {
   int64_t blk_begin; /* first block of this group inside its launch unit */
   int64_t cb_off;    /* compressed columns (flags & 32): first chunk base in cbase */
   int64_t co_off;    /*                                  first offset in coff */
+  int64_t a0_base;   /* affine column 0 (flags & 64): index = a0_base + a0_stride * i */
+  int64_t a0_stride;
   int32_t n_roots, n_slots, n_ret, n_const;
   int32_t tape_len, n_regs, kind, flags;
   int32_t slot_off, sop_off, sop_len, unit;

@@ -42,7 +42,9 @@ enum : int {
   T_EXP = 10, T_LOG = 11, T_POW = 12, T_SEL = 13, T_IMM = 20, T_ST = 21
 };
 enum : int { KIND_TAPE = 0, KIND_SOP = 1 };
-enum : int { FLAG_SELFREF = 1, FLAG_INTERLEAVED = 2, FLAG_SERIAL = 4, FLAG_STREAM = 16, FLAG_W16 = 32 };
+enum : int {
+  FLAG_SELFREF = 1, FLAG_INTERLEAVED = 2, FLAG_SERIAL = 4, FLAG_STREAM = 16, FLAG_W16 = 32, FLAG_AFFINE0 = 64
+};
 enum : int { U_WAVE = 0, U_KIND, U_VARIANT, U_G0, U_G1, U_BLOCKS, U_BS, U_REGS, U_COUNT };
 constexpr int PRE = 8;  // slot loads kept in flight by the tape prologue
 constexpr int MAX_BATCH_WARPS = 8;
@@ -115,6 +117,7 @@ __device__ __forceinline__ int find_group(const int64_t *begin, int g0, int g1, 
 // form base[col][i/32] + off16[col][i] (lower.compress_columns).
 __device__ __forceinline__ uint32_t column_index(const Tables &T, const sgb_group &G, int col, int64_t i,
                                                  bool inter, uint64_t pol) {
+  if (col == 0 && (G.flags & FLAG_AFFINE0)) return (uint32_t)(G.a0_base + G.a0_stride * i);
   if (G.flags & FLAG_W16) {
     const int64_t nch = (G.n + 31) >> 5;
     const uint32_t base = __ldg(T.cbase + G.cb_off + (int64_t)col * nch + (i >> 5));
@@ -550,9 +553,14 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       return fail(-1, "sgb_plan_create: position index outside the value array");
   for (int g = 0; g < d->n_groups; ++g) {  // compressed columns decode inside the value array
     const sgb_group &G = d->groups[g];
+    if ((G.flags & FLAG_AFFINE0) && G.n > 0) {
+      const int64_t first = G.a0_base, last = G.a0_base + G.a0_stride * (G.n - 1);
+      if (first < 0 || last < 0 || first >= d->value_array_size || last >= d->value_array_size)
+        return fail(-1, "sgb_plan_create: affine index column outside the value array");
+    }
     if (!(G.flags & FLAG_W16)) continue;
     const int64_t nch = (G.n + 31) / 32;
-    for (int c = 0; c < G.n_ret; ++c)
+    for (int c = (G.flags & FLAG_AFFINE0) ? 1 : 0; c < G.n_ret; ++c)
       for (int64_t i = 0; i < G.n; ++i)
         if ((int64_t)d->cbase[G.cb_off + c * nch + i / 32] + d->coff[G.co_off + c * G.n + i] >= d->value_array_size)
           return fail(-1, "sgb_plan_create: compressed index outside the value array");

@@ -29,6 +29,7 @@ bit for every op in ``EXACT_OPS``.  What the lowering adds:
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -42,6 +43,7 @@ T_IMM, T_ST = 20, 21
 
 KIND_TAPE, KIND_SOP = 0, 1
 FLAG_SELFREF, FLAG_INTERLEAVED, FLAG_SERIAL, FLAG_EXACT, FLAG_STREAM, FLAG_W16 = 1, 2, 4, 8, 16, 32
+FLAG_AFFINE0 = 64  # index column 0 is a0_base + a0_stride * i: no table read
 CHUNK = 32  # instances per compressed-index chunk (one warp in single-set mode)
 SOP_NEWTERM, SOP_NEG = 1, 2
 SOP_MAX = 32  # factors per sum-of-products template (csrc SOP_MAX)
@@ -50,6 +52,7 @@ SOP_MAX = 32  # factors per sum-of-products template (csrc SOP_MAX)
 GROUP_DTYPE = np.dtype([
     ("n", "<i8"), ("dest_base", "<i8"), ("p_off", "<i8"), ("c_off", "<i8"),
     ("tape_off", "<i8"), ("blk_begin", "<i8"), ("cb_off", "<i8"), ("co_off", "<i8"),
+    ("a0_base", "<i8"), ("a0_stride", "<i8"),
     ("n_roots", "<i4"), ("n_slots", "<i4"), ("n_ret", "<i4"), ("n_const", "<i4"),
     ("tape_len", "<i4"), ("n_regs", "<i4"), ("kind", "<i4"), ("flags", "<i4"),
     ("slot_off", "<i4"), ("sop_off", "<i4"), ("sop_len", "<i4"), ("unit", "<i4"),
@@ -57,7 +60,7 @@ GROUP_DTYPE = np.dtype([
 
 # one row per launch unit (int64 x 8), mirrored by include/sgb.h SGB_UNIT_*
 UNIT_FIELDS = ("wave", "kind", "variant", "group_begin", "group_end", "blocks", "block_size", "smem_regs")
-assert GROUP_DTYPE.itemsize == 112
+assert GROUP_DTYPE.itemsize == 128
 
 
 @dataclass
@@ -399,7 +402,21 @@ def compress_columns(plan, kp):
     return lo.astype(np.uint32).reshape(-1), off.astype(np.uint16).reshape(-1)
 
 
-def lower_plan(plan, compress: bool = True) -> DevicePlanArrays:
+def affine_column0(plan, kp):
+    """(base, stride) when index column 0 is exactly base + stride * i, else None."""
+    n = kp.instances
+    if kp.layout != "coalesced" or not kp.retained or n < 2:
+        return None
+    c0 = np.asarray(plan.positions[kp.p_base: kp.p_base + n], dtype=np.int64)
+    base, stride = int(c0[0]), int(c0[1] - c0[0])
+    if np.array_equal(c0, base + stride * np.arange(n, dtype=np.int64)):
+        return base, stride
+    return None
+
+
+def lower_plan(plan, compress: bool | None = None) -> DevicePlanArrays:
+    if compress is None:
+        compress = os.environ.get("SGB_COMPRESS", "1") != "0"
     read_sets = _read_sets(plan)
     waves = compute_waves(plan, read_sets)
     lowered = [lower_kernel(plan, kp, k) for k, kp in enumerate(plan.kernels)]
@@ -477,7 +494,11 @@ def lower_plan(plan, compress: bool = True) -> DevicePlanArrays:
                     sops.append(np.array([newterm, neg], np.uint32).view(np.int32))
                     n_sop += 2
                 g["blk_begin"] = blk
-                comp = compress_columns(plan, kp) if compress else None
+                aff = affine_column0(plan, kp) if compress else None
+                if aff is not None:
+                    g["flags"] |= FLAG_AFFINE0
+                    g["a0_base"], g["a0_stride"] = aff
+                comp = compress_columns(plan, kp) if compress and len(kp.retained) > (aff is not None) else None
                 if comp is not None:
                     g["flags"] |= FLAG_W16
                     g["cb_off"], g["co_off"] = n_cb, n_co

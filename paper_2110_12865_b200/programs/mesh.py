@@ -183,16 +183,14 @@ def build_lmlt_plan(w: int, a_nnz: int = 6, a_seed: int = 7, a_cols: np.ndarray 
     nf = len(F)
     sh_w, sh_area = _face_struct_hashes()
 
-    # ---- per-face weights and area shares: one group per face orientation ----
-    w_addr = np.empty((nf, 3), np.int64)  # weight of corner c of face f
-    area_addr = np.empty(nf, np.int64)
+    # ---- per-face weights and area shares: anchor = the quad's lower-left vertex ----
+    gap = 2 * w + 8  # structured consumers reach at most w+1 anchors past either end
     tmpl, roots = face_template()
-    for t in range(2):
-        fi = np.arange(t, nf, 2)
-        cols = [3 * F[fi, v] + c for v in range(3) for c in range(3)]
-        res = B.add_group(f"face{t}", 3, tmpl, roots, cols)
-        w_addr[fi] = res[:3].T
-        area_addr[fi] = res[3]
+    v00 = np.repeat(np.arange(nf // 2) // (w - 1) * w + np.arange(nf // 2) % (w - 1), 2)
+    cols = [3 * F[:, v] + c for v in range(3) for c in range(3)]
+    res = B.add_structured("face", 3, tmpl, roots, cols, v00, n, scales=[3] * 9, gap=gap)
+    w_addr = res[:3].T.copy()  # weight of corner c of face f
+    area_addr = res[3].copy()
 
     # ---- L diagonal: weights of both edge ends, creation order (face, corner) ----
     # corner c's weight belongs to the edge opposite corner c: (j,k), (k,i), (i,j)
@@ -211,7 +209,7 @@ def build_lmlt_plan(w: int, a_nnz: int = 6, a_seed: int = 7, a_cols: np.ndarray 
         sel = np.flatnonzero(counts == cnt)
         cols = [w_addr[fid[starts[sel] + s], cid[starts[sel] + s]] for s in range(cnt)]
         T, r = _sum_template(int(cnt))
-        ldiag_addr[verts[sel]] = B.add_group_split(f"ldiag{cnt}", 2, T, r, cols)[0]
+        ldiag_addr[verts[sel]] = B.add_structured(f"ldiag{cnt}", 2, T, r, cols, verts[sel], n, gap=gap)[0]
         ldiag_sh[verts[sel]] = S.sh_apply(S.ADD, [sh_w] * int(cnt))
 
     # ---- L off-diagonal per undirected edge: -w or -w1 + -w2 ----
@@ -229,7 +227,7 @@ def build_lmlt_plan(w: int, a_nnz: int = 6, a_seed: int = 7, a_cols: np.ndarray 
         sel = np.flatnonzero(ecounts == cnt)
         cols = [wa_s[estarts[sel] + s] for s in range(cnt)]
         T, r = _sum_template(int(cnt), neg=True)
-        eaddr[sel] = B.add_group_split(f"loff{cnt}", 2, T, r, cols)[0]
+        eaddr[sel] = B.add_structured(f"loff{cnt}", 2, T, r, cols, ekeys[sel] // n, n, gap=gap)[0]
         esh[sel] = sh_negw if cnt == 1 else S.sh_apply(S.ADD, [sh_negw] * int(cnt))
 
     # ---- M diagonal: area shares in face order ----
@@ -248,7 +246,7 @@ def build_lmlt_plan(w: int, a_nnz: int = 6, a_seed: int = 7, a_cols: np.ndarray 
             continue
         cols = [area_addr[mf[mstarts[sel] + s]] for s in range(cnt)]
         T, r = _sum_template(int(cnt))
-        m_addr[mverts[sel]] = B.add_group_split(f"mdiag{cnt}", 2, T, r, cols)[0]
+        m_addr[mverts[sel]] = B.add_structured(f"mdiag{cnt}", 2, T, r, cols, mverts[sel], n, gap=gap)[0]
         m_sh[mverts[sel]] = S.sh_apply(S.ADD, [sh_area] * int(cnt))
 
     # ---- L in CSR: diagonal + both directions of every edge ----
@@ -265,7 +263,7 @@ def build_lmlt_plan(w: int, a_nnz: int = 6, a_seed: int = 7, a_cols: np.ndarray 
 
     # ---- LM = L * M (one term per entry) ----
     T, r = _product_template()
-    lm_addr = B.add_group_split("lm", 1, T, r, [L_addr, m_addr[L_col]])[0]
+    lm_addr = B.add_structured("lm", 1, T, r, [L_addr, m_addr[L_col]], L_row, n, gap=gap)[0]
     # struct-hash classes: intern the (few) distinct hashes as small ints
     classes: dict[int, int] = {}
     cls_val: list[int] = []
@@ -333,8 +331,8 @@ def build_lmlt_plan(w: int, a_nnz: int = 6, a_seed: int = 7, a_cols: np.ndarray 
             if wa_flag:
                 cols.append(a_var[a_pos[out_slot[sel]]])
             T, r = _sop_template(int(m), wa_flag)
-            res = B.add_group_split(f"out{m}{'a' if wa_flag else ''}", 0, T, r, cols, dest_kind="output",
-                                    keep_cols=(2 * int(m),) if wa_flag else ())
+            res = B.add_structured(f"out{m}{'a' if wa_flag else ''}", 0, T, r, cols,
+                                   out_keys[out_slot[sel]] // n, n, dest_kind="output")
             outputs[out_slot[sel]] = res[0]
     out_rows = out_keys // n
     row_ptr = np.zeros(n + 1, np.int64)

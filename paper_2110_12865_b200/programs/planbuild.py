@@ -12,9 +12,22 @@ coherent slots leave the table.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from ..plan import ExecutionPlan, KernelPlan, Template, align
+
+
+def _row_classes(M: np.ndarray):
+    """np.unique(M, axis=0, return_inverse, return_counts) via a 64-bit row hash (fast)."""
+    M = np.ascontiguousarray(M, dtype=np.int64)
+    h = np.zeros(M.shape[0], dtype=np.uint64)
+    for j in range(M.shape[1]):
+        h = (h ^ M[:, j].astype(np.uint64)) * np.uint64(0x9E3779B97F4A7C15)
+        h ^= h >> np.uint64(29)
+    _, inv, cnt = np.unique(h, return_inverse=True, return_counts=True)
+    return inv.reshape(-1), cnt
 
 
 def detect_offset_coherence(cols: list[np.ndarray]) -> list:
@@ -44,15 +57,18 @@ class PlanBuilder:
 
     def add_group(self, name: str, level: int, template: Template, roots: list[int],
                   slot_addrs: list[np.ndarray], const_cols: list[np.ndarray] | None = None,
-                  dest_kind: str = "intermediate") -> np.ndarray:
-        """Append one group; returns its result addresses, shape (n_roots, N)."""
+                  dest_kind: str = "intermediate", gap: int = 0) -> np.ndarray:
+        """Append one group; returns its result addresses, shape (n_roots, N).
+
+        ``gap`` reserves zero padding after the result range (room for the
+        over-reach of padded structured consumers, see add_structured)."""
         const_cols = const_cols or []
         n = int(len(slot_addrs[0]) if slot_addrs else len(const_cols[0]))
         for col in list(slot_addrs) + list(const_cols):
             if len(col) != n:
                 raise ValueError(f"{name}: ragged slot columns")
         dest = align(self.cursor, self.vector_width)
-        self.cursor = dest + len(roots) * n
+        self.cursor = dest + len(roots) * n + gap
         cols = [np.asarray(c, dtype=np.int64) for c in slot_addrs]
         for c in cols:
             if c.size and (c.min() < 0 or c.max() >= dest):
@@ -109,11 +125,10 @@ class PlanBuilder:
         """
         cols = [np.asarray(c, dtype=np.int64) for c in slot_addrs]
         n = len(cols[0]) if cols else 0
-        if n == 0 or not cols:
+        if n == 0 or not cols or os.environ.get("SGB_SPLIT", "1") == "0":
             return self.add_group(name, level, template, roots, slot_addrs, const_cols, dest_kind)
         src = np.stack([self.producer_ids(c) for c in cols], axis=1)
-        _, sinv, scnt = np.unique(src, axis=0, return_inverse=True, return_counts=True)
-        sinv = sinv.reshape(-1)
+        sinv, scnt = _row_classes(src)
         sinv = np.where(scnt[sinv] >= min_source_class, sinv, -1)
         sig_slots = [s for s in range(1, len(cols)) if s not in keep_cols]
         label = np.full(n, -1, dtype=np.int64)
@@ -125,15 +140,12 @@ class PlanBuilder:
                 next_label += 1
                 continue
             D = np.stack([cols[s][members] - cols[0][members] for s in sig_slots], axis=1)
-            _, inv, counts = np.unique(D, axis=0, return_inverse=True, return_counts=True)
-            inv = inv.reshape(-1)
+            inv, counts = _row_classes(D)
             big = counts >= min_class
-            uniq_big = {c: next_label + k for k, c in enumerate(np.flatnonzero(big).tolist())}
-            next_label += len(uniq_big)
-            rest = next_label
-            next_label += 1
-            label[members] = np.array([uniq_big.get(c, rest) for c in inv.tolist()], dtype=np.int64) \
-                if len(uniq_big) else rest
+            remap = np.full(counts.size, next_label + int(big.sum()), dtype=np.int64)
+            remap[big] = next_label + np.arange(int(big.sum()))
+            label[members] = remap[inv]
+            next_label += int(big.sum()) + 1
         out = np.empty((len(roots), n), dtype=np.int64)
         order = np.argsort(label, kind="stable")
         keys, starts = np.unique(label[order], return_index=True)
@@ -143,6 +155,58 @@ class PlanBuilder:
             sub_const = [np.asarray(c)[sel] for c in (const_cols or [])]
             out[:, sel] = self.add_group(f"{name}_{k}", level, template, roots, [c[sel] for c in cols],
                                          sub_const, dest_kind)
+        return out
+
+    def add_structured(self, name: str, level: int, template: Template, roots: list[int],
+                       slot_addrs: list[np.ndarray], anchor: np.ndarray, n_anchor: int,
+                       scales=None, min_frac: float = 0.2, gap: int = 0,
+                       dest_kind: str = "intermediate") -> np.ndarray:
+        """Anchor-rate layout for the regular interior of a structured mesh.
+
+        Every entity (one instance of ``template``) has an anchor vertex.
+        Entities whose slot addresses are ``scale_s * anchor + rel_s`` with
+        the same ``rel`` vector form a class; every class holding at least
+        ``min_frac * n_anchor`` entities becomes one group with ``n_anchor``
+        instances, instance a = anchor a (anchors outside the class compute
+        the same formula on neighbouring values: padding nobody reads).  In
+        such a group consecutive lanes read consecutive addresses of every
+        slot (whole 128-byte lines per warp instead of one line per lane) and
+        all slots with the slot-0 scale are offset-coherent, i.e. leave the
+        index table.  The remaining entities (mesh boundary) go through
+        ``add_group_split``.  ``gap`` pads each structured group's range so
+        consumers reaching a few anchors past the end stay inside it.
+        """
+        cols = [np.asarray(c, dtype=np.int64) for c in slot_addrs]
+        anchor = np.asarray(anchor, dtype=np.int64)
+        E = len(anchor)
+        scales = [1] * len(cols) if scales is None else list(scales)
+        out = np.empty((len(roots), E), dtype=np.int64)
+        if E == 0:
+            return out
+        rel = np.stack([c - sc * anchor for c, sc in zip(cols, scales)], axis=1)
+        inv, counts = _row_classes(rel)
+        done = np.zeros(E, dtype=bool)
+        big = np.flatnonzero(counts >= max(1, int(min_frac * n_anchor)))
+        for k, cls in enumerate(big.tolist()):
+            members = np.flatnonzero(inv == cls)
+            a = anchor[members]
+            if np.unique(a).size != a.size:
+                continue  # anchors must be unique inside a structured group
+            r = rel[members[0]]
+            grid = np.arange(n_anchor, dtype=np.int64)
+            sub = [sc * grid + int(rv) for sc, rv in zip(scales, r.tolist())]
+            lo = min(int(c.min()) for c in sub)
+            hi = max(int(c.max()) for c in sub)
+            if lo < 0 or hi >= align(self.cursor, self.vector_width):
+                continue  # padding would reach outside the values written so far
+            res = self.add_group(f"{name}_s{k}", level, template, roots, sub, None, dest_kind, gap=gap)
+            out[:, members] = res[:, a]
+            done[members] = True
+        rest = np.flatnonzero(~done)
+        if rest.size:
+            order = rest[np.argsort(anchor[rest], kind="stable")]
+            out[:, order] = self.add_group_split(f"{name}_b", level, template, roots,
+                                                 [c[order] for c in cols], None, dest_kind)
         return out
 
     def finish(self, outputs: np.ndarray, metadata: dict) -> ExecutionPlan:

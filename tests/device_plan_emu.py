@@ -27,6 +27,8 @@ def _decode_addrs(dp, g, i):
     if n_slots == 0:
         return []
     def column(col):
+        if col == 0 and g["flags"] & L.FLAG_AFFINE0:
+            return int(g["a0_base"]) + int(g["a0_stride"]) * np.asarray(i, dtype=np.int64)
         if g["flags"] & L.FLAG_W16:
             nch = (n + L.CHUNK - 1) // L.CHUNK
             base = dp.cbase[g["cb_off"] + col * nch + i // L.CHUNK].astype(np.int64)
