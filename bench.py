@@ -59,7 +59,7 @@ def build_workload(args, rank: int, world: int, barrier=None):
     """Plan + CSR pattern for the configured workload, cached across ranks."""
     from paper_2110_12865_b200.programs.mesh import build_lmlt_plan
 
-    key = f"lmlt_w{args.w}_a6_s7_split{os.environ.get('SGB_SPLIT', '1')}"
+    key = f"lmlt_w{args.w}_a6_s7_split{os.environ.get('SGB_SPLIT', '0')}"
     cache_dir = Path(os.environ.get("SGB_PLAN_CACHE", Path(tempfile.gettempdir()) / "sgb_plan_cache"))
     path = cache_dir / f"{key}.pkl"
     if rank == 0 and not path.exists():

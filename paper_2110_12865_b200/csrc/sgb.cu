@@ -264,8 +264,67 @@ __device__ __forceinline__ void tape_instance(const Tables &T, const sgb_group &
   }
 }
 
-// Single value set: lane = instance.  Scratch file [n_regs][BS] in shared memory.
-template <int BS>
+// VEC instances per thread: one tape decode drives VEC independent evaluations
+// (instances i0 + v*BS, so every v stays lane-coalesced).  Register r of
+// instance v lives at R[(r*VEC + v) * BS].
+template <int BS, int VEC>
+__device__ __forceinline__ void run_tape_vec(const Tables &T, const sgb_group &G, double *R, double *x,
+                                             const int64_t (&iv)[VEC], const bool (&ok)[VEC],
+                                             uint64_t pol) {
+  constexpr int S = VEC * BS;
+  const uint64_t *tp = T.tape + G.tape_off;
+  const bool stream = G.flags & FLAG_STREAM;
+  const int len = G.tape_len;
+  uint64_t next = len > 0 ? __ldg(tp) : 0;
+  for (int pc = 0; pc < len; ++pc) {
+    const uint64_t w = next;
+    if (pc + 1 < len) next = __ldg(tp + pc + 1);
+    const int op = (int)(w & 0x3F);
+    double *D = R + ((unsigned)(w >> 6) & REG_MASK) * S;
+    const double *A = R + ((unsigned)(w >> 20) & REG_MASK) * S;
+    const unsigned bb = (unsigned)(w >> 34) & REG_MASK;
+    const unsigned c = (unsigned)(w >> 48) & REG_MASK;
+    const double *Bp = R + bb * S;
+    if (op == T_MUL) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) D[v * BS] = __dmul_rn(A[v * BS], Bp[v * BS]);
+    } else if (op == T_ADD) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) D[v * BS] = __dadd_rn(A[v * BS], Bp[v * BS]);
+    } else if (op == T_SUB) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) D[v * BS] = __dsub_rn(A[v * BS], Bp[v * BS]);
+    } else if (op == T_IMM) {
+      const double imm = __ldg(T.imm + (bb | (c << 14)));
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) D[v * BS] = imm;
+    } else if (op == T_NEG) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) D[v * BS] = -A[v * BS];
+    } else if (op == T_DIV) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) D[v * BS] = __ddiv_rn(A[v * BS], Bp[v * BS]);
+    } else if (op == T_ST) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v)
+        if (ok[v]) st_result(x + G.dest_base + (int64_t)c * G.n + iv[v], A[v * BS], stream, pol);
+    } else if (op == T_SQRT) {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) D[v * BS] = __dsqrt_rn(A[v * BS]);
+    } else if (op == T_SEL) {
+      const double *C = R + c * S;
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) D[v * BS] = (A[v * BS] < 0.0) ? Bp[v * BS] : C[v * BS];
+    } else {
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) D[v * BS] = slow_op(op, A[v * BS], (int)c);
+    }
+  }
+}
+
+// Single value set: lane = instance (VEC instances per lane).  Scratch file
+// [n_regs][VEC][BS] in shared memory.
+template <int BS, int VEC>
 __global__ void __launch_bounds__(BS) tape_single(Tables T, const int64_t *blk_begin, int g0, int g1,
                                                   double *x) {
   extern __shared__ double scratch[];
@@ -274,14 +333,30 @@ __global__ void __launch_bounds__(BS) tape_single(Tables T, const int64_t *blk_b
   const sgb_group G = T.groups[g];
   const uint64_t pol = evict_first_policy();
   const int tid = threadIdx.x;
-  if (G.flags & FLAG_SERIAL) {  // members read other instances' results: instance order
+  if (VEC == 1 && (G.flags & FLAG_SERIAL)) {  // members read other instances' results: instance order
     if (tid != 0) return;
     for (int64_t i = 0; i < G.n; ++i) tape_instance<BS>(T, G, scratch, x, 1, i, 0, pol);
     return;
   }
-  const int64_t i = (blk - __ldg(blk_begin + g)) * BS + tid;
-  if (i >= G.n) return;
-  tape_instance<BS>(T, G, scratch + tid, x, 1, i, 0, pol);
+  const int64_t i0 = (blk - __ldg(blk_begin + g)) * (BS * VEC) + tid;
+  if (i0 >= G.n) return;
+  if (VEC == 1) {
+    tape_instance<BS>(T, G, scratch + tid, x, 1, i0, 0, pol);
+    return;
+  }
+  int64_t iv[VEC];
+  bool ok[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    iv[v] = i0 + (int64_t)v * BS;
+    ok[v] = iv[v] < G.n;
+    if (!ok[v]) iv[v] = G.n - 1;  // evaluate a valid instance, store nothing
+  }
+  double *R = scratch + tid;
+  const bool inter = G.flags & FLAG_INTERLEAVED;
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) load_slots<VEC * BS>(T, G, R + v * BS, x, 1, iv[v], 0, inter, false, pol);
+  run_tape_vec<BS, VEC>(T, G, R, x, iv, ok, pol);
 }
 
 // Batched: X[addr * ld + b].  A warp owns one instance and sweeps the batch,
@@ -445,14 +520,24 @@ struct sgb_plan {
 
 namespace {
 
-template <int BS>
+template <int BS, int VEC>
 void launch_tape(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_t batch, bool batched,
                  cudaStream_t s) {
-  const size_t smem = (size_t)u.regs * BS * sizeof(double);
-  if (!batched)
-    tape_single<BS><<<(unsigned)u.blocks, BS, smem, s>>>(p->T, p->d_blk, u.g0, u.g1, x);
-  else
+  if (!batched) {
+    const size_t smem = (size_t)u.regs * BS * VEC * sizeof(double);
+    tape_single<BS, VEC><<<(unsigned)u.blocks, BS, smem, s>>>(p->T, p->d_blk, u.g0, u.g1, x);
+  } else {
+    const size_t smem = (size_t)u.regs * BS * sizeof(double);
     tape_batch<BS><<<(unsigned)u.bblocks, BS, smem, s>>>(p->T, p->d_bblk, u.g0, u.g1, x, ld, batch);
+  }
+}
+
+template <int BS>
+void launch_tape_vec(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_t batch, bool batched,
+                     cudaStream_t s) {
+  if (batched || u.variant <= 1) launch_tape<BS, 1>(p, u, x, ld, batch, batched, s);
+  else if (u.variant == 2) launch_tape<BS, 2>(p, u, x, ld, batch, batched, s);
+  else launch_tape<BS, 4>(p, u, x, ld, batch, batched, s);
 }
 
 template <int LMAX>
@@ -471,10 +556,10 @@ void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_
     // the scratch-file stride equals the block size of the launch
     const int bs = batched ? 32 * u.bwarps : u.bs;
     switch (bs) {
-      case 256: launch_tape<256>(p, u, x, ld, batch, batched, s); break;
-      case 128: launch_tape<128>(p, u, x, ld, batch, batched, s); break;
-      case 64: launch_tape<64>(p, u, x, ld, batch, batched, s); break;
-      default: launch_tape<32>(p, u, x, ld, batch, batched, s); break;
+      case 256: launch_tape<256, 1>(p, u, x, ld, batch, batched, s); break;
+      case 128: launch_tape_vec<128>(p, u, x, ld, batch, batched, s); break;
+      case 64: launch_tape_vec<64>(p, u, x, ld, batch, batched, s); break;
+      default: launch_tape_vec<32>(p, u, x, ld, batch, batched, s); break;
     }
   } else {
     switch (u.variant) {
@@ -486,10 +571,19 @@ void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_
   }
 }
 
+template <int BS, int VEC>
+cudaError_t allow_smem_single(int smem_max) {
+  return cudaFuncSetAttribute(tape_single<BS, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+}
+
 template <int BS>
 cudaError_t allow_smem(int smem_max) {
-  cudaError_t e = cudaFuncSetAttribute(tape_single<BS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
-  if (e != cudaSuccess) return e;
+  cudaError_t e;
+  if ((e = allow_smem_single<BS, 1>(smem_max)) != cudaSuccess) return e;
+  if (BS <= 128) {
+    if ((e = allow_smem_single<(BS <= 128 ? BS : 128), 2>(smem_max)) != cudaSuccess) return e;
+    if ((e = allow_smem_single<(BS <= 128 ? BS : 128), 4>(smem_max)) != cudaSuccess) return e;
+  }
   return cudaFuncSetAttribute(tape_batch<BS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
 }
 
@@ -588,7 +682,8 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
     u.regs = (int)r[U_REGS];
     if (u.g0 < 0 || u.g1 > d->n_groups || u.g0 > u.g1 || u.wave < 0 || u.wave >= d->n_waves ||
         (u.kind == KIND_TAPE && (u.bs != 32 && u.bs != 64 && u.bs != 128)) ||
-        (int64_t)u.regs * (u.kind == KIND_TAPE ? u.bs : 0) * 8 > smem_max)
+        (u.kind == KIND_TAPE && (u.variant != 1 && u.variant != 2 && u.variant != 4)) ||
+        (int64_t)u.regs * (u.kind == KIND_TAPE ? u.bs * u.variant : 0) * 8 > smem_max)
       return fail(-1, "sgb_plan_create: bad launch unit " + std::to_string(k));
     // batched: one instance per warp, as many warps per block as the scratch file allows
     u.bwarps = MAX_BATCH_WARPS;

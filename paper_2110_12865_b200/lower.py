@@ -358,6 +358,8 @@ TAPE_BLOCK = 128
 SOP_BLOCK = 256
 SOP_VARIANTS = (4, 8, 16, 32)
 SMEM_LIMIT = 200 * 1024
+TAPE_VECS = (4, 2, 1)  # instances per thread of the tape interpreter, largest that fits
+VEC_SMEM_BUDGET = 56 * 1024  # per block: keeps >= 4 tape blocks resident per SM
 
 
 def block_size_for(n_regs: int) -> int:
@@ -432,14 +434,26 @@ def lower_plan(plan, compress: bool | None = None) -> DevicePlanArrays:
         members = [kl for kl in lowered if kl.wave == w]
         # launch units of this wave: one tape unit, one SOP unit per width class
         plan_units = []
-        tape_m = [kl for kl in members if kl.kind == KIND_TAPE]
-        if tape_m:
+        # tape groups: lane-parallel ones run VEC instances per thread (one
+        # decode per VEC evaluations); self-referencing / serial ones VEC = 1
+        for plain in (True, False):
+            tape_m = [kl for kl in members if kl.kind == KIND_TAPE and
+                      plain == (not kl.flags & (FLAG_SELFREF | FLAG_SERIAL))]
+            if not tape_m:
+                continue
             regs = max(kl.n_regs for kl in tape_m)
             bs = block_size_for(regs)
             if regs * bs * 8 > SMEM_LIMIT:
                 raise ValueError(f"wave {w}: template needs {regs} scratch registers, "
                                  f"more than shared memory holds")
-            plan_units.append((KIND_TAPE, bs, bs, regs, tape_m))
+            vec = 1
+            if plain:
+                forced = int(os.environ.get("SGB_TAPE_VEC", "0"))
+                for v in (TAPE_VECS if not forced else (forced,)):
+                    if regs * v * bs * 8 <= VEC_SMEM_BUDGET or v == 1:
+                        vec = v
+                        break
+            plan_units.append((KIND_TAPE, vec, bs, regs, tape_m))
         for var in SOP_VARIANTS:
             lo = 0 if var == SOP_VARIANTS[0] else SOP_VARIANTS[SOP_VARIANTS.index(var) - 1]
             sm = [kl for kl in members if kl.kind == KIND_SOP and lo < len(kl.sop) <= var]
@@ -506,7 +520,8 @@ def lower_plan(plan, compress: bool | None = None) -> DevicePlanArrays:
                     coffs.append(comp[1])
                     n_cb += comp[0].size
                     n_co += comp[1].size
-                blk += 1 if kl.flags & FLAG_SERIAL else (kp.instances + bs - 1) // bs
+                per_block = bs * (variant if kind == KIND_TAPE else 1)
+                blk += 1 if kl.flags & FLAG_SERIAL else (kp.instances + per_block - 1) // per_block
                 gi += 1
             units.append((w, kind, variant, g_begin, gi, blk, bs, regs))
     cat = lambda xs, dt: (np.concatenate(xs).astype(dt) if xs and sum(len(x) for x in xs)  # noqa: E731

@@ -125,7 +125,7 @@ class PlanBuilder:
         """
         cols = [np.asarray(c, dtype=np.int64) for c in slot_addrs]
         n = len(cols[0]) if cols else 0
-        if n == 0 or not cols or os.environ.get("SGB_SPLIT", "1") == "0":
+        if n == 0 or not cols or os.environ.get("SGB_SPLIT", "0") == "0":
             return self.add_group(name, level, template, roots, slot_addrs, const_cols, dest_kind)
         src = np.stack([self.producer_ids(c) for c in cols], axis=1)
         sinv, scnt = _row_classes(src)

@@ -16,12 +16,13 @@ from paper_2110_12865_b200.programs.mesh import build_lmlt_plan, lmlt_inputs  # 
 w = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
 inputs = lmlt_inputs(w)
 ref = None
-for split in ("0", "1"):
+for split in ("0",):
     os.environ["SGB_SPLIT"] = split
     t0 = time.time()
     plan, _, _ = build_lmlt_plan(w)
     print(f"split={split}: built in {time.time() - t0:.1f}s, {len(plan.kernels)} kernels", flush=True)
-    for comp in (False, True):
+    for comp, vec in ((True, "1"), (True, "2"), (True, "4"), (True, "0")):
+        os.environ["SGB_TAPE_VEC"] = vec
         dp = DevicePlan(plan, lowered=lower_plan(plan, compress=comp))
         x = dp.new_values(inputs)
         out = torch.empty(len(plan.outputs), dtype=torch.float64, device="cuda")
@@ -52,6 +53,6 @@ for split in ("0", "1"):
         for r in range(R):
             for j in range(dp.launches + 1):
                 per[j] += ev[r][j].elapsed_time(ev[r][j + 1]) / R
-        print(f"  compress={comp} same={same} total={per.sum():.3f} ms waves={np.round(per, 4).tolist()} "
+        print(f"  compress={comp} vec={vec} same={same} total={per.sum():.3f} ms waves={np.round(per, 4).tolist()} "
               f"units={dp.units}", flush=True)
         dp.close()
