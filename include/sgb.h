@@ -70,7 +70,7 @@ typedef struct sgb_plan_desc {
   const int64_t *units;    /* [n_units][8]: wave, kind (0 tape, 1 sum-of-products),
                               variant, group_begin, group_end, blocks, block_size,
                               scratch registers per lane */
-  const uint64_t *tape;    /* 64-bit tape words, see lower.py encode() */
+  const uint32_t *tape;    /* [tape_rows][4] device tape words, see lower.assemble() */
   int64_t tape_rows;
   const double *imm;
   int64_t n_imm;

@@ -38,8 +38,7 @@ namespace {
 
 // tape op codes: lower.py T_*
 enum : int {
-  T_ADD = 2, T_SUB = 3, T_MUL = 4, T_DIV = 5, T_NEG = 6, T_SQRT = 7, T_SIN = 8, T_COS = 9,
-  T_EXP = 10, T_LOG = 11, T_POW = 12, T_SEL = 13, T_IMM = 20, T_ST = 21
+  T_MUL = 0, T_ADD, T_SUB, T_DIV, T_MADD, T_NEG, T_SQRT, T_SEL, T_IMM, T_ST, T_SLOW, T_MSUB, T_RMSUB
 };
 enum : int { KIND_TAPE = 0, KIND_SOP = 1 };
 enum : int {
@@ -48,7 +47,6 @@ enum : int {
 enum : int { U_WAVE = 0, U_KIND, U_VARIANT, U_G0, U_G1, U_BLOCKS, U_BS, U_REGS, U_COUNT };
 constexpr int PRE = 8;  // slot loads kept in flight by the tape prologue
 constexpr int MAX_BATCH_WARPS = 8;
-constexpr uint64_t REG_MASK = (1u << 14) - 1;
 
 thread_local std::string g_err;
 
@@ -66,7 +64,7 @@ int fail(int code, const std::string &msg) {
 
 struct Tables {
   const sgb_group *groups;
-  const uint64_t *tape;
+  const uint32_t *tape;  // 4 x u32 per tape word
   const double *imm;
   const int32_t *sop;
   const int32_t *slot_col;
@@ -169,67 +167,132 @@ __device__ __noinline__ double powi(double x, int k) {
 }
 
 // Rare ops live out of line so the interpreter loop stays small.
-__device__ __noinline__ double slow_op(int op, double a, int k) {
-  switch (op) {
-    case T_SIN: return sin(a);
-    case T_COS: return cos(a);
-    case T_EXP: return exp(a);
-    case T_LOG: return log(a);
+__device__ __noinline__ double slow_op(unsigned kind, double a, int k) {
+  switch (kind) {
+    case 0: return sin(a);
+    case 1: return cos(a);
+    case 2: return exp(a);
+    case 3: return log(a);
     default: return powi(a, k);
   }
 }
 
 // ---- tape interpreter ---------------------------------------------------------------
-// Scratch register r of this lane lives at R[r * STRIDE] in shared memory.
-template <int STRIDE>
-__device__ __forceinline__ void run_tape(const Tables &T, const sgb_group &G, double *R, double *x,
-                                         int64_t ld, int64_t i, int64_t b, int phase, bool selfref,
-                                         uint64_t pol) {
-  const uint64_t *tp = T.tape + G.tape_off;
+// Device words (lower.assemble): x = op | nega<<6 | negb<<7 | (c byte offset / 8) << 8,
+// y / z / w = byte offsets of dst / a / b in the lane's scratch column (w is the
+// immediate index, root index or kind<<16|k for IMM / ST / SLOW).  Scratch is
+// shared memory addressed with 32-bit shared addresses; instance v of a lane
+// sits VS bytes after instance 0.
+__device__ __forceinline__ double lds(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void sts(uint32_t addr, double v) {
+  asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
+}
+__device__ __forceinline__ double flip(double v, uint32_t bit) {  // exact negation when bit = 1
+  return __longlong_as_double(__double_as_longlong(v) ^ ((unsigned long long)bit << 63));
+}
+
+template <int VEC, int VS>
+__device__ __forceinline__ void run_tape(const Tables &T, const sgb_group &G, uint32_t Rb, double *x,
+                                         int64_t ld, int64_t b, const int64_t (&iv)[VEC],
+                                         const bool (&ok)[VEC], int phase, bool selfref, uint64_t pol) {
+  const uint4 *tp = reinterpret_cast<const uint4 *>(T.tape) + G.tape_off;
   const bool stream = G.flags & FLAG_STREAM;
   const int len = G.tape_len;
-  uint64_t next = len > 0 ? __ldg(tp) : 0;
+  uint4 next = len > 0 ? __ldg(tp) : make_uint4(0, 0, 0, 0);
   for (int pc = 0; pc < len; ++pc) {
-    const uint64_t w = next;
+    const uint4 w = next;
     if (pc + 1 < len) next = __ldg(tp + pc + 1);  // prefetch the next word
-    const int op = (int)(w & 0x3F);
-    const unsigned dst = (unsigned)(w >> 6) & REG_MASK;
-    const unsigned a = (unsigned)(w >> 20) & REG_MASK;
-    const unsigned bb = (unsigned)(w >> 34) & REG_MASK;
-    const unsigned c = (unsigned)(w >> 48) & REG_MASK;
-    double v;
-    if (op == T_MUL) {
-      v = __dmul_rn(R[a * STRIDE], R[bb * STRIDE]);
-    } else if (op == T_ADD) {
-      v = __dadd_rn(R[a * STRIDE], R[bb * STRIDE]);
-    } else if (op == T_SUB) {
-      v = __dsub_rn(R[a * STRIDE], R[bb * STRIDE]);
-    } else if (op == T_IMM) {
-      v = __ldg(T.imm + (bb | (c << 14)));
-    } else if (op == T_NEG) {
-      v = -R[a * STRIDE];
-    } else if (op == T_DIV) {
-      v = __ddiv_rn(R[a * STRIDE], R[bb * STRIDE]);
-    } else if (op == T_ST) {
-      if (!selfref || (int)c == phase)
-        st_result(x + (G.dest_base + (int64_t)c * G.n + i) * ld + b, R[a * STRIDE], stream, pol);
-      continue;
-    } else if (op == T_SQRT) {
-      v = __dsqrt_rn(R[a * STRIDE]);
-    } else if (op == T_SEL) {
-      v = (R[a * STRIDE] < 0.0) ? R[bb * STRIDE] : R[c * STRIDE];
-    } else {
-      v = slow_op(op, R[a * STRIDE], (int)c);
+    const uint32_t na = (w.x >> 6) & 1u, nb = (w.x >> 7) & 1u;
+    const uint32_t cofs = (w.x >> 8) << 3;
+    switch (w.x & 63u) {
+      case T_MUL:
+#pragma unroll
+        for (int v = 0; v < VEC; ++v)
+          sts(Rb + w.y + v * VS, __dmul_rn(flip(lds(Rb + w.z + v * VS), na), flip(lds(Rb + w.w + v * VS), nb)));
+        break;
+      case T_ADD:
+#pragma unroll
+        for (int v = 0; v < VEC; ++v)
+          sts(Rb + w.y + v * VS, __dadd_rn(flip(lds(Rb + w.z + v * VS), na), flip(lds(Rb + w.w + v * VS), nb)));
+        break;
+      case T_SUB:
+#pragma unroll
+        for (int v = 0; v < VEC; ++v)
+          sts(Rb + w.y + v * VS, __dsub_rn(flip(lds(Rb + w.z + v * VS), na), flip(lds(Rb + w.w + v * VS), nb)));
+        break;
+      case T_MADD:
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          const double p = __dmul_rn(flip(lds(Rb + w.z + v * VS), na), flip(lds(Rb + w.w + v * VS), nb));
+          sts(Rb + w.y + v * VS, __dadd_rn(p, lds(Rb + cofs + v * VS)));
+        }
+        break;
+      case T_MSUB:
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          const double p = __dmul_rn(flip(lds(Rb + w.z + v * VS), na), flip(lds(Rb + w.w + v * VS), nb));
+          sts(Rb + w.y + v * VS, __dsub_rn(p, lds(Rb + cofs + v * VS)));
+        }
+        break;
+      case T_RMSUB:
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+          const double p = __dmul_rn(flip(lds(Rb + w.z + v * VS), na), flip(lds(Rb + w.w + v * VS), nb));
+          sts(Rb + w.y + v * VS, __dsub_rn(lds(Rb + cofs + v * VS), p));
+        }
+        break;
+      case T_DIV:
+#pragma unroll
+        for (int v = 0; v < VEC; ++v)
+          sts(Rb + w.y + v * VS, __ddiv_rn(flip(lds(Rb + w.z + v * VS), na), flip(lds(Rb + w.w + v * VS), nb)));
+        break;
+      case T_NEG:
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) sts(Rb + w.y + v * VS, -lds(Rb + w.z + v * VS));
+        break;
+      case T_SQRT:
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) sts(Rb + w.y + v * VS, __dsqrt_rn(lds(Rb + w.z + v * VS)));
+        break;
+      case T_SEL:
+#pragma unroll
+        for (int v = 0; v < VEC; ++v)
+          sts(Rb + w.y + v * VS,
+              lds(Rb + w.z + v * VS) < 0.0 ? lds(Rb + w.w + v * VS) : lds(Rb + cofs + v * VS));
+        break;
+      case T_IMM: {
+        const double imm = __ldg(T.imm + w.w);
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) sts(Rb + w.y + v * VS, imm);
+        break;
+      }
+      case T_ST:
+        if (!selfref || (int)w.w == phase) {
+#pragma unroll
+          for (int v = 0; v < VEC; ++v)
+            if (ok[v])
+              st_result(x + (G.dest_base + (int64_t)w.w * G.n + iv[v]) * ld + b, lds(Rb + w.z + v * VS),
+                        stream, pol);
+        }
+        break;
+      default:  // T_SLOW
+#pragma unroll
+        for (int v = 0; v < VEC; ++v)
+          sts(Rb + w.y + v * VS, slow_op(w.w >> 16, lds(Rb + w.z + v * VS), (int)(w.w & 0xFFFFu)));
+        break;
     }
-    R[dst * STRIDE] = v;
   }
 }
 
-// Prologue: hoisted slot loads (emit.py:108-124), PRE loads in flight per lane.
-template <int STRIDE>
-__device__ __forceinline__ void load_slots(const Tables &T, const sgb_group &G, double *R,
-                                           const double *x, int64_t ld, int64_t i, int64_t b,
-                                           bool inter, bool coherent_read, uint64_t pol) {
+// Prologue: hoisted slot loads (emit.py:108-124), PRE loads in flight per lane;
+// slot s of this lane's instance goes to byte offset s * stride8.
+__device__ __forceinline__ void load_slots(const Tables &T, const sgb_group &G, uint32_t Rb, uint32_t stride8,
+                                           const double *x, int64_t ld, int64_t i, int64_t b, bool inter,
+                                           bool coherent_read, uint64_t pol) {
   const uint32_t idx0 = slot0_index(T, G, i, inter, pol);
   for (int s0 = 0; s0 < G.n_slots; s0 += PRE) {
     double v[PRE];
@@ -243,87 +306,30 @@ __device__ __forceinline__ void load_slots(const Tables &T, const sgb_group &G, 
     }
 #pragma unroll
     for (int u = 0; u < PRE; ++u)
-      if (s0 + u < G.n_slots) R[(s0 + u) * STRIDE] = v[u];
+      if (s0 + u < G.n_slots) sts(Rb + (uint32_t)(s0 + u) * stride8, v[u]);
   }
   for (int k = 0; k < G.n_const; ++k) {
     const int64_t e = inter ? G.c_off + i * G.n_const + k : G.c_off + (int64_t)k * G.n + i;
-    R[(G.n_slots + k) * STRIDE] = ld_const(T.con + e, pol);
+    sts(Rb + (uint32_t)(G.n_slots + k) * stride8, ld_const(T.con + e, pol));
   }
 }
 
-template <int STRIDE>
-__device__ __forceinline__ void tape_instance(const Tables &T, const sgb_group &G, double *R,
-                                              double *x, int64_t ld, int64_t i, int64_t b,
-                                              uint64_t pol) {
+// One instance, any group (self-referencing groups reload before every root).
+__device__ __forceinline__ void tape_instance(const Tables &T, const sgb_group &G, uint32_t Rb, uint32_t stride8,
+                                              double *x, int64_t ld, int64_t i, int64_t b, uint64_t pol) {
   const bool inter = G.flags & FLAG_INTERLEAVED;
   const bool selfref = G.flags & FLAG_SELFREF;
   const int phases = selfref ? G.n_roots : 1;
+  const int64_t iv[1] = {i};
+  const bool ok[1] = {true};
   for (int ph = 0; ph < phases; ++ph) {
-    load_slots<STRIDE>(T, G, R, x, ld, i, b, inter, selfref, pol);
-    run_tape<STRIDE>(T, G, R, x, ld, i, b, ph, selfref, pol);
+    load_slots(T, G, Rb, stride8, x, ld, i, b, inter, selfref, pol);
+    run_tape<1, 0>(T, G, Rb, x, ld, b, iv, ok, ph, selfref, pol);
   }
 }
 
-// VEC instances per thread: one tape decode drives VEC independent evaluations
-// (instances i0 + v*BS, so every v stays lane-coalesced).  Register r of
-// instance v lives at R[(r*VEC + v) * BS].
-template <int BS, int VEC>
-__device__ __forceinline__ void run_tape_vec(const Tables &T, const sgb_group &G, double *R, double *x,
-                                             const int64_t (&iv)[VEC], const bool (&ok)[VEC],
-                                             uint64_t pol) {
-  constexpr int S = VEC * BS;
-  const uint64_t *tp = T.tape + G.tape_off;
-  const bool stream = G.flags & FLAG_STREAM;
-  const int len = G.tape_len;
-  uint64_t next = len > 0 ? __ldg(tp) : 0;
-  for (int pc = 0; pc < len; ++pc) {
-    const uint64_t w = next;
-    if (pc + 1 < len) next = __ldg(tp + pc + 1);
-    const int op = (int)(w & 0x3F);
-    double *D = R + ((unsigned)(w >> 6) & REG_MASK) * S;
-    const double *A = R + ((unsigned)(w >> 20) & REG_MASK) * S;
-    const unsigned bb = (unsigned)(w >> 34) & REG_MASK;
-    const unsigned c = (unsigned)(w >> 48) & REG_MASK;
-    const double *Bp = R + bb * S;
-    if (op == T_MUL) {
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) D[v * BS] = __dmul_rn(A[v * BS], Bp[v * BS]);
-    } else if (op == T_ADD) {
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) D[v * BS] = __dadd_rn(A[v * BS], Bp[v * BS]);
-    } else if (op == T_SUB) {
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) D[v * BS] = __dsub_rn(A[v * BS], Bp[v * BS]);
-    } else if (op == T_IMM) {
-      const double imm = __ldg(T.imm + (bb | (c << 14)));
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) D[v * BS] = imm;
-    } else if (op == T_NEG) {
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) D[v * BS] = -A[v * BS];
-    } else if (op == T_DIV) {
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) D[v * BS] = __ddiv_rn(A[v * BS], Bp[v * BS]);
-    } else if (op == T_ST) {
-#pragma unroll
-      for (int v = 0; v < VEC; ++v)
-        if (ok[v]) st_result(x + G.dest_base + (int64_t)c * G.n + iv[v], A[v * BS], stream, pol);
-    } else if (op == T_SQRT) {
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) D[v * BS] = __dsqrt_rn(A[v * BS]);
-    } else if (op == T_SEL) {
-      const double *C = R + c * S;
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) D[v * BS] = (A[v * BS] < 0.0) ? Bp[v * BS] : C[v * BS];
-    } else {
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) D[v * BS] = slow_op(op, A[v * BS], (int)c);
-    }
-  }
-}
-
-// Single value set: lane = instance (VEC instances per lane).  Scratch file
-// [n_regs][VEC][BS] in shared memory.
+// Single value set: lane = instance, VEC instances per lane (i0 + v*BS) share each
+// decoded tape word.  Scratch file [n_regs][VEC][BS] doubles in shared memory.
 template <int BS, int VEC>
 __global__ void __launch_bounds__(BS) tape_single(Tables T, const int64_t *blk_begin, int g0, int g1,
                                                   double *x) {
@@ -333,15 +339,18 @@ __global__ void __launch_bounds__(BS) tape_single(Tables T, const int64_t *blk_b
   const sgb_group G = T.groups[g];
   const uint64_t pol = evict_first_policy();
   const int tid = threadIdx.x;
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(scratch);
+  constexpr uint32_t stride8 = BS * VEC * 8;
   if (VEC == 1 && (G.flags & FLAG_SERIAL)) {  // members read other instances' results: instance order
     if (tid != 0) return;
-    for (int64_t i = 0; i < G.n; ++i) tape_instance<BS>(T, G, scratch, x, 1, i, 0, pol);
+    for (int64_t i = 0; i < G.n; ++i) tape_instance(T, G, base, stride8, x, 1, i, 0, pol);
     return;
   }
   const int64_t i0 = (blk - __ldg(blk_begin + g)) * (BS * VEC) + tid;
   if (i0 >= G.n) return;
+  const uint32_t Rb = base + tid * 8;
   if (VEC == 1) {
-    tape_instance<BS>(T, G, scratch + tid, x, 1, i0, 0, pol);
+    tape_instance(T, G, Rb, stride8, x, 1, i0, 0, pol);
     return;
   }
   int64_t iv[VEC];
@@ -352,33 +361,34 @@ __global__ void __launch_bounds__(BS) tape_single(Tables T, const int64_t *blk_b
     ok[v] = iv[v] < G.n;
     if (!ok[v]) iv[v] = G.n - 1;  // evaluate a valid instance, store nothing
   }
-  double *R = scratch + tid;
   const bool inter = G.flags & FLAG_INTERLEAVED;
 #pragma unroll
-  for (int v = 0; v < VEC; ++v) load_slots<VEC * BS>(T, G, R + v * BS, x, 1, iv[v], 0, inter, false, pol);
-  run_tape_vec<BS, VEC>(T, G, R, x, iv, ok, pol);
+  for (int v = 0; v < VEC; ++v) load_slots(T, G, Rb + v * BS * 8, stride8, x, 1, iv[v], 0, inter, false, pol);
+  run_tape<VEC, BS * 8>(T, G, Rb, x, 1, 0, iv, ok, 0, false, pol);
 }
 
-// Batched: X[addr * ld + b].  A warp owns one instance and sweeps the batch,
-// so index loads are warp-uniform and every gather is a contiguous row.
-template <int BS>
-__global__ void __launch_bounds__(BS) tape_batch(Tables T, const int64_t *blk_begin, int g0, int g1,
-                                                 double *X, int64_t ld, int64_t batch) {
+// Batched: X[addr * ld + b].  A warp owns one instance and sweeps the batch, so
+// index loads are warp-uniform and every gather is a contiguous row.  The block
+// is the unit's scratch stride wide (BS = bs * VEC of the unit), VEC = 1.
+__global__ void tape_batch(Tables T, const int64_t *blk_begin, int g0, int g1, double *X, int64_t ld,
+                           int64_t batch) {
   extern __shared__ double scratch[];
   const int64_t blk = blockIdx.x;
   const int g = find_group(blk_begin, g0, g1, blk);
   const sgb_group G = T.groups[g];
   const uint64_t pol = evict_first_policy();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t Rb = (uint32_t)__cvta_generic_to_shared(scratch) + tid * 8;
+  const uint32_t stride8 = blockDim.x * 8;
   if (G.flags & FLAG_SERIAL) {
     if (warp != 0) return;
     for (int64_t i = 0; i < G.n; ++i)
-      for (int64_t b = lane; b < batch; b += 32) tape_instance<BS>(T, G, scratch + tid, X, ld, i, b, pol);
+      for (int64_t b = lane; b < batch; b += 32) tape_instance(T, G, Rb, stride8, X, ld, i, b, pol);
     return;
   }
-  const int64_t i = (blk - __ldg(blk_begin + g)) * (BS >> 5) + warp;
+  const int64_t i = (blk - __ldg(blk_begin + g)) * (blockDim.x >> 5) + warp;
   if (i >= G.n) return;
-  for (int64_t b = lane; b < batch; b += 32) tape_instance<BS>(T, G, scratch + tid, X, ld, i, b, pol);
+  for (int64_t b = lane; b < batch; b += 32) tape_instance(T, G, Rb, stride8, X, ld, i, b, pol);
 }
 
 // ---- sum of products: acc = t0 + t1 + ..., t = f0 * f1 * ... (tape-free) --------------
@@ -415,24 +425,36 @@ __device__ __forceinline__ double sop_fold(const sgb_group &G, uint32_t newterm,
   return have ? __dadd_rn(acc, term) : term;
 }
 
-template <int LMAX>
+// VEC instances per thread (i0 + v*256): VEC x LMAX independent gathers in flight.
+template <int LMAX, int VEC>
 __global__ void __launch_bounds__(256) sop_single(Tables T, const int64_t *blk_begin, int g0, int g1,
                                                   double *x) {
   const int64_t blk = blockIdx.x;
   const int g = find_group(blk_begin, g0, g1, blk);
   const sgb_group G = T.groups[g];
-  const int64_t i = (blk - __ldg(blk_begin + g)) * blockDim.x + threadIdx.x;
-  if (i >= G.n) return;
+  const int64_t i0 = (blk - __ldg(blk_begin + g)) * (256 * VEC) + threadIdx.x;
+  if (i0 >= G.n) return;
   const uint64_t pol = evict_first_policy();
   const uint32_t newterm = (uint32_t)__ldg(T.sop + G.sop_off);
   const uint32_t negm = (uint32_t)__ldg(T.sop + G.sop_off + 1);
-  int64_t addr[LMAX];
-  sop_addrs<LMAX>(T, G, i, addr, pol);
-  double v[LMAX];
+  int64_t addr[VEC][LMAX];
 #pragma unroll
-  for (int f = 0; f < LMAX; ++f)
-    if (f < G.sop_len) v[f] = __ldg(x + addr[f]);
-  st_result(x + G.dest_base + i, sop_fold<LMAX>(G, newterm, negm, v), G.flags & FLAG_STREAM, pol);
+  for (int v = 0; v < VEC; ++v) {
+    const int64_t i = min(i0 + (int64_t)v * 256, G.n - 1);
+    sop_addrs<LMAX>(T, G, i, addr[v], pol);
+  }
+  double val[VEC][LMAX];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v)
+#pragma unroll
+    for (int f = 0; f < LMAX; ++f)
+      if (f < G.sop_len) val[v][f] = __ldg(x + addr[v][f]);
+  const bool stream = G.flags & FLAG_STREAM;
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    const int64_t i = i0 + (int64_t)v * 256;
+    if (i < G.n) st_result(x + G.dest_base + i, sop_fold<LMAX>(G, newterm, negm, val[v]), stream, pol);
+  }
 }
 
 template <int LMAX>
@@ -506,7 +528,7 @@ struct sgb_plan {
   Tables T{};
   sgb_group *d_groups = nullptr;
   int64_t *d_blk = nullptr, *d_bblk = nullptr, *d_outputs = nullptr;
-  uint64_t *d_tape = nullptr;
+  uint32_t *d_tape = nullptr;
   double *d_imm = nullptr, *d_con = nullptr;
   int32_t *d_sop = nullptr, *d_scol = nullptr;
   int64_t *d_sdel = nullptr;
@@ -521,30 +543,23 @@ struct sgb_plan {
 namespace {
 
 template <int BS, int VEC>
-void launch_tape(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_t batch, bool batched,
-                 cudaStream_t s) {
-  if (!batched) {
-    const size_t smem = (size_t)u.regs * BS * VEC * sizeof(double);
-    tape_single<BS, VEC><<<(unsigned)u.blocks, BS, smem, s>>>(p->T, p->d_blk, u.g0, u.g1, x);
-  } else {
-    const size_t smem = (size_t)u.regs * BS * sizeof(double);
-    tape_batch<BS><<<(unsigned)u.bblocks, BS, smem, s>>>(p->T, p->d_bblk, u.g0, u.g1, x, ld, batch);
-  }
+void launch_tape(const sgb_plan *p, const Unit &u, double *x, cudaStream_t s) {
+  const size_t smem = (size_t)u.regs * BS * VEC * sizeof(double);
+  tape_single<BS, VEC><<<(unsigned)u.blocks, BS, smem, s>>>(p->T, p->d_blk, u.g0, u.g1, x);
 }
 
 template <int BS>
-void launch_tape_vec(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_t batch, bool batched,
-                     cudaStream_t s) {
-  if (batched || u.variant <= 1) launch_tape<BS, 1>(p, u, x, ld, batch, batched, s);
-  else if (u.variant == 2) launch_tape<BS, 2>(p, u, x, ld, batch, batched, s);
-  else launch_tape<BS, 4>(p, u, x, ld, batch, batched, s);
+void launch_tape_vec(const sgb_plan *p, const Unit &u, double *x, cudaStream_t s) {
+  if (u.variant <= 1) launch_tape<BS, 1>(p, u, x, s);
+  else if (u.variant == 2) launch_tape<BS, 2>(p, u, x, s);
+  else launch_tape<BS, 4>(p, u, x, s);
 }
 
 template <int LMAX>
 void launch_sop(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_t batch, bool batched,
                 cudaStream_t s) {
   if (!batched)
-    sop_single<LMAX><<<(unsigned)u.blocks, 256, 0, s>>>(p->T, p->d_blk, u.g0, u.g1, x);
+    sop_single<LMAX, (LMAX <= 8 ? 2 : 1)><<<(unsigned)u.blocks, 256, 0, s>>>(p->T, p->d_blk, u.g0, u.g1, x);
   else
     sop_batch<LMAX><<<(unsigned)u.bblocks, 256, 0, s>>>(p->T, p->d_bblk, u.g0, u.g1, x, ld, batch);
 }
@@ -553,13 +568,16 @@ void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_
                  cudaStream_t s) {
   if ((batched ? u.bblocks : u.blocks) == 0) return;
   if (u.kind == KIND_TAPE) {
-    // the scratch-file stride equals the block size of the launch
-    const int bs = batched ? 32 * u.bwarps : u.bs;
-    switch (bs) {
-      case 256: launch_tape<256, 1>(p, u, x, ld, batch, batched, s); break;
-      case 128: launch_tape_vec<128>(p, u, x, ld, batch, batched, s); break;
-      case 64: launch_tape_vec<64>(p, u, x, ld, batch, batched, s); break;
-      default: launch_tape_vec<32>(p, u, x, ld, batch, batched, s); break;
+    if (batched) {  // block = the unit's scratch stride, one instance per warp
+      const int stride = u.bs * u.variant;
+      const size_t smem = (size_t)u.regs * stride * sizeof(double);
+      tape_batch<<<(unsigned)u.bblocks, stride, smem, s>>>(p->T, p->d_bblk, u.g0, u.g1, x, ld, batch);
+      return;
+    }
+    switch (u.bs) {
+      case 128: launch_tape_vec<128>(p, u, x, s); break;
+      case 64: launch_tape_vec<64>(p, u, x, s); break;
+      default: launch_tape_vec<32>(p, u, x, s); break;
     }
   } else {
     switch (u.variant) {
@@ -580,11 +598,8 @@ template <int BS>
 cudaError_t allow_smem(int smem_max) {
   cudaError_t e;
   if ((e = allow_smem_single<BS, 1>(smem_max)) != cudaSuccess) return e;
-  if (BS <= 128) {
-    if ((e = allow_smem_single<(BS <= 128 ? BS : 128), 2>(smem_max)) != cudaSuccess) return e;
-    if ((e = allow_smem_single<(BS <= 128 ? BS : 128), 4>(smem_max)) != cudaSuccess) return e;
-  }
-  return cudaFuncSetAttribute(tape_batch<BS>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+  if ((e = allow_smem_single<BS, 2>(smem_max)) != cudaSuccess) return e;
+  return allow_smem_single<BS, 4>(smem_max);
 }
 
 }  // namespace
@@ -667,7 +682,7 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
   SGB_CUDA(allow_smem<32>(smem_max));
   SGB_CUDA(allow_smem<64>(smem_max));
   SGB_CUDA(allow_smem<128>(smem_max));
-  SGB_CUDA(allow_smem<256>(smem_max));
+  SGB_CUDA(cudaFuncSetAttribute(tape_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
   std::vector<int64_t> blk(d->n_groups, 0), bblk(d->n_groups, 0);
   for (int k = 0; k < d->n_units; ++k) {
     const int64_t *r = d->units + (int64_t)k * U_COUNT;
@@ -685,10 +700,8 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
         (u.kind == KIND_TAPE && (u.variant != 1 && u.variant != 2 && u.variant != 4)) ||
         (int64_t)u.regs * (u.kind == KIND_TAPE ? u.bs * u.variant : 0) * 8 > smem_max)
       return fail(-1, "sgb_plan_create: bad launch unit " + std::to_string(k));
-    // batched: one instance per warp, as many warps per block as the scratch file allows
-    u.bwarps = MAX_BATCH_WARPS;
-    if (u.kind == KIND_TAPE)
-      while (u.bwarps > 1 && (int64_t)u.regs * 32 * u.bwarps * 8 > smem_max) u.bwarps >>= 1;
+    // batched: one instance per warp; tape blocks are the unit's scratch stride wide
+    u.bwarps = u.kind == KIND_TAPE ? (u.bs * u.variant) / 32 : MAX_BATCH_WARPS;
     int64_t acc = 0;
     for (int g = u.g0; g < u.g1; ++g) {
       blk[g] = d->groups[g].blk_begin;
@@ -696,6 +709,25 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       acc += (d->groups[g].flags & FLAG_SERIAL) ? 1 : (d->groups[g].n + u.bwarps - 1) / u.bwarps;
     }
     u.bblocks = acc;
+    if (u.kind == KIND_TAPE) {  // every tape word must stay inside its lane's scratch column
+      const uint64_t limit = (uint64_t)u.regs * u.bs * u.variant * 8;
+      for (int g = u.g0; g < u.g1; ++g) {
+        const sgb_group &G = d->groups[g];
+        if (G.n_slots + G.n_const > u.regs) return fail(-1, "sgb_plan_create: slots exceed the scratch file");
+        for (int64_t k = G.tape_off; k < G.tape_off + G.tape_len; ++k) {
+          const uint32_t *w = d->tape + 4 * k;
+          const uint32_t op = w[0] & 63u;
+          const uint64_t c8 = (uint64_t)(w[0] >> 8) << 3;
+          bool bad = op > T_RMSUB || w[2] >= limit || c8 >= limit;
+          if (op != T_ST) bad = bad || w[1] >= limit;
+          if (op == T_IMM) bad = bad || w[3] >= d->n_imm;
+          else if (op == T_ST) bad = bad || (int64_t)w[3] >= G.n_roots;
+          else if (op == T_SLOW) bad = bad || (w[3] >> 16) > 4;
+          else bad = bad || w[3] >= limit;
+          if (bad) return fail(-1, "sgb_plan_create: malformed tape word in group " + std::to_string(g));
+        }
+      }
+    }
     p->units.push_back(u);
   }
   int rc = 0;
@@ -703,7 +735,7 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       (rc = upload(&p->d_blk, blk.data(), (int64_t)blk.size())) ||
       (rc = upload(&p->d_bblk, bblk.data(), (int64_t)bblk.size())) ||
       (rc = upload(&p->d_outputs, d->outputs, d->n_outputs)) ||
-      (rc = upload(&p->d_tape, d->tape, d->tape_rows)) || (rc = upload(&p->d_imm, d->imm, d->n_imm)) ||
+      (rc = upload(&p->d_tape, d->tape, d->tape_rows * 4)) || (rc = upload(&p->d_imm, d->imm, d->n_imm)) ||
       (rc = upload(&p->d_sop, d->sop, d->n_sop)) || (rc = upload(&p->d_scol, d->slot_col, d->n_slot)) ||
       (rc = upload(&p->d_sdel, d->slot_delta, d->n_slot)) ||
       (rc = upload(&p->d_pos, d->positions, d->n_positions)) ||

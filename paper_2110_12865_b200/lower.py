@@ -86,7 +86,7 @@ class DevicePlanArrays:
     groups: np.ndarray  # GROUP_DTYPE, ordered by (wave, launch unit)
     units: np.ndarray  # int64 [n_units, 8], UNIT_FIELDS
     n_waves: int
-    tape: np.ndarray  # uint64 tape words
+    tape: np.ndarray  # (L, 4) u32 device words, byte offsets of each group's unit stride
     imm: np.ndarray  # f64
     sop: np.ndarray  # int32
     slot_col: np.ndarray  # int32
@@ -163,22 +163,25 @@ def compute_waves(plan, read_sets=None) -> list[int]:
 
 
 # -- tapes ----------------------------------------------------------------------
+#
+# A tape is a list of register-level instructions (one numpy record each):
+#   op, dst, a, b, c   registers; nega / negb flip the sign of operand a / b
+#   aux                immediate index (IMM), root index (ST), kind<<16|k (SLOW)
+# Fusions (all arithmetic-neutral: each op is still one IEEE-rounded operation):
+#   * a single-use NEG child becomes an operand sign flag of its consumer
+#     (-x is exact, so (-a)*b == -(a*b) bit for bit);
+#   * a single-use binary MUL feeding an ADD / SUB step becomes MADD / MSUB /
+#     RMSUB: d = round(round(a*b) +- c) -- two roundings, never an FMA.
+# At packing time every tape is assembled into 16-byte device words with the
+# shared-memory byte offsets of its launch unit (no decode in the kernel).
 
-# 64-bit tape word: op[0:6] dst[6:20] a[20:34] b[34:48] c[48:62]
-# IMM: immediate index = b | c << 14; ST: source a, root c; POW: base a, k c
-REG_MAX = (1 << 14) - 1
+# device op codes (csrc/sgb.cu keeps the same numbering)
+T_MUL, T_ADD, T_SUB, T_DIV, T_MADD, T_NEG, T_SQRT, T_SEL, T_IMM, T_ST, T_SLOW, T_MSUB, T_RMSUB = range(13)
+SLOW_KIND = {int(OpKind.SIN): 0, int(OpKind.COS): 1, int(OpKind.EXP): 2, int(OpKind.LOG): 3, int(OpKind.POW): 4}
+REG_MAX = 4095  # registers per template (scratch byte offsets fit the 24-bit device fields)
 
-
-def encode(op, dst=0, a=0, b=0, c=0) -> int:
-    for v in (dst, a, b, c):
-        if not 0 <= v <= REG_MAX:
-            raise ValueError(f"tape field {v} out of range (max {REG_MAX})")
-    return op | (dst << 6) | (a << 20) | (b << 34) | (c << 48)
-
-
-def decode(word: int):
-    return (word & 0x3F, (word >> 6) & REG_MAX, (word >> 20) & REG_MAX,
-            (word >> 34) & REG_MAX, (word >> 48) & REG_MAX)
+TAPE_DTYPE = np.dtype([("op", "u1"), ("nega", "u1"), ("negb", "u1"), ("dst", "<u4"), ("a", "<u4"),
+                       ("b", "<u4"), ("c", "<u4"), ("aux", "<u4")])
 
 
 class _RegAlloc:
@@ -198,7 +201,7 @@ class _RegAlloc:
 
 
 def compile_tape(kp):
-    """Template -> (tape words uint64, immediates, n_regs, fp64 ops/instance).
+    """Template -> (tape records, immediates, n_regs, fp64 ops/instance).
 
     Registers 0..S-1 hold the position slots, S..S+K-1 the constant slots
     (loaded by the kernel prologue); temporaries are recycled after their
@@ -213,18 +216,100 @@ def compile_tape(kp):
     S, K = len(kp.pos_vars), len(kp.const_vars)
     if S + K > REG_MAX:
         raise ValueError(f"{kp.name}: {S + K} slots exceed the tape register space")
-    order = {ref: j for j, ref in enumerate(live)}
-    last_use = {}
+    root_set = set(roots)
+    uses: dict[int, int] = {}
     for ref in live:
         for c in args[ref]:
-            last_use[c] = order[ref]
-    root_set = set(roots)
+            uses[c] = uses.get(c, 0) + 1
+
+    def single(ref):
+        return uses.get(ref, 0) == 1 and ref not in root_set
+
+    # fusion decisions: NEG folded into its single consumer, MUL folded into ADD/SUB
+    arith = (OpKind.ADD, OpKind.SUB, OpKind.MUL, OpKind.DIV)
+    consumer_op: dict[int, int] = {}
+    for ref in live:
+        for c in args[ref]:
+            consumer_op[c] = int(ops[ref])
+    fold_neg = {ref for ref in live if int(ops[ref]) == OpKind.NEG and single(ref)
+                and consumer_op.get(ref) in arith}
+    fold_mul = set()
+    for ref in live:
+        op = int(ops[ref])
+        if op in (OpKind.ADD, OpKind.SUB):
+            for ch in args[ref]:
+                if int(ops[ch]) == OpKind.MUL and len(args[ch]) == 2 and single(ch):
+                    fold_mul.add(ch)
+    order = {ref: j for j, ref in enumerate(live)}
+    consumers: dict[int, list[int]] = {}
+    for ref in live:
+        for c in args[ref]:
+            consumers.setdefault(c, []).append(ref)
+    # effective position of a node = where its value is actually consumed
+    # (a folded node is evaluated inside its consumer's instruction)
+    eff: dict[int, int] = {}
+    for ref in reversed(live):
+        if ref in fold_mul or ref in fold_neg:
+            eff[ref] = max(eff.get(p, order[p]) for p in consumers[ref])
+        else:
+            eff[ref] = order[ref]
+    last_use: dict[int, int] = {}
+    for ref in live:
+        for c in args[ref]:
+            last_use[c] = max(last_use.get(c, -1), eff[ref])
     ra = _RegAlloc(S + K)
     reg: dict[int, int] = {}
-    words: list[int] = []
+    recs: list[tuple] = []
     imms: list[float] = []
     imm_of: dict[int, int] = {}
     fops = 0
+
+    def emit(op, dst=0, a=0, b=0, c=0, aux=0, nega=0, negb=0):
+        recs.append((op, nega, negb, dst, a, b, c, aux))
+
+    def operand(ch):
+        """(register, negated) of a child, looking through folded NEGs."""
+        neg = 0
+        while ch in fold_neg:
+            neg ^= 1
+            ch = args[ch][0]
+        return reg[ch], neg
+
+    def factors(m):
+        (ra_, na), (rb_, nb) = operand(args[m][0]), operand(args[m][1])
+        return ra_, rb_, na, nb
+
+    def add_step(dst, left, right, sub=False):
+        """dst = left +- right; left is a child ref or ('r', register)."""
+        l_fm = not isinstance(left, tuple) and left in fold_mul
+        r_fm = right in fold_mul
+        if l_fm and not r_fm:  # (a*b) +- c
+            ma, mb, na, nb = factors(left)
+            rr, rn = operand(right)
+            if rn:
+                emit(T_NEG, dst, rr)
+                rr = dst
+            emit(T_MSUB if sub else T_MADD, dst, ma, mb, rr, nega=na, negb=nb)
+            return
+        if r_fm:  # c +- (a*b); a folded left product is materialised first
+            if l_fm:
+                ma, mb, na, nb = factors(left)
+                emit(T_MUL, dst, ma, mb, nega=na, negb=nb)
+                lr = dst
+            elif isinstance(left, tuple):
+                lr = left[1]
+            else:
+                lr, ln = operand(left)
+                if ln:
+                    emit(T_NEG, dst, lr)
+                    lr = dst
+            ma, mb, na, nb = factors(right)
+            emit(T_RMSUB if sub else T_MADD, dst, ma, mb, lr, nega=na, negb=nb)
+            return
+        lr, ln = (left[1], 0) if isinstance(left, tuple) else operand(left)
+        rr, rn = operand(right)
+        emit(T_SUB if sub else T_ADD, dst, lr, rr, nega=ln, negb=rn)
+
     for ref in live:
         op = int(ops[ref])
         a = args[ref]
@@ -232,48 +317,102 @@ def compile_tape(kp):
             v = payload[ref]
             reg[ref] = slot_of[v] if v in slot_of else S + cslot_of[v]
             continue
+        if ref in fold_neg or ref in fold_mul:
+            if ref in fold_mul:
+                fops += 1
+            continue
         if op == OpKind.CONST:
             bits = np.float64(payload[ref]).view(np.uint64).item()
             if bits not in imm_of:
                 imm_of[bits] = len(imms)
                 imms.append(float(payload[ref]))
             d = ra.get()
-            k = imm_of[bits]
-            words.append(encode(T_IMM, d, 0, k & REG_MAX, k >> 14))
+            emit(T_IMM, d, aux=imm_of[bits])
             reg[ref] = d
             continue
         d = ra.get()
-        if op in (OpKind.ADD, OpKind.MUL):
-            t = T_ADD if op == OpKind.ADD else T_MUL
-            words.append(encode(t, d, reg[a[0]], reg[a[1]]))
+        if op == OpKind.ADD:
+            add_step(d, a[0], a[1])
             for ch in a[2:]:
-                words.append(encode(t, d, d, reg[ch]))
+                add_step(d, ("r", d), ch)
             fops += len(a) - 1
-        elif op in (OpKind.SUB, OpKind.DIV):
-            words.append(encode(T_SUB if op == OpKind.SUB else T_DIV, d, reg[a[0]], reg[a[1]]))
+        elif op == OpKind.SUB:
+            add_step(d, a[0], a[1], sub=True)
             fops += 1
-        elif op in (OpKind.NEG, OpKind.SQRT, OpKind.SIN, OpKind.COS, OpKind.EXP, OpKind.LOG):
-            words.append(encode(op, d, reg[a[0]]))
+        elif op == OpKind.MUL:
+            (ra_, na), (rb_, nb) = operand(a[0]), operand(a[1])
+            emit(T_MUL, d, ra_, rb_, nega=na, negb=nb)
+            for ch in a[2:]:
+                rc_, nc = operand(ch)
+                emit(T_MUL, d, d, rc_, negb=nc)
+            fops += len(a) - 1
+        elif op == OpKind.DIV:
+            (ra_, na), (rb_, nb) = operand(a[0]), operand(a[1])
+            emit(T_DIV, d, ra_, rb_, nega=na, negb=nb)
+            fops += 1
+        elif op == OpKind.NEG:
+            emit(T_NEG, d, reg[a[0]])
+            fops += 1
+        elif op == OpKind.SQRT:
+            emit(T_SQRT, d, reg[a[0]])
+            fops += 1
+        elif op in (OpKind.SIN, OpKind.COS, OpKind.EXP, OpKind.LOG):
+            emit(T_SLOW, d, reg[a[0]], aux=SLOW_KIND[op] << 16)
             fops += 1
         elif op == OpKind.POW:
-            words.append(encode(T_POW, d, reg[a[0]], 0, int(payload[a[1]])))
+            emit(T_SLOW, d, reg[a[0]], aux=(SLOW_KIND[op] << 16) | int(payload[a[1]]))
             fops += 1
         elif op == OpKind.SELECT:
-            words.append(encode(T_SEL, d, reg[a[0]], reg[a[1]], reg[a[2]]))
+            emit(T_SEL, d, reg[a[0]], reg[a[1]], reg[a[2]])
             fops += 1
         else:
             raise ValueError(f"{kp.name}: unknown op {op}")
         reg[ref] = d
         # recycle temporaries after their last use (slot registers stay pinned)
-        for ch in set(a):
-            if last_use.get(ch) == order[ref] and ch not in root_set and reg[ch] >= S + K \
-                    and int(ops[ch]) != OpKind.VAR:
+        dead = set()
+        stack = list(a)
+        while stack:
+            ch = stack.pop()
+            if ch in fold_neg or ch in fold_mul:
+                stack.extend(args[ch])
+                continue
+            dead.add(ch)
+        for ch in dead:
+            if last_use.get(ch) is not None and last_use[ch] <= order[ref] and ch not in root_set \
+                    and ch in reg and reg[ch] >= S + K and int(ops[ch]) != OpKind.VAR and reg[ch] != d:
                 ra.put(reg[ch])
+                reg[ch] = -1 - reg[ch]  # mark released (never released twice)
         if ra.top > REG_MAX:
             raise ValueError(f"{kp.name}: template needs more than {REG_MAX} scratch registers")
     for r_idx, root in enumerate(roots):
-        words.append(encode(T_ST, 0, reg[root], 0, r_idx))
-    return np.asarray(words, dtype=np.uint64), imms, max(ra.top, 1), fops
+        emit(T_ST, 0, reg[root] if reg[root] >= 0 else -1 - reg[root], aux=r_idx)
+    tape = np.array(recs, dtype=TAPE_DTYPE) if recs else np.zeros(0, TAPE_DTYPE)
+    return tape, imms, max(ra.top, 1), fops
+
+
+def assemble(tape: np.ndarray, stride: int, imm_base: int) -> np.ndarray:
+    """Register tape -> device words (u32 x4): byte offsets for scratch stride ``stride``.
+
+    x = op | nega<<6 | negb<<7 | (c*stride) << 8;  y = dst*stride*8;
+    z = a*stride*8;  w = b*stride*8, or the immediate index (IMM, plan-wide),
+    the root index (ST) or kind<<16 | k (SLOW).
+    """
+    if tape.size == 0:
+        return np.zeros((0, 4), np.uint32)
+    op = tape["op"].astype(np.uint64)
+    by = np.uint64(stride * 8)
+    if int(max(tape["c"].max(), tape["dst"].max(), tape["a"].max(), tape["b"].max())) * stride >= 1 << 24:
+        raise ValueError("scratch offsets exceed the 24-bit device field")
+    x = op | (tape["nega"].astype(np.uint64) << np.uint64(6)) | (tape["negb"].astype(np.uint64) << np.uint64(7)) \
+        | ((tape["c"].astype(np.uint64) * np.uint64(stride)) << np.uint64(8))
+    y = tape["dst"].astype(np.uint64) * by
+    z = tape["a"].astype(np.uint64) * by
+    wv = tape["b"].astype(np.uint64) * by
+    special = np.isin(tape["op"], [T_IMM, T_ST, T_SLOW])
+    aux = tape["aux"].astype(np.uint64)
+    aux = np.where(tape["op"] == T_IMM, aux + np.uint64(imm_base), aux)
+    wv = np.where(special, aux, wv)
+    return np.stack([x, y, z, wv], axis=1).astype(np.uint32)
 
 
 def _flatten(tmpl, ref, op):
@@ -346,7 +485,7 @@ def lower_kernel(plan, kp, index: int) -> KernelLowering:
                     flags |= FLAG_SERIAL
                     break
     if sop is not None:
-        return KernelLowering(index, kp.name, KIND_SOP, flags, 0, np.zeros(0, np.uint64), [],
+        return KernelLowering(index, kp.name, KIND_SOP, flags, 0, np.zeros(0, TAPE_DTYPE), [],
                               sop, slot_col, slot_delta, ops=fops)
     return KernelLowering(index, kp.name, KIND_TAPE, flags, n_regs, tape, imms,
                           np.zeros(0, np.int32), slot_col, slot_delta, ops=fops)
@@ -360,6 +499,11 @@ SOP_VARIANTS = (4, 8, 16, 32)
 SMEM_LIMIT = 200 * 1024
 TAPE_VECS = (4, 2, 1)  # instances per thread of the tape interpreter, largest that fits
 VEC_SMEM_BUDGET = 56 * 1024  # per block: keeps >= 4 tape blocks resident per SM
+
+
+def sop_vec(width: int) -> int:
+    """Instances per thread of the sum-of-products kernel (csrc sop_single VEC)."""
+    return 2 if width <= 8 else 1
 
 
 def block_size_for(n_regs: int) -> int:
@@ -482,17 +626,8 @@ def lower_plan(plan, compress: bool | None = None) -> DevicePlanArrays:
                 sdel.append(kl.slot_delta)
                 n_slot += len(kl.slot_col)
                 # immediates are renumbered into the plan-wide pool
-                t = kl.tape.copy()
-                if len(t):
-                    is_imm = (t & np.uint64(0x3F)) == np.uint64(T_IMM)
-                    if is_imm.any():
-                        k = ((t[is_imm] >> np.uint64(34)) & np.uint64(REG_MAX)) | \
-                            (((t[is_imm] >> np.uint64(48)) & np.uint64(REG_MAX)) << np.uint64(14))
-                        k = k + np.uint64(n_imm)
-                        if int(k.max()) >= (1 << 28):
-                            raise ValueError("more than 2^28 immediates")
-                        t[is_imm] = (t[is_imm] & np.uint64((1 << 34) - 1)) | \
-                            ((k & np.uint64(REG_MAX)) << np.uint64(34)) | ((k >> np.uint64(14)) << np.uint64(48))
+                stride = bs * variant if kind == KIND_TAPE else bs
+                t = assemble(kl.tape, stride, n_imm)
                 g["tape_off"] = n_tape
                 g["tape_len"] = len(t)
                 tapes.append(t)
@@ -520,7 +655,7 @@ def lower_plan(plan, compress: bool | None = None) -> DevicePlanArrays:
                     coffs.append(comp[1])
                     n_cb += comp[0].size
                     n_co += comp[1].size
-                per_block = bs * (variant if kind == KIND_TAPE else 1)
+                per_block = bs * (variant if kind == KIND_TAPE else sop_vec(variant))
                 blk += 1 if kl.flags & FLAG_SERIAL else (kp.instances + per_block - 1) // per_block
                 gi += 1
             units.append((w, kind, variant, g_begin, gi, blk, bs, regs))
@@ -531,7 +666,7 @@ def lower_plan(plan, compress: bool | None = None) -> DevicePlanArrays:
         groups=groups,
         units=np.asarray(units, np.int64).reshape(-1, len(UNIT_FIELDS)),
         n_waves=n_waves,
-        tape=cat(tapes, np.uint64),
+        tape=cat(tapes, np.uint32).reshape(-1, 4),
         imm=np.asarray(imms, np.float64),
         sop=cat(sops, np.int32),
         slot_col=cat(scol, np.int32),

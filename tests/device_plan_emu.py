@@ -131,50 +131,57 @@ def run_values(dp, inputs) -> np.ndarray:
 
 
 def _tape(dp, g, x, i):
+    """Decode the device tape words (lower.assemble) of this group's launch unit."""
     n = int(g["n"])
+    unit = dp.unit(int(g["unit"]))
+    stride8 = unit["block_size"] * unit["variant"] * 8
     selfref = bool(g["flags"] & L.FLAG_SELFREF)
     phases = int(g["n_roots"]) if selfref else 1
     S, K = int(g["n_slots"]), int(g["n_const"])
+    words = dp.tape[g["tape_off"]: g["tape_off"] + g["tape_len"]].astype(np.int64).tolist()
+    slow = {0: math.sin, 1: math.cos, 2: math.exp, 3: math.log}
     for ph in range(phases):
-        R = [None] * int(g["n_regs"])
-        for s, a in enumerate(_decode_addrs(dp, g, i)):
-            R[s] = x[a].copy()
+        R = {}
+        for s_, a in enumerate(_decode_addrs(dp, g, i)):
+            R[s_] = x[a].copy()
         for k in range(K):
             R[S + k] = _const(dp, g, k, i).copy()
-        for word in dp.tape[g["tape_off"]: g["tape_off"] + g["tape_len"]].tolist():
-            op, dst, a, b, c = L.decode(int(word))
-            if op == L.T_ST:
-                if not selfref or c == ph:
-                    x[g["dest_base"] + c * n + i] = R[a]
-                continue
-            if op == L.T_IMM:
-                v = np.full(len(i), dp.imm[b | (c << 14)])
-            elif op == L.T_ADD:
-                v = R[a] + R[b]
-            elif op == L.T_SUB:
-                v = R[a] - R[b]
-            elif op == L.T_MUL:
-                v = R[a] * R[b]
-            elif op == L.T_DIV:
-                with np.errstate(all="ignore"):
-                    v = R[a] / R[b]
-            elif op == L.T_NEG:
-                v = -R[a]
-            elif op == L.T_SQRT:
-                with np.errstate(all="ignore"):
+        for wx, wy, wz, ww in words:
+            op, na, nb = wx & 63, (wx >> 6) & 1, (wx >> 7) & 1
+            c = ((wx >> 8) << 3) // stride8
+            d, a, b = wy // stride8, wz // stride8, ww // stride8
+            A = (lambda: -R[a] if na else R[a])
+            Bv = (lambda: -R[b] if nb else R[b])
+            with np.errstate(all="ignore"):
+                if op == L.T_ST:
+                    if not selfref or ww == ph:
+                        x[g["dest_base"] + ww * n + i] = R[a]
+                    continue
+                if op == L.T_IMM:
+                    v = np.full(len(i), dp.imm[ww])
+                elif op == L.T_MUL:
+                    v = A() * Bv()
+                elif op == L.T_ADD:
+                    v = A() + Bv()
+                elif op == L.T_SUB:
+                    v = A() - Bv()
+                elif op == L.T_DIV:
+                    v = A() / Bv()
+                elif op == L.T_MADD:
+                    v = (A() * Bv()) + R[c]
+                elif op == L.T_MSUB:
+                    v = (A() * Bv()) - R[c]
+                elif op == L.T_RMSUB:
+                    v = R[c] - (A() * Bv())
+                elif op == L.T_NEG:
+                    v = -R[a]
+                elif op == L.T_SQRT:
                     v = np.sqrt(R[a])
-            elif op == L.T_SIN:
-                v = _vec(math.sin, R[a])
-            elif op == L.T_COS:
-                v = _vec(math.cos, R[a])
-            elif op == L.T_EXP:
-                v = _vec(math.exp, R[a])
-            elif op == L.T_LOG:
-                v = _vec(math.log, R[a])
-            elif op == L.T_POW:
-                v = _dd_powi(R[a], c)
-            elif op == L.T_SEL:
-                v = np.where(R[a] < 0.0, R[b], R[c])
-            else:
-                raise ValueError(f"bad op {op}")
-            R[dst] = v
+                elif op == L.T_SEL:
+                    v = np.where(R[a] < 0.0, R[b], R[c])
+                elif op == L.T_SLOW:
+                    kind, k = ww >> 16, ww & 0xFFFF
+                    v = _dd_powi(R[a], k) if kind == 4 else _vec(slow[kind], R[a])
+                else:
+                    raise ValueError(f"bad op {op}")
+            R[d] = v
