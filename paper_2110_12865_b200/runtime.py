@@ -154,7 +154,7 @@ class DevicePlan:
         keep = dict(
             groups=np.ascontiguousarray(lw.groups, GROUP_DTYPE),
             units=np.ascontiguousarray(lw.units, np.int64),
-            tape=np.ascontiguousarray(lw.tape, np.uint64),
+            tape=np.ascontiguousarray(lw.tape, np.uint32).reshape(-1, 4),
             imm=np.ascontiguousarray(lw.imm, np.float64),
             sop=np.ascontiguousarray(lw.sop, np.int32),
             scol=np.ascontiguousarray(lw.slot_col, np.int32),
@@ -169,7 +169,7 @@ class DevicePlan:
             value_array_size=self.value_array_size, input_count=self.input_count,
             n_groups=len(keep["groups"]), n_waves=lw.n_waves, n_units=len(keep["units"]),
             groups=_ptr(keep["groups"]), units=_ptr(keep["units"]), tape=_ptr(keep["tape"]),
-            tape_rows=keep["tape"].size, imm=_ptr(keep["imm"]), n_imm=keep["imm"].size,
+            tape_rows=keep["tape"].shape[0], imm=_ptr(keep["imm"]), n_imm=keep["imm"].size,
             sop=_ptr(keep["sop"]), n_sop=keep["sop"].size, slot_col=_ptr(keep["scol"]),
             slot_delta=_ptr(keep["sdel"]), n_slot=keep["scol"].size, positions=_ptr(keep["pos"]),
             n_positions=keep["pos"].size, constants=_ptr(keep["con"]), n_constants=keep["con"].size,
