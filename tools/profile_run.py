@@ -1,4 +1,7 @@
-"""Short evaluation loop for ncu captures (not a benchmark: numbers under a profiler are not bench values)."""
+"""Short evaluation loop for ncu captures (not a benchmark: numbers under a profiler are not bench values).
+
+Uses bench.py's plan cache, so a capture after a bench run on the same box skips the plan build.
+"""
 import argparse
 import sys
 import time
@@ -15,14 +18,16 @@ args = ap.parse_args()
 
 import torch  # noqa: E402
 
+import bench  # noqa: E402
 from paper_2110_12865_b200 import DevicePlan  # noqa: E402
-from paper_2110_12865_b200.programs.mesh import build_lmlt_plan, lmlt_inputs  # noqa: E402
+from paper_2110_12865_b200.programs.mesh import lmlt_inputs  # noqa: E402
 
 t0 = time.time()
-plan, _, _ = build_lmlt_plan(args.w)
-print(f"plan built in {time.time() - t0:.1f}s: {len(plan.kernels)} kernels, {len(plan.outputs)} outputs", flush=True)
+key, plan, _, _ = bench.build_workload(args, 0, 1)
+print(f"plan {key} ready in {time.time() - t0:.1f}s: {len(plan.kernels)} kernels, {len(plan.outputs)} outputs",
+      flush=True)
 dp = DevicePlan(plan)
-print("waves", dp.launches, flush=True)
+print("waves", dp.launches, "units", dp.units, flush=True)
 if args.batch:
     X = torch.zeros((plan.value_array_size, args.batch), dtype=torch.float64, device="cuda")
     X[: plan.input_count] = torch.from_numpy(lmlt_inputs(args.w)).cuda()[:, None]
