@@ -55,11 +55,15 @@ def dist_env():
 # -- workload -----------------------------------------------------------------------
 
 
+def workload_key(args) -> str:
+    return f"lmlt_w{args.w}_a6_s7_split{os.environ.get('SGB_SPLIT', '0')}"
+
+
 def build_workload(args, rank: int, world: int, barrier=None):
     """Plan + CSR pattern for the configured workload, cached across ranks."""
     from paper_2110_12865_b200.programs.mesh import build_lmlt_plan
 
-    key = f"lmlt_w{args.w}_a6_s7_split{os.environ.get('SGB_SPLIT', '0')}"
+    key = workload_key(args)
     cache_dir = Path(os.environ.get("SGB_PLAN_CACHE", Path(tempfile.gettempdir()) / "sgb_plan_cache"))
     path = cache_dir / f"{key}.pkl"
     if rank == 0 and not path.exists():
@@ -144,27 +148,63 @@ class ClockSampler:
 # -- CPU reference -------------------------------------------------------------------
 
 
-def cpu_reference(plan, inputs, steps: int, warmup: int, budget_s: float = 20.0):
-    """Emitted-C sg_run (oracle/emit_c.py) with OpenMP on every host thread."""
-    from oracle import emit_c
+def _reference_sg_run(plan, key):
+    """The reference's own emitted C for this plan (oracle/_ref, made by oracle/make_ref.py), or None."""
+    import ctypes
 
+    from oracle import make_ref
+
+    src, ok = make_ref.lookup(plan, key)
+    if src is None or not ok:
+        return None
+    lib = Path(tempfile.gettempdir()) / f"sgb_ref_{key}_{os.getpid()}.so"
+    # emit.py:220 flags + -fopenmp (the emitted source carries `#pragma omp parallel for`)
+    subprocess.run(["cc", "-O3", "-ffp-contract=off", "-fPIC", "-shared", "-fopenmp", "-o", str(lib), str(src), "-lm"],
+                   check=True, capture_output=True)
+    dll = ctypes.CDLL(str(lib))
+    dll.sg_run.restype = None
+    dll.sg_run.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+    con = np.ascontiguousarray(plan.constants, dtype=np.float64)
+    pos = np.ascontiguousarray(plan.positions, dtype=np.uint32)
+
+    def sg_run(x):
+        dll.sg_run(x.ctypes.data, con.ctypes.data if con.size else None, pos.ctypes.data if pos.size else None)
+        return x
+
+    sg_run.keep = (dll, con, pos)
+    return sg_run
+
+
+def cpu_reference(plan, inputs, steps: int, warmup: int, budget_s: float = 20.0, key: str | None = None):
+    """The reference's native evaluator (emitted-C sg_run) with OpenMP on every host thread.
+
+    Prefers the reference's own emitted source (oracle/_ref/<key>.c, kind "reference"); falls back
+    to the restated emitter (oracle/emit_c.py, kind "port") when it is absent or stale.
+    """
     cores = len(os.sched_getaffinity(0))
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
-    run = emit_c.compile_plan(plan, parallel="pragma", openmp=True)
+    sg_run = _reference_sg_run(plan, key) if key else None
+    kind, what = "reference", f"sparsegen.emit.emit_kernel_source output (oracle/_ref/{key}.c)"
+    if sg_run is None:
+        from oracle import emit_c
+
+        sg_run = emit_c.compile_plan(plan, parallel="pragma", openmp=True).sg_run
+        kind, what = "port", "emitted C restated by oracle/emit_c.py (emit.py:153-245)"
     x = np.zeros(plan.value_array_size, np.float64)
-    x[: plan.input_count] = inputs
     for _ in range(max(warmup, 1)):
-        run.sg_run(x)
+        x[:] = 0.0
+        x[: plan.input_count] = inputs
+        sg_run(x)
     times = []
     t_start = time.perf_counter()
     for _ in range(steps):
         t0 = time.perf_counter()
-        run.sg_run(x)
+        sg_run(x)
         times.append(time.perf_counter() - t0)
         if time.perf_counter() - t_start > budget_s:
             break
     t = statistics.mean(times)
-    return {"seconds_per_eval": t, "evals": len(times), "cores": cores, "x": x}
+    return {"seconds_per_eval": t, "evals": len(times), "cores": cores, "x": x, "kind": kind, "what": what}
 
 
 def cpu_model():
@@ -187,16 +227,16 @@ def run_reference(args):
     key, plan, _, _ = build_workload(args, 0, 1)
     n_out = len(plan.outputs)
     inputs = workload_inputs(args, seed=0)
-    res = cpu_reference(plan, inputs, args.steps, args.warmup, budget_s=120.0)
+    res = cpu_reference(plan, inputs, args.steps, args.warmup, budget_s=120.0, key=key)
     v = n_out / res["seconds_per_eval"]
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": res["evals"], "warmup": args.warmup, "ms_per_step": res["seconds_per_eval"] * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": workload_name(args, n_out), "w": args.w},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": res["cores"], "kind": "port",
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": res["cores"], "kind": res["kind"],
                          "sample": f"full plan, {res['evals']} sg_run evaluations after {args.warmup} warm-up; "
-                                   f"emitted C (oracle/emit_c.py) -O3 -ffp-contract=off -fopenmp, {cpu_model()}"},
+                                   f"{res['what']}, cc -O3 -ffp-contract=off -fopenmp, {cpu_model()}"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -337,13 +377,13 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        res = cpu_reference(plan, inputs, args.cpu_steps, 1)
+        res = cpu_reference(plan, inputs, args.cpu_steps, 1, key=key)
         cpu_ok = bool(np.array_equal(res["x"][np.asarray(plan.outputs)].view(np.uint64),
                                      out.cpu().numpy().view(np.uint64)))
-        cpu = {"value": n_out / res["seconds_per_eval"], "unit": UNIT, "cores": res["cores"], "kind": "port",
-               "sample": f"full plan ({n_out} nnz), {res['evals']} sg_run evaluations; emitted C "
-                         f"(oracle/emit_c.py, restating emit.py:153-245) -O3 -ffp-contract=off -fopenmp on "
-                         f"{res['cores']} threads of {cpu_model()}; GPU==CPU bitwise: {cpu_ok}"}
+        cpu = {"value": n_out / res["seconds_per_eval"], "unit": UNIT, "cores": res["cores"], "kind": res["kind"],
+               "sample": f"full plan ({n_out} nnz), {res['evals']} sg_run evaluations; {res['what']}, "
+                         f"cc -O3 -ffp-contract=off -fopenmp on {res['cores']} threads of {cpu_model()}; "
+                         f"GPU==CPU bitwise: {cpu_ok}"}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
