@@ -5,9 +5,11 @@ Default workload = BASELINE.json configs[1] (C2): out = L.M.L^T + A on the
 cotan Laplacian of a 1000 x 1000 grid mesh (10^6 vertices, ~25M output
 nonzeros), plan built by the template-instancing builder
 (paper_2110_12865_b200.programs.mesh; bit-identical to the reference trace,
-tests/test_builders.py).  One step = every dependency wave of the plan + the
-CSR output gather, on inputs already resident in HBM; the value array
-(~430 MB) and tables exceed the 126 MB L2, so no explicit flush is needed.
+tests/test_builders.py).  One step = one CSR-mode evaluation (sgb_run_csr:
+every dependency wave, outputs stored at their CSR positions by the producing
+kernels) on inputs already resident in HBM; the value array (~385 MB), the
+25M-entry CSR output (~200 MB) and the tables exceed the 126 MB L2, so no
+explicit flush is needed.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
@@ -271,7 +273,7 @@ def main():
         barrier = None
 
     from paper_2110_12865_b200 import DevicePlan
-    from paper_2110_12865_b200.metrics import plan_balg, wave_traffic
+    from paper_2110_12865_b200.metrics import csr_wave_traffic, plan_balg
 
     key, plan, row_ptr, col_idx = build_workload(args, rank, world, barrier)
     n_out = len(plan.outputs)
@@ -281,10 +283,12 @@ def main():
     out = torch.empty(n_out, dtype=torch.float64, device=x.device)
     stream = torch.cuda.current_stream()
 
+    if dp.lowered.needs_zero == 2:
+        raise SystemExit("bench: plan reads slots later waves write; re-zeroing per step is not implemented")
+
     # warm-up, then parity of this rank's evaluation against the oracle (rank 0)
     for _ in range(args.warmup):
-        dp.run_values(x)
-        dp.gather_outputs(x, out)
+        dp.run_csr(x, out)
     torch.cuda.synchronize()
     parity = None
     if rank == 0:
@@ -296,17 +300,16 @@ def main():
         log(f"[bench] parity vs oracle: {parity}")
 
     # settle clocks for ~1 s of real work (untimed), sampling clocks throughout
-    n_w = dp.launches
+    n_w = dp.csr_launches
     sampler = ClockSampler(local)
     with sampler:
         t_end = time.perf_counter() + 1.0
         while time.perf_counter() < t_end:
             for _ in range(20):
-                dp.run_values(x)
-                dp.gather_outputs(x, out)
+                dp.run_csr(x, out)
             torch.cuda.synchronize()
-        # ---- timed region ----
-        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_w + 2)] for _ in range(args.steps)]
+        # ---- timed region: one step = every CSR-mode wave (inputs -> CSR values) ----
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_w + 1)] for _ in range(args.steps)]
         if barrier:
             barrier()
         torch.cuda.synchronize()
@@ -314,17 +317,15 @@ def main():
             e = evs[k]
             for w in range(n_w):
                 e[w].record(stream)
-                dp.run_wave(x, w)
+                dp.run_wave(x, w, out=out)
             e[n_w].record(stream)
-            dp.gather_outputs(x, out)
-            e[n_w + 1].record(stream)
         torch.cuda.synchronize()
         if barrier:
             barrier()
-    total_ms = evs[0][0].elapsed_time(evs[-1][n_w + 1])
-    per_launch = np.zeros(n_w + 1)
+    total_ms = evs[0][0].elapsed_time(evs[-1][n_w])
+    per_launch = np.zeros(n_w)
     for e in evs:
-        for j in range(n_w + 1):
+        for j in range(n_w):
             per_launch[j] += e[j].elapsed_time(e[j + 1])
     per_launch /= args.steps
     if world > 1:
@@ -356,7 +357,7 @@ def main():
         return 0
 
     # ---- roofline of the dominant launch ----
-    traffic = wave_traffic(plan, dp.lowered)
+    traffic = csr_wave_traffic(plan, dp.lowered)
     dom = int(np.argmax(per_launch))
     dom_bytes = traffic[dom].bytes
     achieved = dom_bytes / (per_launch[dom] * 1e-3) / 1e9
@@ -396,12 +397,14 @@ def main():
             "parallelism": f"replicas x{world}: one full evaluation per GPU per step (independent value sets)",
             "l2": "no flush: value array + tables exceed the 126 MB L2",
             "clock_settle": "1 s of untimed evaluations before the timed region",
-            "parity": parity, "achieved_hbm_gbs_step": step_bytes / (ms_per_step * 1e-3) / 1e9,
+            "parity": parity, "mode": "CSR (sgb_run_csr: outputs stored by their producers, no gather pass)",
+            "achieved_hbm_gbs_step": step_bytes / (ms_per_step * 1e-3) / 1e9,
             "balg_bytes_step": step_bytes, "balg_bytes_single_pass": plan_balg(plan),
+            "balg_gbs_single_pass": plan_balg(plan) / (ms_per_step * 1e-3) / 1e9,
         },
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": ncu_traffic, "kernel": f"wave_single ({traffic[dom].name})"
-                     if dom < n_w else "gather_outputs", "algorithmic_bytes": dom_bytes,
+                     "frac": achieved / peak, "traffic": ncu_traffic, "kernel": traffic[dom].name,
+                     "algorithmic_bytes": dom_bytes,
                      "avg_launch_ms": float(per_launch[dom]), "peak_source": peak_src},
         "launches": [{"name": t.name, "ms": float(ms), "alg_bytes": t.bytes,
                       "gbs": t.bytes / (ms * 1e-3) / 1e9 if ms > 0 else None}
@@ -409,7 +412,7 @@ def main():
         "e2e": {"value": world * n_out / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * int(plan.input_count),
                 "d2h_bytes_per_step": 8 * n_out, "api": "DevicePlan.run_outputs_host -> sgb_run_outputs_host",
                 "matches_device_run": e2e_ok},
-        "gpu_launches": args.steps * (n_w + 1),
+        "gpu_launches": args.steps * dp.csr_units,
         "clocks": sampler.summary(),
         "cpu_baseline": cpu,
     }

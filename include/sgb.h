@@ -17,6 +17,7 @@
  *     sgb_sg_run(plan, x, c, p)        == sg_run(x, c, p), host buffers
  *     sgb_run_values(plan, x_dev, s)   == sg_run on a device-resident x
  *     sgb_gather_outputs(plan, ...)    == x[plan.outputs] (codegen.py:445)
+ *     sgb_run_csr(plan, x, out, s)     == sg_run + x[plan.outputs] in one pass
  *     sgb_run_outputs_host(plan, ...)  == run(inputs)[plan.outputs], host in/out
  *     sgb_run_batch(plan, X_dev, ...)  == B independent sg_run calls, batch-fastest X
  *
@@ -44,17 +45,20 @@ typedef struct sgb_plan sgb_plan;
 typedef struct sgb_group {
   int64_t n;         /* instances (KernelPlan.instances) */
   int64_t dest_base; /* result r of instance i at dest_base + r*n + i (codegen.py:265) */
-  int64_t p_off;     /* KernelPlan.p_base */
+  int64_t p_off;     /* KernelPlan.p_base (synthetic copy groups: past the plan's table) */
   int64_t c_off;     /* KernelPlan.c_base */
   int64_t tape_off;  /* first tape row */
-  int64_t blk_begin; /* first block of this group inside its launch unit */
   int64_t cb_off;    /* compressed columns (flags & 32): first chunk base in cbase */
   int64_t co_off;    /*                                  first offset in coff */
   int64_t a0_base;   /* affine column 0 (flags & 64): index = a0_base + a0_stride * i */
   int64_t a0_stride;
+  int64_t ob_off;    /* output positions (flags & 128): first chunk base in obase */
+  int64_t oo_off;    /*   first offset in ooff (flags & 128) or entry in opos32 (flags & 256) */
   int32_t n_roots, n_slots, n_ret, n_const;
   int32_t tape_len, n_regs, kind, flags;
   int32_t slot_off, sop_off, sop_len, unit;
+  int32_t variant; /* sum-of-products width class (factors <= 2, 4, 8, 16, 32) */
+  int32_t reserved;
 } sgb_group;
 
 /* Host-side device plan handed to sgb_plan_create (all pointers host memory,
@@ -63,23 +67,27 @@ typedef struct sgb_plan_desc {
   int64_t value_array_size; /* ExecutionPlan.value_array_size */
   int64_t input_count;      /* ExecutionPlan.input_count */
   int32_t n_groups;
-  int32_t n_waves;
+  int32_t n_waves;          /* value-mode waves; a CSR-only unit may use wave n_waves */
   int32_t n_units;
-  int32_t reserved;
-  const sgb_group *groups; /* ordered by (wave, launch unit) */
-  const int64_t *units;    /* [n_units][8]: wave, kind (0 tape, 1 sum-of-products),
-                              variant, group_begin, group_end, blocks, block_size,
-                              scratch registers per lane */
-  const uint32_t *tape;    /* [tape_rows][4] device tape words, see lower.assemble() */
+  int32_t needs_zero;       /* 0: no load reads an unwritten slot; 1: some read slots nothing writes
+                               (zero the buffer once); 2: some read slots a later wave writes
+                               (re-zero before every evaluation, codegen.py:419, 434-443) */
+  const sgb_group *groups;  /* ordered by (wave, launch unit) */
+  const int64_t *units;     /* [n_units][10]: wave, kind (0 tape, 1 sum-of-products), variant (tape VEC),
+                               group_begin, group_end, tile_begin, tile_end, block_size,
+                               scratch registers per lane, flags (1 = CSR mode only) */
+  const int32_t *tiles;     /* [n_tiles][2]: group, first instance -- one block each, in launch order */
+  int64_t n_tiles;
+  const uint32_t *tape;     /* [tape_rows][4] device tape words, see lower.assemble() */
   int64_t tape_rows;
   const double *imm;
   int64_t n_imm;
-  const int32_t *sop; /* per sum-of-products group: newterm mask, neg mask */
+  const uint32_t *sop;      /* per sum-of-products group: newterm mask, negate mask */
   int64_t n_sop;
   const int32_t *slot_col;   /* per slot: retained column or -1 (coherent) */
   const int64_t *slot_delta; /* per slot: coherence delta from slot 0 */
   int64_t n_slot;
-  const uint32_t *positions; /* ExecutionPlan.positions (u32, unchanged) */
+  const uint32_t *positions; /* ExecutionPlan.positions (u32, unchanged) + copy-group columns */
   int64_t n_positions;
   const double *constants; /* ExecutionPlan.constants (f64, unchanged) */
   int64_t n_constants;
@@ -87,6 +95,12 @@ typedef struct sgb_plan_desc {
   int64_t n_cbase;
   const uint16_t *coff; /* compressed index columns: offset per (column, instance) */
   int64_t n_coff;
+  const uint32_t *obase; /* output positions: base per (root, 32 instances) */
+  int64_t n_obase;
+  const uint16_t *ooff; /* output positions: offset per (root, instance), 0xFFFF = not an output */
+  int64_t n_ooff;
+  const uint32_t *opos32; /* output positions, wide form, 0xFFFFFFFF = not an output */
+  int64_t n_opos32;
   const int64_t *outputs; /* ExecutionPlan.outputs */
   int64_t n_outputs;
 } sgb_plan_desc;
@@ -99,20 +113,27 @@ void sgb_plan_destroy(sgb_plan *plan);
  * everything else zero.  All dependency waves are launched on `stream`. */
 int sgb_run_values(sgb_plan *plan, double *x_dev, void *stream);
 
-/* One dependency wave of sgb_run_values (waves must run in order 0..n-1);
- * for per-launch timing and profiling. */
-int sgb_run_wave(sgb_plan *plan, double *x_dev, int wave, void *stream);
+/* inputs -> CSR values in one pass: out_dev[k] == x[outputs[k]] after sg_run
+ * (codegen.py:445), written directly by the producing kernels (no gather).
+ * x_dev holds the inputs and serves as scratch for intermediates; result
+ * ranges nobody re-reads are not written to it. */
+int sgb_run_csr(sgb_plan *plan, double *x_dev, double *out_dev, void *stream);
+
+/* One dependency wave (waves in order 0..sgb_plan_waves(plan, csr)-1); out_dev
+ * NULL = value mode (sgb_run_values), else CSR mode (sgb_run_csr).  For
+ * per-launch timing and profiling. */
+int sgb_run_wave(sgb_plan *plan, double *x_dev, double *out_dev, int wave, void *stream);
 
 /* out_dev[k] = x_dev[outputs[k]]  (codegen.py:445). */
 int sgb_gather_outputs(sgb_plan *plan, const double *x_dev, double *out_dev, void *stream);
 
 /* The reference ABI with host buffers: copies x in, runs, copies x back.
- * c / p must be the plan's own tables (checked by length only: they were
- * uploaded at create time and may be NULL). */
+ * c / p must be the plan's own tables (they were uploaded at create time and
+ * may be NULL). */
 int sgb_sg_run(sgb_plan *plan, double *x_host, const double *c_host, const unsigned *p_host);
 
-/* Host inputs[input_count] -> host outputs[n_outputs]; only those bytes cross
- * PCIe.  Synchronous. */
+/* Host inputs[input_count] -> host outputs[n_outputs] through sgb_run_csr;
+ * only those bytes cross PCIe.  Synchronous. */
 int sgb_run_outputs_host(sgb_plan *plan, const double *inputs_host, double *outputs_host);
 
 /* Batched evaluation: X_dev[addr * ld + b] for b < batch (ld >= batch),
@@ -120,15 +141,19 @@ int sgb_run_outputs_host(sgb_plan *plan, const double *inputs_host, double *outp
  * pass over the index tables. */
 int sgb_run_batch(sgb_plan *plan, double *X_dev, int64_t ld, int64_t batch, void *stream);
 
+/* Batched CSR mode: out_dev[k * ld_out + b] == X[outputs[k] * ld + b] after sgb_run_batch. */
+int sgb_run_batch_csr(sgb_plan *plan, double *X_dev, int64_t ld, int64_t batch, double *out_dev, int64_t ld_out,
+                      void *stream);
+
 /* Outputs of a batched evaluation: out_dev[k * ld_out + b] = X_dev[outputs[k] * ld + b]. */
 int sgb_gather_outputs_batch(sgb_plan *plan, const double *X_dev, int64_t ld, int64_t batch,
                              double *out_dev, int64_t ld_out, void *stream);
 
-/* Dependency waves of the plan (sgb_run_wave range). */
-int sgb_plan_launches(const sgb_plan *plan);
+/* Dependency waves of the plan in value mode (csr = 0) or CSR mode (csr = 1). */
+int sgb_plan_waves(const sgb_plan *plan, int csr);
 
-/* Kernel launches one sgb_run_values issues (launch units, >= waves). */
-int sgb_plan_units(const sgb_plan *plan);
+/* Kernel launches one evaluation issues in value / CSR mode. */
+int sgb_plan_units(const sgb_plan *plan, int csr);
 
 const char *sgb_last_error(void);
 

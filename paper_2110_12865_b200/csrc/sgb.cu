@@ -5,8 +5,8 @@
 // Semantics are those of the reference evaluators interpret_plan
 // (codegen.py:404-512) and the emitted sg_run (emit.py:90-195):
 //   * kernels run in dependency waves; every group of a wave runs inside the
-//     wave's launch units (a tape unit, one sum-of-products unit per width
-//     class) through a block -> group table;
+//     wave's launch units (tape units, one sum-of-products unit) through a
+//     per-block tile table (group, first instance);
 //   * every instance evaluates its template's live nodes in stored order; n-ary
 //     ADD / MUL fold left (codegen.py:472-481); SELECT is c < 0 (codegen.py:490);
 //   * results land at dest_base + r*N + i (codegen.py:492-494);
@@ -16,12 +16,19 @@
 // __ddiv_rn / __dsqrt_rn (never contracted; the file is also built with
 // --fmad=false), so EXACT_OPS templates reproduce the CPU reference bit for bit.
 //
+// CSR mode (sgb_run_csr): results that are outputs (codegen.py:445
+// `x[plan.outputs]`) are stored straight to their CSR position through a
+// per-group output-position table, the sum-of-products tiles of the last wave
+// are scheduled in CSR order so partially written sectors merge in L2, groups
+// nobody re-reads skip the value-array store, and outputs that are inputs or
+// duplicates run as width-1 copy groups.  No separate gather pass.
+//
 // The path is an irregular gather / elementwise graph (no tensor cores): the
 // kernels are built for memory-level parallelism -- every index and value load
-// of an instance is issued before the first use, streaming data (index tables,
+// of a tile is issued before the first use, streaming data (index tables,
 // results nobody re-reads) carries an L2 evict-first policy so the gathered
-// intermediates stay in the 126 MB L2, and the launch units keep register
-// counts low enough for high occupancy.
+// intermediates stay in the 126 MB L2, and register counts stay low enough for
+// 50% occupancy.
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -36,17 +43,28 @@
 
 namespace {
 
-// tape op codes: lower.py T_*
+// tape op codes: lower.py T_*; the op byte of a word is op | nega << 6 | negb << 7
 enum : int {
   T_MUL = 0, T_ADD, T_SUB, T_DIV, T_MADD, T_NEG, T_SQRT, T_SEL, T_IMM, T_ST, T_SLOW, T_MSUB, T_RMSUB
 };
 enum : int { KIND_TAPE = 0, KIND_SOP = 1 };
 enum : int {
-  FLAG_SELFREF = 1, FLAG_INTERLEAVED = 2, FLAG_SERIAL = 4, FLAG_STREAM = 16, FLAG_W16 = 32, FLAG_AFFINE0 = 64
+  FLAG_SELFREF = 1, FLAG_INTERLEAVED = 2, FLAG_SERIAL = 4, FLAG_STREAM = 16, FLAG_W16 = 32,
+  FLAG_AFFINE0 = 64, FLAG_OPOS16 = 128, FLAG_OPOS32 = 256, FLAG_CSR_ONLY = 512, FLAG_COHERENT = 1024
 };
-enum : int { U_WAVE = 0, U_KIND, U_VARIANT, U_G0, U_G1, U_BLOCKS, U_BS, U_REGS, U_COUNT };
-constexpr int PRE = 8;  // slot loads kept in flight by the tape prologue
-constexpr int MAX_BATCH_WARPS = 8;
+enum : int {
+  U_WAVE = 0, U_KIND, U_VARIANT, U_G0, U_G1, U_T0, U_T1, U_BS, U_REGS, U_FLAGS, U_COUNT
+};
+enum : int { UNIT_CSR_ONLY = 1 };
+constexpr int PRE = 8;        // slot loads kept in flight by the tape prologue
+constexpr int SOP_BS = 256;   // sum-of-products block
+constexpr int SOP_BATCH = 16; // factor loads in flight per instance
+constexpr int BATCH_WARPS = 8;
+constexpr uint32_t NONE = 0xFFFFFFFFu;
+
+// instances per thread of the sum-of-products kernel, per width class (lower.SOP_CLASSES)
+__host__ __device__ constexpr int sop_vec(int cls) { return cls <= 1 ? 4 : (cls == 2 ? 2 : 1); }
+__host__ __device__ constexpr int sop_lmax(int cls) { return cls == 0 ? 2 : cls == 1 ? 4 : cls == 2 ? 8 : cls == 3 ? 16 : 32; }
 
 thread_local std::string g_err;
 
@@ -66,13 +84,16 @@ struct Tables {
   const sgb_group *groups;
   const uint32_t *tape;  // 4 x u32 per tape word
   const double *imm;
-  const int32_t *sop;
+  const uint32_t *sop;   // per SOP group: newterm mask, negate mask
   const int32_t *slot_col;
   const int64_t *slot_delta;
   const uint32_t *pos;
   const double *con;
   const uint32_t *cbase;  // compressed columns: per (column, 32-instance chunk) base
   const uint16_t *coff;   //                     per (column, instance) offset
+  const uint32_t *obase;  // output positions: per (root, chunk) base
+  const uint16_t *ooff;   //                   per (root, instance) offset, 0xFFFF = not an output
+  const uint32_t *opos32; //                   wide form, NONE = not an output
 };
 
 // ---- cache-policy helpers ---------------------------------------------------------
@@ -84,69 +105,66 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
 // streaming index-table read: no L1 allocation, L2 evict-first
 __device__ __forceinline__ uint32_t ld_index(const uint32_t *a, uint64_t pol) {
   uint32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
-               : "=r"(v) : "l"(a), "l"(pol));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ uint16_t ld_index16(const uint16_t *a, uint64_t pol) {
+  uint16_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(a), "l"(pol));
   return v;
 }
 __device__ __forceinline__ double ld_const(const double *a, uint64_t pol) {
   double v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
-               : "=d"(v) : "l"(a), "l"(pol));
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
   return v;
 }
-__device__ __forceinline__ void st_result(double *a, double v, bool stream, uint64_t pol) {
-  if (stream)
-    asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
-  else
-    *a = v;
+__device__ __forceinline__ void st_stream(double *a, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
 }
 
-// Largest g in [g0, g1) with begin[g] <= blk (block -> group table lookup).
-__device__ __forceinline__ int find_group(const int64_t *begin, int g0, int g1, int64_t blk) {
-  int lo = g0, hi = g1 - 1;
-  while (lo < hi) {
-    int mid = (lo + hi + 1) >> 1;
-    if (__ldg(begin + mid) <= blk) lo = mid; else hi = mid - 1;
-  }
-  return lo;
-}
-
-// Retained column `col` of instance i: the plan's u32 table, or the compressed
-// form base[col][i/32] + off16[col][i] (lower.compress_columns).
+// Retained column `col` of instance i: affine (column 0 only), the compressed
+// form base[col][i/32] + off16[col][i] (lower.compress_column), or the plan's u32 table.
 __device__ __forceinline__ uint32_t column_index(const Tables &T, const sgb_group &G, int col, int64_t i,
-                                                 bool inter, uint64_t pol) {
+                                                 uint64_t pol) {
   if (col == 0 && (G.flags & FLAG_AFFINE0)) return (uint32_t)(G.a0_base + G.a0_stride * i);
   if (G.flags & FLAG_W16) {
     const int64_t nch = (G.n + 31) >> 5;
-    const uint32_t base = __ldg(T.cbase + G.cb_off + (int64_t)col * nch + (i >> 5));
-    uint16_t off;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;"
-                 : "=h"(off) : "l"(T.coff + G.co_off + (int64_t)col * G.n + i), "l"(pol));
-    return base + off;
+    return __ldg(T.cbase + G.cb_off + (int64_t)col * nch + (i >> 5)) +
+           ld_index16(T.coff + G.co_off + (int64_t)col * G.n + i, pol);
   }
-  const int64_t e = inter ? G.p_off + i * G.n_ret + col : G.p_off + (int64_t)col * G.n + i;
+  const int64_t e = (G.flags & FLAG_INTERLEAVED) ? G.p_off + i * G.n_ret + col : G.p_off + (int64_t)col * G.n + i;
   return ld_index(T.pos + e, pol);
 }
 
-// Index decode == slot_addresses (codegen.py:373-388): retained slot -> its
-// column of the position table; coherent slot -> slot-0 entry + delta.
-__device__ __forceinline__ int64_t slot_addr(const Tables &T, const sgb_group &G, int s, int64_t i,
-                                             bool inter, uint32_t idx0, uint64_t pol) {
-  const int col = __ldg(T.slot_col + G.slot_off + s);
-  if (col < 0) return (int64_t)idx0 + __ldg(T.slot_delta + G.slot_off + s);
-  if (col == 0) return idx0;
-  return (int64_t)column_index(T, G, col, i, inter, pol);
+// Output (CSR) position of root r of instance i, or NONE.
+__device__ __forceinline__ uint32_t out_pos(const Tables &T, const sgb_group &G, int r, int64_t i, uint64_t pol) {
+  if (G.flags & FLAG_OPOS16) {
+    const int64_t nch = (G.n + 31) >> 5;
+    const uint16_t off = ld_index16(T.ooff + G.oo_off + (int64_t)r * G.n + i, pol);
+    return off == 0xFFFFu ? NONE : __ldg(T.obase + G.ob_off + (int64_t)r * nch + (i >> 5)) + off;
+  }
+  if (G.flags & FLAG_OPOS32) return ld_index(T.opos32 + G.oo_off + (int64_t)r * G.n + i, pol);
+  return NONE;
 }
 
-__device__ __forceinline__ uint32_t slot0_index(const Tables &T, const sgb_group &G, int64_t i,
-                                                bool inter, uint64_t pol) {
-  if (G.n_slots == 0) return 0u;
-  return column_index(T, G, 0, i, inter, pol);
+// Store root r of instance i: the value array (unless CSR mode and nobody
+// re-reads it) and, in CSR mode, its output position.
+__device__ __forceinline__ void store_root(const Tables &T, const sgb_group &G, int r, int64_t i, double v,
+                                           double *x, int64_t ld, int64_t b, double *out, int64_t ld_out,
+                                           bool csr, uint64_t pol) {
+  const bool stream = G.flags & FLAG_STREAM;
+  if (!(csr && stream)) {
+    double *a = x + (G.dest_base + (int64_t)r * G.n + i) * ld + b;
+    if (stream) st_stream(a, v, pol); else *a = v;
+  }
+  if (csr) {
+    const uint32_t o = out_pos(T, G, r, i, pol);
+    if (o != NONE) out[(int64_t)o * ld_out + b] = v;
+  }
 }
 
 // ---- double-double integer power (POW k >= 3; k == 2 is an exact x*x) ----------
-__device__ __forceinline__ void dd_mul(double ah, double al, double bh, double bl, double &rh,
-                                       double &rl) {
+__device__ __forceinline__ void dd_mul(double ah, double al, double bh, double bl, double &rh, double &rl) {
   double p = __dmul_rn(ah, bh);
   double e = __fma_rn(ah, bh, -p);
   e = __dadd_rn(e, __dadd_rn(__dmul_rn(ah, bl), __dmul_rn(al, bh)));
@@ -182,7 +200,8 @@ __device__ __noinline__ double slow_op(unsigned kind, double a, int k) {
 // y / z / w = byte offsets of dst / a / b in the lane's scratch column (w is the
 // immediate index, root index or kind<<16|k for IMM / ST / SLOW).  Scratch is
 // shared memory addressed with 32-bit shared addresses; instance v of a lane
-// sits VS bytes after instance 0.
+// sits VS bytes after instance 0.  Sign flags are part of the switch key, so a
+// negated operand is the free negate modifier of DADD / DMUL, not extra work.
 __device__ __forceinline__ double lds(uint32_t addr) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
@@ -191,98 +210,77 @@ __device__ __forceinline__ double lds(uint32_t addr) {
 __device__ __forceinline__ void sts(uint32_t addr, double v) {
   asm volatile("st.shared.f64 [%0], %1;" ::"r"(addr), "d"(v) : "memory");
 }
-__device__ __forceinline__ double flip(double v, uint32_t bit) {  // exact negation when bit = 1
-  return __longlong_as_double(__double_as_longlong(v) ^ ((unsigned long long)bit << 63));
-}
+
+#define SGB_NEG(NA, v) ((NA) ? -(v) : (v))
+#define SGB_BIN(OPC, NA, NB, EXPR)                                                  \
+  case (OPC) | ((NA) << 6) | ((NB) << 7): {                                         \
+    _Pragma("unroll") for (int v = 0; v < VEC; ++v) {                               \
+      const double a = SGB_NEG(NA, lds(pa + v * VS));                               \
+      const double b = SGB_NEG(NB, lds(pb + v * VS));                               \
+      sts(pd + v * VS, EXPR);                                                       \
+    }                                                                               \
+  } break;
+#define SGB_FUSED(OPC, NA, NB, EXPR)                                                \
+  case (OPC) | ((NA) << 6) | ((NB) << 7): {                                         \
+    _Pragma("unroll") for (int v = 0; v < VEC; ++v) {                               \
+      const double a = SGB_NEG(NA, lds(pa + v * VS));                               \
+      const double b = SGB_NEG(NB, lds(pb + v * VS));                               \
+      const double c = lds(pc + v * VS);                                            \
+      sts(pd + v * VS, EXPR);                                                       \
+    }                                                                               \
+  } break;
+#define SGB_SIGNS(M, OPC, EXPR) M(OPC, 0, 0, EXPR) M(OPC, 1, 0, EXPR) M(OPC, 0, 1, EXPR) M(OPC, 1, 1, EXPR)
 
 template <int VEC, int VS>
-__device__ __forceinline__ void run_tape(const Tables &T, const sgb_group &G, uint32_t Rb, double *x,
-                                         int64_t ld, int64_t b, const int64_t (&iv)[VEC],
-                                         const bool (&ok)[VEC], int phase, bool selfref, uint64_t pol) {
+__device__ __forceinline__ void run_tape(const Tables &T, const sgb_group &G, uint32_t Rb, double *x, int64_t ld,
+                                         int64_t b, double *out, int64_t ld_out, bool csr,
+                                         const int64_t (&iv)[VEC], const bool (&ok)[VEC], int phase, bool selfref,
+                                         uint64_t pol) {
   const uint4 *tp = reinterpret_cast<const uint4 *>(T.tape) + G.tape_off;
-  const bool stream = G.flags & FLAG_STREAM;
   const int len = G.tape_len;
   uint4 next = len > 0 ? __ldg(tp) : make_uint4(0, 0, 0, 0);
-  for (int pc = 0; pc < len; ++pc) {
+  for (int k = 0; k < len; ++k) {
     const uint4 w = next;
-    if (pc + 1 < len) next = __ldg(tp + pc + 1);  // prefetch the next word
-    const uint32_t na = (w.x >> 6) & 1u, nb = (w.x >> 7) & 1u;
-    const uint32_t cofs = (w.x >> 8) << 3;
-    switch (w.x & 63u) {
-      case T_MUL:
-#pragma unroll
-        for (int v = 0; v < VEC; ++v)
-          sts(Rb + w.y + v * VS, __dmul_rn(flip(lds(Rb + w.z + v * VS), na), flip(lds(Rb + w.w + v * VS), nb)));
-        break;
-      case T_ADD:
-#pragma unroll
-        for (int v = 0; v < VEC; ++v)
-          sts(Rb + w.y + v * VS, __dadd_rn(flip(lds(Rb + w.z + v * VS), na), flip(lds(Rb + w.w + v * VS), nb)));
-        break;
-      case T_SUB:
-#pragma unroll
-        for (int v = 0; v < VEC; ++v)
-          sts(Rb + w.y + v * VS, __dsub_rn(flip(lds(Rb + w.z + v * VS), na), flip(lds(Rb + w.w + v * VS), nb)));
-        break;
-      case T_MADD:
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) {
-          const double p = __dmul_rn(flip(lds(Rb + w.z + v * VS), na), flip(lds(Rb + w.w + v * VS), nb));
-          sts(Rb + w.y + v * VS, __dadd_rn(p, lds(Rb + cofs + v * VS)));
-        }
-        break;
-      case T_MSUB:
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) {
-          const double p = __dmul_rn(flip(lds(Rb + w.z + v * VS), na), flip(lds(Rb + w.w + v * VS), nb));
-          sts(Rb + w.y + v * VS, __dsub_rn(p, lds(Rb + cofs + v * VS)));
-        }
-        break;
-      case T_RMSUB:
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) {
-          const double p = __dmul_rn(flip(lds(Rb + w.z + v * VS), na), flip(lds(Rb + w.w + v * VS), nb));
-          sts(Rb + w.y + v * VS, __dsub_rn(lds(Rb + cofs + v * VS), p));
-        }
-        break;
-      case T_DIV:
-#pragma unroll
-        for (int v = 0; v < VEC; ++v)
-          sts(Rb + w.y + v * VS, __ddiv_rn(flip(lds(Rb + w.z + v * VS), na), flip(lds(Rb + w.w + v * VS), nb)));
-        break;
+    if (k + 1 < len) next = __ldg(tp + k + 1);  // prefetch the next word
+    const uint32_t pd = Rb + w.y, pa = Rb + w.z, pb = Rb + w.w, pc = Rb + ((w.x >> 8) << 3);
+    switch (w.x & 0xFFu) {
+      SGB_SIGNS(SGB_BIN, T_MUL, __dmul_rn(a, b))
+      SGB_SIGNS(SGB_BIN, T_ADD, __dadd_rn(a, b))
+      SGB_SIGNS(SGB_BIN, T_SUB, __dsub_rn(a, b))
+      SGB_SIGNS(SGB_BIN, T_DIV, __ddiv_rn(a, b))
+      SGB_SIGNS(SGB_FUSED, T_MADD, __dadd_rn(__dmul_rn(a, b), c))
+      SGB_SIGNS(SGB_FUSED, T_MSUB, __dsub_rn(__dmul_rn(a, b), c))
+      SGB_SIGNS(SGB_FUSED, T_RMSUB, __dsub_rn(c, __dmul_rn(a, b)))
       case T_NEG:
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) sts(Rb + w.y + v * VS, -lds(Rb + w.z + v * VS));
+        for (int v = 0; v < VEC; ++v) sts(pd + v * VS, -lds(pa + v * VS));
         break;
       case T_SQRT:
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) sts(Rb + w.y + v * VS, __dsqrt_rn(lds(Rb + w.z + v * VS)));
+        for (int v = 0; v < VEC; ++v) sts(pd + v * VS, __dsqrt_rn(lds(pa + v * VS)));
         break;
       case T_SEL:
 #pragma unroll
         for (int v = 0; v < VEC; ++v)
-          sts(Rb + w.y + v * VS,
-              lds(Rb + w.z + v * VS) < 0.0 ? lds(Rb + w.w + v * VS) : lds(Rb + cofs + v * VS));
+          sts(pd + v * VS, lds(pa + v * VS) < 0.0 ? lds(pb + v * VS) : lds(pc + v * VS));
         break;
       case T_IMM: {
         const double imm = __ldg(T.imm + w.w);
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) sts(Rb + w.y + v * VS, imm);
+        for (int v = 0; v < VEC; ++v) sts(pd + v * VS, imm);
         break;
       }
       case T_ST:
         if (!selfref || (int)w.w == phase) {
 #pragma unroll
           for (int v = 0; v < VEC; ++v)
-            if (ok[v])
-              st_result(x + (G.dest_base + (int64_t)w.w * G.n + iv[v]) * ld + b, lds(Rb + w.z + v * VS),
-                        stream, pol);
+            if (ok[v]) store_root(T, G, (int)w.w, iv[v], lds(pa + v * VS), x, ld, b, out, ld_out, csr, pol);
         }
         break;
       default:  // T_SLOW
 #pragma unroll
         for (int v = 0; v < VEC; ++v)
-          sts(Rb + w.y + v * VS, slow_op(w.w >> 16, lds(Rb + w.z + v * VS), (int)(w.w & 0xFFFFu)));
+          sts(pd + v * VS, slow_op(w.w >> 16, lds(pa + v * VS), (int)(w.w & 0xFFFFu)));
         break;
     }
   }
@@ -291,17 +289,21 @@ __device__ __forceinline__ void run_tape(const Tables &T, const sgb_group &G, ui
 // Prologue: hoisted slot loads (emit.py:108-124), PRE loads in flight per lane;
 // slot s of this lane's instance goes to byte offset s * stride8.
 __device__ __forceinline__ void load_slots(const Tables &T, const sgb_group &G, uint32_t Rb, uint32_t stride8,
-                                           const double *x, int64_t ld, int64_t i, int64_t b, bool inter,
-                                           bool coherent_read, uint64_t pol) {
-  const uint32_t idx0 = slot0_index(T, G, i, inter, pol);
+                                           const double *x, int64_t ld, int64_t i, int64_t b, bool coherent_read,
+                                           uint64_t pol) {
+  const uint32_t idx0 = G.n_slots ? column_index(T, G, 0, i, pol) : 0u;
+  const int32_t *scol = T.slot_col + G.slot_off;
+  const int64_t *sdel = T.slot_delta + G.slot_off;
   for (int s0 = 0; s0 < G.n_slots; s0 += PRE) {
     double v[PRE];
 #pragma unroll
     for (int u = 0; u < PRE; ++u) {
       const int s = s0 + u;
       if (s < G.n_slots) {
-        const int64_t a = slot_addr(T, G, s, i, inter, idx0, pol) * ld + b;
-        v[u] = coherent_read ? x[a] : __ldg(x + a);
+        const int col = __ldg(scol + s);
+        const int64_t a = col < 0 ? (int64_t)idx0 + __ldg(sdel + s)
+                                  : (col == 0 ? (int64_t)idx0 : (int64_t)column_index(T, G, col, i, pol));
+        v[u] = coherent_read ? x[a * ld + b] : __ldg(x + a * ld + b);
       }
     }
 #pragma unroll
@@ -309,48 +311,47 @@ __device__ __forceinline__ void load_slots(const Tables &T, const sgb_group &G, 
       if (s0 + u < G.n_slots) sts(Rb + (uint32_t)(s0 + u) * stride8, v[u]);
   }
   for (int k = 0; k < G.n_const; ++k) {
-    const int64_t e = inter ? G.c_off + i * G.n_const + k : G.c_off + (int64_t)k * G.n + i;
+    const int64_t e = (G.flags & FLAG_INTERLEAVED) ? G.c_off + i * G.n_const + k : G.c_off + (int64_t)k * G.n + i;
     sts(Rb + (uint32_t)(G.n_slots + k) * stride8, ld_const(T.con + e, pol));
   }
 }
 
 // One instance, any group (self-referencing groups reload before every root).
 __device__ __forceinline__ void tape_instance(const Tables &T, const sgb_group &G, uint32_t Rb, uint32_t stride8,
-                                              double *x, int64_t ld, int64_t i, int64_t b, uint64_t pol) {
-  const bool inter = G.flags & FLAG_INTERLEAVED;
+                                              double *x, int64_t ld, int64_t i, int64_t b, double *out,
+                                              int64_t ld_out, bool csr, uint64_t pol) {
   const bool selfref = G.flags & FLAG_SELFREF;
   const int phases = selfref ? G.n_roots : 1;
   const int64_t iv[1] = {i};
   const bool ok[1] = {true};
   for (int ph = 0; ph < phases; ++ph) {
-    load_slots(T, G, Rb, stride8, x, ld, i, b, inter, selfref, pol);
-    run_tape<1, 0>(T, G, Rb, x, ld, b, iv, ok, ph, selfref, pol);
+    load_slots(T, G, Rb, stride8, x, ld, i, b, selfref, pol);
+    run_tape<1, 0>(T, G, Rb, x, ld, b, out, ld_out, csr, iv, ok, ph, selfref, pol);
   }
 }
 
-// Single value set: lane = instance, VEC instances per lane (i0 + v*BS) share each
-// decoded tape word.  Scratch file [n_regs][VEC][BS] doubles in shared memory.
+// Single value set: lane = instance, VEC instances per lane (i0 + tid + v*BS)
+// share each decoded tape word.  Scratch file [n_regs][VEC][BS] in shared memory.
 template <int BS, int VEC>
-__global__ void __launch_bounds__(BS) tape_single(Tables T, const int64_t *blk_begin, int g0, int g1,
-                                                  double *x) {
+__global__ void __launch_bounds__(BS) tape_single(Tables T, const int2 *tiles, double *x, double *out, int csr) {
   extern __shared__ double scratch[];
-  const int64_t blk = blockIdx.x;
-  const int g = find_group(blk_begin, g0, g1, blk);
-  const sgb_group G = T.groups[g];
+  const int2 tl = tiles[blockIdx.x];
+  const sgb_group G = T.groups[tl.x];
+  if (!csr && (G.flags & FLAG_CSR_ONLY)) return;
   const uint64_t pol = evict_first_policy();
   const int tid = threadIdx.x;
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(scratch);
   constexpr uint32_t stride8 = BS * VEC * 8;
   if (VEC == 1 && (G.flags & FLAG_SERIAL)) {  // members read other instances' results: instance order
     if (tid != 0) return;
-    for (int64_t i = 0; i < G.n; ++i) tape_instance(T, G, base, stride8, x, 1, i, 0, pol);
+    for (int64_t i = 0; i < G.n; ++i) tape_instance(T, G, base, stride8, x, 1, i, 0, out, 1, csr, pol);
     return;
   }
-  const int64_t i0 = (blk - __ldg(blk_begin + g)) * (BS * VEC) + tid;
+  const int64_t i0 = (int64_t)tl.y + tid;
   if (i0 >= G.n) return;
   const uint32_t Rb = base + tid * 8;
   if (VEC == 1) {
-    tape_instance(T, G, Rb, stride8, x, 1, i0, 0, pol);
+    tape_instance(T, G, Rb, stride8, x, 1, i0, 0, out, 1, csr, pol);
     return;
   }
   int64_t iv[VEC];
@@ -361,21 +362,20 @@ __global__ void __launch_bounds__(BS) tape_single(Tables T, const int64_t *blk_b
     ok[v] = iv[v] < G.n;
     if (!ok[v]) iv[v] = G.n - 1;  // evaluate a valid instance, store nothing
   }
-  const bool inter = G.flags & FLAG_INTERLEAVED;
 #pragma unroll
-  for (int v = 0; v < VEC; ++v) load_slots(T, G, Rb + v * BS * 8, stride8, x, 1, iv[v], 0, inter, false, pol);
-  run_tape<VEC, BS * 8>(T, G, Rb, x, 1, 0, iv, ok, 0, false, pol);
+  for (int v = 0; v < VEC; ++v) load_slots(T, G, Rb + v * BS * 8, stride8, x, 1, iv[v], 0, false, pol);
+  run_tape<VEC, BS * 8>(T, G, Rb, x, 1, 0, out, 1, csr, iv, ok, 0, false, pol);
 }
 
 // Batched: X[addr * ld + b].  A warp owns one instance and sweeps the batch, so
 // index loads are warp-uniform and every gather is a contiguous row.  The block
-// is the unit's scratch stride wide (BS = bs * VEC of the unit), VEC = 1.
-__global__ void tape_batch(Tables T, const int64_t *blk_begin, int g0, int g1, double *X, int64_t ld,
-                           int64_t batch) {
+// is the unit's scratch stride wide, VEC = 1.
+__global__ void tape_batch(Tables T, const int2 *tiles, double *X, int64_t ld, int64_t batch, double *out,
+                           int64_t ld_out, int csr) {
   extern __shared__ double scratch[];
-  const int64_t blk = blockIdx.x;
-  const int g = find_group(blk_begin, g0, g1, blk);
-  const sgb_group G = T.groups[g];
+  const int2 tl = tiles[blockIdx.x];
+  const sgb_group G = T.groups[tl.x];
+  if (!csr && (G.flags & FLAG_CSR_ONLY)) return;
   const uint64_t pol = evict_first_policy();
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t Rb = (uint32_t)__cvta_generic_to_shared(scratch) + tid * 8;
@@ -383,119 +383,190 @@ __global__ void tape_batch(Tables T, const int64_t *blk_begin, int g0, int g1, d
   if (G.flags & FLAG_SERIAL) {
     if (warp != 0) return;
     for (int64_t i = 0; i < G.n; ++i)
-      for (int64_t b = lane; b < batch; b += 32) tape_instance(T, G, Rb, stride8, X, ld, i, b, pol);
+      for (int64_t b = lane; b < batch; b += 32) tape_instance(T, G, Rb, stride8, X, ld, i, b, out, ld_out, csr, pol);
     return;
   }
-  const int64_t i = (blk - __ldg(blk_begin + g)) * (blockDim.x >> 5) + warp;
+  const int64_t i = (int64_t)tl.y + warp;
   if (i >= G.n) return;
-  for (int64_t b = lane; b < batch; b += 32) tape_instance(T, G, Rb, stride8, X, ld, i, b, pol);
+  for (int64_t b = lane; b < batch; b += 32) tape_instance(T, G, Rb, stride8, X, ld, i, b, out, ld_out, csr, pol);
 }
 
 // ---- sum of products: acc = t0 + t1 + ..., t = f0 * f1 * ... (tape-free) --------------
-template <int LMAX>
-__device__ __forceinline__ void sop_addrs(const Tables &T, const sgb_group &G, int64_t i,
-                                          int64_t (&addr)[LMAX], uint64_t pol) {
-  const bool inter = G.flags & FLAG_INTERLEAVED;
-  const uint32_t idx0 = slot0_index(T, G, i, inter, pol);
-#pragma unroll
-  for (int f = 0; f < LMAX; ++f)
-    if (f < G.sop_len) addr[f] = slot_addr(T, G, f, i, inter, idx0, pol);
-}
+// Fold state across factor batches; identical to the left fold of the template.
+struct SopFold {
+  double acc, term;
+  bool have;
+};
 
-template <int LMAX>
-__device__ __forceinline__ double sop_fold(const sgb_group &G, uint32_t newterm, uint32_t negm,
-                                           const double (&v)[LMAX]) {
-  double acc = 0.0, term = 0.0;
-  bool have = false;
+template <int NB>
+__device__ __forceinline__ void sop_fold(SopFold &st, int f0, int len, uint32_t newterm, uint32_t negm,
+                                         const double (&v)[NB]) {
 #pragma unroll
-  for (int f = 0; f < LMAX; ++f) {
-    if (f < G.sop_len) {
-      const double val = ((negm >> f) & 1u) ? -v[f] : v[f];
+  for (int u = 0; u < NB; ++u) {
+    const int f = f0 + u;
+    if (f < len) {
+      const double val = ((negm >> f) & 1u) ? -v[u] : v[u];
       if ((newterm >> f) & 1u) {
         if (f > 0) {
-          acc = have ? __dadd_rn(acc, term) : term;
-          have = true;
+          st.acc = st.have ? __dadd_rn(st.acc, st.term) : st.term;
+          st.have = true;
         }
-        term = val;
+        st.term = val;
       } else {
-        term = __dmul_rn(term, val);
+        st.term = __dmul_rn(st.term, val);
       }
     }
   }
-  return have ? __dadd_rn(acc, term) : term;
 }
 
-// VEC instances per thread (i0 + v*256): VEC x LMAX independent gathers in flight.
+// Address of factor f (slot f) of instance i with slot-0 index idx0.
+__device__ __forceinline__ int64_t sop_addr(const Tables &T, const sgb_group &G, int f, int64_t i, uint32_t idx0,
+                                            const int32_t *s_col, const int64_t *s_del, bool coherent,
+                                            uint64_t pol) {
+  if (coherent) return (int64_t)idx0 + s_del[f];
+  const int col = s_col[f];
+  if (col < 0) return (int64_t)idx0 + s_del[f];
+  if (col == 0) return idx0;
+  return column_index(T, G, col, i, pol);
+}
+
+// VEC instances per thread (i0 + v*SOP_BS), factors in batches of NB: VEC x NB
+// independent gathers in flight.
 template <int LMAX, int VEC>
-__global__ void __launch_bounds__(256) sop_single(Tables T, const int64_t *blk_begin, int g0, int g1,
-                                                  double *x) {
-  const int64_t blk = blockIdx.x;
-  const int g = find_group(blk_begin, g0, g1, blk);
-  const sgb_group G = T.groups[g];
-  const int64_t i0 = (blk - __ldg(blk_begin + g)) * (256 * VEC) + threadIdx.x;
-  if (i0 >= G.n) return;
-  const uint64_t pol = evict_first_policy();
-  const uint32_t newterm = (uint32_t)__ldg(T.sop + G.sop_off);
-  const uint32_t negm = (uint32_t)__ldg(T.sop + G.sop_off + 1);
-  int64_t addr[VEC][LMAX];
+__device__ __forceinline__ void sop_tile(const Tables &T, const sgb_group &G, int64_t i0, double *x, double *out,
+                                         bool csr, const int32_t *s_col, const int64_t *s_del, uint64_t pol) {
+  constexpr int NB = LMAX < SOP_BATCH ? LMAX : SOP_BATCH;
+  const uint32_t newterm = __ldg(T.sop + 2 * G.sop_off), negm = __ldg(T.sop + 2 * G.sop_off + 1);
+  const int len = G.sop_len;
+  const bool coherent = G.flags & FLAG_COHERENT;
+  int64_t iv[VEC];
+  uint32_t idx0[VEC];
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
-    const int64_t i = min(i0 + (int64_t)v * 256, G.n - 1);
-    sop_addrs<LMAX>(T, G, i, addr[v], pol);
+    iv[v] = min(i0 + (int64_t)v * SOP_BS, G.n - 1);
+    idx0[v] = column_index(T, G, 0, iv[v], pol);
   }
-  double val[VEC][LMAX];
+  SopFold st[VEC];
 #pragma unroll
-  for (int v = 0; v < VEC; ++v)
+  for (int v = 0; v < VEC; ++v) st[v] = SopFold{0.0, 0.0, false};
 #pragma unroll
-    for (int f = 0; f < LMAX; ++f)
-      if (f < G.sop_len) val[v][f] = __ldg(x + addr[v][f]);
-  const bool stream = G.flags & FLAG_STREAM;
+  for (int f0 = 0; f0 < LMAX; f0 += NB) {
+    if (f0 < len) {
+      double val[VEC][NB];
+#pragma unroll
+      for (int v = 0; v < VEC; ++v)
+#pragma unroll
+        for (int u = 0; u < NB; ++u)
+          if (f0 + u < len) val[v][u] = __ldg(x + sop_addr(T, G, f0 + u, iv[v], idx0[v], s_col, s_del, coherent, pol));
+#pragma unroll
+      for (int v = 0; v < VEC; ++v) sop_fold<NB>(st[v], f0, len, newterm, negm, val[v]);
+    }
+  }
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
-    const int64_t i = i0 + (int64_t)v * 256;
-    if (i < G.n) st_result(x + G.dest_base + i, sop_fold<LMAX>(G, newterm, negm, val[v]), stream, pol);
+    const int64_t i = i0 + (int64_t)v * SOP_BS;
+    if (i < G.n) {
+      const double r = st[v].have ? __dadd_rn(st[v].acc, st[v].term) : st[v].term;
+      store_root(T, G, 0, i, r, x, 1, 0, out, 1, csr, pol);
+    }
   }
 }
 
+// One launch per wave for every sum-of-products group; the tile's width class
+// picks the unrolled body (block-uniform switch).
+__global__ void __launch_bounds__(SOP_BS, 4) sop_single(Tables T, const int2 *tiles, double *x, double *out,
+                                                       int csr) {
+  __shared__ int32_t s_col[32];
+  __shared__ int64_t s_del[32];
+  const int2 tl = tiles[blockIdx.x];
+  const sgb_group G = T.groups[tl.x];
+  if (!csr && (G.flags & FLAG_CSR_ONLY)) return;
+  if (threadIdx.x < G.n_slots) {
+    s_col[threadIdx.x] = __ldg(T.slot_col + G.slot_off + threadIdx.x);
+    s_del[threadIdx.x] = __ldg(T.slot_delta + G.slot_off + threadIdx.x);
+  }
+  __syncthreads();
+  const uint64_t pol = evict_first_policy();
+  const int64_t i0 = (int64_t)tl.y + threadIdx.x;
+  if (i0 >= G.n) return;
+  switch (G.variant) {
+    case 0: sop_tile<2, sop_vec(0)>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
+    case 1: sop_tile<4, sop_vec(1)>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
+    case 2: sop_tile<8, sop_vec(2)>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
+    case 3: sop_tile<16, sop_vec(3)>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
+    default: sop_tile<32, sop_vec(4)>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
+  }
+}
+
+// Batched: one instance per warp, lanes sweep the batch; index decode is warp-uniform.
 template <int LMAX>
-__global__ void __launch_bounds__(256) sop_batch(Tables T, const int64_t *blk_begin, int g0, int g1,
-                                                 double *X, int64_t ld, int64_t batch) {
-  const int64_t blk = blockIdx.x;
-  const int g = find_group(blk_begin, g0, g1, blk);
-  const sgb_group G = T.groups[g];
+__device__ __forceinline__ void sop_batch_body(const Tables &T, const sgb_group &G, int64_t i, int lane, double *X,
+                                               int64_t ld, int64_t batch, double *out, int64_t ld_out, bool csr,
+                                               const int32_t *s_col, const int64_t *s_del, uint64_t pol) {
+  constexpr int NB = LMAX < 8 ? LMAX : 8;
+  const uint32_t newterm = __ldg(T.sop + 2 * G.sop_off), negm = __ldg(T.sop + 2 * G.sop_off + 1);
+  const bool coherent = G.flags & FLAG_COHERENT;
+  const int len = G.sop_len;
+  const uint32_t idx0 = column_index(T, G, 0, i, pol);
+  uint32_t addr[LMAX];
+#pragma unroll
+  for (int f = 0; f < LMAX; ++f)
+    if (f < len) addr[f] = (uint32_t)sop_addr(T, G, f, i, idx0, s_col, s_del, coherent, pol);
+  for (int64_t b = lane; b < batch; b += 32) {
+    SopFold st{0.0, 0.0, false};
+#pragma unroll
+    for (int f0 = 0; f0 < LMAX; f0 += NB) {
+      if (f0 < len) {
+        double v[NB];
+#pragma unroll
+        for (int u = 0; u < NB; ++u)
+          if (f0 + u < len) v[u] = __ldg(X + (int64_t)addr[f0 + u] * ld + b);
+        sop_fold<NB>(st, f0, len, newterm, negm, v);
+      }
+    }
+    const double r = st.have ? __dadd_rn(st.acc, st.term) : st.term;
+    store_root(T, G, 0, i, r, X, ld, b, out, ld_out, csr, pol);
+  }
+}
+
+__global__ void __launch_bounds__(BATCH_WARPS * 32) sop_batch(Tables T, const int2 *tiles, double *X, int64_t ld,
+                                                             int64_t batch, double *out, int64_t ld_out, int csr) {
+  __shared__ int32_t s_col[32];
+  __shared__ int64_t s_del[32];
+  const int2 tl = tiles[blockIdx.x];
+  const sgb_group G = T.groups[tl.x];
+  if (!csr && (G.flags & FLAG_CSR_ONLY)) return;
+  if (threadIdx.x < G.n_slots) {
+    s_col[threadIdx.x] = __ldg(T.slot_col + G.slot_off + threadIdx.x);
+    s_del[threadIdx.x] = __ldg(T.slot_delta + G.slot_off + threadIdx.x);
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t i = (blk - __ldg(blk_begin + g)) * (blockDim.x >> 5) + warp;
+  const int64_t i = (int64_t)tl.y + warp;
   if (i >= G.n) return;
   const uint64_t pol = evict_first_policy();
-  const uint32_t newterm = (uint32_t)__ldg(T.sop + G.sop_off);
-  const uint32_t negm = (uint32_t)__ldg(T.sop + G.sop_off + 1);
-  int64_t addr[LMAX];
-  sop_addrs<LMAX>(T, G, i, addr, pol);  // warp-uniform: one index fetch per warp
-  const bool stream = G.flags & FLAG_STREAM;
-  for (int64_t b = lane; b < batch; b += 32) {
-    double v[LMAX];
-#pragma unroll
-    for (int f = 0; f < LMAX; ++f)
-      if (f < G.sop_len) v[f] = __ldg(X + addr[f] * ld + b);
-    st_result(X + (G.dest_base + i) * ld + b, sop_fold<LMAX>(G, newterm, negm, v), stream, pol);
+  switch (G.variant) {
+    case 0: sop_batch_body<2>(T, G, i, lane, X, ld, batch, out, ld_out, csr, s_col, s_del, pol); break;
+    case 1: sop_batch_body<4>(T, G, i, lane, X, ld, batch, out, ld_out, csr, s_col, s_del, pol); break;
+    case 2: sop_batch_body<8>(T, G, i, lane, X, ld, batch, out, ld_out, csr, s_col, s_del, pol); break;
+    case 3: sop_batch_body<16>(T, G, i, lane, X, ld, batch, out, ld_out, csr, s_col, s_del, pol); break;
+    default: sop_batch_body<32>(T, G, i, lane, X, ld, batch, out, ld_out, csr, s_col, s_del, pol); break;
   }
 }
 
-__global__ void gather_outputs(const double *__restrict__ x, const int64_t *__restrict__ outs,
-                               int64_t n, double *__restrict__ out) {
+__global__ void gather_outputs(const double *__restrict__ x, const int64_t *__restrict__ outs, int64_t n,
+                               double *__restrict__ out) {
   const uint64_t pol = evict_first_policy();
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     int64_t a;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s64 %0, [%1], %2;"
-                 : "=l"(a) : "l"(outs + k), "l"(pol));
-    st_result(out + k, __ldg(x + a), true, pol);
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(a) : "l"(outs + k), "l"(pol));
+    st_stream(out + k, __ldg(x + a), pol);
   }
 }
 
 __global__ void gather_outputs_batch(const double *__restrict__ X, int64_t ld, int64_t batch,
-                                     const int64_t *__restrict__ outs, int64_t n,
-                                     double *__restrict__ out, int64_t ld_out) {
+                                     const int64_t *__restrict__ outs, int64_t n, double *__restrict__ out,
+                                     int64_t ld_out) {
   const int64_t k = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (k >= n) return;
   const int64_t src = __ldg(outs + k) * ld;
@@ -512,10 +583,9 @@ int upload(T **dst, const T *src, int64_t n) {
 }
 
 struct Unit {
-  int wave, kind, variant, g0, g1, bs, regs;
-  int64_t blocks;
-  int bwarps;       // batched mode: instances (warps) per block
-  int64_t bblocks;  // batched mode: blocks
+  int wave, kind, variant, g0, g1, bs, regs, flags;
+  int64_t t0, t1;    // single-set tiles [t0, t1)
+  int64_t bt0, bt1;  // batched tiles
 };
 
 }  // namespace
@@ -523,17 +593,20 @@ struct Unit {
 struct sgb_plan {
   int device = 0;
   int64_t vas = 0, n_in = 0, n_out = 0, n_pos = 0, n_con = 0;
-  int n_groups = 0, n_waves = 0;
+  int n_groups = 0, n_waves = 0, csr_waves = 0, needs_zero = 2;
+  bool ws_dirty = false;  // the workspace holds sg_run results (slots CSR mode never writes)
   std::vector<Unit> units;
   Tables T{};
   sgb_group *d_groups = nullptr;
-  int64_t *d_blk = nullptr, *d_bblk = nullptr, *d_outputs = nullptr;
+  int2 *d_tiles = nullptr, *d_btiles = nullptr;
+  int64_t *d_outputs = nullptr;
   uint32_t *d_tape = nullptr;
   double *d_imm = nullptr, *d_con = nullptr;
-  int32_t *d_sop = nullptr, *d_scol = nullptr;
+  uint32_t *d_sop = nullptr;
+  int32_t *d_scol = nullptr;
   int64_t *d_sdel = nullptr;
-  uint32_t *d_pos = nullptr, *d_cbase = nullptr;
-  uint16_t *d_coff = nullptr;
+  uint32_t *d_pos = nullptr, *d_cbase = nullptr, *d_obase = nullptr, *d_opos32 = nullptr;
+  uint16_t *d_coff = nullptr, *d_ooff = nullptr;
   // workspace for the host-buffer entry points
   std::mutex ws_mu;
   double *d_x = nullptr, *d_out = nullptr;
@@ -543,49 +616,40 @@ struct sgb_plan {
 namespace {
 
 template <int BS, int VEC>
-void launch_tape(const sgb_plan *p, const Unit &u, double *x, cudaStream_t s) {
+void launch_tape(const sgb_plan *p, const Unit &u, double *x, double *out, bool csr, cudaStream_t s) {
   const size_t smem = (size_t)u.regs * BS * VEC * sizeof(double);
-  tape_single<BS, VEC><<<(unsigned)u.blocks, BS, smem, s>>>(p->T, p->d_blk, u.g0, u.g1, x);
+  tape_single<BS, VEC><<<(unsigned)(u.t1 - u.t0), BS, smem, s>>>(p->T, p->d_tiles + u.t0, x, out, csr);
 }
 
 template <int BS>
-void launch_tape_vec(const sgb_plan *p, const Unit &u, double *x, cudaStream_t s) {
-  if (u.variant <= 1) launch_tape<BS, 1>(p, u, x, s);
-  else if (u.variant == 2) launch_tape<BS, 2>(p, u, x, s);
-  else launch_tape<BS, 4>(p, u, x, s);
+void launch_tape_vec(const sgb_plan *p, const Unit &u, double *x, double *out, bool csr, cudaStream_t s) {
+  if (u.variant <= 1) launch_tape<BS, 1>(p, u, x, out, csr, s);
+  else if (u.variant == 2) launch_tape<BS, 2>(p, u, x, out, csr, s);
+  else launch_tape<BS, 4>(p, u, x, out, csr, s);
 }
 
-template <int LMAX>
-void launch_sop(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_t batch, bool batched,
-                cudaStream_t s) {
-  if (!batched)
-    sop_single<LMAX, (LMAX <= 8 ? 2 : 1)><<<(unsigned)u.blocks, 256, 0, s>>>(p->T, p->d_blk, u.g0, u.g1, x);
-  else
-    sop_batch<LMAX><<<(unsigned)u.bblocks, 256, 0, s>>>(p->T, p->d_bblk, u.g0, u.g1, x, ld, batch);
-}
-
-void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_t batch, bool batched,
-                 cudaStream_t s) {
-  if ((batched ? u.bblocks : u.blocks) == 0) return;
+void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_t batch, bool batched, double *out,
+                 int64_t ld_out, bool csr, cudaStream_t s) {
+  if ((u.flags & UNIT_CSR_ONLY) && !csr) return;
+  const int64_t blocks = batched ? u.bt1 - u.bt0 : u.t1 - u.t0;
+  if (blocks <= 0) return;
   if (u.kind == KIND_TAPE) {
     if (batched) {  // block = the unit's scratch stride, one instance per warp
       const int stride = u.bs * u.variant;
       const size_t smem = (size_t)u.regs * stride * sizeof(double);
-      tape_batch<<<(unsigned)u.bblocks, stride, smem, s>>>(p->T, p->d_bblk, u.g0, u.g1, x, ld, batch);
+      tape_batch<<<(unsigned)blocks, stride, smem, s>>>(p->T, p->d_btiles + u.bt0, x, ld, batch, out, ld_out, csr);
       return;
     }
     switch (u.bs) {
-      case 128: launch_tape_vec<128>(p, u, x, s); break;
-      case 64: launch_tape_vec<64>(p, u, x, s); break;
-      default: launch_tape_vec<32>(p, u, x, s); break;
+      case 128: launch_tape_vec<128>(p, u, x, out, csr, s); break;
+      case 64: launch_tape_vec<64>(p, u, x, out, csr, s); break;
+      default: launch_tape_vec<32>(p, u, x, out, csr, s); break;
     }
+  } else if (batched) {
+    sop_batch<<<(unsigned)blocks, BATCH_WARPS * 32, 0, s>>>(p->T, p->d_btiles + u.bt0, x, ld, batch, out, ld_out,
+                                                            csr);
   } else {
-    switch (u.variant) {
-      case 4: launch_sop<4>(p, u, x, ld, batch, batched, s); break;
-      case 8: launch_sop<8>(p, u, x, ld, batch, batched, s); break;
-      case 16: launch_sop<16>(p, u, x, ld, batch, batched, s); break;
-      default: launch_sop<32>(p, u, x, ld, batch, batched, s); break;
-    }
+    sop_single<<<(unsigned)blocks, SOP_BS, 0, s>>>(p->T, p->d_tiles + u.t0, x, out, csr);
   }
 }
 
@@ -602,21 +666,40 @@ cudaError_t allow_smem(int smem_max) {
   return allow_smem_single<BS, 4>(smem_max);
 }
 
+// per-entry validation of a compressed table: base[c][i/32] + off[c][i] < limit (off == skip allowed)
+bool w16_ok(const uint32_t *base, const uint16_t *off, int64_t n, int cols, int c0, int64_t limit, bool allow_skip) {
+  const int64_t nch = (n + 31) / 32;
+  for (int c = c0; c < cols; ++c)
+    for (int64_t i = 0; i < n; ++i) {
+      const uint16_t o = off[c * n + i];
+      if (allow_skip && o == 0xFFFFu) continue;
+      if ((int64_t)base[c * nch + i / 32] + o >= limit) return false;
+    }
+  return true;
+}
+
 }  // namespace
 
 extern "C" {
 
 const char *sgb_last_error(void) { return g_err.c_str(); }
 
-int sgb_plan_launches(const sgb_plan *p) { return p ? p->n_waves : 0; }
+int sgb_plan_waves(const sgb_plan *p, int csr) { return p ? (csr ? p->csr_waves : p->n_waves) : 0; }
 
-int sgb_plan_units(const sgb_plan *p) { return p ? (int)p->units.size() : 0; }
+int sgb_plan_units(const sgb_plan *p, int csr) {
+  if (!p) return 0;
+  int k = 0;
+  for (const Unit &u : p->units)
+    if (csr || !(u.flags & UNIT_CSR_ONLY)) ++k;
+  return k;
+}
 
 void sgb_plan_destroy(sgb_plan *p) {
   if (!p) return;
   cudaSetDevice(p->device);
-  void *bufs[] = {p->d_groups, p->d_blk, p->d_bblk, p->d_outputs, p->d_tape, p->d_imm, p->d_con,
-                  p->d_sop, p->d_scol, p->d_sdel, p->d_pos, p->d_x, p->d_out, p->d_cbase, p->d_coff};
+  void *bufs[] = {p->d_groups, p->d_tiles, p->d_btiles, p->d_outputs, p->d_tape, p->d_imm, p->d_con,
+                  p->d_sop, p->d_scol, p->d_sdel, p->d_pos, p->d_x, p->d_out, p->d_cbase, p->d_coff,
+                  p->d_obase, p->d_ooff, p->d_opos32};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (p->ws_stream) cudaStreamDestroy(p->ws_stream);
@@ -631,7 +714,9 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
   cudaDeviceProp prop;
   SGB_CUDA(cudaGetDeviceProperties(&prop, device));
   if (prop.major != 10) return fail(-2, "sgb_plan_create: libsgb is built for sm_100a (B200) only");
-  if (d->n_waves < 0 || d->n_groups < 0 || d->n_units < 0) return fail(-1, "sgb_plan_create: negative counts");
+  if (d->n_waves < 0 || d->n_groups < 0 || d->n_units < 0 || d->n_tiles < 0)
+    return fail(-1, "sgb_plan_create: negative counts");
+  if (d->value_array_size >= (int64_t)1 << 32) return fail(-1, "sgb_plan_create: value array exceeds u32 addressing");
   p->device = device;
   p->vas = d->value_array_size;
   p->n_in = d->input_count;
@@ -640,19 +725,30 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
   p->n_con = d->n_constants;
   p->n_groups = d->n_groups;
   p->n_waves = d->n_waves;
+  if (d->needs_zero < 0 || d->needs_zero > 2) return fail(-1, "sgb_plan_create: needs_zero must be 0, 1 or 2");
+  p->needs_zero = d->needs_zero;
   // host-side validation of every table entry the kernels trust
   for (int g = 0; g < d->n_groups; ++g) {
     const sgb_group &G = d->groups[g];
+    const int64_t nch = (G.n + 31) / 32;
     const bool bad =
-        G.n < 0 || G.dest_base < d->input_count || G.dest_base + G.n_roots * G.n > d->value_array_size ||
+        G.n < 0 ||
+        ((G.flags & FLAG_CSR_ONLY) ? !(G.flags & FLAG_STREAM)  // copy groups never store to the value array
+                                   : (G.dest_base < d->input_count || G.dest_base + G.n_roots * G.n > d->value_array_size)) ||
         G.p_off < 0 || G.p_off + (int64_t)G.n_ret * G.n > d->n_positions || G.c_off < 0 ||
         G.c_off + (int64_t)G.n_const * G.n > d->n_constants || G.tape_off < 0 ||
         G.tape_off + G.tape_len > d->tape_rows || G.slot_off < 0 || G.slot_off + G.n_slots > d->n_slot ||
         (G.n_slots > 0 && G.n_ret < 1) ||
-        (G.kind == KIND_SOP && (G.sop_len > 32 || G.sop_len != G.n_slots || G.sop_off + 2 > d->n_sop)) ||
-        ((G.flags & FLAG_W16) && (G.cb_off < 0 || G.co_off < 0 ||
-                                  G.cb_off + (int64_t)G.n_ret * ((G.n + 31) / 32) > d->n_cbase ||
-                                  G.co_off + (int64_t)G.n_ret * G.n > d->n_coff));
+        (G.kind == KIND_SOP && (G.sop_len < 1 || G.sop_len > 32 || G.sop_len != G.n_slots ||
+                                2 * (int64_t)G.sop_off + 2 > d->n_sop || G.variant < 0 || G.variant > 4 ||
+                                G.sop_len > sop_lmax(G.variant) || G.n_roots != 1)) ||
+        ((G.flags & FLAG_W16) && (G.cb_off < 0 || G.co_off < 0 || G.cb_off + (int64_t)G.n_ret * nch > d->n_cbase ||
+                                  G.co_off + (int64_t)G.n_ret * G.n > d->n_coff)) ||
+        ((G.flags & FLAG_OPOS16) && (G.ob_off < 0 || G.oo_off < 0 ||
+                                     G.ob_off + (int64_t)G.n_roots * nch > d->n_obase ||
+                                     G.oo_off + (int64_t)G.n_roots * G.n > d->n_ooff)) ||
+        ((G.flags & FLAG_OPOS32) && (G.oo_off < 0 || G.oo_off + (int64_t)G.n_roots * G.n > d->n_opos32)) ||
+        ((G.flags & FLAG_COHERENT) && G.n_ret != 1);
     if (bad) return fail(-1, "sgb_plan_create: group " + std::to_string(g) + " is out of range");
     for (int s = 0; s < G.n_slots; ++s)
       if (d->slot_col[G.slot_off + s] >= G.n_ret) return fail(-1, "sgb_plan_create: bad slot column");
@@ -660,19 +756,54 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
   for (int64_t k = 0; k < d->n_positions; ++k)
     if ((int64_t)d->positions[k] >= d->value_array_size)
       return fail(-1, "sgb_plan_create: position index outside the value array");
-  for (int g = 0; g < d->n_groups; ++g) {  // compressed columns decode inside the value array
+  for (int g = 0; g < d->n_groups; ++g) {  // compressed / affine / coherent decodes stay inside the value array
     const sgb_group &G = d->groups[g];
-    if ((G.flags & FLAG_AFFINE0) && G.n > 0) {
+    if (G.n == 0) continue;
+    if (G.flags & FLAG_AFFINE0) {
       const int64_t first = G.a0_base, last = G.a0_base + G.a0_stride * (G.n - 1);
       if (first < 0 || last < 0 || first >= d->value_array_size || last >= d->value_array_size)
         return fail(-1, "sgb_plan_create: affine index column outside the value array");
     }
-    if (!(G.flags & FLAG_W16)) continue;
-    const int64_t nch = (G.n + 31) / 32;
-    for (int c = (G.flags & FLAG_AFFINE0) ? 1 : 0; c < G.n_ret; ++c)
-      for (int64_t i = 0; i < G.n; ++i)
-        if ((int64_t)d->cbase[G.cb_off + c * nch + i / 32] + d->coff[G.co_off + c * G.n + i] >= d->value_array_size)
-          return fail(-1, "sgb_plan_create: compressed index outside the value array");
+    if ((G.flags & FLAG_W16) &&
+        !w16_ok(d->cbase + G.cb_off, d->coff + G.co_off, G.n, G.n_ret, (G.flags & FLAG_AFFINE0) ? 1 : 0,
+                d->value_array_size, false))
+      return fail(-1, "sgb_plan_create: compressed index outside the value array");
+    if ((G.flags & FLAG_OPOS16) &&
+        !w16_ok(d->obase + G.ob_off, d->ooff + G.oo_off, G.n, G.n_roots, 0, d->n_outputs, true))
+      return fail(-1, "sgb_plan_create: output position outside the output array");
+    if (G.flags & FLAG_OPOS32)
+      for (int64_t e = 0; e < (int64_t)G.n_roots * G.n; ++e) {
+        const uint32_t o = d->opos32[G.oo_off + e];
+        if (o != NONE && (int64_t)o >= d->n_outputs) return fail(-1, "sgb_plan_create: output position out of range");
+      }
+    // slot-0 relative decodes (coherent slots): the extremes of column 0 plus each delta
+    int64_t lo = INT64_MAX, hi = INT64_MIN;
+    for (int s = 0; s < G.n_slots; ++s) {
+      if (d->slot_col[G.slot_off + s] >= 0) continue;
+      lo = lo < d->slot_delta[G.slot_off + s] ? lo : d->slot_delta[G.slot_off + s];
+      hi = hi > d->slot_delta[G.slot_off + s] ? hi : d->slot_delta[G.slot_off + s];
+    }
+    if (lo <= hi) {  // every instance's slot-0 index + delta must be a valid address
+      int64_t mn = INT64_MAX, mx = INT64_MIN;
+      if (G.flags & FLAG_AFFINE0) {
+        const int64_t a = G.a0_base, b = G.a0_base + G.a0_stride * (G.n - 1);
+        mn = a < b ? a : b;
+        mx = a > b ? a : b;
+      } else {
+        const int64_t nch = (G.n + 31) / 32;
+        for (int64_t i = 0; i < G.n; ++i) {
+          int64_t v;
+          if (G.flags & FLAG_W16) v = (int64_t)d->cbase[G.cb_off + i / 32] + d->coff[G.co_off + i];
+          else if (G.flags & FLAG_INTERLEAVED) v = d->positions[G.p_off + i * G.n_ret];
+          else v = d->positions[G.p_off + i];
+          mn = v < mn ? v : mn;
+          mx = v > mx ? v : mx;
+          (void)nch;
+        }
+      }
+      if (mn + lo < 0 || mx + hi >= d->value_array_size)
+        return fail(-1, "sgb_plan_create: coherent slot decodes outside the value array");
+    }
   }
   for (int64_t k = 0; k < d->n_outputs; ++k)
     if (d->outputs[k] < 0 || d->outputs[k] >= d->value_array_size)
@@ -683,7 +814,8 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
   SGB_CUDA(allow_smem<64>(smem_max));
   SGB_CUDA(allow_smem<128>(smem_max));
   SGB_CUDA(cudaFuncSetAttribute(tape_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
-  std::vector<int64_t> blk(d->n_groups, 0), bblk(d->n_groups, 0);
+  std::vector<int2> btiles;
+  int max_wave = -1;
   for (int k = 0; k < d->n_units; ++k) {
     const int64_t *r = d->units + (int64_t)k * U_COUNT;
     Unit u;
@@ -692,30 +824,50 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
     u.variant = (int)r[U_VARIANT];
     u.g0 = (int)r[U_G0];
     u.g1 = (int)r[U_G1];
-    u.blocks = r[U_BLOCKS];
+    u.t0 = r[U_T0];
+    u.t1 = r[U_T1];
     u.bs = (int)r[U_BS];
     u.regs = (int)r[U_REGS];
-    if (u.g0 < 0 || u.g1 > d->n_groups || u.g0 > u.g1 || u.wave < 0 || u.wave >= d->n_waves ||
+    u.flags = (int)r[U_FLAGS];
+    const bool csr_only = u.flags & UNIT_CSR_ONLY;
+    if (u.g0 < 0 || u.g1 > d->n_groups || u.g0 > u.g1 || u.wave < 0 ||
+        (csr_only ? u.wave != d->n_waves : u.wave >= d->n_waves) || u.t0 < 0 || u.t1 > d->n_tiles ||
+        u.t0 > u.t1 || (u.kind != KIND_TAPE && u.kind != KIND_SOP) ||
         (u.kind == KIND_TAPE && (u.bs != 32 && u.bs != 64 && u.bs != 128)) ||
         (u.kind == KIND_TAPE && (u.variant != 1 && u.variant != 2 && u.variant != 4)) ||
         (int64_t)u.regs * (u.kind == KIND_TAPE ? u.bs * u.variant : 0) * 8 > smem_max)
       return fail(-1, "sgb_plan_create: bad launch unit " + std::to_string(k));
-    // batched: one instance per warp; tape blocks are the unit's scratch stride wide
-    u.bwarps = u.kind == KIND_TAPE ? (u.bs * u.variant) / 32 : MAX_BATCH_WARPS;
-    int64_t acc = 0;
-    for (int g = u.g0; g < u.g1; ++g) {
-      blk[g] = d->groups[g].blk_begin;
-      bblk[g] = acc;
-      acc += (d->groups[g].flags & FLAG_SERIAL) ? 1 : (d->groups[g].n + u.bwarps - 1) / u.bwarps;
+    max_wave = u.wave > max_wave ? u.wave : max_wave;
+    for (int64_t t = u.t0; t < u.t1; ++t) {  // tiles name groups of this unit and start inside them
+      const int32_t *tl = d->tiles + 2 * t;
+      if (tl[0] < u.g0 || tl[0] >= u.g1 || tl[1] < 0 || (int64_t)tl[1] >= d->groups[tl[0]].n)
+        return fail(-1, "sgb_plan_create: bad tile in unit " + std::to_string(k));
     }
-    u.bblocks = acc;
+    for (int g = u.g0; g < u.g1; ++g) {
+      const sgb_group &G = d->groups[g];
+      if (G.kind != u.kind) return fail(-1, "sgb_plan_create: group kind differs from its unit");
+      if (u.kind == KIND_TAPE && (G.flags & FLAG_SERIAL) && u.variant != 1)
+        return fail(-1, "sgb_plan_create: serial group in a vectorised tape unit");
+    }
+    // batched tiles: one instance per warp (tape blocks are the unit's scratch stride wide)
+    const int bwarps = u.kind == KIND_TAPE ? (u.bs * u.variant) / 32 : BATCH_WARPS;
+    u.bt0 = (int64_t)btiles.size();
+    for (int g = u.g0; g < u.g1; ++g) {
+      const sgb_group &G = d->groups[g];
+      if (G.flags & FLAG_SERIAL) {
+        if (G.n > 0) btiles.push_back(make_int2(g, 0));
+        continue;
+      }
+      for (int64_t i = 0; i < G.n; i += bwarps) btiles.push_back(make_int2(g, (int)i));
+    }
+    u.bt1 = (int64_t)btiles.size();
     if (u.kind == KIND_TAPE) {  // every tape word must stay inside its lane's scratch column
       const uint64_t limit = (uint64_t)u.regs * u.bs * u.variant * 8;
       for (int g = u.g0; g < u.g1; ++g) {
         const sgb_group &G = d->groups[g];
         if (G.n_slots + G.n_const > u.regs) return fail(-1, "sgb_plan_create: slots exceed the scratch file");
-        for (int64_t k = G.tape_off; k < G.tape_off + G.tape_len; ++k) {
-          const uint32_t *w = d->tape + 4 * k;
+        for (int64_t k2 = G.tape_off; k2 < G.tape_off + G.tape_len; ++k2) {
+          const uint32_t *w = d->tape + 4 * k2;
           const uint32_t op = w[0] & 63u;
           const uint64_t c8 = (uint64_t)(w[0] >> 8) << 3;
           bool bad = op > T_RMSUB || w[2] >= limit || c8 >= limit;
@@ -730,20 +882,23 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
     }
     p->units.push_back(u);
   }
+  p->csr_waves = max_wave + 1 > p->n_waves ? max_wave + 1 : p->n_waves;
   int rc = 0;
   if ((rc = upload(&p->d_groups, d->groups, d->n_groups)) ||
-      (rc = upload(&p->d_blk, blk.data(), (int64_t)blk.size())) ||
-      (rc = upload(&p->d_bblk, bblk.data(), (int64_t)bblk.size())) ||
+      (rc = upload(&p->d_tiles, reinterpret_cast<const int2 *>(d->tiles), d->n_tiles)) ||
+      (rc = upload(&p->d_btiles, btiles.data(), (int64_t)btiles.size())) ||
       (rc = upload(&p->d_outputs, d->outputs, d->n_outputs)) ||
       (rc = upload(&p->d_tape, d->tape, d->tape_rows * 4)) || (rc = upload(&p->d_imm, d->imm, d->n_imm)) ||
       (rc = upload(&p->d_sop, d->sop, d->n_sop)) || (rc = upload(&p->d_scol, d->slot_col, d->n_slot)) ||
       (rc = upload(&p->d_sdel, d->slot_delta, d->n_slot)) ||
       (rc = upload(&p->d_pos, d->positions, d->n_positions)) ||
       (rc = upload(&p->d_con, d->constants, d->n_constants)) ||
-      (rc = upload(&p->d_cbase, d->cbase, d->n_cbase)) || (rc = upload(&p->d_coff, d->coff, d->n_coff)))
+      (rc = upload(&p->d_cbase, d->cbase, d->n_cbase)) || (rc = upload(&p->d_coff, d->coff, d->n_coff)) ||
+      (rc = upload(&p->d_obase, d->obase, d->n_obase)) || (rc = upload(&p->d_ooff, d->ooff, d->n_ooff)) ||
+      (rc = upload(&p->d_opos32, d->opos32, d->n_opos32)))
     return rc;
-  p->T = Tables{p->d_groups, p->d_tape, p->d_imm, p->d_sop, p->d_scol, p->d_sdel,
-                p->d_pos, p->d_con, p->d_cbase, p->d_coff};
+  p->T = Tables{p->d_groups, p->d_tape, p->d_imm, p->d_sop, p->d_scol, p->d_sdel, p->d_pos,
+                p->d_con, p->d_cbase, p->d_coff, p->d_obase, p->d_ooff, p->d_opos32};
   return 0;
 }
 
@@ -761,18 +916,28 @@ int sgb_plan_create(const sgb_plan_desc *d, int device, sgb_plan **out) {
   return 0;
 }
 
-int sgb_run_wave(sgb_plan *p, double *x, int wave, void *stream) {
+int sgb_run_wave(sgb_plan *p, double *x, double *out, int wave, void *stream) {
   if (!p || (!x && p->vas)) return fail(-1, "sgb_run_wave: null argument");
-  if (wave < 0 || wave >= p->n_waves) return fail(-1, "sgb_run_wave: wave out of range");
+  const bool csr = out != nullptr;
+  if (wave < 0 || wave >= (csr ? p->csr_waves : p->n_waves)) return fail(-1, "sgb_run_wave: wave out of range");
+  if (csr && p->n_out == 0) return 0;
   for (const Unit &u : p->units)
-    if (u.wave == wave) launch_unit(p, u, x, 1, 1, false, (cudaStream_t)stream);
+    if (u.wave == wave) launch_unit(p, u, x, 1, 1, false, out, 1, csr, (cudaStream_t)stream);
   SGB_CUDA(cudaGetLastError());
   return 0;
 }
 
 int sgb_run_values(sgb_plan *p, double *x, void *stream) {
   if (!p || (!x && p->vas)) return fail(-1, "sgb_run_values: null argument");
-  for (const Unit &u : p->units) launch_unit(p, u, x, 1, 1, false, (cudaStream_t)stream);
+  for (const Unit &u : p->units) launch_unit(p, u, x, 1, 1, false, nullptr, 1, false, (cudaStream_t)stream);
+  SGB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int sgb_run_csr(sgb_plan *p, double *x, double *out, void *stream) {
+  if (!p || (!x && p->vas) || (!out && p->n_out)) return fail(-1, "sgb_run_csr: null argument");
+  if (!p->n_out) return 0;
+  for (const Unit &u : p->units) launch_unit(p, u, x, 1, 1, false, out, 1, true, (cudaStream_t)stream);
   SGB_CUDA(cudaGetLastError());
   return 0;
 }
@@ -780,7 +945,17 @@ int sgb_run_values(sgb_plan *p, double *x, void *stream) {
 int sgb_run_batch(sgb_plan *p, double *X, int64_t ld, int64_t batch, void *stream) {
   if (!p || (!X && p->vas)) return fail(-1, "sgb_run_batch: null argument");
   if (batch < 1 || ld < batch) return fail(-1, "sgb_run_batch: need 1 <= batch <= ld");
-  for (const Unit &u : p->units) launch_unit(p, u, X, ld, batch, true, (cudaStream_t)stream);
+  for (const Unit &u : p->units) launch_unit(p, u, X, ld, batch, true, nullptr, 1, false, (cudaStream_t)stream);
+  SGB_CUDA(cudaGetLastError());
+  return 0;
+}
+
+int sgb_run_batch_csr(sgb_plan *p, double *X, int64_t ld, int64_t batch, double *out, int64_t ld_out,
+                      void *stream) {
+  if (!p || (!X && p->vas) || (!out && p->n_out)) return fail(-1, "sgb_run_batch_csr: null argument");
+  if (batch < 1 || ld < batch || ld_out < batch) return fail(-1, "sgb_run_batch_csr: need 1 <= batch <= ld, ld_out");
+  if (!p->n_out) return 0;
+  for (const Unit &u : p->units) launch_unit(p, u, X, ld, batch, true, out, ld_out, true, (cudaStream_t)stream);
   SGB_CUDA(cudaGetLastError());
   return 0;
 }
@@ -797,15 +972,15 @@ int sgb_gather_outputs(sgb_plan *p, const double *x, double *out, void *stream) 
   return 0;
 }
 
-int sgb_gather_outputs_batch(sgb_plan *p, const double *X, int64_t ld, int64_t batch, double *out,
-                             int64_t ld_out, void *stream) {
+int sgb_gather_outputs_batch(sgb_plan *p, const double *X, int64_t ld, int64_t batch, double *out, int64_t ld_out,
+                             void *stream) {
   if (!p) return fail(-1, "sgb_gather_outputs_batch: null plan");
   if (!p->n_out) return 0;
   if (!X || !out || batch < 1 || ld < batch || ld_out < batch)
     return fail(-1, "sgb_gather_outputs_batch: bad arguments");
   const int64_t blocks = (p->n_out + 7) / 8;
-  gather_outputs_batch<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(X, ld, batch, p->d_outputs,
-                                                                          p->n_out, out, ld_out);
+  gather_outputs_batch<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(X, ld, batch, p->d_outputs, p->n_out,
+                                                                          out, ld_out);
   SGB_CUDA(cudaGetLastError());
   return 0;
 }
@@ -813,7 +988,11 @@ int sgb_gather_outputs_batch(sgb_plan *p, const double *X, int64_t ld, int64_t b
 static int ensure_ws(sgb_plan *p) {
   SGB_CUDA(cudaSetDevice(p->device));
   if (!p->ws_stream) SGB_CUDA(cudaStreamCreateWithFlags(&p->ws_stream, cudaStreamNonBlocking));
-  if (!p->d_x && p->vas) SGB_CUDA(cudaMalloc((void **)&p->d_x, sizeof(double) * (size_t)p->vas));
+  if (!p->d_x && p->vas) {
+    SGB_CUDA(cudaMalloc((void **)&p->d_x, sizeof(double) * (size_t)p->vas));
+    // never-written slots (padding, reads before writes) read as zero (codegen.py:419)
+    SGB_CUDA(cudaMemset(p->d_x, 0, sizeof(double) * (size_t)p->vas));
+  }
   if (!p->d_out && p->n_out) SGB_CUDA(cudaMalloc((void **)&p->d_out, sizeof(double) * (size_t)p->n_out));
   return 0;
 }
@@ -827,6 +1006,7 @@ int sgb_sg_run(sgb_plan *p, double *x_host, const double *c_host, const unsigned
   if (rc) return rc;
   if (!p->vas) return 0;
   SGB_CUDA(cudaMemcpyAsync(p->d_x, x_host, sizeof(double) * (size_t)p->vas, cudaMemcpyHostToDevice, p->ws_stream));
+  p->ws_dirty = true;
   if ((rc = sgb_run_values(p, p->d_x, p->ws_stream))) return rc;
   SGB_CUDA(cudaMemcpyAsync(x_host, p->d_x, sizeof(double) * (size_t)p->vas, cudaMemcpyDeviceToHost, p->ws_stream));
   SGB_CUDA(cudaStreamSynchronize(p->ws_stream));
@@ -838,17 +1018,16 @@ int sgb_run_outputs_host(sgb_plan *p, const double *inputs, double *outputs) {
   std::lock_guard<std::mutex> lk(p->ws_mu);
   int rc = ensure_ws(p);
   if (rc) return rc;
-  if (p->vas) {
-    // padding and not-yet-written ranges read as zero (codegen.py:419)
+  if (!p->n_out) return 0;
+  // zero-reads (padding, read-before-write) must see zeros: re-zero when a previous
+  // evaluation may have written them (every time for read-before-write plans)
+  if ((p->needs_zero == 2 || (p->needs_zero == 1 && p->ws_dirty)) && p->vas > p->n_in)
     SGB_CUDA(cudaMemsetAsync(p->d_x + p->n_in, 0, sizeof(double) * (size_t)(p->vas - p->n_in), p->ws_stream));
-    if (p->n_in)
-      SGB_CUDA(cudaMemcpyAsync(p->d_x, inputs, sizeof(double) * (size_t)p->n_in, cudaMemcpyHostToDevice, p->ws_stream));
-    if ((rc = sgb_run_values(p, p->d_x, p->ws_stream))) return rc;
-  }
-  if (p->n_out) {
-    if ((rc = sgb_gather_outputs(p, p->d_x, p->d_out, p->ws_stream))) return rc;
-    SGB_CUDA(cudaMemcpyAsync(outputs, p->d_out, sizeof(double) * (size_t)p->n_out, cudaMemcpyDeviceToHost, p->ws_stream));
-  }
+  p->ws_dirty = false;
+  if (p->n_in)
+    SGB_CUDA(cudaMemcpyAsync(p->d_x, inputs, sizeof(double) * (size_t)p->n_in, cudaMemcpyHostToDevice, p->ws_stream));
+  if ((rc = sgb_run_csr(p, p->d_x, p->d_out, p->ws_stream))) return rc;
+  SGB_CUDA(cudaMemcpyAsync(outputs, p->d_out, sizeof(double) * (size_t)p->n_out, cudaMemcpyDeviceToHost, p->ws_stream));
   SGB_CUDA(cudaStreamSynchronize(p->ws_stream));
   return 0;
 }

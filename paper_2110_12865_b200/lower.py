@@ -44,23 +44,32 @@ T_IMM, T_ST = 20, 21
 KIND_TAPE, KIND_SOP = 0, 1
 FLAG_SELFREF, FLAG_INTERLEAVED, FLAG_SERIAL, FLAG_EXACT, FLAG_STREAM, FLAG_W16 = 1, 2, 4, 8, 16, 32
 FLAG_AFFINE0 = 64  # index column 0 is a0_base + a0_stride * i: no table read
+FLAG_OPOS16 = 128  # output positions: u32 base per 32 instances + u16 offset (0xFFFF = not an output)
+FLAG_OPOS32 = 256  # output positions: u32 per instance (0xFFFFFFFF = not an output)
+FLAG_CSR_ONLY = 512  # synthetic copy group: runs in CSR mode only
+FLAG_COHERENT = 1024  # one retained column: every slot is column 0 + delta
+UNIT_CSR_ONLY = 1
 CHUNK = 32  # instances per compressed-index chunk (one warp in single-set mode)
+NONE32 = 0xFFFFFFFF
 SOP_NEWTERM, SOP_NEG = 1, 2
-SOP_MAX = 32  # factors per sum-of-products template (csrc SOP_MAX)
+SOP_MAX = 32  # factors per sum-of-products template (csrc SOP classes)
+SOP_CLASSES = (2, 4, 8, 16, 32)  # width classes of the sum-of-products kernel (csrc sop_lmax)
 
 # one record per group, mirrored by struct sgb_group in include/sgb.h
 GROUP_DTYPE = np.dtype([
     ("n", "<i8"), ("dest_base", "<i8"), ("p_off", "<i8"), ("c_off", "<i8"),
-    ("tape_off", "<i8"), ("blk_begin", "<i8"), ("cb_off", "<i8"), ("co_off", "<i8"),
-    ("a0_base", "<i8"), ("a0_stride", "<i8"),
+    ("tape_off", "<i8"), ("cb_off", "<i8"), ("co_off", "<i8"),
+    ("a0_base", "<i8"), ("a0_stride", "<i8"), ("ob_off", "<i8"), ("oo_off", "<i8"),
     ("n_roots", "<i4"), ("n_slots", "<i4"), ("n_ret", "<i4"), ("n_const", "<i4"),
     ("tape_len", "<i4"), ("n_regs", "<i4"), ("kind", "<i4"), ("flags", "<i4"),
     ("slot_off", "<i4"), ("sop_off", "<i4"), ("sop_len", "<i4"), ("unit", "<i4"),
+    ("variant", "<i4"), ("reserved", "<i4"),
 ])
 
-# one row per launch unit (int64 x 8), mirrored by include/sgb.h SGB_UNIT_*
-UNIT_FIELDS = ("wave", "kind", "variant", "group_begin", "group_end", "blocks", "block_size", "smem_regs")
-assert GROUP_DTYPE.itemsize == 128
+# one row per launch unit (int64 x 10), mirrored by csrc U_*
+UNIT_FIELDS = ("wave", "kind", "variant", "group_begin", "group_end", "tile_begin", "tile_end",
+               "block_size", "smem_regs", "flags")
+assert GROUP_DTYPE.itemsize == 144
 
 
 @dataclass
@@ -84,25 +93,35 @@ class DevicePlanArrays:
     """Host-side device plan: flat arrays handed to sgb_plan_create."""
 
     groups: np.ndarray  # GROUP_DTYPE, ordered by (wave, launch unit)
-    units: np.ndarray  # int64 [n_units, 8], UNIT_FIELDS
-    n_waves: int
+    units: np.ndarray  # int64 [n_units, 10], UNIT_FIELDS
+    tiles: np.ndarray  # int32 [n_tiles, 2]: group, first instance (one block each, launch order)
+    n_waves: int  # value-mode waves (a CSR-only unit may use wave n_waves)
     tape: np.ndarray  # (L, 4) u32 device words, byte offsets of each group's unit stride
     imm: np.ndarray  # f64
-    sop: np.ndarray  # int32
+    sop: np.ndarray  # u32 pairs (newterm mask, negate mask)
     slot_col: np.ndarray  # int32
     slot_delta: np.ndarray  # int64
     cbase: np.ndarray  # u32 per (column, 32-instance chunk) base of compressed columns
     coff: np.ndarray  # u16 per (column, instance) offset from its chunk base
-    positions: np.ndarray  # u32 (the plan's table, unchanged)
+    obase: np.ndarray  # u32 per (root, chunk) base of output positions
+    ooff: np.ndarray  # u16 per (root, instance) output-position offset, 0xFFFF = none
+    opos32: np.ndarray  # u32 wide output positions
+    positions: np.ndarray  # u32: the plan's table, unchanged, then copy-group columns
     constants: np.ndarray  # f64 (the plan's table, unchanged)
     outputs: np.ndarray  # int64
     value_array_size: int
     input_count: int
+    needs_zero: int = 2  # ZERO_NONE / ZERO_ONCE / ZERO_EVERY
     kernels: list = field(default_factory=list)
+    copies: list = field(default_factory=list)  # (wave, source addresses, CSR positions) per copy group
     exact: bool = True
 
     def unit(self, u: int) -> dict:
         return dict(zip(UNIT_FIELDS, (int(v) for v in self.units[u])))
+
+    @property
+    def csr_waves(self) -> int:
+        return max([self.n_waves] + [int(w) + 1 for w in self.units[:, 0]]) if len(self.units) else self.n_waves
 
 
 # -- waves ----------------------------------------------------------------------
@@ -495,15 +514,21 @@ def lower_kernel(plan, kp, index: int) -> KernelLowering:
 
 TAPE_BLOCK = 128
 SOP_BLOCK = 256
-SOP_VARIANTS = (4, 8, 16, 32)
 SMEM_LIMIT = 200 * 1024
 TAPE_VECS = (4, 2, 1)  # instances per thread of the tape interpreter, largest that fits
-VEC_SMEM_BUDGET = 56 * 1024  # per block: keeps >= 4 tape blocks resident per SM
+VEC_SMEM_BUDGET = 104 * 1024  # per block: keeps >= 2 tape blocks resident per SM
 
 
-def sop_vec(width: int) -> int:
-    """Instances per thread of the sum-of-products kernel (csrc sop_single VEC)."""
-    return 2 if width <= 8 else 1
+def sop_class(width: int) -> int:
+    for c, lim in enumerate(SOP_CLASSES):
+        if width <= lim:
+            return c
+    raise ValueError(f"sum-of-products width {width} exceeds {SOP_MAX}")
+
+
+def sop_vec(cls: int) -> int:
+    """Instances per thread of the sum-of-products kernel (csrc sop_vec)."""
+    return 4 if cls <= 1 else (2 if cls == 2 else 1)
 
 
 def block_size_for(n_regs: int) -> int:
@@ -514,50 +539,148 @@ def block_size_for(n_regs: int) -> int:
     return bs
 
 
-def _stream_flags(plan, lowered, read_sets):
-    """Groups whose results no later kernel reads: their stores may evict-first."""
-    reads = [r for r in read_sets if r.size]
-    allr = np.unique(np.concatenate(reads)) if reads else np.zeros(0, np.int64)
-    for kl in lowered:
-        kp = plan.kernels[kl.index]
-        lo, hi = kp.dest_base, kp.dest_base + kp.n_roots * kp.instances
-        a, b = np.searchsorted(allr, [lo, hi])
-        if b == a:
-            kl.flags |= FLAG_STREAM
+def compress_column(col: np.ndarray, allow_none: bool = False):
+    """Per-chunk base + u16 offset encoding of one index column (u32 values).
 
-
-def compress_columns(plan, kp):
-    """Per-chunk base + u16 offset encoding of a group's retained index columns.
-
-    Column r of instance i decodes to ``cbase[r*nchunks + i//32] + coff[r*N + i]``:
-    2 bytes per entry plus 4 bytes per 32 instances instead of 4 bytes per
-    entry.  Returns None when some chunk spans 65536 addresses or more (the
-    group then keeps the plan's u32 table) or the layout is interleaved.
+    Entry i decodes to ``base[i // 32] + off[i]``.  With ``allow_none``
+    entries equal to NONE32 become offset 0xFFFF (skipped by the kernel).
+    Returns None when some chunk spans 0xFFFF addresses or more.
     """
-    n, r = kp.instances, len(kp.retained)
-    if kp.layout != "coalesced" or r == 0 or n < CHUNK:
-        return None
-    cols = np.asarray(plan.positions[kp.p_base: kp.p_base + r * n], dtype=np.int64).reshape(r, n)
+    col = np.asarray(col, dtype=np.int64)
+    n = col.size
     nch = (n + CHUNK - 1) // CHUNK
     pad = nch * CHUNK - n
-    padded = np.concatenate([cols, np.repeat(cols[:, -1:], pad, axis=1)], axis=1).reshape(r, nch, CHUNK)
-    lo = padded.min(axis=2)
-    if int((padded.max(axis=2) - lo).max()) >= 1 << 16:
+    none = col == NONE32 if allow_none else np.zeros(n, bool)
+    big = np.iinfo(np.int64).max
+    lo_src = np.where(none, big, col)
+    hi_src = np.where(none, -1, col)
+    lo = np.concatenate([lo_src, np.full(pad, big)]).reshape(nch, CHUNK).min(axis=1)
+    hi = np.concatenate([hi_src, np.full(pad, -1)]).reshape(nch, CHUNK).max(axis=1)
+    empty = hi < 0
+    lo = np.where(empty, 0, lo)
+    if nch and int((hi - lo)[~empty].max(initial=0)) >= 0xFFFF:
         return None
-    off = (padded - lo[:, :, None]).reshape(r, nch * CHUNK)[:, :n]
-    return lo.astype(np.uint32).reshape(-1), off.astype(np.uint16).reshape(-1)
+    off = col - np.repeat(lo, CHUNK)[:n]
+    off = np.where(none, 0xFFFF, off)
+    return lo.astype(np.uint32), off.astype(np.uint16)
 
 
-def affine_column0(plan, kp):
+def affine_column0(col0: np.ndarray):
     """(base, stride) when index column 0 is exactly base + stride * i, else None."""
-    n = kp.instances
-    if kp.layout != "coalesced" or not kp.retained or n < 2:
+    n = col0.size
+    if n < 2:
         return None
-    c0 = np.asarray(plan.positions[kp.p_base: kp.p_base + n], dtype=np.int64)
+    c0 = np.asarray(col0, dtype=np.int64)
     base, stride = int(c0[0]), int(c0[1] - c0[0])
     if np.array_equal(c0, base + stride * np.arange(n, dtype=np.int64)):
         return base, stride
     return None
+
+
+@dataclass
+class _Group:
+    """One device group before packing: a plan kernel or a synthetic copy group."""
+
+    kind: int
+    flags: int
+    n: int
+    n_roots: int
+    dest_base: int
+    p_off: int
+    c_off: int
+    n_const: int
+    slot_col: np.ndarray
+    slot_delta: np.ndarray
+    columns: list  # retained index columns (int64 arrays) in retained order
+    layout: str
+    wave: int
+    n_regs: int = 0
+    tape: np.ndarray = None
+    imms: list = field(default_factory=list)
+    sop: np.ndarray = None
+    opos: np.ndarray = None  # (n_roots, n) int64 output positions, NONE32 = not an output
+    kernel: int = -1
+
+
+def _output_map(plan, lowered, waves):
+    """First CSR position of every result slot, and the outputs no kernel result covers.
+
+    Returns (opos per kernel [(R, N) arrays or None], residual positions, residual addresses).
+    """
+    outs = np.asarray(plan.outputs, dtype=np.int64)
+    k = np.arange(outs.size, dtype=np.int64)
+    order = np.argsort(outs, kind="stable")
+    so = outs[order]
+    first = np.ones(so.size, bool)
+    first[1:] = so[1:] != so[:-1]
+    covered = np.zeros(outs.size, bool)
+    opos = []
+    for kl in lowered:
+        kp = plan.kernels[kl.index]
+        lo, hi = kp.dest_base, kp.dest_base + kp.n_roots * kp.instances
+        a, b = np.searchsorted(so, [lo, hi])
+        sel = np.nonzero(first[a:b])[0] + a
+        if sel.size == 0:
+            opos.append(None)
+            continue
+        table = np.full(kp.n_roots * kp.instances, NONE32, dtype=np.int64)
+        table[so[sel] - lo] = k[order[sel]]
+        covered[order[sel]] = True
+        opos.append(table.reshape(kp.n_roots, kp.instances))
+    res_k = np.nonzero(~covered)[0]
+    return opos, res_k, outs[res_k]
+
+
+def _owner_waves(plan, waves, addrs):
+    """Wave after which each address holds its final value (-1: input or never written)."""
+    ks = plan.kernels
+    out = np.full(addrs.size, -1, dtype=np.int64)
+    if not ks or not addrs.size:
+        return out
+    starts = np.array([kp.dest_base for kp in ks], np.int64)
+    ends = np.array([kp.dest_base + kp.n_roots * kp.instances for kp in ks], np.int64)
+    order = np.argsort(starts, kind="stable")
+    pos = np.searchsorted(starts[order], addrs, side="right") - 1
+    ok = pos >= 0
+    own = np.where(ok, order[np.maximum(pos, 0)], 0)
+    inside = ok & (addrs < ends[own])
+    w = np.asarray(waves, np.int64)
+    out[inside] = w[own[inside]]
+    return out
+
+
+ZERO_NONE, ZERO_ONCE, ZERO_EVERY = 0, 1, 2
+
+
+def _needs_zero(plan, waves, reads) -> int:
+    """Which zeros of the value array the evaluation relies on (codegen.py:419).
+
+    ``reads`` is a list of (wave, addresses).  ZERO_ONCE: some load reads a
+    slot nothing writes (alignment padding, structural gaps) -- zeroing the
+    buffer once suffices.  ZERO_EVERY: some load reads a slot a later wave
+    writes (the interpreter's read-before-write, codegen.py:434-443) -- a
+    re-used buffer must be re-zeroed before every evaluation.
+    """
+    level = ZERO_NONE
+    for wk, addrs in reads:
+        addrs = addrs[addrs >= plan.input_count]
+        if not addrs.size:
+            continue
+        ow = _owner_waves(plan, waves, addrs)
+        if np.any(ow >= wk):
+            return ZERO_EVERY
+        if np.any(ow < 0):
+            level = ZERO_ONCE
+    return level
+
+
+def _tile_keys(g: _Group, starts: np.ndarray, tile: int) -> np.ndarray:
+    """Smallest output position in each tile (-1 for tiles without outputs)."""
+    if g.opos is None or g.n == 0:
+        return np.full(starts.size, -1, np.int64)
+    o = np.where(g.opos == NONE32, np.iinfo(np.int64).max, g.opos).min(axis=0)
+    m = np.minimum.reduceat(o, starts) if starts.size else o[:0]
+    return np.where(m == np.iinfo(np.int64).max, -1, m)
 
 
 def lower_plan(plan, compress: bool | None = None) -> DevicePlanArrays:
@@ -568,28 +691,67 @@ def lower_plan(plan, compress: bool | None = None) -> DevicePlanArrays:
     lowered = [lower_kernel(plan, kp, k) for k, kp in enumerate(plan.kernels)]
     for kl, w in zip(lowered, waves):
         kl.wave = w
-    _stream_flags(plan, lowered, read_sets)
     n_waves = (max(waves) + 1) if waves else 0
-    groups = np.zeros(len(lowered), GROUP_DTYPE)
-    tapes, imms, sops, scol, sdel, units, cbases, coffs = [], [], [], [], [], [], [], []
-    n_tape = n_imm = n_sop = n_slot = n_cb = n_co = 0
-    gi = 0
-    for w in range(n_waves):
-        members = [kl for kl in lowered if kl.wave == w]
-        # launch units of this wave: one tape unit, one SOP unit per width class
+    opos, res_k, res_addr = _output_map(plan, lowered, waves)
+    # copy groups: outputs that are inputs, duplicates or padding (CSR mode only)
+    avail = _owner_waves(plan, waves, res_addr) + 1  # first wave that may read the source
+    last = max(n_waves - 1, 0)
+    copy_sets = [(min(last, n_waves), avail <= last), (n_waves, avail > last)]
+    # stream flags: results no later kernel (or copy group) reads
+    reads = [r for r in read_sets if r.size] + ([res_addr] if res_addr.size else [])
+    allr = np.unique(np.concatenate(reads)) if reads else np.zeros(0, np.int64)
+    groups: list[_Group] = []
+    for kl in lowered:
+        kp = plan.kernels[kl.index]
+        lo, hi = kp.dest_base, kp.dest_base + kp.n_roots * kp.instances
+        a, b = np.searchsorted(allr, [lo, hi])
+        if b == a:
+            kl.flags |= FLAG_STREAM
+        n, r = kp.instances, len(kp.retained)
+        seg = np.asarray(plan.positions[kp.p_base: kp.p_base + r * n], dtype=np.int64)
+        cols = list(seg.reshape(r, n) if kp.layout == "coalesced" else seg.reshape(n, r).T)
+        flags = kl.flags | (FLAG_COHERENT if r == 1 and kp.pos_vars else 0)
+        groups.append(_Group(kl.kind, flags, n, kp.n_roots, kp.dest_base, kp.p_base, kp.c_base,
+                             len(kp.const_vars), kl.slot_col, kl.slot_delta, cols, kp.layout, kl.wave,
+                             kl.n_regs, kl.tape, kl.imms, kl.sop, opos[kl.index], kl.index))
+    extra_pos = []
+    p_next = int(np.asarray(plan.positions).size)
+    copy_waves = []
+    for wv, sel in copy_sets:
+        if not np.any(sel):
+            continue
+        addr, kk = res_addr[sel], res_k[sel]
+        ordr = np.argsort(kk, kind="stable")  # CSR order: coalesced stores
+        addr, kk = addr[ordr], kk[ordr]
+        groups.append(_Group(KIND_SOP, FLAG_CSR_ONLY | FLAG_STREAM | FLAG_COHERENT | FLAG_EXACT, int(addr.size), 1,
+                             int(plan.input_count), p_next, 0, 0, np.zeros(1, np.int32), np.zeros(1, np.int64),
+                             [addr], "coalesced", wv, sop=np.array([SOP_NEWTERM], np.int32),
+                             opos=kk.reshape(1, -1)))
+        extra_pos.append(addr.astype(np.uint32))
+        p_next += addr.size
+        copy_waves.append(wv)
+    needs_zero = _needs_zero(plan, waves, list(zip(waves, read_sets)) +
+                             [(g.wave, g.columns[0]) for g in groups if g.flags & FLAG_CSR_ONLY])
+    total_waves = max([n_waves] + [w + 1 for w in copy_waves])
+
+    # -- launch units and tiles ---------------------------------------------------------
+    packed = np.zeros(len(groups), GROUP_DTYPE)
+    order_groups: list[int] = []
+    units, tiles_all = [], []
+    tapes, imms, sops, scol, sdel, cbases, coffs, obases, ooffs, op32 = ([] for _ in range(10))
+    n_tape = n_imm = n_sop = n_slot = n_cb = n_co = n_ob = n_oo = n_o32 = 0
+    for w in range(total_waves):
+        members = [j for j, g in enumerate(groups) if g.wave == w]
         plan_units = []
-        # tape groups: lane-parallel ones run VEC instances per thread (one
-        # decode per VEC evaluations); self-referencing / serial ones VEC = 1
         for plain in (True, False):
-            tape_m = [kl for kl in members if kl.kind == KIND_TAPE and
-                      plain == (not kl.flags & (FLAG_SELFREF | FLAG_SERIAL))]
-            if not tape_m:
+            tm = [j for j in members if groups[j].kind == KIND_TAPE and
+                  plain == (not groups[j].flags & (FLAG_SELFREF | FLAG_SERIAL))]
+            if not tm:
                 continue
-            regs = max(kl.n_regs for kl in tape_m)
+            regs = max(groups[j].n_regs for j in tm)
             bs = block_size_for(regs)
             if regs * bs * 8 > SMEM_LIMIT:
-                raise ValueError(f"wave {w}: template needs {regs} scratch registers, "
-                                 f"more than shared memory holds")
+                raise ValueError(f"wave {w}: template needs {regs} scratch registers, more than shared memory holds")
             vec = 1
             if plain:
                 forced = int(os.environ.get("SGB_TAPE_VEC", "0"))
@@ -597,87 +759,117 @@ def lower_plan(plan, compress: bool | None = None) -> DevicePlanArrays:
                     if regs * v * bs * 8 <= VEC_SMEM_BUDGET or v == 1:
                         vec = v
                         break
-            plan_units.append((KIND_TAPE, vec, bs, regs, tape_m))
-        for var in SOP_VARIANTS:
-            lo = 0 if var == SOP_VARIANTS[0] else SOP_VARIANTS[SOP_VARIANTS.index(var) - 1]
-            sm = [kl for kl in members if kl.kind == KIND_SOP and lo < len(kl.sop) <= var]
-            if sm:
-                plan_units.append((KIND_SOP, var, SOP_BLOCK, 0, sm))
+            plan_units.append((KIND_TAPE, vec, bs, regs, tm))
+        sm = [j for j in members if groups[j].kind == KIND_SOP]
+        if sm:
+            plan_units.append((KIND_SOP, 0, SOP_BLOCK, 0, sm))
         for kind, variant, bs, regs, ms in plan_units:
-            g_begin = gi
-            blk = 0
-            for kl in ms:
-                kp = plan.kernels[kl.index]
-                g = groups[gi]
-                g["n"] = kp.instances
-                g["dest_base"] = kp.dest_base
-                g["p_off"] = kp.p_base
-                g["c_off"] = kp.c_base
-                g["n_roots"] = kp.n_roots
-                g["n_slots"] = len(kp.pos_vars)
-                g["n_ret"] = len(kp.retained)
-                g["n_const"] = len(kp.const_vars)
-                g["kind"] = kl.kind
-                g["flags"] = kl.flags
-                g["n_regs"] = kl.n_regs
-                g["unit"] = len(units)
-                g["slot_off"] = n_slot
-                scol.append(kl.slot_col)
-                sdel.append(kl.slot_delta)
-                n_slot += len(kl.slot_col)
-                # immediates are renumbered into the plan-wide pool
-                stride = bs * variant if kind == KIND_TAPE else bs
-                t = assemble(kl.tape, stride, n_imm)
-                g["tape_off"] = n_tape
-                g["tape_len"] = len(t)
-                tapes.append(t)
-                n_tape += len(t)
-                imms.extend(kl.imms)
-                n_imm += len(kl.imms)
-                g["sop_off"] = n_sop
-                g["sop_len"] = len(kl.sop)
-                if kl.kind == KIND_SOP:
-                    # device form: bit f of word 0 = factor f starts a term, word 1 = negate
-                    newterm = sum(1 << f for f, d in enumerate(kl.sop.tolist()) if d & SOP_NEWTERM)
-                    neg = sum(1 << f for f, d in enumerate(kl.sop.tolist()) if d & SOP_NEG)
-                    sops.append(np.array([newterm, neg], np.uint32).view(np.int32))
-                    n_sop += 2
-                g["blk_begin"] = blk
-                aff = affine_column0(plan, kp) if compress else None
-                if aff is not None:
-                    g["flags"] |= FLAG_AFFINE0
-                    g["a0_base"], g["a0_stride"] = aff
-                comp = compress_columns(plan, kp) if compress and len(kp.retained) > (aff is not None) else None
-                if comp is not None:
-                    g["flags"] |= FLAG_W16
-                    g["cb_off"], g["co_off"] = n_cb, n_co
-                    cbases.append(comp[0])
-                    coffs.append(comp[1])
-                    n_cb += comp[0].size
-                    n_co += comp[1].size
-                per_block = bs * (variant if kind == KIND_TAPE else sop_vec(variant))
-                blk += 1 if kl.flags & FLAG_SERIAL else (kp.instances + per_block - 1) // per_block
-                gi += 1
-            units.append((w, kind, variant, g_begin, gi, blk, bs, regs))
+            g_begin = len(order_groups)
+            unit_tiles, unit_keys = [], []
+            for j in ms:
+                g = groups[j]
+                gi = len(order_groups)
+                order_groups.append(j)
+                rec = packed[gi]
+                rec["n"], rec["dest_base"], rec["p_off"], rec["c_off"] = g.n, g.dest_base, g.p_off, g.c_off
+                rec["n_roots"], rec["n_slots"], rec["n_ret"] = g.n_roots, len(g.slot_col), len(g.columns)
+                rec["n_const"], rec["kind"], rec["n_regs"], rec["unit"] = g.n_const, g.kind, g.n_regs, len(units)
+                rec["slot_off"] = n_slot
+                scol.append(g.slot_col)
+                sdel.append(g.slot_delta)
+                n_slot += len(g.slot_col)
+                flags = g.flags
+                if kind == KIND_TAPE:
+                    t = assemble(g.tape, bs * variant, n_imm)
+                    rec["tape_off"], rec["tape_len"] = n_tape, len(t)
+                    tapes.append(t)
+                    n_tape += len(t)
+                    imms.extend(g.imms)
+                    n_imm += len(g.imms)
+                    tile = bs * variant
+                else:
+                    cls = sop_class(len(g.sop))
+                    rec["variant"], rec["sop_off"], rec["sop_len"] = cls, n_sop, len(g.sop)
+                    newterm = sum(1 << f for f, d in enumerate(g.sop.tolist()) if d & SOP_NEWTERM)
+                    neg = sum(1 << f for f, d in enumerate(g.sop.tolist()) if d & SOP_NEG)
+                    sops.append(np.array([newterm, neg], np.uint32))
+                    n_sop += 1
+                    tile = bs * sop_vec(cls)
+                # index columns: affine column 0, compressed columns
+                if compress and g.layout == "coalesced" and g.columns:
+                    aff = affine_column0(g.columns[0])
+                    if aff is not None:
+                        flags |= FLAG_AFFINE0
+                        rec["a0_base"], rec["a0_stride"] = aff
+                    if len(g.columns) > (aff is not None) and g.n >= CHUNK:
+                        comp = [compress_column(c) for c in g.columns]
+                        if all(c is not None for c in comp):
+                            flags |= FLAG_W16
+                            rec["cb_off"], rec["co_off"] = n_cb, n_co
+                            for cb, co in comp:
+                                cbases.append(cb)
+                                coffs.append(co)
+                                n_cb += cb.size
+                                n_co += co.size
+                # output positions
+                if g.opos is not None:
+                    comp = [compress_column(row, allow_none=True) for row in g.opos]
+                    if all(c is not None for c in comp):
+                        flags |= FLAG_OPOS16
+                        rec["ob_off"], rec["oo_off"] = n_ob, n_oo
+                        for ob, oo in comp:
+                            obases.append(ob)
+                            ooffs.append(oo)
+                            n_ob += ob.size
+                            n_oo += oo.size
+                    else:
+                        flags |= FLAG_OPOS32
+                        rec["oo_off"] = n_o32
+                        op32.append(g.opos.reshape(-1).astype(np.uint32))
+                        n_o32 += g.opos.size
+                rec["flags"] = flags
+                if flags & FLAG_SERIAL:
+                    starts = np.zeros(1 if g.n else 0, np.int64)
+                else:
+                    starts = np.arange(0, g.n, tile, dtype=np.int64)
+                unit_tiles.append(np.stack([np.full(starts.size, gi, np.int64), starts], axis=1))
+                unit_keys.append(_tile_keys(g, starts, tile))
+            t = np.concatenate(unit_tiles) if unit_tiles else np.zeros((0, 2), np.int64)
+            keys = np.concatenate(unit_keys) if unit_keys else np.zeros(0, np.int64)
+            if np.any(keys >= 0):  # CSR-ordered schedule: partial sectors of the output merge in L2
+                t = t[np.argsort(keys, kind="stable")]
+            t0 = sum(len(x) for x in tiles_all)
+            tiles_all.append(t)
+            uflags = UNIT_CSR_ONLY if w >= n_waves else 0
+            units.append((w, kind, variant, g_begin, len(order_groups), t0, t0 + len(t), bs, regs, uflags))
     cat = lambda xs, dt: (np.concatenate(xs).astype(dt) if xs and sum(len(x) for x in xs)  # noqa: E731
                           else np.zeros(0, dt))
     exact = all(kl.flags & FLAG_EXACT for kl in lowered)
+    positions = np.ascontiguousarray(plan.positions, dtype=np.uint32)
+    if extra_pos:
+        positions = np.concatenate([positions] + extra_pos)
     return DevicePlanArrays(
-        groups=groups,
+        groups=packed,
         units=np.asarray(units, np.int64).reshape(-1, len(UNIT_FIELDS)),
+        tiles=cat(tiles_all, np.int32).reshape(-1, 2),
         n_waves=n_waves,
         tape=cat(tapes, np.uint32).reshape(-1, 4),
         imm=np.asarray(imms, np.float64),
-        sop=cat(sops, np.int32),
+        sop=cat(sops, np.uint32),
         slot_col=cat(scol, np.int32),
         slot_delta=cat(sdel, np.int64),
         cbase=cat(cbases, np.uint32),
         coff=cat(coffs, np.uint16),
-        positions=np.ascontiguousarray(plan.positions, dtype=np.uint32),
+        obase=cat(obases, np.uint32),
+        ooff=cat(ooffs, np.uint16),
+        opos32=cat(op32, np.uint32),
+        positions=positions,
         constants=np.ascontiguousarray(plan.constants, dtype=np.float64),
         outputs=np.asarray(plan.outputs, np.int64),
         value_array_size=int(plan.value_array_size),
         input_count=int(plan.input_count),
+        needs_zero=int(needs_zero),
         kernels=lowered,
+        copies=[(g.wave, g.columns[0], g.opos[0]) for g in groups if g.flags & FLAG_CSR_ONLY],
         exact=exact,
     )

@@ -68,6 +68,47 @@ def wave_traffic(plan, lowered, batch: int = 1) -> list[LaunchTraffic]:
     return out
 
 
+def csr_wave_traffic(plan, lowered, batch: int = 1) -> list[LaunchTraffic]:
+    """Per CSR-mode wave (sgb_run_csr): compulsory bytes of each launch wave.
+
+    index + constants as above; reads = 8 B per distinct address loaded by the
+    wave's groups and copy groups; writes = 8 B per result slot a later wave
+    re-reads plus 8 B per output value stored (first occurrence by its
+    producer, the rest by copy groups).  Output-position tables are an
+    encoding overhead of this backend, not algorithmic bytes.
+    """
+    outs = np.asarray(plan.outputs, dtype=np.int64)
+    uniq = np.unique(outs)
+    waves = max([lowered.n_waves] + [w + 1 for w, _, _ in lowered.copies])
+    out = []
+    for w in range(waves):
+        idx = con = wr = ops = 0
+        addrs = []
+        for kl in lowered.kernels:
+            if kl.wave != w:
+                continue
+            kp = plan.kernels[kl.index]
+            idx += 4 * len(kp.retained) * kp.instances
+            con += 8 * len(kp.const_vars) * kp.instances
+            ops += kl.ops * kp.instances * batch
+            lo, hi = kp.dest_base, kp.dest_base + kp.n_roots * kp.instances
+            if kl.flags & 16:  # FLAG_STREAM: only the outputs are stored
+                a, b = np.searchsorted(uniq, [lo, hi])
+                wr += 8 * int(b - a) * batch
+            else:
+                wr += 8 * kp.n_roots * kp.instances * batch
+            if kp.pos_vars:
+                addrs.append(np.unique(np.concatenate(slot_addresses(plan, kp))))
+        for cw, src, _ in lowered.copies:
+            if cw == w:
+                idx += 4 * src.size
+                wr += 8 * src.size * batch
+                addrs.append(np.unique(src))
+        reads = int(np.unique(np.concatenate(addrs)).size) if addrs else 0
+        out.append(LaunchTraffic(f"csr_wave{w}", idx, con, 8 * reads * batch, wr, ops))
+    return out
+
+
 def plan_balg(plan) -> int:
     """SURVEY §8(d) single-evaluation B_alg of the plan (intermediates once)."""
     P = int(np.asarray(plan.positions).size)

@@ -47,9 +47,11 @@ class _Desc(ctypes.Structure):
         ("n_groups", ctypes.c_int32),
         ("n_waves", ctypes.c_int32),
         ("n_units", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("needs_zero", ctypes.c_int32),
         ("groups", ctypes.c_void_p),
         ("units", ctypes.c_void_p),
+        ("tiles", ctypes.c_void_p),
+        ("n_tiles", ctypes.c_int64),
         ("tape", ctypes.c_void_p),
         ("tape_rows", ctypes.c_int64),
         ("imm", ctypes.c_void_p),
@@ -67,15 +69,21 @@ class _Desc(ctypes.Structure):
         ("n_cbase", ctypes.c_int64),
         ("coff", ctypes.c_void_p),
         ("n_coff", ctypes.c_int64),
+        ("obase", ctypes.c_void_p),
+        ("n_obase", ctypes.c_int64),
+        ("ooff", ctypes.c_void_p),
+        ("n_ooff", ctypes.c_int64),
+        ("opos32", ctypes.c_void_p),
+        ("n_opos32", ctypes.c_int64),
         ("outputs", ctypes.c_void_p),
         ("n_outputs", ctypes.c_int64),
     ]
 
 
 SYMBOLS = (
-    "sgb_plan_create", "sgb_plan_destroy", "sgb_run_values", "sgb_gather_outputs",
-    "sgb_sg_run", "sgb_run_outputs_host", "sgb_run_batch", "sgb_gather_outputs_batch",
-    "sgb_plan_launches", "sgb_last_error", "sgb_run_wave", "sgb_plan_units",
+    "sgb_plan_create", "sgb_plan_destroy", "sgb_run_values", "sgb_run_csr", "sgb_gather_outputs",
+    "sgb_sg_run", "sgb_run_outputs_host", "sgb_run_batch", "sgb_run_batch_csr", "sgb_gather_outputs_batch",
+    "sgb_plan_waves", "sgb_last_error", "sgb_run_wave", "sgb_plan_units",
 )
 
 
@@ -95,14 +103,16 @@ def load_library(path: Path | str | None = None):
             "sgb_plan_create": (i32, [ctypes.POINTER(_Desc), i32, ctypes.POINTER(vp)]),
             "sgb_plan_destroy": (None, [vp]),
             "sgb_run_values": (i32, [vp, vp, vp]),
-            "sgb_run_wave": (i32, [vp, vp, i32, vp]),
+            "sgb_run_csr": (i32, [vp, vp, vp, vp]),
+            "sgb_run_wave": (i32, [vp, vp, vp, i32, vp]),
             "sgb_gather_outputs": (i32, [vp, vp, vp, vp]),
             "sgb_sg_run": (i32, [vp, vp, vp, vp]),
             "sgb_run_outputs_host": (i32, [vp, vp, vp]),
             "sgb_run_batch": (i32, [vp, vp, i64, i64, vp]),
+            "sgb_run_batch_csr": (i32, [vp, vp, i64, i64, vp, i64, vp]),
             "sgb_gather_outputs_batch": (i32, [vp, vp, i64, i64, vp, i64, vp]),
-            "sgb_plan_launches": (i32, [vp]),
-            "sgb_plan_units": (i32, [vp]),
+            "sgb_plan_waves": (i32, [vp, i32]),
+            "sgb_plan_units": (i32, [vp, i32]),
             "sgb_last_error": (ctypes.c_char_p, []),
         }
         for name, (res, args) in sig.items():
@@ -154,33 +164,43 @@ class DevicePlan:
         keep = dict(
             groups=np.ascontiguousarray(lw.groups, GROUP_DTYPE),
             units=np.ascontiguousarray(lw.units, np.int64),
+            tiles=np.ascontiguousarray(lw.tiles, np.int32).reshape(-1, 2),
             tape=np.ascontiguousarray(lw.tape, np.uint32).reshape(-1, 4),
             imm=np.ascontiguousarray(lw.imm, np.float64),
-            sop=np.ascontiguousarray(lw.sop, np.int32),
+            sop=np.ascontiguousarray(lw.sop, np.uint32),
             scol=np.ascontiguousarray(lw.slot_col, np.int32),
             sdel=np.ascontiguousarray(lw.slot_delta, np.int64),
             pos=np.ascontiguousarray(lw.positions, np.uint32),
             con=np.ascontiguousarray(lw.constants, np.float64),
             cbase=np.ascontiguousarray(lw.cbase, np.uint32),
             coff=np.ascontiguousarray(lw.coff, np.uint16),
+            obase=np.ascontiguousarray(lw.obase, np.uint32),
+            ooff=np.ascontiguousarray(lw.ooff, np.uint16),
+            opos32=np.ascontiguousarray(lw.opos32, np.uint32),
             outs=np.ascontiguousarray(lw.outputs, np.int64),
         )
         d = _Desc(
             value_array_size=self.value_array_size, input_count=self.input_count,
             n_groups=len(keep["groups"]), n_waves=lw.n_waves, n_units=len(keep["units"]),
-            groups=_ptr(keep["groups"]), units=_ptr(keep["units"]), tape=_ptr(keep["tape"]),
+            needs_zero=int(lw.needs_zero),
+            groups=_ptr(keep["groups"]), units=_ptr(keep["units"]), tiles=_ptr(keep["tiles"]),
+            n_tiles=keep["tiles"].shape[0], tape=_ptr(keep["tape"]),
             tape_rows=keep["tape"].shape[0], imm=_ptr(keep["imm"]), n_imm=keep["imm"].size,
             sop=_ptr(keep["sop"]), n_sop=keep["sop"].size, slot_col=_ptr(keep["scol"]),
             slot_delta=_ptr(keep["sdel"]), n_slot=keep["scol"].size, positions=_ptr(keep["pos"]),
             n_positions=keep["pos"].size, constants=_ptr(keep["con"]), n_constants=keep["con"].size,
             cbase=_ptr(keep["cbase"]), n_cbase=keep["cbase"].size, coff=_ptr(keep["coff"]),
-            n_coff=keep["coff"].size, outputs=_ptr(keep["outs"]), n_outputs=keep["outs"].size,
+            n_coff=keep["coff"].size, obase=_ptr(keep["obase"]), n_obase=keep["obase"].size,
+            ooff=_ptr(keep["ooff"]), n_ooff=keep["ooff"].size, opos32=_ptr(keep["opos32"]),
+            n_opos32=keep["opos32"].size, outputs=_ptr(keep["outs"]), n_outputs=keep["outs"].size,
         )
         torch.cuda.init()
         _check(self._lib.sgb_plan_create(ctypes.byref(d), self.device, ctypes.byref(self._handle)),
                "sgb_plan_create")
-        self.launches = int(self._lib.sgb_plan_launches(self._handle))  # waves
-        self.units = int(self._lib.sgb_plan_units(self._handle))  # kernel launches per evaluation
+        self.launches = int(self._lib.sgb_plan_waves(self._handle, 0))  # value-mode waves
+        self.csr_launches = int(self._lib.sgb_plan_waves(self._handle, 1))  # CSR-mode waves
+        self.units = int(self._lib.sgb_plan_units(self._handle, 0))  # kernel launches per evaluation
+        self.csr_units = int(self._lib.sgb_plan_units(self._handle, 1))
 
     def close(self):
         if self._handle:
@@ -221,9 +241,22 @@ class DevicePlan:
                                         _stream_handle(stream)), "sgb_run_values")
         return x
 
-    def run_wave(self, x, wave: int, stream=None):
-        """One dependency wave (profiling / per-launch timing)."""
-        _check(self._lib.sgb_run_wave(self._handle, ctypes.c_void_p(x.data_ptr()), int(wave),
+    def run_csr(self, x, out=None, stream=None):
+        """inputs (placed in x) -> CSR values in one pass; x is scratch for intermediates."""
+        import torch
+
+        self._check_tensor(x, self.value_array_size, "x")
+        if out is None:
+            out = torch.empty(self.n_outputs, dtype=torch.float64, device=x.device)
+        self._check_tensor(out, self.n_outputs, "out")
+        _check(self._lib.sgb_run_csr(self._handle, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()),
+                                     _stream_handle(stream)), "sgb_run_csr")
+        return out
+
+    def run_wave(self, x, wave: int, out=None, stream=None):
+        """One dependency wave (profiling / per-launch timing); ``out`` given = CSR mode."""
+        _check(self._lib.sgb_run_wave(self._handle, ctypes.c_void_p(x.data_ptr()),
+                                      ctypes.c_void_p(out.data_ptr() if out is not None else 0), int(wave),
                                       _stream_handle(stream)), "sgb_run_wave")
         return x
 
@@ -247,6 +280,22 @@ class DevicePlan:
         _check(self._lib.sgb_run_batch(self._handle, ctypes.c_void_p(X.data_ptr()), X.stride(0),
                                        X.shape[1], _stream_handle(stream)), "sgb_run_batch")
         return X
+
+    def run_batch_csr(self, X, out=None, stream=None):
+        """Batched CSR mode: out[k, b] = value of output k in value set b (no gather pass)."""
+        import torch
+
+        self._check_tensor(X, self.value_array_size, "X")
+        if X.dim() != 2:
+            raise ValueError("X must be [value_array_size, batch]")
+        if out is None:
+            out = torch.empty((self.n_outputs, X.shape[1]), dtype=torch.float64, device=X.device)
+        if out.dim() != 2 or out.shape[1] < X.shape[1] or out.shape[0] != self.n_outputs or out.stride(1) != 1:
+            raise ValueError("out must be [n_outputs, >= batch] with unit column stride")
+        _check(self._lib.sgb_run_batch_csr(self._handle, ctypes.c_void_p(X.data_ptr()), X.stride(0), X.shape[1],
+                                           ctypes.c_void_p(out.data_ptr()), out.stride(0), _stream_handle(stream)),
+               "sgb_run_batch_csr")
+        return out
 
     def gather_outputs_batch(self, X, out=None, stream=None):
         import torch

@@ -26,6 +26,7 @@ def _decode_addrs(dp, g, i):
     n, nret = int(g["n"]), int(g["n_ret"])
     if n_slots == 0:
         return []
+
     def column(col):
         if col == 0 and g["flags"] & L.FLAG_AFFINE0:
             return int(g["a0_base"]) + int(g["a0_stride"]) * np.asarray(i, dtype=np.int64)
@@ -40,13 +41,43 @@ def _decode_addrs(dp, g, i):
     out = []
     for s in range(n_slots):
         col = int(cols[s])
-        if col < 0:
+        if col < 0 or g["flags"] & L.FLAG_COHERENT:
             out.append(idx0 + int(dels[s]))
         elif col == 0:
             out.append(idx0)
         else:
             out.append(column(col))
     return out
+
+
+def _out_pos(dp, g, r, i):
+    """Output positions of root r (int64, -1 = not an output)."""
+    n = int(g["n"])
+    if g["flags"] & L.FLAG_OPOS16:
+        nch = (n + L.CHUNK - 1) // L.CHUNK
+        off = dp.ooff[g["oo_off"] + r * n + i].astype(np.int64)
+        base = dp.obase[g["ob_off"] + r * nch + i // L.CHUNK].astype(np.int64)
+        return np.where(off == 0xFFFF, -1, base + off)
+    if g["flags"] & L.FLAG_OPOS32:
+        o = dp.opos32[g["oo_off"] + r * n + i].astype(np.int64)
+        return np.where(o == L.NONE32, -1, o)
+    return np.full(len(i), -1, np.int64)
+
+
+class _Store:
+    """store_root of csrc/sgb.cu."""
+
+    def __init__(self, dp, x, out):
+        self.dp, self.x, self.out = dp, x, out
+
+    def __call__(self, g, r, i, v):
+        csr = self.out is not None
+        if not (csr and g["flags"] & L.FLAG_STREAM):
+            self.x[g["dest_base"] + r * int(g["n"]) + i] = v
+        if csr:
+            o = _out_pos(self.dp, g, r, i)
+            m = o >= 0
+            self.out[o[m]] = np.asarray(v)[m] if np.ndim(v) else v
 
 
 def _const(dp, g, k, i):
@@ -94,23 +125,48 @@ def _vec(fn, a):
     return np.array([fn(v) for v in a.tolist()], dtype=np.float64)
 
 
-def run_values(dp, inputs) -> np.ndarray:
-    x = np.zeros(dp.value_array_size, np.float64)
-    x[: dp.input_count] = inputs
+def check_tiles(dp):
+    """Every (non-serial) group's instances are covered by exactly one tile of its unit."""
     for u in range(len(dp.units)):
-        # groups of one wave are independent; units run in wave order
         unit = dp.unit(u)
+        t = dp.tiles[unit["tile_begin"]: unit["tile_end"]]
         for gi in range(unit["group_begin"], unit["group_end"]):
             g = dp.groups[gi]
+            starts = np.sort(t[t[:, 0] == gi, 1].astype(np.int64))
+            n = int(g["n"])
+            if g["flags"] & L.FLAG_SERIAL:
+                assert starts.tolist() == ([0] if n else [])
+                continue
+            if g["kind"] == L.KIND_SOP:
+                tile = L.SOP_BLOCK * L.sop_vec(int(g["variant"]))
+            else:
+                tile = unit["block_size"] * unit["variant"]
+            assert starts.tolist() == list(range(0, n, tile)), (u, gi)
+
+
+def _run(dp, inputs, csr: bool):
+    x = np.zeros(dp.value_array_size, np.float64)
+    x[: dp.input_count] = inputs
+    out = np.full(len(dp.outputs), np.nan) if csr else None
+    store = _Store(dp, x, out)
+    for u in range(len(dp.units)):
+        # groups of one unit are independent; units run in wave order
+        unit = dp.unit(u)
+        if unit["flags"] & L.UNIT_CSR_ONLY and not csr:
+            continue
+        for gi in range(unit["group_begin"], unit["group_end"]):
+            g = dp.groups[gi]
+            if g["flags"] & L.FLAG_CSR_ONLY and not csr:
+                continue
             n = int(g["n"])
             if g["flags"] & L.FLAG_SERIAL:
                 for i in range(n):
-                    _tape(dp, g, x, np.array([i]))
+                    _tape(dp, g, x, np.array([i]), store)
                 continue
             i = np.arange(n, dtype=np.int64)
             if g["kind"] == L.KIND_SOP:
-                nt = int(dp.sop[g["sop_off"]]) & 0xFFFFFFFF
-                ng = int(dp.sop[g["sop_off"] + 1]) & 0xFFFFFFFF
+                nt = int(dp.sop[2 * g["sop_off"]])
+                ng = int(dp.sop[2 * g["sop_off"] + 1])
                 addrs = _decode_addrs(dp, g, i)
                 acc = term = None
                 for f in range(int(g["sop_len"])):
@@ -124,13 +180,22 @@ def run_values(dp, inputs) -> np.ndarray:
                     else:
                         term = term * v
                 res = term if acc is None else acc + term
-                x[g["dest_base"] + i] = res
+                store(g, 0, i, res)
             else:
-                _tape(dp, g, x, i)
-    return x
+                _tape(dp, g, x, i, store)
+    return x, out
 
 
-def _tape(dp, g, x, i):
+def run_values(dp, inputs) -> np.ndarray:
+    return _run(dp, inputs, csr=False)[0]
+
+
+def run_csr(dp, inputs) -> np.ndarray:
+    """CSR mode: the outputs written directly by the producing groups and copy groups."""
+    return _run(dp, inputs, csr=True)[1]
+
+
+def _tape(dp, g, x, i, store):
     """Decode the device tape words (lower.assemble) of this group's launch unit."""
     n = int(g["n"])
     unit = dp.unit(int(g["unit"]))
@@ -155,7 +220,7 @@ def _tape(dp, g, x, i):
             with np.errstate(all="ignore"):
                 if op == L.T_ST:
                     if not selfref or ww == ph:
-                        x[g["dest_base"] + ww * n + i] = R[a]
+                        store(g, ww, i, R[a])
                     continue
                 if op == L.T_IMM:
                     v = np.full(len(i), dp.imm[ww])

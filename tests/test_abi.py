@@ -28,8 +28,8 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_group_record_matches_header():
-    # sgb_group: 10 int64 + 12 int32 (the gcc probe below checks every offset)
-    assert GROUP_DTYPE.itemsize == 10 * 8 + 12 * 4
+    # sgb_group: 11 int64 + 14 int32 (the gcc probe below checks every offset)
+    assert GROUP_DTYPE.itemsize == 11 * 8 + 14 * 4
 
 
 def test_desc_layout_matches_header(tmp_path):

@@ -7,6 +7,7 @@ from conftest import bits
 from paper_2110_12865_b200.lower import (
     KIND_SOP, KIND_TAPE, compute_waves, lower_plan, recognise_sop,
 )
+from paper_2110_12865_b200 import lower as L
 from paper_2110_12865_b200.plan import load_plan
 
 
@@ -14,6 +15,14 @@ def test_emulated_device_plan_matches_reference_bitwise(golden):
     dp = lower_plan(golden.plan)
     x = emu.run_values(dp, golden.inputs)
     assert np.array_equal(bits(x), bits(golden.values))
+
+
+def test_emulated_csr_mode_matches_reference_outputs(golden):
+    """CSR mode: producers store outputs at their CSR positions, copy groups cover the rest."""
+    dp = lower_plan(golden.plan)
+    emu.check_tiles(dp)
+    out = emu.run_csr(dp, golden.inputs)
+    assert np.array_equal(bits(out), bits(golden.outputs))
 
 
 def test_waves_respect_producers(golden):
@@ -38,6 +47,22 @@ def test_lmlt_is_mostly_sum_of_products():
     n_sop = int(np.sum(dp.groups["kind"] == KIND_SOP))
     assert n_sop >= len(plan.kernels) // 2
     assert dp.n_waves == 5  # L.M.L^T + A needs 5 waves
+    # the output groups write their CSR positions directly
+    assert np.sum((dp.groups["flags"] & (L.FLAG_OPOS16 | L.FLAG_OPOS32)) != 0) >= 5
+
+
+def test_builder_plan_csr_mode_copy_group():
+    """Builder plan: A-only outputs are input slots -> one CSR-only copy group in the last wave."""
+    from oracle import oracle
+    from paper_2110_12865_b200.programs.mesh import build_lmlt_plan, lmlt_inputs
+
+    plan, _, _ = build_lmlt_plan(20)
+    dp = lower_plan(plan)
+    copy = (dp.groups["flags"] & L.FLAG_CSR_ONLY) != 0
+    assert copy.sum() == 1 and dp.needs_zero == L.ZERO_ONCE  # structural gaps read as zero
+    assert int(dp.units[-1][0]) == dp.n_waves - 1  # no extra CSR-only wave: sources are inputs
+    inputs = lmlt_inputs(20)
+    assert np.array_equal(bits(emu.run_csr(dp, inputs)), bits(oracle.run_outputs(plan, inputs)))
 
 
 def test_sop_rejects_right_nested_products():
@@ -55,7 +80,9 @@ def test_broken_schedule_still_matches_interpreter(tmp_path):
     plan.kernels.append(plan.kernels.pop(0))
     inputs = np.random.default_rng(0).uniform(0.5, 2.0, plan.input_count)
     want = oracle.run_values(plan, inputs)
-    got = emu.run_values(lower_plan(plan), inputs)
+    dp = lower_plan(plan)
+    assert dp.needs_zero == L.ZERO_EVERY
+    got = emu.run_values(dp, inputs)
     assert np.array_equal(bits(got), bits(want))
 
 
