@@ -31,14 +31,13 @@ print("waves", dp.launches, "units", dp.units, flush=True)
 if args.batch:
     X = torch.zeros((plan.value_array_size, args.batch), dtype=torch.float64, device="cuda")
     X[: plan.input_count] = torch.from_numpy(lmlt_inputs(args.w)).cuda()[:, None]
+    out = torch.empty((len(plan.outputs), args.batch), dtype=torch.float64, device="cuda")
     for _ in range(args.evals):
-        dp.run_batch(X)
-        dp.gather_outputs_batch(X)
+        dp.run_batch_csr(X, out)
 else:
     x = dp.new_values(lmlt_inputs(args.w))
     out = torch.empty(len(plan.outputs), dtype=torch.float64, device="cuda")
     for _ in range(args.evals):
-        dp.run_values(x)
-        dp.gather_outputs(x, out)
+        dp.run_csr(x, out)
 torch.cuda.synchronize()
 print("done", flush=True)
