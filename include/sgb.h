@@ -58,7 +58,7 @@ typedef struct sgb_group {
   int32_t tape_len, n_regs, kind, flags;
   int32_t slot_off, sop_off, sop_len, unit;
   int32_t variant; /* sum-of-products width class (factors <= 2, 4, 8, 16, 32) */
-  int32_t reserved;
+  int32_t shape;   /* sum-of-products shape: 0 generic, 1 plain sum, 2 two-factor products (+ single tail) */
 } sgb_group;
 
 /* Host-side device plan handed to sgb_plan_create (all pointers host memory,

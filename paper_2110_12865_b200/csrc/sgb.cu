@@ -63,7 +63,7 @@ constexpr int BATCH_WARPS = 8;
 constexpr uint32_t NONE = 0xFFFFFFFFu;
 
 // instances per thread of the sum-of-products kernel, per width class (lower.SOP_CLASSES)
-__host__ __device__ constexpr int sop_vec(int cls) { return cls <= 1 ? 4 : (cls == 2 ? 2 : 1); }
+__host__ __device__ constexpr int sop_vec(int cls) { return cls == 0 ? 8 : cls == 1 ? 4 : cls == 2 ? 2 : 1; }
 __host__ __device__ constexpr int sop_lmax(int cls) { return cls == 0 ? 2 : cls == 1 ? 4 : cls == 2 ? 8 : cls == 3 ? 16 : 32; }
 
 thread_local std::string g_err;
@@ -99,23 +99,23 @@ struct Tables {
 // ---- cache-policy helpers ---------------------------------------------------------
 __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 // streaming index-table read: no L1 allocation, L2 evict-first
 __device__ __forceinline__ uint32_t ld_index(const uint32_t *a, uint64_t pol) {
   uint32_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
   return v;
 }
 __device__ __forceinline__ uint16_t ld_index16(const uint16_t *a, uint64_t pol) {
   uint16_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(a), "l"(pol));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(a), "l"(pol));
   return v;
 }
 __device__ __forceinline__ double ld_const(const double *a, uint64_t pol) {
   double v;
-  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
   return v;
 }
 __device__ __forceinline__ void st_stream(double *a, double v, uint64_t pol) {
@@ -145,6 +145,15 @@ __device__ __forceinline__ uint32_t out_pos(const Tables &T, const sgb_group &G,
   }
   if (G.flags & FLAG_OPOS32) return ld_index(T.opos32 + G.oo_off + (int64_t)r * G.n + i, pol);
   return NONE;
+}
+
+// Value-array store of a result (skipped in CSR mode when nobody re-reads it).
+__device__ __forceinline__ void store_x(const sgb_group &G, int r, int64_t i, double v, double *x, int64_t ld,
+                                        int64_t b, bool csr, uint64_t pol) {
+  const bool stream = G.flags & FLAG_STREAM;
+  if (csr && stream) return;
+  double *a = x + (G.dest_base + (int64_t)r * G.n + i) * ld + b;
+  if (stream) st_stream(a, v, pol); else *a = v;
 }
 
 // Store root r of instance i: the value array (unless CSR mode and nobody
@@ -392,7 +401,105 @@ __global__ void tape_batch(Tables T, const int2 *tiles, double *X, int64_t ld, i
 }
 
 // ---- sum of products: acc = t0 + t1 + ..., t = f0 * f1 * ... (tape-free) --------------
-// Fold state across factor batches; identical to the left fold of the template.
+// Address of factor f (slot f) of instance i with slot-0 index idx0.  Coherent
+// slots are slot 0 + delta in 32-bit modular arithmetic (every address < 2^32).
+__device__ __forceinline__ uint32_t sop_addr(const Tables &T, const sgb_group &G, int f, int64_t i, uint32_t idx0,
+                                             const int32_t *s_col, const int32_t *s_del, bool coherent,
+                                             uint64_t pol) {
+  if (coherent) return idx0 + (uint32_t)s_del[f];
+  const int col = s_col[f];
+  if (col < 0) return idx0 + (uint32_t)s_del[f];
+  if (col == 0) return idx0;
+  return column_index(T, G, col, i, pol);
+}
+
+__device__ __forceinline__ double neg_if(double v, uint32_t negm, int f) {
+  return ((negm >> f) & 1u) ? -v : v;
+}
+
+// Template shapes recognised by the lowering (lower.SOP_SHAPE_*): a generic
+// sum of products (term-start mask), a plain sum (every factor is a term) and
+// a sum of two-factor products with an optional single-factor tail.  All are
+// the template's own left fold, bit for bit.
+enum : int { SHAPE_GENERIC = 0, SHAPE_SUM = 1, SHAPE_PAIRS = 2 };
+
+template <int SHAPE, int LMAX, bool NEG>
+__device__ __forceinline__ double sop_eval(const double (&v)[LMAX], int len, uint32_t newterm, uint32_t negm) {
+  if (SHAPE == SHAPE_SUM) {
+    double acc = NEG ? neg_if(v[0], negm, 0) : v[0];
+#pragma unroll
+    for (int f = 1; f < LMAX; ++f)
+      if (f < len) acc = __dadd_rn(acc, NEG ? neg_if(v[f], negm, f) : v[f]);
+    return acc;
+  } else if (SHAPE == SHAPE_PAIRS) {
+    double acc = __dmul_rn(NEG ? neg_if(v[0], negm, 0) : v[0], NEG ? neg_if(v[1], negm, 1) : v[1]);
+#pragma unroll
+    for (int f = 2; f + 1 < LMAX; f += 2)
+      if (f + 1 < len)
+        acc = __dadd_rn(acc, __dmul_rn(NEG ? neg_if(v[f], negm, f) : v[f], NEG ? neg_if(v[f + 1], negm, f + 1) : v[f + 1]));
+    if (len & 1) {  // single-factor tail (e.g. "+ A_ij")
+#pragma unroll
+      for (int f = 2; f < LMAX; f += 2)
+        if (f == len - 1) acc = __dadd_rn(acc, NEG ? neg_if(v[f], negm, f) : v[f]);
+    }
+    return acc;
+  } else {
+    double acc = 0.0, term = 0.0;
+    bool have = false;
+#pragma unroll
+    for (int f = 0; f < LMAX; ++f) {
+      if (f < len) {
+        const double val = neg_if(v[f], negm, f);
+        if ((newterm >> f) & 1u) {
+          if (f > 0) {
+            acc = have ? __dadd_rn(acc, term) : term;
+            have = true;
+          }
+          term = val;
+        } else {
+          term = __dmul_rn(term, val);
+        }
+      }
+    }
+    return have ? __dadd_rn(acc, term) : term;
+  }
+}
+
+// VEC instances per thread (i0 + v*SOP_BS): index, output-position and value
+// loads of all VEC instances are issued before the first fold.
+template <int SHAPE, int LMAX, int VEC>
+__device__ __forceinline__ void sop_tile(const Tables &T, const sgb_group &G, int64_t i0, double *x, double *out,
+                                         bool csr, const int32_t *s_col, const int32_t *s_del, uint64_t pol) {
+  const uint32_t newterm = __ldg(T.sop + 2 * G.sop_off), negm = __ldg(T.sop + 2 * G.sop_off + 1);
+  const int len = G.sop_len;
+  const bool coherent = G.flags & FLAG_COHERENT;
+  int64_t iv[VEC];
+  uint32_t idx0[VEC], op[VEC];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    iv[v] = min(i0 + (int64_t)v * SOP_BS, G.n - 1);
+    idx0[v] = column_index(T, G, 0, iv[v], pol);
+    op[v] = csr ? out_pos(T, G, 0, iv[v], pol) : NONE;
+  }
+  double val[VEC][LMAX];
+#pragma unroll
+  for (int v = 0; v < VEC; ++v)
+#pragma unroll
+    for (int f = 0; f < LMAX; ++f)
+      if (f < len) val[v][f] = __ldg(x + sop_addr(T, G, f, iv[v], idx0[v], s_col, s_del, coherent, pol));
+#pragma unroll
+  for (int v = 0; v < VEC; ++v) {
+    const int64_t i = i0 + (int64_t)v * SOP_BS;
+    if (i < G.n) {
+      const double r = negm ? sop_eval<SHAPE, LMAX, true>(val[v], len, newterm, negm)
+                            : sop_eval<SHAPE, LMAX, false>(val[v], len, newterm, negm);
+      store_x(G, 0, i, r, x, 1, 0, csr, pol);
+      if (op[v] != NONE) out[op[v]] = r;
+    }
+  }
+}
+
+// Wide templates (> 16 factors): factor batches of SOP_BATCH keep registers bounded.
 struct SopFold {
   double acc, term;
   bool have;
@@ -405,7 +512,7 @@ __device__ __forceinline__ void sop_fold(SopFold &st, int f0, int len, uint32_t 
   for (int u = 0; u < NB; ++u) {
     const int f = f0 + u;
     if (f < len) {
-      const double val = ((negm >> f) & 1u) ? -v[u] : v[u];
+      const double val = neg_if(v[u], negm, f);
       if ((newterm >> f) & 1u) {
         if (f > 0) {
           st.acc = st.have ? __dadd_rn(st.acc, st.term) : st.term;
@@ -419,82 +526,62 @@ __device__ __forceinline__ void sop_fold(SopFold &st, int f0, int len, uint32_t 
   }
 }
 
-// Address of factor f (slot f) of instance i with slot-0 index idx0.
-__device__ __forceinline__ int64_t sop_addr(const Tables &T, const sgb_group &G, int f, int64_t i, uint32_t idx0,
-                                            const int32_t *s_col, const int64_t *s_del, bool coherent,
-                                            uint64_t pol) {
-  if (coherent) return (int64_t)idx0 + s_del[f];
-  const int col = s_col[f];
-  if (col < 0) return (int64_t)idx0 + s_del[f];
-  if (col == 0) return idx0;
-  return column_index(T, G, col, i, pol);
-}
-
-// VEC instances per thread (i0 + v*SOP_BS), factors in batches of NB: VEC x NB
-// independent gathers in flight.
-template <int LMAX, int VEC>
-__device__ __forceinline__ void sop_tile(const Tables &T, const sgb_group &G, int64_t i0, double *x, double *out,
-                                         bool csr, const int32_t *s_col, const int64_t *s_del, uint64_t pol) {
-  constexpr int NB = LMAX < SOP_BATCH ? LMAX : SOP_BATCH;
+__device__ __forceinline__ void sop_tile_wide(const Tables &T, const sgb_group &G, int64_t i, double *x, double *out,
+                                              bool csr, const int32_t *s_col, const int32_t *s_del, uint64_t pol) {
   const uint32_t newterm = __ldg(T.sop + 2 * G.sop_off), negm = __ldg(T.sop + 2 * G.sop_off + 1);
   const int len = G.sop_len;
   const bool coherent = G.flags & FLAG_COHERENT;
-  int64_t iv[VEC];
-  uint32_t idx0[VEC];
+  const uint32_t idx0 = column_index(T, G, 0, i, pol);
+  const uint32_t op = csr ? out_pos(T, G, 0, i, pol) : NONE;
+  SopFold st{0.0, 0.0, false};
 #pragma unroll
-  for (int v = 0; v < VEC; ++v) {
-    iv[v] = min(i0 + (int64_t)v * SOP_BS, G.n - 1);
-    idx0[v] = column_index(T, G, 0, iv[v], pol);
-  }
-  SopFold st[VEC];
-#pragma unroll
-  for (int v = 0; v < VEC; ++v) st[v] = SopFold{0.0, 0.0, false};
-#pragma unroll
-  for (int f0 = 0; f0 < LMAX; f0 += NB) {
+  for (int f0 = 0; f0 < 32; f0 += SOP_BATCH) {
     if (f0 < len) {
-      double val[VEC][NB];
+      double val[SOP_BATCH];
 #pragma unroll
-      for (int v = 0; v < VEC; ++v)
-#pragma unroll
-        for (int u = 0; u < NB; ++u)
-          if (f0 + u < len) val[v][u] = __ldg(x + sop_addr(T, G, f0 + u, iv[v], idx0[v], s_col, s_del, coherent, pol));
-#pragma unroll
-      for (int v = 0; v < VEC; ++v) sop_fold<NB>(st[v], f0, len, newterm, negm, val[v]);
+      for (int u = 0; u < SOP_BATCH; ++u)
+        if (f0 + u < len) val[u] = __ldg(x + sop_addr(T, G, f0 + u, i, idx0, s_col, s_del, coherent, pol));
+      sop_fold<SOP_BATCH>(st, f0, len, newterm, negm, val);
     }
   }
-#pragma unroll
-  for (int v = 0; v < VEC; ++v) {
-    const int64_t i = i0 + (int64_t)v * SOP_BS;
-    if (i < G.n) {
-      const double r = st[v].have ? __dadd_rn(st[v].acc, st[v].term) : st[v].term;
-      store_root(T, G, 0, i, r, x, 1, 0, out, 1, csr, pol);
-    }
+  const double r = st.have ? __dadd_rn(st.acc, st.term) : st.term;
+  store_x(G, 0, i, r, x, 1, 0, csr, pol);
+  if (op != NONE) out[op] = r;
+}
+
+template <int SHAPE>
+__device__ __forceinline__ void sop_dispatch(const Tables &T, const sgb_group &G, int64_t i0, double *x, double *out,
+                                             bool csr, const int32_t *s_col, const int32_t *s_del, uint64_t pol) {
+  switch (G.variant) {
+    case 0: sop_tile<SHAPE, 2, sop_vec(0)>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
+    case 1: sop_tile<SHAPE, 4, sop_vec(1)>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
+    case 2: sop_tile<SHAPE, 8, sop_vec(2)>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
+    case 3: sop_tile<SHAPE, 16, sop_vec(3)>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
+    default: sop_tile_wide(T, G, i0, x, out, csr, s_col, s_del, pol); break;
   }
 }
 
-// One launch per wave for every sum-of-products group; the tile's width class
-// picks the unrolled body (block-uniform switch).
-__global__ void __launch_bounds__(SOP_BS, 4) sop_single(Tables T, const int2 *tiles, double *x, double *out,
+// One launch per wave for every sum-of-products group; the tile's shape and
+// width class pick the unrolled body (block-uniform switch).
+__global__ void __launch_bounds__(SOP_BS, 3) sop_single(Tables T, const int2 *tiles, double *x, double *out,
                                                        int csr) {
   __shared__ int32_t s_col[32];
-  __shared__ int64_t s_del[32];
+  __shared__ int32_t s_del[32];
   const int2 tl = tiles[blockIdx.x];
   const sgb_group G = T.groups[tl.x];
   if (!csr && (G.flags & FLAG_CSR_ONLY)) return;
   if (threadIdx.x < G.n_slots) {
     s_col[threadIdx.x] = __ldg(T.slot_col + G.slot_off + threadIdx.x);
-    s_del[threadIdx.x] = __ldg(T.slot_delta + G.slot_off + threadIdx.x);
+    s_del[threadIdx.x] = (int32_t)__ldg(T.slot_delta + G.slot_off + threadIdx.x);
   }
   __syncthreads();
   const uint64_t pol = evict_first_policy();
   const int64_t i0 = (int64_t)tl.y + threadIdx.x;
   if (i0 >= G.n) return;
-  switch (G.variant) {
-    case 0: sop_tile<2, sop_vec(0)>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
-    case 1: sop_tile<4, sop_vec(1)>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
-    case 2: sop_tile<8, sop_vec(2)>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
-    case 3: sop_tile<16, sop_vec(3)>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
-    default: sop_tile<32, sop_vec(4)>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
+  switch (G.shape) {
+    case SHAPE_SUM: sop_dispatch<SHAPE_SUM>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
+    case SHAPE_PAIRS: sop_dispatch<SHAPE_PAIRS>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
+    default: sop_dispatch<SHAPE_GENERIC>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
   }
 }
 
@@ -502,16 +589,17 @@ __global__ void __launch_bounds__(SOP_BS, 4) sop_single(Tables T, const int2 *ti
 template <int LMAX>
 __device__ __forceinline__ void sop_batch_body(const Tables &T, const sgb_group &G, int64_t i, int lane, double *X,
                                                int64_t ld, int64_t batch, double *out, int64_t ld_out, bool csr,
-                                               const int32_t *s_col, const int64_t *s_del, uint64_t pol) {
+                                               const int32_t *s_col, const int32_t *s_del, uint64_t pol) {
   constexpr int NB = LMAX < 8 ? LMAX : 8;
   const uint32_t newterm = __ldg(T.sop + 2 * G.sop_off), negm = __ldg(T.sop + 2 * G.sop_off + 1);
   const bool coherent = G.flags & FLAG_COHERENT;
   const int len = G.sop_len;
   const uint32_t idx0 = column_index(T, G, 0, i, pol);
+  const uint32_t op = csr ? out_pos(T, G, 0, i, pol) : NONE;
   uint32_t addr[LMAX];
 #pragma unroll
   for (int f = 0; f < LMAX; ++f)
-    if (f < len) addr[f] = (uint32_t)sop_addr(T, G, f, i, idx0, s_col, s_del, coherent, pol);
+    if (f < len) addr[f] = sop_addr(T, G, f, i, idx0, s_col, s_del, coherent, pol);
   for (int64_t b = lane; b < batch; b += 32) {
     SopFold st{0.0, 0.0, false};
 #pragma unroll
@@ -525,20 +613,21 @@ __device__ __forceinline__ void sop_batch_body(const Tables &T, const sgb_group 
       }
     }
     const double r = st.have ? __dadd_rn(st.acc, st.term) : st.term;
-    store_root(T, G, 0, i, r, X, ld, b, out, ld_out, csr, pol);
+    store_x(G, 0, i, r, X, ld, b, csr, pol);
+    if (op != NONE) out[(int64_t)op * ld_out + b] = r;
   }
 }
 
 __global__ void __launch_bounds__(BATCH_WARPS * 32) sop_batch(Tables T, const int2 *tiles, double *X, int64_t ld,
                                                              int64_t batch, double *out, int64_t ld_out, int csr) {
   __shared__ int32_t s_col[32];
-  __shared__ int64_t s_del[32];
+  __shared__ int32_t s_del[32];
   const int2 tl = tiles[blockIdx.x];
   const sgb_group G = T.groups[tl.x];
   if (!csr && (G.flags & FLAG_CSR_ONLY)) return;
   if (threadIdx.x < G.n_slots) {
     s_col[threadIdx.x] = __ldg(T.slot_col + G.slot_off + threadIdx.x);
-    s_del[threadIdx.x] = __ldg(T.slot_delta + G.slot_off + threadIdx.x);
+    s_del[threadIdx.x] = (int32_t)__ldg(T.slot_delta + G.slot_off + threadIdx.x);
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -741,6 +830,7 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
         (G.n_slots > 0 && G.n_ret < 1) ||
         (G.kind == KIND_SOP && (G.sop_len < 1 || G.sop_len > 32 || G.sop_len != G.n_slots ||
                                 2 * (int64_t)G.sop_off + 2 > d->n_sop || G.variant < 0 || G.variant > 4 ||
+                                G.shape < 0 || G.shape > 2 ||
                                 G.sop_len > sop_lmax(G.variant) || G.n_roots != 1)) ||
         ((G.flags & FLAG_W16) && (G.cb_off < 0 || G.co_off < 0 || G.cb_off + (int64_t)G.n_ret * nch > d->n_cbase ||
                                   G.co_off + (int64_t)G.n_ret * G.n > d->n_coff)) ||

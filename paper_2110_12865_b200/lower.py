@@ -63,7 +63,7 @@ GROUP_DTYPE = np.dtype([
     ("n_roots", "<i4"), ("n_slots", "<i4"), ("n_ret", "<i4"), ("n_const", "<i4"),
     ("tape_len", "<i4"), ("n_regs", "<i4"), ("kind", "<i4"), ("flags", "<i4"),
     ("slot_off", "<i4"), ("sop_off", "<i4"), ("sop_len", "<i4"), ("unit", "<i4"),
-    ("variant", "<i4"), ("reserved", "<i4"),
+    ("variant", "<i4"), ("shape", "<i4"),
 ])
 
 # one row per launch unit (int64 x 10), mirrored by csrc U_*
@@ -528,7 +528,21 @@ def sop_class(width: int) -> int:
 
 def sop_vec(cls: int) -> int:
     """Instances per thread of the sum-of-products kernel (csrc sop_vec)."""
-    return 4 if cls <= 1 else (2 if cls == 2 else 1)
+    return (8, 4, 2, 1, 1)[cls]
+
+
+SOP_SHAPE_GENERIC, SOP_SHAPE_SUM, SOP_SHAPE_PAIRS = 0, 1, 2
+
+
+def sop_shape(desc) -> int:
+    """Kernel shape of a sum-of-products descriptor (csrc SHAPE_*); arithmetic is identical."""
+    starts = [bool(d & SOP_NEWTERM) for d in np.asarray(desc).tolist()]
+    n = len(starts)
+    if all(starts):
+        return SOP_SHAPE_SUM
+    if n >= 2 and all(starts[f] == (f % 2 == 0) for f in range(n - (n & 1))) and (n % 2 == 0 or starts[-1]):
+        return SOP_SHAPE_PAIRS
+    return SOP_SHAPE_GENERIC
 
 
 def block_size_for(n_regs: int) -> int:
@@ -790,6 +804,7 @@ def lower_plan(plan, compress: bool | None = None) -> DevicePlanArrays:
                 else:
                     cls = sop_class(len(g.sop))
                     rec["variant"], rec["sop_off"], rec["sop_len"] = cls, n_sop, len(g.sop)
+                    rec["shape"] = sop_shape(g.sop)
                     newterm = sum(1 << f for f, d in enumerate(g.sop.tolist()) if d & SOP_NEWTERM)
                     neg = sum(1 << f for f, d in enumerate(g.sop.tolist()) if d & SOP_NEG)
                     sops.append(np.array([newterm, neg], np.uint32))

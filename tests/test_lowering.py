@@ -93,3 +93,13 @@ def test_tape_register_reuse_bounded():
         if kl.kind == KIND_TAPE:
             live = len(kp.template_arena.ops)
             assert kl.n_regs <= live + len(kp.pos_vars) + len(kp.const_vars)
+
+
+def test_sop_shapes():
+    N, NEG = L.SOP_NEWTERM, L.SOP_NEG
+    assert L.sop_shape([N, N | NEG, N]) == L.SOP_SHAPE_SUM
+    assert L.sop_shape([N, 0, N, 0]) == L.SOP_SHAPE_PAIRS
+    assert L.sop_shape([N, 0, N | NEG, 0, N]) == L.SOP_SHAPE_PAIRS  # two products + single tail
+    assert L.sop_shape([N, 0, 0]) == L.SOP_SHAPE_GENERIC  # one three-factor product
+    assert L.sop_shape([N, 0, N]) == L.SOP_SHAPE_PAIRS
+    assert L.sop_shape([N, N, 0]) == L.SOP_SHAPE_GENERIC

@@ -1,4 +1,4 @@
-"""Time every launch of one evaluation for builder / lowering variants (dev tool)."""
+"""Time every CSR-mode launch of one evaluation for lowering variants (dev tool, not the bench)."""
 import os
 import sys
 import time
@@ -6,53 +6,49 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
+import argparse  # noqa: E402
+
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
+import bench  # noqa: E402
 from paper_2110_12865_b200 import DevicePlan  # noqa: E402
 from paper_2110_12865_b200.lower import lower_plan  # noqa: E402
-from paper_2110_12865_b200.programs.mesh import build_lmlt_plan, lmlt_inputs  # noqa: E402
+from paper_2110_12865_b200.programs.mesh import lmlt_inputs  # noqa: E402
 
 w = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
+variants = sys.argv[2].split(",") if len(sys.argv) > 2 else ["vec=0"]
+key, plan, _, _ = bench.build_workload(argparse.Namespace(w=w), 0, 1)
 inputs = lmlt_inputs(w)
 ref = None
-for split in ("0",):
-    os.environ["SGB_SPLIT"] = split
+for var in variants:
+    env = dict(kv.split("=") for kv in var.split(";") if kv)
+    os.environ["SGB_TAPE_VEC"] = env.get("vec", "0")
+    os.environ["SGB_COMPRESS"] = env.get("compress", "1")
     t0 = time.time()
-    plan, _, _ = build_lmlt_plan(w)
-    print(f"split={split}: built in {time.time() - t0:.1f}s, {len(plan.kernels)} kernels", flush=True)
-    for comp, vec in ((True, "1"), (True, "2"), (True, "4"), (True, "0")):
-        os.environ["SGB_TAPE_VEC"] = vec
-        dp = DevicePlan(plan, lowered=lower_plan(plan, compress=comp))
-        x = dp.new_values(inputs)
-        out = torch.empty(len(plan.outputs), dtype=torch.float64, device="cuda")
-        for _ in range(5):
-            dp.run_values(x)
-            dp.gather_outputs(x, out)
-        torch.cuda.synchronize()
-        got = out.cpu().numpy()
-        if ref is None:
-            ref = got
-        same = np.array_equal(got.view(np.uint64), ref.view(np.uint64))
-        R = 20
-        ev = [[torch.cuda.Event(enable_timing=True) for _ in range(dp.units + 2)] for _ in range(R)]
-        for r in range(R):
-            k = 0
-            for wv in range(dp.launches):
-                for u in range(dp.units):
-                    pass
-            # one event per wave
-            for wv in range(dp.launches):
-                ev[r][wv].record()
-                dp.run_wave(x, wv)
-            ev[r][dp.launches].record()
-            dp.gather_outputs(x, out)
-            ev[r][dp.launches + 1].record()
-        torch.cuda.synchronize()
-        per = np.zeros(dp.launches + 1)
-        for r in range(R):
-            for j in range(dp.launches + 1):
-                per[j] += ev[r][j].elapsed_time(ev[r][j + 1]) / R
-        print(f"  compress={comp} vec={vec} same={same} total={per.sum():.3f} ms waves={np.round(per, 4).tolist()} "
-              f"units={dp.units}", flush=True)
-        dp.close()
+    dp = DevicePlan(plan, lowered=lower_plan(plan))
+    x = dp.new_values(inputs)
+    out = torch.empty(len(plan.outputs), dtype=torch.float64, device="cuda")
+    for _ in range(5):
+        dp.run_csr(x, out)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()
+    if ref is None:
+        ref = got
+    same = np.array_equal(got.view(np.uint64), ref.view(np.uint64))
+    R = 20
+    nw = dp.csr_launches
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nw + 1)] for _ in range(R)]
+    for r in range(R):
+        for wv in range(nw):
+            ev[r][wv].record()
+            dp.run_wave(x, wv, out=out)
+        ev[r][nw].record()
+    torch.cuda.synchronize()
+    per = np.zeros(nw)
+    for r in range(R):
+        for j in range(nw):
+            per[j] += ev[r][j].elapsed_time(ev[r][j + 1]) / R
+    print(f"{var}: same={same} total={per.sum():.4f} ms waves={np.round(per, 4).tolist()} "
+          f"(lower+upload {time.time() - t0:.1f}s)", flush=True)
+    dp.close()
