@@ -63,7 +63,7 @@ constexpr int BATCH_WARPS = 8;
 constexpr uint32_t NONE = 0xFFFFFFFFu;
 
 // instances per thread of the sum-of-products kernel, per width class (lower.SOP_CLASSES)
-__host__ __device__ constexpr int sop_vec(int cls) { return cls == 0 ? 8 : cls == 1 ? 4 : cls == 2 ? 2 : 1; }
+__host__ __device__ constexpr int sop_vec(int cls) { return cls <= 1 ? 4 : cls == 2 ? 2 : 1; }
 __host__ __device__ constexpr int sop_lmax(int cls) { return cls == 0 ? 2 : cls == 1 ? 4 : cls == 2 ? 8 : cls == 3 ? 16 : 32; }
 
 thread_local std::string g_err;
@@ -102,22 +102,12 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
   asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
-// streaming index-table read: no L1 allocation, L2 evict-first
-__device__ __forceinline__ uint32_t ld_index(const uint32_t *a, uint64_t pol) {
-  uint32_t v;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ uint16_t ld_index16(const uint16_t *a, uint64_t pol) {
-  uint16_t v;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;" : "=h"(v) : "l"(a), "l"(pol));
-  return v;
-}
-__device__ __forceinline__ double ld_const(const double *a, uint64_t pol) {
-  double v;
-  asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
-  return v;
-}
+// streaming index-table reads (ld.global.cs: evict-first).  Real load
+// intrinsics, not asm: the compiler never speculates them past the guards that
+// keep a missing table's pointer from being dereferenced.
+__device__ __forceinline__ uint32_t ld_index(const uint32_t *a, uint64_t) { return __ldcs(a); }
+__device__ __forceinline__ uint16_t ld_index16(const uint16_t *a, uint64_t) { return __ldcs(a); }
+__device__ __forceinline__ double ld_const(const double *a, uint64_t) { return __ldcs(a); }
 __device__ __forceinline__ void st_stream(double *a, double v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
 }
@@ -342,38 +332,41 @@ __device__ __forceinline__ void tape_instance(const Tables &T, const sgb_group &
 // Single value set: lane = instance, VEC instances per lane (i0 + tid + v*BS)
 // share each decoded tape word.  Scratch file [n_regs][VEC][BS] in shared memory.
 template <int BS, int VEC>
-__global__ void __launch_bounds__(BS) tape_single(Tables T, const int2 *tiles, double *x, double *out, int csr) {
+__global__ void __launch_bounds__(BS) tape_single(Tables T, const int2 *tiles, int64_t n_tiles, double *x,
+                                                  double *out, int csr) {
   extern __shared__ double scratch[];
-  const int2 tl = tiles[blockIdx.x];
-  const sgb_group G = T.groups[tl.x];
-  if (!csr && (G.flags & FLAG_CSR_ONLY)) return;
   const uint64_t pol = evict_first_policy();
   const int tid = threadIdx.x;
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(scratch);
   constexpr uint32_t stride8 = BS * VEC * 8;
-  if (VEC == 1 && (G.flags & FLAG_SERIAL)) {  // members read other instances' results: instance order
-    if (tid != 0) return;
-    for (int64_t i = 0; i < G.n; ++i) tape_instance(T, G, base, stride8, x, 1, i, 0, out, 1, csr, pol);
-    return;
-  }
-  const int64_t i0 = (int64_t)tl.y + tid;
-  if (i0 >= G.n) return;
-  const uint32_t Rb = base + tid * 8;
-  if (VEC == 1) {
-    tape_instance(T, G, Rb, stride8, x, 1, i0, 0, out, 1, csr, pol);
-    return;
-  }
-  int64_t iv[VEC];
-  bool ok[VEC];
+  for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {  // persistent: the grid is the resident capacity
+    const int2 tl = tiles[t];
+    const sgb_group G = T.groups[tl.x];
+    if (!csr && (G.flags & FLAG_CSR_ONLY)) continue;
+    if (VEC == 1 && (G.flags & FLAG_SERIAL)) {  // members read other instances' results: instance order
+      if (tid == 0)
+        for (int64_t i = 0; i < G.n; ++i) tape_instance(T, G, base, stride8, x, 1, i, 0, out, 1, csr, pol);
+      continue;
+    }
+    const int64_t i0 = (int64_t)tl.y + tid;
+    if (i0 >= G.n) continue;
+    const uint32_t Rb = base + tid * 8;
+    if (VEC == 1) {
+      tape_instance(T, G, Rb, stride8, x, 1, i0, 0, out, 1, csr, pol);
+      continue;
+    }
+    int64_t iv[VEC];
+    bool ok[VEC];
 #pragma unroll
-  for (int v = 0; v < VEC; ++v) {
-    iv[v] = i0 + (int64_t)v * BS;
-    ok[v] = iv[v] < G.n;
-    if (!ok[v]) iv[v] = G.n - 1;  // evaluate a valid instance, store nothing
-  }
+    for (int v = 0; v < VEC; ++v) {
+      iv[v] = i0 + (int64_t)v * BS;
+      ok[v] = iv[v] < G.n;
+      if (!ok[v]) iv[v] = G.n - 1;  // evaluate a valid instance, store nothing
+    }
 #pragma unroll
-  for (int v = 0; v < VEC; ++v) load_slots(T, G, Rb + v * BS * 8, stride8, x, 1, iv[v], 0, false, pol);
-  run_tape<VEC, BS * 8>(T, G, Rb, x, 1, 0, out, 1, csr, iv, ok, 0, false, pol);
+    for (int v = 0; v < VEC; ++v) load_slots(T, G, Rb + v * BS * 8, stride8, x, 1, iv[v], 0, false, pol);
+    run_tape<VEC, BS * 8>(T, G, Rb, x, 1, 0, out, 1, csr, iv, ok, 0, false, pol);
+  }
 }
 
 // Batched: X[addr * ld + b].  A warp owns one instance and sweeps the batch, so
@@ -403,9 +396,9 @@ __global__ void tape_batch(Tables T, const int2 *tiles, double *X, int64_t ld, i
 // ---- sum of products: acc = t0 + t1 + ..., t = f0 * f1 * ... (tape-free) --------------
 // Address of factor f (slot f) of instance i with slot-0 index idx0.  Coherent
 // slots are slot 0 + delta in 32-bit modular arithmetic (every address < 2^32).
+template <class C, class D>
 __device__ __forceinline__ uint32_t sop_addr(const Tables &T, const sgb_group &G, int f, int64_t i, uint32_t idx0,
-                                             const int32_t *s_col, const int32_t *s_del, bool coherent,
-                                             uint64_t pol) {
+                                             const C &s_col, const D &s_del, bool coherent, uint64_t pol) {
   if (coherent) return idx0 + (uint32_t)s_del[f];
   const int col = s_col[f];
   if (col < 0) return idx0 + (uint32_t)s_del[f];
@@ -465,11 +458,26 @@ __device__ __forceinline__ double sop_eval(const double (&v)[LMAX], int len, uin
   }
 }
 
-// VEC instances per thread (i0 + v*SOP_BS): index, output-position and value
-// loads of all VEC instances are issued before the first fold.
+// Address of factor f of instance i: slot deltas / columns are warp-uniform
+// loads (L1 hits after the first tile of a group), issued right before use.
+__device__ __forceinline__ uint32_t factor_addr(const Tables &T, const sgb_group &G, int f, int64_t i, uint32_t idx0,
+                                                bool coherent, uint64_t pol) {
+  const uint32_t d = (uint32_t)__ldg(T.slot_delta + G.slot_off + f);
+  if (coherent) return idx0 + d;
+  const int col = __ldg(T.slot_col + G.slot_off + f);
+  if (col < 0) return idx0 + d;
+  if (col == 0) return idx0;
+  return column_index(T, G, col, i, pol);
+}
+
+// VEC instances per lane (i0 + v*32): index, output-position and value loads of
+// all VEC instances are issued before the first fold.
+// Out of line per (shape, width class): each body gets the kernel's whole
+// register budget instead of one giant inlined switch.
 template <int SHAPE, int LMAX, int VEC>
-__device__ __forceinline__ void sop_tile(const Tables &T, const sgb_group &G, int64_t i0, double *x, double *out,
-                                         bool csr, const int32_t *s_col, const int32_t *s_del, uint64_t pol) {
+__device__ __noinline__ void sop_tile(const Tables &T, int g, int64_t i0, double *x, double *out, bool csr) {
+  const uint64_t pol = evict_first_policy();
+  const sgb_group G = T.groups[g];
   const uint32_t newterm = __ldg(T.sop + 2 * G.sop_off), negm = __ldg(T.sop + 2 * G.sop_off + 1);
   const int len = G.sop_len;
   const bool coherent = G.flags & FLAG_COHERENT;
@@ -477,7 +485,7 @@ __device__ __forceinline__ void sop_tile(const Tables &T, const sgb_group &G, in
   uint32_t idx0[VEC], op[VEC];
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
-    iv[v] = min(i0 + (int64_t)v * SOP_BS, G.n - 1);
+    iv[v] = min(i0 + (int64_t)v * 32, G.n - 1);
     idx0[v] = column_index(T, G, 0, iv[v], pol);
     op[v] = csr ? out_pos(T, G, 0, iv[v], pol) : NONE;
   }
@@ -486,10 +494,10 @@ __device__ __forceinline__ void sop_tile(const Tables &T, const sgb_group &G, in
   for (int v = 0; v < VEC; ++v)
 #pragma unroll
     for (int f = 0; f < LMAX; ++f)
-      if (f < len) val[v][f] = __ldg(x + sop_addr(T, G, f, iv[v], idx0[v], s_col, s_del, coherent, pol));
+      if (f < len) val[v][f] = __ldg(x + factor_addr(T, G, f, iv[v], idx0[v], coherent, pol));
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
-    const int64_t i = i0 + (int64_t)v * SOP_BS;
+    const int64_t i = i0 + (int64_t)v * 32;
     if (i < G.n) {
       const double r = negm ? sop_eval<SHAPE, LMAX, true>(val[v], len, newterm, negm)
                             : sop_eval<SHAPE, LMAX, false>(val[v], len, newterm, negm);
@@ -526,8 +534,10 @@ __device__ __forceinline__ void sop_fold(SopFold &st, int f0, int len, uint32_t 
   }
 }
 
-__device__ __forceinline__ void sop_tile_wide(const Tables &T, const sgb_group &G, int64_t i, double *x, double *out,
-                                              bool csr, const int32_t *s_col, const int32_t *s_del, uint64_t pol) {
+__device__ __noinline__ void sop_tile_wide(const Tables &T, int g, int64_t i, double *x, double *out, bool csr) {
+  const uint64_t pol = evict_first_policy();
+  const sgb_group G = T.groups[g];
+  if (i >= G.n) return;
   const uint32_t newterm = __ldg(T.sop + 2 * G.sop_off), negm = __ldg(T.sop + 2 * G.sop_off + 1);
   const int len = G.sop_len;
   const bool coherent = G.flags & FLAG_COHERENT;
@@ -540,7 +550,7 @@ __device__ __forceinline__ void sop_tile_wide(const Tables &T, const sgb_group &
       double val[SOP_BATCH];
 #pragma unroll
       for (int u = 0; u < SOP_BATCH; ++u)
-        if (f0 + u < len) val[u] = __ldg(x + sop_addr(T, G, f0 + u, i, idx0, s_col, s_del, coherent, pol));
+        if (f0 + u < len) val[u] = __ldg(x + factor_addr(T, G, f0 + u, i, idx0, coherent, pol));
       sop_fold<SOP_BATCH>(st, f0, len, newterm, negm, val);
     }
   }
@@ -550,38 +560,41 @@ __device__ __forceinline__ void sop_tile_wide(const Tables &T, const sgb_group &
 }
 
 template <int SHAPE>
-__device__ __forceinline__ void sop_dispatch(const Tables &T, const sgb_group &G, int64_t i0, double *x, double *out,
-                                             bool csr, const int32_t *s_col, const int32_t *s_del, uint64_t pol) {
-  switch (G.variant) {
-    case 0: sop_tile<SHAPE, 2, sop_vec(0)>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
-    case 1: sop_tile<SHAPE, 4, sop_vec(1)>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
-    case 2: sop_tile<SHAPE, 8, sop_vec(2)>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
-    case 3: sop_tile<SHAPE, 16, sop_vec(3)>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
-    default: sop_tile_wide(T, G, i0, x, out, csr, s_col, s_del, pol); break;
+__device__ __forceinline__ void sop_dispatch(const Tables &T, int g, int variant, int64_t i0, double *x, double *out,
+                                             bool csr) {
+  switch (variant) {
+    case 0: sop_tile<SHAPE, 2, sop_vec(0)>(T, g, i0, x, out, csr); break;
+    case 1: sop_tile<SHAPE, 4, sop_vec(1)>(T, g, i0, x, out, csr); break;
+    case 2: sop_tile<SHAPE, 8, sop_vec(2)>(T, g, i0, x, out, csr); break;
+    case 3: sop_tile<SHAPE, 16, sop_vec(3)>(T, g, i0, x, out, csr); break;
+    default: sop_tile_wide(T, g, i0, x, out, csr); break;
   }
 }
 
-// One launch per wave for every sum-of-products group; the tile's shape and
-// width class pick the unrolled body (block-uniform switch).
-__global__ void __launch_bounds__(SOP_BS, 3) sop_single(Tables T, const int2 *tiles, double *x, double *out,
-                                                       int csr) {
-  __shared__ int32_t s_col[32];
-  __shared__ int32_t s_del[32];
-  const int2 tl = tiles[blockIdx.x];
-  const sgb_group G = T.groups[tl.x];
-  if (!csr && (G.flags & FLAG_CSR_ONLY)) return;
-  if (threadIdx.x < G.n_slots) {
-    s_col[threadIdx.x] = __ldg(T.slot_col + G.slot_off + threadIdx.x);
-    s_del[threadIdx.x] = (int32_t)__ldg(T.slot_delta + G.slot_off + threadIdx.x);
-  }
-  __syncthreads();
-  const uint64_t pol = evict_first_policy();
-  const int64_t i0 = (int64_t)tl.y + threadIdx.x;
-  if (i0 >= G.n) return;
-  switch (G.shape) {
-    case SHAPE_SUM: sop_dispatch<SHAPE_SUM>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
-    case SHAPE_PAIRS: sop_dispatch<SHAPE_PAIRS>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
-    default: sop_dispatch<SHAPE_GENERIC>(T, G, i0, x, out, csr, s_col, s_del, pol); break;
+// Persistent sum-of-products launch (one per wave): every warp walks the unit's
+// warp tiles t = warp, warp + W, ... (tiles of 32 x VEC instances in launch
+// order -- CSR order for output groups), prefetching its next tile entry.  No
+// block-level synchronisation and no per-CTA prologue: the grid is sized to
+// the resident capacity of the chip.
+__global__ void __launch_bounds__(SOP_BS, 4) sop_single(Tables T, const int2 *tiles, int64_t n_tiles, double *x,
+                                                       double *out, int csr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (t >= n_tiles) return;
+  int2 nxt = tiles[t];
+  for (; t < n_tiles; t += W) {
+    const int2 tl = nxt;
+    if (t + W < n_tiles) nxt = tiles[t + W];
+    const sgb_group *Gp = T.groups + tl.x;
+    const int flags = __ldg(&Gp->flags), shape = __ldg(&Gp->shape), variant = __ldg(&Gp->variant);
+    if (!csr && (flags & FLAG_CSR_ONLY)) continue;
+    const int64_t i0 = (int64_t)tl.y + lane;
+    switch (shape) {
+      case SHAPE_SUM: sop_dispatch<SHAPE_SUM>(T, tl.x, variant, i0, x, out, csr); break;
+      case SHAPE_PAIRS: sop_dispatch<SHAPE_PAIRS>(T, tl.x, variant, i0, x, out, csr); break;
+      default: sop_dispatch<SHAPE_GENERIC>(T, tl.x, variant, i0, x, out, csr); break;
+    }
   }
 }
 
@@ -673,6 +686,7 @@ int upload(T **dst, const T *src, int64_t n) {
 
 struct Unit {
   int wave, kind, variant, g0, g1, bs, regs, flags;
+  int64_t grid;      // single-set persistent grid (blocks)
   int64_t t0, t1;    // single-set tiles [t0, t1)
   int64_t bt0, bt1;  // batched tiles
 };
@@ -707,7 +721,7 @@ namespace {
 template <int BS, int VEC>
 void launch_tape(const sgb_plan *p, const Unit &u, double *x, double *out, bool csr, cudaStream_t s) {
   const size_t smem = (size_t)u.regs * BS * VEC * sizeof(double);
-  tape_single<BS, VEC><<<(unsigned)(u.t1 - u.t0), BS, smem, s>>>(p->T, p->d_tiles + u.t0, x, out, csr);
+  tape_single<BS, VEC><<<(unsigned)u.grid, BS, smem, s>>>(p->T, p->d_tiles + u.t0, u.t1 - u.t0, x, out, csr);
 }
 
 template <int BS>
@@ -715,6 +729,25 @@ void launch_tape_vec(const sgb_plan *p, const Unit &u, double *x, double *out, b
   if (u.variant <= 1) launch_tape<BS, 1>(p, u, x, out, csr, s);
   else if (u.variant == 2) launch_tape<BS, 2>(p, u, x, out, csr, s);
   else launch_tape<BS, 4>(p, u, x, out, csr, s);
+}
+
+template <int BS, int VEC>
+cudaError_t tape_occupancy(int regs, int *nb) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(nb, tape_single<BS, VEC>, BS, (size_t)regs * BS * VEC * 8);
+}
+
+cudaError_t tape_occupancy_any(int bs, int vec, int regs, int *nb) {
+  switch (bs * 8 + vec) {
+    case 128 * 8 + 4: return tape_occupancy<128, 4>(regs, nb);
+    case 128 * 8 + 2: return tape_occupancy<128, 2>(regs, nb);
+    case 128 * 8 + 1: return tape_occupancy<128, 1>(regs, nb);
+    case 64 * 8 + 4: return tape_occupancy<64, 4>(regs, nb);
+    case 64 * 8 + 2: return tape_occupancy<64, 2>(regs, nb);
+    case 64 * 8 + 1: return tape_occupancy<64, 1>(regs, nb);
+    case 32 * 8 + 4: return tape_occupancy<32, 4>(regs, nb);
+    case 32 * 8 + 2: return tape_occupancy<32, 2>(regs, nb);
+    default: return tape_occupancy<32, 1>(regs, nb);
+  }
 }
 
 void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_t batch, bool batched, double *out,
@@ -738,7 +771,7 @@ void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_
     sop_batch<<<(unsigned)blocks, BATCH_WARPS * 32, 0, s>>>(p->T, p->d_btiles + u.bt0, x, ld, batch, out, ld_out,
                                                             csr);
   } else {
-    sop_single<<<(unsigned)blocks, SOP_BS, 0, s>>>(p->T, p->d_tiles + u.t0, x, out, csr);
+    sop_single<<<(unsigned)u.grid, SOP_BS, 0, s>>>(p->T, p->d_tiles + u.t0, u.t1 - u.t0, x, out, csr);
   }
 }
 
@@ -928,6 +961,19 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
         (int64_t)u.regs * (u.kind == KIND_TAPE ? u.bs * u.variant : 0) * 8 > smem_max)
       return fail(-1, "sgb_plan_create: bad launch unit " + std::to_string(k));
     max_wave = u.wave > max_wave ? u.wave : max_wave;
+    {  // persistent grid: resident capacity of the chip, at most one block (warp for SOP) per tile
+      int nb = 0;
+      if (u.kind == KIND_TAPE) {
+        SGB_CUDA(tape_occupancy_any(u.bs, u.variant, u.regs, &nb));
+        u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
+        if (u.grid > u.t1 - u.t0) u.grid = u.t1 - u.t0;
+      } else {
+        SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sop_single, SOP_BS, 0));
+        u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
+        const int64_t need = (u.t1 - u.t0 + SOP_BS / 32 - 1) / (SOP_BS / 32);
+        if (u.grid > need) u.grid = need;
+      }
+    }
     for (int64_t t = u.t0; t < u.t1; ++t) {  // tiles name groups of this unit and start inside them
       const int32_t *tl = d->tiles + 2 * t;
       if (tl[0] < u.g0 || tl[0] >= u.g1 || tl[1] < 0 || (int64_t)tl[1] >= d->groups[tl[0]].n)

@@ -528,7 +528,7 @@ def sop_class(width: int) -> int:
 
 def sop_vec(cls: int) -> int:
     """Instances per thread of the sum-of-products kernel (csrc sop_vec)."""
-    return (8, 4, 2, 1, 1)[cls]
+    return (4, 4, 2, 1, 1)[cls]
 
 
 SOP_SHAPE_GENERIC, SOP_SHAPE_SUM, SOP_SHAPE_PAIRS = 0, 1, 2
@@ -809,7 +809,7 @@ def lower_plan(plan, compress: bool | None = None) -> DevicePlanArrays:
                     neg = sum(1 << f for f, d in enumerate(g.sop.tolist()) if d & SOP_NEG)
                     sops.append(np.array([newterm, neg], np.uint32))
                     n_sop += 1
-                    tile = bs * sop_vec(cls)
+                    tile = 32 * sop_vec(cls)  # warp tile of the persistent kernel
                 # index columns: affine column 0, compressed columns
                 if compress and g.layout == "coalesced" and g.columns:
                     aff = affine_column0(g.columns[0])

@@ -138,7 +138,7 @@ def check_tiles(dp):
                 assert starts.tolist() == ([0] if n else [])
                 continue
             if g["kind"] == L.KIND_SOP:
-                tile = L.SOP_BLOCK * L.sop_vec(int(g["variant"]))
+                tile = 32 * L.sop_vec(int(g["variant"]))
             else:
                 tile = unit["block_size"] * unit["variant"]
             assert starts.tolist() == list(range(0, n, tile)), (u, gi)
