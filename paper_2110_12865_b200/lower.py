@@ -851,7 +851,8 @@ def lower_plan(plan, compress: bool | None = None) -> DevicePlanArrays:
                 unit_keys.append(_tile_keys(g, starts, tile))
             t = np.concatenate(unit_tiles) if unit_tiles else np.zeros((0, 2), np.int64)
             keys = np.concatenate(unit_keys) if unit_keys else np.zeros(0, np.int64)
-            if np.any(keys >= 0):  # CSR-ordered schedule: partial sectors of the output merge in L2
+            if np.any(keys >= 0) and os.environ.get("SGB_TILE_ORDER", "csr") == "csr":
+                # CSR-ordered schedule: partial sectors of the output merge in L2
                 t = t[np.argsort(keys, kind="stable")]
             t0 = sum(len(x) for x in tiles_all)
             tiles_all.append(t)

@@ -25,6 +25,8 @@ for var in variants:
     env = dict(kv.split("=") for kv in var.split(";") if kv)
     os.environ["SGB_TAPE_VEC"] = env.get("vec", "0")
     os.environ["SGB_COMPRESS"] = env.get("compress", "1")
+    os.environ["SGB_TILE_ORDER"] = env.get("order", "csr")
+    mode = env.get("mode", "csr")
     t0 = time.time()
     dp = DevicePlan(plan, lowered=lower_plan(plan))
     x = dp.new_values(inputs)
@@ -37,12 +39,12 @@ for var in variants:
         ref = got
     same = np.array_equal(got.view(np.uint64), ref.view(np.uint64))
     R = 20
-    nw = dp.csr_launches
+    nw = dp.csr_launches if mode == "csr" else dp.launches
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(nw + 1)] for _ in range(R)]
     for r in range(R):
         for wv in range(nw):
             ev[r][wv].record()
-            dp.run_wave(x, wv, out=out)
+            dp.run_wave(x, wv, out=out if mode == "csr" else None)
         ev[r][nw].record()
     torch.cuda.synchronize()
     per = np.zeros(nw)
