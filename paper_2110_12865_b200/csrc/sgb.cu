@@ -94,6 +94,7 @@ struct Tables {
   const uint32_t *obase;  // output positions: per (root, chunk) base
   const uint16_t *ooff;   //                   per (root, instance) offset, 0xFFFF = not an output
   const uint32_t *opos32; //                   wide form, NONE = not an output
+  const uint32_t *fbase;  // sum-of-products fast path: per-factor base address
 };
 
 // ---- cache-policy helpers ---------------------------------------------------------
@@ -470,44 +471,79 @@ __device__ __forceinline__ uint32_t factor_addr(const Tables &T, const sgb_group
   return column_index(T, G, col, i, pol);
 }
 
-// VEC instances per lane (i0 + v*32): index, output-position and value loads of
-// all VEC instances are issued before the first fold.
-// Out of line per (shape, width class): each body gets the kernel's whole
-// register budget instead of one giant inlined switch.
+// Compact per-group descriptor of the single-set sum-of-products kernel (48 B,
+// built by sgb_plan_create from the group records): everything a warp needs per
+// tile in three uniform 16-byte loads.
+struct __align__(16) SopDesc {
+  int32_t n;
+  uint32_t dest_base;
+  uint32_t meta;  // len | shape << 6 | variant << 8 | fast << 11 | csr_only << 12 | stream << 13 |
+                  // opos16 << 14 | opos32 << 15
+  int32_t stride; // fast path: factor f of instance i is at fbase[f] + stride * i
+  uint32_t newterm, negm;
+  uint32_t fbase_off;  // fast path: first factor base in Tables::fbase
+  int32_t g;           // group record (generic path)
+  uint32_t ob_off, oo_off;
+  uint32_t pad0, pad1;
+};
+enum : uint32_t {
+  M_FAST = 1u << 11, M_CSR_ONLY = 1u << 12, M_STREAM = 1u << 13, M_OPOS16 = 1u << 14, M_OPOS32 = 1u << 15
+};
+
+__device__ __forceinline__ uint32_t desc_out_pos(const Tables &T, const SopDesc &d, uint32_t i) {
+  if (d.meta & M_OPOS16) {
+    const uint16_t off = __ldcs(T.ooff + d.oo_off + i);
+    return off == 0xFFFFu ? NONE : __ldg(T.obase + d.ob_off + (i >> 5)) + off;
+  }
+  if (d.meta & M_OPOS32) return __ldcs(T.opos32 + d.oo_off + i);
+  return NONE;
+}
+
+__device__ __forceinline__ void desc_store(const SopDesc &d, uint32_t i, uint32_t op, double r, double *x,
+                                           double *out, bool csr, uint64_t pol) {
+  if (!(csr && (d.meta & M_STREAM))) {
+    double *a = x + (d.dest_base + (uint64_t)i);
+    if (d.meta & M_STREAM) st_stream(a, r, pol); else *a = r;
+  }
+  if (op != NONE) out[op] = r;
+}
+
+// Fast path (affine column 0, every slot coherent): VEC instances per lane
+// (i0 + v*32); output-position and value loads of all VEC instances are issued
+// before the first fold.
 template <int SHAPE, int LMAX, int VEC>
-__device__ __noinline__ void sop_tile(const Tables &T, int g, int64_t i0, double *x, double *out, bool csr) {
-  const uint64_t pol = evict_first_policy();
-  const sgb_group G = T.groups[g];
-  const uint32_t newterm = __ldg(T.sop + 2 * G.sop_off), negm = __ldg(T.sop + 2 * G.sop_off + 1);
-  const int len = G.sop_len;
-  const bool coherent = G.flags & FLAG_COHERENT;
-  int64_t iv[VEC];
-  uint32_t idx0[VEC], op[VEC];
+__device__ __forceinline__ void sop_fast(const Tables &T, const SopDesc &d, uint32_t i0, double *x, double *out,
+                                         bool csr, uint64_t pol) {
+  const int len = d.meta & 63u;
+  uint32_t fb[LMAX];
+#pragma unroll
+  for (int f = 0; f < LMAX; ++f) fb[f] = f < len ? __ldg(T.fbase + d.fbase_off + f) : 0u;
+  uint32_t iv[VEC], op[VEC];
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
-    iv[v] = min(i0 + (int64_t)v * 32, G.n - 1);
-    idx0[v] = column_index(T, G, 0, iv[v], pol);
-    op[v] = csr ? out_pos(T, G, 0, iv[v], pol) : NONE;
+    iv[v] = min(i0 + (uint32_t)(v * 32), (uint32_t)d.n - 1u);
+    op[v] = csr ? desc_out_pos(T, d, iv[v]) : NONE;
   }
   double val[VEC][LMAX];
 #pragma unroll
-  for (int v = 0; v < VEC; ++v)
+  for (int v = 0; v < VEC; ++v) {
+    const uint32_t off = (uint32_t)d.stride * iv[v];
 #pragma unroll
     for (int f = 0; f < LMAX; ++f)
-      if (f < len) val[v][f] = __ldg(x + factor_addr(T, G, f, iv[v], idx0[v], coherent, pol));
+      if (f < len) val[v][f] = __ldg(x + (fb[f] + off));
+  }
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
-    const int64_t i = i0 + (int64_t)v * 32;
-    if (i < G.n) {
-      const double r = negm ? sop_eval<SHAPE, LMAX, true>(val[v], len, newterm, negm)
-                            : sop_eval<SHAPE, LMAX, false>(val[v], len, newterm, negm);
-      store_x(G, 0, i, r, x, 1, 0, csr, pol);
-      if (op[v] != NONE) out[op[v]] = r;
+    const uint32_t i = i0 + (uint32_t)(v * 32);
+    if (i < (uint32_t)d.n) {
+      const double r = d.negm ? sop_eval<SHAPE, LMAX, true>(val[v], len, d.newterm, d.negm)
+                              : sop_eval<SHAPE, LMAX, false>(val[v], len, d.newterm, d.negm);
+      desc_store(d, i, op[v], r, x, out, csr, pol);
     }
   }
 }
 
-// Wide templates (> 16 factors): factor batches of SOP_BATCH keep registers bounded.
+// Wide templates and the general index forms: factor batches of SOP_BATCH.
 struct SopFold {
   double acc, term;
   bool have;
@@ -534,67 +570,90 @@ __device__ __forceinline__ void sop_fold(SopFold &st, int f0, int len, uint32_t 
   }
 }
 
-__device__ __noinline__ void sop_tile_wide(const Tables &T, int g, int64_t i, double *x, double *out, bool csr) {
+// General path: any index form (u32 table, compressed, interleaved, per-slot
+// columns), one instance per lane, out of line so the fast bodies keep their
+// registers.
+__device__ __noinline__ void sop_general(const Tables &T, const SopDesc &d, uint32_t i, double *x, double *out,
+                                         bool csr) {
+  if (i >= (uint32_t)d.n) return;
   const uint64_t pol = evict_first_policy();
-  const sgb_group G = T.groups[g];
-  if (i >= G.n) return;
-  const uint32_t newterm = __ldg(T.sop + 2 * G.sop_off), negm = __ldg(T.sop + 2 * G.sop_off + 1);
-  const int len = G.sop_len;
+  const sgb_group G = T.groups[d.g];
+  const int len = d.meta & 63u;
   const bool coherent = G.flags & FLAG_COHERENT;
   const uint32_t idx0 = column_index(T, G, 0, i, pol);
-  const uint32_t op = csr ? out_pos(T, G, 0, i, pol) : NONE;
+  const uint32_t op = csr ? desc_out_pos(T, d, i) : NONE;
   SopFold st{0.0, 0.0, false};
+#pragma unroll 1
+  for (int f0 = 0; f0 < len; f0 += 8) {
+    double val[8];
 #pragma unroll
-  for (int f0 = 0; f0 < 32; f0 += SOP_BATCH) {
-    if (f0 < len) {
-      double val[SOP_BATCH];
-#pragma unroll
-      for (int u = 0; u < SOP_BATCH; ++u)
-        if (f0 + u < len) val[u] = __ldg(x + factor_addr(T, G, f0 + u, i, idx0, coherent, pol));
-      sop_fold<SOP_BATCH>(st, f0, len, newterm, negm, val);
-    }
+    for (int u = 0; u < 8; ++u)
+      if (f0 + u < len) val[u] = __ldg(x + factor_addr(T, G, f0 + u, i, idx0, coherent, pol));
+    sop_fold<8>(st, f0, len, d.newterm, d.negm, val);
   }
   const double r = st.have ? __dadd_rn(st.acc, st.term) : st.term;
-  store_x(G, 0, i, r, x, 1, 0, csr, pol);
-  if (op != NONE) out[op] = r;
+  desc_store(d, i, op, r, x, out, csr, pol);
 }
 
-template <int SHAPE>
-__device__ __forceinline__ void sop_dispatch(const Tables &T, int g, int variant, int64_t i0, double *x, double *out,
-                                             bool csr) {
-  switch (variant) {
-    case 0: sop_tile<SHAPE, 2, sop_vec(0)>(T, g, i0, x, out, csr); break;
-    case 1: sop_tile<SHAPE, 4, sop_vec(1)>(T, g, i0, x, out, csr); break;
-    case 2: sop_tile<SHAPE, 8, sop_vec(2)>(T, g, i0, x, out, csr); break;
-    case 3: sop_tile<SHAPE, 16, sop_vec(3)>(T, g, i0, x, out, csr); break;
-    default: sop_tile_wide(T, g, i0, x, out, csr); break;
-  }
-}
-
-// Persistent sum-of-products launch (one per wave): every warp walks the unit's
-// warp tiles t = warp, warp + W, ... (tiles of 32 x VEC instances in launch
-// order -- CSR order for output groups), prefetching its next tile entry.  No
-// block-level synchronisation and no per-CTA prologue: the grid is sized to
-// the resident capacity of the chip.
-__global__ void __launch_bounds__(SOP_BS, 4) sop_single(Tables T, const int2 *tiles, int64_t n_tiles, double *x,
-                                                       double *out, int csr) {
-  const int lane = threadIdx.x & 31;
+// Persistent sum-of-products launches: one kernel per (shape, width class) of
+// the fast path plus one for the general index forms, so every body gets its
+// own register allocation.  Every warp walks its unit's warp tiles t = warp,
+// warp + W, ... (tiles of 32 x VEC instances in launch order -- CSR order for
+// output groups), prefetching its next tile entry; no block synchronisation and
+// no per-CTA prologue, the grid is the resident capacity of the chip.
+template <int SHAPE, int LMAX, int VEC>
+__global__ void __launch_bounds__(SOP_BS, 4) sop_fast_unit(Tables T, const SopDesc *D, const int2 *tiles,
+                                                          int64_t n_tiles, double *x, double *out, int csr) {
+  const uint32_t lane = threadIdx.x & 31;
   const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
   int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (t >= n_tiles) return;
+  const uint64_t pol = evict_first_policy();
   int2 nxt = tiles[t];
   for (; t < n_tiles; t += W) {
     const int2 tl = nxt;
     if (t + W < n_tiles) nxt = tiles[t + W];
-    const sgb_group *Gp = T.groups + tl.x;
-    const int flags = __ldg(&Gp->flags), shape = __ldg(&Gp->shape), variant = __ldg(&Gp->variant);
-    if (!csr && (flags & FLAG_CSR_ONLY)) continue;
-    const int64_t i0 = (int64_t)tl.y + lane;
-    switch (shape) {
-      case SHAPE_SUM: sop_dispatch<SHAPE_SUM>(T, tl.x, variant, i0, x, out, csr); break;
-      case SHAPE_PAIRS: sop_dispatch<SHAPE_PAIRS>(T, tl.x, variant, i0, x, out, csr); break;
-      default: sop_dispatch<SHAPE_GENERIC>(T, tl.x, variant, i0, x, out, csr); break;
-    }
+    const SopDesc d = D[tl.x];
+    if (!csr && (d.meta & M_CSR_ONLY)) continue;
+    sop_fast<SHAPE, LMAX, VEC>(T, d, (uint32_t)tl.y + lane, x, out, csr, pol);
+  }
+}
+
+__global__ void __launch_bounds__(SOP_BS, 4) sop_general_unit(Tables T, const SopDesc *D, const int2 *tiles,
+                                                             int64_t n_tiles, double *x, double *out, int csr) {
+  const uint32_t lane = threadIdx.x & 31;
+  const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n_tiles; t += W) {
+    const int2 tl = tiles[t];
+    const SopDesc d = D[tl.x];
+    if (!csr && (d.meta & M_CSR_ONLY)) continue;
+    const int vec = sop_vec((d.meta >> 8) & 7u);
+    for (int v = 0; v < vec; ++v) sop_general(T, d, (uint32_t)tl.y + lane + 32u * v, x, out, csr);
+  }
+}
+
+// unit variant codes (lower.sop_unit_code): fast path = shape * 8 + width class, general = 64
+constexpr int SOP_GENERAL_CODE = 64;
+
+#define SGB_SOP_KERNEL(SH, CLS) sop_fast_unit<SH, sop_lmax(CLS), sop_vec(CLS)>
+typedef void (*sop_kernel_t)(Tables, const SopDesc *, const int2 *, int64_t, double *, double *, int);
+
+__host__ sop_kernel_t sop_kernel_for(int code) {
+  switch (code) {
+    case SHAPE_GENERIC * 8 + 0: return SGB_SOP_KERNEL(SHAPE_GENERIC, 0);
+    case SHAPE_GENERIC * 8 + 1: return SGB_SOP_KERNEL(SHAPE_GENERIC, 1);
+    case SHAPE_GENERIC * 8 + 2: return SGB_SOP_KERNEL(SHAPE_GENERIC, 2);
+    case SHAPE_GENERIC * 8 + 3: return SGB_SOP_KERNEL(SHAPE_GENERIC, 3);
+    case SHAPE_SUM * 8 + 0: return SGB_SOP_KERNEL(SHAPE_SUM, 0);
+    case SHAPE_SUM * 8 + 1: return SGB_SOP_KERNEL(SHAPE_SUM, 1);
+    case SHAPE_SUM * 8 + 2: return SGB_SOP_KERNEL(SHAPE_SUM, 2);
+    case SHAPE_SUM * 8 + 3: return SGB_SOP_KERNEL(SHAPE_SUM, 3);
+    case SHAPE_PAIRS * 8 + 0: return SGB_SOP_KERNEL(SHAPE_PAIRS, 0);
+    case SHAPE_PAIRS * 8 + 1: return SGB_SOP_KERNEL(SHAPE_PAIRS, 1);
+    case SHAPE_PAIRS * 8 + 2: return SGB_SOP_KERNEL(SHAPE_PAIRS, 2);
+    case SHAPE_PAIRS * 8 + 3: return SGB_SOP_KERNEL(SHAPE_PAIRS, 3);
+    case SOP_GENERAL_CODE: return sop_general_unit;
+    default: return nullptr;
   }
 }
 
@@ -710,6 +769,8 @@ struct sgb_plan {
   int64_t *d_sdel = nullptr;
   uint32_t *d_pos = nullptr, *d_cbase = nullptr, *d_obase = nullptr, *d_opos32 = nullptr;
   uint16_t *d_coff = nullptr, *d_ooff = nullptr;
+  SopDesc *d_sopd = nullptr;
+  uint32_t *d_fbase = nullptr;
   // workspace for the host-buffer entry points
   std::mutex ws_mu;
   double *d_x = nullptr, *d_out = nullptr;
@@ -771,7 +832,8 @@ void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_
     sop_batch<<<(unsigned)blocks, BATCH_WARPS * 32, 0, s>>>(p->T, p->d_btiles + u.bt0, x, ld, batch, out, ld_out,
                                                             csr);
   } else {
-    sop_single<<<(unsigned)u.grid, SOP_BS, 0, s>>>(p->T, p->d_tiles + u.t0, u.t1 - u.t0, x, out, csr);
+    sop_kernel_for(u.variant)<<<(unsigned)u.grid, SOP_BS, 0, s>>>(p->T, p->d_sopd, p->d_tiles + u.t0, u.t1 - u.t0,
+                                                                  x, out, csr);
   }
 }
 
@@ -786,6 +848,13 @@ cudaError_t allow_smem(int smem_max) {
   if ((e = allow_smem_single<BS, 1>(smem_max)) != cudaSuccess) return e;
   if ((e = allow_smem_single<BS, 2>(smem_max)) != cudaSuccess) return e;
   return allow_smem_single<BS, 4>(smem_max);
+}
+
+// Sum-of-products groups the fast kernels take: affine column 0, one retained
+// column (every slot = column 0 + delta), width class <= 16 factors.
+bool sop_fast_ok(const sgb_group &G) {
+  return (G.flags & FLAG_AFFINE0) && G.n_ret == 1 && G.variant <= 3 && !(G.flags & FLAG_INTERLEAVED) &&
+         G.a0_stride >= INT32_MIN && G.a0_stride <= INT32_MAX;
 }
 
 // per-entry validation of a compressed table: base[c][i/32] + off[c][i] < limit (off == skip allowed)
@@ -821,7 +890,7 @@ void sgb_plan_destroy(sgb_plan *p) {
   cudaSetDevice(p->device);
   void *bufs[] = {p->d_groups, p->d_tiles, p->d_btiles, p->d_outputs, p->d_tape, p->d_imm, p->d_con,
                   p->d_sop, p->d_scol, p->d_sdel, p->d_pos, p->d_x, p->d_out, p->d_cbase, p->d_coff,
-                  p->d_obase, p->d_ooff, p->d_opos32};
+                  p->d_obase, p->d_ooff, p->d_opos32, p->d_sopd, p->d_fbase};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (p->ws_stream) cudaStreamDestroy(p->ws_stream);
@@ -968,7 +1037,8 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
         u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
         if (u.grid > u.t1 - u.t0) u.grid = u.t1 - u.t0;
       } else {
-        SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sop_single, SOP_BS, 0));
+        if (!sop_kernel_for(u.variant)) return fail(-1, "sgb_plan_create: bad sum-of-products unit variant");
+        SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, sop_kernel_for(u.variant), SOP_BS, 0));
         u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
         const int64_t need = (u.t1 - u.t0 + SOP_BS / 32 - 1) / (SOP_BS / 32);
         if (u.grid > need) u.grid = need;
@@ -982,6 +1052,9 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
     for (int g = u.g0; g < u.g1; ++g) {
       const sgb_group &G = d->groups[g];
       if (G.kind != u.kind) return fail(-1, "sgb_plan_create: group kind differs from its unit");
+      if (u.kind == KIND_SOP && u.variant != SOP_GENERAL_CODE &&
+          (!sop_fast_ok(G) || u.variant != G.shape * 8 + G.variant))
+        return fail(-1, "sgb_plan_create: group does not fit its sum-of-products unit");
       if (u.kind == KIND_TAPE && (G.flags & FLAG_SERIAL) && u.variant != 1)
         return fail(-1, "sgb_plan_create: serial group in a vectorised tape unit");
     }
@@ -1019,6 +1092,35 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
     p->units.push_back(u);
   }
   p->csr_waves = max_wave + 1 > p->n_waves ? max_wave + 1 : p->n_waves;
+  // compact sum-of-products descriptors (+ fast-path factor bases)
+  std::vector<SopDesc> sopd(d->n_groups);
+  std::vector<uint32_t> fbase;
+  if (d->n_obase >= ((int64_t)1 << 32) || d->n_ooff >= ((int64_t)1 << 32) || d->n_opos32 >= ((int64_t)1 << 32))
+    return fail(-1, "sgb_plan_create: output-position tables exceed u32 offsets");
+  for (int g = 0; g < d->n_groups; ++g) {
+    const sgb_group &G = d->groups[g];
+    SopDesc &sd = sopd[g];
+    memset(&sd, 0, sizeof(sd));
+    if (G.kind != KIND_SOP) continue;
+    if (G.n >= ((int64_t)1 << 31)) return fail(-1, "sgb_plan_create: sum-of-products group exceeds 2^31 instances");
+    const bool fast = sop_fast_ok(G);
+    sd.n = (int32_t)G.n;
+    sd.dest_base = (uint32_t)G.dest_base;
+    sd.meta = (uint32_t)G.sop_len | ((uint32_t)G.shape << 6) | ((uint32_t)G.variant << 8) | (fast ? M_FAST : 0u) |
+              ((G.flags & FLAG_CSR_ONLY) ? M_CSR_ONLY : 0u) | ((G.flags & FLAG_STREAM) ? M_STREAM : 0u) |
+              ((G.flags & FLAG_OPOS16) ? M_OPOS16 : 0u) | ((G.flags & FLAG_OPOS32) ? M_OPOS32 : 0u);
+    sd.stride = (int32_t)G.a0_stride;
+    sd.newterm = d->sop[2 * G.sop_off];
+    sd.negm = d->sop[2 * G.sop_off + 1];
+    sd.g = g;
+    sd.ob_off = (uint32_t)G.ob_off;
+    sd.oo_off = (uint32_t)G.oo_off;
+    if (fast) {
+      sd.fbase_off = (uint32_t)fbase.size();
+      for (int f = 0; f < G.sop_len; ++f)  // slot 0 is the affine column itself (delta 0)
+        fbase.push_back((uint32_t)(G.a0_base + (d->slot_col[G.slot_off + f] < 0 ? d->slot_delta[G.slot_off + f] : 0)));
+    }
+  }
   int rc = 0;
   if ((rc = upload(&p->d_groups, d->groups, d->n_groups)) ||
       (rc = upload(&p->d_tiles, reinterpret_cast<const int2 *>(d->tiles), d->n_tiles)) ||
@@ -1031,10 +1133,12 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       (rc = upload(&p->d_con, d->constants, d->n_constants)) ||
       (rc = upload(&p->d_cbase, d->cbase, d->n_cbase)) || (rc = upload(&p->d_coff, d->coff, d->n_coff)) ||
       (rc = upload(&p->d_obase, d->obase, d->n_obase)) || (rc = upload(&p->d_ooff, d->ooff, d->n_ooff)) ||
-      (rc = upload(&p->d_opos32, d->opos32, d->n_opos32)))
+      (rc = upload(&p->d_opos32, d->opos32, d->n_opos32)) ||
+      (rc = upload(&p->d_sopd, sopd.data(), (int64_t)sopd.size())) ||
+      (rc = upload(&p->d_fbase, fbase.data(), (int64_t)fbase.size())))
     return rc;
   p->T = Tables{p->d_groups, p->d_tape, p->d_imm, p->d_sop, p->d_scol, p->d_sdel, p->d_pos,
-                p->d_con, p->d_cbase, p->d_coff, p->d_obase, p->d_ooff, p->d_opos32};
+                p->d_con, p->d_cbase, p->d_coff, p->d_obase, p->d_ooff, p->d_opos32, p->d_fbase};
   return 0;
 }
 

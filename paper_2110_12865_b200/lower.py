@@ -534,6 +534,22 @@ def sop_vec(cls: int) -> int:
 SOP_SHAPE_GENERIC, SOP_SHAPE_SUM, SOP_SHAPE_PAIRS = 0, 1, 2
 
 
+SOP_GENERAL_CODE = 64  # csrc SOP_GENERAL_CODE
+
+
+def sop_unit_code(g, compress: bool) -> int:
+    """Kernel of a sum-of-products group: fast path shape * 8 + width class, or the general kernel."""
+    cls = sop_class(len(g.sop))
+    fast = (compress and g.layout == "coalesced" and len(g.columns) == 1 and cls <= 3
+            and affine_column0(g.columns[0]) is not None and -2**31 <= g_stride(g) < 2**31)
+    return sop_shape(g.sop) * 8 + cls if fast else SOP_GENERAL_CODE
+
+
+def g_stride(g) -> int:
+    c = g.columns[0]
+    return int(c[1] - c[0]) if len(c) > 1 else 0
+
+
 def sop_shape(desc) -> int:
     """Kernel shape of a sum-of-products descriptor (csrc SHAPE_*); arithmetic is identical."""
     starts = [bool(d & SOP_NEWTERM) for d in np.asarray(desc).tolist()]
@@ -774,9 +790,12 @@ def lower_plan(plan, compress: bool | None = None) -> DevicePlanArrays:
                         vec = v
                         break
             plan_units.append((KIND_TAPE, vec, bs, regs, tm))
-        sm = [j for j in members if groups[j].kind == KIND_SOP]
-        if sm:
-            plan_units.append((KIND_SOP, 0, SOP_BLOCK, 0, sm))
+        codes: dict[int, list] = {}
+        for j in members:
+            if groups[j].kind == KIND_SOP:
+                codes.setdefault(sop_unit_code(groups[j], compress), []).append(j)
+        for code in sorted(codes):  # one persistent launch per kernel body
+            plan_units.append((KIND_SOP, code, SOP_BLOCK, 0, codes[code]))
         for kind, variant, bs, regs, ms in plan_units:
             g_begin = len(order_groups)
             unit_tiles, unit_keys = [], []
