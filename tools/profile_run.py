@@ -14,6 +14,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--w", type=int, default=1000)
 ap.add_argument("--evals", type=int, default=3)
 ap.add_argument("--batch", type=int, default=0)
+ap.add_argument("--mode", choices=("csr", "val"), default="csr")
 args = ap.parse_args()
 
 import torch  # noqa: E402
@@ -27,7 +28,7 @@ key, plan, _, _ = bench.build_workload(args, 0, 1)
 print(f"plan {key} ready in {time.time() - t0:.1f}s: {len(plan.kernels)} kernels, {len(plan.outputs)} outputs",
       flush=True)
 dp = DevicePlan(plan)
-print("waves", dp.launches, "units", dp.units, flush=True)
+print("waves", dp.launches, "units", dp.units, "csr units", dp.csr_units, flush=True)
 if args.batch:
     X = torch.zeros((plan.value_array_size, args.batch), dtype=torch.float64, device="cuda")
     X[: plan.input_count] = torch.from_numpy(lmlt_inputs(args.w)).cuda()[:, None]
@@ -38,6 +39,9 @@ else:
     x = dp.new_values(lmlt_inputs(args.w))
     out = torch.empty(len(plan.outputs), dtype=torch.float64, device="cuda")
     for _ in range(args.evals):
-        dp.run_csr(x, out)
+        if args.mode == "csr":
+            dp.run_csr(x, out)
+        else:
+            dp.run_values(x)
 torch.cuda.synchronize()
 print("done", flush=True)
