@@ -273,7 +273,7 @@ def main():
         barrier = None
 
     from paper_2110_12865_b200 import DevicePlan
-    from paper_2110_12865_b200.metrics import csr_wave_traffic, plan_balg
+    from paper_2110_12865_b200.metrics import csr_wave_traffic, plan_balg, wave_traffic
 
     key, plan, row_ptr, col_idx = build_workload(args, rank, world, barrier)
     n_out = len(plan.outputs)
@@ -357,7 +357,9 @@ def main():
         return 0
 
     # ---- roofline of the dominant launch ----
-    traffic = csr_wave_traffic(plan, dp.lowered)
+    direct = bool(np.any(dp.lowered.groups["flags"] & (384)))  # FLAG_OPOS16 | FLAG_OPOS32
+    traffic = csr_wave_traffic(plan, dp.lowered) if direct else wave_traffic(plan, dp.lowered)
+    assert len(traffic) == n_w, (len(traffic), n_w)
     dom = int(np.argmax(per_launch))
     dom_bytes = traffic[dom].bytes
     achieved = dom_bytes / (per_launch[dom] * 1e-3) / 1e9
@@ -397,7 +399,8 @@ def main():
             "parallelism": f"replicas x{world}: one full evaluation per GPU per step (independent value sets)",
             "l2": "no flush: value array + tables exceed the 126 MB L2",
             "clock_settle": "1 s of untimed evaluations before the timed region",
-            "parity": parity, "mode": "CSR (sgb_run_csr: outputs stored by their producers, no gather pass)",
+            "parity": parity, "mode": ("CSR, direct stores (sgb_run_csr)" if direct else
+                                       "CSR (sgb_run_csr: value-array waves + u32-indexed output gather)"),
             "achieved_hbm_gbs_step": step_bytes / (ms_per_step * 1e-3) / 1e9,
             "balg_bytes_step": step_bytes, "balg_bytes_single_pass": plan_balg(plan),
             "balg_gbs_single_pass": plan_balg(plan) / (ms_per_step * 1e-3) / 1e9,

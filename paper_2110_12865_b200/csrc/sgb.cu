@@ -35,6 +35,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -428,13 +429,14 @@ __device__ __forceinline__ double sop_eval(const double (&v)[LMAX], int len, uin
   } else if (SHAPE == SHAPE_PAIRS) {
     double acc = __dmul_rn(NEG ? neg_if(v[0], negm, 0) : v[0], NEG ? neg_if(v[1], negm, 1) : v[1]);
 #pragma unroll
-    for (int f = 2; f + 1 < LMAX; f += 2)
-      if (f + 1 < len)
-        acc = __dadd_rn(acc, __dmul_rn(NEG ? neg_if(v[f], negm, f) : v[f], NEG ? neg_if(v[f + 1], negm, f + 1) : v[f + 1]));
-    if (len & 1) {  // single-factor tail (e.g. "+ A_ij")
-#pragma unroll
-      for (int f = 2; f < LMAX; f += 2)
-        if (f == len - 1) acc = __dadd_rn(acc, NEG ? neg_if(v[f], negm, f) : v[f]);
+    for (int f = 2; f < LMAX; f += 2) {
+      const double a = NEG ? neg_if(v[f], negm, f) : v[f];
+      if (f + 1 < len) {
+        const double b = NEG ? neg_if(v[f + 1], negm, f + 1) : v[f + 1];
+        acc = __dadd_rn(acc, __dmul_rn(a, b));
+      } else if (f < len) {  // single-factor tail (e.g. "+ A_ij"), len odd
+        acc = __dadd_rn(acc, a);
+      }
     }
     return acc;
   } else {
@@ -529,8 +531,7 @@ __device__ __forceinline__ void sop_fast(const Tables &T, const SopDesc &d, uint
   for (int v = 0; v < VEC; ++v) {
     const uint32_t off = (uint32_t)d.stride * iv[v];
 #pragma unroll
-    for (int f = 0; f < LMAX; ++f)
-      if (f < len) val[v][f] = __ldg(x + (fb[f] + off));
+    for (int f = 0; f < LMAX; ++f) val[v][f] = f < len ? __ldg(x + (fb[f] + off)) : 0.0;
   }
 #pragma unroll
   for (int v = 0; v < VEC; ++v) {
@@ -602,7 +603,7 @@ __device__ __noinline__ void sop_general(const Tables &T, const SopDesc &d, uint
 // output groups), prefetching its next tile entry; no block synchronisation and
 // no per-CTA prologue, the grid is the resident capacity of the chip.
 template <int SHAPE, int LMAX, int VEC>
-__global__ void __launch_bounds__(SOP_BS, 4) sop_fast_unit(Tables T, const SopDesc *D, const int2 *tiles,
+__global__ void __launch_bounds__(SOP_BS, 3) sop_fast_unit(Tables T, const SopDesc *D, const int2 *tiles,
                                                           int64_t n_tiles, double *x, double *out, int csr) {
   const uint32_t lane = threadIdx.x & 31;
   const int64_t W = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -715,14 +716,13 @@ __global__ void __launch_bounds__(BATCH_WARPS * 32) sop_batch(Tables T, const in
   }
 }
 
-__global__ void gather_outputs(const double *__restrict__ x, const int64_t *__restrict__ outs, int64_t n,
-                               double *__restrict__ out) {
+// CSR values out[k] = x[outputs[k]] (codegen.py:445): u32 index stream
+// (evict-first), gathered value, streaming store.
+__global__ void __launch_bounds__(256) gather_outputs(const double *__restrict__ x, const uint32_t *__restrict__ outs,
+                                                      int64_t n, double *__restrict__ out) {
   const uint64_t pol = evict_first_policy();
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-    int64_t a;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(a) : "l"(outs + k), "l"(pol));
-    st_stream(out + k, __ldg(x + a), pol);
-  }
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+    st_stream(out + k, __ldg(x + __ldcs(outs + k)), pol);
 }
 
 __global__ void gather_outputs_batch(const double *__restrict__ X, int64_t ld, int64_t batch,
@@ -762,6 +762,8 @@ struct sgb_plan {
   sgb_group *d_groups = nullptr;
   int2 *d_tiles = nullptr, *d_btiles = nullptr;
   int64_t *d_outputs = nullptr;
+  uint32_t *d_outputs32 = nullptr;
+  bool direct_csr = false;  // some group stores its outputs at their CSR positions (FLAG_OPOS*)
   uint32_t *d_tape = nullptr;
   double *d_imm = nullptr, *d_con = nullptr;
   uint32_t *d_sop = nullptr;
@@ -775,6 +777,11 @@ struct sgb_plan {
   std::mutex ws_mu;
   double *d_x = nullptr, *d_out = nullptr;
   cudaStream_t ws_stream = nullptr;
+  // fork / join of the independent launch units of one wave
+  std::vector<cudaStream_t> aux;
+  std::vector<cudaEvent_t> ev_join;
+  cudaEvent_t ev_fork = nullptr;
+  std::mutex run_mu;  // the aux streams / events are per plan: one launch sequence at a time
 };
 
 namespace {
@@ -875,14 +882,19 @@ extern "C" {
 
 const char *sgb_last_error(void) { return g_err.c_str(); }
 
-int sgb_plan_waves(const sgb_plan *p, int csr) { return p ? (csr ? p->csr_waves : p->n_waves) : 0; }
+int sgb_plan_waves(const sgb_plan *p, int csr) {
+  if (!p) return 0;
+  if (!csr) return p->n_waves;
+  return p->direct_csr ? p->csr_waves : p->n_waves + (p->n_out > 0 ? 1 : 0);  // + the gather
+}
 
 int sgb_plan_units(const sgb_plan *p, int csr) {
   if (!p) return 0;
+  const bool direct = csr && p->direct_csr;
   int k = 0;
   for (const Unit &u : p->units)
-    if (csr || !(u.flags & UNIT_CSR_ONLY)) ++k;
-  return k;
+    if (direct || !(u.flags & UNIT_CSR_ONLY)) ++k;
+  return k + (csr && !p->direct_csr && p->n_out > 0 ? 1 : 0);
 }
 
 void sgb_plan_destroy(sgb_plan *p) {
@@ -890,10 +902,13 @@ void sgb_plan_destroy(sgb_plan *p) {
   cudaSetDevice(p->device);
   void *bufs[] = {p->d_groups, p->d_tiles, p->d_btiles, p->d_outputs, p->d_tape, p->d_imm, p->d_con,
                   p->d_sop, p->d_scol, p->d_sdel, p->d_pos, p->d_x, p->d_out, p->d_cbase, p->d_coff,
-                  p->d_obase, p->d_ooff, p->d_opos32, p->d_sopd, p->d_fbase};
+                  p->d_obase, p->d_ooff, p->d_opos32, p->d_sopd, p->d_fbase, p->d_outputs32};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (p->ws_stream) cudaStreamDestroy(p->ws_stream);
+  for (cudaStream_t a : p->aux) cudaStreamDestroy(a);
+  for (cudaEvent_t e : p->ev_join) cudaEventDestroy(e);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   delete p;
 }
 
@@ -1092,6 +1107,36 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
     p->units.push_back(u);
   }
   p->csr_waves = max_wave + 1 > p->n_waves ? max_wave + 1 : p->n_waves;
+  {  // per wave: largest unit first (caller's stream); the others co-run on aux streams
+    std::stable_sort(p->units.begin(), p->units.end(), [](const Unit &a, const Unit &b) {
+      return a.wave != b.wave ? a.wave < b.wave : (a.t1 - a.t0) > (b.t1 - b.t0);
+    });
+    int max_units = 1;
+    for (int w = 0; w <= max_wave; ++w) {
+      int n = 0;
+      for (const Unit &u : p->units) n += u.wave == w;
+      max_units = n > max_units ? n : max_units;
+      if (n < 2) continue;
+      for (Unit &u : p->units)  // leave one block per SM to the co-running units
+        if (u.wave == w && u.grid > prop.multiProcessorCount) {
+          const int64_t cap = u.grid - prop.multiProcessorCount;
+          if (cap >= prop.multiProcessorCount) u.grid = cap;
+        }
+    }
+    const int n_aux = max_units - 1 < 8 ? max_units - 1 : 8;
+    SGB_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+    for (int k = 0; k < n_aux; ++k) {
+      cudaStream_t a;
+      cudaEvent_t e;
+      SGB_CUDA(cudaStreamCreateWithFlags(&a, cudaStreamNonBlocking));
+      p->aux.push_back(a);
+      SGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      p->ev_join.push_back(e);
+    }
+  }
+  std::vector<uint32_t> outputs32(d->outputs, d->outputs + d->n_outputs);
+  for (int g = 0; g < d->n_groups; ++g)
+    if (d->groups[g].flags & (FLAG_OPOS16 | FLAG_OPOS32)) p->direct_csr = true;
   // compact sum-of-products descriptors (+ fast-path factor bases)
   std::vector<SopDesc> sopd(d->n_groups);
   std::vector<uint32_t> fbase;
@@ -1135,6 +1180,7 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       (rc = upload(&p->d_obase, d->obase, d->n_obase)) || (rc = upload(&p->d_ooff, d->ooff, d->n_ooff)) ||
       (rc = upload(&p->d_opos32, d->opos32, d->n_opos32)) ||
       (rc = upload(&p->d_sopd, sopd.data(), (int64_t)sopd.size())) ||
+      (rc = upload(&p->d_outputs32, outputs32.data(), (int64_t)outputs32.size())) ||
       (rc = upload(&p->d_fbase, fbase.data(), (int64_t)fbase.size())))
     return rc;
   p->T = Tables{p->d_groups, p->d_tape, p->d_imm, p->d_sop, p->d_scol, p->d_sdel, p->d_pos,
@@ -1156,38 +1202,84 @@ int sgb_plan_create(const sgb_plan_desc *d, int device, sgb_plan **out) {
   return 0;
 }
 
+// All units of one wave are independent: the largest runs on the caller's
+// stream, the others on the plan's aux streams forked from / joined back into it.
+static int launch_wave(sgb_plan *p, int wave, double *x, int64_t ld, int64_t batch, bool batched, double *out,
+                       int64_t ld_out, bool csr, cudaStream_t s) {
+  const Unit *us[64];
+  int n = 0;
+  for (const Unit &u : p->units)
+    if (u.wave == wave && (csr || !(u.flags & UNIT_CSR_ONLY)) && n < 64) us[n++] = &u;
+  if (n == 0) return 0;
+  const int k_aux = n - 1 < (int)p->aux.size() ? n - 1 : (int)p->aux.size();
+  if (k_aux > 0) SGB_CUDA(cudaEventRecord(p->ev_fork, s));
+  for (int k = 0; k < k_aux; ++k) SGB_CUDA(cudaStreamWaitEvent(p->aux[k], p->ev_fork, 0));
+  launch_unit(p, *us[0], x, ld, batch, batched, out, ld_out, csr, s);
+  for (int k = 1; k < n; ++k) {
+    cudaStream_t sk = k - 1 < k_aux ? p->aux[k - 1] : s;
+    launch_unit(p, *us[k], x, ld, batch, batched, out, ld_out, csr, sk);
+  }
+  for (int k = 0; k < k_aux; ++k) {
+    SGB_CUDA(cudaEventRecord(p->ev_join[k], p->aux[k]));
+    SGB_CUDA(cudaStreamWaitEvent(s, p->ev_join[k], 0));
+  }
+  return 0;
+}
+
+static int launch_gather(sgb_plan *p, const double *x, int64_t ld, int64_t batch, bool batched, double *out,
+                         int64_t ld_out, cudaStream_t s);
+
+// CSR mode without direct stores: every wave in value mode, then the output gather.
+static int launch_all(sgb_plan *p, double *x, int64_t ld, int64_t batch, bool batched, double *out, int64_t ld_out,
+                      bool csr, cudaStream_t s) {
+  std::lock_guard<std::mutex> lk(p->run_mu);
+  const bool direct = csr && p->direct_csr;
+  const int waves = direct ? p->csr_waves : p->n_waves;
+  for (int w = 0; w < waves; ++w) {
+    int rc = launch_wave(p, w, x, ld, batch, batched, out, ld_out, direct, s);
+    if (rc) return rc;
+  }
+  if (csr && !direct) {
+    int rc = launch_gather(p, x, ld, batch, batched, out, ld_out, s);
+    if (rc) return rc;
+  }
+  SGB_CUDA(cudaGetLastError());
+  return 0;
+}
+
 int sgb_run_wave(sgb_plan *p, double *x, double *out, int wave, void *stream) {
   if (!p || (!x && p->vas)) return fail(-1, "sgb_run_wave: null argument");
   const bool csr = out != nullptr;
-  if (wave < 0 || wave >= (csr ? p->csr_waves : p->n_waves)) return fail(-1, "sgb_run_wave: wave out of range");
+  if (wave < 0 || wave >= sgb_plan_waves(p, csr)) return fail(-1, "sgb_run_wave: wave out of range");
   if (csr && p->n_out == 0) return 0;
-  for (const Unit &u : p->units)
-    if (u.wave == wave) launch_unit(p, u, x, 1, 1, false, out, 1, csr, (cudaStream_t)stream);
+  std::lock_guard<std::mutex> lk(p->run_mu);
+  if (csr && !p->direct_csr && wave == p->n_waves) {  // the output gather
+    int rc = launch_gather(p, x, 1, 1, false, out, 1, (cudaStream_t)stream);
+    if (rc) return rc;
+    SGB_CUDA(cudaGetLastError());
+    return 0;
+  }
+  int rc = launch_wave(p, wave, x, 1, 1, false, out, 1, csr && p->direct_csr, (cudaStream_t)stream);
+  if (rc) return rc;
   SGB_CUDA(cudaGetLastError());
   return 0;
 }
 
 int sgb_run_values(sgb_plan *p, double *x, void *stream) {
   if (!p || (!x && p->vas)) return fail(-1, "sgb_run_values: null argument");
-  for (const Unit &u : p->units) launch_unit(p, u, x, 1, 1, false, nullptr, 1, false, (cudaStream_t)stream);
-  SGB_CUDA(cudaGetLastError());
-  return 0;
+  return launch_all(p, x, 1, 1, false, nullptr, 1, false, (cudaStream_t)stream);
 }
 
 int sgb_run_csr(sgb_plan *p, double *x, double *out, void *stream) {
   if (!p || (!x && p->vas) || (!out && p->n_out)) return fail(-1, "sgb_run_csr: null argument");
   if (!p->n_out) return 0;
-  for (const Unit &u : p->units) launch_unit(p, u, x, 1, 1, false, out, 1, true, (cudaStream_t)stream);
-  SGB_CUDA(cudaGetLastError());
-  return 0;
+  return launch_all(p, x, 1, 1, false, out, 1, true, (cudaStream_t)stream);
 }
 
 int sgb_run_batch(sgb_plan *p, double *X, int64_t ld, int64_t batch, void *stream) {
   if (!p || (!X && p->vas)) return fail(-1, "sgb_run_batch: null argument");
   if (batch < 1 || ld < batch) return fail(-1, "sgb_run_batch: need 1 <= batch <= ld");
-  for (const Unit &u : p->units) launch_unit(p, u, X, ld, batch, true, nullptr, 1, false, (cudaStream_t)stream);
-  SGB_CUDA(cudaGetLastError());
-  return 0;
+  return launch_all(p, X, ld, batch, true, nullptr, 1, false, (cudaStream_t)stream);
 }
 
 int sgb_run_batch_csr(sgb_plan *p, double *X, int64_t ld, int64_t batch, double *out, int64_t ld_out,
@@ -1195,8 +1287,20 @@ int sgb_run_batch_csr(sgb_plan *p, double *X, int64_t ld, int64_t batch, double 
   if (!p || (!X && p->vas) || (!out && p->n_out)) return fail(-1, "sgb_run_batch_csr: null argument");
   if (batch < 1 || ld < batch || ld_out < batch) return fail(-1, "sgb_run_batch_csr: need 1 <= batch <= ld, ld_out");
   if (!p->n_out) return 0;
-  for (const Unit &u : p->units) launch_unit(p, u, X, ld, batch, true, out, ld_out, true, (cudaStream_t)stream);
-  SGB_CUDA(cudaGetLastError());
+  return launch_all(p, X, ld, batch, true, out, ld_out, true, (cudaStream_t)stream);
+}
+
+static int launch_gather(sgb_plan *p, const double *x, int64_t ld, int64_t batch, bool batched, double *out,
+                         int64_t ld_out, cudaStream_t s) {
+  if (!p->n_out) return 0;
+  if (batched) {
+    const int64_t blocks = (p->n_out + 7) / 8;
+    gather_outputs_batch<<<(unsigned)blocks, 256, 0, s>>>(x, ld, batch, p->d_outputs, p->n_out, out, ld_out);
+  } else {
+    int64_t blocks = (p->n_out + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    gather_outputs<<<(unsigned)blocks, 256, 0, s>>>(x, p->d_outputs32, p->n_out, out);
+  }
   return 0;
 }
 
@@ -1207,7 +1311,7 @@ int sgb_gather_outputs(sgb_plan *p, const double *x, double *out, void *stream) 
   const int bs = 256;
   int64_t blocks = (p->n_out + bs - 1) / bs;
   if (blocks > 148 * 32) blocks = 148 * 32;
-  gather_outputs<<<(unsigned)blocks, bs, 0, (cudaStream_t)stream>>>(x, p->d_outputs, p->n_out, out);
+  gather_outputs<<<(unsigned)blocks, bs, 0, (cudaStream_t)stream>>>(x, p->d_outputs32, p->n_out, out);
   SGB_CUDA(cudaGetLastError());
   return 0;
 }

@@ -713,9 +713,19 @@ def _tile_keys(g: _Group, starts: np.ndarray, tile: int) -> np.ndarray:
     return np.where(m == np.iinfo(np.int64).max, -1, m)
 
 
-def lower_plan(plan, compress: bool | None = None) -> DevicePlanArrays:
+def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = None) -> DevicePlanArrays:
+    """ExecutionPlan -> device plan.
+
+    ``direct_csr``: output groups store their CSR values through output-position
+    tables and CSR-only copy groups cover inputs / duplicates (sgb_run_csr
+    without a gather pass).  Off by default: on B200 the 8-byte scattered stores
+    cost more than the coalesced value-array stores + one u32-indexed gather
+    (profiles/r06).
+    """
     if compress is None:
         compress = os.environ.get("SGB_COMPRESS", "1") != "0"
+    if direct_csr is None:
+        direct_csr = os.environ.get("SGB_DIRECT_CSR", "0") == "1"
     read_sets = _read_sets(plan)
     waves = compute_waves(plan, read_sets)
     lowered = [lower_kernel(plan, kp, k) for k, kp in enumerate(plan.kernels)]
@@ -723,6 +733,9 @@ def lower_plan(plan, compress: bool | None = None) -> DevicePlanArrays:
         kl.wave = w
     n_waves = (max(waves) + 1) if waves else 0
     opos, res_k, res_addr = _output_map(plan, lowered, waves)
+    if not direct_csr:
+        opos = [None] * len(lowered)
+        res_k = res_addr = np.zeros(0, np.int64)
     # copy groups: outputs that are inputs, duplicates or padding (CSR mode only)
     avail = _owner_waves(plan, waves, res_addr) + 1  # first wave that may read the source
     last = max(n_waves - 1, 0)

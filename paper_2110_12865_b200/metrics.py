@@ -9,7 +9,7 @@ once:
   + reads            8 * (distinct value-array addresses the wave loads)
   + writes           8 * (result slots the wave writes: sum N*R)
 
-and for the output gather ``8 * n_out`` (index) + ``8 * distinct output
+and for the output gather ``4 * n_out`` (u32 index) + ``8 * distinct output
 addresses`` + ``8 * n_out`` (CSR values written).  Summed over a plan this is
 the §8(d) ``B_alg`` with intermediates counted once per launch that touches
 them (they cross HBM between launches), so it is >= the single-pass figure
@@ -63,7 +63,7 @@ def wave_traffic(plan, lowered, batch: int = 1) -> list[LaunchTraffic]:
         out.append(LaunchTraffic(f"wave{w}", idx, con, 8 * reads * batch, wr, ops))
     outs = np.asarray(plan.outputs, dtype=np.int64)
     n_out = int(outs.size)
-    out.append(LaunchTraffic("gather_outputs", 8 * n_out, 0, 8 * int(np.unique(outs).size) * batch,
+    out.append(LaunchTraffic("gather_outputs", 4 * n_out, 0, 8 * int(np.unique(outs).size) * batch,
                              8 * n_out * batch, 0))
     return out
 

@@ -191,7 +191,10 @@ def run_values(dp, inputs) -> np.ndarray:
 
 
 def run_csr(dp, inputs) -> np.ndarray:
-    """CSR mode: the outputs written directly by the producing groups and copy groups."""
+    """CSR mode: direct stores by the producing groups and copy groups, or value mode + gather."""
+    direct = bool(np.any(dp.groups["flags"] & (L.FLAG_OPOS16 | L.FLAG_OPOS32)))
+    if not direct:
+        return _run(dp, inputs, csr=False)[0][dp.outputs]
     return _run(dp, inputs, csr=True)[1]
 
 

@@ -77,13 +77,15 @@ def test_device_resident_run_on_torch(golden):
     assert out.shape[0] == len(golden.plan.outputs)
 
 
-def test_csr_mode_writes_outputs_directly(golden):
-    """sgb_run_csr: producers store CSR values, copy groups cover inputs / duplicates; no gather."""
+@pytest.mark.parametrize("direct", [False, True])
+def test_csr_mode(golden, direct):
+    """sgb_run_csr: value waves + gather, or (direct) producers store CSR values and copy groups
+    cover inputs / duplicates."""
     import torch
 
-    from paper_2110_12865_b200 import DevicePlan
+    from paper_2110_12865_b200 import DevicePlan, lower_plan
 
-    dp = DevicePlan(golden.plan)
+    dp = DevicePlan(golden.plan, lowered=lower_plan(golden.plan, direct_csr=direct))
     x = dp.new_values(golden.inputs)
     out = torch.full((len(golden.plan.outputs),), float("nan"), dtype=torch.float64, device=x.device)
     dp.run_csr(x, out)

@@ -19,7 +19,7 @@ def test_emulated_device_plan_matches_reference_bitwise(golden):
 
 def test_emulated_csr_mode_matches_reference_outputs(golden):
     """CSR mode: producers store outputs at their CSR positions, copy groups cover the rest."""
-    dp = lower_plan(golden.plan)
+    dp = lower_plan(golden.plan, direct_csr=True)
     emu.check_tiles(dp)
     out = emu.run_csr(dp, golden.inputs)
     assert np.array_equal(bits(out), bits(golden.outputs))
@@ -43,7 +43,7 @@ def test_waves_respect_producers(golden):
 
 def test_lmlt_is_mostly_sum_of_products():
     plan = load_plan("tests/golden/lmlt_w12")
-    dp = lower_plan(plan)
+    dp = lower_plan(plan, direct_csr=True)
     n_sop = int(np.sum(dp.groups["kind"] == KIND_SOP))
     assert n_sop >= len(plan.kernels) // 2
     assert dp.n_waves == 5  # L.M.L^T + A needs 5 waves
@@ -57,7 +57,7 @@ def test_builder_plan_csr_mode_copy_group():
     from paper_2110_12865_b200.programs.mesh import build_lmlt_plan, lmlt_inputs
 
     plan, _, _ = build_lmlt_plan(20)
-    dp = lower_plan(plan)
+    dp = lower_plan(plan, direct_csr=True)
     copy = (dp.groups["flags"] & L.FLAG_CSR_ONLY) != 0
     assert copy.sum() == 1 and dp.needs_zero == L.ZERO_ONCE  # structural gaps read as zero
     assert int(dp.units[-1][0]) == dp.n_waves - 1  # no extra CSR-only wave: sources are inputs
