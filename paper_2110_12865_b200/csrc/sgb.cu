@@ -44,7 +44,8 @@
 
 namespace {
 
-// tape op codes: lower.py T_*; the op byte of a word is op | nega << 6 | negb << 7
+// tape op codes: lower.py T_*; the key byte of a word is op << 2 | nega << 1 | negb
+// (dense, so the interpreter switch compiles to one indirect branch)
 enum : int {
   T_MUL = 0, T_ADD, T_SUB, T_DIV, T_MADD, T_NEG, T_SQRT, T_SEL, T_IMM, T_ST, T_SLOW, T_MSUB, T_RMSUB
 };
@@ -56,7 +57,8 @@ enum : int {
 enum : int {
   U_WAVE = 0, U_KIND, U_VARIANT, U_G0, U_G1, U_T0, U_T1, U_BS, U_REGS, U_FLAGS, U_COUNT
 };
-enum : int { UNIT_CSR_ONLY = 1 };
+enum : int { UNIT_CSR_ONLY = 1, UNIT_JIT = 2 };
+constexpr int JIT_BLOCK = 256;  // jit.py JIT_BLOCK
 constexpr int PRE = 8;        // slot loads kept in flight by the tape prologue
 constexpr int SOP_BS = 256;   // sum-of-products block
 constexpr int SOP_BATCH = 16; // factor loads in flight per instance
@@ -197,7 +199,7 @@ __device__ __noinline__ double slow_op(unsigned kind, double a, int k) {
 }
 
 // ---- tape interpreter ---------------------------------------------------------------
-// Device words (lower.assemble): x = op | nega<<6 | negb<<7 | (c byte offset / 8) << 8,
+// Device words (lower.assemble): x = op<<2 | nega<<1 | negb | (c byte offset / 8) << 8,
 // y / z / w = byte offsets of dst / a / b in the lane's scratch column (w is the
 // immediate index, root index or kind<<16|k for IMM / ST / SLOW).  Scratch is
 // shared memory addressed with 32-bit shared addresses; instance v of a lane
@@ -214,7 +216,7 @@ __device__ __forceinline__ void sts(uint32_t addr, double v) {
 
 #define SGB_NEG(NA, v) ((NA) ? -(v) : (v))
 #define SGB_BIN(OPC, NA, NB, EXPR)                                                  \
-  case (OPC) | ((NA) << 6) | ((NB) << 7): {                                         \
+  case ((OPC) << 2) | ((NA) << 1) | (NB): {                                         \
     _Pragma("unroll") for (int v = 0; v < VEC; ++v) {                               \
       const double a = SGB_NEG(NA, lds(pa + v * VS));                               \
       const double b = SGB_NEG(NB, lds(pb + v * VS));                               \
@@ -222,7 +224,7 @@ __device__ __forceinline__ void sts(uint32_t addr, double v) {
     }                                                                               \
   } break;
 #define SGB_FUSED(OPC, NA, NB, EXPR)                                                \
-  case (OPC) | ((NA) << 6) | ((NB) << 7): {                                         \
+  case ((OPC) << 2) | ((NA) << 1) | (NB): {                                         \
     _Pragma("unroll") for (int v = 0; v < VEC; ++v) {                               \
       const double a = SGB_NEG(NA, lds(pa + v * VS));                               \
       const double b = SGB_NEG(NB, lds(pb + v * VS));                               \
@@ -252,26 +254,26 @@ __device__ __forceinline__ void run_tape(const Tables &T, const sgb_group &G, ui
       SGB_SIGNS(SGB_FUSED, T_MADD, __dadd_rn(__dmul_rn(a, b), c))
       SGB_SIGNS(SGB_FUSED, T_MSUB, __dsub_rn(__dmul_rn(a, b), c))
       SGB_SIGNS(SGB_FUSED, T_RMSUB, __dsub_rn(c, __dmul_rn(a, b)))
-      case T_NEG:
+      case T_NEG << 2:
 #pragma unroll
         for (int v = 0; v < VEC; ++v) sts(pd + v * VS, -lds(pa + v * VS));
         break;
-      case T_SQRT:
+      case T_SQRT << 2:
 #pragma unroll
         for (int v = 0; v < VEC; ++v) sts(pd + v * VS, __dsqrt_rn(lds(pa + v * VS)));
         break;
-      case T_SEL:
+      case T_SEL << 2:
 #pragma unroll
         for (int v = 0; v < VEC; ++v)
           sts(pd + v * VS, lds(pa + v * VS) < 0.0 ? lds(pb + v * VS) : lds(pc + v * VS));
         break;
-      case T_IMM: {
+      case T_IMM << 2: {
         const double imm = __ldg(T.imm + w.w);
 #pragma unroll
         for (int v = 0; v < VEC; ++v) sts(pd + v * VS, imm);
         break;
       }
-      case T_ST:
+      case T_ST << 2:
         if (!selfref || (int)w.w == phase) {
 #pragma unroll
           for (int v = 0; v < VEC; ++v)
@@ -722,7 +724,7 @@ __global__ void __launch_bounds__(256) gather_outputs(const double *__restrict__
                                                       int64_t n, double *__restrict__ out) {
   const uint64_t pol = evict_first_policy();
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
-    st_stream(out + k, __ldg(x + __ldcs(outs + k)), pol);
+    st_stream(out + k, __ldg(x + __ldg(outs + k)), pol);
 }
 
 __global__ void gather_outputs_batch(const double *__restrict__ X, int64_t ld, int64_t batch,
@@ -745,6 +747,9 @@ int upload(T **dst, const T *src, int64_t n) {
 
 struct Unit {
   int wave, kind, variant, g0, g1, bs, regs, flags;
+  int index;                   // position in sgb_plan_desc.units (names the specialised kernels)
+  const void *jit = nullptr;   // specialised tape kernels (cudaKernel_t), UNIT_JIT
+  const void *jitb = nullptr;
   int64_t grid;      // single-set persistent grid (blocks)
   int64_t t0, t1;    // single-set tiles [t0, t1)
   int64_t bt0, bt1;  // batched tiles
@@ -772,6 +777,7 @@ struct sgb_plan {
   uint32_t *d_pos = nullptr, *d_cbase = nullptr, *d_obase = nullptr, *d_opos32 = nullptr;
   uint16_t *d_coff = nullptr, *d_ooff = nullptr;
   SopDesc *d_sopd = nullptr;
+  cudaLibrary_t jit_lib = nullptr;
   uint32_t *d_fbase = nullptr;
   // workspace for the host-buffer entry points
   std::mutex ws_mu;
@@ -823,6 +829,22 @@ void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_
   if ((u.flags & UNIT_CSR_ONLY) && !csr) return;
   const int64_t blocks = batched ? u.bt1 - u.bt0 : u.t1 - u.t0;
   if (blocks <= 0) return;
+  if (u.flags & UNIT_JIT) {  // specialised straight-line kernels (jit.py)
+    const int2 *tiles = batched ? p->d_btiles + u.bt0 : p->d_tiles + u.t0;
+    int64_t n = blocks;
+    int c = csr ? 1 : 0;
+    Tables T = p->T;
+    if (batched) {
+      int64_t ld_ = ld, batch_ = batch, ldo = ld_out;
+      void *args[] = {&T, &tiles, &n, &x, &ld_, &batch_, &out, &ldo, &c};
+      const int64_t grid = blocks < u.grid ? blocks : u.grid;
+      cudaLaunchKernel(u.jitb, dim3((unsigned)grid), dim3(JIT_BLOCK), args, 0, s);
+    } else {
+      void *args[] = {&T, &tiles, &n, &x, &out, &c};
+      cudaLaunchKernel(u.jit, dim3((unsigned)u.grid), dim3(JIT_BLOCK), args, 0, s);
+    }
+    return;
+  }
   if (u.kind == KIND_TAPE) {
     if (batched) {  // block = the unit's scratch stride, one instance per warp
       const int stride = u.bs * u.variant;
@@ -906,6 +928,7 @@ void sgb_plan_destroy(sgb_plan *p) {
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (p->ws_stream) cudaStreamDestroy(p->ws_stream);
+  if (p->jit_lib) cudaLibraryUnload(p->jit_lib);
   for (cudaStream_t a : p->aux) cudaStreamDestroy(a);
   for (cudaEvent_t e : p->ev_join) cudaEventDestroy(e);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
@@ -1021,6 +1044,10 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
   SGB_CUDA(allow_smem<64>(smem_max));
   SGB_CUDA(allow_smem<128>(smem_max));
   SGB_CUDA(cudaFuncSetAttribute(tape_batch, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max));
+  if (d->jit_cubin_size > 0) {
+    if (!d->jit_cubin) return fail(-1, "sgb_plan_create: null specialised-kernel cubin");
+    SGB_CUDA(cudaLibraryLoadData(&p->jit_lib, d->jit_cubin, nullptr, nullptr, 0, nullptr, nullptr, 0));
+  }
   std::vector<int2> btiles;
   int max_wave = -1;
   for (int k = 0; k < d->n_units; ++k) {
@@ -1036,18 +1063,34 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
     u.bs = (int)r[U_BS];
     u.regs = (int)r[U_REGS];
     u.flags = (int)r[U_FLAGS];
+    u.index = k;
     const bool csr_only = u.flags & UNIT_CSR_ONLY;
+    const bool jit = u.flags & UNIT_JIT;
+    if (jit) {
+      if (u.kind != KIND_TAPE || u.bs != JIT_BLOCK || u.variant != 1 || !p->jit_lib)
+        return fail(-1, "sgb_plan_create: specialised unit " + std::to_string(k) + " without its kernels");
+      cudaKernel_t kf, kb;
+      const std::string nf = "sgb_tape_u" + std::to_string(k), nbn = "sgb_tape_b" + std::to_string(k);
+      SGB_CUDA(cudaLibraryGetKernel(&kf, p->jit_lib, nf.c_str()));
+      SGB_CUDA(cudaLibraryGetKernel(&kb, p->jit_lib, nbn.c_str()));
+      u.jit = (const void *)kf;
+      u.jitb = (const void *)kb;
+    }
     if (u.g0 < 0 || u.g1 > d->n_groups || u.g0 > u.g1 || u.wave < 0 ||
         (csr_only ? u.wave != d->n_waves : u.wave >= d->n_waves) || u.t0 < 0 || u.t1 > d->n_tiles ||
         u.t0 > u.t1 || (u.kind != KIND_TAPE && u.kind != KIND_SOP) ||
-        (u.kind == KIND_TAPE && (u.bs != 32 && u.bs != 64 && u.bs != 128)) ||
+        (u.kind == KIND_TAPE && !jit && (u.bs != 32 && u.bs != 64 && u.bs != 128)) ||
         (u.kind == KIND_TAPE && (u.variant != 1 && u.variant != 2 && u.variant != 4)) ||
         (int64_t)u.regs * (u.kind == KIND_TAPE ? u.bs * u.variant : 0) * 8 > smem_max)
       return fail(-1, "sgb_plan_create: bad launch unit " + std::to_string(k));
     max_wave = u.wave > max_wave ? u.wave : max_wave;
     {  // persistent grid: resident capacity of the chip, at most one block (warp for SOP) per tile
       int nb = 0;
-      if (u.kind == KIND_TAPE) {
+      if (jit) {
+        SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, u.jit, JIT_BLOCK, 0));
+        u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
+        if (u.grid > u.t1 - u.t0) u.grid = u.t1 - u.t0;
+      } else if (u.kind == KIND_TAPE) {
         SGB_CUDA(tape_occupancy_any(u.bs, u.variant, u.regs, &nb));
         u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
         if (u.grid > u.t1 - u.t0) u.grid = u.t1 - u.t0;
@@ -1085,14 +1128,17 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       for (int64_t i = 0; i < G.n; i += bwarps) btiles.push_back(make_int2(g, (int)i));
     }
     u.bt1 = (int64_t)btiles.size();
-    if (u.kind == KIND_TAPE) {  // every tape word must stay inside its lane's scratch column
+    if (u.kind == KIND_TAPE && !jit) {  // every tape word must stay inside its lane's scratch column
       const uint64_t limit = (uint64_t)u.regs * u.bs * u.variant * 8;
       for (int g = u.g0; g < u.g1; ++g) {
         const sgb_group &G = d->groups[g];
         if (G.n_slots + G.n_const > u.regs) return fail(-1, "sgb_plan_create: slots exceed the scratch file");
         for (int64_t k2 = G.tape_off; k2 < G.tape_off + G.tape_len; ++k2) {
           const uint32_t *w = d->tape + 4 * k2;
-          const uint32_t op = w[0] & 63u;
+          const uint32_t op = (w[0] & 0xFFu) >> 2;
+          if (op != T_MUL && op != T_ADD && op != T_SUB && op != T_DIV && op != T_MADD && op != T_MSUB &&
+              op != T_RMSUB && (w[0] & 3u))
+            return fail(-1, "sgb_plan_create: sign flags on an op that takes none");
           const uint64_t c8 = (uint64_t)(w[0] >> 8) << 3;
           bool bad = op > T_RMSUB || w[2] >= limit || c8 >= limit;
           if (op != T_ST) bad = bad || w[1] >= limit;
@@ -1298,7 +1344,7 @@ static int launch_gather(sgb_plan *p, const double *x, int64_t ld, int64_t batch
     gather_outputs_batch<<<(unsigned)blocks, 256, 0, s>>>(x, ld, batch, p->d_outputs, p->n_out, out, ld_out);
   } else {
     int64_t blocks = (p->n_out + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > 148 * 32) blocks = 148 * 32;
     gather_outputs<<<(unsigned)blocks, 256, 0, s>>>(x, p->d_outputs32, p->n_out, out);
   }
   return 0;

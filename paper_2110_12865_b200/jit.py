@@ -1,0 +1,296 @@
+"""Specialised tape kernels: a tape unit's groups compiled to straight-line sm_100a code.
+
+The reference's native evaluator is code generation -- ``emit_kernel_source``
+prints one C function per group and ``compile_plan`` compiles it with ``cc``
+(emit.py:153-245); the paper's GPU backend does the same for GPUs
+(PAPER.md:253-260).  This module is that step for the B200: every group of a
+plain tape unit (lower.py) becomes one case of a persistent kernel whose body
+is the group's device tape unrolled into SSA registers -- the interpreter's
+shared-memory scratch file and per-word dispatch disappear, so the body runs
+from registers at FP64 issue rate.
+
+Arithmetic is exactly the tape's: every record is one ``__dadd_rn`` /
+``__dsub_rn`` / ``__dmul_rn`` / ``__ddiv_rn`` / ``__dsqrt_rn`` (fused
+MADD/MSUB/RMSUB stay two roundings), immediates are exact bit patterns,
+NVRTC runs with ``-fmad=false``; results are bit-identical to the interpreter
+(tests/test_gpu_parity.py runs both).  Index decode, constants and stores are
+baked in per group (N, dest_base, p_base, deltas...) like the emitted C bakes
+them (emit.py:99-150).
+
+Compiled with NVRTC (``libnvrtc.so.12``, loaded with ctypes) for
+``sm_100a``; cubins are cached by source hash.  The C ABI receives the cubin
+in the device plan (``sgb_plan_desc.jit_cubin``) and launches kernel
+``sgb_tape_u<unit>`` for each unit it names.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import hashlib
+import os
+import struct
+from pathlib import Path
+
+import numpy as np
+
+from . import lower as L
+
+JIT_BLOCK = 256  # threads per block = instances per tile of a specialised unit
+CACHE = Path(os.environ.get("SGB_JIT_CACHE", Path.home() / ".cache" / "sgb_jit"))
+
+_PREAMBLE = r"""
+typedef unsigned int u32;
+typedef unsigned short u16;
+typedef long long i64;
+typedef unsigned long long u64;
+struct Tables {  // == csrc/sgb.cu Tables
+  const void *groups; const u32 *tape; const double *imm; const u32 *sop; const int *slot_col;
+  const i64 *slot_delta; const u32 *pos; const double *con; const u32 *cbase; const u16 *coff;
+  const u32 *obase; const u16 *ooff; const u32 *opos32; const u32 *fbase;
+};
+#define NONE 0xFFFFFFFFu
+__device__ __forceinline__ double bits(u64 b) { return __longlong_as_double((long long)b); }
+__device__ __forceinline__ void dd_mul(double ah, double al, double bh, double bl, double &rh, double &rl) {
+  double p = __dmul_rn(ah, bh);
+  double e = __fma_rn(ah, bh, -p);
+  e = __dadd_rn(e, __dadd_rn(__dmul_rn(ah, bl), __dmul_rn(al, bh)));
+  rh = __dadd_rn(p, e);
+  rl = __dsub_rn(e, __dsub_rn(rh, p));
+}
+__device__ __noinline__ double powi(double x, int k) {  // == csrc powi
+  if (k == 2) return __dmul_rn(x, x);
+  double rh = 1.0, rl = 0.0, bh = x, bl = 0.0;
+  while (k) {
+    if (k & 1) dd_mul(rh, rl, bh, bl, rh, rl);
+    k >>= 1;
+    if (k) dd_mul(bh, bl, bh, bl, bh, bl);
+  }
+  double r = __dadd_rn(rh, rl);
+  return isfinite(r) ? r : rh;
+}
+__device__ __forceinline__ void st_stream(double *a, double v) { __stcs(a, v); }
+"""
+
+_BIN = {L.T_MUL: "__dmul_rn({a}, {b})", L.T_ADD: "__dadd_rn({a}, {b})", L.T_SUB: "__dsub_rn({a}, {b})",
+        L.T_DIV: "__ddiv_rn({a}, {b})", L.T_MADD: "__dadd_rn(__dmul_rn({a}, {b}), {c})",
+        L.T_MSUB: "__dsub_rn(__dmul_rn({a}, {b}), {c})", L.T_RMSUB: "__dsub_rn({c}, __dmul_rn({a}, {b}))"}
+_SLOW = {0: "sin({a})", 1: "cos({a})", 2: "exp({a})", 3: "log({a})"}
+
+
+def _imm(v: float) -> str:
+    return f"bits(0x{np.float64(v).view(np.uint64).item():016x}ULL)"
+
+
+def _column(rec, col: int, dp) -> str:
+    """Index expression (u32) of retained column ``col`` for instance ``i``."""
+    n = int(rec["n"])
+    f = int(rec["flags"])
+    if col == 0 and f & L.FLAG_AFFINE0:
+        return f"(u32)({int(rec['a0_base'])}LL + {int(rec['a0_stride'])}LL * i)"
+    if f & L.FLAG_W16:
+        nch = (n + 31) // 32
+        return (f"(__ldg(T.cbase + {int(rec['cb_off']) + col * nch}LL + (i >> 5)) + "
+                f"(u32)__ldcs(T.coff + {int(rec['co_off']) + col * n}LL + i))")
+    if f & L.FLAG_INTERLEAVED:
+        return f"__ldcs(T.pos + {int(rec['p_off'])}LL + i * {int(rec['n_ret'])} + {col})"
+    return f"__ldcs(T.pos + {int(rec['p_off']) + col * n}LL + i)"
+
+
+def _out_pos(rec, r: int) -> str | None:
+    n = int(rec["n"])
+    f = int(rec["flags"])
+    if f & L.FLAG_OPOS16:
+        nch = (n + 31) // 32
+        return (f"[&]() {{ const u16 o = __ldcs(T.ooff + {int(rec['oo_off']) + r * n}LL + i); "
+                f"return o == 0xFFFF ? NONE : __ldg(T.obase + {int(rec['ob_off']) + r * nch}LL + (i >> 5)) + o; }}()")
+    if f & L.FLAG_OPOS32:
+        return f"__ldcs(T.opos32 + {int(rec['oo_off']) + r * n}LL + i)"
+    return None
+
+
+def group_body(dp, gi: int, tape: np.ndarray, imms: list, batched: bool = False) -> list[str]:
+    """Straight-line CUDA for instance ``i`` of packed group ``gi`` (register tape -> SSA).
+
+    Batched: value set ``b`` of ``X[addr * ld + b]`` (lane = value set).
+    """
+    X = (lambda a: f"x + (u64)({a}) * ld + b") if batched else (lambda a: f"x + ({a})")
+    rec = dp.groups[gi]
+    n, S, K = int(rec["n"]), int(rec["n_slots"]), int(rec["n_const"])
+    flags = int(rec["flags"])
+    cols = dp.slot_col[rec["slot_off"]: rec["slot_off"] + S]
+    dels = dp.slot_delta[rec["slot_off"]: rec["slot_off"] + S]
+    out = []
+    reg: dict[int, str] = {}
+    if S:
+        out.append(f"const u32 idx0 = {_column(rec, 0, dp)};")
+    for s in range(S):
+        c = int(cols[s])
+        if c < 0:
+            addr = f"idx0 + (u32)({int(dels[s])}LL)"
+        elif c == 0:
+            addr = "idx0"
+        else:
+            addr = _column(rec, c, dp)
+        out.append(f"const double s{s} = __ldg({X(addr)});")
+        reg[s] = f"s{s}"
+    for k in range(K):
+        e = (f"{int(rec['c_off'])}LL + i * {K} + {k}" if flags & L.FLAG_INTERLEAVED
+             else f"{int(rec['c_off']) + k * n}LL + i")
+        out.append(f"const double k{k} = __ldcs(T.con + {e});")
+        reg[S + k] = f"k{k}"
+    stream = bool(flags & L.FLAG_STREAM)
+    for j, t in enumerate(tape.tolist()):
+        op, na, nb, dst, a, b, c, aux = t
+        A = ("-" if na else "") + reg.get(a, "0.0")
+        B = ("-" if nb else "") + reg.get(b, "0.0")
+        C = reg.get(c, "0.0")
+        if op == L.T_ST:
+            r = aux
+            v = reg[a]
+            x_addr = X(f"{int(rec['dest_base']) + r * n}LL + i")
+            store = f"st_stream({x_addr}, {v});" if stream else f"*({x_addr}) = {v};"
+            if stream:
+                out.append(f"if (!csr) {store}")
+            else:
+                out.append(store)
+            op_expr = _out_pos(rec, r)
+            if op_expr is not None:
+                dst_o = "out[(u64)o * ld_out + b]" if batched else "out[o]"
+                out.append(f"if (csr) {{ const u32 o = {op_expr}; if (o != NONE) {dst_o} = {v}; }}")
+            continue
+        if op == L.T_IMM:
+            expr = _imm(imms[aux])
+        elif op in _BIN:
+            expr = _BIN[op].format(a=f"({A})", b=f"({B})", c=C)
+        elif op == L.T_NEG:
+            expr = f"-{reg[a]}"
+        elif op == L.T_SQRT:
+            expr = f"__dsqrt_rn({reg[a]})"
+        elif op == L.T_SEL:
+            expr = f"({reg[a]} < 0.0 ? {reg[b]} : {C})"
+        elif op == L.T_SLOW:
+            kind, k = aux >> 16, aux & 0xFFFF
+            expr = f"powi({reg[a]}, {k})" if kind == 4 else _SLOW[kind].format(a=reg[a])
+        else:
+            raise ValueError(f"unknown tape op {op}")
+        out.append(f"const double t{j} = {expr};")
+        reg[dst] = f"t{j}"
+    return out
+
+
+def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
+    """Persistent kernels for tape unit ``u``: a case per group.
+
+    ``sgb_tape_u<u>``: one value set, one instance per thread (tiles of JIT_BLOCK
+    instances).  ``sgb_tape_b<u>``: batched, one instance per warp, lanes sweep
+    the value sets (tiles of JIT_BLOCK / 32 instances, csrc btiles).
+    """
+    unit = dp.unit(u)
+    out = []
+    for batched in (False, True):
+        if batched:
+            head = [f'extern "C" __global__ void __launch_bounds__({JIT_BLOCK}) sgb_tape_b{u}(',
+                    "    Tables T, const int2 *tiles, i64 n_tiles, double *x, i64 ld, i64 batch, double *out,",
+                    "    i64 ld_out, int csr) {",
+                    "  for (i64 t = blockIdx.x; t < n_tiles; t += gridDim.x) {",
+                    "    const int2 tl = tiles[t];",
+                    "    const i64 i = (i64)tl.y + (threadIdx.x >> 5);",
+                    "    for (i64 b = threadIdx.x & 31; b < batch; b += 32) {",
+                    "    switch (tl.x) {"]
+        else:
+            head = [f'extern "C" __global__ void __launch_bounds__({JIT_BLOCK}) sgb_tape_u{u}(',
+                    "    Tables T, const int2 *tiles, i64 n_tiles, double *x, double *out, int csr) {",
+                    "  for (i64 t = blockIdx.x; t < n_tiles; t += gridDim.x) {",
+                    "    const int2 tl = tiles[t];",
+                    "    const i64 i = (i64)tl.y + threadIdx.x;",
+                    "    {",
+                    "    switch (tl.x) {"]
+        out += head
+        for gi in range(unit["group_begin"], unit["group_end"]):
+            rec = dp.groups[gi]
+            out.append(f"    case {gi}: {{")
+            out.append(f"      if (i >= {int(rec['n'])}LL) break;")
+            if rec["flags"] & L.FLAG_CSR_ONLY:
+                out.append("      if (!csr) break;")
+            out += ["      " + ln for ln in group_body(dp, gi, tapes[gi], imms[gi], batched)]
+            out.append("    } break;")
+        out += ["    default: break;", "    }", "    }", "  }", "}", ""]
+    return "\n".join(out)
+
+
+# -- NVRTC ------------------------------------------------------------------------------
+
+_nvrtc = None
+
+
+def _lib():
+    global _nvrtc
+    if _nvrtc is None:
+        last = None
+        for name in (os.environ.get("SGB_NVRTC"), "libnvrtc.so.12", "/usr/local/cuda/lib64/libnvrtc.so.12"):
+            if not name:
+                continue
+            try:
+                _nvrtc = ctypes.CDLL(name)
+                break
+            except OSError as e:
+                last = e
+        if _nvrtc is None:
+            raise RuntimeError(f"NVRTC not found: {last}")
+    return _nvrtc
+
+
+def available() -> bool:
+    try:
+        _lib()
+        return True
+    except RuntimeError:
+        return False
+
+
+def compile_cubin(src: str, name: str = "sgb_tape.cu") -> bytes:
+    """NVRTC -> sm_100a cubin (no GPU needed); cached by source hash."""
+    key = hashlib.sha1(src.encode()).hexdigest()
+    path = CACHE / f"{key}.cubin"
+    if path.exists():
+        return path.read_bytes()
+    lib = _lib()
+    prog = ctypes.c_void_p()
+    rc = lib.nvrtcCreateProgram(ctypes.byref(prog), src.encode(), name.encode(), 0, None, None)
+    if rc:
+        raise RuntimeError(f"nvrtcCreateProgram failed ({rc})")
+    opts = [b"--gpu-architecture=sm_100a", b"-fmad=false", b"-std=c++17", b"-default-device", b"-lineinfo",
+            b"--extra-device-vectorization"]
+    arr = (ctypes.c_char_p * len(opts))(*opts)
+    rc = lib.nvrtcCompileProgram(prog, len(opts), arr)
+    if rc:
+        size = ctypes.c_size_t()
+        lib.nvrtcGetProgramLogSize(prog, ctypes.byref(size))
+        log = ctypes.create_string_buffer(size.value)
+        lib.nvrtcGetProgramLog(prog, log)
+        lib.nvrtcDestroyProgram(ctypes.byref(prog))
+        raise RuntimeError(f"NVRTC compile failed ({rc}):\n{log.value.decode(errors='replace')[:4000]}")
+    size = ctypes.c_size_t()
+    lib.nvrtcGetCUBINSize(prog, ctypes.byref(size))
+    buf = ctypes.create_string_buffer(size.value)
+    lib.nvrtcGetCUBIN(prog, buf)
+    lib.nvrtcDestroyProgram(ctypes.byref(prog))
+    cubin = buf.raw
+    try:
+        CACHE.mkdir(parents=True, exist_ok=True)
+        tmp = path.with_suffix(f".{os.getpid()}.tmp")
+        tmp.write_bytes(cubin)
+        os.replace(tmp, path)
+    except OSError:
+        pass
+    return cubin
+
+
+def specialise(dp, tapes: dict, imms: dict, units: list[int]) -> tuple[bytes, str]:
+    """Compile the given tape units of a lowered plan; returns (cubin, source)."""
+    src = _PREAMBLE + "\n".join(unit_source(dp, u, tapes, imms) for u in units)
+    return compile_cubin(src), src
+
+
+def _pack_u32(vals) -> bytes:
+    return struct.pack(f"<{len(vals)}I", *vals)

@@ -49,6 +49,8 @@ FLAG_OPOS32 = 256  # output positions: u32 per instance (0xFFFFFFFF = not an out
 FLAG_CSR_ONLY = 512  # synthetic copy group: runs in CSR mode only
 FLAG_COHERENT = 1024  # one retained column: every slot is column 0 + delta
 UNIT_CSR_ONLY = 1
+UNIT_JIT = 2  # tape unit compiled to straight-line code (jit.py), one instance per thread
+JIT_BLOCK = 256
 CHUNK = 32  # instances per compressed-index chunk (one warp in single-set mode)
 NONE32 = 0xFFFFFFFF
 SOP_NEWTERM, SOP_NEG = 1, 2
@@ -115,6 +117,8 @@ class DevicePlanArrays:
     kernels: list = field(default_factory=list)
     copies: list = field(default_factory=list)  # (wave, source addresses, CSR positions) per copy group
     exact: bool = True
+    jit_cubin: bytes = b""  # specialised tape units (UNIT_JIT): kernels sgb_tape_u<unit>, see jit.py
+    jit_source: str = ""
 
     def unit(self, u: int) -> dict:
         return dict(zip(UNIT_FIELDS, (int(v) for v in self.units[u])))
@@ -412,7 +416,7 @@ def compile_tape(kp):
 def assemble(tape: np.ndarray, stride: int, imm_base: int) -> np.ndarray:
     """Register tape -> device words (u32 x4): byte offsets for scratch stride ``stride``.
 
-    x = op | nega<<6 | negb<<7 | (c*stride) << 8;  y = dst*stride*8;
+    x = op<<2 | nega<<1 | negb | (c*stride) << 8;  y = dst*stride*8;
     z = a*stride*8;  w = b*stride*8, or the immediate index (IMM, plan-wide),
     the root index (ST) or kind<<16 | k (SLOW).
     """
@@ -422,7 +426,7 @@ def assemble(tape: np.ndarray, stride: int, imm_base: int) -> np.ndarray:
     by = np.uint64(stride * 8)
     if int(max(tape["c"].max(), tape["dst"].max(), tape["a"].max(), tape["b"].max())) * stride >= 1 << 24:
         raise ValueError("scratch offsets exceed the 24-bit device field")
-    x = op | (tape["nega"].astype(np.uint64) << np.uint64(6)) | (tape["negb"].astype(np.uint64) << np.uint64(7)) \
+    x = (op << np.uint64(2)) | (tape["nega"].astype(np.uint64) << np.uint64(1)) | tape["negb"].astype(np.uint64) \
         | ((tape["c"].astype(np.uint64) * np.uint64(stride)) << np.uint64(8))
     y = tape["dst"].astype(np.uint64) * by
     z = tape["a"].astype(np.uint64) * by
@@ -713,7 +717,8 @@ def _tile_keys(g: _Group, starts: np.ndarray, tile: int) -> np.ndarray:
     return np.where(m == np.iinfo(np.int64).max, -1, m)
 
 
-def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = None) -> DevicePlanArrays:
+def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = None,
+               jit: bool | None = None) -> DevicePlanArrays:
     """ExecutionPlan -> device plan.
 
     ``direct_csr``: output groups store their CSR values through output-position
@@ -726,6 +731,12 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         compress = os.environ.get("SGB_COMPRESS", "1") != "0"
     if direct_csr is None:
         direct_csr = os.environ.get("SGB_DIRECT_CSR", "0") == "1"
+    if jit is None:  # specialised (compiled) tape units -- see jit.py; SGB_TAPE_JIT=0 keeps the interpreter
+        jit = os.environ.get("SGB_TAPE_JIT", "1") != "0"
+    if jit:
+        from . import jit as _jit
+
+        jit = _jit.available()
     read_sets = _read_sets(plan)
     waves = compute_waves(plan, read_sets)
     lowered = [lower_kernel(plan, kp, k) for k, kp in enumerate(plan.kernels)]
@@ -783,6 +794,7 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     units, tiles_all = [], []
     tapes, imms, sops, scol, sdel, cbases, coffs, obases, ooffs, op32 = ([] for _ in range(10))
     n_tape = n_imm = n_sop = n_slot = n_cb = n_co = n_ob = n_oo = n_o32 = 0
+    jit_tapes, jit_imms, jit_units = {}, {}, []
     for w in range(total_waves):
         members = [j for j, g in enumerate(groups) if g.wave == w]
         plan_units = []
@@ -796,6 +808,9 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
             if regs * bs * 8 > SMEM_LIMIT:
                 raise ValueError(f"wave {w}: template needs {regs} scratch registers, more than shared memory holds")
             vec = 1
+            if plain and jit:  # one instance per thread, registers instead of the scratch file
+                plan_units.append((KIND_TAPE, 1, JIT_BLOCK, 0, tm))
+                continue
             if plain:
                 forced = int(os.environ.get("SGB_TAPE_VEC", "0"))
                 for v in (TAPE_VECS if not forced else (forced,)):
@@ -826,7 +841,9 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                 n_slot += len(g.slot_col)
                 flags = g.flags
                 if kind == KIND_TAPE:
-                    t = assemble(g.tape, bs * variant, n_imm)
+                    jit_tapes[gi] = g.tape
+                    jit_imms[gi] = g.imms
+                    t = assemble(g.tape, bs * variant, n_imm) if regs else np.zeros((0, 4), np.uint32)
                     rec["tape_off"], rec["tape_len"] = n_tape, len(t)
                     tapes.append(t)
                     n_tape += len(t)
@@ -889,6 +906,9 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
             t0 = sum(len(x) for x in tiles_all)
             tiles_all.append(t)
             uflags = UNIT_CSR_ONLY if w >= n_waves else 0
+            if kind == KIND_TAPE and regs == 0:
+                uflags |= UNIT_JIT
+                jit_units.append(len(units))
             units.append((w, kind, variant, g_begin, len(order_groups), t0, t0 + len(t), bs, regs, uflags))
     cat = lambda xs, dt: (np.concatenate(xs).astype(dt) if xs and sum(len(x) for x in xs)  # noqa: E731
                           else np.zeros(0, dt))
@@ -896,7 +916,7 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     positions = np.ascontiguousarray(plan.positions, dtype=np.uint32)
     if extra_pos:
         positions = np.concatenate([positions] + extra_pos)
-    return DevicePlanArrays(
+    dp = DevicePlanArrays(
         groups=packed,
         units=np.asarray(units, np.int64).reshape(-1, len(UNIT_FIELDS)),
         tiles=cat(tiles_all, np.int32).reshape(-1, 2),
@@ -921,3 +941,8 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         copies=[(g.wave, g.columns[0], g.opos[0]) for g in groups if g.flags & FLAG_CSR_ONLY],
         exact=exact,
     )
+    if jit_units:
+        from . import jit as _jit
+
+        dp.jit_cubin, dp.jit_source = _jit.specialise(dp, jit_tapes, jit_imms, jit_units)
+    return dp

@@ -77,6 +77,8 @@ class _Desc(ctypes.Structure):
         ("n_opos32", ctypes.c_int64),
         ("outputs", ctypes.c_void_p),
         ("n_outputs", ctypes.c_int64),
+        ("jit_cubin", ctypes.c_void_p),
+        ("jit_cubin_size", ctypes.c_int64),
     ]
 
 
@@ -178,6 +180,7 @@ class DevicePlan:
             ooff=np.ascontiguousarray(lw.ooff, np.uint16),
             opos32=np.ascontiguousarray(lw.opos32, np.uint32),
             outs=np.ascontiguousarray(lw.outputs, np.int64),
+            cubin=np.frombuffer(lw.jit_cubin, dtype=np.uint8).copy() if lw.jit_cubin else np.zeros(0, np.uint8),
         )
         d = _Desc(
             value_array_size=self.value_array_size, input_count=self.input_count,
@@ -193,6 +196,7 @@ class DevicePlan:
             n_coff=keep["coff"].size, obase=_ptr(keep["obase"]), n_obase=keep["obase"].size,
             ooff=_ptr(keep["ooff"]), n_ooff=keep["ooff"].size, opos32=_ptr(keep["opos32"]),
             n_opos32=keep["opos32"].size, outputs=_ptr(keep["outs"]), n_outputs=keep["outs"].size,
+            jit_cubin=_ptr(keep["cubin"]), jit_cubin_size=keep["cubin"].size,
         )
         torch.cuda.init()
         _check(self._lib.sgb_plan_create(ctypes.byref(d), self.device, ctypes.byref(self._handle)),

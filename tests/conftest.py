@@ -60,7 +60,7 @@ class Golden:
     def exact(self):
         from paper_2110_12865_b200.lower import lower_plan
 
-        return lower_plan(self.plan).exact
+        return lower_plan(self.plan, jit=False).exact
 
 
 @pytest.fixture(params=golden_names())

@@ -140,7 +140,7 @@ def check_tiles(dp):
             if g["kind"] == L.KIND_SOP:
                 tile = 32 * L.sop_vec(int(g["variant"]))
             else:
-                tile = unit["block_size"] * unit["variant"]
+                tile = unit["block_size"] * unit["variant"]  # JIT units: block_size 256, variant 1
             assert starts.tolist() == list(range(0, n, tile)), (u, gi)
 
 
@@ -202,6 +202,8 @@ def _tape(dp, g, x, i, store):
     """Decode the device tape words (lower.assemble) of this group's launch unit."""
     n = int(g["n"])
     unit = dp.unit(int(g["unit"]))
+    if unit["flags"] & L.UNIT_JIT:
+        raise ValueError("emulate with jit=False: specialised units carry no tape words")
     stride8 = unit["block_size"] * unit["variant"] * 8
     selfref = bool(g["flags"] & L.FLAG_SELFREF)
     phases = int(g["n_roots"]) if selfref else 1
@@ -215,7 +217,7 @@ def _tape(dp, g, x, i, store):
         for k in range(K):
             R[S + k] = _const(dp, g, k, i).copy()
         for wx, wy, wz, ww in words:
-            op, na, nb = wx & 63, (wx >> 6) & 1, (wx >> 7) & 1
+            op, na, nb = (wx & 0xFF) >> 2, (wx >> 1) & 1, wx & 1
             c = ((wx >> 8) << 3) // stride8
             d, a, b = wy // stride8, wz // stride8, ww // stride8
             A = (lambda: -R[a] if na else R[a])

@@ -101,6 +101,23 @@ def test_csr_mode(golden, direct):
             assert _close(got, want)
 
 
+def test_tape_interpreter_matches_specialised_kernels(golden):
+    """The hand-written tape interpreter and the specialised (jit.py) tape kernels agree bit for bit."""
+    import torch
+
+    from paper_2110_12865_b200 import DevicePlan, lower_plan
+
+    xs = []
+    for jit in (False, True):
+        dp = DevicePlan(golden.plan, lowered=lower_plan(golden.plan, jit=jit))
+        x = dp.new_values(golden.inputs)
+        dp.run_values(x)
+        torch.cuda.synchronize()
+        xs.append(x.cpu().numpy())
+        check(xs[-1], golden)
+    assert np.array_equal(bits(xs[0]), bits(xs[1]))
+
+
 def test_run_wave_by_wave_equals_run(golden):
     import torch
 

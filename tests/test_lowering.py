@@ -1,6 +1,7 @@
 """Device-plan lowering, proven on CPU through an emulator of the kernels."""
 
 import numpy as np
+import pytest
 
 import device_plan_emu as emu
 from conftest import bits
@@ -12,14 +13,14 @@ from paper_2110_12865_b200.plan import load_plan
 
 
 def test_emulated_device_plan_matches_reference_bitwise(golden):
-    dp = lower_plan(golden.plan)
+    dp = lower_plan(golden.plan, jit=False)
     x = emu.run_values(dp, golden.inputs)
     assert np.array_equal(bits(x), bits(golden.values))
 
 
 def test_emulated_csr_mode_matches_reference_outputs(golden):
     """CSR mode: producers store outputs at their CSR positions, copy groups cover the rest."""
-    dp = lower_plan(golden.plan, direct_csr=True)
+    dp = lower_plan(golden.plan, direct_csr=True, jit=False)
     emu.check_tiles(dp)
     out = emu.run_csr(dp, golden.inputs)
     assert np.array_equal(bits(out), bits(golden.outputs))
@@ -43,7 +44,7 @@ def test_waves_respect_producers(golden):
 
 def test_lmlt_is_mostly_sum_of_products():
     plan = load_plan("tests/golden/lmlt_w12")
-    dp = lower_plan(plan, direct_csr=True)
+    dp = lower_plan(plan, direct_csr=True, jit=False)
     n_sop = int(np.sum(dp.groups["kind"] == KIND_SOP))
     assert n_sop >= len(plan.kernels) // 2
     assert dp.n_waves == 5  # L.M.L^T + A needs 5 waves
@@ -57,7 +58,7 @@ def test_builder_plan_csr_mode_copy_group():
     from paper_2110_12865_b200.programs.mesh import build_lmlt_plan, lmlt_inputs
 
     plan, _, _ = build_lmlt_plan(20)
-    dp = lower_plan(plan, direct_csr=True)
+    dp = lower_plan(plan, direct_csr=True, jit=False)
     copy = (dp.groups["flags"] & L.FLAG_CSR_ONLY) != 0
     assert copy.sum() == 1 and dp.needs_zero == L.ZERO_ONCE  # structural gaps read as zero
     assert int(dp.units[-1][0]) == dp.n_waves - 1  # no extra CSR-only wave: sources are inputs
@@ -80,7 +81,7 @@ def test_broken_schedule_still_matches_interpreter(tmp_path):
     plan.kernels.append(plan.kernels.pop(0))
     inputs = np.random.default_rng(0).uniform(0.5, 2.0, plan.input_count)
     want = oracle.run_values(plan, inputs)
-    dp = lower_plan(plan)
+    dp = lower_plan(plan, jit=False)
     assert dp.needs_zero == L.ZERO_EVERY
     got = emu.run_values(dp, inputs)
     assert np.array_equal(bits(got), bits(want))
@@ -88,7 +89,7 @@ def test_broken_schedule_still_matches_interpreter(tmp_path):
 
 def test_tape_register_reuse_bounded():
     plan = load_plan("tests/golden/prog_energy-hessian_4x4_tag")
-    dp = lower_plan(plan)
+    dp = lower_plan(plan, jit=False)
     for kl, kp in zip(dp.kernels, plan.kernels):
         if kl.kind == KIND_TAPE:
             live = len(kp.template_arena.ops)
@@ -103,3 +104,20 @@ def test_sop_shapes():
     assert L.sop_shape([N, 0, 0]) == L.SOP_SHAPE_GENERIC  # one three-factor product
     assert L.sop_shape([N, 0, N]) == L.SOP_SHAPE_PAIRS
     assert L.sop_shape([N, N, 0]) == L.SOP_SHAPE_GENERIC
+
+
+@pytest.mark.parametrize("name", ["lmlt_w7", "prog_energy-hessian_4x4_tag", "transc37", "toy256_interleaved",
+                                  "tagged_pair", "acc9_lpow3_simp"])
+def test_specialised_tape_units_compile(name):
+    """jit.py: the tape units compile to sm_100a cubins with NVRTC (no GPU needed)."""
+    from conftest import Golden
+    from paper_2110_12865_b200 import jit
+
+    if not jit.available():
+        pytest.skip("NVRTC not available")
+    dp = lower_plan(Golden(name).plan, jit=True)
+    n_jit = sum(1 for u in range(len(dp.units)) if dp.unit(u)["flags"] & L.UNIT_JIT)
+    n_tape_plain = sum(1 for kl in dp.kernels if kl.kind == L.KIND_TAPE and not kl.flags & (L.FLAG_SELFREF | L.FLAG_SERIAL))
+    assert (n_jit > 0) == (n_tape_plain > 0)
+    if n_jit:
+        assert dp.jit_cubin[:4] == b"\x7fELF" and "sgb_tape_u" in dp.jit_source

@@ -26,6 +26,7 @@ for var in variants:
     os.environ["SGB_TAPE_VEC"] = env.get("vec", "0")
     os.environ["SGB_COMPRESS"] = env.get("compress", "1")
     os.environ["SGB_TILE_ORDER"] = env.get("order", "csr")
+    os.environ["SGB_TAPE_JIT"] = env.get("jit", "1")
     mode = env.get("mode", "csr")
     t0 = time.time()
     dp = DevicePlan(plan, lowered=lower_plan(plan))
