@@ -15,6 +15,6 @@ echo "bench rc=$?" >> $OUT/status.txt
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv \
    --log-file $OUT/launches.csv python tools/profile_run.py --evals 3 > $OUT/ncu_launches.log 2>&1
 echo "ncu launches rc=$?" >> $OUT/status.txt
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"sop|tape" -s 4 -c 4 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"sop|tape" -s 15 -c 15 \
    -o $OUT/prof_full python tools/profile_run.py --evals 2 > $OUT/ncu_full.log 2>&1
 echo "ncu full rc=$?" >> $OUT/status.txt
