@@ -1102,6 +1102,10 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
         if (u.grid > need) u.grid = need;
       }
     }
+    if (jit)
+      for (int g = u.g0; g < u.g1; ++g)
+        if (d->groups[g].flags & (FLAG_SELFREF | FLAG_SERIAL))
+          return fail(-1, "sgb_plan_create: self-referencing group in a specialised unit");
     for (int64_t t = u.t0; t < u.t1; ++t) {  // tiles name groups of this unit and start inside them
       const int32_t *tl = d->tiles + 2 * t;
       if (tl[0] < u.g0 || tl[0] >= u.g1 || tl[1] < 0 || (int64_t)tl[1] >= d->groups[tl[0]].n)

@@ -708,6 +708,11 @@ def _needs_zero(plan, waves, reads) -> int:
     return level
 
 
+def _copy_tape() -> np.ndarray:
+    """Tape of a copy group: store slot 0 as root 0."""
+    return np.array([(T_ST, 0, 0, 0, 0, 0, 0, 0)], dtype=TAPE_DTYPE)
+
+
 def _tile_keys(g: _Group, starts: np.ndarray, tile: int) -> np.ndarray:
     """Smallest output position in each tile (-1 for tiles without outputs)."""
     if g.opos is None or g.n == 0:
@@ -798,6 +803,11 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     for w in range(total_waves):
         members = [j for j, g in enumerate(groups) if g.wave == w]
         plan_units = []
+        if jit:  # every plain group of the wave (tape or sum-of-products) in one specialised kernel
+            sj = [j for j in members if not groups[j].flags & (FLAG_SELFREF | FLAG_SERIAL)]
+            if sj:
+                plan_units.append((KIND_TAPE, 1, JIT_BLOCK, 0, sj))
+            members = [j for j in members if j not in set(sj)]
         for plain in (True, False):
             tm = [j for j in members if groups[j].kind == KIND_TAPE and
                   plain == (not groups[j].flags & (FLAG_SELFREF | FLAG_SERIAL))]
@@ -808,9 +818,6 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
             if regs * bs * 8 > SMEM_LIMIT:
                 raise ValueError(f"wave {w}: template needs {regs} scratch registers, more than shared memory holds")
             vec = 1
-            if plain and jit:  # one instance per thread, registers instead of the scratch file
-                plan_units.append((KIND_TAPE, 1, JIT_BLOCK, 0, tm))
-                continue
             if plain:
                 forced = int(os.environ.get("SGB_TAPE_VEC", "0"))
                 for v in (TAPE_VECS if not forced else (forced,)):
@@ -834,14 +841,14 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                 rec = packed[gi]
                 rec["n"], rec["dest_base"], rec["p_off"], rec["c_off"] = g.n, g.dest_base, g.p_off, g.c_off
                 rec["n_roots"], rec["n_slots"], rec["n_ret"] = g.n_roots, len(g.slot_col), len(g.columns)
-                rec["n_const"], rec["kind"], rec["n_regs"], rec["unit"] = g.n_const, g.kind, g.n_regs, len(units)
+                rec["n_const"], rec["kind"], rec["n_regs"], rec["unit"] = g.n_const, kind, g.n_regs, len(units)
                 rec["slot_off"] = n_slot
                 scol.append(g.slot_col)
                 sdel.append(g.slot_delta)
                 n_slot += len(g.slot_col)
                 flags = g.flags
                 if kind == KIND_TAPE:
-                    jit_tapes[gi] = g.tape
+                    jit_tapes[gi] = g.tape if g.tape is not None else _copy_tape()
                     jit_imms[gi] = g.imms
                     t = assemble(g.tape, bs * variant, n_imm) if regs else np.zeros((0, 4), np.uint32)
                     rec["tape_off"], rec["tape_len"] = n_tape, len(t)
