@@ -178,6 +178,12 @@ def group_body(dp, gi: int, tape: np.ndarray, imms: list, batched: bool = False)
     return out
 
 
+def _check_stores(tape, n_roots: int, gi: int):
+    roots = sorted(int(t[7]) for t in tape.tolist() if t[0] == L.T_ST)
+    if roots != list(range(n_roots)):
+        raise ValueError(f"group {gi}: tape stores roots {roots}, expected 0..{n_roots - 1}")
+
+
 def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
     """Persistent kernels for tape unit ``u``: a case per group.
 
@@ -208,6 +214,7 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
         out += head
         for gi in range(unit["group_begin"], unit["group_end"]):
             rec = dp.groups[gi]
+            _check_stores(tapes[gi], int(rec["n_roots"]), gi)
             out.append(f"    case {gi}: {{")
             out.append(f"      if (i >= {int(rec['n'])}LL) break;")
             if rec["flags"] & L.FLAG_CSR_ONLY:

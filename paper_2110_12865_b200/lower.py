@@ -507,8 +507,8 @@ def lower_kernel(plan, kp, index: int) -> KernelLowering:
                 if not np.array_equal(inst, np.arange(kp.instances)[inside]):
                     flags |= FLAG_SERIAL
                     break
-    if sop is not None:
-        return KernelLowering(index, kp.name, KIND_SOP, flags, 0, np.zeros(0, TAPE_DTYPE), [],
+    if sop is not None:  # the tape is kept: specialised units (jit.py) compile every group from its tape
+        return KernelLowering(index, kp.name, KIND_SOP, flags, n_regs, tape, imms,
                               sop, slot_col, slot_delta, ops=fops)
     return KernelLowering(index, kp.name, KIND_TAPE, flags, n_regs, tape, imms,
                           np.zeros(0, np.int32), slot_col, slot_delta, ops=fops)
