@@ -76,7 +76,8 @@ typedef struct sgb_plan_desc {
   const int64_t *units;     /* [n_units][10]: wave, kind (0 tape, 1 sum-of-products), variant (tape VEC),
                                group_begin, group_end, tile_begin, tile_end, block_size,
                                scratch registers per lane, flags (1 = CSR mode only,
-                               2 = specialised tape unit in jit_cubin) */
+                               2 = specialised unit in jit_cubin, 4 = value mode only,
+                               8 = CSR windows: tile range = window range) */
   const int32_t *tiles;     /* [n_tiles][2]: group, first instance -- one block each, in launch order */
   int64_t n_tiles;
   const uint32_t *tape;     /* [tape_rows][4] device tape words, see lower.assemble() */
@@ -104,9 +105,13 @@ typedef struct sgb_plan_desc {
   int64_t n_opos32;
   const int64_t *outputs; /* ExecutionPlan.outputs */
   int64_t n_outputs;
-  const void *jit_cubin;  /* sm_100a cubin with the specialised tape units (units flag 2): kernels
-                             sgb_tape_u<unit> / sgb_tape_b<unit> (paper_2110_12865_b200/jit.py) */
+  const void *jit_cubin;  /* sm_100a cubin with the specialised units (units flag 2): kernels
+                             sgb_tape_u<unit> / sgb_tape_b<unit> / sgb_window_u<unit> (jit.py) */
   int64_t jit_cubin_size;
+  const int32_t *win_pieces; /* CSR windows (units flag 8): [n][4] group, first instance, count, item prefix */
+  int64_t n_win_pieces;
+  const int64_t *win_off;    /* [n_windows + 1] first piece of each window of 4096 outputs */
+  int64_t n_win_off;
 } sgb_plan_desc;
 
 /* Upload a device plan to `device`.  Replaces compile_plan (emit.py:198-245). */

@@ -57,8 +57,10 @@ enum : int {
 enum : int {
   U_WAVE = 0, U_KIND, U_VARIANT, U_G0, U_G1, U_T0, U_T1, U_BS, U_REGS, U_FLAGS, U_COUNT
 };
-enum : int { UNIT_CSR_ONLY = 1, UNIT_JIT = 2 };
+enum : int { UNIT_CSR_ONLY = 1, UNIT_JIT = 2, UNIT_VALUE_ONLY = 4, UNIT_WINDOW = 8 };
 constexpr int JIT_BLOCK = 256;  // jit.py JIT_BLOCK
+constexpr int WIN = 4096;       // lower.WIN: outputs per CSR window
+constexpr int MAX_WINDOW_PIECES = 512;  // jit.MAX_WINDOW_PIECES
 constexpr int PRE = 8;        // slot loads kept in flight by the tape prologue
 constexpr int SOP_BS = 256;   // sum-of-products block
 constexpr int SOP_BATCH = 16; // factor loads in flight per instance
@@ -778,6 +780,8 @@ struct sgb_plan {
   uint16_t *d_coff = nullptr, *d_ooff = nullptr;
   SopDesc *d_sopd = nullptr;
   cudaLibrary_t jit_lib = nullptr;
+  int4 *d_wpieces = nullptr;
+  int64_t *d_woff = nullptr;
   uint32_t *d_fbase = nullptr;
   // workspace for the host-buffer entry points
   std::mutex ws_mu;
@@ -829,6 +833,17 @@ void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_
   if ((u.flags & UNIT_CSR_ONLY) && !csr) return;
   const int64_t blocks = batched ? u.bt1 - u.bt0 : u.t1 - u.t0;
   if (blocks <= 0) return;
+  if (!batched && csr && (u.flags & UNIT_VALUE_ONLY)) return;
+  if (u.flags & UNIT_WINDOW) {  // CSR windows (jit.py window_source)
+    const int4 *pieces = p->d_wpieces;
+    const int64_t *woff = p->d_woff + u.t0;
+    int64_t n = u.t1 - u.t0, w0 = u.t0, n_out = p->n_out;
+    Tables T = p->T;
+    void *args[] = {&T, &pieces, &woff, &n, &w0, &x, &out, &n_out};
+    cudaLaunchKernel(u.jit, dim3((unsigned)u.grid), dim3(JIT_BLOCK), args, (size_t)WIN * sizeof(double), s);
+    return;
+  }
+  if ((u.flags & UNIT_CSR_ONLY) && batched) return;
   if (u.flags & UNIT_JIT) {  // specialised straight-line kernels (jit.py)
     const int2 *tiles = batched ? p->d_btiles + u.bt0 : p->d_tiles + u.t0;
     int64_t n = blocks;
@@ -924,7 +939,8 @@ void sgb_plan_destroy(sgb_plan *p) {
   cudaSetDevice(p->device);
   void *bufs[] = {p->d_groups, p->d_tiles, p->d_btiles, p->d_outputs, p->d_tape, p->d_imm, p->d_con,
                   p->d_sop, p->d_scol, p->d_sdel, p->d_pos, p->d_x, p->d_out, p->d_cbase, p->d_coff,
-                  p->d_obase, p->d_ooff, p->d_opos32, p->d_sopd, p->d_fbase, p->d_outputs32};
+                  p->d_obase, p->d_ooff, p->d_opos32, p->d_sopd, p->d_fbase, p->d_outputs32,
+                  p->d_wpieces, p->d_woff};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (p->ws_stream) cudaStreamDestroy(p->ws_stream);
@@ -1066,7 +1082,31 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
     u.index = k;
     const bool csr_only = u.flags & UNIT_CSR_ONLY;
     const bool jit = u.flags & UNIT_JIT;
-    if (jit) {
+    const bool window = u.flags & UNIT_WINDOW;
+    if (window) {
+      if (!jit || !csr_only || !p->jit_lib || u.t0 < 0 || u.t1 >= d->n_win_off)
+        return fail(-1, "sgb_plan_create: bad CSR-window unit " + std::to_string(k));
+      cudaKernel_t kw;
+      const std::string nw = "sgb_window_u" + std::to_string(k);
+      SGB_CUDA(cudaLibraryGetKernel(&kw, p->jit_lib, nw.c_str()));
+      u.jit = (const void *)kw;
+      for (int64_t w = u.t0; w < u.t1; ++w) {  // pieces: groups of this unit, instance ranges inside them,
+        const int64_t a = d->win_off[w], b = d->win_off[w + 1];  // running item prefix, window positions
+        if (a < 0 || b < a || b > d->n_win_pieces || b - a > MAX_WINDOW_PIECES)
+          return fail(-1, "sgb_plan_create: bad CSR-window piece range");
+        int64_t prefix = 0;
+        for (int64_t q = a; q < b; ++q) {
+          const int32_t *pc = d->win_pieces + 4 * q;
+          if (pc[0] < u.g0 || pc[0] >= u.g1 || pc[1] < 0 || pc[2] < 1 ||
+              (int64_t)pc[1] + pc[2] > d->groups[pc[0]].n || pc[3] != prefix ||
+              !(d->groups[pc[0]].flags & (FLAG_OPOS16 | FLAG_OPOS32)))
+            return fail(-1, "sgb_plan_create: bad CSR-window piece");
+          prefix += pc[2];
+        }
+        if (prefix >= ((int64_t)1 << 31)) return fail(-1, "sgb_plan_create: CSR window too large");
+      }
+      if ((u.t1 - u.t0) * (int64_t)WIN < d->n_outputs) return fail(-1, "sgb_plan_create: CSR windows miss outputs");
+    } else if (jit) {
       if (u.kind != KIND_TAPE || u.bs != JIT_BLOCK || u.variant != 1 || !p->jit_lib)
         return fail(-1, "sgb_plan_create: specialised unit " + std::to_string(k) + " without its kernels");
       cudaKernel_t kf, kb;
@@ -1086,7 +1126,11 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
     max_wave = u.wave > max_wave ? u.wave : max_wave;
     {  // persistent grid: resident capacity of the chip, at most one block (warp for SOP) per tile
       int nb = 0;
-      if (jit) {
+      if (window) {
+        SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, u.jit, JIT_BLOCK, (size_t)WIN * sizeof(double)));
+        u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
+        if (u.grid > u.t1 - u.t0) u.grid = u.t1 - u.t0;
+      } else if (jit) {
         SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, u.jit, JIT_BLOCK, 0));
         u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
         if (u.grid > u.t1 - u.t0) u.grid = u.t1 - u.t0;
@@ -1106,7 +1150,7 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       for (int g = u.g0; g < u.g1; ++g)
         if (d->groups[g].flags & (FLAG_SELFREF | FLAG_SERIAL))
           return fail(-1, "sgb_plan_create: self-referencing group in a specialised unit");
-    for (int64_t t = u.t0; t < u.t1; ++t) {  // tiles name groups of this unit and start inside them
+    for (int64_t t = window ? u.t1 : u.t0; t < u.t1; ++t) {  // tiles name groups of this unit, start inside them
       const int32_t *tl = d->tiles + 2 * t;
       if (tl[0] < u.g0 || tl[0] >= u.g1 || tl[1] < 0 || (int64_t)tl[1] >= d->groups[tl[0]].n)
         return fail(-1, "sgb_plan_create: bad tile in unit " + std::to_string(k));
@@ -1120,10 +1164,11 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       if (u.kind == KIND_TAPE && (G.flags & FLAG_SERIAL) && u.variant != 1)
         return fail(-1, "sgb_plan_create: serial group in a vectorised tape unit");
     }
-    // batched tiles: one instance per warp (tape blocks are the unit's scratch stride wide)
+    // batched tiles: one instance per warp (tape blocks are the unit's scratch stride wide);
+    // CSR windows are single-set only (batched CSR = batched values + gather)
     const int bwarps = u.kind == KIND_TAPE ? (u.bs * u.variant) / 32 : BATCH_WARPS;
     u.bt0 = (int64_t)btiles.size();
-    for (int g = u.g0; g < u.g1; ++g) {
+    for (int g = window ? u.g1 : u.g0; g < u.g1; ++g) {
       const sgb_group &G = d->groups[g];
       if (G.flags & FLAG_SERIAL) {
         if (G.n > 0) btiles.push_back(make_int2(g, 0));
@@ -1231,6 +1276,8 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       (rc = upload(&p->d_opos32, d->opos32, d->n_opos32)) ||
       (rc = upload(&p->d_sopd, sopd.data(), (int64_t)sopd.size())) ||
       (rc = upload(&p->d_outputs32, outputs32.data(), (int64_t)outputs32.size())) ||
+      (rc = upload(&p->d_wpieces, reinterpret_cast<const int4 *>(d->win_pieces), d->n_win_pieces)) ||
+      (rc = upload(&p->d_woff, d->win_off, d->n_win_off)) ||
       (rc = upload(&p->d_fbase, fbase.data(), (int64_t)fbase.size())))
     return rc;
   p->T = Tables{p->d_groups, p->d_tape, p->d_imm, p->d_sop, p->d_scol, p->d_sdel, p->d_pos,
@@ -1283,7 +1330,7 @@ static int launch_gather(sgb_plan *p, const double *x, int64_t ld, int64_t batch
 static int launch_all(sgb_plan *p, double *x, int64_t ld, int64_t batch, bool batched, double *out, int64_t ld_out,
                       bool csr, cudaStream_t s) {
   std::lock_guard<std::mutex> lk(p->run_mu);
-  const bool direct = csr && p->direct_csr;
+  const bool direct = csr && p->direct_csr && !batched;  // batched CSR: batched values + gather
   const int waves = direct ? p->csr_waves : p->n_waves;
   for (int w = 0; w < waves; ++w) {
     int rc = launch_wave(p, w, x, ld, batch, batched, out, ld_out, direct, s);

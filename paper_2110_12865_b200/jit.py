@@ -108,10 +108,12 @@ def _out_pos(rec, r: int) -> str | None:
     return None
 
 
-def group_body(dp, gi: int, tape: np.ndarray, imms: list, batched: bool = False) -> list[str]:
+def group_body(dp, gi: int, tape: np.ndarray, imms: list, batched: bool = False, window: bool = False) -> list[str]:
     """Straight-line CUDA for instance ``i`` of packed group ``gi`` (register tape -> SSA).
 
-    Batched: value set ``b`` of ``X[addr * ld + b]`` (lane = value set).
+    Batched: value set ``b`` of ``X[addr * ld + b]`` (lane = value set).  Window:
+    the CSR value goes to the block's shared window ``buf[o - kwin_]`` (no
+    value-array store: window members are never re-read).
     """
     X = (lambda a: f"x + (u64)({a}) * ld + b") if batched else (lambda a: f"x + ({a})")
     rec = dp.groups[gi]
@@ -144,6 +146,9 @@ def group_body(dp, gi: int, tape: np.ndarray, imms: list, batched: bool = False)
         A = ("-" if na else "") + reg.get(a, "0.0")
         B = ("-" if nb else "") + reg.get(b, "0.0")
         C = reg.get(c, "0.0")
+        if op == L.T_ST and window:
+            out.append(f"{{ const u32 o = {_out_pos(rec, aux)}; if (o != NONE) buf[o - kwin_] = {reg[a]}; }}")
+            continue
         if op == L.T_ST:
             r = aux
             v = reg[a]
@@ -293,9 +298,52 @@ def compile_cubin(src: str, name: str = "sgb_tape.cu") -> bytes:
     return cubin
 
 
+MAX_WINDOW_PIECES = 512
+
+
+def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
+    """CSR-window kernel of unit ``u``: a block assembles WIN consecutive outputs in shared
+    memory from its window's pieces (group, instance range), then writes them coalesced."""
+    unit = dp.unit(u)
+    out = [f'extern "C" __global__ void __launch_bounds__({JIT_BLOCK}) sgb_window_u{u}(',
+           "    Tables T, const int4 *pieces, const i64 *win_off, i64 n_win, i64 w0, double *x, double *out,",
+           "    i64 n_out) {",
+           "  extern __shared__ double buf[];",
+           f"  __shared__ int4 sp[{MAX_WINDOW_PIECES}];",
+           "  for (i64 w = blockIdx.x; w < n_win; w += gridDim.x) {",
+           "    const i64 p0 = win_off[w], np_ = win_off[w + 1] - p0;",
+           "    for (i64 j = threadIdx.x; j < np_; j += blockDim.x) sp[j] = pieces[p0 + j];",
+           "    __syncthreads();",
+           f"    const i64 kwin_ = (w0 + w) * {L.WIN}LL;",
+           "    const int total = np_ ? sp[np_ - 1].w + sp[np_ - 1].z : 0;",
+           "    int p = 0;",
+           "    for (int item = threadIdx.x; item < total; item += blockDim.x) {",
+           "      while (p + 1 < np_ && sp[p + 1].w <= item) ++p;",
+           "      const i64 i = (i64)sp[p].y + (item - sp[p].w);",
+           "      switch (sp[p].x) {"]
+    for gi in range(unit["group_begin"], unit["group_end"]):
+        _check_stores(tapes[gi], int(dp.groups[gi]["n_roots"]), gi)
+        out.append(f"      case {gi}: {{")
+        out += ["        " + ln for ln in group_body(dp, gi, tapes[gi], imms[gi], window=True)]
+        out.append("      } break;")
+    out += ["      default: break;", "      }", "    }", "    __syncthreads();",
+            f"    const i64 cnt = n_out - kwin_ < {L.WIN}LL ? n_out - kwin_ : {L.WIN}LL;",
+            "    for (i64 j = threadIdx.x; j < cnt; j += blockDim.x) __stcs(out + kwin_ + j, buf[j]);",
+            "    __syncthreads();", "  }", "}", ""]
+    return "\n".join(out)
+
+
 def specialise(dp, tapes: dict, imms: dict, units: list[int]) -> tuple[bytes, str]:
     """Compile the given tape units of a lowered plan; returns (cubin, source)."""
-    src = _PREAMBLE + "\n".join(unit_source(dp, u, tapes, imms) for u in units)
+    parts = []
+    for u in units:
+        if dp.unit(u)["flags"] & L.UNIT_WINDOW:
+            if dp.win_off is not None and len(dp.win_off) > 1 and int(np.diff(dp.win_off).max()) > MAX_WINDOW_PIECES:
+                raise ValueError("a CSR window has more pieces than the kernel stages")
+            parts.append(window_source(dp, u, tapes, imms))
+        else:
+            parts.append(unit_source(dp, u, tapes, imms))
+    src = _PREAMBLE + "\n".join(parts)
     return compile_cubin(src), src
 
 

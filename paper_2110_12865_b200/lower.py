@@ -50,6 +50,9 @@ FLAG_CSR_ONLY = 512  # synthetic copy group: runs in CSR mode only
 FLAG_COHERENT = 1024  # one retained column: every slot is column 0 + delta
 UNIT_CSR_ONLY = 1
 UNIT_JIT = 2  # tape unit compiled to straight-line code (jit.py), one instance per thread
+UNIT_VALUE_ONLY = 4  # value-mode twin of a CSR-window unit (skipped by sgb_run_csr)
+UNIT_WINDOW = 8  # CSR windows: each block assembles WIN consecutive outputs in shared memory
+WIN = 4096  # outputs per CSR window (32 KB of shared memory)
 JIT_BLOCK = 256
 CHUNK = 32  # instances per compressed-index chunk (one warp in single-set mode)
 NONE32 = 0xFFFFFFFF
@@ -119,6 +122,9 @@ class DevicePlanArrays:
     exact: bool = True
     jit_cubin: bytes = b""  # specialised tape units (UNIT_JIT): kernels sgb_tape_u<unit>, see jit.py
     jit_source: str = ""
+    win_pieces: np.ndarray = None  # int32 [n, 4]: group, first instance, count, item prefix (CSR windows)
+    win_off: np.ndarray = None  # int64 [n_windows + 1]: first piece of each window
+    window_units: list = field(default_factory=list)
 
     def unit(self, u: int) -> dict:
         return dict(zip(UNIT_FIELDS, (int(v) for v in self.units[u])))
@@ -634,6 +640,8 @@ class _Group:
     sop: np.ndarray = None
     opos: np.ndarray = None  # (n_roots, n) int64 output positions, NONE32 = not an output
     kernel: int = -1
+    window_value: bool = False  # value-mode twin of a CSR-window member (runs in value mode only)
+    window: bool = False  # CSR-window member (window unit, CSR mode only)
 
 
 def _output_map(plan, lowered, waves):
@@ -708,6 +716,65 @@ def _needs_zero(plan, waves, reads) -> int:
     return level
 
 
+def _window_members(plan, lowered, opos, n_waves):
+    """Kernel indices whose outputs a CSR-window unit can assemble, or None.
+
+    Requires every output-producing group of the last wave to be a plain,
+    single-root, never re-read group whose output positions increase with the
+    instance (each window then takes one contiguous instance range of it) and
+    every other output to be final before the last wave (copy pieces).
+    """
+    if n_waves == 0 or not len(plan.outputs):
+        return None
+    last = n_waves - 1
+    members = []
+    for kl, o in zip(lowered, opos):
+        if o is None or kl.wave != last:
+            continue
+        if kl.flags & (FLAG_SELFREF | FLAG_SERIAL) or o.shape[0] != 1:
+            return None
+        v = o[0][o[0] != NONE32]
+        if v.size > 1 and not np.all(np.diff(v) > 0):
+            return None
+        members.append(kl.index)
+    if not members:
+        return None
+    # outputs not produced by members must come from inputs or earlier waves
+    outs = np.asarray(plan.outputs, dtype=np.int64)
+    covered = np.zeros(outs.size, bool)
+    for kl, o in zip(lowered, opos):
+        if o is not None and kl.index in set(members):
+            covered[o[o != NONE32]] = True
+    rest = outs[~covered]
+    waves = [kl.wave for kl in lowered]
+    if rest.size and np.any(_owner_waves(plan, waves, rest) >= last):
+        return None
+    return members
+
+
+def _window_pieces(packed, gis, n_out, pieces, win_off, win_opos):
+    """Per CSR window [k0, k0 + WIN): one (group, first instance, count, prefix) piece per member."""
+    n_win = (n_out + WIN - 1) // WIN
+    starts = np.arange(n_win, dtype=np.int64) * WIN
+    per = []  # per member: (gi, lo idx, hi idx) arrays over windows
+    for gi in gis:
+        o = win_opos[gi]
+        valid = np.nonzero(o != NONE32)[0]
+        ov = o[valid]
+        lo = np.searchsorted(ov, starts)
+        hi = np.searchsorted(ov, starts + WIN)
+        per.append((gi, valid, lo, hi))
+    for w in range(n_win):
+        prefix = 0
+        for gi, valid, lo, hi in per:
+            if hi[w] > lo[w]:
+                i0 = int(valid[lo[w]])
+                cnt = int(valid[hi[w] - 1]) - i0 + 1
+                pieces.append((gi, i0, cnt, prefix))
+                prefix += cnt
+        win_off.append(len(pieces))
+
+
 def _copy_tape() -> np.ndarray:
     """Tape of a copy group: store slot 0 as root 0."""
     return np.array([(T_ST, 0, 0, 0, 0, 0, 0, 0)], dtype=TAPE_DTYPE)
@@ -723,7 +790,7 @@ def _tile_keys(g: _Group, starts: np.ndarray, tile: int) -> np.ndarray:
 
 
 def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = None,
-               jit: bool | None = None) -> DevicePlanArrays:
+               jit: bool | None = None, csr_window: bool | None = None) -> DevicePlanArrays:
     """ExecutionPlan -> device plan.
 
     ``direct_csr``: output groups store their CSR values through output-position
@@ -742,6 +809,9 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         from . import jit as _jit
 
         jit = _jit.available()
+    if csr_window is None:  # CSR windows of the last wave (specialised units only), see _window_plan
+        csr_window = os.environ.get("SGB_CSR_WINDOW", "1") != "0"
+    csr_window = bool(csr_window and jit)
     read_sets = _read_sets(plan)
     waves = compute_waves(plan, read_sets)
     lowered = [lower_kernel(plan, kp, k) for k, kp in enumerate(plan.kernels)]
@@ -749,7 +819,21 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         kl.wave = w
     n_waves = (max(waves) + 1) if waves else 0
     opos, res_k, res_addr = _output_map(plan, lowered, waves)
-    if not direct_csr:
+    window = _window_members(plan, lowered, opos, n_waves) if csr_window and not direct_csr else None
+    if window is not None:
+        # CSR windows: only last-wave members keep output positions; every other output
+        # (inputs, duplicates, earlier waves' results) is a copy piece of its window
+        keep = set(window)
+        opos = [o if kl.index in keep else None for kl, o in zip(lowered, opos)]
+        outs = np.asarray(plan.outputs, dtype=np.int64)
+        covered = np.zeros(outs.size, bool)
+        for o in opos:
+            if o is not None:
+                v = o[o != NONE32]
+                covered[v] = True
+        res_k = np.nonzero(~covered)[0]
+        res_addr = outs[res_k]
+    elif not direct_csr:
         opos = [None] * len(lowered)
         res_k = res_addr = np.zeros(0, np.int64)
     # copy groups: outputs that are inputs, duplicates or padding (CSR mode only)
@@ -760,6 +844,7 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     reads = [r for r in read_sets if r.size] + ([res_addr] if res_addr.size else [])
     allr = np.unique(np.concatenate(reads)) if reads else np.zeros(0, np.int64)
     groups: list[_Group] = []
+    win_groups: list[_Group] = []  # window members (CSR-only records; value-mode twins stay in `groups`)
     for kl in lowered:
         kp = plan.kernels[kl.index]
         lo, hi = kp.dest_base, kp.dest_base + kp.n_roots * kp.instances
@@ -770,9 +855,16 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         seg = np.asarray(plan.positions[kp.p_base: kp.p_base + r * n], dtype=np.int64)
         cols = list(seg.reshape(r, n) if kp.layout == "coalesced" else seg.reshape(n, r).T)
         flags = kl.flags | (FLAG_COHERENT if r == 1 and kp.pos_vars else 0)
+        in_window = window is not None and kl.index in window
         groups.append(_Group(kl.kind, flags, n, kp.n_roots, kp.dest_base, kp.p_base, kp.c_base,
                              len(kp.const_vars), kl.slot_col, kl.slot_delta, cols, kp.layout, kl.wave,
-                             kl.n_regs, kl.tape, kl.imms, kl.sop, opos[kl.index], kl.index))
+                             kl.n_regs, kl.tape, kl.imms, kl.sop, None if in_window else opos[kl.index],
+                             kl.index, window_value=in_window))
+        if in_window:
+            win_groups.append(_Group(kl.kind, flags | FLAG_CSR_ONLY, n, kp.n_roots, kp.dest_base, kp.p_base,
+                                     kp.c_base, len(kp.const_vars), kl.slot_col, kl.slot_delta, cols, kp.layout,
+                                     kl.wave, kl.n_regs, kl.tape, kl.imms, kl.sop, opos[kl.index], kl.index,
+                                     window=True))
     extra_pos = []
     p_next = int(np.asarray(plan.positions).size)
     copy_waves = []
@@ -782,15 +874,18 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         addr, kk = res_addr[sel], res_k[sel]
         ordr = np.argsort(kk, kind="stable")  # CSR order: coalesced stores
         addr, kk = addr[ordr], kk[ordr]
-        groups.append(_Group(KIND_SOP, FLAG_CSR_ONLY | FLAG_STREAM | FLAG_COHERENT | FLAG_EXACT, int(addr.size), 1,
-                             int(plan.input_count), p_next, 0, 0, np.zeros(1, np.int32), np.zeros(1, np.int64),
-                             [addr], "coalesced", wv, sop=np.array([SOP_NEWTERM], np.int32),
-                             opos=kk.reshape(1, -1)))
+        cg = _Group(KIND_SOP, FLAG_CSR_ONLY | FLAG_STREAM | FLAG_COHERENT | FLAG_EXACT, int(addr.size), 1,
+                    int(plan.input_count), p_next, 0, 0, np.zeros(1, np.int32), np.zeros(1, np.int64),
+                    [addr], "coalesced", wv, sop=np.array([SOP_NEWTERM], np.int32),
+                    opos=kk.reshape(1, -1), window=window is not None)
+        (win_groups if window is not None else groups).append(cg)
         extra_pos.append(addr.astype(np.uint32))
         p_next += addr.size
         copy_waves.append(wv)
     needs_zero = _needs_zero(plan, waves, list(zip(waves, read_sets)) +
-                             [(g.wave, g.columns[0]) for g in groups if g.flags & FLAG_CSR_ONLY])
+                             [(g.wave, g.columns[0]) for g in groups + win_groups
+                              if g.flags & FLAG_CSR_ONLY and g.tape is None])
+    groups = groups + win_groups
     total_waves = max([n_waves] + [w + 1 for w in copy_waves])
 
     # -- launch units and tiles ---------------------------------------------------------
@@ -800,13 +895,21 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     tapes, imms, sops, scol, sdel, cbases, coffs, obases, ooffs, op32 = ([] for _ in range(10))
     n_tape = n_imm = n_sop = n_slot = n_cb = n_co = n_ob = n_oo = n_o32 = 0
     jit_tapes, jit_imms, jit_units = {}, {}, []
+    win_pieces: list = []
+    win_off = [0]
+    win_opos: dict = {}
+    window_units: list = []
+    n_out_total = len(plan.outputs)
     for w in range(total_waves):
         members = [j for j, g in enumerate(groups) if g.wave == w]
         plan_units = []
         if jit:  # every plain group of the wave (tape or sum-of-products) in one specialised kernel
             sj = [j for j in members if not groups[j].flags & (FLAG_SELFREF | FLAG_SERIAL)]
-            if sj:
-                plan_units.append((KIND_TAPE, 1, JIT_BLOCK, 0, sj))
+            for sel, tag in (([j for j in sj if not groups[j].window and not groups[j].window_value], 0),
+                             ([j for j in sj if groups[j].window_value], UNIT_VALUE_ONLY),
+                             ([j for j in sj if groups[j].window], UNIT_WINDOW)):
+                if sel:
+                    plan_units.append((KIND_TAPE, 1, JIT_BLOCK, tag, sel))
             members = [j for j in members if j not in set(sj)]
         for plain in (True, False):
             tm = [j for j in members if groups[j].kind == KIND_TAPE and
@@ -832,6 +935,10 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         for code in sorted(codes):  # one persistent launch per kernel body
             plan_units.append((KIND_SOP, code, SOP_BLOCK, 0, codes[code]))
         for kind, variant, bs, regs, ms in plan_units:
+            utag = 0
+            if kind == KIND_TAPE and bs == JIT_BLOCK and variant == 1 and regs in (0, UNIT_VALUE_ONLY, UNIT_WINDOW) \
+                    and all(not groups[j].flags & (FLAG_SELFREF | FLAG_SERIAL) for j in ms) and jit:
+                utag, regs = regs, 0
             g_begin = len(order_groups)
             unit_tiles, unit_keys = [], []
             for j in ms:
@@ -883,6 +990,8 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                                 n_cb += cb.size
                                 n_co += co.size
                 # output positions
+                if g.window:
+                    win_opos[gi] = g.opos[0]
                 if g.opos is not None:
                     comp = [compress_column(row, allow_none=True) for row in g.opos]
                     if all(c is not None for c in comp):
@@ -905,8 +1014,19 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                     starts = np.arange(0, g.n, tile, dtype=np.int64)
                 unit_tiles.append(np.stack([np.full(starts.size, gi, np.int64), starts], axis=1))
                 unit_keys.append(_tile_keys(g, starts, tile))
-            t = np.concatenate(unit_tiles) if unit_tiles else np.zeros((0, 2), np.int64)
-            keys = np.concatenate(unit_keys) if unit_keys else np.zeros(0, np.int64)
+            if utag == UNIT_WINDOW:
+                t = np.zeros((0, 2), np.int64)
+                keys = np.zeros(0, np.int64)
+                w0 = len(win_off) - 1
+                _window_pieces(packed, list(range(g_begin, len(order_groups))), n_out_total, win_pieces, win_off,
+                               win_opos)
+                t = np.zeros((len(win_off) - 1 - w0, 2), np.int64)  # placeholder rows: the unit's windows
+                t[:, 1] = np.arange(w0, len(win_off) - 1)
+                window_units.append((len(units), w0, len(win_off) - 1))
+                keys = np.full(len(t), -1, np.int64)
+            else:
+                t = np.concatenate(unit_tiles) if unit_tiles else np.zeros((0, 2), np.int64)
+                keys = np.concatenate(unit_keys) if unit_keys else np.zeros(0, np.int64)
             if np.any(keys >= 0) and os.environ.get("SGB_TILE_ORDER", "csr") == "csr":
                 # CSR-ordered schedule: partial sectors of the output merge in L2
                 t = t[np.argsort(keys, kind="stable")]
@@ -916,6 +1036,10 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
             if kind == KIND_TAPE and regs == 0:
                 uflags |= UNIT_JIT
                 jit_units.append(len(units))
+            if utag == UNIT_VALUE_ONLY:
+                uflags |= UNIT_VALUE_ONLY
+            elif utag == UNIT_WINDOW:
+                uflags |= UNIT_WINDOW | UNIT_CSR_ONLY
             units.append((w, kind, variant, g_begin, len(order_groups), t0, t0 + len(t), bs, regs, uflags))
     cat = lambda xs, dt: (np.concatenate(xs).astype(dt) if xs and sum(len(x) for x in xs)  # noqa: E731
                           else np.zeros(0, dt))
@@ -945,9 +1069,12 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         input_count=int(plan.input_count),
         needs_zero=int(needs_zero),
         kernels=lowered,
-        copies=[(g.wave, g.columns[0], g.opos[0]) for g in groups if g.flags & FLAG_CSR_ONLY],
+        copies=[(g.wave, g.columns[0], g.opos[0]) for g in groups if g.flags & FLAG_CSR_ONLY and g.tape is None],
         exact=exact,
     )
+    dp.win_pieces = np.asarray(win_pieces, np.int32).reshape(-1, 4)
+    dp.win_off = np.asarray(win_off, np.int64)
+    dp.window_units = window_units
     if jit_units:
         from . import jit as _jit
 

@@ -79,6 +79,10 @@ class _Desc(ctypes.Structure):
         ("n_outputs", ctypes.c_int64),
         ("jit_cubin", ctypes.c_void_p),
         ("jit_cubin_size", ctypes.c_int64),
+        ("win_pieces", ctypes.c_void_p),
+        ("n_win_pieces", ctypes.c_int64),
+        ("win_off", ctypes.c_void_p),
+        ("n_win_off", ctypes.c_int64),
     ]
 
 
@@ -181,6 +185,9 @@ class DevicePlan:
             opos32=np.ascontiguousarray(lw.opos32, np.uint32),
             outs=np.ascontiguousarray(lw.outputs, np.int64),
             cubin=np.frombuffer(lw.jit_cubin, dtype=np.uint8).copy() if lw.jit_cubin else np.zeros(0, np.uint8),
+            wpieces=np.ascontiguousarray(lw.win_pieces if lw.win_pieces is not None else np.zeros((0, 4)),
+                                         np.int32).reshape(-1, 4),
+            woff=np.ascontiguousarray(lw.win_off if lw.win_off is not None else np.zeros(1), np.int64),
         )
         d = _Desc(
             value_array_size=self.value_array_size, input_count=self.input_count,
@@ -197,6 +204,8 @@ class DevicePlan:
             ooff=_ptr(keep["ooff"]), n_ooff=keep["ooff"].size, opos32=_ptr(keep["opos32"]),
             n_opos32=keep["opos32"].size, outputs=_ptr(keep["outs"]), n_outputs=keep["outs"].size,
             jit_cubin=_ptr(keep["cubin"]), jit_cubin_size=keep["cubin"].size,
+            win_pieces=_ptr(keep["wpieces"]), n_win_pieces=keep["wpieces"].shape[0],
+            win_off=_ptr(keep["woff"]), n_win_off=keep["woff"].size,
         )
         torch.cuda.init()
         _check(self._lib.sgb_plan_create(ctypes.byref(d), self.device, ctypes.byref(self._handle)),

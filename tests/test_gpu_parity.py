@@ -77,15 +77,17 @@ def test_device_resident_run_on_torch(golden):
     assert out.shape[0] == len(golden.plan.outputs)
 
 
-@pytest.mark.parametrize("direct", [False, True])
-def test_csr_mode(golden, direct):
-    """sgb_run_csr: value waves + gather, or (direct) producers store CSR values and copy groups
-    cover inputs / duplicates."""
+@pytest.mark.parametrize("mode", ["gather", "window", "direct", "interpreter"])
+def test_csr_mode(golden, mode):
+    """sgb_run_csr: value waves + gather; CSR windows (last-wave outputs assembled in shared memory,
+    coalesced stores); direct scattered stores; the hand-written kernels only (gather)."""
     import torch
 
     from paper_2110_12865_b200 import DevicePlan, lower_plan
 
-    dp = DevicePlan(golden.plan, lowered=lower_plan(golden.plan, direct_csr=direct))
+    kw = {"gather": dict(csr_window=False), "window": dict(csr_window=True), "direct": dict(direct_csr=True),
+          "interpreter": dict(jit=False)}[mode]
+    dp = DevicePlan(golden.plan, lowered=lower_plan(golden.plan, **kw))
     x = dp.new_values(golden.inputs)
     out = torch.full((len(golden.plan.outputs),), float("nan"), dtype=torch.float64, device=x.device)
     dp.run_csr(x, out)
