@@ -1117,7 +1117,8 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       u.jitb = (const void *)kb;
     }
     if (u.g0 < 0 || u.g1 > d->n_groups || u.g0 > u.g1 || u.wave < 0 ||
-        (csr_only ? u.wave != d->n_waves : u.wave >= d->n_waves) || u.t0 < 0 || u.t1 > d->n_tiles ||
+        (csr_only ? u.wave > d->n_waves : u.wave >= d->n_waves) || u.t0 < 0 ||
+        (!(u.flags & UNIT_WINDOW) && u.t1 > d->n_tiles) ||
         u.t0 > u.t1 || (u.kind != KIND_TAPE && u.kind != KIND_SOP) ||
         (u.kind == KIND_TAPE && !jit && (u.bs != 32 && u.bs != 64 && u.bs != 128)) ||
         (u.kind == KIND_TAPE && (u.variant != 1 && u.variant != 2 && u.variant != 4)) ||

@@ -1014,16 +1014,15 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                     starts = np.arange(0, g.n, tile, dtype=np.int64)
                 unit_tiles.append(np.stack([np.full(starts.size, gi, np.int64), starts], axis=1))
                 unit_keys.append(_tile_keys(g, starts, tile))
-            if utag == UNIT_WINDOW:
-                t = np.zeros((0, 2), np.int64)
-                keys = np.zeros(0, np.int64)
+            if utag == UNIT_WINDOW:  # the unit's tile range is its window range [w0, w1) in win_off
                 w0 = len(win_off) - 1
                 _window_pieces(packed, list(range(g_begin, len(order_groups))), n_out_total, win_pieces, win_off,
                                win_opos)
-                t = np.zeros((len(win_off) - 1 - w0, 2), np.int64)  # placeholder rows: the unit's windows
-                t[:, 1] = np.arange(w0, len(win_off) - 1)
                 window_units.append((len(units), w0, len(win_off) - 1))
-                keys = np.full(len(t), -1, np.int64)
+                units.append((w, kind, variant, g_begin, len(order_groups), w0, len(win_off) - 1, bs, regs,
+                              UNIT_CSR_ONLY | UNIT_JIT | UNIT_WINDOW))
+                jit_units.append(len(units) - 1)
+                continue
             else:
                 t = np.concatenate(unit_tiles) if unit_tiles else np.zeros((0, 2), np.int64)
                 keys = np.concatenate(unit_keys) if unit_keys else np.zeros(0, np.int64)
