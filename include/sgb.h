@@ -110,7 +110,7 @@ typedef struct sgb_plan_desc {
   int64_t jit_cubin_size;
   const int32_t *win_pieces; /* CSR windows (units flag 8): [n][4] group, first instance, count, item prefix */
   int64_t n_win_pieces;
-  const int64_t *win_off;    /* [n_windows + 1] first piece of each window of 4096 outputs */
+  const int64_t *win_off;    /* [n_windows + 1] first piece of each window of 2048 outputs */
   int64_t n_win_off;
 } sgb_plan_desc;
 

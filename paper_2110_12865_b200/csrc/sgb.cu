@@ -59,7 +59,7 @@ enum : int {
 };
 enum : int { UNIT_CSR_ONLY = 1, UNIT_JIT = 2, UNIT_VALUE_ONLY = 4, UNIT_WINDOW = 8 };
 constexpr int JIT_BLOCK = 256;  // jit.py JIT_BLOCK
-constexpr int WIN = 4096;       // lower.WIN: outputs per CSR window
+constexpr int WIN = 2048;       // lower.WIN: outputs per CSR window
 constexpr int MAX_WINDOW_PIECES = 512;  // jit.MAX_WINDOW_PIECES
 constexpr int PRE = 8;        // slot loads kept in flight by the tape prologue
 constexpr int SOP_BS = 256;   // sum-of-products block
@@ -1107,7 +1107,8 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       }
       if ((u.t1 - u.t0) * (int64_t)WIN < d->n_outputs) return fail(-1, "sgb_plan_create: CSR windows miss outputs");
     } else if (jit) {
-      if (u.kind != KIND_TAPE || u.bs != JIT_BLOCK || u.variant != 1 || !p->jit_lib)
+      if (u.kind != KIND_TAPE || u.bs != JIT_BLOCK || (u.variant != 1 && u.variant != 2 && u.variant != 4) ||
+          !p->jit_lib)
         return fail(-1, "sgb_plan_create: specialised unit " + std::to_string(k) + " without its kernels");
       cudaKernel_t kf, kb;
       const std::string nf = "sgb_tape_u" + std::to_string(k), nbn = "sgb_tape_b" + std::to_string(k);
@@ -1167,7 +1168,7 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
     }
     // batched tiles: one instance per warp (tape blocks are the unit's scratch stride wide);
     // CSR windows are single-set only (batched CSR = batched values + gather)
-    const int bwarps = u.kind == KIND_TAPE ? (u.bs * u.variant) / 32 : BATCH_WARPS;
+    const int bwarps = jit ? JIT_BLOCK / 32 : u.kind == KIND_TAPE ? (u.bs * u.variant) / 32 : BATCH_WARPS;
     u.bt0 = (int64_t)btiles.size();
     for (int g = window ? u.g1 : u.g0; g < u.g1; ++g) {
       const sgb_group &G = d->groups[g];

@@ -81,36 +81,39 @@ def _imm(v: float) -> str:
     return f"bits(0x{np.float64(v).view(np.uint64).item():016x}ULL)"
 
 
-def _column(rec, col: int, dp) -> str:
+def _column(rec, col: int, i: str = "i") -> str:
     """Index expression (u32) of retained column ``col`` for instance ``i``."""
     n = int(rec["n"])
     f = int(rec["flags"])
     if col == 0 and f & L.FLAG_AFFINE0:
-        return f"(u32)({int(rec['a0_base'])}LL + {int(rec['a0_stride'])}LL * i)"
+        return f"(u32)({int(rec['a0_base'])}LL + {int(rec['a0_stride'])}LL * {i})"
     if f & L.FLAG_W16:
         nch = (n + 31) // 32
-        return (f"(__ldg(T.cbase + {int(rec['cb_off']) + col * nch}LL + (i >> 5)) + "
-                f"(u32)__ldcs(T.coff + {int(rec['co_off']) + col * n}LL + i))")
+        return (f"(__ldg(T.cbase + {int(rec['cb_off']) + col * nch}LL + ({i} >> 5)) + "
+                f"(u32)__ldcs(T.coff + {int(rec['co_off']) + col * n}LL + {i}))")
     if f & L.FLAG_INTERLEAVED:
-        return f"__ldcs(T.pos + {int(rec['p_off'])}LL + i * {int(rec['n_ret'])} + {col})"
-    return f"__ldcs(T.pos + {int(rec['p_off']) + col * n}LL + i)"
+        return f"__ldcs(T.pos + {int(rec['p_off'])}LL + {i} * {int(rec['n_ret'])} + {col})"
+    return f"__ldcs(T.pos + {int(rec['p_off']) + col * n}LL + {i})"
 
 
-def _out_pos(rec, r: int) -> str | None:
+def _out_pos(rec, r: int, i: str = "i") -> str | None:
     n = int(rec["n"])
     f = int(rec["flags"])
     if f & L.FLAG_OPOS16:
         nch = (n + 31) // 32
-        return (f"[&]() {{ const u16 o = __ldcs(T.ooff + {int(rec['oo_off']) + r * n}LL + i); "
-                f"return o == 0xFFFF ? NONE : __ldg(T.obase + {int(rec['ob_off']) + r * nch}LL + (i >> 5)) + o; }}()")
+        return (f"[&]() {{ const u16 o_ = __ldcs(T.ooff + {int(rec['oo_off']) + r * n}LL + {i}); "
+                f"return o_ == 0xFFFF ? NONE : __ldg(T.obase + {int(rec['ob_off']) + r * nch}LL + ({i} >> 5)) + o_; }}()")
     if f & L.FLAG_OPOS32:
-        return f"__ldcs(T.opos32 + {int(rec['oo_off']) + r * n}LL + i)"
+        return f"__ldcs(T.opos32 + {int(rec['oo_off']) + r * n}LL + {i})"
     return None
 
 
-def group_body(dp, gi: int, tape: np.ndarray, imms: list, batched: bool = False, window: bool = False) -> list[str]:
-    """Straight-line CUDA for instance ``i`` of packed group ``gi`` (register tape -> SSA).
+def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: str = "",
+                batched: bool = False, window: bool = False) -> tuple[list[str], list[str]]:
+    """Straight-line CUDA for instance ``iv`` of packed group ``gi`` (register tape -> SSA).
 
+    Returns (load lines, compute + store lines) so several instances' loads can be
+    issued before any of them computes.  Variables carry suffix ``sfx``.
     Batched: value set ``b`` of ``X[addr * ld + b]`` (lane = value set).  Window:
     the CSR value goes to the block's shared window ``buf[o - kwin_]`` (no
     value-array store: window members are never re-read).
@@ -121,47 +124,46 @@ def group_body(dp, gi: int, tape: np.ndarray, imms: list, batched: bool = False,
     flags = int(rec["flags"])
     cols = dp.slot_col[rec["slot_off"]: rec["slot_off"] + S]
     dels = dp.slot_delta[rec["slot_off"]: rec["slot_off"] + S]
-    out = []
+    loads, comp = [], []
     reg: dict[int, str] = {}
+    i = iv
+    col = lambda c: _column(rec, c, i)  # noqa: E731
     if S:
-        out.append(f"const u32 idx0 = {_column(rec, 0, dp)};")
-    for s in range(S):
-        c = int(cols[s])
+        loads.append(f"const u32 idx0{sfx} = {col(0)};")
+    for s_ in range(S):
+        c = int(cols[s_])
         if c < 0:
-            addr = f"idx0 + (u32)({int(dels[s])}LL)"
+            addr = f"idx0{sfx} + (u32)({int(dels[s_])}LL)"
         elif c == 0:
-            addr = "idx0"
+            addr = f"idx0{sfx}"
         else:
-            addr = _column(rec, c, dp)
-        out.append(f"const double s{s} = __ldg({X(addr)});")
-        reg[s] = f"s{s}"
+            addr = col(c)
+        loads.append(f"const double s{s_}{sfx} = __ldg({X(addr)});")
+        reg[s_] = f"s{s_}{sfx}"
     for k in range(K):
-        e = (f"{int(rec['c_off'])}LL + i * {K} + {k}" if flags & L.FLAG_INTERLEAVED
-             else f"{int(rec['c_off']) + k * n}LL + i")
-        out.append(f"const double k{k} = __ldcs(T.con + {e});")
-        reg[S + k] = f"k{k}"
+        e = (f"{int(rec['c_off'])}LL + {i} * {K} + {k}" if flags & L.FLAG_INTERLEAVED
+             else f"{int(rec['c_off']) + k * n}LL + {i}")
+        loads.append(f"const double k{k}{sfx} = __ldcs(T.con + {e});")
+        reg[S + k] = f"k{k}{sfx}"
     stream = bool(flags & L.FLAG_STREAM)
+    opos = lambda r: _out_pos(rec, r, i)  # noqa: E731
     for j, t in enumerate(tape.tolist()):
         op, na, nb, dst, a, b, c, aux = t
         A = ("-" if na else "") + reg.get(a, "0.0")
         B = ("-" if nb else "") + reg.get(b, "0.0")
         C = reg.get(c, "0.0")
         if op == L.T_ST and window:
-            out.append(f"{{ const u32 o = {_out_pos(rec, aux)}; if (o != NONE) buf[o - kwin_] = {reg[a]}; }}")
+            comp.append(f"if (ok{sfx}) {{ const u32 o = {opos(aux)}; if (o != NONE) buf[o - kwin_] = {reg[a]}; }}")
             continue
         if op == L.T_ST:
             r = aux
             v = reg[a]
-            x_addr = X(f"{int(rec['dest_base']) + r * n}LL + i")
+            x_addr = X(f"{int(rec['dest_base']) + r * n}LL + {i}")
             store = f"st_stream({x_addr}, {v});" if stream else f"*({x_addr}) = {v};"
-            if stream:
-                out.append(f"if (!csr) {store}")
-            else:
-                out.append(store)
-            op_expr = _out_pos(rec, r)
-            if op_expr is not None:
+            comp.append(f"if (ok{sfx}{' && !csr' if stream else ''}) {store}")
+            if _out_pos(rec, r) is not None:
                 dst_o = "out[(u64)o * ld_out + b]" if batched else "out[o]"
-                out.append(f"if (csr) {{ const u32 o = {op_expr}; if (o != NONE) {dst_o} = {v}; }}")
+                comp.append(f"if (ok{sfx} && csr) {{ const u32 o = {opos(r)}; if (o != NONE) {dst_o} = {v}; }}")
             continue
         if op == L.T_IMM:
             expr = _imm(imms[aux])
@@ -178,9 +180,28 @@ def group_body(dp, gi: int, tape: np.ndarray, imms: list, batched: bool = False,
             expr = f"powi({reg[a]}, {k})" if kind == 4 else _SLOW[kind].format(a=reg[a])
         else:
             raise ValueError(f"unknown tape op {op}")
-        out.append(f"const double t{j} = {expr};")
-        reg[dst] = f"t{j}"
-    return out
+        comp.append(f"const double t{j}{sfx} = {expr};")
+        reg[dst] = f"t{j}{sfx}"
+    return loads, comp
+
+
+def group_vec_body(dp, gi, tape, imms, vec: int, base: str, stride: int, batched=False, window=False,
+                   limit: str | None = None):
+    """VEC instances base + v*stride: every instance's loads first, then the computes.
+
+    ``limit``: instance v is valid only if ``limit`` (with ``{v}`` = v * stride) holds too.
+    """
+    n = int(dp.groups[gi]["n"])
+    lines, comps = [], []
+    for v in range(vec):
+        lines.append(f"const i64 iv{v} = {base} + {v * stride}LL;")
+        extra = f" && ({limit.format(v=v * stride)})" if limit else ""
+        lines.append(f"const bool ok_{v} = iv{v} < {n}LL{extra};")
+        lines.append(f"const i64 ic{v} = ok_{v} ? iv{v} : {n - 1}LL;")
+        ld, cp = group_parts(dp, gi, tape, imms, iv=f"ic{v}", sfx=f"_{v}", batched=batched, window=window)
+        lines += ld
+        comps += cp
+    return lines + comps
 
 
 def _check_stores(tape, n_roots: int, gi: int):
@@ -217,6 +238,7 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
                     "    {",
                     "    switch (tl.x) {"]
         out += head
+        vec = 1 if batched else max(1, int(unit["variant"]))
         for gi in range(unit["group_begin"], unit["group_end"]):
             rec = dp.groups[gi]
             _check_stores(tapes[gi], int(rec["n_roots"]), gi)
@@ -224,7 +246,8 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
             out.append(f"      if (i >= {int(rec['n'])}LL) break;")
             if rec["flags"] & L.FLAG_CSR_ONLY:
                 out.append("      if (!csr) break;")
-            out += ["      " + ln for ln in group_body(dp, gi, tapes[gi], imms[gi], batched)]
+            out += ["      " + ln for ln in group_vec_body(dp, gi, tapes[gi], imms[gi], vec, "i", JIT_BLOCK,
+                                                            batched=batched)]
             out.append("    } break;")
         out += ["    default: break;", "    }", "    }", "  }", "}", ""]
     return "\n".join(out)
@@ -301,32 +324,38 @@ def compile_cubin(src: str, name: str = "sgb_tape.cu") -> bytes:
 MAX_WINDOW_PIECES = 512
 
 
+WINDOW_VEC = 4
+
+
 def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
     """CSR-window kernel of unit ``u``: a block assembles WIN consecutive outputs in shared
-    memory from its window's pieces (group, instance range), then writes them coalesced."""
+    memory from its window's pieces (group, instance range) -- warps take pieces, lanes
+    take WINDOW_VEC instances each with all loads in flight -- then writes them coalesced."""
     unit = dp.unit(u)
+    step = 32 * WINDOW_VEC
     out = [f'extern "C" __global__ void __launch_bounds__({JIT_BLOCK}) sgb_window_u{u}(',
            "    Tables T, const int4 *pieces, const i64 *win_off, i64 n_win, i64 w0, double *x, double *out,",
            "    i64 n_out) {",
            "  extern __shared__ double buf[];",
            f"  __shared__ int4 sp[{MAX_WINDOW_PIECES}];",
+           "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;",
            "  for (i64 w = blockIdx.x; w < n_win; w += gridDim.x) {",
            "    const i64 p0 = win_off[w], np_ = win_off[w + 1] - p0;",
            "    for (i64 j = threadIdx.x; j < np_; j += blockDim.x) sp[j] = pieces[p0 + j];",
            "    __syncthreads();",
            f"    const i64 kwin_ = (w0 + w) * {L.WIN}LL;",
-           "    const int total = np_ ? sp[np_ - 1].w + sp[np_ - 1].z : 0;",
-           "    int p = 0;",
-           "    for (int item = threadIdx.x; item < total; item += blockDim.x) {",
-           "      while (p + 1 < np_ && sp[p + 1].w <= item) ++p;",
-           "      const i64 i = (i64)sp[p].y + (item - sp[p].w);",
-           "      switch (sp[p].x) {"]
+           f"    for (int q = warp; q < np_; q += {JIT_BLOCK // 32}) {{",
+           "      const int4 pc = sp[q];",
+           f"      for (int c = lane; c < pc.z; c += {step}) {{",
+           "        const i64 i = (i64)pc.y + c;",
+           "        switch (pc.x) {"]
     for gi in range(unit["group_begin"], unit["group_end"]):
         _check_stores(tapes[gi], int(dp.groups[gi]["n_roots"]), gi)
-        out.append(f"      case {gi}: {{")
-        out += ["        " + ln for ln in group_body(dp, gi, tapes[gi], imms[gi], window=True)]
-        out.append("      } break;")
-    out += ["      default: break;", "      }", "    }", "    __syncthreads();",
+        out.append(f"        case {gi}: {{")
+        out += ["          " + ln for ln in group_vec_body(dp, gi, tapes[gi], imms[gi], WINDOW_VEC, "i", 32,
+                                                           window=True, limit="c + {v} < pc.z")]
+        out.append("        } break;")
+    out += ["        default: break;", "        }", "      }", "    }", "    __syncthreads();",
             f"    const i64 cnt = n_out - kwin_ < {L.WIN}LL ? n_out - kwin_ : {L.WIN}LL;",
             "    for (i64 j = threadIdx.x; j < cnt; j += blockDim.x) __stcs(out + kwin_ + j, buf[j]);",
             "    __syncthreads();", "  }", "}", ""]

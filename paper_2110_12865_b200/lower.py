@@ -52,7 +52,7 @@ UNIT_CSR_ONLY = 1
 UNIT_JIT = 2  # tape unit compiled to straight-line code (jit.py), one instance per thread
 UNIT_VALUE_ONLY = 4  # value-mode twin of a CSR-window unit (skipped by sgb_run_csr)
 UNIT_WINDOW = 8  # CSR windows: each block assembles WIN consecutive outputs in shared memory
-WIN = 4096  # outputs per CSR window (32 KB of shared memory)
+WIN = 2048  # outputs per CSR window (16 KB of shared memory)
 JIT_BLOCK = 256
 CHUNK = 32  # instances per compressed-index chunk (one warp in single-set mode)
 NONE32 = 0xFFFFFFFF
@@ -775,6 +775,16 @@ def _window_pieces(packed, gis, n_out, pieces, win_off, win_opos):
         win_off.append(len(pieces))
 
 
+def jit_vec(groups, sel) -> int:
+    """Instances per thread of a specialised unit: all of them keep their loads in flight
+    together, so small templates take 4, mid-size 2, big element templates 1."""
+    if os.environ.get("SGB_JIT_VEC"):
+        return int(os.environ["SGB_JIT_VEC"])
+    width = max(len(groups[j].slot_col) + groups[j].n_const + (len(groups[j].tape) if groups[j].tape is not None
+                                                               else 1) // 4 for j in sel)
+    return 4 if width <= 24 else (2 if width <= 64 else 1)
+
+
 def _copy_tape() -> np.ndarray:
     """Tape of a copy group: store slot 0 as root 0."""
     return np.array([(T_ST, 0, 0, 0, 0, 0, 0, 0)], dtype=TAPE_DTYPE)
@@ -909,7 +919,8 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                              ([j for j in sj if groups[j].window_value], UNIT_VALUE_ONLY),
                              ([j for j in sj if groups[j].window], UNIT_WINDOW)):
                 if sel:
-                    plan_units.append((KIND_TAPE, 1, JIT_BLOCK, tag, sel))
+                    plan_units.append((KIND_TAPE, jit_vec(groups, sel) if tag != UNIT_WINDOW else 1,
+                                       JIT_BLOCK, tag, sel))
             members = [j for j in members if j not in set(sj)]
         for plain in (True, False):
             tm = [j for j in members if groups[j].kind == KIND_TAPE and
@@ -936,7 +947,7 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
             plan_units.append((KIND_SOP, code, SOP_BLOCK, 0, codes[code]))
         for kind, variant, bs, regs, ms in plan_units:
             utag = 0
-            if kind == KIND_TAPE and bs == JIT_BLOCK and variant == 1 and regs in (0, UNIT_VALUE_ONLY, UNIT_WINDOW) \
+            if kind == KIND_TAPE and bs == JIT_BLOCK and regs in (0, UNIT_VALUE_ONLY, UNIT_WINDOW) \
                     and all(not groups[j].flags & (FLAG_SELFREF | FLAG_SERIAL) for j in ms) and jit:
                 utag, regs = regs, 0
             g_begin = len(order_groups)
