@@ -330,10 +330,10 @@ WINDOW_VEC = 4
 def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
     """CSR-window kernel of unit ``u``: a block assembles WIN consecutive outputs in shared
     memory from its window's pieces (group, instance range) -- warps take pieces, lanes
-    take WINDOW_VEC instances each with all loads in flight -- then writes them coalesced."""
+    take VEC instances each (VEC per group: all of a lane's loads stay in flight within the
+    register budget) -- then writes them coalesced."""
     unit = dp.unit(u)
-    step = 32 * WINDOW_VEC
-    out = [f'extern "C" __global__ void __launch_bounds__({JIT_BLOCK}) sgb_window_u{u}(',
+    out = [f'extern "C" __global__ void __launch_bounds__({JIT_BLOCK}, 3) sgb_window_u{u}(',
            "    Tables T, const int4 *pieces, const i64 *win_off, i64 n_win, i64 w0, double *x, double *out,",
            "    i64 n_out) {",
            "  extern __shared__ double buf[];",
@@ -346,16 +346,17 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
            f"    const i64 kwin_ = (w0 + w) * {L.WIN}LL;",
            f"    for (int q = warp; q < np_; q += {JIT_BLOCK // 32}) {{",
            "      const int4 pc = sp[q];",
-           f"      for (int c = lane; c < pc.z; c += {step}) {{",
-           "        const i64 i = (i64)pc.y + c;",
-           "        switch (pc.x) {"]
+           "      switch (pc.x) {"]
     for gi in range(unit["group_begin"], unit["group_end"]):
-        _check_stores(tapes[gi], int(dp.groups[gi]["n_roots"]), gi)
-        out.append(f"        case {gi}: {{")
-        out += ["          " + ln for ln in group_vec_body(dp, gi, tapes[gi], imms[gi], WINDOW_VEC, "i", 32,
-                                                           window=True, limit="c + {v} < pc.z")]
-        out.append("        } break;")
-    out += ["        default: break;", "        }", "      }", "    }", "    __syncthreads();",
+        rec = dp.groups[gi]
+        _check_stores(tapes[gi], int(rec["n_roots"]), gi)
+        vec = max(1, min(WINDOW_VEC, 12 // max(1, int(rec["n_slots"]) + int(rec["n_const"]))))
+        out.append(f"      case {gi}: for (int c = lane; c < pc.z; c += {32 * vec}) {{")
+        out.append("        const i64 i = (i64)pc.y + c;")
+        out += ["        " + ln for ln in group_vec_body(dp, gi, tapes[gi], imms[gi], vec, "i", 32,
+                                                         window=True, limit="c + {v} < pc.z")]
+        out.append("      } break;")
+    out += ["      default: break;", "      }", "    }", "    __syncthreads();",
             f"    const i64 cnt = n_out - kwin_ < {L.WIN}LL ? n_out - kwin_ : {L.WIN}LL;",
             "    for (i64 j = threadIdx.x; j < cnt; j += blockDim.x) __stcs(out + kwin_ + j, buf[j]);",
             "    __syncthreads();", "  }", "}", ""]

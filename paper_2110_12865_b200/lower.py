@@ -819,8 +819,8 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         from . import jit as _jit
 
         jit = _jit.available()
-    if csr_window is None:  # CSR windows of the last wave (specialised units only), see _window_plan
-        csr_window = os.environ.get("SGB_CSR_WINDOW", "1") != "0"
+    if csr_window is None:  # CSR windows of the last wave (specialised units only), see _window_members
+        csr_window = os.environ.get("SGB_CSR_WINDOW", "0") == "1"
     csr_window = bool(csr_window and jit)
     read_sets = _read_sets(plan)
     waves = compute_waves(plan, read_sets)

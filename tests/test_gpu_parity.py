@@ -14,6 +14,8 @@ from conftest import bits
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-12
+WINDOW_CASES = {"lmlt_w7", "lmlt_w12", "spgemm_n60_k4", "toy256", "toy256_interleaved", "acc1_expr1_s1",
+                "prog_cotan_4x4_tag", "prog_energy-hessian_4x4_tag", "transc37", "tagged_pair"}
 
 
 def _close(got, want):
@@ -85,6 +87,8 @@ def test_csr_mode(golden, mode):
 
     from paper_2110_12865_b200 import DevicePlan, lower_plan
 
+    if mode == "window" and golden.name not in WINDOW_CASES:
+        pytest.skip("CSR windows: representative subset (each case compiles its own window kernel)")
     kw = {"gather": dict(csr_window=False), "window": dict(csr_window=True), "direct": dict(direct_csr=True),
           "interpreter": dict(jit=False)}[mode]
     dp = DevicePlan(golden.plan, lowered=lower_plan(golden.plan, **kw))
