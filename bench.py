@@ -245,6 +245,213 @@ def run_reference(args):
     return 0
 
 
+def _peak_gbs():
+    peaks_path = ROOT / "MEASURED_PEAKS.json"
+    if peaks_path.exists():
+        return float(json.loads(peaks_path.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def run_batched(args):
+    """C5: one L.M.L^T+A plan (GridMesh(200,200), 991,912 out nnz) x 256 value sets, the value sets
+    sharded across the ranks (strong scaling: the 256 sets are the whole job); no collective in the
+    step.  ``--gather`` adds the NCCL gather of every rank's CSR block to rank 0 (timed separately)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2110_12865_b200 import DevicePlan
+    from paper_2110_12865_b200.metrics import plan_balg, wave_traffic
+    from paper_2110_12865_b200.programs.mesh import lmlt_inputs
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    barrier = dist.barrier if world > 1 else None
+    args.w = args.w5
+    key, plan, _, _ = build_workload(args, rank, world, barrier)
+    n_out, n_in = len(plan.outputs), int(plan.input_count)
+    total = args.batch
+    per = [total // world + (1 if r < total % world else 0) for r in range(world)]
+    b, first = per[rank], sum(per[:rank])
+    sets = list(range(first, first + b))  # value set s = lmlt_inputs(seed=s)
+    host_in = np.stack([lmlt_inputs(args.w, seed=s_) for s_ in sets], axis=1)  # [n_in, b]
+    dp = DevicePlan(plan, device=local)
+    X = torch.zeros((plan.value_array_size, b), dtype=torch.float64, device=f"cuda:{local}")
+    X[:n_in] = torch.from_numpy(host_in).to(X.device)
+    out = torch.empty((n_out, b), dtype=torch.float64, device=X.device)
+    for _ in range(args.warmup):
+        dp.run_batch_csr(X, out)
+    torch.cuda.synchronize()
+    parity = None
+    if rank == 0:
+        from oracle import oracle
+
+        enc = oracle.encode_plan(plan)
+        ok = all(np.array_equal(oracle.run_outputs(plan, host_in[:, j], enc).view(np.uint64),
+                                out[:, j].cpu().numpy().view(np.uint64)) for j in range(min(b, 3)))
+        parity = "bitwise (value sets 0-2 vs oracle)" if ok else "MISMATCH"
+        log(f"[bench c5] parity: {parity}")
+    stream = torch.cuda.current_stream()
+    sampler = ClockSampler(local)
+    with sampler:
+        t_end = time.perf_counter() + 1.0
+        while time.perf_counter() < t_end:
+            dp.run_batch_csr(X, out)
+            torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        if barrier:
+            barrier()
+        torch.cuda.synchronize()
+        for e0, e1 in evs:
+            e0.record(stream)
+            dp.run_batch_csr(X, out)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        if barrier:
+            barrier()
+    ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=X.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    gather_ms = None
+    if args.gather and world > 1:  # NCCL gather of the CSR blocks to rank 0 (all ranks' shards, equal-size pad)
+        bmax = max(per)
+        send = torch.zeros((n_out, bmax), dtype=torch.float64, device=X.device)
+        send[:, :b] = out
+        recv = [torch.empty_like(send) for _ in range(world)] if rank == 0 else None
+        for _ in range(2):
+            dist.gather(send, recv, dst=0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        dist.gather(send, recv, dst=0)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=X.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        gather_ms = float(t.item())
+    # e2e through the public API: host inputs (pinned) -> device -> batched CSR -> host
+    hin = torch.from_numpy(np.ascontiguousarray(host_in)).pin_memory()
+    hout = torch.empty((n_out, b), dtype=torch.float64).pin_memory()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        X[:n_in].copy_(hin, non_blocking=True)
+        dp.run_batch_csr(X, out)
+        hout.copy_(out, non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=X.device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    if rank != 0:
+        dist.destroy_process_group()
+        return 0
+    traffic = wave_traffic(plan, dp.lowered, batch=b)
+    step_bytes = sum(t.bytes for t in traffic)
+    peak, peak_src = _peak_gbs()
+    achieved = step_bytes / (ms * 1e-3) / 1e9  # whole step (per-launch events are not recorded here)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        k_cpu = 8  # bounded sample: 8 value sets through the reference's emitted sg_run (OpenMP)
+        res = cpu_reference(plan, host_in[:, 0], k_cpu, 1, key=key)
+        cpu = {"value": n_out / res["seconds_per_eval"], "unit": UNIT, "cores": res["cores"], "kind": res["kind"],
+               "sample": f"{res['evals']} sequential sg_run evaluations of one value set (the reference has no batch "
+                         f"API; SURVEY 8(d) C5); {res['what']}, cc -O3 -ffp-contract=off -fopenmp"}
+    line = {
+        "metric": METRIC, "value": total * n_out / (ms * 1e-3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C5 batched: L.M.L^T+A plan on a {args.w}x{args.w} grid ({n_out} out nnz) x "
+                               f"{total} value sets, {per} per rank", "out_nnz": n_out, "value_sets": total,
+                   "parallelism": f"value sets sharded over {world} GPU(s), plan replicated, no collective in the step",
+                   "l2": "no flush: X (%.1f GB per rank) exceeds L2" % (plan.value_array_size * b * 8 / 1e9),
+                   "parity": parity, "nccl_gather_ms": gather_ms},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel": "whole batched step (waves + gather)", "algorithmic_bytes": step_bytes,
+                     "peak_source": peak_src, "balg_single_pass_per_set": plan_balg(plan)},
+        "e2e": {"value": total * n_out / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * n_in * b,
+                "d2h_bytes_per_step": 8 * n_out * b},
+        "gpu_launches": dp.csr_units, "clocks": sampler.summary(), "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_spgemm(args):
+    """C1: C = A.B, random CSR 2000x2000, 10 nnz/row -- the reference's own plan (tests/golden/spgemm_n2000_k10,
+    written by sparsegen.codegen.save_plan).  3.5 MB per evaluation sits in L2, so every step flushes L2
+    (untimed) before the timed evaluation."""
+    import torch
+
+    from paper_2110_12865_b200 import DevicePlan, load_plan
+
+    gdir = ROOT / "tests" / "golden" / "spgemm_n2000_k10"
+    plan = load_plan(gdir)
+    with np.load(gdir / "vectors.npz") as z:
+        inputs, ref_values = z["inputs"], z["values"]
+    n_out = len(plan.outputs)
+    dp = DevicePlan(plan)
+    x = dp.new_values(inputs)
+    out = torch.empty(n_out, dtype=torch.float64, device=x.device)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device=x.device)  # 512 MB > L2
+    for _ in range(args.warmup):
+        dp.run_csr(x, out)
+    torch.cuda.synchronize()
+    want = ref_values[np.asarray(plan.outputs, np.int64)]
+    parity = "bitwise vs reference interpret_plan" if np.array_equal(out.cpu().numpy().view(np.uint64),
+                                                                     want.view(np.uint64)) else "MISMATCH"
+    stream = torch.cuda.current_stream()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(0)
+    with sampler:
+        for e0, e1 in evs:
+            flush.fill_(1.0)
+            e0.record(stream)
+            dp.run_csr(x, out)
+            e1.record(stream)
+        torch.cuda.synchronize()
+    ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / args.steps
+    inp_h = torch.from_numpy(inputs).pin_memory().numpy()
+    out_h = torch.empty(n_out, dtype=torch.float64).pin_memory().numpy()
+    dp.run_outputs_host(inp_h, out_h)
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps * 20):
+        dp.run_outputs_host(inp_h, out_h)
+    e2e_s = (time.perf_counter() - t0) / (args.e2e_steps * 20)
+    cpu = None
+    if not args.no_cpu_baseline:
+        res = cpu_reference(plan, inputs, 200, 5, key="spgemm_n2000_k10")
+        cpu = {"value": n_out / res["seconds_per_eval"], "unit": UNIT, "cores": res["cores"], "kind": res["kind"],
+               "sample": f"{res['evals']} sg_run evaluations ({res['what']}, cc -O3 -ffp-contract=off -fopenmp); "
+                         f"the reference's plan build (trace 0.94 s + build_plan 2.85 s, SURVEY 6.3) is not included"}
+    peak, peak_src = _peak_gbs()
+    from paper_2110_12865_b200.metrics import plan_balg
+
+    bal = plan_balg(plan)
+    line = {
+        "metric": METRIC, "value": n_out / (ms * 1e-3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C1 spgemm C=A.B, random CSR 2000x2000 10 nnz/row, {n_out} out nnz (reference plan)",
+                   "l2": "flushed (512 MB write) before every timed evaluation", "parity": parity},
+        "roofline": {"bound": "hbm", "achieved": bal / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                     "frac": bal / (ms * 1e-3) / 1e9 / peak, "traffic": None, "kernel": "whole evaluation",
+                     "algorithmic_bytes": bal, "peak_source": peak_src},
+        "e2e": {"value": n_out / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * int(plan.input_count),
+                "d2h_bytes_per_step": 8 * n_out},
+        "gpu_launches": dp.csr_units, "clocks": sampler.summary(), "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -255,11 +462,20 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=20)
+    ap.add_argument("--config", choices=("c1", "c2", "c5"), default="c2",
+                    help="BASELINE.json config: c2 (default, configs[1]), c1 spgemm, c5 batched")
+    ap.add_argument("--w5", type=int, default=200, help="C5 grid width")
+    ap.add_argument("--batch", type=int, default=256, help="C5 value sets (whole job)")
+    ap.add_argument("--gather", action="store_true", help="C5: also time the NCCL gather to rank 0")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "c5":
+        return run_batched(args)
+    if args.config == "c1":
+        return run_spgemm(args)
 
     import torch
     import torch.distributed as dist

@@ -100,17 +100,27 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--w", type=int, default=1000)
     ap.add_argument("--if-stale", action="store_true")
+    ap.add_argument("--golden", nargs="*", default=["spgemm_n2000_k10"],
+                    help="also emit for these reference-built golden plans (bench C1)")
     args = ap.parse_args()
     sys.path.insert(0, str(ROOT))
     import bench
+    from paper_2110_12865_b200.plan import load_plan
 
-    key = bench.workload_key(argparse.Namespace(w=args.w))
-    if args.if_stale and up_to_date(key):
-        print(f"oracle/_ref/{key}.c is up to date")
-        return
-    key, plan, _, _ = bench.build_workload(argparse.Namespace(w=args.w), 0, 1)
-    src = emit_for_plan(plan, key)
-    print(f"wrote {src} ({src.stat().st_size / 1e6:.1f} MB) for {key}")
+    for name in args.golden:
+        if args.if_stale and (REF_DIR / f"{name}.c").exists():
+            continue
+        src = emit_for_plan(load_plan(ROOT / "tests" / "golden" / name), name)
+        print(f"wrote {src}")
+    for w in (args.w, 200):  # C2 and the C5 plan
+        key = bench.workload_key(argparse.Namespace(w=w))
+        if args.if_stale and up_to_date(key):
+            print(f"oracle/_ref/{key}.c is up to date")
+            continue
+        key, plan, _, _ = bench.build_workload(argparse.Namespace(w=w), 0, 1)
+        src = emit_for_plan(plan, key)
+        print(f"wrote {src} ({src.stat().st_size / 1e6:.1f} MB) for {key}")
+
 
 
 if __name__ == "__main__":
