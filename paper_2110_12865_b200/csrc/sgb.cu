@@ -729,13 +729,24 @@ __global__ void __launch_bounds__(256) gather_outputs(const double *__restrict__
     st_stream(out + k, __ldg(x + __ldg(outs + k)), pol);
 }
 
+// Batched outputs: one output per warp, lanes over value sets, 4 value sets per lane
+// per iteration with all loads issued first.
 __global__ void gather_outputs_batch(const double *__restrict__ X, int64_t ld, int64_t batch,
                                      const int64_t *__restrict__ outs, int64_t n, double *__restrict__ out,
                                      int64_t ld_out) {
   const int64_t k = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (k >= n) return;
-  const int64_t src = __ldg(outs + k) * ld;
-  for (int64_t b = threadIdx.x & 31; b < batch; b += 32) out[k * ld_out + b] = __ldg(X + src + b);
+  const double *src = X + __ldg(outs + k) * ld;
+  double *dst = out + k * ld_out;
+  for (int64_t b = threadIdx.x & 31; b < batch; b += 128) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (b + 32 * u < batch) v[u] = __ldg(src + b + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (b + 32 * u < batch) __stcs(dst + b + 32 * u, v[u]);
+  }
 }
 
 template <class T>

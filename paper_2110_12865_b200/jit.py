@@ -36,6 +36,7 @@ import numpy as np
 from . import lower as L
 
 JIT_BLOCK = 256  # threads per block = instances per tile of a specialised unit
+BATCH_VEC = 4  # batched kernels: value sets per lane per iteration (loads of all in flight)
 CACHE = Path(os.environ.get("SGB_JIT_CACHE", Path.home() / ".cache" / "sgb_jit"))
 
 _PREAMBLE = r"""
@@ -109,7 +110,7 @@ def _out_pos(rec, r: int, i: str = "i") -> str | None:
 
 
 def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: str = "",
-                batched: bool = False, window: bool = False) -> tuple[list[str], list[str]]:
+                batched: bool = False, window: bool = False, bv: str = "b") -> tuple[list[str], list[str]]:
     """Straight-line CUDA for instance ``iv`` of packed group ``gi`` (register tape -> SSA).
 
     Returns (load lines, compute + store lines) so several instances' loads can be
@@ -118,7 +119,7 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
     the CSR value goes to the block's shared window ``buf[o - kwin_]`` (no
     value-array store: window members are never re-read).
     """
-    X = (lambda a: f"x + (u64)({a}) * ld + b") if batched else (lambda a: f"x + ({a})")
+    X = (lambda a: f"x + (u64)({a}) * ld + {bv}") if batched else (lambda a: f"x + ({a})")
     rec = dp.groups[gi]
     n, S, K = int(rec["n"]), int(rec["n_slots"]), int(rec["n_const"])
     flags = int(rec["flags"])
@@ -162,7 +163,7 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
             store = f"st_stream({x_addr}, {v});" if stream else f"*({x_addr}) = {v};"
             comp.append(f"if (ok{sfx}{' && !csr' if stream else ''}) {store}")
             if _out_pos(rec, r) is not None:
-                dst_o = "out[(u64)o * ld_out + b]" if batched else "out[o]"
+                dst_o = f"out[(u64)o * ld_out + {bv}]" if batched else "out[o]"
                 comp.append(f"if (ok{sfx} && csr) {{ const u32 o = {opos(r)}; if (o != NONE) {dst_o} = {v}; }}")
             continue
         if op == L.T_IMM:
@@ -183,6 +184,29 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
         comp.append(f"const double t{j}{sfx} = {expr};")
         reg[dst] = f"t{j}{sfx}"
     return loads, comp
+
+
+def group_batch_body(dp, gi, tape, imms, vec: int) -> list[str]:
+    """Batched: instance ``i`` for value sets b + 32 v (v < vec), loads of all of them first."""
+    n = int(dp.groups[gi]["n"])
+    lines, comps = [], []
+    shared = None
+    for v in range(vec):
+        lines.append(f"const i64 b{v} = b + {32 * v}LL;")
+        lines.append(f"const bool ok_{v} = b{v} < batch;")
+        lines.append(f"const i64 bc{v} = ok_{v} ? b{v} : batch - 1;")
+        ld, cp = group_parts(dp, gi, tape, imms, iv="i", sfx=f"_{v}", batched=True, bv=f"bc{v}")
+        # the index decode (idx0 / column loads) is the same for every value set: emit it once
+        if shared is None:
+            shared = [ln for ln in ld if ln.startswith("const u32 idx0")]
+            lines = shared[:1] + lines if shared else lines
+        ld = [ln.replace(f"idx0_{v}", "idx0_0") for ln in ld if not ln.startswith("const u32 idx0")]
+        cp = [ln.replace(f"idx0_{v}", "idx0_0") for ln in cp]
+        lines += ld
+        comps += cp
+    if shared:
+        lines = [shared[0].replace("idx0_0", "idx0_0")] + [ln for ln in lines if ln != shared[0]]
+    return lines + comps
 
 
 def group_vec_body(dp, gi, tape, imms, vec: int, base: str, stride: int, batched=False, window=False,
@@ -227,7 +251,7 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
                     "  for (i64 t = blockIdx.x; t < n_tiles; t += gridDim.x) {",
                     "    const int2 tl = tiles[t];",
                     "    const i64 i = (i64)tl.y + (threadIdx.x >> 5);",
-                    "    for (i64 b = threadIdx.x & 31; b < batch; b += 32) {",
+                    f"    for (i64 b = threadIdx.x & 31; b < batch; b += {32 * BATCH_VEC}) {{",
                     "    switch (tl.x) {"]
         else:
             head = [f'extern "C" __global__ void __launch_bounds__({JIT_BLOCK}) sgb_tape_u{u}(',
@@ -246,8 +270,9 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
             out.append(f"      if (i >= {int(rec['n'])}LL) break;")
             if rec["flags"] & L.FLAG_CSR_ONLY:
                 out.append("      if (!csr) break;")
-            out += ["      " + ln for ln in group_vec_body(dp, gi, tapes[gi], imms[gi], vec, "i", JIT_BLOCK,
-                                                            batched=batched)]
+            body = (group_batch_body(dp, gi, tapes[gi], imms[gi], BATCH_VEC) if batched else
+                    group_vec_body(dp, gi, tapes[gi], imms[gi], vec, "i", JIT_BLOCK))
+            out += ["      " + ln for ln in body]
             out.append("    } break;")
         out += ["    default: break;", "    }", "    }", "  }", "}", ""]
     return "\n".join(out)
