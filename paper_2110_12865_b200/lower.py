@@ -799,8 +799,12 @@ def _tile_keys(g: _Group, starts: np.ndarray, tile: int) -> np.ndarray:
     return np.where(m == np.iinfo(np.int64).max, -1, m)
 
 
+JIT_MIN_N = 4096  # groups with fewer instances stay on the hand-written kernels (NVRTC time buys nothing)
+
+
 def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = None,
-               jit: bool | None = None, csr_window: bool | None = None) -> DevicePlanArrays:
+               jit: bool | None = None, csr_window: bool | None = None,
+               jit_min_n: int | None = None) -> DevicePlanArrays:
     """ExecutionPlan -> device plan.
 
     ``direct_csr``: output groups store their CSR values through output-position
@@ -819,6 +823,8 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         from . import jit as _jit
 
         jit = _jit.available()
+    if jit_min_n is None:
+        jit_min_n = int(os.environ.get("SGB_JIT_MIN_N", JIT_MIN_N))
     if csr_window is None:  # CSR windows of the last wave (specialised units only), see _window_members
         csr_window = os.environ.get("SGB_CSR_WINDOW", "0") == "1"
     csr_window = bool(csr_window and jit)
@@ -913,8 +919,9 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     for w in range(total_waves):
         members = [j for j, g in enumerate(groups) if g.wave == w]
         plan_units = []
-        if jit:  # every plain group of the wave (tape or sum-of-products) in one specialised kernel
-            sj = [j for j in members if not groups[j].flags & (FLAG_SELFREF | FLAG_SERIAL)]
+        if jit:  # every big plain group of the wave (tape or sum-of-products) in one specialised kernel
+            sj = [j for j in members if not groups[j].flags & (FLAG_SELFREF | FLAG_SERIAL)
+                  and (groups[j].n >= jit_min_n or groups[j].window or groups[j].window_value)]
             for sel, tag in (([j for j in sj if not groups[j].window and not groups[j].window_value], 0),
                              ([j for j in sj if groups[j].window_value], UNIT_VALUE_ONLY),
                              ([j for j in sj if groups[j].window], UNIT_WINDOW)):

@@ -14,7 +14,7 @@ from conftest import bits
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-12
-WINDOW_CASES = {"lmlt_w7", "lmlt_w12", "spgemm_n60_k4", "toy256", "toy256_interleaved", "acc1_expr1_s1",
+WINDOW_CASES = {"lmlt_w7", "lmlt_w12", "spgemm_n60_k4", "toy256", "toy256_interleaved", "cli_cotan_simp",
                 "prog_cotan_4x4_tag", "prog_energy-hessian_4x4_tag", "transc37", "tagged_pair"}
 
 
@@ -107,21 +107,45 @@ def test_csr_mode(golden, mode):
             assert _close(got, want)
 
 
-def test_tape_interpreter_matches_specialised_kernels(golden):
-    """The hand-written tape interpreter and the specialised (jit.py) tape kernels agree bit for bit."""
+JIT_CASES = ["lmlt_w7", "lmlt_w12", "prog_energy-hessian_4x4_tag", "transc37", "transc37_nosimp",
+             "toy256_interleaved", "tagged_pair", "acc9_lpow3_simp", "spgemm_n60_k4", "selfref", "coord96",
+             "select_edge", "prog_cotan_4x4_tag", "cli_lpow4_simp"]
+
+
+@pytest.mark.parametrize("name", JIT_CASES)
+@pytest.mark.parametrize("batch", [0, 5, 64])
+def test_specialised_kernels_match_hand_written(name, batch):
+    """Every group specialised (jit.py, jit_min_n=0) == the hand-written kernels only, bit for bit,
+    single value set and batched."""
     import torch
 
+    from conftest import Golden
     from paper_2110_12865_b200 import DevicePlan, lower_plan
 
-    xs = []
+    golden = Golden(name)
+    plan = golden.plan
+    rng = np.random.default_rng(batch)
+    ins = rng.uniform(0.5, 2.0, (max(batch, 1), plan.input_count))
+    ins[0] = golden.inputs
+    outs = []
     for jit in (False, True):
-        dp = DevicePlan(golden.plan, lowered=lower_plan(golden.plan, jit=jit))
-        x = dp.new_values(golden.inputs)
-        dp.run_values(x)
+        dp = DevicePlan(plan, lowered=lower_plan(plan, jit=jit, jit_min_n=0))
+        if batch:
+            X = torch.zeros((plan.value_array_size, batch), dtype=torch.float64, device="cuda")
+            X[: plan.input_count] = torch.from_numpy(ins.T.copy()).cuda()
+            dp.run_batch(X)
+            o = dp.run_batch_csr(torch.where(torch.arange(plan.value_array_size, device="cuda")[:, None]
+                                             < plan.input_count, X, torch.zeros_like(X)))
+            outs.append((X.cpu().numpy(), o.cpu().numpy()))
+        else:
+            x = dp.new_values(golden.inputs)
+            dp.run_values(x)
+            outs.append((x.cpu().numpy(), dp.run_csr(dp.new_values(golden.inputs)).cpu().numpy()))
         torch.cuda.synchronize()
-        xs.append(x.cpu().numpy())
-        check(xs[-1], golden)
-    assert np.array_equal(bits(xs[0]), bits(xs[1]))
+    if not batch:
+        check(outs[1][0], golden)
+    assert np.array_equal(bits(outs[0][0]), bits(outs[1][0]))
+    assert np.array_equal(bits(outs[0][1]), bits(outs[1][1]))
 
 
 def test_run_wave_by_wave_equals_run(golden):

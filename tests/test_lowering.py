@@ -106,8 +106,11 @@ def test_sop_shapes():
     assert L.sop_shape([N, N, 0]) == L.SOP_SHAPE_GENERIC
 
 
-@pytest.mark.parametrize("name", ["lmlt_w7", "prog_energy-hessian_4x4_tag", "transc37", "toy256_interleaved",
-                                  "tagged_pair", "acc9_lpow3_simp"])
+JIT_CASES = ["lmlt_w7", "prog_energy-hessian_4x4_tag", "transc37", "toy256_interleaved", "tagged_pair",
+             "acc9_lpow3_simp", "spgemm_n60_k4", "selfref", "coord96"]
+
+
+@pytest.mark.parametrize("name", JIT_CASES)
 def test_specialised_tape_units_compile(name):
     """jit.py: the tape units compile to sm_100a cubins with NVRTC (no GPU needed)."""
     from conftest import Golden
@@ -115,9 +118,9 @@ def test_specialised_tape_units_compile(name):
 
     if not jit.available():
         pytest.skip("NVRTC not available")
-    dp = lower_plan(Golden(name).plan, jit=True)
+    dp = lower_plan(Golden(name).plan, jit=True, jit_min_n=0)
     n_jit = sum(1 for u in range(len(dp.units)) if dp.unit(u)["flags"] & L.UNIT_JIT)
-    n_tape_plain = sum(1 for kl in dp.kernels if kl.kind == L.KIND_TAPE and not kl.flags & (L.FLAG_SELFREF | L.FLAG_SERIAL))
-    assert (n_jit > 0) == (n_tape_plain > 0)
+    n_plain = sum(1 for kl in dp.kernels if not kl.flags & (L.FLAG_SELFREF | L.FLAG_SERIAL))
+    assert (n_jit > 0) == (n_plain > 0)
     if n_jit:
         assert dp.jit_cubin[:4] == b"\x7fELF" and "sgb_tape_u" in dp.jit_source
