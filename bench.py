@@ -271,9 +271,11 @@ def run_batched(args):
     args.w = args.w5
     key, plan, _, _ = build_workload(args, rank, world, barrier)
     n_out, n_in = len(plan.outputs), int(plan.input_count)
+    from paper_2110_12865_b200.shard import gather_csr, max_over_ranks, shard_value_sets
+
     total = args.batch
-    per = [total // world + (1 if r < total % world else 0) for r in range(world)]
-    b, first = per[rank], sum(per[:rank])
+    per = [shard_value_sets(total, world, r)[1] for r in range(world)]
+    first, b = shard_value_sets(total, world, rank)
     sets = list(range(first, first + b))  # value set s = lmlt_inputs(seed=s)
     host_in = np.stack([lmlt_inputs(args.w, seed=s_) for s_ in sets], axis=1)  # [n_in, b]
     dp = DevicePlan(plan, device=local)
@@ -310,29 +312,19 @@ def run_batched(args):
         torch.cuda.synchronize()
         if barrier:
             barrier()
-    ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=X.device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(sum(e0.elapsed_time(e1) for e0, e1 in evs) / args.steps, X.device)
     gather_ms = None
-    if args.gather and world > 1:  # NCCL gather of the CSR blocks to rank 0 (all ranks' shards, equal-size pad)
-        bmax = max(per)
-        send = torch.zeros((n_out, bmax), dtype=torch.float64, device=X.device)
-        send[:, :b] = out
-        recv = [torch.empty_like(send) for _ in range(world)] if rank == 0 else None
+    if args.gather and world > 1:  # NCCL gather of every rank's CSR block to rank 0 (not in the step)
         for _ in range(2):
-            dist.gather(send, recv, dst=0)
+            gather_csr(out, total)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
         e0.record(stream)
-        dist.gather(send, recv, dst=0)
+        gather_csr(out, total)
         e1.record(stream)
         torch.cuda.synchronize()
-        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=X.device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        gather_ms = float(t.item())
+        gather_ms = max_over_ranks(e0.elapsed_time(e1), X.device)
     # e2e through the public API: host inputs (pinned) -> device -> batched CSR -> host
     hin = torch.from_numpy(np.ascontiguousarray(host_in)).pin_memory()
     hout = torch.empty((n_out, b), dtype=torch.float64).pin_memory()
@@ -343,11 +335,7 @@ def run_batched(args):
         dp.run_batch_csr(X, out)
         hout.copy_(out, non_blocking=True)
         torch.cuda.synchronize()
-    e2e_s = (time.perf_counter() - t0) / args.e2e_steps
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=X.device)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / args.e2e_steps, X.device)
     if rank != 0:
         dist.destroy_process_group()
         return 0

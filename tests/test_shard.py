@@ -1,0 +1,82 @@
+"""Multi-process sharding of value sets on CPU: gloo, world size 2.
+
+The N>1 bench path shards independent value sets across ranks with no
+collective in the step and gathers CSR blocks only on request; here every rank
+evaluates its shard with the oracle (the GPU is not needed to check the
+partitioning logic) and the gathered result must equal the single-process
+evaluation of all value sets.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2110_12865_b200.shard import gather_csr, max_over_ranks, shard_value_sets
+
+
+@pytest.mark.parametrize("total,world", [(256, 1), (256, 2), (256, 8), (7, 3), (3, 8), (0, 2)])
+def test_shards_cover_every_value_set_once(total, world):
+    seen = []
+    for r in range(world):
+        first, count = shard_value_sets(total, world, r)
+        seen.extend(range(first, first + count))
+    assert seen == list(range(total))
+    sizes = [shard_value_sets(total, world, r)[1] for r in range(world)]
+    assert max(sizes) - min(sizes) <= 1
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, total, result_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        from pathlib import Path
+
+        root = Path(__file__).resolve().parent.parent
+        sys.path.insert(0, str(root))
+        sys.path.insert(0, str(root / "tests"))
+        from conftest import Golden
+        from oracle import oracle
+
+        g = Golden("lmlt_w7")
+        plan = g.plan
+        first, count = shard_value_sets(total, world, rank)
+        enc = oracle.encode_plan(plan)
+        block = np.stack([oracle.run_outputs(plan, np.random.default_rng(s).uniform(0.5, 2.0, plan.input_count),
+                                             enc) for s in range(first, first + count)], axis=1) \
+            if count else np.zeros((len(plan.outputs), 0))
+        full = gather_csr(torch.from_numpy(np.ascontiguousarray(block)), total)
+        slowest = max_over_ranks(float(rank + 1))
+        if rank == 0:
+            np.save(result_path, full.numpy())
+            assert slowest == float(world)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("total", [5, 6])
+def test_gloo_world2_gather_equals_single_process(tmp_path, total):
+    world = 2
+    path = tmp_path / "full.npy"
+    mp.spawn(_worker, args=(world, _free_port(), total, str(path)), nprocs=world, join=True)
+    got = np.load(path)
+    from conftest import Golden, bits
+    from oracle import oracle
+
+    g = Golden("lmlt_w7")
+    want = np.stack([oracle.run_outputs(g.plan, np.random.default_rng(s).uniform(0.5, 2.0, g.plan.input_count))
+                     for s in range(total)], axis=1)
+    assert got.shape == want.shape
+    assert np.array_equal(bits(got), bits(want))
