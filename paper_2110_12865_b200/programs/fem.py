@@ -149,6 +149,19 @@ def element_template():
     return T, troots, sh, rank
 
 
+def shared_nodes(T, roots) -> list[int]:
+    """Non-leaf nodes with two or more consumers, ascending: the template's stack locals
+    (what local_decompose would keep, decompose.py:346-388); arithmetic is unchanged."""
+    from ..plan import reachable
+
+    live = reachable(T, roots)
+    uses: dict[int, int] = {}
+    for ref in live:
+        for c in T.args[ref]:
+            uses[c] = uses.get(c, 0) + 1
+    return [ref for ref in live if T.ops[ref] not in (OpKind.VAR, OpKind.CONST) and uses.get(ref, 0) >= 2]
+
+
 def _sum_template(k: int):
     T = Template()
     vs = [T.var(s) for s in range(k)]
@@ -170,7 +183,8 @@ def build_fem_plan(m: int, vector_width: int = 4):
     # element group: slots 0..11 positions, 12..21 element data
     cols = [3 * tets[:, a] + i for a in range(4) for i in range(3)]
     cols += [ndof + N_ELEM_VARS * np.arange(ne, dtype=np.int64) + k for k in range(N_ELEM_VARS)]
-    res = B.add_group("nh_elem", 0, T, troots, cols, dest_kind="block")  # (78, ne)
+    res = B.add_group("nh_elem", 0, T, troots, cols, dest_kind="block",
+                      locals_=shared_nodes(T, troots))  # (78, ne)
     # triplets (cell, contribution): both halves of every off-diagonal entry
     nq = len(UPPER)
     d1 = np.array([u for u, _ in UPPER])

@@ -57,7 +57,7 @@ class PlanBuilder:
 
     def add_group(self, name: str, level: int, template: Template, roots: list[int],
                   slot_addrs: list[np.ndarray], const_cols: list[np.ndarray] | None = None,
-                  dest_kind: str = "intermediate", gap: int = 0) -> np.ndarray:
+                  dest_kind: str = "intermediate", gap: int = 0, locals_: list[int] | None = None) -> np.ndarray:
         """Append one group; returns its result addresses, shape (n_roots, N).
 
         ``gap`` reserves zero padding after the result range (room for the
@@ -92,7 +92,7 @@ class PlanBuilder:
         kp = KernelPlan(
             name=name, level=level, dest_kind=dest_kind, instances=n, n_roots=len(roots),
             dest_base=dest, template_arena=template, template_roots=list(roots),
-            template_locals=[], pos_vars=list(range(n_pos)),
+            template_locals=list(locals_ or []), pos_vars=list(range(n_pos)),
             const_vars=list(range(n_pos, n_pos + len(const_cols))),
             coherence=coh, retained=retained, p_base=p_base, c_base=c_base, layout="coalesced",
         )
