@@ -165,23 +165,20 @@ def _ragged_groups(keys: np.ndarray):
     return keys[starts], starts, counts
 
 
-def build_lmlt_plan(w: int, a_nnz: int = 6, a_seed: int = 7, a_cols: np.ndarray | None = None,
-                    vector_width: int = 4):
-    """ExecutionPlan for out = L.M.L^T + A on a w x w cotan grid mesh.
+def build_cotan(B, w: int, with_mass: bool = True):
+    """Cotan Laplacian L (and lumped mass M) of the w x w grid mesh as plan groups.
 
-    Returns ``(plan, row_ptr, col_idx)``; ``plan.outputs`` follow the CSR order
-    of ``out``.  Inputs: 3n coordinates (vertex v at 3v..3v+2), then the
-    n*a_nnz values of A in pattern order (first_var = 3n).
+    Restates ``build_operator(..., weighting="cotan", with_mass)`` (sparse.py:343-395)
+    over vertex coordinates at inputs 3v..3v+2.  Returns a dict of numpy arrays:
+    L in CSR order (L_row, L_col, L_addr, L_sh, L_ptr), per undirected edge
+    (ekeys = a*n+b with a<b, eaddr), the diagonal (ldiag_addr) and, with mass,
+    m_addr / m_sh (M diagonal).
     """
     n = w * w
-    if a_cols is None:
-        a_cols = random_pattern_rows(n, min(a_nnz, n), a_seed)
-    a_nnz = a_cols.shape[1]
-    input_count = 3 * n + n * a_nnz
-    B = PlanBuilder(input_count, vector_width)
     F = grid_faces(w, w)
     nf = len(F)
     sh_w, sh_area = _face_struct_hashes()
+    gap = 2 * w + 8  # structured consumers reach at most w+1 anchors past either end
 
     # ---- per-face weights and area shares: anchor = the quad's lower-left vertex ----
     gap = 2 * w + 8  # structured consumers reach at most w+1 anchors past either end
@@ -230,24 +227,26 @@ def build_lmlt_plan(w: int, a_nnz: int = 6, a_seed: int = 7, a_cols: np.ndarray 
         eaddr[sel] = B.add_structured(f"loff{cnt}", 2, T, r, cols, ekeys[sel] // n, n, gap=gap)[0]
         esh[sel] = sh_negw if cnt == 1 else S.sh_apply(S.ADD, [sh_negw] * int(cnt))
 
-    # ---- M diagonal: area shares in face order ----
-    mv = F.reshape(-1)
-    mf = np.repeat(np.arange(nf), 3)
-    order = np.lexsort((mf, mv))
-    mv, mf = mv[order], mf[order]
-    mverts, mstarts, mcounts = _ragged_groups(mv)
-    m_addr = np.empty(n, np.int64)
-    m_sh = np.empty(n, dtype=object)
-    for cnt in np.unique(mcounts):
-        sel = np.flatnonzero(mcounts == cnt)
-        if cnt == 1:
-            m_addr[mverts[sel]] = area_addr[mf[mstarts[sel]]]
-            m_sh[mverts[sel]] = sh_area
-            continue
-        cols = [area_addr[mf[mstarts[sel] + s]] for s in range(cnt)]
-        T, r = _sum_template(int(cnt))
-        m_addr[mverts[sel]] = B.add_structured(f"mdiag{cnt}", 2, T, r, cols, mverts[sel], n, gap=gap)[0]
-        m_sh[mverts[sel]] = S.sh_apply(S.ADD, [sh_area] * int(cnt))
+    m_addr = m_sh = None
+    if with_mass:
+        # ---- M diagonal: area shares in face order ----
+        mv = F.reshape(-1)
+        mf = np.repeat(np.arange(nf), 3)
+        order = np.lexsort((mf, mv))
+        mv, mf = mv[order], mf[order]
+        mverts, mstarts, mcounts = _ragged_groups(mv)
+        m_addr = np.empty(n, np.int64)
+        m_sh = np.empty(n, dtype=object)
+        for cnt in np.unique(mcounts):
+            sel = np.flatnonzero(mcounts == cnt)
+            if cnt == 1:
+                m_addr[mverts[sel]] = area_addr[mf[mstarts[sel]]]
+                m_sh[mverts[sel]] = sh_area
+                continue
+            cols = [area_addr[mf[mstarts[sel] + s]] for s in range(cnt)]
+            T, r = _sum_template(int(cnt))
+            m_addr[mverts[sel]] = B.add_structured(f"mdiag{cnt}", 2, T, r, cols, mverts[sel], n, gap=gap)[0]
+            m_sh[mverts[sel]] = S.sh_apply(S.ADD, [sh_area] * int(cnt))
 
     # ---- L in CSR: diagonal + both directions of every edge ----
     ea, eb = ekeys // n, ekeys % n
@@ -260,6 +259,32 @@ def build_lmlt_plan(w: int, a_nnz: int = 6, a_seed: int = 7, a_cols: np.ndarray 
     L_ptr = np.zeros(n + 1, np.int64)
     np.add.at(L_ptr, L_row + 1, 1)
     L_ptr = np.cumsum(L_ptr)
+
+    return dict(L_row=L_row, L_col=L_col, L_addr=L_addr, L_sh=L_sh, L_ptr=L_ptr, ekeys=ekeys, eaddr=eaddr,
+                ldiag_addr=ldiag_addr, m_addr=m_addr, m_sh=m_sh, gap=gap)
+
+
+def build_lmlt_plan(w: int, a_nnz: int = 6, a_seed: int = 7, a_cols: np.ndarray | None = None,
+                    vector_width: int = 4):
+    """ExecutionPlan for out = L.M.L^T + A on a w x w cotan grid mesh.
+
+    Returns ``(plan, row_ptr, col_idx)``; ``plan.outputs`` follow the CSR order
+    of ``out``.  Inputs: 3n coordinates (vertex v at 3v..3v+2), then the
+    n*a_nnz values of A in pattern order (first_var = 3n).
+    """
+    n = w * w
+    if a_cols is None:
+        a_cols = random_pattern_rows(n, min(a_nnz, n), a_seed)
+    a_nnz = a_cols.shape[1]
+    input_count = 3 * n + n * a_nnz
+    B = PlanBuilder(input_count, vector_width)
+    F = grid_faces(w, w)
+    nf = len(F)
+    sh_w, sh_area = _face_struct_hashes()
+
+    cot = build_cotan(B, w, with_mass=True)
+    L_row, L_col, L_addr, L_sh, L_ptr = cot["L_row"], cot["L_col"], cot["L_addr"], cot["L_sh"], cot["L_ptr"]
+    m_addr, m_sh, gap = cot["m_addr"], cot["m_sh"], cot["gap"]
 
     # ---- LM = L * M (one term per entry) ----
     T, r = _product_template()

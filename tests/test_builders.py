@@ -91,3 +91,20 @@ def test_fem_element_template_counts():
     T, roots, sh, rank = element_template()
     assert len(roots) == 78
     assert len(reachable(T, roots)) < 3000  # hand-structured: ~1.5k ops, not the 68k of naive autodiff
+
+
+@pytest.mark.parametrize("w", [3, 5])
+def test_arap_builder_matches_reference_trace(w):
+    """C4: the ARAP builder (L via the C2 cotan restatement, per-valence rotation / rhs templates)
+    == the reference trace (tests/golden/arap_w*): same L pattern, every output bit-identical."""
+    from paper_2110_12865_b200.programs.arap import arap_inputs, build_arap_plan
+
+    g = Golden(f"arap_w{w}")
+    plan, row_ptr, col_idx = build_arap_plan(w)
+    assert np.array_equal(row_ptr, g.vec["row_ptr"])
+    assert np.array_equal(col_idx, g.vec["col_idx"])
+    assert np.array_equal(arap_inputs(w), g.inputs)
+    out = oracle.run_outputs(plan, g.inputs)
+    assert np.array_equal(bits(out), bits(g.oracle))
+    x = emu.run_values(lower_plan(plan, jit=False), g.inputs)
+    assert np.array_equal(bits(x[np.asarray(plan.outputs)]), bits(g.oracle))

@@ -15,6 +15,11 @@ def test_oracle_matches_reference_interpreter_bitwise(golden):
 
 def test_oracle_outputs_match_eval_numeric(golden):
     out = oracle.run_outputs(golden.plan, golden.inputs)
+    if golden.meta.get("reference_plan_defect"):
+        # the reference's own plan is wrong here (meta.json says why); pin that it still is
+        o = golden.oracle
+        assert not np.allclose(out, o, rtol=1e-6, atol=0)
+        return
     if golden.meta["oracle_bitwise"]:
         assert np.array_equal(bits(out), bits(golden.oracle))
     else:
