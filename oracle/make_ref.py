@@ -48,7 +48,9 @@ def plan_fingerprint(plan) -> str:
 
 
 BUILDER_SOURCES = ("paper_2110_12865_b200/programs/mesh.py", "paper_2110_12865_b200/programs/planbuild.py",
-                   "paper_2110_12865_b200/programs/structhash.py", "paper_2110_12865_b200/plan.py")
+                   "paper_2110_12865_b200/programs/structhash.py", "paper_2110_12865_b200/plan.py",
+                   "paper_2110_12865_b200/programs/fem.py", "paper_2110_12865_b200/programs/arap.py",
+                   "paper_2110_12865_b200/programs/symtrace.py")
 
 
 def builder_hash() -> str:
@@ -112,12 +114,14 @@ def main():
             continue
         src = emit_for_plan(load_plan(ROOT / "tests" / "golden" / name), name)
         print(f"wrote {src}")
-    for w in (args.w, 200):  # C2 and the C5 plan
-        key = bench.workload_key(argparse.Namespace(w=w))
+    cfgs = [argparse.Namespace(config="c2", w=w) for w in (args.w, 200)]  # C2 and the C5 plan
+    cfgs += [argparse.Namespace(config="c3", m=55), argparse.Namespace(config="c4", w4=708)]
+    for ns in cfgs:
+        key = bench.workload_key(ns)
         if args.if_stale and up_to_date(key):
             print(f"oracle/_ref/{key}.c is up to date")
             continue
-        key, plan, _, _ = bench.build_workload(argparse.Namespace(w=w), 0, 1)
+        key, plan, _, _ = bench.build_workload(ns, 0, 1)
         src = emit_for_plan(plan, key)
         print(f"wrote {src} ({src.stat().st_size / 1e6:.1f} MB) for {key}")
 

@@ -82,10 +82,28 @@ def _imm(v: float) -> str:
     return f"bits(0x{np.float64(v).view(np.uint64).item():016x}ULL)"
 
 
-def _column(rec, col: int, i: str = "i") -> str:
+def _affine(dp, rec, col: int):
+    """(base, stride) when retained column ``col`` of the group is base + stride * i (baked in, no load)."""
+    n = int(rec["n"])
+    if n < 2 or rec["flags"] & L.FLAG_INTERLEAVED:
+        return None
+    if col == 0 and rec["flags"] & L.FLAG_AFFINE0:
+        return int(rec["a0_base"]), int(rec["a0_stride"])
+    off = int(rec["p_off"]) + col * n
+    c = np.asarray(dp.positions[off: off + n], dtype=np.int64)
+    base, stride = int(c[0]), int(c[1] - c[0])
+    if np.array_equal(c, base + stride * np.arange(n, dtype=np.int64)):
+        return base, stride
+    return None
+
+
+def _column(rec, col: int, i: str = "i", dp=None) -> str:
     """Index expression (u32) of retained column ``col`` for instance ``i``."""
     n = int(rec["n"])
     f = int(rec["flags"])
+    aff = _affine(dp, rec, col) if dp is not None else None
+    if aff is not None:
+        return f"(u32)({aff[0]}LL + {aff[1]}LL * {i})"
     if col == 0 and f & L.FLAG_AFFINE0:
         return f"(u32)({int(rec['a0_base'])}LL + {int(rec['a0_stride'])}LL * {i})"
     if f & L.FLAG_W16:
@@ -128,7 +146,7 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
     loads, comp = [], []
     reg: dict[int, str] = {}
     i = iv
-    col = lambda c: _column(rec, c, i)  # noqa: E731
+    col = lambda c: _column(rec, c, i, dp)  # noqa: E731
     if S:
         loads.append(f"const u32 idx0{sfx} = {col(0)};")
     for s_ in range(S):

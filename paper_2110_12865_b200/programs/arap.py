@@ -144,7 +144,8 @@ def build_arap_plan(w: int, vector_width: int = 4):
             cols += [nb_addr[nb_start[verts] + k]] + [3 * j + c for c in range(3)] + \
                     [3 * n + 3 * j + c for c in range(3)]
         T, roots = _rotation_template(v)
-        R_addr[:, verts] = B.add_group(f"rot{v}", 1, T, roots, cols, dest_kind="block")
+        scales = [3] * 6 + [1, 3, 3, 3, 3, 3, 3] * v  # positions 3/vertex, L entries 1/anchor
+        R_addr[:, verts] = B.add_affine_classes(f"rot{v}", 1, T, roots, cols, verts, scales, dest_kind="block")
     b_addr = np.empty((3, n), np.int64)
     for v in np.unique(val).tolist():
         verts = np.flatnonzero(val == v)
@@ -153,7 +154,8 @@ def build_arap_plan(w: int, vector_width: int = 4):
             j = nb_col[nb_start[verts] + k]
             cols += [nb_addr[nb_start[verts] + k]] + [R_addr[c, j] for c in range(9)] + [3 * j + c for c in range(3)]
         T, roots = _rhs_template(v)
-        b_addr[:, verts] = B.add_group(f"rhs{v}", 0, T, roots, cols, dest_kind="output")
+        scales = [1] * 9 + [3] * 3 + ([1] * 10 + [3] * 3) * v
+        b_addr[:, verts] = B.add_affine_classes(f"rhs{v}", 0, T, roots, cols, verts, scales, dest_kind="output")
     outputs = np.concatenate([L_addr, b_addr.T.reshape(-1)])
     plan = B.finish(outputs, {"program": "arap", "w": w, "rotation": "gram-schmidt"})
     return plan, L_ptr, L_col

@@ -202,22 +202,30 @@ def build_fem_plan(m: int, vector_width: int = 4):
     sh_rank = {h: r for r, h in enumerate(sorted(set(sh.tolist())))}
     shq = np.array([sh_rank[h] for h in sh.tolist()], dtype=np.int64)
     cell = rows * ndof + colsc
-    order = np.lexsort((rank[qq], ee, shq[qq], cell))
-    cell_s, q_s, e_s = cell[order], qq[order], ee[order]
+    # cells (r, c) and (c, r) sum the same contributions: the reference's hash-consing
+    # makes them ONE node (expr.py:252-255) -- sums are built for r <= c only
+    upper = rows <= colsc
+    ucell_all = np.unique(cell)
+    cell_u, q_u, e_u = cell[upper], qq[upper], ee[upper]
+    order = np.lexsort((rank[q_u], e_u, shq[q_u], cell_u))
+    cell_s, q_s, e_s = cell_u[order], q_u[order], e_u[order]
     addr = res[q_s, e_s]
     starts = np.flatnonzero(np.concatenate([[True], cell_s[1:] != cell_s[:-1]]))
     counts = np.diff(np.concatenate([starts, [cell_s.size]]))
     ucell = cell_s[starts]
-    out_addr = np.empty(ucell.size, dtype=np.int64)
+    up_addr = np.empty(ucell.size, dtype=np.int64)
     single = counts == 1
-    out_addr[single] = addr[starts[single]]
+    up_addr[single] = addr[starts[single]]
     for k in np.unique(counts[~single]).tolist():
         sel = np.flatnonzero(counts == k)
         slot_cols = [addr[starts[sel] + j] for j in range(k)]
         tk, rk = _sum_template(k)
-        out_addr[sel] = B.add_group(f"nh_sum{k}", 1, tk, rk, slot_cols, dest_kind="output")[0]
-    r = ucell // ndof
-    c = ucell % ndof
+        up_addr[sel] = B.add_group(f"nh_sum{k}", 1, tk, rk, slot_cols, dest_kind="output")[0]
+    r = ucell_all // ndof
+    c = ucell_all % ndof
+    canon = np.minimum(r, c) * ndof + np.maximum(r, c)
+    out_addr = up_addr[np.searchsorted(ucell, canon)]
+    ucell = ucell_all
     row_ptr = np.zeros(ndof + 1, dtype=np.int64)
     np.add.at(row_ptr, r + 1, 1)
     row_ptr = np.cumsum(row_ptr)

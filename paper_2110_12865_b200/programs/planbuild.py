@@ -209,6 +209,48 @@ class PlanBuilder:
                                                  [c[order] for c in cols], None, dest_kind)
         return out
 
+    def add_affine_classes(self, name: str, level: int, template: Template, roots: list[int],
+                           slot_addrs: list[np.ndarray], anchor: np.ndarray, scales, min_members: int = 4096,
+                           min_fill: float = 0.5, dest_kind: str = "intermediate") -> np.ndarray:
+        """Groups whose every index column is affine in the instance.
+
+        Entities with the same offset vector ``addr_s - scale_s * anchor`` form
+        a class; a class with at least ``min_members`` entities filling at
+        least ``min_fill`` of its anchor range [a_lo, a_hi] becomes one group
+        of a_hi - a_lo + 1 instances, instance k = anchor a_lo + k (anchors of
+        the range outside the class compute the same formula on in-range
+        neighbour values: results nobody reads).  Every slot is then
+        ``scale_s * (a_lo + k) + rel_s``: affine column 0, coherent rest (one
+        index column, lane-contiguous gathers).  The rest goes to add_group.
+        """
+        cols = [np.asarray(c, dtype=np.int64) for c in slot_addrs]
+        anchor = np.asarray(anchor, dtype=np.int64)
+        E = len(anchor)
+        out = np.empty((len(roots), E), dtype=np.int64)
+        if E == 0:
+            return out
+        sc = np.asarray(list(scales), dtype=np.int64)
+        rel = np.stack([c - s_ * anchor for c, s_ in zip(cols, sc.tolist())], axis=1)
+        inv, counts = _row_classes(rel)
+        done = np.zeros(E, dtype=bool)
+        for k, cls in enumerate(np.flatnonzero(counts >= min_members).tolist()):
+            members = np.flatnonzero(inv == cls)
+            a = anchor[members]
+            a_lo, a_hi = int(a.min()), int(a.max())
+            if np.unique(a).size != a.size or a.size < min_fill * (a_hi - a_lo + 1):
+                continue
+            r = rel[members[0]]
+            grid = np.arange(a_lo, a_hi + 1, dtype=np.int64)
+            sub = [s_ * grid + int(rv) for s_, rv in zip(sc.tolist(), r.tolist())]
+            res = self.add_group(f"{name}_a{k}", level, template, roots, sub, None, dest_kind)
+            out[:, members] = res[:, a - a_lo]
+            done[members] = True
+        rest = np.flatnonzero(~done)
+        if rest.size:
+            out[:, rest] = self.add_group(f"{name}_r", level, template, roots, [c[rest] for c in cols], None,
+                                          dest_kind)
+        return out
+
     def finish(self, outputs: np.ndarray, metadata: dict) -> ExecutionPlan:
         outputs = np.asarray(outputs, dtype=np.int64)
         return ExecutionPlan(
