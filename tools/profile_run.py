@@ -15,13 +15,15 @@ ap.add_argument("--w", type=int, default=1000)
 ap.add_argument("--evals", type=int, default=3)
 ap.add_argument("--batch", type=int, default=0)
 ap.add_argument("--mode", choices=("csr", "val"), default="csr")
+ap.add_argument("--config", choices=("c2", "c3", "c4"), default="c2")
+ap.add_argument("--m", type=int, default=55)
+ap.add_argument("--w4", type=int, default=708)
 args = ap.parse_args()
 
 import torch  # noqa: E402
 
 import bench  # noqa: E402
 from paper_2110_12865_b200 import DevicePlan  # noqa: E402
-from paper_2110_12865_b200.programs.mesh import lmlt_inputs  # noqa: E402
 
 t0 = time.time()
 key, plan, _, _ = bench.build_workload(args, 0, 1)
@@ -31,12 +33,12 @@ dp = DevicePlan(plan)
 print("waves", dp.launches, "units", dp.units, "csr units", dp.csr_units, flush=True)
 if args.batch:
     X = torch.zeros((plan.value_array_size, args.batch), dtype=torch.float64, device="cuda")
-    X[: plan.input_count] = torch.from_numpy(lmlt_inputs(args.w)).cuda()[:, None]
+    X[: plan.input_count] = torch.from_numpy(bench.workload_inputs(args, 0)).cuda()[:, None]
     out = torch.empty((len(plan.outputs), args.batch), dtype=torch.float64, device="cuda")
     for _ in range(args.evals):
         dp.run_batch_csr(X, out)
 else:
-    x = dp.new_values(lmlt_inputs(args.w))
+    x = dp.new_values(bench.workload_inputs(args, 0))
     out = torch.empty(len(plan.outputs), dtype=torch.float64, device="cuda")
     for _ in range(args.evals):
         if args.mode == "csr":
