@@ -911,6 +911,7 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     tapes, imms, sops, scol, sdel, cbases, coffs, obases, ooffs, op32 = ([] for _ in range(10))
     n_tape = n_imm = n_sop = n_slot = n_cb = n_co = n_ob = n_oo = n_o32 = 0
     jit_tapes, jit_imms, jit_units = {}, {}, []
+    big_plan = any(g.n >= jit_min_n for g in groups) and jit_min_n > 0
     win_pieces: list = []
     win_off = [0]
     win_opos: dict = {}
@@ -919,9 +920,11 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     for w in range(total_waves):
         members = [j for j, g in enumerate(groups) if g.wave == w]
         plan_units = []
-        if jit:  # every big plain group of the wave (tape or sum-of-products) in one specialised kernel
+        if jit:  # every big plain group of the wave (tape or sum-of-products) in one specialised kernel;
+            # in a big plan the small groups of the wave join it (a tiny boundary group on the
+            # interpreter would outlast the whole specialised unit it runs beside)
             sj = [j for j in members if not groups[j].flags & (FLAG_SELFREF | FLAG_SERIAL)
-                  and (groups[j].n >= jit_min_n or groups[j].window or groups[j].window_value)]
+                  and (groups[j].n >= jit_min_n or big_plan or groups[j].window or groups[j].window_value)]
             for sel, tag in (([j for j in sj if not groups[j].window and not groups[j].window_value], 0),
                              ([j for j in sj if groups[j].window_value], UNIT_VALUE_ONLY),
                              ([j for j in sj if groups[j].window], UNIT_WINDOW)):
