@@ -800,6 +800,7 @@ def _tile_keys(g: _Group, starts: np.ndarray, tile: int) -> np.ndarray:
 
 
 JIT_MIN_N = 4096  # groups with fewer instances stay on the hand-written kernels (NVRTC time buys nothing)
+JIT_MAX_WAVE_GROUPS = 48  # ...unless they share a wave of at most this many groups with a big one
 
 
 def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = None,
@@ -911,7 +912,6 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     tapes, imms, sops, scol, sdel, cbases, coffs, obases, ooffs, op32 = ([] for _ in range(10))
     n_tape = n_imm = n_sop = n_slot = n_cb = n_co = n_ob = n_oo = n_o32 = 0
     jit_tapes, jit_imms, jit_units = {}, {}, []
-    big_plan = any(g.n >= jit_min_n for g in groups) and jit_min_n > 0
     win_pieces: list = []
     win_off = [0]
     win_opos: dict = {}
@@ -923,8 +923,10 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         if jit:  # every big plain group of the wave (tape or sum-of-products) in one specialised kernel;
             # in a big plan the small groups of the wave join it (a tiny boundary group on the
             # interpreter would outlast the whole specialised unit it runs beside)
-            sj = [j for j in members if not groups[j].flags & (FLAG_SELFREF | FLAG_SERIAL)
-                  and (groups[j].n >= jit_min_n or big_plan or groups[j].window or groups[j].window_value)]
+            plain_w = [j for j in members if not groups[j].flags & (FLAG_SELFREF | FLAG_SERIAL)]
+            big_wave = any(groups[j].n >= jit_min_n for j in plain_w) and len(plain_w) <= JIT_MAX_WAVE_GROUPS
+            sj = [j for j in plain_w
+                  if groups[j].n >= jit_min_n or big_wave or groups[j].window or groups[j].window_value]
             for sel, tag in (([j for j in sj if not groups[j].window and not groups[j].window_value], 0),
                              ([j for j in sj if groups[j].window_value], UNIT_VALUE_ONLY),
                              ([j for j in sj if groups[j].window], UNIT_WINDOW)):
