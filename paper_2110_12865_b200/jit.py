@@ -261,6 +261,9 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
     """
     unit = dp.unit(u)
     out = []
+    big = max(len(tapes[gi]) for gi in range(unit["group_begin"], unit["group_end"]))
+    # huge element templates: cap registers so two blocks (16 warps) stay resident per SM
+    min_blocks = int(os.environ.get("SGB_JIT_MINBLOCKS", "2" if big > 400 else "1"))
     for batched in (False, True):
         if batched:
             head = [f'extern "C" __global__ void __launch_bounds__({JIT_BLOCK}) sgb_tape_b{u}(',
@@ -272,7 +275,7 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
                     f"    for (i64 b = threadIdx.x & 31; b < batch; b += {32 * BATCH_VEC}) {{",
                     "    switch (tl.x) {"]
         else:
-            head = [f'extern "C" __global__ void __launch_bounds__({JIT_BLOCK}) sgb_tape_u{u}(',
+            head = [f'extern "C" __global__ void __launch_bounds__({JIT_BLOCK}, {min_blocks}) sgb_tape_u{u}(',
                     "    Tables T, const int2 *tiles, i64 n_tiles, double *x, double *out, int csr) {",
                     "  for (i64 t = blockIdx.x; t < n_tiles; t += gridDim.x) {",
                     "    const int2 tl = tiles[t];",

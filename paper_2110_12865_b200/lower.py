@@ -1049,9 +1049,15 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
             else:
                 t = np.concatenate(unit_tiles) if unit_tiles else np.zeros((0, 2), np.int64)
                 keys = np.concatenate(unit_keys) if unit_keys else np.zeros(0, np.int64)
-            if np.any(keys >= 0) and os.environ.get("SGB_TILE_ORDER", "csr") == "csr":
+            order_mode = os.environ.get("SGB_TILE_ORDER", "csr")
+            if np.any(keys >= 0) and order_mode == "csr":
                 # CSR-ordered schedule: partial sectors of the output merge in L2
                 t = t[np.argsort(keys, kind="stable")]
+            elif kind == KIND_TAPE and regs == 0 and order_mode != "group":
+                # specialised units: interleave the groups' tiles by instance, so groups that
+                # gather the same producer ranges (structured mesh groups) read them while they
+                # are still in L2
+                t = t[np.argsort(t[:, 1], kind="stable")]
             t0 = sum(len(x) for x in tiles_all)
             tiles_all.append(t)
             uflags = UNIT_CSR_ONLY if w >= n_waves else 0

@@ -14,13 +14,21 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_2110_12865_b200 import DevicePlan  # noqa: E402
 from paper_2110_12865_b200.lower import lower_plan  # noqa: E402
-from paper_2110_12865_b200.programs.mesh import lmlt_inputs  # noqa: E402
 
 w = int(sys.argv[1]) if len(sys.argv) > 1 else 1000
 variants = sys.argv[2].split(",") if len(sys.argv) > 2 else ["vec=0"]
-key, plan, _, _ = bench.build_workload(argparse.Namespace(w=w), 0, 1)
-inputs = lmlt_inputs(w)
-ref = None
+plans = {}
+
+
+def get_plan(cfg):
+    if cfg not in plans:
+        ns = argparse.Namespace(config=cfg, w=w, m=55, w4=708)
+        plans[cfg] = (bench.build_workload(ns, 0, 1)[1], bench.workload_inputs(ns, 0))
+    return plans[cfg]
+
+
+
+refs = {}
 for var in variants:
     env = dict(kv.split("=") for kv in var.split(";") if kv)
     os.environ["SGB_TAPE_VEC"] = env.get("vec", "0")
@@ -29,7 +37,13 @@ for var in variants:
     os.environ["SGB_TAPE_JIT"] = env.get("jit", "1")
     os.environ["SGB_CSR_WINDOW"] = env.get("window", "1")
     os.environ["SGB_DIRECT_CSR"] = env.get("direct", "0")
+    os.environ["SGB_JIT_MINBLOCKS"] = env.get("minblocks", "")
+    if not os.environ["SGB_JIT_MINBLOCKS"]:
+        del os.environ["SGB_JIT_MINBLOCKS"]
+    cfg = env.get("config", "c2")
     mode = env.get("mode", "csr")
+    plan, inputs = get_plan(cfg)
+    ref = refs.get(cfg)
     t0 = time.time()
     dp = DevicePlan(plan, lowered=lower_plan(plan))
     x = dp.new_values(inputs)
@@ -39,7 +53,7 @@ for var in variants:
     torch.cuda.synchronize()
     got = out.cpu().numpy()
     if ref is None:
-        ref = got
+        ref = refs[cfg] = got
     same = np.array_equal(got.view(np.uint64), ref.view(np.uint64))
     R = 20
     nw = dp.csr_launches if mode == "csr" else dp.launches
