@@ -262,8 +262,8 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
     unit = dp.unit(u)
     out = []
     big = max(len(tapes[gi]) for gi in range(unit["group_begin"], unit["group_end"]))
-    # huge element templates: cap registers so two blocks (16 warps) stay resident per SM
-    min_blocks = int(os.environ.get("SGB_JIT_MINBLOCKS", "2" if big > 400 else "1"))
+    # register cap (blocks per SM): huge templates run best uncapped -- spills cost more than occupancy
+    min_blocks = int(os.environ.get("SGB_JIT_MINBLOCKS", "1"))  # 2 measured 2.7x slower on C3 (r24)
     for batched in (False, True):
         if batched:
             head = [f'extern "C" __global__ void __launch_bounds__({JIT_BLOCK}) sgb_tape_b{u}(',

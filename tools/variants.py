@@ -35,7 +35,7 @@ for var in variants:
     os.environ["SGB_COMPRESS"] = env.get("compress", "1")
     os.environ["SGB_TILE_ORDER"] = env.get("order", "csr")
     os.environ["SGB_TAPE_JIT"] = env.get("jit", "1")
-    os.environ["SGB_CSR_WINDOW"] = env.get("window", "1")
+    os.environ["SGB_CSR_WINDOW"] = env.get("window", "0")
     os.environ["SGB_DIRECT_CSR"] = env.get("direct", "0")
     os.environ["SGB_JIT_MINBLOCKS"] = env.get("minblocks", "")
     if not os.environ["SGB_JIT_MINBLOCKS"]:
