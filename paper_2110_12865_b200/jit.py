@@ -263,7 +263,7 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
     out = []
     big = max(len(tapes[gi]) for gi in range(unit["group_begin"], unit["group_end"]))
     # register cap (blocks per SM): huge templates run best uncapped -- spills cost more than occupancy
-    min_blocks = int(os.environ.get("SGB_JIT_MINBLOCKS", "1"))  # 2 measured 2.7x slower on C3 (r24)
+    min_blocks = int(os.environ.get("SGB_JIT_MINBLOCKS", "0"))  # 2 measured 2.7x slower on C3 (r24)
     for batched in (False, True):
         if batched:
             head = [f'extern "C" __global__ void __launch_bounds__({JIT_BLOCK}) sgb_tape_b{u}(',
@@ -275,7 +275,8 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
                     f"    for (i64 b = threadIdx.x & 31; b < batch; b += {32 * BATCH_VEC}) {{",
                     "    switch (tl.x) {"]
         else:
-            head = [f'extern "C" __global__ void __launch_bounds__({JIT_BLOCK}, {min_blocks}) sgb_tape_u{u}(',
+            bounds = f"{JIT_BLOCK}, {min_blocks}" if min_blocks > 1 else f"{JIT_BLOCK}"
+            head = [f'extern "C" __global__ void __launch_bounds__({bounds}) sgb_tape_u{u}(',
                     "    Tables T, const int2 *tiles, i64 n_tiles, double *x, double *out, int csr) {",
                     "  for (i64 t = blockIdx.x; t < n_tiles; t += gridDim.x) {",
                     "    const int2 tl = tiles[t];",
