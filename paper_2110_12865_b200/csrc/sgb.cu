@@ -1190,6 +1190,8 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       for (int64_t i = 0; i < G.n; i += bwarps) btiles.push_back(make_int2(g, (int)i));
     }
     u.bt1 = (int64_t)btiles.size();
+    if (jit)  // as the single-set tiles (lower.py): interleave the groups' tiles by instance for L2 reuse
+      std::stable_sort(btiles.begin() + u.bt0, btiles.end(), [](const int2 &a, const int2 &b) { return a.y < b.y; });
     if (u.kind == KIND_TAPE && !jit) {  // every tape word must stay inside its lane's scratch column
       const uint64_t limit = (uint64_t)u.regs * u.bs * u.variant * 8;
       for (int g = u.g0; g < u.g1; ++g) {
