@@ -88,7 +88,9 @@ def build_workload(args, rank: int, world: int, barrier=None):
     """Plan + CSR pattern for the configured workload, cached across ranks."""
     key = workload_key(args)
     cache_dir = Path(os.environ.get("SGB_PLAN_CACHE", Path(tempfile.gettempdir()) / "sgb_plan_cache"))
-    path = cache_dir / f"{key}.pkl"
+    from paper_2110_12865_b200.programs import builder_hash  # a cache is valid only for its builder sources
+
+    path = cache_dir / f"{key}.{builder_hash()[:12]}.pkl"
     if rank == 0 and not path.exists():
         t0 = time.perf_counter()
         plan, row_ptr, col_idx = _build(args)

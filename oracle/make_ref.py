@@ -47,17 +47,11 @@ def plan_fingerprint(plan) -> str:
     return h.hexdigest()
 
 
-BUILDER_SOURCES = ("paper_2110_12865_b200/programs/mesh.py", "paper_2110_12865_b200/programs/planbuild.py",
-                   "paper_2110_12865_b200/programs/structhash.py", "paper_2110_12865_b200/plan.py",
-                   "paper_2110_12865_b200/programs/fem.py", "paper_2110_12865_b200/programs/arap.py",
-                   "paper_2110_12865_b200/programs/symtrace.py")
-
-
 def builder_hash() -> str:
-    h = hashlib.sha1()
-    for f in BUILDER_SOURCES:
-        h.update((ROOT / f).read_bytes())
-    return h.hexdigest()
+    sys.path.insert(0, str(ROOT))
+    from paper_2110_12865_b200.programs import builder_hash as bh
+
+    return bh()
 
 
 def up_to_date(key: str) -> bool:
