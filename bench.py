@@ -436,11 +436,12 @@ def run_spgemm(args):
     stream = torch.cuda.current_stream()
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     sampler = ClockSampler(0)
+    graph = dp.capture_csr(x, out)  # launch-bound: one graph launch per evaluation
     with sampler:
         for e0, e1 in evs:
             flush.fill_(1.0)
             e0.record(stream)
-            dp.run_csr(x, out)
+            graph.replay()
             e1.record(stream)
         torch.cuda.synchronize()
     ms = sum(e0.elapsed_time(e1) for e0, e1 in evs) / args.steps
@@ -466,7 +467,8 @@ def run_spgemm(args):
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"C1 spgemm C=A.B, random CSR 2000x2000 10 nnz/row, {n_out} out nnz (reference plan)",
-                   "l2": "flushed (512 MB write) before every timed evaluation", "parity": parity},
+                   "l2": "flushed (512 MB write) before every timed evaluation", "parity": parity,
+                   "launch": "CUDA graph of one sgb_run_csr evaluation, replayed per step"},
         "roofline": {"bound": "hbm", "achieved": bal / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                      "frac": bal / (ms * 1e-3) / 1e9 / peak, "traffic": None, "kernel": "whole evaluation",
                      "algorithmic_bytes": bal, "peak_source": peak_src},
@@ -556,11 +558,23 @@ def main():
             for _ in range(20):
                 dp.run_csr(x, out)
             torch.cuda.synchronize()
-        # ---- timed region: one step = every CSR-mode wave (inputs -> CSR values) ----
-        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_w + 1)] for _ in range(args.steps)]
+        # ---- timed region: one step = one CSR-mode evaluation (inputs -> CSR values), replayed
+        #      as a CUDA graph of every wave's launches and the output gather ----
+        graph = dp.capture_csr(x, out)
+        steps_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    for _ in range(args.steps)]
         if barrier:
             barrier()
         torch.cuda.synchronize()
+        for e0, e1 in steps_ev:
+            e0.record(stream)
+            graph.replay()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        if barrier:
+            barrier()
+        # per-launch breakdown (separate pass, wave by wave with events between launches)
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_w + 1)] for _ in range(args.steps)]
         for k in range(args.steps):
             e = evs[k]
             for w in range(n_w):
@@ -568,9 +582,7 @@ def main():
                 dp.run_wave(x, w, out=out)
             e[n_w].record(stream)
         torch.cuda.synchronize()
-        if barrier:
-            barrier()
-    total_ms = evs[0][0].elapsed_time(evs[-1][n_w])
+    total_ms = sum(e0.elapsed_time(e1) for e0, e1 in steps_ev)
     per_launch = np.zeros(n_w)
     for e in evs:
         for j in range(n_w):
@@ -649,6 +661,8 @@ def main():
             "clock_settle": "1 s of untimed evaluations before the timed region",
             "parity": parity, "mode": ("CSR, direct stores (sgb_run_csr)" if direct else
                                        "CSR (sgb_run_csr: value-array waves + u32-indexed output gather)"),
+            "launch": "CUDA graph of one sgb_run_csr evaluation replayed per step; per-launch times from a "
+                      "separate wave-by-wave pass",
             "achieved_hbm_gbs_step": step_bytes / (ms_per_step * 1e-3) / 1e9,
             "balg_bytes_step": step_bytes, "balg_bytes_single_pass": plan_balg(plan),
             "balg_gbs_single_pass": plan_balg(plan) / (ms_per_step * 1e-3) / 1e9,

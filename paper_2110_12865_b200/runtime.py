@@ -266,6 +266,25 @@ class DevicePlan:
                                      _stream_handle(stream)), "sgb_run_csr")
         return out
 
+    def capture_csr(self, x, out, batch: bool = False):
+        """A CUDA graph of one CSR-mode evaluation on these buffers (``graph.replay()`` re-runs it).
+
+        All launches of the evaluation -- every wave's units on the caller's stream and the
+        forked aux streams, and the output gather -- are captured once, so a replay costs one
+        graph launch instead of one launch per unit (launch-bound plans such as C1).
+        """
+        import torch
+
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream(device=x.device)
+        s.wait_stream(torch.cuda.current_stream(x.device))
+        with torch.cuda.stream(s):  # warm the launch path outside the capture
+            self.run_batch_csr(x, out) if batch else self.run_csr(x, out)
+        torch.cuda.current_stream(x.device).wait_stream(s)
+        with torch.cuda.graph(g):
+            self.run_batch_csr(x, out) if batch else self.run_csr(x, out)
+        return g
+
     def run_wave(self, x, wave: int, out=None, stream=None):
         """One dependency wave (profiling / per-launch timing); ``out`` given = CSR mode."""
         _check(self._lib.sgb_run_wave(self._handle, ctypes.c_void_p(x.data_ptr()),

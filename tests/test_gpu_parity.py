@@ -209,3 +209,24 @@ def test_wrong_input_length_raises():
     run = compile_plan(g.plan)
     with pytest.raises(ValueError):
         run(np.zeros(3))
+
+
+@pytest.mark.parametrize("name", ["lmlt_w12", "spgemm_n60_k4", "prog_energy-hessian_4x4_tag", "fem_nh_m2", "arap_w5"])
+def test_cuda_graph_replay_equals_run(name):
+    """capture_csr: a replayed CUDA graph of one evaluation (all units, aux streams, gather) == sgb_run_csr."""
+    import torch
+
+    from conftest import Golden
+    from paper_2110_12865_b200 import DevicePlan
+
+    g = Golden(name)
+    dp = DevicePlan(g.plan)
+    x = dp.new_values(g.inputs)
+    out = torch.empty(len(g.plan.outputs), dtype=torch.float64, device=x.device)
+    want = dp.run_csr(dp.new_values(g.inputs)).cpu().numpy()
+    graph = dp.capture_csr(x, out)
+    out.fill_(float("nan"))
+    graph.replay()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(out.cpu().numpy()), bits(want))
