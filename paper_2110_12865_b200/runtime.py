@@ -277,12 +277,19 @@ class DevicePlan:
 
         g = torch.cuda.CUDAGraph()
         s = torch.cuda.Stream(device=x.device)
+        rezero = self.lowered.needs_zero == 2  # reads precede writes: every evaluation starts from zeros
+
+        def body():
+            if rezero:
+                x[self.input_count:].zero_()
+            self.run_batch_csr(x, out) if batch else self.run_csr(x, out)
+
         s.wait_stream(torch.cuda.current_stream(x.device))
         with torch.cuda.stream(s):  # warm the launch path outside the capture
-            self.run_batch_csr(x, out) if batch else self.run_csr(x, out)
+            body()
         torch.cuda.current_stream(x.device).wait_stream(s)
         with torch.cuda.graph(g):
-            self.run_batch_csr(x, out) if batch else self.run_csr(x, out)
+            body()
         return g
 
     def run_wave(self, x, wave: int, out=None, stream=None):
