@@ -36,7 +36,7 @@ import numpy as np
 from . import lower as L
 
 JIT_BLOCK = 256  # threads per block = instances per tile of a specialised unit
-BATCH_VEC = 4  # batched kernels: value sets per lane per iteration (loads of all in flight)
+BATCH_VEC = int(os.environ.get("SGB_BATCH_VEC", "4"))  # batched: value sets per lane per iteration
 CACHE = Path(os.environ.get("SGB_JIT_CACHE", Path.home() / ".cache" / "sgb_jit"))
 
 _PREAMBLE = r"""

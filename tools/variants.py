@@ -41,6 +41,11 @@ for var in variants:
     if not os.environ["SGB_JIT_MINBLOCKS"]:
         del os.environ["SGB_JIT_MINBLOCKS"]
     cfg = env.get("config", "c2")
+    for k_, e_ in (("jitvec", "SGB_JIT_VEC"), ("bvec", "SGB_BATCH_VEC")):
+        if k_ in env:
+            os.environ[e_] = env[k_]
+        else:
+            os.environ.pop(e_, None)
     mode = env.get("mode", "csr")
     plan, inputs = get_plan(cfg)
     ref = refs.get(cfg)
