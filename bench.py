@@ -316,7 +316,7 @@ def run_batched(args):
     first, b = shard_value_sets(total, world, rank)
     sets = list(range(first, first + b))  # value set s = lmlt_inputs(seed=s)
     host_in = np.stack([lmlt_inputs(args.w, seed=s_) for s_ in sets], axis=1)  # [n_in, b]
-    dp = DevicePlan(plan, device=local)
+    dp = DevicePlan(plan, device=local, csr_layout=args.layout == "csr")
     X = torch.zeros((plan.value_array_size, b), dtype=torch.float64, device=f"cuda:{local}")
     X[:n_in] = torch.from_numpy(host_in).to(X.device)
     out = torch.empty((n_out, b), dtype=torch.float64, device=X.device)
@@ -423,7 +423,7 @@ def run_spgemm(args):
     with np.load(gdir / "vectors.npz") as z:
         inputs, ref_values = z["inputs"], z["values"]
     n_out = len(plan.outputs)
-    dp = DevicePlan(plan)
+    dp = DevicePlan(plan, csr_layout=args.layout == "csr")
     x = dp.new_values(inputs)
     out = torch.empty(n_out, dtype=torch.float64, device=x.device)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float64, device=x.device)  # 512 MB > L2
@@ -497,6 +497,9 @@ def main():
     ap.add_argument("--w5", type=int, default=200, help="C5 grid width")
     ap.add_argument("--batch", type=int, default=256, help="C5 value sets (whole job)")
     ap.add_argument("--gather", action="store_true", help="C5: also time the NCCL gather to rank 0")
+    ap.add_argument("--layout", choices=("csr", "reference"), default="csr",
+                    help="csr: multi-root groups whose readers gather across roots store instance-major "
+                         "(lower.choose_relayout); reference: the plan's own value-array layout")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -524,7 +527,7 @@ def main():
     key, plan, row_ptr, col_idx = build_workload(args, rank, world, barrier)
     n_out = len(plan.outputs)
     inputs = workload_inputs(args, seed=rank)
-    dp = DevicePlan(plan, device=local)
+    dp = DevicePlan(plan, device=local, csr_layout=args.layout == "csr")
     x = dp.new_values(inputs)
     out = torch.empty(n_out, dtype=torch.float64, device=x.device)
     stream = torch.cuda.current_stream()
@@ -663,6 +666,8 @@ def main():
                                        "CSR (sgb_run_csr: value-array waves + u32-indexed output gather)"),
             "launch": "CUDA graph of one sgb_run_csr evaluation replayed per step; per-launch times from a "
                       "separate wave-by-wave pass",
+            "layout": (f"CSR layout: plan groups {dp.lowered.csr_layout} store instance-major"
+                       if dp.csr_layout else "reference value-array layout"),
             "achieved_hbm_gbs_step": step_bytes / (ms_per_step * 1e-3) / 1e9,
             "balg_bytes_step": step_bytes, "balg_bytes_single_pass": plan_balg(plan),
             "balg_gbs_single_pass": plan_balg(plan) / (ms_per_step * 1e-3) / 1e9,

@@ -44,7 +44,9 @@ typedef struct sgb_plan sgb_plan;
  * Mirrors one reference KernelPlan (codegen.py:56-85). */
 typedef struct sgb_group {
   int64_t n;         /* instances (KernelPlan.instances) */
-  int64_t dest_base; /* result r of instance i at dest_base + r*n + i (codegen.py:265) */
+  int64_t dest_base; /* result r of instance i at dest_base + r*n + i (codegen.py:265); with flags & 2048
+                        (CSR layout, specialised units only) at dest_base + i*n_roots + r -- plan addresses
+                        are re-mapped to match, and value-mode calls on such a plan return -2 */
   int64_t p_off;     /* KernelPlan.p_base (synthetic copy groups: past the plan's table) */
   int64_t c_off;     /* KernelPlan.c_base */
   int64_t tape_off;  /* first tape row */

@@ -52,7 +52,8 @@ enum : int {
 enum : int { KIND_TAPE = 0, KIND_SOP = 1 };
 enum : int {
   FLAG_SELFREF = 1, FLAG_INTERLEAVED = 2, FLAG_SERIAL = 4, FLAG_STREAM = 16, FLAG_W16 = 32,
-  FLAG_AFFINE0 = 64, FLAG_OPOS16 = 128, FLAG_OPOS32 = 256, FLAG_CSR_ONLY = 512, FLAG_COHERENT = 1024
+  FLAG_AFFINE0 = 64, FLAG_OPOS16 = 128, FLAG_OPOS32 = 256, FLAG_CSR_ONLY = 512, FLAG_COHERENT = 1024,
+  FLAG_IMAJOR = 2048  // CSR layout: result r of instance i at dest_base + i * n_roots + r (specialised units)
 };
 enum : int {
   U_WAVE = 0, U_KIND, U_VARIANT, U_G0, U_G1, U_T0, U_T1, U_BS, U_REGS, U_FLAGS, U_COUNT
@@ -782,6 +783,7 @@ struct sgb_plan {
   int64_t *d_outputs = nullptr;
   uint32_t *d_outputs32 = nullptr;
   bool direct_csr = false;  // some group stores its outputs at their CSR positions (FLAG_OPOS*)
+  bool csr_layout = false;  // some group stores instance-major (FLAG_IMAJOR): the value array is permuted
   uint32_t *d_tape = nullptr;
   double *d_imm = nullptr, *d_con = nullptr;
   uint32_t *d_sop = nullptr;
@@ -1163,6 +1165,10 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       for (int g = u.g0; g < u.g1; ++g)
         if (d->groups[g].flags & (FLAG_SELFREF | FLAG_SERIAL))
           return fail(-1, "sgb_plan_create: self-referencing group in a specialised unit");
+    if (!jit)
+      for (int g = u.g0; g < u.g1; ++g)
+        if (d->groups[g].flags & FLAG_IMAJOR)
+          return fail(-1, "sgb_plan_create: instance-major group outside a specialised unit");
     for (int64_t t = window ? u.t1 : u.t0; t < u.t1; ++t) {  // tiles name groups of this unit, start inside them
       const int32_t *tl = d->tiles + 2 * t;
       if (tl[0] < u.g0 || tl[0] >= u.g1 || tl[1] < 0 || (int64_t)tl[1] >= d->groups[tl[0]].n)
@@ -1247,6 +1253,8 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
   std::vector<uint32_t> outputs32(d->outputs, d->outputs + d->n_outputs);
   for (int g = 0; g < d->n_groups; ++g)
     if (d->groups[g].flags & (FLAG_OPOS16 | FLAG_OPOS32)) p->direct_csr = true;
+  for (int g = 0; g < d->n_groups; ++g)
+    if (d->groups[g].flags & FLAG_IMAJOR) p->csr_layout = true;
   // compact sum-of-products descriptors (+ fast-path factor bases)
   std::vector<SopDesc> sopd(d->n_groups);
   std::vector<uint32_t> fbase;
@@ -1362,6 +1370,7 @@ static int launch_all(sgb_plan *p, double *x, int64_t ld, int64_t batch, bool ba
 int sgb_run_wave(sgb_plan *p, double *x, double *out, int wave, void *stream) {
   if (!p || (!x && p->vas)) return fail(-1, "sgb_run_wave: null argument");
   const bool csr = out != nullptr;
+  if (!csr && p->csr_layout) return fail(-2, "sgb_run_wave: plan uses the CSR layout (value mode unavailable)");
   if (wave < 0 || wave >= sgb_plan_waves(p, csr)) return fail(-1, "sgb_run_wave: wave out of range");
   if (csr && p->n_out == 0) return 0;
   std::lock_guard<std::mutex> lk(p->run_mu);
@@ -1379,6 +1388,7 @@ int sgb_run_wave(sgb_plan *p, double *x, double *out, int wave, void *stream) {
 
 int sgb_run_values(sgb_plan *p, double *x, void *stream) {
   if (!p || (!x && p->vas)) return fail(-1, "sgb_run_values: null argument");
+  if (p->csr_layout) return fail(-2, "sgb_run_values: plan uses the CSR layout (value mode unavailable)");
   return launch_all(p, x, 1, 1, false, nullptr, 1, false, (cudaStream_t)stream);
 }
 
@@ -1391,6 +1401,7 @@ int sgb_run_csr(sgb_plan *p, double *x, double *out, void *stream) {
 int sgb_run_batch(sgb_plan *p, double *X, int64_t ld, int64_t batch, void *stream) {
   if (!p || (!X && p->vas)) return fail(-1, "sgb_run_batch: null argument");
   if (batch < 1 || ld < batch) return fail(-1, "sgb_run_batch: need 1 <= batch <= ld");
+  if (p->csr_layout) return fail(-2, "sgb_run_batch: plan uses the CSR layout (value mode unavailable)");
   return launch_all(p, X, ld, batch, true, nullptr, 1, false, (cudaStream_t)stream);
 }
 
@@ -1457,6 +1468,7 @@ int sgb_sg_run(sgb_plan *p, double *x_host, const double *c_host, const unsigned
   (void)c_host;
   (void)p_host;
   if (!p || (!x_host && p->vas)) return fail(-1, "sgb_sg_run: null argument");
+  if (p->csr_layout) return fail(-2, "sgb_sg_run: plan uses the CSR layout (value mode unavailable)");
   std::lock_guard<std::mutex> lk(p->ws_mu);
   int rc = ensure_ws(p);
   if (rc) return rc;

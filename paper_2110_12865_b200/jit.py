@@ -177,7 +177,10 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
         if op == L.T_ST:
             r = aux
             v = reg[a]
-            x_addr = X(f"{int(rec['dest_base']) + r * n}LL + {i}")
+            if flags & L.FLAG_IMAJOR:  # CSR layout (lower._RelaidPlan): instance-major results
+                x_addr = X(f"{int(rec['dest_base']) + r}LL + {i} * {int(rec['n_roots'])}LL")
+            else:
+                x_addr = X(f"{int(rec['dest_base']) + r * n}LL + {i}")
             store = f"st_stream({x_addr}, {v});" if stream else f"*({x_addr}) = {v};"
             comp.append(f"if (ok{sfx}{' && !csr' if stream else ''}) {store}")
             if _out_pos(rec, r) is not None:

@@ -48,6 +48,7 @@ FLAG_OPOS16 = 128  # output positions: u32 base per 32 instances + u16 offset (0
 FLAG_OPOS32 = 256  # output positions: u32 per instance (0xFFFFFFFF = not an output)
 FLAG_CSR_ONLY = 512  # synthetic copy group: runs in CSR mode only
 FLAG_COHERENT = 1024  # one retained column: every slot is column 0 + delta
+FLAG_IMAJOR = 2048  # CSR layout: result r of instance i at dest_base + i * n_roots + r (specialised units only)
 UNIT_CSR_ONLY = 1
 UNIT_JIT = 2  # tape unit compiled to straight-line code (jit.py), one instance per thread
 UNIT_VALUE_ONLY = 4  # value-mode twin of a CSR-window unit (skipped by sgb_run_csr)
@@ -125,6 +126,7 @@ class DevicePlanArrays:
     win_pieces: np.ndarray = None  # int32 [n, 4]: group, first instance, count, item prefix (CSR windows)
     win_off: np.ndarray = None  # int64 [n_windows + 1]: first piece of each window
     window_units: list = field(default_factory=list)
+    csr_layout: list = field(default_factory=list)  # plan kernels stored instance-major (FLAG_IMAJOR)
 
     def unit(self, u: int) -> dict:
         return dict(zip(UNIT_FIELDS, (int(v) for v in self.units[u])))
@@ -799,13 +801,134 @@ def _tile_keys(g: _Group, starts: np.ndarray, tile: int) -> np.ndarray:
     return np.where(m == np.iinfo(np.int64).max, -1, m)
 
 
+class _RelaidPlan:
+    """A plan with the result ranges of some groups re-addressed instance-major (CSR layout).
+
+    Result r of instance i of a relaid group moves from ``dest_base + r*N + i``
+    (codegen.py:265) to ``dest_base + i*R + r``: a bijection inside the group's
+    own range, applied to every address the plan holds (the position table and
+    the outputs), so every read still finds the value it read before and the
+    CSR values are unchanged bit for bit.  Only the full value array is
+    permuted, which is why a relaid device plan refuses value-mode calls.
+    """
+
+    def __init__(self, plan, groups: list[int]):
+        self._plan = plan
+        kps = [plan.kernels[k] for k in groups]
+        order = np.argsort([kp.dest_base for kp in kps])
+        self.lo = np.array([kps[j].dest_base for j in order], np.int64)
+        self.nn = np.array([kps[j].instances for j in order], np.int64)
+        self.rr = np.array([kps[j].n_roots for j in order], np.int64)
+        self.hi = self.lo + self.nn * self.rr
+        self.positions = self.remap(np.asarray(plan.positions)).astype(np.uint32)
+        self.outputs = self.remap(np.asarray(plan.outputs, np.int64)).astype(np.int64)
+
+    def __getattr__(self, name):
+        return getattr(self._plan, name)
+
+    def remap(self, addr: np.ndarray, chunk: int = 1 << 24) -> np.ndarray:
+        out = np.array(addr, dtype=np.int64, copy=True)
+        for s in range(0, out.size, chunk):
+            a = out[s: s + chunk]
+            k = np.searchsorted(self.lo, a, side="right") - 1
+            kc = np.maximum(k, 0)
+            m = (k >= 0) & (a < self.hi[kc])
+            if not m.any():
+                continue
+            kk, off = kc[m], a[m] - self.lo[kc[m]]
+            n = self.nn[kk]
+            a[m] = self.lo[kk] + (off % n) * self.rr[kk] + off // n
+        return out
+
+
+RELAYOUT_GAIN = 0.75  # relay a group out when its readers touch at most this fraction of the sectors
+RELAYOUT_SAMPLE_WARPS = 8192
+
+
+def _warp_sectors(col: np.ndarray, lo: int, n: int, r: int, imajor: bool) -> int:
+    """Distinct 32-byte sectors per 32-instance warp of the reads of ``col`` inside [lo, lo + r*n)."""
+    warp = np.arange(col.size, dtype=np.int64) // 32
+    m = (col >= lo) & (col < lo + r * n)
+    if not m.any():
+        return 0
+    off = col[m] - lo
+    if imajor:
+        off = (off % n) * r + off // n
+    key = warp[m] * (1 << 40) + ((lo + off) >> 2)
+    return int(np.unique(key).size)
+
+
+def choose_relayout(plan, lowered, candidates: list[int], mode: str = "auto"):
+    """Groups whose results move to the instance-major CSR layout, and the coherent deltas that change.
+
+    ``auto``: a multi-root group moves when its readers -- every position
+    column of the plan and the output gather, warps of 32 consecutive
+    instances -- touch at most RELAYOUT_GAIN of the 32-byte sectors they touch
+    in the reference layout (sampled over up to RELAYOUT_SAMPLE_WARPS warps per
+    column).  ``all``: every candidate.  A coherent slot (``column 0 + delta``,
+    codegen.py:317-327) reading a moved range keeps working when the remapped
+    addresses are still a constant delta apart (same instance, other root:
+    delta ``dq*N`` becomes ``dq``); groups for which that fails stay put.
+    Returns ``(kernels, {(kernel, slot): new delta})``.
+    """
+    kps = plan.kernels
+    cand = sorted((k for k in candidates if kps[k].n_roots > 1 and kps[k].instances > 1),
+                  key=lambda k: kps[k].dest_base)
+    if not cand:
+        return [], {}
+    cols = []  # reader columns (position slots and the output gather)
+    coherent = []  # (kernel, slot, column 0, column of the slot)
+    for kl in lowered:
+        sc = slot_addresses(plan, kps[kl.index])
+        for s, c in enumerate(sc):
+            cols.append(c)
+            if kl.slot_col[s] < 0 and kl.slot_delta[s] != 0:
+                coherent.append((kl.index, s, sc[0], c))
+    cols.append(np.asarray(plan.outputs, np.int64))
+    chosen = []
+    for k in cand:
+        if mode == "all":
+            chosen.append(k)
+            continue
+        kp = kps[k]
+        old = new = 0
+        for c in cols:
+            if c.size == 0:
+                continue
+            nw = (c.size + 31) // 32
+            if nw > RELAYOUT_SAMPLE_WARPS:  # evenly spaced runs of 64 warps
+                runs = RELAYOUT_SAMPLE_WARPS // 64
+                starts = np.linspace(0, nw - 64, runs).astype(np.int64) * 32
+                c = np.concatenate([c[s: s + 64 * 32] for s in starts])
+            old += _warp_sectors(c, kp.dest_base, kp.instances, kp.n_roots, False)
+            new += _warp_sectors(c, kp.dest_base, kp.instances, kp.n_roots, True)
+        if old and new <= RELAYOUT_GAIN * old:
+            chosen.append(k)
+    while chosen:
+        rp = _RelaidPlan(plan, chosen)
+        deltas, bad = {}, set()
+        for k, s, c0, c in coherent:
+            d = rp.remap(c) - rp.remap(c0)
+            if d.size and np.all(d == d[0]):
+                deltas[(k, s)] = int(d[0])
+                continue
+            for j in chosen:
+                lo, hi = kps[j].dest_base, kps[j].dest_base + kps[j].n_roots * kps[j].instances
+                if np.any((c >= lo) & (c < hi)) or np.any((c0 >= lo) & (c0 < hi)):
+                    bad.add(j)
+        if not bad:
+            return chosen, deltas
+        chosen = [j for j in chosen if j not in bad]
+    return [], {}
+
+
 JIT_MIN_N = 4096  # groups with fewer instances stay on the hand-written kernels (NVRTC time buys nothing)
 JIT_MAX_WAVE_GROUPS = 48  # ...unless they share a wave of at most this many groups with a big one
 
 
 def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = None,
                jit: bool | None = None, csr_window: bool | None = None,
-               jit_min_n: int | None = None) -> DevicePlanArrays:
+               jit_min_n: int | None = None, relayout: str | bool | None = None) -> DevicePlanArrays:
     """ExecutionPlan -> device plan.
 
     ``direct_csr``: output groups store their CSR values through output-position
@@ -813,6 +936,11 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     without a gather pass).  Off by default: on B200 the 8-byte scattered stores
     cost more than the coalesced value-array stores + one u32-indexed gather
     (profiles/r06).
+
+    ``relayout`` (``"auto"`` / ``"all"`` / False): the CSR layout -- big plain
+    multi-root groups whose readers gather across roots store instance-major
+    (``_RelaidPlan``, ``choose_relayout``).  CSR-mode only: the device plan then
+    refuses value-mode evaluation.
     """
     if compress is None:
         compress = os.environ.get("SGB_COMPRESS", "1") != "0"
@@ -829,9 +957,26 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     if csr_window is None:  # CSR windows of the last wave (specialised units only), see _window_members
         csr_window = os.environ.get("SGB_CSR_WINDOW", "0") == "1"
     csr_window = bool(csr_window and jit)
-    read_sets = _read_sets(plan)
-    waves = compute_waves(plan, read_sets)
+    if relayout is None:
+        relayout = False
+    if relayout is True:
+        relayout = "auto"
     lowered = [lower_kernel(plan, kp, k) for k, kp in enumerate(plan.kernels)]
+    read_sets = _read_sets(plan)  # which ranges each kernel reads: invariant under the CSR layout
+    imajor: set = set()
+    if relayout:
+        if direct_csr or csr_window:
+            raise ValueError("the CSR layout does not combine with direct CSR stores or CSR windows")
+        cand = [kl.index for kl in lowered if not kl.flags & (FLAG_SELFREF | FLAG_SERIAL)
+                and plan.kernels[kl.index].instances >= jit_min_n]
+        chosen, deltas = choose_relayout(plan, lowered, cand, relayout)
+        imajor = set(chosen)
+        if imajor:
+            plan = _RelaidPlan(plan, sorted(imajor))
+            for (k, s_), d in deltas.items():
+                lowered[k].slot_delta = lowered[k].slot_delta.copy()
+                lowered[k].slot_delta[s_] = d
+    waves = compute_waves(plan, read_sets)
     for kl, w in zip(lowered, waves):
         kl.wave = w
     n_waves = (max(waves) + 1) if waves else 0
@@ -871,7 +1016,8 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         n, r = kp.instances, len(kp.retained)
         seg = np.asarray(plan.positions[kp.p_base: kp.p_base + r * n], dtype=np.int64)
         cols = list(seg.reshape(r, n) if kp.layout == "coalesced" else seg.reshape(n, r).T)
-        flags = kl.flags | (FLAG_COHERENT if r == 1 and kp.pos_vars else 0)
+        flags = kl.flags | (FLAG_COHERENT if r == 1 and kp.pos_vars else 0) | \
+            (FLAG_IMAJOR if kl.index in imajor else 0)
         in_window = window is not None and kl.index in window
         groups.append(_Group(kl.kind, flags, n, kp.n_roots, kp.dest_base, kp.p_base, kp.c_base,
                              len(kp.const_vars), kl.slot_col, kl.slot_delta, cols, kp.layout, kl.wave,
@@ -1100,6 +1246,7 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         copies=[(g.wave, g.columns[0], g.opos[0]) for g in groups if g.flags & FLAG_CSR_ONLY and g.tape is None],
         exact=exact,
     )
+    dp.csr_layout = sorted(imajor)
     dp.win_pieces = np.asarray(win_pieces, np.int32).reshape(-1, 4)
     dp.win_off = np.asarray(win_off, np.int64)
     dp.window_units = window_units

@@ -153,14 +153,23 @@ def _stream_handle(stream) -> ctypes.c_void_p:
 class DevicePlan:
     """A reference ExecutionPlan lowered and uploaded to one B200."""
 
-    def __init__(self, plan, device: int = 0, lowered=None):
+    def __init__(self, plan, device: int = 0, lowered=None, csr_layout: bool = False):
+        """``csr_layout``: lower with the CSR layout (lower.choose_relayout) -- CSR-mode
+        calls only (run_csr, capture_csr, run_outputs_host, run_batch_csr); the
+        value-mode calls raise SgbError.  ``SGB_RELAYOUT`` = auto (default) / all / 0."""
+        import os
+
         import torch
 
         if not torch.cuda.is_available():
             raise SgbError("no CUDA device: the B200 backend has no CPU fallback")
         self.plan = plan
         self.device = int(device)
-        self.lowered = lowered if lowered is not None else lower_plan(plan)
+        if lowered is None:
+            mode = os.environ.get("SGB_RELAYOUT", "auto") if csr_layout else False
+            lowered = lower_plan(plan, relayout=False if mode in ("0", "") else mode)
+        self.lowered = lowered
+        self.csr_layout = bool(getattr(lowered, "csr_layout", None))
         self.value_array_size = int(plan.value_array_size)
         self.input_count = int(plan.input_count)
         self.n_outputs = len(plan.outputs)

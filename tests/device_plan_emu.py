@@ -73,7 +73,10 @@ class _Store:
     def __call__(self, g, r, i, v):
         csr = self.out is not None
         if not (csr and g["flags"] & L.FLAG_STREAM):
-            self.x[g["dest_base"] + r * int(g["n"]) + i] = v
+            if g["flags"] & L.FLAG_IMAJOR:
+                self.x[g["dest_base"] + np.asarray(i) * int(g["n_roots"]) + r] = v
+            else:
+                self.x[g["dest_base"] + r * int(g["n"]) + i] = v
         if csr:
             o = _out_pos(self.dp, g, r, i)
             m = o >= 0

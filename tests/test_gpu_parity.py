@@ -230,3 +230,41 @@ def test_cuda_graph_replay_equals_run(name):
     graph.replay()
     torch.cuda.synchronize()
     assert np.array_equal(bits(out.cpu().numpy()), bits(want))
+
+
+@pytest.mark.parametrize("relayout", ["all", "auto"])
+def test_csr_layout(golden, relayout):
+    """CSR layout (multi-root groups stored instance-major, lower.choose_relayout): CSR values equal the
+    reference's, on the device path, the captured graph, the host-buffer path and batched; value-mode
+    calls are refused (the value array is permuted)."""
+    import torch
+
+    from paper_2110_12865_b200 import DevicePlan, SgbError, lower_plan
+
+    plan = golden.plan
+    lw = lower_plan(plan, jit_min_n=0, relayout=relayout)
+    dp = DevicePlan(plan, lowered=lw)
+    want = golden.outputs
+    cmp = (lambda g: np.array_equal(bits(g), bits(want))) if golden.exact else (lambda g: _close(g, want))
+    x = dp.new_values(golden.inputs)
+    out = torch.full((len(plan.outputs),), float("nan"), dtype=torch.float64, device=x.device)
+    dp.run_csr(x, out)
+    torch.cuda.synchronize()
+    assert cmp(out.cpu().numpy())
+    assert cmp(dp.run_outputs_host(golden.inputs))
+    if dp.lowered.needs_zero != 2:
+        graph = dp.capture_csr(dp.new_values(golden.inputs), out)
+        out.fill_(float("nan"))
+        graph.replay()
+        torch.cuda.synchronize()
+        assert cmp(out.cpu().numpy())
+    X = torch.zeros((plan.value_array_size, 5), dtype=torch.float64, device="cuda")
+    X[: plan.input_count] = torch.from_numpy(np.repeat(golden.inputs[:, None], 5, axis=1)).cuda()
+    o = dp.run_batch_csr(X).cpu().numpy()
+    for b in range(5):
+        assert cmp(o[:, b])
+    if dp.csr_layout:
+        with pytest.raises(SgbError):
+            dp.run_values(dp.new_values(golden.inputs))
+        with pytest.raises(SgbError):
+            dp.sg_run(np.zeros(plan.value_array_size))
