@@ -869,7 +869,7 @@ void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_
       cudaLaunchKernel(u.jitb, dim3((unsigned)grid), dim3(JIT_BLOCK), args, 0, s);
     } else {
       void *args[] = {&T, &tiles, &n, &x, &out, &c};
-      cudaLaunchKernel(u.jit, dim3((unsigned)u.grid), dim3(JIT_BLOCK), args, 0, s);
+      cudaLaunchKernel(u.jit, dim3((unsigned)u.grid), dim3(JIT_BLOCK), args, (size_t)u.regs, s);
     }
     return;
   }
@@ -1129,6 +1129,8 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       SGB_CUDA(cudaLibraryGetKernel(&kb, p->jit_lib, nbn.c_str()));
       u.jit = (const void *)kf;
       u.jitb = (const void *)kb;
+      if (u.regs > 48 * 1024)  // staging buffer of instance-major groups (jit.py _stage_out)
+        SGB_CUDA(cudaFuncSetAttribute(u.jit, cudaFuncAttributeMaxDynamicSharedMemorySize, u.regs));
     }
     if (u.g0 < 0 || u.g1 > d->n_groups || u.g0 > u.g1 || u.wave < 0 ||
         (csr_only ? u.wave > d->n_waves : u.wave >= d->n_waves) || u.t0 < 0 ||
@@ -1136,7 +1138,8 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
         u.t0 > u.t1 || (u.kind != KIND_TAPE && u.kind != KIND_SOP) ||
         (u.kind == KIND_TAPE && !jit && (u.bs != 32 && u.bs != 64 && u.bs != 128)) ||
         (u.kind == KIND_TAPE && (u.variant != 1 && u.variant != 2 && u.variant != 4)) ||
-        (int64_t)u.regs * (u.kind == KIND_TAPE ? u.bs * u.variant : 0) * 8 > smem_max)
+        (jit ? (int64_t)u.regs : (int64_t)u.regs * (u.kind == KIND_TAPE ? u.bs * u.variant : 0) * 8) > smem_max ||
+        u.regs < 0)
       return fail(-1, "sgb_plan_create: bad launch unit " + std::to_string(k));
     max_wave = u.wave > max_wave ? u.wave : max_wave;
     {  // persistent grid: resident capacity of the chip, at most one block (warp for SOP) per tile
@@ -1146,7 +1149,7 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
         u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
         if (u.grid > u.t1 - u.t0) u.grid = u.t1 - u.t0;
       } else if (jit) {
-        SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, u.jit, JIT_BLOCK, 0));
+        SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, u.jit, JIT_BLOCK, (size_t)u.regs));
         u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
         if (u.grid > u.t1 - u.t0) u.grid = u.t1 - u.t0;
       } else if (u.kind == KIND_TAPE) {

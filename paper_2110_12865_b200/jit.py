@@ -128,14 +128,18 @@ def _out_pos(rec, r: int, i: str = "i") -> str | None:
 
 
 def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: str = "",
-                batched: bool = False, window: bool = False, bv: str = "b") -> tuple[list[str], list[str]]:
+                batched: bool = False, window: bool = False, bv: str = "b",
+                stage: str | None = None) -> tuple[list[str], list[str]]:
     """Straight-line CUDA for instance ``iv`` of packed group ``gi`` (register tape -> SSA).
 
     Returns (load lines, compute + store lines) so several instances' loads can be
     issued before any of them computes.  Variables carry suffix ``sfx``.
     Batched: value set ``b`` of ``X[addr * ld + b]`` (lane = value set).  Window:
     the CSR value goes to the block's shared window ``buf[o - kwin_]`` (no
-    value-array store: window members are never re-read).
+    value-array store: window members are never re-read).  Stage: an
+    instance-major group's results go to the block's staging buffer at
+    ``stage_[(stage) * RP + r]`` (``stage`` = the instance's offset in the tile,
+    RP = lower.stage_stride); the unit writes the tile out coalesced.
     """
     X = (lambda a: f"x + (u64)({a}) * ld + {bv}") if batched else (lambda a: f"x + ({a})")
     rec = dp.groups[gi]
@@ -173,6 +177,9 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
         C = reg.get(c, "0.0")
         if op == L.T_ST and window:
             comp.append(f"if (ok{sfx}) {{ const u32 o = {opos(aux)}; if (o != NONE) buf[o - kwin_] = {reg[a]}; }}")
+            continue
+        if op == L.T_ST and stage is not None:
+            comp.append(f"if (ok{sfx}) stage_[({stage}) * {L.stage_stride(int(rec['n_roots']))} + {aux}] = {reg[a]};")
             continue
         if op == L.T_ST:
             r = aux
@@ -231,7 +238,7 @@ def group_batch_body(dp, gi, tape, imms, vec: int) -> list[str]:
 
 
 def group_vec_body(dp, gi, tape, imms, vec: int, base: str, stride: int, batched=False, window=False,
-                   limit: str | None = None):
+                   limit: str | None = None, stage: bool = False):
     """VEC instances base + v*stride: every instance's loads first, then the computes.
 
     ``limit``: instance v is valid only if ``limit`` (with ``{v}`` = v * stride) holds too.
@@ -243,7 +250,8 @@ def group_vec_body(dp, gi, tape, imms, vec: int, base: str, stride: int, batched
         extra = f" && ({limit.format(v=v * stride)})" if limit else ""
         lines.append(f"const bool ok_{v} = iv{v} < {n}LL{extra};")
         lines.append(f"const i64 ic{v} = ok_{v} ? iv{v} : {n - 1}LL;")
-        ld, cp = group_parts(dp, gi, tape, imms, iv=f"ic{v}", sfx=f"_{v}", batched=batched, window=window)
+        ld, cp = group_parts(dp, gi, tape, imms, iv=f"ic{v}", sfx=f"_{v}", batched=batched, window=window,
+                             stage=f"threadIdx.x + {v * stride}" if stage else None)
         lines += ld
         comps += cp
     return lines + comps
@@ -253,6 +261,20 @@ def _check_stores(tape, n_roots: int, gi: int):
     roots = sorted(int(t[7]) for t in tape.tolist() if t[0] == L.T_ST)
     if roots != list(range(n_roots)):
         raise ValueError(f"group {gi}: tape stores roots {roots}, expected 0..{n_roots - 1}")
+
+
+def _stage_out(rec, vec: int) -> list[str]:
+    """Write a staged tile of an instance-major group: its instances' results are one contiguous
+    run ``dest_base + tile_start * R ...`` of the value array, stored by consecutive threads."""
+    n, R = int(rec["n"]), int(rec["n_roots"])
+    rp = L.stage_stride(R)
+    st = "__stcs(x + base_ + k_, v_)" if rec["flags"] & L.FLAG_STREAM else "x[base_ + k_] = v_"
+    return ["__syncthreads();",
+            f"{{ const i64 cnt_ = min((i64){JIT_BLOCK * vec}, {n}LL - (i64)tl.y) * {R};",
+            f"  const i64 base_ = {int(rec['dest_base'])}LL + (i64)tl.y * {R}LL;",
+            f"  for (i64 k_ = threadIdx.x; k_ < cnt_; k_ += {JIT_BLOCK}) {{",
+            f"    const i64 q_ = k_ / {R}; const double v_ = stage_[q_ * {rp} + (k_ - q_ * {R})]; {st}; }} }}",
+            "__syncthreads();"]
 
 
 def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
@@ -281,6 +303,7 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
             bounds = f"{JIT_BLOCK}, {min_blocks}" if min_blocks > 1 else f"{JIT_BLOCK}"
             head = [f'extern "C" __global__ void __launch_bounds__({bounds}) sgb_tape_u{u}(',
                     "    Tables T, const int2 *tiles, i64 n_tiles, double *x, double *out, int csr) {",
+                    "  extern __shared__ double stage_[];",
                     "  for (i64 t = blockIdx.x; t < n_tiles; t += gridDim.x) {",
                     "    const int2 tl = tiles[t];",
                     "    const i64 i = (i64)tl.y + threadIdx.x;",
@@ -291,13 +314,17 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
         for gi in range(unit["group_begin"], unit["group_end"]):
             rec = dp.groups[gi]
             _check_stores(tapes[gi], int(rec["n_roots"]), gi)
+            staged = not batched and bool(rec["flags"] & L.FLAG_IMAJOR)
             out.append(f"    case {gi}: {{")
-            out.append(f"      if (i >= {int(rec['n'])}LL) break;")
+            if not staged:  # (a staged tile keeps every thread: the block synchronises)
+                out.append(f"      if (i >= {int(rec['n'])}LL) break;")
             if rec["flags"] & L.FLAG_CSR_ONLY:
                 out.append("      if (!csr) break;")
             body = (group_batch_body(dp, gi, tapes[gi], imms[gi], BATCH_VEC) if batched else
-                    group_vec_body(dp, gi, tapes[gi], imms[gi], vec, "i", JIT_BLOCK))
+                    group_vec_body(dp, gi, tapes[gi], imms[gi], vec, "i", JIT_BLOCK, stage=staged))
             out += ["      " + ln for ln in body]
+            if staged:
+                out += ["      " + ln for ln in _stage_out(rec, vec)]
             out.append("    } break;")
         out += ["    default: break;", "    }", "    }", "  }", "}", ""]
     return "\n".join(out)

@@ -34,7 +34,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .plan import EXACT_OPS, OpKind, reachable, slot_addresses
+from .plan import EXACT_OPS, OpKind, reachable, slot_addresses, unique_addresses
 
 # device op codes (csrc/sgb_device.cuh keeps the same numbering)
 T_ADD, T_SUB, T_MUL, T_DIV, T_NEG, T_SQRT = 2, 3, 4, 5, 6, 7
@@ -146,7 +146,7 @@ def _read_sets(plan):
         cols = slot_addresses(plan, kp)
         if cols:
             a = np.concatenate(cols)
-            a = np.unique(a[a >= plan.input_count])
+            a = unique_addresses(a[a >= plan.input_count])
         else:
             a = np.zeros(0, np.int64)
         out.append(a)
@@ -812,7 +812,7 @@ class _RelaidPlan:
     permuted, which is why a relaid device plan refuses value-mode calls.
     """
 
-    def __init__(self, plan, groups: list[int]):
+    def __init__(self, plan, groups: list[int], tables: bool = True):
         self._plan = plan
         kps = [plan.kernels[k] for k in groups]
         order = np.argsort([kp.dest_base for kp in kps])
@@ -820,8 +820,9 @@ class _RelaidPlan:
         self.nn = np.array([kps[j].instances for j in order], np.int64)
         self.rr = np.array([kps[j].n_roots for j in order], np.int64)
         self.hi = self.lo + self.nn * self.rr
-        self.positions = self.remap(np.asarray(plan.positions)).astype(np.uint32)
-        self.outputs = self.remap(np.asarray(plan.outputs, np.int64)).astype(np.int64)
+        if tables:
+            self.positions = self.remap(np.asarray(plan.positions)).astype(np.uint32)
+            self.outputs = self.remap(np.asarray(plan.outputs, np.int64)).astype(np.int64)
 
     def __getattr__(self, name):
         return getattr(self._plan, name)
@@ -905,7 +906,7 @@ def choose_relayout(plan, lowered, candidates: list[int], mode: str = "auto"):
         if old and new <= RELAYOUT_GAIN * old:
             chosen.append(k)
     while chosen:
-        rp = _RelaidPlan(plan, chosen)
+        rp = _RelaidPlan(plan, chosen, tables=False)
         deltas, bad = {}, set()
         for k, s, c0, c in coherent:
             d = rp.remap(c) - rp.remap(c0)
@@ -920,6 +921,21 @@ def choose_relayout(plan, lowered, candidates: list[int], mode: str = "auto"):
             return chosen, deltas
         chosen = [j for j in chosen if j not in bad]
     return [], {}
+
+
+STAGE_LIMIT = 200 * 1024  # shared memory a specialised unit may stage instance-major results in
+MAX_IMAJOR_ROOTS = 96  # ... so relaid groups have at most this many roots (JIT_BLOCK * 97 * 8 B fits)
+
+
+def stage_stride(n_roots: int) -> int:
+    """Doubles per instance in the staging buffer (odd: conflict-free 8-byte shared-memory rows)."""
+    return n_roots | 1
+
+
+def stage_bytes(groups, sel, vec: int) -> int:
+    """Dynamic shared memory of a specialised unit: one staged tile of its largest relaid group."""
+    rp = [stage_stride(groups[j].n_roots) for j in sel if groups[j].flags & FLAG_IMAJOR]
+    return JIT_BLOCK * vec * max(rp) * 8 if rp else 0
 
 
 JIT_MIN_N = 4096  # groups with fewer instances stay on the hand-written kernels (NVRTC time buys nothing)
@@ -968,7 +984,8 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         if direct_csr or csr_window:
             raise ValueError("the CSR layout does not combine with direct CSR stores or CSR windows")
         cand = [kl.index for kl in lowered if not kl.flags & (FLAG_SELFREF | FLAG_SERIAL)
-                and plan.kernels[kl.index].instances >= jit_min_n]
+                and plan.kernels[kl.index].instances >= jit_min_n
+                and plan.kernels[kl.index].n_roots <= MAX_IMAJOR_ROOTS]
         chosen, deltas = choose_relayout(plan, lowered, cand, relayout)
         imajor = set(chosen)
         if imajor:
@@ -1004,7 +1021,7 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     copy_sets = [(min(last, n_waves), avail <= last), (n_waves, avail > last)]
     # stream flags: results no later kernel (or copy group) reads
     reads = [r for r in read_sets if r.size] + ([res_addr] if res_addr.size else [])
-    allr = np.unique(np.concatenate(reads)) if reads else np.zeros(0, np.int64)
+    allr = unique_addresses(np.concatenate(reads)) if reads else np.zeros(0, np.int64)
     groups: list[_Group] = []
     win_groups: list[_Group] = []  # window members (CSR-only records; value-mode twins stay in `groups`)
     for kl in lowered:
@@ -1077,8 +1094,10 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                              ([j for j in sj if groups[j].window_value], UNIT_VALUE_ONLY),
                              ([j for j in sj if groups[j].window], UNIT_WINDOW)):
                 if sel:
-                    plan_units.append((KIND_TAPE, jit_vec(groups, sel) if tag != UNIT_WINDOW else 1,
-                                       JIT_BLOCK, tag, sel))
+                    vec = jit_vec(groups, sel) if tag != UNIT_WINDOW else 1
+                    while vec > 1 and stage_bytes(groups, sel, vec) > STAGE_LIMIT:
+                        vec //= 2
+                    plan_units.append((KIND_TAPE, vec, JIT_BLOCK, tag, sel))
             members = [j for j in members if j not in set(sj)]
         for plain in (True, False):
             tm = [j for j in members if groups[j].kind == KIND_TAPE and
@@ -1104,10 +1123,12 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         for code in sorted(codes):  # one persistent launch per kernel body
             plan_units.append((KIND_SOP, code, SOP_BLOCK, 0, codes[code]))
         for kind, variant, bs, regs, ms in plan_units:
-            utag = 0
+            utag, jit_unit = 0, False
             if kind == KIND_TAPE and bs == JIT_BLOCK and regs in (0, UNIT_VALUE_ONLY, UNIT_WINDOW) \
                     and all(not groups[j].flags & (FLAG_SELFREF | FLAG_SERIAL) for j in ms) and jit:
-                utag, regs = regs, 0
+                utag, regs, jit_unit = regs, 0, True
+                if utag == 0:  # specialised unit: regs carries the staging bytes of its relaid groups
+                    regs = stage_bytes(groups, ms, variant)
             g_begin = len(order_groups)
             unit_tiles, unit_keys = [], []
             for j in ms:
@@ -1199,7 +1220,12 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
             if np.any(keys >= 0) and order_mode == "csr":
                 # CSR-ordered schedule: partial sectors of the output merge in L2
                 t = t[np.argsort(keys, kind="stable")]
-            elif kind == KIND_TAPE and regs == 0 and order_mode != "group":
+            elif jit_unit and order_mode == "frac":
+                # specialised units: interleave the groups' tiles by the fraction of the group
+                # they reach, so groups of different sizes sweep their (mesh-ordered) instances in step
+                nn = np.array([groups[order_groups[g]].n for g in t[:, 0]], np.float64) if len(t) else t[:, 1]
+                t = t[np.argsort(t[:, 1] / np.maximum(nn, 1), kind="stable")]
+            elif jit_unit and order_mode != "group":
                 # specialised units: interleave the groups' tiles by instance, so groups that
                 # gather the same producer ranges (structured mesh groups) read them while they
                 # are still in L2
@@ -1207,7 +1233,7 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
             t0 = sum(len(x) for x in tiles_all)
             tiles_all.append(t)
             uflags = UNIT_CSR_ONLY if w >= n_waves else 0
-            if kind == KIND_TAPE and regs == 0:
+            if jit_unit:
                 uflags |= UNIT_JIT
                 jit_units.append(len(units))
             if utag == UNIT_VALUE_ONLY:

@@ -25,7 +25,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .plan import slot_addresses
+from .plan import slot_addresses, unique_addresses
 
 
 @dataclass
@@ -58,12 +58,12 @@ def wave_traffic(plan, lowered, batch: int = 1) -> list[LaunchTraffic]:
             wr += 8 * kp.n_roots * kp.instances * batch
             ops += kl.ops * kp.instances * batch
             if kp.pos_vars:
-                addrs.append(np.unique(np.concatenate(slot_addresses(plan, kp))))
-        reads = int(np.unique(np.concatenate(addrs)).size) if addrs else 0
+                addrs.append(unique_addresses(np.concatenate(slot_addresses(plan, kp))))
+        reads = int(unique_addresses(np.concatenate(addrs)).size) if addrs else 0
         out.append(LaunchTraffic(f"wave{w}", idx, con, 8 * reads * batch, wr, ops))
     outs = np.asarray(plan.outputs, dtype=np.int64)
     n_out = int(outs.size)
-    out.append(LaunchTraffic("gather_outputs", 4 * n_out, 0, 8 * int(np.unique(outs).size) * batch,
+    out.append(LaunchTraffic("gather_outputs", 4 * n_out, 0, 8 * int(unique_addresses(outs).size) * batch,
                              8 * n_out * batch, 0))
     return out
 
@@ -78,7 +78,7 @@ def csr_wave_traffic(plan, lowered, batch: int = 1) -> list[LaunchTraffic]:
     encoding overhead of this backend, not algorithmic bytes.
     """
     outs = np.asarray(plan.outputs, dtype=np.int64)
-    uniq = np.unique(outs)
+    uniq = unique_addresses(outs)
     waves = max([lowered.n_waves] + [w + 1 for w, _, _ in lowered.copies])
     out = []
     for w in range(waves):
@@ -98,13 +98,13 @@ def csr_wave_traffic(plan, lowered, batch: int = 1) -> list[LaunchTraffic]:
             else:
                 wr += 8 * kp.n_roots * kp.instances * batch
             if kp.pos_vars:
-                addrs.append(np.unique(np.concatenate(slot_addresses(plan, kp))))
+                addrs.append(unique_addresses(np.concatenate(slot_addresses(plan, kp))))
         for cw, src, _ in lowered.copies:
             if cw == w:
                 idx += 4 * src.size
                 wr += 8 * src.size * batch
-                addrs.append(np.unique(src))
-        reads = int(np.unique(np.concatenate(addrs)).size) if addrs else 0
+                addrs.append(unique_addresses(src))
+        reads = int(unique_addresses(np.concatenate(addrs)).size) if addrs else 0
         out.append(LaunchTraffic(f"csr_wave{w}", idx, con, 8 * reads * batch, wr, ops))
     return out
 
@@ -118,7 +118,7 @@ def plan_balg(plan) -> int:
     for kp in plan.kernels:
         for col in slot_addresses(plan, kp):
             reread.append(col[col >= plan.input_count])
-    n_reread = int(np.unique(np.concatenate(reread)).size) if reread else 0
+    n_reread = int(unique_addresses(np.concatenate(reread)).size) if reread else 0
     outs = np.asarray(plan.outputs, dtype=np.int64)
-    dup = int(outs.size - np.unique(outs).size)
+    dup = int(outs.size - unique_addresses(outs).size)
     return 4 * P + 8 * C + 8 * (int(plan.input_count) + n_res + n_reread + dup)

@@ -401,3 +401,16 @@ def validate_plan(plan, src="plan") -> None:
             raise ValueError(f"{src}: {kp.name} slot 0 must be retained")
         if kp.layout not in ("coalesced", "interleaved"):
             raise ValueError(f"{src}: {kp.name} unknown layout {kp.layout!r}")
+
+
+def unique_addresses(a) -> np.ndarray:
+    """Sorted unique non-negative addresses (np.unique through a bitmap: O(n), no hash or sort)."""
+    a = np.asarray(a)
+    if a.size == 0:
+        return np.zeros(0, np.int64)
+    hi = int(a.max()) + 1
+    if hi > 64 * a.size + (1 << 20):  # sparse: the bitmap would cost more than a sort
+        return np.unique(a.astype(np.int64))
+    mark = np.zeros(hi, dtype=bool)
+    mark[a] = True
+    return np.flatnonzero(mark).astype(np.int64)

@@ -18,6 +18,7 @@ ap.add_argument("--mode", choices=("csr", "val"), default="csr")
 ap.add_argument("--config", choices=("c2", "c3", "c4"), default="c2")
 ap.add_argument("--m", type=int, default=55)
 ap.add_argument("--w4", type=int, default=708)
+ap.add_argument("--layout", choices=("csr", "reference"), default="csr")
 args = ap.parse_args()
 
 import torch  # noqa: E402
@@ -29,7 +30,7 @@ t0 = time.time()
 key, plan, _, _ = bench.build_workload(args, 0, 1)
 print(f"plan {key} ready in {time.time() - t0:.1f}s: {len(plan.kernels)} kernels, {len(plan.outputs)} outputs",
       flush=True)
-dp = DevicePlan(plan)
+dp = DevicePlan(plan, csr_layout=args.layout == "csr" and args.mode == "csr")
 print("waves", dp.launches, "units", dp.units, "csr units", dp.csr_units, flush=True)
 if args.batch:
     X = torch.zeros((plan.value_array_size, args.batch), dtype=torch.float64, device="cuda")
