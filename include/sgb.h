@@ -147,6 +147,15 @@ int sgb_sg_run(sgb_plan *plan, double *x_host, const double *c_host, const unsig
  * only those bytes cross PCIe.  Synchronous. */
 int sgb_run_outputs_host(sgb_plan *plan, const double *inputs_host, double *outputs_host);
 
+/* n_sets independent value sets through host buffers, pipelined: set k's
+ * inputs (inputs_host + k * in_stride, in_stride >= 0, 0 = the same inputs
+ * every set) copy in while set k-1 evaluates and set k-2's CSR values
+ * (outputs_host + k * out_stride) copy out.  Equals n_sets calls of
+ * sgb_run_outputs_host (emit.py:237-241 per set); use pinned host memory for
+ * the copies to overlap.  Synchronous. */
+int sgb_run_outputs_host_many(sgb_plan *plan, int64_t n_sets, const double *inputs_host, int64_t in_stride,
+                              double *outputs_host, int64_t out_stride);
+
 /* Batched evaluation: X_dev[addr * ld + b] for b < batch (ld >= batch),
  * inputs placed, results written in place.  Independent value sets share one
  * pass over the index tables. */

@@ -800,6 +800,9 @@ struct sgb_plan {
   std::mutex ws_mu;
   double *d_x = nullptr, *d_out = nullptr;
   cudaStream_t ws_stream = nullptr;
+  // second workspace + copy streams of the pipelined host-buffer stream (sgb_run_outputs_host_many)
+  double *d_x2 = nullptr, *d_out2 = nullptr;
+  cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
   // fork / join of the independent launch units of one wave
   std::vector<cudaStream_t> aux;
   std::vector<cudaEvent_t> ev_join;
@@ -953,10 +956,12 @@ void sgb_plan_destroy(sgb_plan *p) {
   void *bufs[] = {p->d_groups, p->d_tiles, p->d_btiles, p->d_outputs, p->d_tape, p->d_imm, p->d_con,
                   p->d_sop, p->d_scol, p->d_sdel, p->d_pos, p->d_x, p->d_out, p->d_cbase, p->d_coff,
                   p->d_obase, p->d_ooff, p->d_opos32, p->d_sopd, p->d_fbase, p->d_outputs32,
-                  p->d_wpieces, p->d_woff};
+                  p->d_wpieces, p->d_woff, p->d_x2, p->d_out2};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (p->ws_stream) cudaStreamDestroy(p->ws_stream);
+  if (p->h2d_stream) cudaStreamDestroy(p->h2d_stream);
+  if (p->d2h_stream) cudaStreamDestroy(p->d2h_stream);
   if (p->jit_lib) cudaLibraryUnload(p->jit_lib);
   for (cudaStream_t a : p->aux) cudaStreamDestroy(a);
   for (cudaEvent_t e : p->ev_join) cudaEventDestroy(e);
@@ -1462,6 +1467,7 @@ static int ensure_ws(sgb_plan *p) {
     SGB_CUDA(cudaMalloc((void **)&p->d_x, sizeof(double) * (size_t)p->vas));
     // never-written slots (padding, reads before writes) read as zero (codegen.py:419)
     SGB_CUDA(cudaMemset(p->d_x, 0, sizeof(double) * (size_t)p->vas));
+    SGB_CUDA(cudaDeviceSynchronize());  // the non-blocking ws_stream does not order after the legacy stream
   }
   if (!p->d_out && p->n_out) SGB_CUDA(cudaMalloc((void **)&p->d_out, sizeof(double) * (size_t)p->n_out));
   return 0;
@@ -1501,6 +1507,67 @@ int sgb_run_outputs_host(sgb_plan *p, const double *inputs, double *outputs) {
   SGB_CUDA(cudaMemcpyAsync(outputs, p->d_out, sizeof(double) * (size_t)p->n_out, cudaMemcpyDeviceToHost, p->ws_stream));
   SGB_CUDA(cudaStreamSynchronize(p->ws_stream));
   return 0;
+}
+
+
+// A stream of value sets through host buffers: set k's inputs go in on the H2D stream while set
+// k-1 evaluates and set k-2's CSR values come back on the D2H stream (two device workspaces,
+// PCIe is full duplex).  Same results as n_sets calls of sgb_run_outputs_host.
+int sgb_run_outputs_host_many(sgb_plan *p, int64_t n_sets, const double *inputs, int64_t in_stride,
+                              double *outputs, int64_t out_stride) {
+  if (!p) return fail(-1, "sgb_run_outputs_host_many: null plan");
+  if (n_sets < 0 || in_stride < 0 || (n_sets > 1 && out_stride < p->n_out))
+    return fail(-1, "sgb_run_outputs_host_many: bad set count or stride");
+  if (n_sets == 0 || !p->n_out) return 0;
+  if ((!inputs && p->n_in) || !outputs) return fail(-1, "sgb_run_outputs_host_many: null buffer");
+  std::lock_guard<std::mutex> lk(p->ws_mu);
+  int rc = ensure_ws(p);
+  if (rc) return rc;
+  if (!p->h2d_stream) SGB_CUDA(cudaStreamCreateWithFlags(&p->h2d_stream, cudaStreamNonBlocking));
+  if (!p->d2h_stream) SGB_CUDA(cudaStreamCreateWithFlags(&p->d2h_stream, cudaStreamNonBlocking));
+  if (n_sets > 1 && !p->d_x2 && p->vas) {
+    SGB_CUDA(cudaMalloc((void **)&p->d_x2, sizeof(double) * (size_t)p->vas));
+    // zeroed on the evaluation stream, so ordered before set 1 evaluates (codegen.py:419)
+    SGB_CUDA(cudaMemsetAsync(p->d_x2, 0, sizeof(double) * (size_t)p->vas, p->ws_stream));
+  }
+  if (n_sets > 1 && !p->d_out2) SGB_CUDA(cudaMalloc((void **)&p->d_out2, sizeof(double) * (size_t)p->n_out));
+  double *xs[2] = {p->d_x, p->d_x2}, *os[2] = {p->d_out, p->d_out2};
+  cudaEvent_t ev_in[2], ev_run[2], ev_outd[2];
+  for (int j = 0; j < 2; ++j) {
+    SGB_CUDA(cudaEventCreateWithFlags(&ev_in[j], cudaEventDisableTiming));
+    SGB_CUDA(cudaEventCreateWithFlags(&ev_run[j], cudaEventDisableTiming));
+    SGB_CUDA(cudaEventCreateWithFlags(&ev_outd[j], cudaEventDisableTiming));
+  }
+  for (int64_t k = 0; k < n_sets && !rc; ++k) {
+    const int j = (int)(k & 1);
+    double *x = xs[j], *o = os[j];
+    if (k >= 2) SGB_CUDA(cudaStreamWaitEvent(p->h2d_stream, ev_run[j], 0));  // set k-2 done reading x
+    if (p->n_in)
+      SGB_CUDA(cudaMemcpyAsync(x, inputs + k * in_stride, sizeof(double) * (size_t)p->n_in, cudaMemcpyHostToDevice,
+                               p->h2d_stream));
+    SGB_CUDA(cudaEventRecord(ev_in[j], p->h2d_stream));
+    SGB_CUDA(cudaStreamWaitEvent(p->ws_stream, ev_in[j], 0));
+    if (k >= 2) SGB_CUDA(cudaStreamWaitEvent(p->ws_stream, ev_outd[j], 0));  // set k-2's values are out
+    const bool dirty = j == 0 && p->ws_dirty;
+    if ((p->needs_zero == 2 || (p->needs_zero == 1 && dirty)) && p->vas > p->n_in)
+      SGB_CUDA(cudaMemsetAsync(x + p->n_in, 0, sizeof(double) * (size_t)(p->vas - p->n_in), p->ws_stream));
+    if (j == 0) p->ws_dirty = false;
+    rc = sgb_run_csr(p, x, o, p->ws_stream);
+    SGB_CUDA(cudaEventRecord(ev_run[j], p->ws_stream));
+    SGB_CUDA(cudaStreamWaitEvent(p->d2h_stream, ev_run[j], 0));
+    SGB_CUDA(cudaMemcpyAsync(outputs + k * out_stride, o, sizeof(double) * (size_t)p->n_out, cudaMemcpyDeviceToHost,
+                             p->d2h_stream));
+    SGB_CUDA(cudaEventRecord(ev_outd[j], p->d2h_stream));
+  }
+  SGB_CUDA(cudaStreamSynchronize(p->h2d_stream));
+  SGB_CUDA(cudaStreamSynchronize(p->ws_stream));
+  SGB_CUDA(cudaStreamSynchronize(p->d2h_stream));
+  for (int j = 0; j < 2; ++j) {
+    cudaEventDestroy(ev_in[j]);
+    cudaEventDestroy(ev_run[j]);
+    cudaEventDestroy(ev_outd[j]);
+  }
+  return rc;
 }
 
 }  // extern "C"

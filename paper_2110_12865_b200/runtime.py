@@ -88,7 +88,7 @@ class _Desc(ctypes.Structure):
 
 SYMBOLS = (
     "sgb_plan_create", "sgb_plan_destroy", "sgb_run_values", "sgb_run_csr", "sgb_gather_outputs",
-    "sgb_sg_run", "sgb_run_outputs_host", "sgb_run_batch", "sgb_run_batch_csr", "sgb_gather_outputs_batch",
+    "sgb_sg_run", "sgb_run_outputs_host", "sgb_run_outputs_host_many", "sgb_run_batch", "sgb_run_batch_csr", "sgb_gather_outputs_batch",
     "sgb_plan_waves", "sgb_last_error", "sgb_run_wave", "sgb_plan_units",
 )
 
@@ -114,6 +114,7 @@ def load_library(path: Path | str | None = None):
             "sgb_gather_outputs": (i32, [vp, vp, vp, vp]),
             "sgb_sg_run": (i32, [vp, vp, vp, vp]),
             "sgb_run_outputs_host": (i32, [vp, vp, vp]),
+            "sgb_run_outputs_host_many": (i32, [vp, i64, vp, i64, vp, i64]),
             "sgb_run_batch": (i32, [vp, vp, i64, i64, vp]),
             "sgb_run_batch_csr": (i32, [vp, vp, i64, i64, vp, i64, vp]),
             "sgb_gather_outputs_batch": (i32, [vp, vp, i64, i64, vp, i64, vp]),
@@ -375,6 +376,33 @@ class DevicePlan:
             out = np.empty(self.n_outputs, np.float64)
         _check(self._lib.sgb_run_outputs_host(self._handle, _ptr(inputs), _ptr(out)),
                "sgb_run_outputs_host")
+        return out
+
+    def run_outputs_host_many(self, inputs: np.ndarray, out: np.ndarray | None = None) -> np.ndarray:
+        """A stream of value sets, host buffers in and out: ``inputs`` is (n_sets, input_count)
+        (or (input_count,) for the same inputs every set), ``out`` (n_sets, n_outputs).  Copies
+        in, evaluation and copies out of consecutive sets overlap (sgb_run_outputs_host_many);
+        pass pinned arrays for the overlap."""
+        if inputs.dtype != np.float64 or not inputs.flags.c_contiguous:
+            inputs = np.ascontiguousarray(inputs, dtype=np.float64)
+        if inputs.ndim == 1:
+            if inputs.shape != (self.input_count,):
+                raise ValueError(f"plan expects {self.input_count} input values, got {inputs.size}")
+            if out is None:
+                raise ValueError("out (n_sets, n_outputs) is required when one input set is repeated")
+            in_stride = 0
+        elif inputs.ndim == 2 and inputs.shape[1] == self.input_count:
+            in_stride = self.input_count
+        else:
+            raise ValueError(f"inputs must be (n_sets, {self.input_count}), got {inputs.shape}")
+        n_sets = out.shape[0] if out is not None else inputs.shape[0]
+        if out is None:
+            out = np.empty((n_sets, self.n_outputs), np.float64)
+        if (out.dtype != np.float64 or not out.flags.c_contiguous or out.shape != (n_sets, self.n_outputs)
+                or (in_stride and inputs.shape[0] != n_sets)):
+            raise ValueError("out must be a contiguous float64 (n_sets, n_outputs) array matching inputs")
+        _check(self._lib.sgb_run_outputs_host_many(self._handle, n_sets, _ptr(inputs), in_stride, _ptr(out),
+                                                   self.n_outputs), "sgb_run_outputs_host_many")
         return out
 
 

@@ -252,6 +252,9 @@ def test_csr_layout(golden, relayout):
     torch.cuda.synchronize()
     assert cmp(out.cpu().numpy())
     assert cmp(dp.run_outputs_host(golden.inputs))
+    many = dp.run_outputs_host_many(np.stack([golden.inputs] * 3))
+    for k in range(3):
+        assert cmp(many[k])
     if dp.lowered.needs_zero != 2:
         graph = dp.capture_csr(dp.new_values(golden.inputs), out)
         out.fill_(float("nan"))
@@ -268,3 +271,28 @@ def test_csr_layout(golden, relayout):
             dp.run_values(dp.new_values(golden.inputs))
         with pytest.raises(SgbError):
             dp.sg_run(np.zeros(plan.value_array_size))
+
+
+def test_outputs_host_many(golden):
+    """The pipelined host-buffer stream (sgb_run_outputs_host_many): every set equals the reference's
+    values, distinct value sets stay distinct (set k's inputs scaled), one repeated input set works."""
+    from paper_2110_12865_b200 import DevicePlan
+
+    plan = golden.plan
+    dp = DevicePlan(plan)
+    want = golden.outputs
+    cmp = (lambda g: np.array_equal(bits(g), bits(want))) if golden.exact else (lambda g: _close(g, want))
+    n = 5
+    ins = np.stack([golden.inputs] * n)
+    ins[1] *= 1.5
+    ins[3] *= 0.75
+    got = dp.run_outputs_host_many(ins)
+    for k in (0, 2, 4):
+        assert cmp(got[k])
+    for k in (1, 3):
+        ref = dp.run_outputs_host(ins[k])
+        assert np.array_equal(bits(got[k]), bits(ref))
+    rep = dp.run_outputs_host_many(golden.inputs, np.empty((4, len(plan.outputs))))
+    for k in range(4):
+        assert cmp(rep[k])
+    assert cmp(dp.run_outputs_host(golden.inputs))  # the single-set path after the stream
