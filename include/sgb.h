@@ -135,6 +135,12 @@ int sgb_run_csr(sgb_plan *plan, double *x_dev, double *out_dev, void *stream);
  * per-launch timing and profiling. */
 int sgb_run_wave(sgb_plan *plan, double *x_dev, double *out_dev, int wave, void *stream);
 
+/* Swap in another schedule of the same tiles (int32 pairs group, first
+ * instance; n_tiles equal to the plan's, every unit's range a permutation of
+ * its own tiles).  Results are unchanged; used by the runtime's per-wave
+ * schedule autotuning.  Synchronous. */
+int sgb_plan_set_tiles(sgb_plan *plan, const int32_t *tiles, int64_t n_tiles);
+
 /* out_dev[k] = x_dev[outputs[k]]  (codegen.py:445). */
 int sgb_gather_outputs(sgb_plan *plan, const double *x_dev, double *out_dev, void *stream);
 

@@ -780,6 +780,7 @@ struct sgb_plan {
   Tables T{};
   sgb_group *d_groups = nullptr;
   int2 *d_tiles = nullptr, *d_btiles = nullptr;
+  int64_t n_tiles = 0;
   int64_t *d_outputs = nullptr;
   uint32_t *d_outputs32 = nullptr;
   bool direct_csr = false;  // some group stores its outputs at their CSR positions (FLAG_OPOS*)
@@ -1294,7 +1295,7 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
   }
   int rc = 0;
   if ((rc = upload(&p->d_groups, d->groups, d->n_groups)) ||
-      (rc = upload(&p->d_tiles, reinterpret_cast<const int2 *>(d->tiles), d->n_tiles)) ||
+      (p->n_tiles = d->n_tiles, rc = upload(&p->d_tiles, reinterpret_cast<const int2 *>(d->tiles), d->n_tiles)) ||
       (rc = upload(&p->d_btiles, btiles.data(), (int64_t)btiles.size())) ||
       (rc = upload(&p->d_outputs, d->outputs, d->n_outputs)) ||
       (rc = upload(&p->d_tape, d->tape, d->tape_rows * 4)) || (rc = upload(&p->d_imm, d->imm, d->n_imm)) ||
@@ -1568,6 +1569,20 @@ int sgb_run_outputs_host_many(sgb_plan *p, int64_t n_sets, const double *inputs,
     cudaEventDestroy(ev_outd[j]);
   }
   return rc;
+}
+
+
+// Replace the (single-set) tile table: same length, each unit's range [t0, t1) a permutation of
+// its own tiles (a different schedule of the same work).  Stream-ordered after prior work on the
+// legacy stream; synchronous.
+int sgb_plan_set_tiles(sgb_plan *p, const int32_t *tiles, int64_t n_tiles) {
+  if (!p || (!tiles && n_tiles)) return fail(-1, "sgb_plan_set_tiles: null argument");
+  if (n_tiles != p->n_tiles) return fail(-1, "sgb_plan_set_tiles: tile count differs from the plan's");
+  std::lock_guard<std::mutex> lk(p->run_mu);
+  SGB_CUDA(cudaSetDevice(p->device));
+  SGB_CUDA(cudaDeviceSynchronize());
+  if (n_tiles) SGB_CUDA(cudaMemcpy(p->d_tiles, tiles, sizeof(int2) * (size_t)n_tiles, cudaMemcpyHostToDevice));
+  return 0;
 }
 
 }  // extern "C"

@@ -127,6 +127,9 @@ class DevicePlanArrays:
     win_off: np.ndarray = None  # int64 [n_windows + 1]: first piece of each window
     window_units: list = field(default_factory=list)
     csr_layout: list = field(default_factory=list)  # plan kernels stored instance-major (FLAG_IMAJOR)
+    # the same tiles with every multi-group specialised unit in fraction-interleaved order (None when
+    # no unit has a second candidate); DevicePlan times both schedules per wave (runtime.autotune)
+    tiles_alt: np.ndarray = None
 
     def unit(self, u: int) -> dict:
         return dict(zip(UNIT_FIELDS, (int(v) for v in self.units[u])))
@@ -1071,7 +1074,7 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     # -- launch units and tiles ---------------------------------------------------------
     packed = np.zeros(len(groups), GROUP_DTYPE)
     order_groups: list[int] = []
-    units, tiles_all = [], []
+    units, tiles_all, tiles_alt, any_alt = [], [], [], False
     tapes, imms, sops, scol, sdel, cbases, coffs, obases, ooffs, op32 = ([] for _ in range(10))
     n_tape = n_imm = n_sop = n_slot = n_cb = n_co = n_ob = n_oo = n_o32 = 0
     jit_tapes, jit_imms, jit_units = {}, {}, []
@@ -1216,8 +1219,13 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
             else:
                 t = np.concatenate(unit_tiles) if unit_tiles else np.zeros((0, 2), np.int64)
                 keys = np.concatenate(unit_keys) if unit_keys else np.zeros(0, np.int64)
-            order_mode = os.environ.get("SGB_TILE_ORDER", "csr")
-            if np.any(keys >= 0) and order_mode == "csr":
+            order_mode = os.environ.get("SGB_TILE_ORDER", "auto")
+            t_alt = None
+            if jit_unit and order_mode == "auto" and not np.any(keys >= 0) and len(np.unique(t[:, 0])) > 1:
+                # two candidate schedules; DevicePlan times both per wave and keeps the faster
+                nn = np.array([groups[order_groups[g]].n for g in t[:, 0]], np.float64)
+                t_alt = t[np.argsort(t[:, 1] / np.maximum(nn, 1), kind="stable")]
+            if np.any(keys >= 0) and order_mode in ("csr", "auto"):
                 # CSR-ordered schedule: partial sectors of the output merge in L2
                 t = t[np.argsort(keys, kind="stable")]
             elif jit_unit and order_mode == "frac":
@@ -1232,6 +1240,8 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                 t = t[np.argsort(t[:, 1], kind="stable")]
             t0 = sum(len(x) for x in tiles_all)
             tiles_all.append(t)
+            tiles_alt.append(t if t_alt is None else t_alt)
+            any_alt = any_alt or t_alt is not None
             uflags = UNIT_CSR_ONLY if w >= n_waves else 0
             if jit_unit:
                 uflags |= UNIT_JIT
@@ -1251,6 +1261,7 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         groups=packed,
         units=np.asarray(units, np.int64).reshape(-1, len(UNIT_FIELDS)),
         tiles=cat(tiles_all, np.int32).reshape(-1, 2),
+        tiles_alt=cat(tiles_alt, np.int32).reshape(-1, 2) if any_alt else None,
         n_waves=n_waves,
         tape=cat(tapes, np.uint32).reshape(-1, 4),
         imm=np.asarray(imms, np.float64),

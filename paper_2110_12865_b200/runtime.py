@@ -89,7 +89,7 @@ class _Desc(ctypes.Structure):
 SYMBOLS = (
     "sgb_plan_create", "sgb_plan_destroy", "sgb_run_values", "sgb_run_csr", "sgb_gather_outputs",
     "sgb_sg_run", "sgb_run_outputs_host", "sgb_run_outputs_host_many", "sgb_run_batch", "sgb_run_batch_csr", "sgb_gather_outputs_batch",
-    "sgb_plan_waves", "sgb_last_error", "sgb_run_wave", "sgb_plan_units",
+    "sgb_plan_waves", "sgb_last_error", "sgb_run_wave", "sgb_plan_units", "sgb_plan_set_tiles",
 )
 
 
@@ -120,6 +120,7 @@ def load_library(path: Path | str | None = None):
             "sgb_gather_outputs_batch": (i32, [vp, vp, i64, i64, vp, i64, vp]),
             "sgb_plan_waves": (i32, [vp, i32]),
             "sgb_plan_units": (i32, [vp, i32]),
+            "sgb_plan_set_tiles": (i32, [vp, vp, i64]),
             "sgb_last_error": (ctypes.c_char_p, []),
         }
         for name, (res, args) in sig.items():
@@ -224,6 +225,69 @@ class DevicePlan:
         self.csr_launches = int(self._lib.sgb_plan_waves(self._handle, 1))  # CSR-mode waves
         self.units = int(self._lib.sgb_plan_units(self._handle, 0))  # kernel launches per evaluation
         self.csr_units = int(self._lib.sgb_plan_units(self._handle, 1))
+        self.tile_order = {}  # wave -> schedule kept by autotune ("inst" / "frac")
+        if getattr(lw, "tiles_alt", None) is not None and os.environ.get("SGB_AUTOTUNE", "1") != "0":
+            self.autotune()
+
+    def set_tiles(self, tiles: np.ndarray):
+        """Swap in another schedule of the plan's tiles (sgb_plan_set_tiles)."""
+        t = np.ascontiguousarray(tiles, np.int32).reshape(-1, 2)
+        _check(self._lib.sgb_plan_set_tiles(self._handle, _ptr(t), t.shape[0]), "sgb_plan_set_tiles")
+
+    def autotune(self, reps: int = 5, gain: float = 0.98):
+        """Per wave, keep the faster of the two tile schedules lower_plan offers for its multi-group
+        specialised units: instances interleaved by index (``tiles``) or by the fraction of their
+        group (``tiles_alt``).  Each wave is timed alone with CUDA events in CSR mode, both
+        schedules twice, min over ``reps`` launches; results never depend on the schedule."""
+        import torch
+
+        from .lower import UNIT_JIT
+
+        lw = self.lowered
+        base = np.ascontiguousarray(lw.tiles, np.int32).reshape(-1, 2)
+        alt = np.ascontiguousarray(lw.tiles_alt, np.int32).reshape(-1, 2)
+        cand = {}
+        for u in range(len(lw.units)):
+            r = lw.unit(u)
+            t0, t1 = r["tile_begin"], r["tile_end"]
+            if r["flags"] & UNIT_JIT and t1 > t0 and not np.array_equal(base[t0:t1], alt[t0:t1]):
+                cand.setdefault(r["wave"], []).append((t0, t1))
+        if not cand or not self.n_outputs:
+            return
+        rng = np.random.default_rng(0)
+        x = self.new_values(rng.uniform(0.5, 2.0, self.input_count))
+        out = torch.empty(self.n_outputs, dtype=torch.float64, device=x.device)
+        self.run_csr(x, out)
+        stream = torch.cuda.current_stream(x.device)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+
+        def time_waves():
+            ms = {}
+            for w in cand:
+                for e0, e1 in evs:
+                    e0.record(stream)
+                    self.run_wave(x, w, out, stream)
+                    e1.record(stream)
+                torch.cuda.synchronize(x.device)
+                ms[w] = min(e0.elapsed_time(e1) for e0, e1 in evs)
+            return ms
+
+        best = {w: [np.inf, np.inf] for w in cand}
+        for _ in range(2):
+            for k, tiles in enumerate((base, alt)):
+                self.set_tiles(tiles)
+                for w, v in time_waves().items():
+                    best[w][k] = min(best[w][k], v)
+        final = base.copy()
+        for w, ranges in cand.items():
+            use_alt = best[w][1] < gain * best[w][0]
+            self.tile_order[w] = "frac" if use_alt else "inst"
+            if use_alt:
+                for t0, t1 in ranges:
+                    final[t0:t1] = alt[t0:t1]
+        self.tile_timings = {w: tuple(v) for w, v in best.items()}
+        self.set_tiles(final)
+        self.tiles = final
 
     def close(self):
         if self._handle:

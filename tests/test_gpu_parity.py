@@ -296,3 +296,26 @@ def test_outputs_host_many(golden):
     for k in range(4):
         assert cmp(rep[k])
     assert cmp(dp.run_outputs_host(golden.inputs))  # the single-set path after the stream
+
+
+def test_tile_schedules_bitwise(golden):
+    """Both tile schedules lower_plan offers (instance / fraction interleave of multi-group specialised
+    units) give the same bits; sgb_plan_set_tiles refuses a table of another length."""
+    import torch
+
+    from paper_2110_12865_b200 import DevicePlan, SgbError, lower_plan
+
+    plan = golden.plan
+    lw = lower_plan(plan, jit_min_n=0)
+    dp = DevicePlan(plan, lowered=lw)
+    x = dp.new_values(golden.inputs)
+    want = dp.run_csr(x).cpu().numpy()
+    assert (np.array_equal(bits(want), bits(golden.outputs)) if golden.exact else _close(want, golden.outputs))
+    if lw.tiles_alt is not None:
+        for t in (lw.tiles_alt, lw.tiles):
+            dp.set_tiles(t)
+            got = dp.run_csr(dp.new_values(golden.inputs)).cpu().numpy()
+            torch.cuda.synchronize()
+            assert np.array_equal(bits(got), bits(want))
+    with pytest.raises(SgbError):
+        dp.set_tiles(np.zeros((len(lw.tiles) + 1, 2), np.int32))
