@@ -19,7 +19,13 @@ ap.add_argument("--config", choices=("c2", "c3", "c4"), default="c2")
 ap.add_argument("--m", type=int, default=55)
 ap.add_argument("--w4", type=int, default=708)
 ap.add_argument("--layout", choices=("csr", "reference"), default="csr")
+ap.add_argument("--schedule", choices=("auto", "inst", "frac"), default="inst",
+                help="tile schedule: auto = DevicePlan.autotune (its timing launches distort a capture)")
 args = ap.parse_args()
+if args.schedule != "auto":
+    import os
+
+    os.environ["SGB_AUTOTUNE"] = "0"
 
 import torch  # noqa: E402
 
@@ -31,6 +37,8 @@ key, plan, _, _ = bench.build_workload(args, 0, 1)
 print(f"plan {key} ready in {time.time() - t0:.1f}s: {len(plan.kernels)} kernels, {len(plan.outputs)} outputs",
       flush=True)
 dp = DevicePlan(plan, csr_layout=args.layout == "csr" and args.mode == "csr")
+if args.schedule == "frac" and dp.lowered.tiles_alt is not None:
+    dp.set_tiles(dp.lowered.tiles_alt)
 print("waves", dp.launches, "units", dp.units, "csr units", dp.csr_units, flush=True)
 if args.batch:
     X = torch.zeros((plan.value_array_size, args.batch), dtype=torch.float64, device="cuda")
