@@ -410,6 +410,48 @@ class DevicePlan:
                "sgb_run_batch_csr")
         return out
 
+    def run_batch_outputs_host(self, inputs, out):
+        """Value sets through host buffers in chunks, pipelined: ``inputs`` a pinned float64 tensor
+        (chunks, input_count, cb), ``out`` (chunks, n_outputs, cb).  Chunk c's inputs copy in on a
+        copy stream while chunk c-1 evaluates (sgb_run_batch_csr, current stream) and chunk c-2's
+        CSR values copy out on another; two device workspaces.  Synchronous."""
+        import torch
+
+        if inputs.dim() != 3 or inputs.shape[1] != self.input_count or inputs.dtype != torch.float64:
+            raise ValueError(f"inputs must be float64 (chunks, {self.input_count}, cb)")
+        n_chunks, _, cb = inputs.shape
+        if tuple(out.shape) != (n_chunks, self.n_outputs, cb) or out.dtype != torch.float64:
+            raise ValueError(f"out must be float64 ({n_chunks}, {self.n_outputs}, {cb})")
+        dev = torch.device(f"cuda:{self.device}")
+        comp = torch.cuda.current_stream(dev)
+        h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        nj = min(2, n_chunks)
+        X = [torch.zeros((self.value_array_size, cb), dtype=torch.float64, device=dev) for _ in range(nj)]
+        O = [torch.empty((self.n_outputs, cb), dtype=torch.float64, device=dev) for _ in range(nj)]
+        ev_in, ev_run, ev_out = ([torch.cuda.Event() for _ in range(nj)] for _ in range(3))
+        comp.synchronize()  # the workspaces are zeroed before the copy streams touch them
+        rezero = int(self.lowered.needs_zero) == 2
+        for c in range(n_chunks):
+            j = c % nj
+            if c >= nj:
+                h2d.wait_event(ev_run[j])  # chunk c-2 has finished reading X[j]
+            with torch.cuda.stream(h2d):
+                X[j][: self.input_count].copy_(inputs[c], non_blocking=True)
+            ev_in[j].record(h2d)
+            comp.wait_event(ev_in[j])
+            if c >= nj:
+                comp.wait_event(ev_out[j])  # chunk c-2's CSR values are out of O[j]
+            if rezero:
+                X[j][self.input_count:].zero_()
+            self.run_batch_csr(X[j], O[j], stream=comp)
+            ev_run[j].record(comp)
+            d2h.wait_event(ev_run[j])
+            with torch.cuda.stream(d2h):
+                out[c].copy_(O[j], non_blocking=True)
+            ev_out[j].record(d2h)
+        torch.cuda.synchronize(dev)
+        return out
+
     def gather_outputs_batch(self, X, out=None, stream=None):
         import torch
 

@@ -296,6 +296,15 @@ def test_outputs_host_many(golden):
     for k in range(4):
         assert cmp(rep[k])
     assert cmp(dp.run_outputs_host(golden.inputs))  # the single-set path after the stream
+    # chunked batched stream: 3 chunks of 2 value sets
+    import torch
+
+    sets = np.stack([golden.inputs * f for f in (1.0, 1.5, 0.75, 1.25, 1.0, 2.0)])  # (6, n_in)
+    hin = torch.from_numpy(np.ascontiguousarray(sets.reshape(3, 2, -1).transpose(0, 2, 1)))
+    hout = torch.empty((3, len(plan.outputs), 2), dtype=torch.float64)
+    dp.run_batch_outputs_host(hin, hout)
+    for k in range(6):
+        assert np.array_equal(bits(hout[k // 2, :, k % 2].numpy()), bits(dp.run_outputs_host(sets[k])))
 
 
 def test_tile_schedules_bitwise(golden):
