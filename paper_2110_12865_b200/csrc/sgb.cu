@@ -33,6 +33,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -58,7 +59,7 @@ enum : int {
 enum : int {
   U_WAVE = 0, U_KIND, U_VARIANT, U_G0, U_G1, U_T0, U_T1, U_BS, U_REGS, U_FLAGS, U_COUNT
 };
-enum : int { UNIT_CSR_ONLY = 1, UNIT_JIT = 2, UNIT_VALUE_ONLY = 4, UNIT_WINDOW = 8 };
+enum : int { UNIT_CSR_ONLY = 1, UNIT_JIT = 2, UNIT_VALUE_ONLY = 4, UNIT_WINDOW = 8, UNIT_GRID_TILES = 1 << 20 };
 constexpr int JIT_BLOCK = 256;  // jit.py JIT_BLOCK
 constexpr int WIN = 2048;       // lower.WIN: outputs per CSR window
 constexpr int MAX_WINDOW_PIECES = 512;  // jit.MAX_WINDOW_PIECES
@@ -1157,6 +1158,13 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       } else if (jit) {
         SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, u.jit, JIT_BLOCK, (size_t)u.regs));
         u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
+        // SGB_JIT_GRID=tiles: one block per tile, the hardware dispatching blocks in tile order as
+        // SMs free up (persistent grid-stride blocks drift apart over a long sweep)
+        const char *jg = getenv("SGB_JIT_GRID");
+        if (jg && !strcmp(jg, "tiles") && u.t1 - u.t0 <= 0x7fffffffLL) {
+          u.grid = u.t1 - u.t0;
+          u.flags |= UNIT_GRID_TILES;
+        }
         if (u.grid > u.t1 - u.t0) u.grid = u.t1 - u.t0;
       } else if (u.kind == KIND_TAPE) {
         SGB_CUDA(tape_occupancy_any(u.bs, u.variant, u.regs, &nb));
@@ -1243,7 +1251,7 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       max_units = n > max_units ? n : max_units;
       if (n < 2) continue;
       for (Unit &u : p->units)  // leave one block per SM to the co-running units
-        if (u.wave == w && u.grid > prop.multiProcessorCount) {
+        if (u.wave == w && u.grid > prop.multiProcessorCount && !(u.flags & UNIT_GRID_TILES)) {
           const int64_t cap = u.grid - prop.multiProcessorCount;
           if (cap >= prop.multiProcessorCount) u.grid = cap;
         }
