@@ -707,8 +707,8 @@ def main():
                       "separate wave-by-wave pass",
             "layout": (f"CSR layout: plan groups {dp.lowered.csr_layout} store instance-major"
                        if dp.csr_layout else "reference value-array layout"),
-            "tile_schedule": ({str(w): f"{o} (inst {dp.tile_timings[w][0]:.4f} ms, frac {dp.tile_timings[w][1]:.4f} ms)"
-                               for w, o in dp.tile_order.items()} if dp.tile_order else "single candidate"),
+            "tile_schedule": ({str(w): {"kept": o, **{k: round(v, 4) for k, v in dp.tile_timings[w].items()}}
+                               for w, o in dp.tile_order.items()} if dp.tile_order else "no specialised units"),
             "achieved_hbm_gbs_step": step_bytes / (ms_per_step * 1e-3) / 1e9,
             "balg_bytes_step": step_bytes, "balg_bytes_single_pass": plan_balg(plan),
             "balg_gbs_single_pass": plan_balg(plan) / (ms_per_step * 1e-3) / 1e9,

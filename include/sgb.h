@@ -141,6 +141,12 @@ int sgb_run_wave(sgb_plan *plan, double *x_dev, double *out_dev, int wave, void 
  * schedule autotuning.  Synchronous. */
 int sgb_plan_set_tiles(sgb_plan *plan, const int32_t *tiles, int64_t n_tiles);
 
+/* Launch grid of the specialised units of one wave: tiles = 0 a persistent
+ * grid sized to the resident capacity (blocks stride over the tiles), 1 one
+ * block per tile (dispatched in tile order).  Returns how many units were
+ * switched (>= 0) or a negative error code.  Synchronous. */
+int sgb_plan_set_wave_grid(sgb_plan *plan, int wave, int tiles);
+
 /* out_dev[k] = x_dev[outputs[k]]  (codegen.py:445). */
 int sgb_gather_outputs(sgb_plan *plan, const double *x_dev, double *out_dev, void *stream);
 

@@ -59,7 +59,7 @@ enum : int {
 enum : int {
   U_WAVE = 0, U_KIND, U_VARIANT, U_G0, U_G1, U_T0, U_T1, U_BS, U_REGS, U_FLAGS, U_COUNT
 };
-enum : int { UNIT_CSR_ONLY = 1, UNIT_JIT = 2, UNIT_VALUE_ONLY = 4, UNIT_WINDOW = 8, UNIT_GRID_TILES = 1 << 20 };
+enum : int { UNIT_CSR_ONLY = 1, UNIT_JIT = 2, UNIT_VALUE_ONLY = 4, UNIT_WINDOW = 8 };
 constexpr int JIT_BLOCK = 256;  // jit.py JIT_BLOCK
 constexpr int WIN = 2048;       // lower.WIN: outputs per CSR window
 constexpr int MAX_WINDOW_PIECES = 512;  // jit.MAX_WINDOW_PIECES
@@ -765,7 +765,8 @@ struct Unit {
   int index;                   // position in sgb_plan_desc.units (names the specialised kernels)
   const void *jit = nullptr;   // specialised tape kernels (cudaKernel_t), UNIT_JIT
   const void *jitb = nullptr;
-  int64_t grid;      // single-set persistent grid (blocks)
+  int64_t grid;      // single-set grid in use (blocks)
+  int64_t grid_p = 0, grid_t = 0;  // specialised units: persistent grid / one block per tile
   int64_t t0, t1;    // single-set tiles [t0, t1)
   int64_t bt0, bt1;  // batched tiles
 };
@@ -1158,13 +1159,6 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       } else if (jit) {
         SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, u.jit, JIT_BLOCK, (size_t)u.regs));
         u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
-        // SGB_JIT_GRID=tiles: one block per tile, the hardware dispatching blocks in tile order as
-        // SMs free up (persistent grid-stride blocks drift apart over a long sweep)
-        const char *jg = getenv("SGB_JIT_GRID");
-        if (jg && !strcmp(jg, "tiles") && u.t1 - u.t0 <= 0x7fffffffLL) {
-          u.grid = u.t1 - u.t0;
-          u.flags |= UNIT_GRID_TILES;
-        }
         if (u.grid > u.t1 - u.t0) u.grid = u.t1 - u.t0;
       } else if (u.kind == KIND_TAPE) {
         SGB_CUDA(tape_occupancy_any(u.bs, u.variant, u.regs, &nb));
@@ -1251,11 +1245,23 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       max_units = n > max_units ? n : max_units;
       if (n < 2) continue;
       for (Unit &u : p->units)  // leave one block per SM to the co-running units
-        if (u.wave == w && u.grid > prop.multiProcessorCount && !(u.flags & UNIT_GRID_TILES)) {
+        if (u.wave == w && u.grid > prop.multiProcessorCount) {
           const int64_t cap = u.grid - prop.multiProcessorCount;
           if (cap >= prop.multiProcessorCount) u.grid = cap;
         }
     }
+    // specialised units have two grids: the persistent one (resident capacity, tiles grid-strided)
+    // and one block per tile, the hardware dispatching blocks in tile order as SMs free up --
+    // persistent blocks drift apart over a long sweep and widen its L2 working set.
+    // sgb_plan_set_wave_grid picks per wave (runtime autotune); SGB_JIT_GRID=tiles sets the default.
+    const char *jg = getenv("SGB_JIT_GRID");
+    const bool tiles_default = jg && !strcmp(jg, "tiles");
+    for (Unit &u : p->units)
+      if ((u.flags & UNIT_JIT) && !(u.flags & UNIT_WINDOW)) {
+        u.grid_p = u.grid;
+        u.grid_t = u.t1 - u.t0 < 0x7fffffffLL ? u.t1 - u.t0 : 0x7fffffffLL;
+        if (tiles_default && u.grid_t > 0) u.grid = u.grid_t;
+      }
     const int n_aux = max_units - 1 < 8 ? max_units - 1 : 8;
     SGB_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
     for (int k = 0; k < n_aux; ++k) {
@@ -1591,6 +1597,23 @@ int sgb_plan_set_tiles(sgb_plan *p, const int32_t *tiles, int64_t n_tiles) {
   SGB_CUDA(cudaDeviceSynchronize());
   if (n_tiles) SGB_CUDA(cudaMemcpy(p->d_tiles, tiles, sizeof(int2) * (size_t)n_tiles, cudaMemcpyHostToDevice));
   return 0;
+}
+
+
+// Grid of the specialised units of one wave: persistent (tiles = 0) or one block per tile
+// (tiles = 1).  Returns the number of units switched (0 when the wave has none).  Synchronous.
+int sgb_plan_set_wave_grid(sgb_plan *p, int wave, int tiles) {
+  if (!p) return fail(-1, "sgb_plan_set_wave_grid: null plan");
+  std::lock_guard<std::mutex> lk(p->run_mu);
+  SGB_CUDA(cudaSetDevice(p->device));
+  SGB_CUDA(cudaDeviceSynchronize());
+  int n = 0;
+  for (Unit &u : p->units)
+    if (u.wave == wave && u.grid_p > 0 && u.grid_t > 0) {
+      u.grid = tiles ? u.grid_t : u.grid_p;
+      ++n;
+    }
+  return n;
 }
 
 }  // extern "C"

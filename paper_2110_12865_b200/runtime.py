@@ -90,6 +90,7 @@ SYMBOLS = (
     "sgb_plan_create", "sgb_plan_destroy", "sgb_run_values", "sgb_run_csr", "sgb_gather_outputs",
     "sgb_sg_run", "sgb_run_outputs_host", "sgb_run_outputs_host_many", "sgb_run_batch", "sgb_run_batch_csr", "sgb_gather_outputs_batch",
     "sgb_plan_waves", "sgb_last_error", "sgb_run_wave", "sgb_plan_units", "sgb_plan_set_tiles",
+    "sgb_plan_set_wave_grid",
 )
 
 
@@ -121,6 +122,7 @@ def load_library(path: Path | str | None = None):
             "sgb_plan_waves": (i32, [vp, i32]),
             "sgb_plan_units": (i32, [vp, i32]),
             "sgb_plan_set_tiles": (i32, [vp, vp, i64]),
+            "sgb_plan_set_wave_grid": (i32, [vp, i32, i32]),
             "sgb_last_error": (ctypes.c_char_p, []),
         }
         for name, (res, args) in sig.items():
@@ -225,8 +227,8 @@ class DevicePlan:
         self.csr_launches = int(self._lib.sgb_plan_waves(self._handle, 1))  # CSR-mode waves
         self.units = int(self._lib.sgb_plan_units(self._handle, 0))  # kernel launches per evaluation
         self.csr_units = int(self._lib.sgb_plan_units(self._handle, 1))
-        self.tile_order = {}  # wave -> schedule kept by autotune ("inst" / "frac")
-        if getattr(lw, "tiles_alt", None) is not None and os.environ.get("SGB_AUTOTUNE", "1") != "0":
+        self.tile_order = {}  # wave -> (schedule, grid) kept by autotune
+        if os.environ.get("SGB_AUTOTUNE", "1") != "0":
             self.autotune()
 
     def set_tiles(self, tiles: np.ndarray):
@@ -234,25 +236,36 @@ class DevicePlan:
         t = np.ascontiguousarray(tiles, np.int32).reshape(-1, 2)
         _check(self._lib.sgb_plan_set_tiles(self._handle, _ptr(t), t.shape[0]), "sgb_plan_set_tiles")
 
+    def set_wave_grid(self, wave: int, tiles: bool) -> int:
+        """Specialised units of ``wave``: persistent grid (False) or one block per tile (True)."""
+        rc = int(self._lib.sgb_plan_set_wave_grid(self._handle, int(wave), int(bool(tiles))))
+        if rc < 0:
+            _check(rc, "sgb_plan_set_wave_grid")
+        return rc
+
     def autotune(self, reps: int = 5, gain: float = 0.98):
-        """Per wave, keep the faster of the two tile schedules lower_plan offers for its multi-group
-        specialised units: instances interleaved by index (``tiles``) or by the fraction of their
-        group (``tiles_alt``).  Each wave is timed alone with CUDA events in CSR mode, both
-        schedules twice, min over ``reps`` launches; results never depend on the schedule."""
+        """Per wave, keep the fastest launch configuration of its specialised units: tile schedule
+        instance- (``tiles``) or fraction-interleaved (``tiles_alt``, when lower_plan offers one) x
+        grid persistent or one block per tile.  Each wave is timed alone with CUDA events in CSR
+        mode, every candidate twice, min over ``reps`` launches; a candidate replaces the default
+        (instance order, persistent) only when ``gain`` x faster.  Results never depend on it."""
         import torch
 
-        from .lower import UNIT_JIT
+        from .lower import UNIT_JIT, UNIT_WINDOW
 
         lw = self.lowered
         base = np.ascontiguousarray(lw.tiles, np.int32).reshape(-1, 2)
-        alt = np.ascontiguousarray(lw.tiles_alt, np.int32).reshape(-1, 2)
-        cand = {}
+        alt = (np.ascontiguousarray(lw.tiles_alt, np.int32).reshape(-1, 2)
+               if getattr(lw, "tiles_alt", None) is not None else None)
+        waves, ranges = set(), {}
         for u in range(len(lw.units)):
             r = lw.unit(u)
             t0, t1 = r["tile_begin"], r["tile_end"]
-            if r["flags"] & UNIT_JIT and t1 > t0 and not np.array_equal(base[t0:t1], alt[t0:t1]):
-                cand.setdefault(r["wave"], []).append((t0, t1))
-        if not cand or not self.n_outputs:
+            if r["flags"] & UNIT_JIT and not r["flags"] & UNIT_WINDOW and t1 > t0:
+                waves.add(r["wave"])
+                if alt is not None and not np.array_equal(base[t0:t1], alt[t0:t1]):
+                    ranges.setdefault(r["wave"], []).append((t0, t1))
+        if not waves or not self.n_outputs:
             return
         rng = np.random.default_rng(0)
         x = self.new_values(rng.uniform(0.5, 2.0, self.input_count))
@@ -261,31 +274,38 @@ class DevicePlan:
         stream = torch.cuda.current_stream(x.device)
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
 
-        def time_waves():
-            ms = {}
-            for w in cand:
-                for e0, e1 in evs:
-                    e0.record(stream)
-                    self.run_wave(x, w, out, stream)
-                    e1.record(stream)
-                torch.cuda.synchronize(x.device)
-                ms[w] = min(e0.elapsed_time(e1) for e0, e1 in evs)
-            return ms
+        def time_wave(w):
+            for e0, e1 in evs:
+                e0.record(stream)
+                self.run_wave(x, w, out, stream)
+                e1.record(stream)
+            torch.cuda.synchronize(x.device)
+            return min(e0.elapsed_time(e1) for e0, e1 in evs)
 
-        best = {w: [np.inf, np.inf] for w in cand}
+        cands = [("inst", False), ("inst", True)] + ([("frac", False), ("frac", True)] if ranges else [])
+        best = {w: {} for w in waves}
         for _ in range(2):
-            for k, tiles in enumerate((base, alt)):
-                self.set_tiles(tiles)
-                for w, v in time_waves().items():
-                    best[w][k] = min(best[w][k], v)
+            for order, tiles in cands:
+                self.set_tiles(alt if order == "frac" else base)
+                for w in waves:
+                    if order == "frac" and w not in ranges:
+                        continue
+                    self.set_wave_grid(w, tiles)
+                    key = (order, tiles)
+                    best[w][key] = min(best[w].get(key, np.inf), time_wave(w))
         final = base.copy()
-        for w, ranges in cand.items():
-            use_alt = best[w][1] < gain * best[w][0]
-            self.tile_order[w] = "frac" if use_alt else "inst"
-            if use_alt:
-                for t0, t1 in ranges:
+        for w in sorted(waves):
+            t_def = best[w][("inst", False)]
+            key = min(best[w], key=best[w].get)
+            if best[w][key] >= gain * t_def:
+                key = ("inst", False)
+            self.set_wave_grid(w, key[1])
+            if key[0] == "frac":
+                for t0, t1 in ranges[w]:
                     final[t0:t1] = alt[t0:t1]
-        self.tile_timings = {w: tuple(v) for w, v in best.items()}
+            self.tile_order[w] = f"{key[0]}/{'tiles' if key[1] else 'persistent'}"
+        self.tile_timings = {w: {f"{o}/{'tiles' if g else 'persistent'}": v for (o, g), v in d.items()}
+                             for w, d in best.items()}
         self.set_tiles(final)
         self.tiles = final
 

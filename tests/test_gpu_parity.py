@@ -326,5 +326,10 @@ def test_tile_schedules_bitwise(golden):
             got = dp.run_csr(dp.new_values(golden.inputs)).cpu().numpy()
             torch.cuda.synchronize()
             assert np.array_equal(bits(got), bits(want))
+    for w in range(dp.csr_launches):  # both grids of the specialised units, every wave
+        for tiles in (True, False):
+            dp.set_wave_grid(w, tiles)
+            got = dp.run_csr(dp.new_values(golden.inputs)).cpu().numpy()
+            assert np.array_equal(bits(got), bits(want))
     with pytest.raises(SgbError):
         dp.set_tiles(np.zeros((len(lw.tiles) + 1, 2), np.int32))

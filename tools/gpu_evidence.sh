@@ -26,5 +26,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sgb
    -o $OUT/prof_c2 python tools/profile_run.py --config c2 --evals 3 > $OUT/ncu_full_c2.log 2>&1
 echo "full c2 rc=$?" >> $OUT/status.txt
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"sgb_tape" -s 2 -c 2 \
-   -o $OUT/prof_c3 python tools/profile_run.py --config c3 --evals 2 --schedule frac > $OUT/ncu_full_c3.log 2>&1
+   -o $OUT/prof_c3 python tools/profile_run.py --config c3 --evals 2 --schedule frac --grid tiles > $OUT/ncu_full_c3.log 2>&1
 echo "full c3 rc=$?" >> $OUT/status.txt

@@ -21,6 +21,8 @@ ap.add_argument("--w4", type=int, default=708)
 ap.add_argument("--layout", choices=("csr", "reference"), default="csr")
 ap.add_argument("--schedule", choices=("auto", "inst", "frac"), default="inst",
                 help="tile schedule: auto = DevicePlan.autotune (its timing launches distort a capture)")
+ap.add_argument("--grid", choices=("persistent", "tiles"), default="persistent",
+                help="specialised-unit grid when --schedule is not auto")
 args = ap.parse_args()
 if args.schedule != "auto":
     import os
@@ -39,6 +41,9 @@ print(f"plan {key} ready in {time.time() - t0:.1f}s: {len(plan.kernels)} kernels
 dp = DevicePlan(plan, csr_layout=args.layout == "csr" and args.mode == "csr")
 if args.schedule == "frac" and dp.lowered.tiles_alt is not None:
     dp.set_tiles(dp.lowered.tiles_alt)
+if args.schedule != "auto" and args.grid == "tiles":
+    for w in range(dp.csr_launches):
+        dp.set_wave_grid(w, True)
 print("waves", dp.launches, "units", dp.units, "csr units", dp.csr_units, flush=True)
 if args.batch:
     X = torch.zeros((plan.value_array_size, args.batch), dtype=torch.float64, device="cuda")
