@@ -871,7 +871,9 @@ void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_
     if (batched) {
       int64_t ld_ = ld, batch_ = batch, ldo = ld_out;
       void *args[] = {&T, &tiles, &n, &x, &ld_, &batch_, &out, &ldo, &c};
-      const int64_t grid = blocks < u.grid ? blocks : u.grid;
+      // the batched kernels keep the persistent grid (the per-wave grid choice is tuned single-set)
+      const int64_t cap = u.grid_p > 0 ? u.grid_p : u.grid;
+      const int64_t grid = blocks < cap ? blocks : cap;
       cudaLaunchKernel(u.jitb, dim3((unsigned)grid), dim3(JIT_BLOCK), args, 0, s);
     } else {
       void *args[] = {&T, &tiles, &n, &x, &out, &c};
