@@ -871,8 +871,13 @@ void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_
     if (batched) {
       int64_t ld_ = ld, batch_ = batch, ldo = ld_out;
       void *args[] = {&T, &tiles, &n, &x, &ld_, &batch_, &out, &ldo, &c};
-      // the batched kernels keep the persistent grid (the per-wave grid choice is tuned single-set)
-      const int64_t cap = u.grid_p > 0 ? u.grid_p : u.grid;
+      // the batched kernels keep the persistent grid (the per-wave grid choice is tuned single-set);
+      // SGB_BATCH_GRID=tiles launches one block per batched tile instead
+      static const bool batch_tiles = [] {
+        const char *e = getenv("SGB_BATCH_GRID");
+        return e && !strcmp(e, "tiles");
+      }();
+      const int64_t cap = batch_tiles ? blocks : (u.grid_p > 0 ? u.grid_p : u.grid);
       const int64_t grid = blocks < cap ? blocks : cap;
       cudaLaunchKernel(u.jitb, dim3((unsigned)grid), dim3(JIT_BLOCK), args, 0, s);
     } else {
