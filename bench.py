@@ -460,15 +460,18 @@ def run_spgemm(args):
     for _ in range(args.e2e_steps * 20):
         dp.run_outputs_host(inp_h, out_h)
     serial_s = (time.perf_counter() - t0) / (args.e2e_steps * 20)
-    k_sets = args.e2e_steps * 20
-    ins_h = torch.from_numpy(np.ascontiguousarray(np.broadcast_to(inputs, (k_sets, inputs.size)))).pin_memory()
-    outs_h = torch.empty((k_sets, n_out), dtype=torch.float64).pin_memory()
-    dp.run_outputs_host_many(ins_h.numpy()[:2], outs_h.numpy()[:2])  # warm (second workspace)
+    # a small plan is launch-bound per value set: the e2e stream carries value sets in batched chunks
+    # (sgb_run_batch_csr per chunk, copies of neighbouring chunks overlapping)
+    n_chunks, cb = 8, max(1, args.e2e_steps * 20 // 8)
+    k_sets = n_chunks * cb
+    hin = torch.from_numpy(np.ascontiguousarray(np.broadcast_to(inputs[None, :, None],
+                                                                (n_chunks, inputs.size, cb)))).pin_memory()
+    hout = torch.empty((n_chunks, n_out, cb), dtype=torch.float64).pin_memory()
+    dp.run_batch_outputs_host(hin, hout)  # warm
     t0 = time.perf_counter()
-    dp.run_outputs_host_many(ins_h.numpy(), outs_h.numpy())
+    dp.run_batch_outputs_host(hin, hout)
     e2e_s = (time.perf_counter() - t0) / k_sets
-    got = outs_h.numpy()
-    e2e_ok = bool(np.all(got.view(np.uint64) == out.cpu().numpy().view(np.uint64)[None, :]))
+    e2e_ok = bool(np.all(hout.numpy().view(np.uint64) == out.cpu().numpy().view(np.uint64)[None, :, None]))
     cpu = None
     if not args.no_cpu_baseline:
         res = cpu_reference(plan, inputs, 200, 5, key="spgemm_n2000_k10")
@@ -491,8 +494,9 @@ def run_spgemm(args):
                      "algorithmic_bytes": bal, "peak_source": peak_src},
         "e2e": {"value": n_out / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * int(plan.input_count),
                 "d2h_bytes_per_step": 8 * n_out,
-                "api": (f"DevicePlan.run_outputs_host_many -> sgb_run_outputs_host_many: {k_sets} value sets from "
-                        "pinned host memory, copy in / evaluate / copy out pipelined, wall clock over the call"),
+                "api": (f"DevicePlan.run_batch_outputs_host: {k_sets} value sets from pinned host memory in "
+                        f"{n_chunks} chunks of {cb} (sgb_run_batch_csr per chunk), copy in / evaluate / copy out "
+                        "pipelined on three streams, wall clock over the call"),
                 "serial_value": n_out / serial_s,
                 "serial_api": "DevicePlan.run_outputs_host -> sgb_run_outputs_host, one synchronous call per step",
                 "matches_device_run": e2e_ok},
