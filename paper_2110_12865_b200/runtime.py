@@ -446,10 +446,15 @@ class DevicePlan:
         comp = torch.cuda.current_stream(dev)
         h2d, d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
         nj = min(2, n_chunks)
-        X = [torch.zeros((self.value_array_size, cb), dtype=torch.float64, device=dev) for _ in range(nj)]
-        O = [torch.empty((self.n_outputs, cb), dtype=torch.float64, device=dev) for _ in range(nj)]
+        ws = getattr(self, "_batch_ws", None)
+        if ws is None or ws[0] != cb or len(ws[1]) < nj:
+            # kept across calls: CSR evaluations never write the slots a plan reads as zero
+            X = [torch.zeros((self.value_array_size, cb), dtype=torch.float64, device=dev) for _ in range(nj)]
+            O = [torch.empty((self.n_outputs, cb), dtype=torch.float64, device=dev) for _ in range(nj)]
+            self._batch_ws = ws = (cb, X, O)
+        X, O = ws[1], ws[2]
         ev_in, ev_run, ev_out = ([torch.cuda.Event() for _ in range(nj)] for _ in range(3))
-        comp.synchronize()  # the workspaces are zeroed before the copy streams touch them
+        comp.synchronize()  # the workspaces are zeroed / free before the copy streams touch them
         rezero = int(self.lowered.needs_zero) == 2
         for c in range(n_chunks):
             j = c % nj
