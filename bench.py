@@ -26,6 +26,7 @@ timed region is bracketed by barriers and the max over ranks is reported.
 from __future__ import annotations
 
 import argparse
+import dataclasses
 import json
 import os
 import pickle
@@ -523,6 +524,10 @@ def main():
     ap.add_argument("--w5", type=int, default=200, help="C5 grid width")
     ap.add_argument("--batch", type=int, default=256, help="C5 value sets (whole job)")
     ap.add_argument("--gather", action="store_true", help="C5: also time the NCCL gather to rank 0")
+    ap.add_argument("--split", choices=("replicas", "outputs"), default="replicas",
+                    help="N>1: replicas (one evaluation per rank) or one evaluation with its CSR outputs split")
+    ap.add_argument("--split-world", type=int, default=0, help="outputs split: ways (default = world size)")
+    ap.add_argument("--split-rank", type=int, default=None, help="outputs split: this process's slice")
     ap.add_argument("--layout", choices=("csr", "reference"), default="csr",
                     help="csr: multi-root groups whose readers gather across roots store instance-major "
                          "(lower.choose_relayout); reference: the plan's own value-array layout")
@@ -551,9 +556,29 @@ def main():
     from paper_2110_12865_b200.metrics import csr_wave_traffic, plan_balg, wave_traffic
 
     key, plan, row_ptr, col_idx = build_workload(args, rank, world, barrier)
+    n_total = len(plan.outputs)
+    split = None
+    if args.split == "outputs":
+        # one evaluation, CSR outputs partitioned: this rank computes its slice's producer cone
+        from paper_2110_12865_b200 import lower_plan
+        from paper_2110_12865_b200.shard import shard_device_plan, shard_outputs
+
+        s_world = args.split_world or world
+        s_rank = rank if args.split_rank is None else args.split_rank
+        lo, hi = shard_outputs(n_total, s_world, s_rank)
+        lw_full = lower_plan(plan, relayout=False)
+        full_tiles = lw_full.units[:, 6] - lw_full.units[:, 5]
+        plan, lw_s = shard_device_plan(plan, lw_full, lo, hi)
+        split = {"world": s_world, "rank": s_rank, "outputs": [lo, hi],
+                 "tiles_kept": int(len(lw_s.tiles)), "tiles_full": int(len(lw_full.tiles)),
+                 "unit_tile_frac": [(int(k), int(f)) for k, f in zip(lw_s.units[:, 6] - lw_s.units[:, 5], full_tiles)]}
+        dp = DevicePlan(plan, device=local, lowered=lw_s)
+        inputs = workload_inputs(args, seed=0)  # every rank: the same value set
+        args.no_cpu_baseline = True  # the CPU reference evaluates whole plans (the N=1 line carries it)
+    else:
+        inputs = workload_inputs(args, seed=rank)
+        dp = DevicePlan(plan, device=local, csr_layout=args.layout == "csr")
     n_out = len(plan.outputs)
-    inputs = workload_inputs(args, seed=rank)
-    dp = DevicePlan(plan, device=local, csr_layout=args.layout == "csr")
     x = dp.new_values(inputs)
     out = torch.empty(n_out, dtype=torch.float64, device=x.device)
     stream = torch.cuda.current_stream()
@@ -569,7 +594,9 @@ def main():
     if rank == 0:
         from oracle import oracle
 
-        want = oracle.run_outputs(plan, inputs)
+        want = oracle.run_outputs(getattr(plan, "_plan", plan), inputs)
+        if split:
+            want = want[split["outputs"][0]: split["outputs"][1]]
         got = out.cpu().numpy()
         parity = "bitwise" if np.array_equal(got.view(np.uint64), want.view(np.uint64)) else "MISMATCH"
         if parity == "MISMATCH" and not dp.lowered.exact:  # LOG / EXP / ...: CUDA libm vs glibc
@@ -622,7 +649,8 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = world * n_out / (ms_per_step * 1e-3)
+    job_out = n_total if split and split["world"] == world else world * n_out  # outputs the whole job produces
+    value = job_out / (ms_per_step * 1e-3)
 
     # ---- end to end through the public host-buffer API (pinned host memory) ----
     # (a) one synchronous call per step (sgb_run_outputs_host): copy in, evaluate, copy out
@@ -666,6 +694,16 @@ def main():
     direct = bool(np.any(dp.lowered.groups["flags"] & (384)))  # FLAG_OPOS16 | FLAG_OPOS32
     traffic = csr_wave_traffic(plan, dp.lowered) if direct else wave_traffic(plan, dp.lowered)
     assert len(traffic) == n_w, (len(traffic), n_w)
+    if split:  # full-plan bytes scaled by the share of each wave's tiles the shard keeps (approximate)
+        units = dp.lowered.units
+        for w_, t in enumerate(traffic):
+            sel = [j for j in range(len(units)) if int(units[j, 0]) == w_]
+            kept = sum(split["unit_tile_frac"][j][0] for j in sel)
+            full = sum(split["unit_tile_frac"][j][1] for j in sel)
+            if full:
+                f = kept / full
+                traffic[w_] = dataclasses.replace(t, index_bytes=int(t.index_bytes * f), const_bytes=int(t.const_bytes * f),
+                                                  read_bytes=int(t.read_bytes * f), write_bytes=int(t.write_bytes * f))
     dom = int(np.argmax(per_launch))
     dom_bytes = traffic[dom].bytes
     achieved = dom_bytes / (per_launch[dom] * 1e-3) / 1e9
@@ -697,12 +735,17 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong" if split else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {
             "workload": workload_name(args, n_out), "w": args.w, "out_nnz": n_out,
             "value_array": int(plan.value_array_size), "kernels": len(plan.kernels),
             "waves": n_w, "index_entries": int(np.asarray(plan.positions).size),
-            "parallelism": f"replicas x{world}: one full evaluation per GPU per step (independent value sets)",
+            "parallelism": (f"replicas x{world}: one full evaluation per GPU per step (independent value sets)"
+                            if not split else
+                            f"one evaluation, CSR outputs split {split['world']} ways (shard.shard_device_plan): "
+                            f"this rank computes outputs {split['outputs']} from its producer cone "
+                            f"({split['tiles_kept']} of {split['tiles_full']} tiles); no collective in the step"),
+            "split": split,
             "l2": "no flush: value array + tables exceed the 126 MB L2",
             "clock_settle": "1 s of untimed evaluations before the timed region",
             "parity": parity, "mode": ("CSR, direct stores (sgb_run_csr)" if direct else
@@ -724,12 +767,12 @@ def main():
         "launches": [{"name": t.name, "ms": float(ms), "alg_bytes": t.bytes,
                       "gbs": t.bytes / (ms * 1e-3) / 1e9 if ms > 0 else None}
                      for t, ms in zip(traffic, per_launch)],
-        "e2e": {"value": world * n_out / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * int(plan.input_count),
+        "e2e": {"value": job_out / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * int(plan.input_count),
                 "d2h_bytes_per_step": 8 * n_out,
                 "api": (f"DevicePlan.run_outputs_host_many -> sgb_run_outputs_host_many: {k_sets} value sets "
                         "from pinned host memory, per-set copy in / evaluate / copy out pipelined on "
                         "three streams, wall clock over the whole call"),
-                "serial_value": world * n_out / serial_s,
+                "serial_value": job_out / serial_s,
                 "serial_api": "DevicePlan.run_outputs_host -> sgb_run_outputs_host, one synchronous call per step",
                 "matches_device_run": e2e_ok},
         "gpu_launches": args.steps * dp.csr_units,

@@ -57,3 +57,110 @@ def max_over_ranks(value: float, device=None, group=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+# -- one large evaluation: output nonzeros partitioned, each rank its producer cone ----------
+
+
+class _OutputSlice:
+    """An ExecutionPlan view whose outputs are the CSR positions [lo, hi) (codegen.py:88-98 fields)."""
+
+    def __init__(self, plan, lo: int, hi: int):
+        import numpy as np
+
+        self._plan = plan
+        self.outputs = np.asarray(plan.outputs, np.int64)[lo:hi]
+        self.output_range = (lo, hi)
+
+    def __getattr__(self, name):
+        return getattr(self._plan, name)
+
+
+def shard_outputs(total: int, world: int, rank: int) -> tuple[int, int]:
+    """[lo, hi) of the CSR value array ``rank`` evaluates: contiguous, sizes differ by at most one."""
+    first, count = shard_value_sets(total, world, rank)
+    return first, first + count
+
+
+def output_cone(plan, lo: int, hi: int):
+    """Per plan kernel, the instances the CSR outputs [lo, hi) depend on (bool mask of length N).
+
+    Walks the dependency waves backwards from the output addresses: an instance
+    is needed when one of its results (``dest_base + r*N + i``, codegen.py:265)
+    is needed, and then every address its slots load (``slot_addresses``,
+    codegen.py:373-388) is needed.
+    """
+    import numpy as np
+
+    from .lower import compute_waves
+    from .plan import slot_addresses
+
+    need = np.zeros(int(plan.value_array_size), bool)
+    need[np.asarray(plan.outputs, np.int64)[lo:hi]] = True
+    waves = compute_waves(plan)
+    masks = {}
+    for k in sorted(range(len(plan.kernels)), key=lambda j: -waves[j]):
+        kp = plan.kernels[k]
+        n, r = kp.instances, kp.n_roots
+        if n == 0:
+            masks[k] = np.zeros(0, bool)
+            continue
+        m = need[kp.dest_base: kp.dest_base + r * n].reshape(r, n).any(axis=0)
+        masks[k] = m
+        if m.any():
+            for col in slot_addresses(plan, kp):
+                need[col[m]] = True
+    return masks
+
+
+def shard_device_plan(plan, lowered, lo: int, hi: int):
+    """(plan view, lowered view) computing only the CSR outputs [lo, hi): every launch unit keeps the
+    tiles that hold an instance of the outputs' producer cone, the gather only those outputs.  The
+    value-array layout is unchanged (addresses, index tables and the specialised kernels are the
+    full plan's), so the shard's CSR values equal the full evaluation's [lo, hi) bit for bit.
+    CSR-mode single-set calls only (run_csr / capture_csr / run_outputs_host)."""
+    import dataclasses
+
+    import numpy as np
+
+    from . import lower as L
+
+    if getattr(lowered, "csr_layout", None):
+        raise ValueError("output sharding needs the reference value-array layout (csr_layout off)")
+    if int(lowered.needs_zero) == 2:
+        raise ValueError("output sharding needs a plan without reads before writes")
+    if np.any(lowered.groups["flags"] & (L.FLAG_OPOS16 | L.FLAG_OPOS32)) or lowered.window_units:
+        raise ValueError("output sharding supports the gather output mode only")
+    masks = output_cone(plan, lo, hi)
+    by_base = {int(kp.dest_base): k for k, kp in enumerate(plan.kernels) if kp.instances}
+    tiles = np.asarray(lowered.tiles).reshape(-1, 2)
+    units = np.array(lowered.units, np.int64, copy=True)
+    keep_t, t_cur = [], 0
+    for u in range(len(units)):
+        ur = lowered.unit(u)
+        t = tiles[ur["tile_begin"]: ur["tile_end"]]
+        keep = np.zeros(len(t), bool)
+        for j, (gi, s) in enumerate(t.tolist()):
+            g = lowered.groups[gi]
+            k = by_base.get(int(g["dest_base"]))
+            if k is None:  # not a plan kernel: keep
+                keep[j] = True
+                continue
+            if g["flags"] & L.FLAG_SERIAL:
+                keep[j] = bool(masks[k].any())
+                continue
+            size = (32 * L.sop_vec(int(g["variant"])) if g["kind"] == L.KIND_SOP
+                    else ur["block_size"] * ur["variant"])
+            keep[j] = bool(masks[k][s: s + size].any())
+        kt = t[keep]
+        units[u, UNIT_TB], units[u, UNIT_TE] = t_cur, t_cur + len(kt)
+        t_cur += len(kt)
+        keep_t.append(kt)
+    new_tiles = np.concatenate(keep_t).astype(np.int32) if keep_t else np.zeros((0, 2), np.int32)
+    view = _OutputSlice(plan, lo, hi)
+    lw = dataclasses.replace(lowered, tiles=new_tiles.reshape(-1, 2), units=units,
+                             outputs=np.asarray(lowered.outputs, np.int64)[lo:hi], tiles_alt=None)
+    return view, lw
+
+
+UNIT_TB, UNIT_TE = 5, 6  # lower.UNIT_FIELDS tile_begin / tile_end

@@ -147,7 +147,18 @@ def check_tiles(dp):
             assert starts.tolist() == list(range(0, n, tile)), (u, gi)
 
 
-def _run(dp, inputs, csr: bool):
+def _tile_instances(dp, unit, gi, g, n):
+    """Instances of group ``gi`` its unit's tiles cover (a sharded tile table covers a subset)."""
+    t = dp.tiles[unit["tile_begin"]: unit["tile_end"]]
+    starts = np.sort(t[t[:, 0] == gi, 1].astype(np.int64))
+    size = 32 * L.sop_vec(int(g["variant"])) if g["kind"] == L.KIND_SOP else unit["block_size"] * unit["variant"]
+    if not starts.size:
+        return np.zeros(0, np.int64)
+    i = (starts[:, None] + np.arange(size, dtype=np.int64)[None, :]).reshape(-1)
+    return i[i < n]
+
+
+def _run(dp, inputs, csr: bool, by_tiles: bool = False):
     x = np.zeros(dp.value_array_size, np.float64)
     x[: dp.input_count] = inputs
     out = np.full(len(dp.outputs), np.nan) if csr else None
@@ -166,7 +177,7 @@ def _run(dp, inputs, csr: bool):
                 for i in range(n):
                     _tape(dp, g, x, np.array([i]), store)
                 continue
-            i = np.arange(n, dtype=np.int64)
+            i = _tile_instances(dp, unit, gi, g, n) if by_tiles else np.arange(n, dtype=np.int64)
             if g["kind"] == L.KIND_SOP:
                 nt = int(dp.sop[2 * g["sop_off"]])
                 ng = int(dp.sop[2 * g["sop_off"] + 1])
@@ -193,11 +204,12 @@ def run_values(dp, inputs) -> np.ndarray:
     return _run(dp, inputs, csr=False)[0]
 
 
-def run_csr(dp, inputs) -> np.ndarray:
-    """CSR mode: direct stores by the producing groups and copy groups, or value mode + gather."""
+def run_csr(dp, inputs, by_tiles: bool = False) -> np.ndarray:
+    """CSR mode: direct stores by the producing groups and copy groups, or value mode + gather.
+    ``by_tiles``: evaluate only the instances the tile table covers (output-sharded plans)."""
     direct = bool(np.any(dp.groups["flags"] & (L.FLAG_OPOS16 | L.FLAG_OPOS32)))
     if not direct:
-        return _run(dp, inputs, csr=False)[0][dp.outputs]
+        return _run(dp, inputs, csr=False, by_tiles=by_tiles)[0][dp.outputs]
     return _run(dp, inputs, csr=True)[1]
 
 

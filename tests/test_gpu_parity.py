@@ -333,3 +333,27 @@ def test_tile_schedules_bitwise(golden):
             assert np.array_equal(bits(got), bits(want))
     with pytest.raises(SgbError):
         dp.set_tiles(np.zeros((len(lw.tiles) + 1, 2), np.int32))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_output_shards_on_device(golden, world):
+    """One evaluation with its CSR outputs split (shard.shard_device_plan): each shard's device plan,
+    running only the tiles of its producer cone, gives the full evaluation's slice bit for bit."""
+    from paper_2110_12865_b200 import DevicePlan, lower_plan
+    from paper_2110_12865_b200.shard import shard_device_plan, shard_outputs
+
+    plan = golden.plan
+    lw = lower_plan(plan, jit_min_n=0)
+    if lw.needs_zero == 2:
+        pytest.skip("reads before writes: output sharding refuses the plan")
+    full = DevicePlan(plan, lowered=lw).run_outputs_host(golden.inputs)
+    n_out = len(plan.outputs)
+    for r in range(world):
+        lo, hi = shard_outputs(n_out, world, r)
+        if hi == lo:
+            continue
+        view, slw = shard_device_plan(plan, lw, lo, hi)
+        dp = DevicePlan(view, lowered=slw)
+        got = dp.run_csr(dp.new_values(golden.inputs)).cpu().numpy()
+        assert np.array_equal(bits(got), bits(full[lo:hi]))
+        assert np.array_equal(bits(dp.run_outputs_host(golden.inputs)), bits(full[lo:hi]))

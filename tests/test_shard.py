@@ -80,3 +80,46 @@ def test_gloo_world2_gather_equals_single_process(tmp_path, total):
                      for s in range(total)], axis=1)
     assert got.shape == want.shape
     assert np.array_equal(bits(got), bits(want))
+
+
+# -- one evaluation, output nonzeros partitioned (shard.shard_device_plan) --------------------
+
+
+@pytest.mark.parametrize("name", ["lmlt_w7", "spgemm_n60_k4", "prog_energy-hessian_4x4_tag"])
+@pytest.mark.parametrize("world", [2, 3])
+def test_output_shards_match_full_evaluation(name, world):
+    """Every rank's output cone, evaluated alone by the device-plan emulator over its filtered tile
+    table, gives the full evaluation's CSR values [lo, hi) bit for bit; the shards tile the outputs."""
+    from conftest import Golden, bits
+
+    import device_plan_emu as emu
+    from paper_2110_12865_b200 import lower_plan
+    from paper_2110_12865_b200.shard import shard_device_plan, shard_outputs
+
+    g = Golden(name)
+    lw = lower_plan(g.plan, jit=False)
+    full = emu.run_csr(lw, g.inputs)
+    n_out = len(g.plan.outputs)
+    covered = []
+    for r in range(world):
+        lo, hi = shard_outputs(n_out, world, r)
+        covered.extend(range(lo, hi))
+        view, slw = shard_device_plan(g.plan, lw, lo, hi)
+        assert len(view.outputs) == hi - lo and len(slw.outputs) == hi - lo
+        assert len(slw.tiles) <= len(lw.tiles)
+        got = emu.run_csr(slw, g.inputs, by_tiles=True)
+        assert np.array_equal(bits(got), bits(full[lo:hi]))
+    assert covered == list(range(n_out))
+
+
+def test_output_cone_shrinks_with_the_slice():
+    """On a mesh plan the cone of half the outputs is well under the whole plan."""
+    from conftest import Golden
+
+    from paper_2110_12865_b200.shard import output_cone
+
+    g = Golden("lmlt_w7")
+    n_out = len(g.plan.outputs)
+    whole = sum(int(m.sum()) for m in output_cone(g.plan, 0, n_out).values())
+    half = sum(int(m.sum()) for m in output_cone(g.plan, 0, n_out // 2).values())
+    assert 0 < half < whole
