@@ -123,3 +123,51 @@ def test_output_cone_shrinks_with_the_slice():
     whole = sum(int(m.sum()) for m in output_cone(g.plan, 0, n_out).values())
     half = sum(int(m.sum()) for m in output_cone(g.plan, 0, n_out // 2).values())
     assert 0 < half < whole
+
+
+def _split_worker(rank, world, port, result_path):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import sys
+        from pathlib import Path
+
+        root = Path(__file__).resolve().parent.parent
+        sys.path.insert(0, str(root))
+        sys.path.insert(0, str(root / "tests"))
+        import device_plan_emu as emu
+        from conftest import Golden
+
+        from paper_2110_12865_b200 import lower_plan
+        from paper_2110_12865_b200.shard import shard_device_plan, shard_outputs
+
+        g = Golden("lmlt_w7")
+        n_out = len(g.plan.outputs)
+        lo, hi = shard_outputs(n_out, world, rank)
+        _, slw = shard_device_plan(g.plan, lower_plan(g.plan, jit=False), lo, hi)
+        mine = torch.from_numpy(emu.run_csr(slw, g.inputs, by_tiles=True))
+        width = max(shard_outputs(n_out, world, r)[1] - shard_outputs(n_out, world, r)[0] for r in range(world))
+        send = torch.zeros(width, dtype=torch.float64)
+        send[: hi - lo] = mine
+        parts = [torch.empty_like(send) for _ in range(world)]
+        dist.all_gather(parts, send)
+        if rank == 0:
+            full = torch.cat([parts[r][: shard_outputs(n_out, world, r)[1] - shard_outputs(n_out, world, r)[0]]
+                              for r in range(world)])
+            np.save(result_path, full.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_output_split_equals_oracle(tmp_path):
+    """Two processes each evaluate half of one evaluation's CSR outputs from their producer cone;
+    the gathered halves equal the oracle's full evaluation bit for bit."""
+    world = 2
+    path = tmp_path / "split.npy"
+    mp.spawn(_split_worker, args=(world, _free_port(), str(path)), nprocs=world, join=True)
+    from conftest import Golden, bits
+    from oracle import oracle
+
+    g = Golden("lmlt_w7")
+    assert np.array_equal(bits(np.load(path)), bits(oracle.run_outputs(g.plan, g.inputs)))
