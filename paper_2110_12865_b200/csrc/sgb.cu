@@ -787,6 +787,7 @@ struct Unit {
   const void *jitb = nullptr;
   int64_t grid;      // single-set grid in use (blocks)
   int64_t grid_p = 0, grid_t = 0;  // specialised units: persistent grid / one block per tile
+  int64_t grid_b = 0;              // specialised units, batched kernels: persistent grid
   int64_t t0, t1;    // single-set tiles [t0, t1)
   int64_t bt0, bt1;  // batched tiles
 };
@@ -891,13 +892,13 @@ void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_
     if (batched) {
       int64_t ld_ = ld, batch_ = batch, ldo = ld_out;
       void *args[] = {&T, &tiles, &n, &x, &ld_, &batch_, &out, &ldo, &c};
-      // the batched kernels keep the persistent grid (the per-wave grid choice is tuned single-set);
-      // SGB_BATCH_GRID=tiles launches one block per batched tile instead
+      // the batched kernels run a persistent grid of their own occupancy (the per-wave grid choice is
+      // tuned single-set); SGB_BATCH_GRID=tiles launches one block per batched tile instead
       static const bool batch_tiles = [] {
         const char *e = getenv("SGB_BATCH_GRID");
         return e && !strcmp(e, "tiles");
       }();
-      const int64_t cap = batch_tiles ? blocks : (u.grid_p > 0 ? u.grid_p : u.grid);
+      const int64_t cap = batch_tiles ? blocks : (u.grid_b > 0 ? u.grid_b : u.grid);
       const int64_t grid = blocks < cap ? blocks : cap;
       cudaLaunchKernel(u.jitb, dim3((unsigned)grid), dim3(JIT_BLOCK), args, 0, s);
     } else {
@@ -1234,6 +1235,13 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       for (int64_t i = 0; i < G.n; i += bwarps) btiles.push_back(make_int2(g, (int)i));
     }
     u.bt1 = (int64_t)btiles.size();
+    if (jit && u.jitb) {  // the batched kernel's own resident capacity (not the single-set grid,
+                          // which is capped by the single-set tile count -- 256x fewer tiles)
+      int nbb = 0;
+      SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nbb, u.jitb, JIT_BLOCK, 0));
+      u.grid_b = (int64_t)(nbb > 0 ? nbb : 1) * prop.multiProcessorCount;
+      if (u.grid_b > u.bt1 - u.bt0) u.grid_b = u.bt1 - u.bt0;
+    }
     if (jit)  // as the single-set tiles (lower.py): interleave the groups' tiles by instance for L2 reuse
       std::stable_sort(btiles.begin() + u.bt0, btiles.end(), [](const int2 &a, const int2 &b) { return a.y < b.y; });
     if (u.kind == KIND_TAPE && !jit) {  // every tape word must stay inside its lane's scratch column
