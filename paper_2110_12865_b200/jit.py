@@ -36,7 +36,8 @@ import numpy as np
 from . import lower as L
 
 JIT_BLOCK = 256  # threads per block = instances per tile of a specialised unit
-BATCH_VEC = int(os.environ.get("SGB_BATCH_VEC", "4"))  # batched: value sets per lane per iteration
+BATCH_VEC = int(os.environ.get("SGB_BATCH_VEC", "8"))  # batched: value sets per lane per iteration (8: r45)
+BATCH_VEC_SMALL_TAPE = 128  # tape words up to which a unit's batched kernel uses BATCH_VEC (else <= 4)
 CACHE = Path(os.environ.get("SGB_JIT_CACHE", Path.home() / ".cache" / "sgb_jit"))
 
 _PREAMBLE = r"""
@@ -289,6 +290,9 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
     big = max(len(tapes[gi]) for gi in range(unit["group_begin"], unit["group_end"]))
     # register cap (blocks per SM): huge templates run best uncapped -- spills cost more than occupancy
     min_blocks = int(os.environ.get("SGB_JIT_MINBLOCKS", "0"))  # 2 measured 2.7x slower on C3 (r24)
+    # batched value sets per lane: 8 for small templates (C5: 2.90 -> 2.47 ms, r45); big templates keep
+    # 4 (their register file is full already, and the body is compiled once per value set)
+    bvec = BATCH_VEC if big <= BATCH_VEC_SMALL_TAPE else min(BATCH_VEC, 4)
     for batched in (False, True):
         if batched:
             head = [f'extern "C" __global__ void __launch_bounds__({JIT_BLOCK}) sgb_tape_b{u}(',
@@ -297,7 +301,7 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
                     "  for (i64 t = blockIdx.x; t < n_tiles; t += gridDim.x) {",
                     "    const int2 tl = tiles[t];",
                     "    const i64 i = (i64)tl.y + (threadIdx.x >> 5);",
-                    f"    for (i64 b = threadIdx.x & 31; b < batch; b += {32 * BATCH_VEC}) {{",
+                    f"    for (i64 b = threadIdx.x & 31; b < batch; b += {32 * bvec}) {{",
                     "    switch (tl.x) {"]
         else:
             bounds = f"{JIT_BLOCK}, {min_blocks}" if min_blocks > 1 else f"{JIT_BLOCK}"
@@ -320,7 +324,7 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
                 out.append(f"      if (i >= {int(rec['n'])}LL) break;")
             if rec["flags"] & L.FLAG_CSR_ONLY:
                 out.append("      if (!csr) break;")
-            body = (group_batch_body(dp, gi, tapes[gi], imms[gi], BATCH_VEC) if batched else
+            body = (group_batch_body(dp, gi, tapes[gi], imms[gi], bvec) if batched else
                     group_vec_body(dp, gi, tapes[gi], imms[gi], vec, "i", JIT_BLOCK, stage=staged))
             out += ["      " + ln for ln in body]
             if staged:

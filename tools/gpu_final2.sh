@@ -8,7 +8,7 @@ export SGB_PLAN_CACHE=/tmp/sgb_plan_cache_$TAG
 echo "smoke rc=$?" >> $OUT/status.txt
 ( time timeout 1500 python -m pytest tests -m gpu -x -q ) > $OUT/pytest_gpu.log 2>&1
 echo "pytest rc=$?" >> $OUT/status.txt
-for C in c1 c5; do
+for C in c1 c5 c3 c4; do
   timeout 900 python bench.py --config $C --steps 10 --warmup 3 > $OUT/bench_$C.json 2> $OUT/bench_$C.err
   echo "bench $C rc=$?" >> $OUT/status.txt
 done
