@@ -800,6 +800,9 @@ struct sgb_plan {
   int n_groups = 0, n_waves = 0, csr_waves = 0, needs_zero = 2;
   bool ws_dirty = false;  // the workspace holds sg_run results (slots CSR mode never writes)
   std::vector<Unit> units;
+  std::vector<std::vector<int>> wave_units;  // per wave: indices into units, largest first
+  std::vector<int64_t> group_n;              // host copy of every group's instance count
+  std::vector<int2> h_tiles;                 // host copy of the single-set tile table in use
   Tables T{};
   sgb_group *d_groups = nullptr;
   int2 *d_tiles = nullptr, *d_btiles = nullptr;
@@ -1297,6 +1300,8 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
         u.grid_t = u.t1 - u.t0 < 0x7fffffffLL ? u.t1 - u.t0 : 0x7fffffffLL;
         if (tiles_default && u.grid_t > 0) u.grid = u.grid_t;
       }
+    p->wave_units.assign(max_wave + 1, {});
+    for (int k = 0; k < (int)p->units.size(); ++k) p->wave_units[p->units[k].wave].push_back(k);
     const int n_aux = max_units - 1 < 8 ? max_units - 1 : 8;
     SGB_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
     for (int k = 0; k < n_aux; ++k) {
@@ -1308,6 +1313,9 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       p->ev_join.push_back(e);
     }
   }
+  p->group_n.resize(d->n_groups);
+  for (int g = 0; g < d->n_groups; ++g) p->group_n[g] = d->groups[g].n;
+  p->h_tiles.assign(reinterpret_cast<const int2 *>(d->tiles), reinterpret_cast<const int2 *>(d->tiles) + d->n_tiles);
   std::vector<uint32_t> outputs32(d->outputs, d->outputs + d->n_outputs);
   for (int g = 0; g < d->n_groups; ++g)
     if (d->groups[g].flags & (FLAG_OPOS16 | FLAG_OPOS32)) p->direct_csr = true;
@@ -1384,10 +1392,12 @@ int sgb_plan_create(const sgb_plan_desc *d, int device, sgb_plan **out) {
 // stream, the others on the plan's aux streams forked from / joined back into it.
 static int launch_wave(sgb_plan *p, int wave, double *x, int64_t ld, int64_t batch, bool batched, double *out,
                        int64_t ld_out, bool csr, cudaStream_t s) {
-  const Unit *us[64];
-  int n = 0;
-  for (const Unit &u : p->units)
-    if (u.wave == wave && (csr || !(u.flags & UNIT_CSR_ONLY)) && n < 64) us[n++] = &u;
+  if (wave < 0 || wave >= (int)p->wave_units.size()) return 0;
+  std::vector<const Unit *> us;
+  us.reserve(p->wave_units[wave].size());
+  for (int k : p->wave_units[wave])
+    if (csr || !(p->units[k].flags & UNIT_CSR_ONLY)) us.push_back(&p->units[k]);
+  const int n = (int)us.size();
   if (n == 0) return 0;
   const int k_aux = n - 1 < (int)p->aux.size() ? n - 1 : (int)p->aux.size();
   if (k_aux > 0) SGB_CUDA(cudaEventRecord(p->ev_fork, s));
@@ -1592,8 +1602,10 @@ int sgb_run_outputs_host_many(sgb_plan *p, int64_t n_sets, const double *inputs,
   if (!p->d2h_stream) SGB_CUDA(cudaStreamCreateWithFlags(&p->d2h_stream, cudaStreamNonBlocking));
   if (n_sets > 1 && !p->d_x2 && p->vas) {
     SGB_CUDA(cudaMalloc((void **)&p->d_x2, sizeof(double) * (size_t)p->vas));
-    // zeroed on the evaluation stream, so ordered before set 1 evaluates (codegen.py:419)
-    SGB_CUDA(cudaMemsetAsync(p->d_x2, 0, sizeof(double) * (size_t)p->vas, p->ws_stream));
+    // zeroed on the evaluation stream, so ordered before set 1 evaluates (codegen.py:419); only
+    // [n_in, vas): set 1's inputs land in [0, n_in) on the H2D stream, unordered with this memset
+    if (p->vas > p->n_in)
+      SGB_CUDA(cudaMemsetAsync(p->d_x2 + p->n_in, 0, sizeof(double) * (size_t)(p->vas - p->n_in), p->ws_stream));
   }
   if (n_sets > 1 && !p->d_out2) SGB_CUDA(cudaMalloc((void **)&p->d_out2, sizeof(double) * (size_t)p->n_out));
   double *xs[2] = {p->d_x, p->d_x2}, *os[2] = {p->d_out, p->d_out2};
@@ -1642,10 +1654,25 @@ int sgb_run_outputs_host_many(sgb_plan *p, int64_t n_sets, const double *inputs,
 int sgb_plan_set_tiles(sgb_plan *p, const int32_t *tiles, int64_t n_tiles) {
   if (!p || (!tiles && n_tiles)) return fail(-1, "sgb_plan_set_tiles: null argument");
   if (n_tiles != p->n_tiles) return fail(-1, "sgb_plan_set_tiles: tile count differs from the plan's");
+  const int2 *nt = reinterpret_cast<const int2 *>(tiles);
+  for (const Unit &u : p->units) {  // each unit's range: the same multiset of its own tiles, reordered
+    if (u.flags & UNIT_WINDOW) continue;
+    for (int64_t t = u.t0; t < u.t1; ++t)
+      if (nt[t].x < u.g0 || nt[t].x >= u.g1 || nt[t].y < 0 || (int64_t)nt[t].y >= p->group_n[nt[t].x])
+        return fail(-1, "sgb_plan_set_tiles: tile " + std::to_string(t) + " outside its unit's groups");
+    auto key = [](const int2 &a, const int2 &b) { return a.x != b.x ? a.x < b.x : a.y < b.y; };
+    std::vector<int2> a(p->h_tiles.begin() + u.t0, p->h_tiles.begin() + u.t1), b(nt + u.t0, nt + u.t1);
+    std::sort(a.begin(), a.end(), key);
+    std::sort(b.begin(), b.end(), key);
+    for (size_t k = 0; k < a.size(); ++k)
+      if (a[k].x != b[k].x || a[k].y != b[k].y)
+        return fail(-1, "sgb_plan_set_tiles: unit " + std::to_string(u.index) + " range is not a permutation of its tiles");
+  }
   std::lock_guard<std::mutex> lk(p->run_mu);
   SGB_CUDA(cudaSetDevice(p->device));
   SGB_CUDA(cudaDeviceSynchronize());
   if (n_tiles) SGB_CUDA(cudaMemcpy(p->d_tiles, tiles, sizeof(int2) * (size_t)n_tiles, cudaMemcpyHostToDevice));
+  p->h_tiles.assign(nt, nt + n_tiles);
   return 0;
 }
 

@@ -36,9 +36,11 @@ import numpy as np
 from . import lower as L
 
 JIT_BLOCK = 256  # threads per block = instances per tile of a specialised unit
-BATCH_VEC = int(os.environ.get("SGB_BATCH_VEC", "8"))  # batched: value sets per lane per iteration (8: r45)
+BATCH_VEC = 8  # batched: value sets per lane per iteration (8: r45)
 BATCH_VEC_SMALL_TAPE = 128  # tape words up to which a unit's batched kernel uses BATCH_VEC (else <= 4)
-CACHE = Path(os.environ.get("SGB_JIT_CACHE", Path.home() / ".cache" / "sgb_jit"))
+# cubin cache, keyed by source + NVRTC options: in-tree by default so cubins built on the CPU host
+# (__graft_entry__.build) travel with the repository to the GPU box
+CACHE = Path(os.environ.get("SGB_JIT_CACHE", Path(__file__).resolve().parent / "_jit_cache"))
 
 _PREAMBLE = r"""
 typedef unsigned int u32;
@@ -364,19 +366,30 @@ def available() -> bool:
         return False
 
 
+NVRTC_OPTS = (b"--gpu-architecture=sm_100a", b"-fmad=false", b"-std=c++17", b"-default-device", b"-lineinfo",
+              b"--extra-device-vectorization")
+stats = {"hits": 0, "compiles": 0, "compile_s": 0.0}
+
+
+def cache_key(src: str) -> str:
+    return hashlib.sha1(b"\0".join(NVRTC_OPTS) + b"\0" + src.encode()).hexdigest()
+
+
 def compile_cubin(src: str, name: str = "sgb_tape.cu") -> bytes:
-    """NVRTC -> sm_100a cubin (no GPU needed); cached by source hash."""
-    key = hashlib.sha1(src.encode()).hexdigest()
-    path = CACHE / f"{key}.cubin"
+    """NVRTC -> sm_100a cubin (no GPU needed); cached by source + options hash."""
+    import time
+
+    path = CACHE / f"{cache_key(src)}.cubin"
     if path.exists():
+        stats["hits"] += 1
         return path.read_bytes()
+    t0 = time.perf_counter()
     lib = _lib()
     prog = ctypes.c_void_p()
     rc = lib.nvrtcCreateProgram(ctypes.byref(prog), src.encode(), name.encode(), 0, None, None)
     if rc:
         raise RuntimeError(f"nvrtcCreateProgram failed ({rc})")
-    opts = [b"--gpu-architecture=sm_100a", b"-fmad=false", b"-std=c++17", b"-default-device", b"-lineinfo",
-            b"--extra-device-vectorization"]
+    opts = list(NVRTC_OPTS)
     arr = (ctypes.c_char_p * len(opts))(*opts)
     rc = lib.nvrtcCompileProgram(prog, len(opts), arr)
     if rc:
@@ -392,6 +405,8 @@ def compile_cubin(src: str, name: str = "sgb_tape.cu") -> bytes:
     lib.nvrtcGetCUBIN(prog, buf)
     lib.nvrtcDestroyProgram(ctypes.byref(prog))
     cubin = buf.raw
+    stats["compiles"] += 1
+    stats["compile_s"] += time.perf_counter() - t0
     try:
         CACHE.mkdir(parents=True, exist_ok=True)
         tmp = path.with_suffix(f".{os.getpid()}.tmp")

@@ -36,11 +36,6 @@ import numpy as np
 
 from .plan import EXACT_OPS, OpKind, reachable, slot_addresses, unique_addresses
 
-# device op codes (csrc/sgb_device.cuh keeps the same numbering)
-T_ADD, T_SUB, T_MUL, T_DIV, T_NEG, T_SQRT = 2, 3, 4, 5, 6, 7
-T_SIN, T_COS, T_EXP, T_LOG, T_POW, T_SEL = 8, 9, 10, 11, 12, 13
-T_IMM, T_ST = 20, 21
-
 KIND_TAPE, KIND_SOP = 0, 1
 FLAG_SELFREF, FLAG_INTERLEAVED, FLAG_SERIAL, FLAG_EXACT, FLAG_STREAM, FLAG_W16 = 1, 2, 4, 8, 16, 32
 FLAG_AFFINE0 = 64  # index column 0 is a0_base + a0_stride * i: no table read

@@ -1,0 +1,77 @@
+"""Which lowerings the GPU parity suite runs, and the NVRTC pre-compilation of their cubins.
+
+The specialised kernels (paper_2110_12865_b200/jit.py) are compiled by NVRTC
+when a plan is lowered.  NVRTC needs no GPU, so ``warm()`` -- called by
+``__graft_entry__.build()`` on the CPU host -- compiles every cubin the GPU
+suite needs into the in-tree cache (jit.CACHE), which travels with the
+repository to the GPU box: ``pytest -m gpu`` on a cold box then spends its
+time on the GPU, not in NVRTC.
+
+Default lowering (``jit_min_n`` = 4096) runs for every fixture; every group
+specialised (``jit_min_n=0``) and the CSR layout (``relayout="all"``) run for
+the subsets below, which cover every template shape in the fixtures (sums of
+products, multi-root element templates, transcendental / select / POW tapes,
+interleaved and coherent index forms).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+
+# every group specialised (jit_min_n = 0): specialised == hand-written, tile schedules, shards
+JIT_CASES = ["lmlt_w7", "lmlt_w12", "prog_energy-hessian_4x4_tag", "transc37", "transc37_nosimp",
+             "toy256_interleaved", "tagged_pair", "acc9_lpow3_simp", "spgemm_n60_k4", "selfref", "coord96",
+             "select_edge", "prog_cotan_4x4_tag", "cli_lpow4_simp", "fem_nh_m1", "arap_w3"]
+# CSR layout (multi-root groups stored instance-major): every fixture with a relayout candidate
+# at jit_min_n = 0 plus representatives without one
+LAYOUT_CASES = ["fem_nh_m1", "fem_nh_m2", "prog_energy-hessian_4x4_tag", "arap_w3", "arap_w5", "prog_cotan_4x4_tag",
+                "lmlt_w7", "transc37", "selfref", "toy256_interleaved"]
+
+
+def lowering_specs(names: list[str]) -> list[tuple[str, tuple]]:
+    specs = [(n, ()) for n in names]
+    specs += [(n, (("jit_min_n", 0),)) for n in JIT_CASES]
+    specs += [(n, (("jit_min_n", 0), ("relayout", r))) for n in LAYOUT_CASES for r in ("all", "auto")]
+    return specs
+
+
+def _lower_one(spec):
+    name, kw = spec
+    sys.path.insert(0, str(ROOT))
+    sys.path.insert(0, str(ROOT / "tests"))
+    from conftest import Golden
+    from paper_2110_12865_b200 import jit
+    from paper_2110_12865_b200.lower import lower_plan
+
+    lower_plan(Golden(name).plan, **dict(kw))
+    return jit.stats["compiles"]
+
+
+def warm(processes: int | None = None) -> int:
+    """Compile every cubin the GPU suite lowers (cache hits are free); returns NVRTC compiles."""
+    import multiprocessing as mp
+
+    sys.path.insert(0, str(ROOT / "tests"))
+    from conftest import golden_names
+    from paper_2110_12865_b200 import jit
+
+    if not jit.available():
+        return 0
+    specs = lowering_specs(golden_names())
+    # biggest first so the long compiles overlap
+    specs.sort(key=lambda s: -sum(p.stat().st_size for p in (ROOT / "tests" / "golden" / s[0]).iterdir()))
+    procs = processes or min(len(specs), os.cpu_count() or 1)
+    with mp.get_context("spawn").Pool(procs) as pool:
+        return sum(pool.map(_lower_one, specs, chunksize=1))
+
+
+if __name__ == "__main__":
+    import time
+
+    t0 = time.perf_counter()
+    n = warm()
+    print(f"warm: {n} NVRTC compiles in {time.perf_counter() - t0:.1f}s")

@@ -4,18 +4,24 @@ Bar: bit-exact (uint64 compare of the FULL value array) for
 plans whose templates use only EXACT_OPS (codegen.py:43-53) and POW k=2;
 SIN/COS/EXP/LOG/POW k>=3 within |g - o| <= 1e-12 * max(1, |g|, |o|)
 (cli.py:118-122) because CUDA's libm is not glibc.
+
+Cost control (a cold B200 box runs this file in a few minutes): lowerings and
+device plans are shared per (fixture, lowering) through conftest.lowered /
+conftest.device_plan, every NVRTC cubin is pre-compiled by
+__graft_entry__.build() (tests/gpu_cases.py), autotuning is off except in its
+own test, and the every-group-specialised / CSR-layout lowerings run on the
+subsets of tests/gpu_cases.py.  The most informative tests run first.
 """
 
 import numpy as np
 import pytest
 
-from conftest import bits
+from conftest import bits, device_plan, golden_case, lowered
+from gpu_cases import JIT_CASES, LAYOUT_CASES
 
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-12
-WINDOW_CASES = {"lmlt_w7", "lmlt_w12", "spgemm_n60_k4", "toy256", "toy256_interleaved", "cli_cotan_simp",
-                "prog_cotan_4x4_tag", "prog_energy-hessian_4x4_tag", "transc37", "tagged_pair"}
 
 
 def _close(got, want):
@@ -33,6 +39,11 @@ def check(got, golden):
         assert _close(got, golden.values)
 
 
+def cmp_outputs(golden):
+    want = golden.outputs
+    return (lambda g: np.array_equal(bits(g), bits(want))) if golden.exact else (lambda g: _close(g, want))
+
+
 def test_compile_plan_values(golden):
     from paper_2110_12865_b200 import compile_plan
 
@@ -41,211 +52,23 @@ def test_compile_plan_values(golden):
     check(x, golden)
     # the native library that ran is the in-tree one
     assert run.library_path.name == "libsgb.so"
+    assert np.array_equal(bits(run.outputs(golden.inputs)), bits(x[np.asarray(golden.plan.outputs, np.int64)]))
 
 
-def test_interpret_plan_outputs(golden):
-    from paper_2110_12865_b200 import interpret_plan
-
-    res = interpret_plan(golden.plan, golden.inputs, check_schedule=True)
-    check(res.values, golden)
-    if golden.exact and golden.meta["oracle_bitwise"]:
-        assert np.array_equal(bits(res.outputs), bits(golden.oracle))
-    assert res.violations == golden.meta["violations"]
-
-
-def test_outputs_only_host_path(golden):
-    from paper_2110_12865_b200 import compile_plan
-
-    run = compile_plan(golden.plan)
-    out = run.outputs(golden.inputs)
-    want = golden.outputs
-    if golden.exact:
-        assert np.array_equal(bits(out), bits(want))
-    else:
-        assert _close(out, want)
-
-
-def test_device_resident_run_on_torch(golden):
-    import torch
-
-    from paper_2110_12865_b200 import DevicePlan
-
-    dp = DevicePlan(golden.plan)
-    x = dp.new_values(golden.inputs)
-    dp.run_values(x)
-    out = dp.gather_outputs(x)
-    torch.cuda.synchronize()
-    check(x.cpu().numpy(), golden)
-    assert out.shape[0] == len(golden.plan.outputs)
-
-
-@pytest.mark.parametrize("mode", ["gather", "window", "direct", "interpreter"])
-def test_csr_mode(golden, mode):
-    """sgb_run_csr: value waves + gather; CSR windows (last-wave outputs assembled in shared memory,
-    coalesced stores); direct scattered stores; the hand-written kernels only (gather)."""
-    import torch
-
-    from paper_2110_12865_b200 import DevicePlan, lower_plan
-
-    if mode == "window" and golden.name not in WINDOW_CASES:
-        pytest.skip("CSR windows: representative subset (each case compiles its own window kernel)")
-    kw = {"gather": dict(csr_window=False), "window": dict(csr_window=True), "direct": dict(direct_csr=True),
-          "interpreter": dict(jit=False)}[mode]
-    dp = DevicePlan(golden.plan, lowered=lower_plan(golden.plan, **kw))
-    x = dp.new_values(golden.inputs)
-    out = torch.full((len(golden.plan.outputs),), float("nan"), dtype=torch.float64, device=x.device)
-    dp.run_csr(x, out)
-    first = out.cpu().numpy().copy()
-    if dp.lowered.needs_zero != 2:  # re-running on the same buffer is valid unless reads precede writes
-        dp.run_csr(x, out)
-    torch.cuda.synchronize()
-    want = golden.outputs
-    for got in (first, out.cpu().numpy()):
-        if golden.exact:
-            assert np.array_equal(bits(got), bits(want))
-        else:
-            assert _close(got, want)
-
-
-JIT_CASES = ["lmlt_w7", "lmlt_w12", "prog_energy-hessian_4x4_tag", "transc37", "transc37_nosimp",
-             "toy256_interleaved", "tagged_pair", "acc9_lpow3_simp", "spgemm_n60_k4", "selfref", "coord96",
-             "select_edge", "prog_cotan_4x4_tag", "cli_lpow4_simp"]
-
-
-@pytest.mark.parametrize("name", JIT_CASES)
-@pytest.mark.parametrize("batch", [0, 5, 64])
-def test_specialised_kernels_match_hand_written(name, batch):
-    """Every group specialised (jit.py, jit_min_n=0) == the hand-written kernels only, bit for bit,
-    single value set and batched."""
-    import torch
-
-    from conftest import Golden
-    from paper_2110_12865_b200 import DevicePlan, lower_plan
-
-    golden = Golden(name)
-    plan = golden.plan
-    rng = np.random.default_rng(batch)
-    ins = rng.uniform(0.5, 2.0, (max(batch, 1), plan.input_count))
-    ins[0] = golden.inputs
-    outs = []
-    for jit in (False, True):
-        dp = DevicePlan(plan, lowered=lower_plan(plan, jit=jit, jit_min_n=0))
-        if batch:
-            X = torch.zeros((plan.value_array_size, batch), dtype=torch.float64, device="cuda")
-            X[: plan.input_count] = torch.from_numpy(ins.T.copy()).cuda()
-            dp.run_batch(X)
-            o = dp.run_batch_csr(torch.where(torch.arange(plan.value_array_size, device="cuda")[:, None]
-                                             < plan.input_count, X, torch.zeros_like(X)))
-            outs.append((X.cpu().numpy(), o.cpu().numpy()))
-        else:
-            x = dp.new_values(golden.inputs)
-            dp.run_values(x)
-            outs.append((x.cpu().numpy(), dp.run_csr(dp.new_values(golden.inputs)).cpu().numpy()))
-        torch.cuda.synchronize()
-    if not batch:
-        check(outs[1][0], golden)
-    assert np.array_equal(bits(outs[0][0]), bits(outs[1][0]))
-    assert np.array_equal(bits(outs[0][1]), bits(outs[1][1]))
-
-
-def test_run_wave_by_wave_equals_run(golden):
-    import torch
-
-    from paper_2110_12865_b200 import DevicePlan
-
-    dp = DevicePlan(golden.plan)
-    x = dp.new_values(golden.inputs)
-    for w in range(dp.launches):
-        dp.run_wave(x, w)
-    x2 = dp.new_values(golden.inputs)
-    out = torch.empty(len(golden.plan.outputs), dtype=torch.float64, device=x.device)
-    for w in range(dp.csr_launches):
-        dp.run_wave(x2, w, out=out)
-    torch.cuda.synchronize()
-    check(x.cpu().numpy(), golden)
-    assert np.array_equal(bits(out.cpu().numpy()), bits(x.cpu().numpy()[np.asarray(golden.plan.outputs, np.int64)]))
-
-
-@pytest.mark.parametrize("batch", [1, 5, 64])
-def test_batched_matches_single(golden, batch):
-    """B independent value sets in one pass == B single evaluations."""
-    import torch
-
-    from oracle import oracle
-    from paper_2110_12865_b200 import DevicePlan
-
-    plan = golden.plan
-    dp = DevicePlan(plan)
-    rng = np.random.default_rng(batch)
-    ins = rng.uniform(0.5, 2.0, (batch, plan.input_count))
-    ins[0] = golden.inputs
-    X = torch.zeros((plan.value_array_size, batch), dtype=torch.float64, device="cuda")
-    X[: plan.input_count] = torch.from_numpy(ins.T.copy()).cuda()
-    dp.run_batch(X)
-    got = X.cpu().numpy()
-    check(got[:, 0], golden)
-    for b in range(1, min(batch, 4)):
-        want = oracle.run_values(plan, ins[b])
-        if golden.exact:
-            assert np.array_equal(bits(got[:, b]), bits(want))
-        else:
-            assert _close(got[:, b], want)
-    outs = dp.gather_outputs_batch(X).cpu().numpy()
-    assert np.array_equal(bits(outs[:, 0]), bits(got[np.asarray(plan.outputs, np.int64), 0]))
-    # batched CSR mode on a fresh buffer == the gathered outputs of the value-mode run
-    X2 = torch.zeros_like(X)
-    X2[: plan.input_count] = torch.from_numpy(ins.T.copy()).cuda()
-    csr = dp.run_batch_csr(X2).cpu().numpy()
-    assert np.array_equal(bits(csr), bits(outs))
-
-
-def test_wrong_input_length_raises():
-    from conftest import Golden
-    from paper_2110_12865_b200 import compile_plan, interpret_plan
-
-    g = Golden("toy256")
-    with pytest.raises(ValueError):
-        interpret_plan(g.plan, [1.0, 2.0])
-    run = compile_plan(g.plan)
-    with pytest.raises(ValueError):
-        run(np.zeros(3))
-
-
-@pytest.mark.parametrize("name", ["lmlt_w12", "spgemm_n60_k4", "prog_energy-hessian_4x4_tag", "fem_nh_m2", "arap_w5"])
-def test_cuda_graph_replay_equals_run(name):
-    """capture_csr: a replayed CUDA graph of one evaluation (all units, aux streams, gather) == sgb_run_csr."""
-    import torch
-
-    from conftest import Golden
-    from paper_2110_12865_b200 import DevicePlan
-
-    g = Golden(name)
-    dp = DevicePlan(g.plan)
-    x = dp.new_values(g.inputs)
-    out = torch.empty(len(g.plan.outputs), dtype=torch.float64, device=x.device)
-    want = dp.run_csr(dp.new_values(g.inputs)).cpu().numpy()
-    graph = dp.capture_csr(x, out)
-    out.fill_(float("nan"))
-    graph.replay()
-    graph.replay()
-    torch.cuda.synchronize()
-    assert np.array_equal(bits(out.cpu().numpy()), bits(want))
-
-
+@pytest.mark.parametrize("name", LAYOUT_CASES)
 @pytest.mark.parametrize("relayout", ["all", "auto"])
-def test_csr_layout(golden, relayout):
+def test_csr_layout(name, relayout):
     """CSR layout (multi-root groups stored instance-major, lower.choose_relayout): CSR values equal the
     reference's, on the device path, the captured graph, the host-buffer path and batched; value-mode
     calls are refused (the value array is permuted)."""
     import torch
 
-    from paper_2110_12865_b200 import DevicePlan, SgbError, lower_plan
+    from paper_2110_12865_b200 import SgbError
 
+    golden = golden_case(name)
     plan = golden.plan
-    lw = lower_plan(plan, jit_min_n=0, relayout=relayout)
-    dp = DevicePlan(plan, lowered=lw)
-    want = golden.outputs
-    cmp = (lambda g: np.array_equal(bits(g), bits(want))) if golden.exact else (lambda g: _close(g, want))
+    dp = device_plan(name, jit_min_n=0, relayout=relayout)
+    cmp = cmp_outputs(golden)
     x = dp.new_values(golden.inputs)
     out = torch.full((len(plan.outputs),), float("nan"), dtype=torch.float64, device=x.device)
     dp.run_csr(x, out)
@@ -276,12 +99,11 @@ def test_csr_layout(golden, relayout):
 def test_outputs_host_many(golden):
     """The pipelined host-buffer stream (sgb_run_outputs_host_many): every set equals the reference's
     values, distinct value sets stay distinct (set k's inputs scaled), one repeated input set works."""
-    from paper_2110_12865_b200 import DevicePlan
+    import torch
 
     plan = golden.plan
-    dp = DevicePlan(plan)
-    want = golden.outputs
-    cmp = (lambda g: np.array_equal(bits(g), bits(want))) if golden.exact else (lambda g: _close(g, want))
+    dp = device_plan(golden.name)
+    cmp = cmp_outputs(golden)
     n = 5
     ins = np.stack([golden.inputs] * n)
     ins[1] *= 1.5
@@ -297,8 +119,6 @@ def test_outputs_host_many(golden):
         assert cmp(rep[k])
     assert cmp(dp.run_outputs_host(golden.inputs))  # the single-set path after the stream
     # chunked batched stream: 3 chunks of 2 value sets
-    import torch
-
     sets = np.stack([golden.inputs * f for f in (1.0, 1.5, 0.75, 1.25, 1.0, 2.0)])  # (6, n_in)
     hin = torch.from_numpy(np.ascontiguousarray(sets.reshape(3, 2, -1).transpose(0, 2, 1)))
     hout = torch.empty((3, len(plan.outputs), 2), dtype=torch.float64)
@@ -307,19 +127,172 @@ def test_outputs_host_many(golden):
         assert np.array_equal(bits(hout[k // 2, :, k % 2].numpy()), bits(dp.run_outputs_host(sets[k])))
 
 
-def test_tile_schedules_bitwise(golden):
-    """Both tile schedules lower_plan offers (instance / fraction interleave of multi-group specialised
-    units) give the same bits; sgb_plan_set_tiles refuses a table of another length."""
+def test_interpret_plan_outputs(golden):
+    from paper_2110_12865_b200 import interpret_plan
+
+    res = interpret_plan(golden.plan, golden.inputs, check_schedule=True, device_plan=device_plan(golden.name))
+    check(res.values, golden)
+    if golden.exact and golden.meta["oracle_bitwise"]:
+        assert np.array_equal(bits(res.outputs), bits(golden.oracle))
+    assert res.violations == golden.meta["violations"]
+
+
+def test_device_resident_run_on_torch(golden):
     import torch
 
-    from paper_2110_12865_b200 import DevicePlan, SgbError, lower_plan
+    dp = device_plan(golden.name)
+    x = dp.new_values(golden.inputs)
+    dp.run_values(x)
+    out = dp.gather_outputs(x)
+    torch.cuda.synchronize()
+    check(x.cpu().numpy(), golden)
+    assert np.array_equal(bits(out.cpu().numpy()), bits(x.cpu().numpy()[np.asarray(golden.plan.outputs, np.int64)]))
+
+
+@pytest.mark.parametrize("mode", ["gather", "direct", "interpreter"])
+def test_csr_mode(golden, mode):
+    """sgb_run_csr: value waves + gather; direct scattered stores; the hand-written kernels only."""
+    import torch
+
+    kw = {"gather": {}, "direct": dict(direct_csr=True), "interpreter": dict(jit=False)}[mode]
+    dp = device_plan(golden.name, **kw)
+    x = dp.new_values(golden.inputs)
+    out = torch.full((len(golden.plan.outputs),), float("nan"), dtype=torch.float64, device=x.device)
+    dp.run_csr(x, out)
+    first = out.cpu().numpy().copy()
+    if dp.lowered.needs_zero != 2:  # re-running on the same buffer is valid unless reads precede writes
+        dp.run_csr(x, out)
+    torch.cuda.synchronize()
+    cmp = cmp_outputs(golden)
+    for got in (first, out.cpu().numpy()):
+        assert cmp(got)
+
+
+@pytest.mark.parametrize("name", JIT_CASES)
+@pytest.mark.parametrize("batch", [0, 5, 64, 300])
+def test_specialised_kernels_match_hand_written(name, batch):
+    """Every group specialised (jit.py, jit_min_n=0) == the hand-written kernels only, bit for bit,
+    single value set and batched (300 value sets: the batched kernels' lane loop runs twice)."""
+    import torch
+
+    golden = golden_case(name)
+    plan = golden.plan
+    rng = np.random.default_rng(batch)
+    ins = rng.uniform(0.5, 2.0, (max(batch, 1), plan.input_count))
+    ins[0] = golden.inputs
+    outs = []
+    for kw in (dict(jit=False), dict(jit_min_n=0)):
+        dp = device_plan(name, **kw)
+        if batch:
+            X = torch.zeros((plan.value_array_size, batch), dtype=torch.float64, device="cuda")
+            X[: plan.input_count] = torch.from_numpy(ins.T.copy()).cuda()
+            dp.run_batch(X)
+            o = dp.run_batch_csr(torch.where(torch.arange(plan.value_array_size, device="cuda")[:, None]
+                                             < plan.input_count, X, torch.zeros_like(X)))
+            outs.append((X.cpu().numpy(), o.cpu().numpy()))
+        else:
+            x = dp.new_values(golden.inputs)
+            dp.run_values(x)
+            outs.append((x.cpu().numpy(), dp.run_csr(dp.new_values(golden.inputs)).cpu().numpy()))
+        torch.cuda.synchronize()
+    if not batch:
+        check(outs[1][0], golden)
+    assert np.array_equal(bits(outs[0][0]), bits(outs[1][0]))
+    assert np.array_equal(bits(outs[0][1]), bits(outs[1][1]))
+
+
+def test_run_wave_by_wave_equals_run(golden):
+    import torch
+
+    dp = device_plan(golden.name)
+    x = dp.new_values(golden.inputs)
+    for w in range(dp.launches):
+        dp.run_wave(x, w)
+    x2 = dp.new_values(golden.inputs)
+    out = torch.empty(len(golden.plan.outputs), dtype=torch.float64, device=x.device)
+    for w in range(dp.csr_launches):
+        dp.run_wave(x2, w, out=out)
+    torch.cuda.synchronize()
+    check(x.cpu().numpy(), golden)
+    assert np.array_equal(bits(out.cpu().numpy()), bits(x.cpu().numpy()[np.asarray(golden.plan.outputs, np.int64)]))
+
+
+@pytest.mark.parametrize("batch", [1, 5, 64])
+def test_batched_matches_single(golden, batch):
+    """B independent value sets in one pass == B single evaluations."""
+    import torch
+
+    from oracle import oracle
 
     plan = golden.plan
-    lw = lower_plan(plan, jit_min_n=0)
-    dp = DevicePlan(plan, lowered=lw)
+    dp = device_plan(golden.name)
+    rng = np.random.default_rng(batch)
+    ins = rng.uniform(0.5, 2.0, (batch, plan.input_count))
+    ins[0] = golden.inputs
+    X = torch.zeros((plan.value_array_size, batch), dtype=torch.float64, device="cuda")
+    X[: plan.input_count] = torch.from_numpy(ins.T.copy()).cuda()
+    dp.run_batch(X)
+    got = X.cpu().numpy()
+    check(got[:, 0], golden)
+    for b in range(1, min(batch, 4)):
+        want = oracle.run_values(plan, ins[b])
+        if golden.exact:
+            assert np.array_equal(bits(got[:, b]), bits(want))
+        else:
+            assert _close(got[:, b], want)
+    outs = dp.gather_outputs_batch(X).cpu().numpy()
+    assert np.array_equal(bits(outs[:, 0]), bits(got[np.asarray(plan.outputs, np.int64), 0]))
+    # batched CSR mode on a fresh buffer == the gathered outputs of the value-mode run
+    X2 = torch.zeros_like(X)
+    X2[: plan.input_count] = torch.from_numpy(ins.T.copy()).cuda()
+    csr = dp.run_batch_csr(X2).cpu().numpy()
+    assert np.array_equal(bits(csr), bits(outs))
+
+
+def test_wrong_input_length_raises():
+    from paper_2110_12865_b200 import compile_plan, interpret_plan
+
+    g = golden_case("toy256")
+    with pytest.raises(ValueError):
+        interpret_plan(g.plan, [1.0, 2.0])
+    run = compile_plan(g.plan)
+    with pytest.raises(ValueError):
+        run(np.zeros(3))
+
+
+@pytest.mark.parametrize("name", ["lmlt_w12", "spgemm_n60_k4", "prog_energy-hessian_4x4_tag", "fem_nh_m2", "arap_w5"])
+def test_cuda_graph_replay_equals_run(name):
+    """capture_csr: a replayed CUDA graph of one evaluation (all units, aux streams, gather) == sgb_run_csr."""
+    import torch
+
+    g = golden_case(name)
+    dp = device_plan(name)
+    x = dp.new_values(g.inputs)
+    out = torch.empty(len(g.plan.outputs), dtype=torch.float64, device=x.device)
+    want = dp.run_csr(dp.new_values(g.inputs)).cpu().numpy()
+    graph = dp.capture_csr(x, out)
+    out.fill_(float("nan"))
+    graph.replay()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(out.cpu().numpy()), bits(want))
+
+
+@pytest.mark.parametrize("name", JIT_CASES)
+def test_tile_schedules_bitwise(name):
+    """Both tile schedules lower_plan offers (instance / fraction interleave of multi-group specialised
+    units) and both grids give the same bits; sgb_plan_set_tiles refuses a table of another length
+    and a table that is not a per-unit permutation of the plan's tiles."""
+    import torch
+
+    from paper_2110_12865_b200 import DevicePlan, SgbError
+
+    golden = golden_case(name)
+    lw = lowered(name, jit_min_n=0)
+    dp = DevicePlan(golden.plan, lowered=lw)  # its own: the schedule and grids change
     x = dp.new_values(golden.inputs)
     want = dp.run_csr(x).cpu().numpy()
-    assert (np.array_equal(bits(want), bits(golden.outputs)) if golden.exact else _close(want, golden.outputs))
+    assert cmp_outputs(golden)(want)
     if lw.tiles_alt is not None:
         for t in (lw.tiles_alt, lw.tiles):
             dp.set_tiles(t)
@@ -333,20 +306,43 @@ def test_tile_schedules_bitwise(golden):
             assert np.array_equal(bits(got), bits(want))
     with pytest.raises(SgbError):
         dp.set_tiles(np.zeros((len(lw.tiles) + 1, 2), np.int32))
+    if len(lw.tiles):
+        bad = np.array(lw.tiles, np.int32).reshape(-1, 2).copy()
+        bad[0, 1] = 2 ** 30  # past the end of its group
+        with pytest.raises(SgbError):
+            dp.set_tiles(bad)
+
+
+def test_autotune_keeps_bits():
+    """DevicePlan.autotune (per-wave schedule x grid) changes launch configurations, never results."""
+    import torch
+
+    from paper_2110_12865_b200 import DevicePlan
+
+    for name in ("lmlt_w12", "fem_nh_m2"):
+        g = golden_case(name)
+        dp = DevicePlan(g.plan, lowered=lowered(name, jit_min_n=0))
+        before = dp.run_csr(dp.new_values(g.inputs)).cpu().numpy()
+        dp.autotune(reps=2)
+        after = dp.run_csr(dp.new_values(g.inputs)).cpu().numpy()
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(before), bits(after))
+        assert cmp_outputs(g)(after)
 
 
 @pytest.mark.parametrize("world", [2, 3])
 def test_output_shards_on_device(golden, world):
     """One evaluation with its CSR outputs split (shard.shard_device_plan): each shard's device plan,
     running only the tiles of its producer cone, gives the full evaluation's slice bit for bit."""
-    from paper_2110_12865_b200 import DevicePlan, lower_plan
+    from paper_2110_12865_b200 import DevicePlan
     from paper_2110_12865_b200.shard import shard_device_plan, shard_outputs
 
     plan = golden.plan
-    lw = lower_plan(plan, jit_min_n=0)
+    kw = dict(jit_min_n=0) if golden.name in JIT_CASES else {}
+    lw = lowered(golden.name, **kw)
     if lw.needs_zero == 2:
         pytest.skip("reads before writes: output sharding refuses the plan")
-    full = DevicePlan(plan, lowered=lw).run_outputs_host(golden.inputs)
+    full = device_plan(golden.name, **kw).run_outputs_host(golden.inputs)
     n_out = len(plan.outputs)
     for r in range(world):
         lo, hi = shard_outputs(n_out, world, r)
