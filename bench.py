@@ -691,7 +691,7 @@ def main():
         return 0
 
     # ---- roofline of the dominant launch ----
-    direct = bool(np.any(dp.lowered.groups["flags"] & (384)))  # FLAG_OPOS16 | FLAG_OPOS32
+    direct = bool(np.any(dp.lowered.groups["flags"] & (384 | 4096)))  # FLAG_OPOS16 | FLAG_OPOS32 | FLAG_WPOS16
     traffic = csr_wave_traffic(plan, dp.lowered) if direct else wave_traffic(plan, dp.lowered)
     assert len(traffic) == n_w, (len(traffic), n_w)
     if split:  # full-plan bytes scaled by the share of each wave's tiles the shard keeps (approximate)

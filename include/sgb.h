@@ -110,10 +110,21 @@ typedef struct sgb_plan_desc {
   const void *jit_cubin;  /* sm_100a cubin with the specialised units (units flag 2): kernels
                              sgb_tape_u<unit> / sgb_tape_b<unit> / sgb_window_u<unit> (jit.py) */
   int64_t jit_cubin_size;
-  const int32_t *win_pieces; /* CSR windows (units flag 8): [n][4] group, first instance, count, item prefix */
-  int64_t n_win_pieces;
-  const int64_t *win_off;    /* [n_windows + 1] first piece of each window of 2048 outputs */
-  int64_t n_win_off;
+  /* CSR windows (units flag 8, at most one such unit, lower._csr_windows): window w assembles the
+     outputs [win_k[w], win_k[w+1]) in shared memory; member j (= group group_begin + j of the unit,
+     flags 4096: root r of instance i goes to window position ooff[oo_off + r*n + i], 0xFFFF none)
+     contributes instances [first, first + count) = win_pieces[w*J + j]; the outputs no member
+     produces are copied from the value array: copy_src[c] -> window position copy_pos[c] for
+     c in [win_copy[w], win_copy[w+1]). */
+  const int32_t *win_pieces; /* [n_windows * J][2]: first instance, instance count */
+  int64_t n_win_pieces;      /* n_windows * J pairs */
+  const int64_t *win_k;      /* [n_windows + 1]: window start positions, win_k[n_windows] = n_outputs */
+  int64_t n_win_k;
+  const int64_t *win_copy;   /* [n_windows + 1]: first copy of each window */
+  int64_t n_win_copy;
+  const uint32_t *copy_src;  /* [n_copy] value-array address of each copied output */
+  const uint16_t *copy_pos;  /* [n_copy] its position in its window */
+  int64_t n_copy;
 } sgb_plan_desc;
 
 /* Upload a device plan to `device`.  Replaces compile_plan (emit.py:198-245). */
@@ -124,10 +135,12 @@ void sgb_plan_destroy(sgb_plan *plan);
  * everything else zero.  All dependency waves are launched on `stream`. */
 int sgb_run_values(sgb_plan *plan, double *x_dev, void *stream);
 
-/* inputs -> CSR values in one pass: out_dev[k] == x[outputs[k]] after sg_run
- * (codegen.py:445), written directly by the producing kernels (no gather).
- * x_dev holds the inputs and serves as scratch for intermediates; result
- * ranges nobody re-reads are not written to it. */
+/* inputs -> CSR values: out_dev[k] == x[outputs[k]] after sg_run (codegen.py:445).
+ * x_dev holds the inputs and serves as scratch for intermediates.  With CSR
+ * windows (the default lowering when the last wave qualifies) the last wave
+ * assembles the CSR array window by window in shared memory and writes it
+ * coalesced -- no separate gather; otherwise the value waves run and one
+ * u32-indexed gather copies the outputs. */
 int sgb_run_csr(sgb_plan *plan, double *x_dev, double *out_dev, void *stream);
 
 /* One dependency wave (waves in order 0..sgb_plan_waves(plan, csr)-1); out_dev

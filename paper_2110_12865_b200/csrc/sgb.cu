@@ -54,15 +54,14 @@ enum : int { KIND_TAPE = 0, KIND_SOP = 1 };
 enum : int {
   FLAG_SELFREF = 1, FLAG_INTERLEAVED = 2, FLAG_SERIAL = 4, FLAG_STREAM = 16, FLAG_W16 = 32,
   FLAG_AFFINE0 = 64, FLAG_OPOS16 = 128, FLAG_OPOS32 = 256, FLAG_CSR_ONLY = 512, FLAG_COHERENT = 1024,
-  FLAG_IMAJOR = 2048  // CSR layout: result r of instance i at dest_base + i * n_roots + r (specialised units)
+  FLAG_IMAJOR = 2048,  // CSR layout: result r of instance i at dest_base + i * n_roots + r (specialised units)
+  FLAG_WPOS16 = 4096   // CSR-window member: root r of instance i at window position ooff[oo_off + r*n + i]
 };
 enum : int {
   U_WAVE = 0, U_KIND, U_VARIANT, U_G0, U_G1, U_T0, U_T1, U_BS, U_REGS, U_FLAGS, U_COUNT
 };
 enum : int { UNIT_CSR_ONLY = 1, UNIT_JIT = 2, UNIT_VALUE_ONLY = 4, UNIT_WINDOW = 8 };
 constexpr int JIT_BLOCK = 256;  // jit.py JIT_BLOCK
-constexpr int WIN = 2048;       // lower.WIN: outputs per CSR window
-constexpr int MAX_WINDOW_PIECES = 512;  // jit.MAX_WINDOW_PIECES
 constexpr int PRE = 8;        // slot loads kept in flight by the tape prologue
 constexpr int SOP_BS = 256;   // sum-of-products block
 constexpr int SOP_BATCH = 16; // factor loads in flight per instance
@@ -820,8 +819,10 @@ struct sgb_plan {
   uint16_t *d_coff = nullptr, *d_ooff = nullptr;
   SopDesc *d_sopd = nullptr;
   cudaLibrary_t jit_lib = nullptr;
-  int4 *d_wpieces = nullptr;
-  int64_t *d_woff = nullptr;
+  int2 *d_wpieces = nullptr;  // CSR windows: [n_win][J] first instance, count
+  int64_t *d_wk = nullptr, *d_wcopy = nullptr;
+  uint32_t *d_csrc = nullptr;
+  uint16_t *d_cpos = nullptr;
   uint32_t *d_fbase = nullptr;
   // workspace for the host-buffer entry points
   std::mutex ws_mu;
@@ -877,13 +878,16 @@ void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_
   const int64_t blocks = batched ? u.bt1 - u.bt0 : u.t1 - u.t0;
   if (blocks <= 0) return;
   if (!batched && csr && (u.flags & UNIT_VALUE_ONLY)) return;
-  if (u.flags & UNIT_WINDOW) {  // CSR windows (jit.py window_source)
-    const int4 *pieces = p->d_wpieces;
-    const int64_t *woff = p->d_woff + u.t0;
-    int64_t n = u.t1 - u.t0, w0 = u.t0, n_out = p->n_out;
+  if (u.flags & UNIT_WINDOW) {  // CSR windows (jit.py window_source): one block per window
+    const int2 *pieces = p->d_wpieces;
+    const int64_t *wk = p->d_wk, *wc = p->d_wcopy;
+    const uint32_t *csrc = p->d_csrc;
+    const uint16_t *cpos = p->d_cpos;
+    int64_t n = u.t1 - u.t0;
     Tables T = p->T;
-    void *args[] = {&T, &pieces, &woff, &n, &w0, &x, &out, &n_out};
-    cudaLaunchKernel(u.jit, dim3((unsigned)u.grid), dim3(JIT_BLOCK), args, (size_t)WIN * sizeof(double), s);
+    const double *xc = x;
+    void *args[] = {&T, &pieces, &wk, &wc, &csrc, &cpos, &n, &xc, &out};
+    cudaLaunchKernel(u.jit, dim3((unsigned)u.grid), dim3(JIT_BLOCK), args, (size_t)u.regs, s);
     return;
   }
   if ((u.flags & UNIT_CSR_ONLY) && batched) return;
@@ -990,7 +994,7 @@ void sgb_plan_destroy(sgb_plan *p) {
   void *bufs[] = {p->d_groups, p->d_tiles, p->d_btiles, p->d_outputs, p->d_tape, p->d_imm, p->d_con,
                   p->d_sop, p->d_scol, p->d_sdel, p->d_pos, p->d_x, p->d_out, p->d_cbase, p->d_coff,
                   p->d_obase, p->d_ooff, p->d_opos32, p->d_sopd, p->d_fbase, p->d_outputs32,
-                  p->d_wpieces, p->d_woff, p->d_x2, p->d_out2};
+                  p->d_wpieces, p->d_wk, p->d_wcopy, p->d_csrc, p->d_cpos, p->d_x2, p->d_out2};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (p->ws_stream) cudaStreamDestroy(p->ws_stream);
@@ -1046,6 +1050,8 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
                                      G.ob_off + (int64_t)G.n_roots * nch > d->n_obase ||
                                      G.oo_off + (int64_t)G.n_roots * G.n > d->n_ooff)) ||
         ((G.flags & FLAG_OPOS32) && (G.oo_off < 0 || G.oo_off + (int64_t)G.n_roots * G.n > d->n_opos32)) ||
+        ((G.flags & FLAG_WPOS16) && (G.oo_off < 0 || G.oo_off + (int64_t)G.n_roots * G.n > d->n_ooff ||
+                                     (G.flags & (FLAG_OPOS16 | FLAG_OPOS32)) || !(G.flags & FLAG_CSR_ONLY))) ||
         ((G.flags & FLAG_COHERENT) && G.n_ret != 1);
     if (bad) return fail(-1, "sgb_plan_create: group " + std::to_string(g) + " is out of range");
     for (int s = 0; s < G.n_slots; ++s)
@@ -1118,6 +1124,7 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
   }
   std::vector<int2> btiles;
   int max_wave = -1;
+  bool has_window = false;
   for (int k = 0; k < d->n_units; ++k) {
     const int64_t *r = d->units + (int64_t)k * U_COUNT;
     Unit u;
@@ -1136,28 +1143,40 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
     const bool jit = u.flags & UNIT_JIT;
     const bool window = u.flags & UNIT_WINDOW;
     if (window) {
-      if (!jit || !csr_only || !p->jit_lib || u.t0 < 0 || u.t1 >= d->n_win_off)
+      const int64_t n_win = d->n_win_k - 1, J = u.g1 - u.g0;
+      if (!jit || !csr_only || !p->jit_lib || u.t0 != 0 || u.t1 != n_win || n_win < 1 || J < 1 ||
+          d->n_win_pieces != n_win * J || d->n_win_copy != d->n_win_k || u.regs < 8 || has_window)
         return fail(-1, "sgb_plan_create: bad CSR-window unit " + std::to_string(k));
+      has_window = true;
       cudaKernel_t kw;
       const std::string nw = "sgb_window_u" + std::to_string(k);
       SGB_CUDA(cudaLibraryGetKernel(&kw, p->jit_lib, nw.c_str()));
       u.jit = (const void *)kw;
-      for (int64_t w = u.t0; w < u.t1; ++w) {  // pieces: groups of this unit, instance ranges inside them,
-        const int64_t a = d->win_off[w], b = d->win_off[w + 1];  // running item prefix, window positions
-        if (a < 0 || b < a || b > d->n_win_pieces || b - a > MAX_WINDOW_PIECES)
-          return fail(-1, "sgb_plan_create: bad CSR-window piece range");
-        int64_t prefix = 0;
-        for (int64_t q = a; q < b; ++q) {
-          const int32_t *pc = d->win_pieces + 4 * q;
-          if (pc[0] < u.g0 || pc[0] >= u.g1 || pc[1] < 0 || pc[2] < 1 ||
-              (int64_t)pc[1] + pc[2] > d->groups[pc[0]].n || pc[3] != prefix ||
-              !(d->groups[pc[0]].flags & (FLAG_OPOS16 | FLAG_OPOS32)))
-            return fail(-1, "sgb_plan_create: bad CSR-window piece");
-          prefix += pc[2];
+      if (u.regs > 48 * 1024) SGB_CUDA(cudaFuncSetAttribute(u.jit, cudaFuncAttributeMaxDynamicSharedMemorySize, u.regs));
+      const int64_t wmax = u.regs / 8;  // the window buffer (doubles)
+      if (d->win_k[0] != 0 || d->win_k[n_win] != d->n_outputs || d->win_copy[0] != 0 || d->win_copy[n_win] != d->n_copy)
+        return fail(-1, "sgb_plan_create: CSR windows do not cover the outputs / copies");
+      for (int g = u.g0; g < u.g1; ++g)
+        if (!(d->groups[g].flags & FLAG_WPOS16) || (d->groups[g].flags & FLAG_SELFREF))
+          return fail(-1, "sgb_plan_create: CSR-window member without window positions");
+      for (int64_t w = 0; w < n_win; ++w) {
+        const int64_t len = d->win_k[w + 1] - d->win_k[w];
+        if (len < 0 || len > wmax || d->win_copy[w + 1] < d->win_copy[w])
+          return fail(-1, "sgb_plan_create: bad CSR window " + std::to_string(w));
+        for (int64_t c = d->win_copy[w]; c < d->win_copy[w + 1]; ++c)
+          if ((int64_t)d->copy_src[c] >= d->value_array_size || (int64_t)d->copy_pos[c] >= len)
+            return fail(-1, "sgb_plan_create: bad CSR-window copy");
+        for (int64_t j = 0; j < J; ++j) {  // every staged position of every piece stays inside its window
+          const int32_t a = d->win_pieces[2 * (w * J + j)], cnt = d->win_pieces[2 * (w * J + j) + 1];
+          const sgb_group &G = d->groups[u.g0 + j];
+          if (a < 0 || cnt < 0 || (int64_t)a + cnt > G.n) return fail(-1, "sgb_plan_create: bad CSR-window piece");
+          for (int r = 0; r < G.n_roots; ++r)
+            for (int64_t i = a; i < (int64_t)a + cnt; ++i) {
+              const uint16_t o = d->ooff[G.oo_off + (int64_t)r * G.n + i];
+              if (o != 0xFFFFu && (int64_t)o >= len) return fail(-1, "sgb_plan_create: window position out of range");
+            }
         }
-        if (prefix >= ((int64_t)1 << 31)) return fail(-1, "sgb_plan_create: CSR window too large");
       }
-      if ((u.t1 - u.t0) * (int64_t)WIN < d->n_outputs) return fail(-1, "sgb_plan_create: CSR windows miss outputs");
     } else if (jit) {
       if (u.kind != KIND_TAPE || u.bs != JIT_BLOCK || (u.variant != 1 && u.variant != 2 && u.variant != 4) ||
           !p->jit_lib)
@@ -1184,9 +1203,7 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
     {  // persistent grid: resident capacity of the chip, at most one block (warp for SOP) per tile
       int nb = 0;
       if (window) {
-        SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, u.jit, JIT_BLOCK, (size_t)WIN * sizeof(double)));
-        u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
-        if (u.grid > u.t1 - u.t0) u.grid = u.t1 - u.t0;
+        u.grid = u.t1 - u.t0;  // one block per window, dispatched in CSR order
       } else if (jit) {
         SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, u.jit, JIT_BLOCK, (size_t)u.regs));
         u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
@@ -1317,8 +1334,8 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
   for (int g = 0; g < d->n_groups; ++g) p->group_n[g] = d->groups[g].n;
   p->h_tiles.assign(reinterpret_cast<const int2 *>(d->tiles), reinterpret_cast<const int2 *>(d->tiles) + d->n_tiles);
   std::vector<uint32_t> outputs32(d->outputs, d->outputs + d->n_outputs);
-  for (int g = 0; g < d->n_groups; ++g)
-    if (d->groups[g].flags & (FLAG_OPOS16 | FLAG_OPOS32)) p->direct_csr = true;
+  for (int g = 0; g < d->n_groups; ++g)  // CSR mode without the gather: direct stores or CSR windows
+    if (d->groups[g].flags & (FLAG_OPOS16 | FLAG_OPOS32 | FLAG_WPOS16)) p->direct_csr = true;
   for (int g = 0; g < d->n_groups; ++g)
     if (d->groups[g].flags & FLAG_IMAJOR) p->csr_layout = true;
   // compact sum-of-products descriptors (+ fast-path factor bases)
@@ -1365,8 +1382,9 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       (rc = upload(&p->d_opos32, d->opos32, d->n_opos32)) ||
       (rc = upload(&p->d_sopd, sopd.data(), (int64_t)sopd.size())) ||
       (rc = upload(&p->d_outputs32, outputs32.data(), (int64_t)outputs32.size())) ||
-      (rc = upload(&p->d_wpieces, reinterpret_cast<const int4 *>(d->win_pieces), d->n_win_pieces)) ||
-      (rc = upload(&p->d_woff, d->win_off, d->n_win_off)) ||
+      (rc = upload(&p->d_wpieces, reinterpret_cast<const int2 *>(d->win_pieces), d->n_win_pieces)) ||
+      (rc = upload(&p->d_wk, d->win_k, d->n_win_k)) || (rc = upload(&p->d_wcopy, d->win_copy, d->n_win_copy)) ||
+      (rc = upload(&p->d_csrc, d->copy_src, d->n_copy)) || (rc = upload(&p->d_cpos, d->copy_pos, d->n_copy)) ||
       (rc = upload(&p->d_fbase, fbase.data(), (int64_t)fbase.size())))
     return rc;
   p->T = Tables{p->d_groups, p->d_tape, p->d_imm, p->d_sop, p->d_scol, p->d_sdel, p->d_pos,

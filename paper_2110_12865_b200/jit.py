@@ -132,19 +132,21 @@ def _out_pos(rec, r: int, i: str = "i") -> str | None:
 
 def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: str = "",
                 batched: bool = False, window: bool = False, bv: str = "b",
-                stage: str | None = None) -> tuple[list[str], list[str]]:
+                stage: str | None = None, guard: str | None = None) -> tuple[list[str], list[str]]:
     """Straight-line CUDA for instance ``iv`` of packed group ``gi`` (register tape -> SSA).
 
     Returns (load lines, compute + store lines) so several instances' loads can be
     issued before any of them computes.  Variables carry suffix ``sfx``.
     Batched: value set ``b`` of ``X[addr * ld + b]`` (lane = value set).  Window:
-    the CSR value goes to the block's shared window ``buf[o - kwin_]`` (no
-    value-array store: window members are never re-read).  Stage: an
-    instance-major group's results go to the block's staging buffer at
-    ``stage_[(stage) * RP + r]`` (``stage`` = the instance's offset in the tile,
-    RP = lower.stage_stride); the unit writes the tile out coalesced.
+    the CSR value goes to the block's shared window ``buf[wpos]`` (no value-array
+    store: window members are never re-read).  Stage: an instance-major group's
+    results go to the block's staging buffer at ``stage_[(stage) * RP + r]``
+    (``stage`` = the instance's offset in the tile, RP = lower.stage_stride); the
+    unit writes the tile out coalesced.  ``guard``: every load is predicated on it
+    (lanes without an instance issue no memory traffic).
     """
     X = (lambda a: f"x + (u64)({a}) * ld + {bv}") if batched else (lambda a: f"x + ({a})")
+    G = (lambda e, z: f"({guard}) ? ({e}) : {z}") if guard else (lambda e, z: e)  # noqa: E731
     rec = dp.groups[gi]
     n, S, K = int(rec["n"]), int(rec["n_slots"]), int(rec["n_const"])
     flags = int(rec["flags"])
@@ -155,7 +157,7 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
     i = iv
     col = lambda c: _column(rec, c, i, dp)  # noqa: E731
     if S:
-        loads.append(f"const u32 idx0{sfx} = {col(0)};")
+        loads.append(f"const u32 idx0{sfx} = {G(col(0), '0u')};")
     for s_ in range(S):
         c = int(cols[s_])
         if c < 0:
@@ -164,12 +166,12 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
             addr = f"idx0{sfx}"
         else:
             addr = col(c)
-        loads.append(f"const double s{s_}{sfx} = __ldg({X(addr)});")
+        loads.append(f"const double s{s_}{sfx} = {G(f'__ldg({X(addr)})', '0.0')};")
         reg[s_] = f"s{s_}{sfx}"
     for k in range(K):
         e = (f"{int(rec['c_off'])}LL + {i} * {K} + {k}" if flags & L.FLAG_INTERLEAVED
              else f"{int(rec['c_off']) + k * n}LL + {i}")
-        loads.append(f"const double k{k}{sfx} = __ldcs(T.con + {e});")
+        loads.append(f"const double k{k}{sfx} = {G(f'__ldcs(T.con + {e})', '0.0')};")
         reg[S + k] = f"k{k}{sfx}"
     stream = bool(flags & L.FLAG_STREAM)
     opos = lambda r: _out_pos(rec, r, i)  # noqa: E731
@@ -178,8 +180,9 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
         A = ("-" if na else "") + reg.get(a, "0.0")
         B = ("-" if nb else "") + reg.get(b, "0.0")
         C = reg.get(c, "0.0")
-        if op == L.T_ST and window:
-            comp.append(f"if (ok{sfx}) {{ const u32 o = {opos(aux)}; if (o != NONE) buf[o - kwin_] = {reg[a]}; }}")
+        if op == L.T_ST and window:  # CSR-window member: FLAG_WPOS16 position in the block's window
+            comp.append(f"if (ok{sfx}) {{ const u16 o = __ldcs(T.ooff + {int(rec['oo_off']) + aux * n}LL + {i}); "
+                        f"if (o != 0xFFFF) buf[o] = {reg[a]}; }}")
             continue
         if op == L.T_ST and stage is not None:
             comp.append(f"if (ok{sfx}) stage_[({stage}) * {L.stage_stride(int(rec['n_roots']))} + {aux}] = {reg[a]};")
@@ -417,45 +420,88 @@ def compile_cubin(src: str, name: str = "sgb_tape.cu") -> bytes:
     return cubin
 
 
-MAX_WINDOW_PIECES = 512
-
-
-WINDOW_VEC = 4
+WINDOW_LOADS = 32  # loads in flight per thread across the members of one chunk of a window kernel
+COPY_UNROLL = 4  # copied outputs per thread in flight
 
 
 def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
-    """CSR-window kernel of unit ``u``: a block assembles WIN consecutive outputs in shared
-    memory from its window's pieces (group, instance range) -- warps take pieces, lanes
-    take VEC instances each (VEC per group: all of a lane's loads stay in flight within the
-    register budget) -- then writes them coalesced."""
+    """CSR-window kernel of unit ``u`` (lower._csr_windows): block w assembles the outputs
+    [win_k[w], win_k[w+1]) in shared memory and writes them out with 16-byte streaming stores.
+
+    Work inside a window is block-uniform, so nothing diverges: the outputs copied from the
+    value array (inputs, earlier waves' results) first, then the members in chunks -- every
+    member of a chunk takes its piece (instance range) with one instance per thread, all the
+    chunk's loads issued before its computes (WINDOW_LOADS per thread) -- each result stored at
+    its FLAG_WPOS16 position in the window.  Members store nothing to the value array (the last
+    wave: never re-read), so every output crosses HBM once, coalesced.
+    """
     unit = dp.unit(u)
-    out = [f'extern "C" __global__ void __launch_bounds__({JIT_BLOCK}, 3) sgb_window_u{u}(',
-           "    Tables T, const int4 *pieces, const i64 *win_off, i64 n_win, i64 w0, double *x, double *out,",
-           "    i64 n_out) {",
-           "  extern __shared__ double buf[];",
-           f"  __shared__ int4 sp[{MAX_WINDOW_PIECES}];",
-           "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;",
-           "  for (i64 w = blockIdx.x; w < n_win; w += gridDim.x) {",
-           "    const i64 p0 = win_off[w], np_ = win_off[w + 1] - p0;",
-           "    for (i64 j = threadIdx.x; j < np_; j += blockDim.x) sp[j] = pieces[p0 + j];",
-           "    __syncthreads();",
-           f"    const i64 kwin_ = (w0 + w) * {L.WIN}LL;",
-           f"    for (int q = warp; q < np_; q += {JIT_BLOCK // 32}) {{",
-           "      const int4 pc = sp[q];",
-           "      switch (pc.x) {"]
-    for gi in range(unit["group_begin"], unit["group_end"]):
+    g0, g1 = unit["group_begin"], unit["group_end"]
+    J = g1 - g0
+    chunks, cur, width = [], [], 0
+    for gi in range(g0, g1):
         rec = dp.groups[gi]
         _check_stores(tapes[gi], int(rec["n_roots"]), gi)
-        vec = max(1, min(WINDOW_VEC, 12 // max(1, int(rec["n_slots"]) + int(rec["n_const"]))))
-        out.append(f"      case {gi}: for (int c = lane; c < pc.z; c += {32 * vec}) {{")
-        out.append("        const i64 i = (i64)pc.y + c;")
-        out += ["        " + ln for ln in group_vec_body(dp, gi, tapes[gi], imms[gi], vec, "i", 32,
-                                                         window=True, limit="c + {v} < pc.z")]
-        out.append("      } break;")
-    out += ["      default: break;", "      }", "    }", "    __syncthreads();",
-            f"    const i64 cnt = n_out - kwin_ < {L.WIN}LL ? n_out - kwin_ : {L.WIN}LL;",
-            "    for (i64 j = threadIdx.x; j < cnt; j += blockDim.x) __stcs(out + kwin_ + j, buf[j]);",
-            "    __syncthreads();", "  }", "}", ""]
+        wdt = max(1, int(rec["n_slots"]) + int(rec["n_const"]))
+        if cur and width + wdt > WINDOW_LOADS:
+            chunks.append(cur)
+            cur, width = [], 0
+        cur.append(gi)
+        width += wdt
+    if cur:
+        chunks.append(cur)
+    B = JIT_BLOCK
+    out = [f'extern "C" __global__ void __launch_bounds__({B}) sgb_window_u{u}(',
+           "    Tables T, const int2 *pieces, const i64 *win_k, const i64 *copy_off, const u32 *copy_src,",
+           "    const u16 *copy_pos, i64 n_win, const double *x, double *out) {",
+           "  extern __shared__ double buf[];",
+           f"  __shared__ int2 sp[{J}];",
+           "  const int tid = threadIdx.x;",
+           "  for (i64 w = blockIdx.x; w < n_win; w += gridDim.x) {",
+           f"    for (int j = tid; j < {J}; j += {B}) sp[j] = __ldg(pieces + w * {J} + j);",
+           "    const i64 k0 = __ldg(win_k + w), len_ = __ldg(win_k + w + 1) - k0;",
+           "    const i64 c0_ = __ldg(copy_off + w), c1_ = __ldg(copy_off + w + 1);",
+           "    __syncthreads();",
+           f"    for (i64 c = c0_ + tid; c < c1_; c += {B * COPY_UNROLL}) {{",
+           f"      double cv_[{COPY_UNROLL}]; u16 cp_[{COPY_UNROLL}];",
+           "#pragma unroll",
+           f"      for (int q = 0; q < {COPY_UNROLL}; ++q) if (c + q * {B} < c1_) {{",
+           f"        cp_[q] = __ldcs(copy_pos + c + q * {B}); cv_[q] = __ldg(x + __ldcs(copy_src + c + q * {B})); }}",
+           "#pragma unroll",
+           f"      for (int q = 0; q < {COPY_UNROLL}; ++q) if (c + q * {B} < c1_) buf[cp_[q]] = cv_[q];",
+           "    }"]
+    for chunk in chunks:
+        cmax = "0"
+        for gi in chunk:
+            cmax = f"max({cmax}, sp[{gi - g0}].y)"
+        out.append(f"    for (int c0 = 0, cmax_ = {cmax}; c0 < cmax_; c0 += {B}) {{")
+        loads, comps = [], []
+        for gi in chunk:
+            j = gi - g0
+            out.append(f"      const bool ok_{j} = c0 + tid < sp[{j}].y;")
+            out.append(f"      const i64 i_{j} = ok_{j} ? (i64)sp[{j}].x + c0 + tid : 0;")
+            ld, cp = group_parts(dp, gi, tapes[gi], imms[gi], iv=f"i_{j}", sfx=f"_{j}", window=True,
+                                 guard=f"ok_{j}")
+            loads += ld
+            comps += cp
+        out += ["      " + ln for ln in loads + comps]
+        out.append("    }")
+    out += ["    __syncthreads();",
+            "    {",
+            "      double *o_ = out + k0;",
+            "      const i64 head = (i64)((reinterpret_cast<unsigned long long>(o_) >> 3) & 1ull);",
+            "      if (tid == 0 && head && len_ > 0) __stcs(o_, buf[0]);",
+            "      const i64 np_ = (len_ - head) >> 1;",
+            f"      for (i64 q = tid; q < np_; q += {B}) {{",
+            "        double2 v_; v_.x = buf[head + 2 * q]; v_.y = buf[head + 2 * q + 1];",
+            "        __stcs(reinterpret_cast<double2 *>(o_ + head) + q, v_);",
+            "      }",
+            "      if (tid == 0 && len_ > head && ((len_ - head) & 1)) __stcs(o_ + len_ - 1, buf[len_ - 1]);",
+            "    }",
+            "    __syncthreads();",
+            "  }",
+            "}",
+            ""]
     return "\n".join(out)
 
 
@@ -464,8 +510,6 @@ def specialise(dp, tapes: dict, imms: dict, units: list[int]) -> tuple[bytes, st
     parts = []
     for u in units:
         if dp.unit(u)["flags"] & L.UNIT_WINDOW:
-            if dp.win_off is not None and len(dp.win_off) > 1 and int(np.diff(dp.win_off).max()) > MAX_WINDOW_PIECES:
-                raise ValueError("a CSR window has more pieces than the kernel stages")
             parts.append(window_source(dp, u, tapes, imms))
         else:
             parts.append(unit_source(dp, u, tapes, imms))

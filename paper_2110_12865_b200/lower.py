@@ -44,11 +44,11 @@ FLAG_OPOS32 = 256  # output positions: u32 per instance (0xFFFFFFFF = not an out
 FLAG_CSR_ONLY = 512  # synthetic copy group: runs in CSR mode only
 FLAG_COHERENT = 1024  # one retained column: every slot is column 0 + delta
 FLAG_IMAJOR = 2048  # CSR layout: result r of instance i at dest_base + i * n_roots + r (specialised units only)
+FLAG_WPOS16 = 4096  # CSR-window member: root r of instance i goes to its window's position ooff[oo_off + r*n + i]
 UNIT_CSR_ONLY = 1
 UNIT_JIT = 2  # tape unit compiled to straight-line code (jit.py), one instance per thread
 UNIT_VALUE_ONLY = 4  # value-mode twin of a CSR-window unit (skipped by sgb_run_csr)
-UNIT_WINDOW = 8  # CSR windows: each block assembles WIN consecutive outputs in shared memory
-WIN = 2048  # outputs per CSR window (16 KB of shared memory)
+UNIT_WINDOW = 8  # CSR windows: each block assembles one window of consecutive outputs in shared memory
 JIT_BLOCK = 256
 CHUNK = 32  # instances per compressed-index chunk (one warp in single-set mode)
 NONE32 = 0xFFFFFFFF
@@ -118,9 +118,11 @@ class DevicePlanArrays:
     exact: bool = True
     jit_cubin: bytes = b""  # specialised tape units (UNIT_JIT): kernels sgb_tape_u<unit>, see jit.py
     jit_source: str = ""
-    win_pieces: np.ndarray = None  # int32 [n, 4]: group, first instance, count, item prefix (CSR windows)
-    win_off: np.ndarray = None  # int64 [n_windows + 1]: first piece of each window
+    windows: "CsrWindows" = None  # CSR windows of the last wave (the window unit's pieces and copies)
+    window_members: list = field(default_factory=list)  # plan kernels the window unit evaluates
     window_units: list = field(default_factory=list)
+    jit_tapes: dict = field(default_factory=dict)  # packed group -> register tape of specialised units
+    jit_imms: dict = field(default_factory=dict)
     csr_layout: list = field(default_factory=list)  # plan kernels stored instance-major (FLAG_IMAJOR)
     # the same tiles with every multi-group specialised unit in fraction-interleaved order (None when
     # no unit has a second candidate); DevicePlan times both schedules per wave (runtime.autotune)
@@ -642,6 +644,7 @@ class _Group:
     kernel: int = -1
     window_value: bool = False  # value-mode twin of a CSR-window member (runs in value mode only)
     window: bool = False  # CSR-window member (window unit, CSR mode only)
+    wpos: np.ndarray = None  # CSR-window member: (n_roots, n) uint16 position in its window
 
 
 def _output_map(plan, lowered, waves):
@@ -719,10 +722,12 @@ def _needs_zero(plan, waves, reads) -> int:
 def _window_members(plan, lowered, opos, n_waves):
     """Kernel indices whose outputs a CSR-window unit can assemble, or None.
 
-    Requires every output-producing group of the last wave to be a plain,
-    single-root, never re-read group whose output positions increase with the
-    instance (each window then takes one contiguous instance range of it) and
-    every other output to be final before the last wave (copy pieces).
+    Requires every output-producing group of the last wave to be a plain
+    (not self-referencing), never re-read group whose instances' first output
+    positions increase with the instance (each window then takes one
+    contiguous instance range of it), and every other output -- inputs,
+    earlier waves' results, duplicates -- to be final before the last wave
+    (the windows copy those from the value array).
     """
     if n_waves == 0 or not len(plan.outputs):
         return None
@@ -731,9 +736,10 @@ def _window_members(plan, lowered, opos, n_waves):
     for kl, o in zip(lowered, opos):
         if o is None or kl.wave != last:
             continue
-        if kl.flags & (FLAG_SELFREF | FLAG_SERIAL) or o.shape[0] != 1:
+        if kl.flags & (FLAG_SELFREF | FLAG_SERIAL):
             return None
-        v = o[0][o[0] != NONE32]
+        first = np.where(o == NONE32, np.iinfo(np.int64).max, o).min(axis=0)
+        v = first[first != np.iinfo(np.int64).max]
         if v.size > 1 and not np.all(np.diff(v) > 0):
             return None
         members.append(kl.index)
@@ -742,8 +748,9 @@ def _window_members(plan, lowered, opos, n_waves):
     # outputs not produced by members must come from inputs or earlier waves
     outs = np.asarray(plan.outputs, dtype=np.int64)
     covered = np.zeros(outs.size, bool)
+    keep = set(members)
     for kl, o in zip(lowered, opos):
-        if o is not None and kl.index in set(members):
+        if o is not None and kl.index in keep:
             covered[o[o != NONE32]] = True
     rest = outs[~covered]
     waves = [kl.wave for kl in lowered]
@@ -752,27 +759,108 @@ def _window_members(plan, lowered, opos, n_waves):
     return members
 
 
-def _window_pieces(packed, gis, n_out, pieces, win_off, win_opos):
-    """Per CSR window [k0, k0 + WIN): one (group, first instance, count, prefix) piece per member."""
-    n_win = (n_out + WIN - 1) // WIN
-    starts = np.arange(n_win, dtype=np.int64) * WIN
-    per = []  # per member: (gi, lo idx, hi idx) arrays over windows
-    for gi in gis:
-        o = win_opos[gi]
-        valid = np.nonzero(o != NONE32)[0]
-        ov = o[valid]
-        lo = np.searchsorted(ov, starts)
-        hi = np.searchsorted(ov, starts + WIN)
-        per.append((gi, valid, lo, hi))
-    for w in range(n_win):
-        prefix = 0
-        for gi, valid, lo, hi in per:
-            if hi[w] > lo[w]:
-                i0 = int(valid[lo[w]])
-                cnt = int(valid[hi[w] - 1]) - i0 + 1
-                pieces.append((gi, i0, cnt, prefix))
-                prefix += cnt
-        win_off.append(len(pieces))
+WIN_ROWS = 240  # anchor instances per CSR window (block of JIT_BLOCK threads: 16 lanes of slack)
+WIN_MAX = 7936  # outputs per CSR window (62 KB of shared memory: 3 windows resident per SM)
+WIN_MIN = 1024  # windows are not cut shorter than this unless the anchor forces it
+
+
+@dataclass
+class CsrWindows:
+    """CSR windows of the last wave (``_csr_windows``): window w assembles outputs [k[w], k[w+1])."""
+
+    k: np.ndarray  # int64 [n_win + 1] window start positions
+    pieces: np.ndarray  # int32 [n_win, J, 2]: member j's first instance and instance count in window w
+    wpos: list  # per member: uint16 (R, N) position of root r of instance i in its window, 0xFFFF = none
+    copy_off: np.ndarray  # int64 [n_win + 1]: copies of window w are [copy_off[w], copy_off[w+1])
+    copy_src: np.ndarray  # uint32: value-array address of each copied output (CSR order)
+    copy_pos: np.ndarray  # uint16: its position in its window
+
+
+def _csr_windows(member_opos: list, n_out: int, copy_k: np.ndarray, copy_addr: np.ndarray,
+                 rows: int = WIN_ROWS, wmax: int = WIN_MAX) -> CsrWindows:
+    """Cut the CSR value array into windows for the window unit (jit.window_source).
+
+    ``member_opos``: per member group its (R, N) CSR positions (NONE32 = not an output), first
+    positions increasing with the instance.  Windows never split an instance's outputs (its
+    roots stay in one window), hold at most ``wmax`` outputs, and -- anchored on the member with
+    the most outputs -- cover ``rows`` consecutive anchor instances when that fits, so on mesh
+    plans (instance = vertex = CSR row) every member's piece is about ``rows`` instances: one
+    pass of a 256-thread block.  ``copy_k`` / ``copy_addr``: the outputs the members do not
+    produce (CSR positions, value-array sources).
+    """
+    big = np.iinfo(np.int64).max
+    firsts, lasts = [], []
+    for o in member_opos:
+        valid = o != NONE32
+        firsts.append(np.where(valid, o, big).min(axis=0))
+        lasts.append(np.where(valid, o, -1).max(axis=0))
+    # cuts inside an instance's [first, last] output range are not allowed
+    cover = np.zeros(n_out + 2, np.int64)
+    for f, l_ in zip(firsts, lasts):
+        m = l_ > f
+        np.add.at(cover, f[m] + 1, 1)
+        np.add.at(cover, l_[m] + 1, -1)
+    blocked = np.cumsum(cover)[: n_out + 1] > 0  # blocked[p]: a cut before position p splits an instance
+    allowed = np.flatnonzero(~blocked)
+    allowed = allowed[(allowed > 0) & (allowed <= n_out)]
+    if not allowed.size or allowed[-1] != n_out:
+        allowed = np.append(allowed, n_out)
+    counts = [int((f != big).sum()) for f in firsts]
+    anchor = int(np.argmax(counts)) if counts else -1
+    # preferred cuts: the first output of every ``rows``-th anchor instance (snapped to an allowed cut)
+    pref = np.zeros(0, np.int64)
+    if anchor >= 0:
+        fa = firsts[anchor]
+        valid = np.flatnonzero(fa != big)
+        q = np.searchsorted(valid, np.arange(rows, fa.size, rows))  # first valid instance >= m * rows
+        starts = fa[valid[q[q < valid.size]]]
+        j = np.searchsorted(allowed, starts, side="right") - 1
+        pref = np.unique(allowed[j[j >= 0]])
+    k = [0]
+    while k[-1] < n_out:
+        cur = k[-1]
+        lim = cur + wmax
+        # the next preferred cut, if the window stays within wmax; else the last allowed cut in reach
+        j = np.searchsorted(pref, cur, side="right")
+        nxt = int(pref[j]) if j < pref.size and pref[j] <= lim else None
+        if nxt is not None and nxt - cur < WIN_MIN and j + 1 < pref.size and pref[j + 1] <= lim:
+            # tiny windows (anchor sparse here): merge preferred steps up to WIN_MIN
+            jj = np.searchsorted(pref, min(lim, cur + WIN_MIN), side="right") - 1
+            nxt = int(pref[max(jj, j)])
+        if nxt is None:
+            jj = np.searchsorted(allowed, lim, side="right") - 1
+            if jj < 0 or allowed[jj] <= cur:
+                raise ValueError("an instance's outputs span more than one CSR window")
+            nxt = int(allowed[jj])
+        k.append(nxt)
+    k = np.asarray(k, np.int64)
+    n_win = k.size - 1
+    J = len(member_opos)
+    pieces = np.zeros((n_win, J, 2), np.int32)
+    wpos = []
+    for j, (o, f) in enumerate(zip(member_opos, firsts)):
+        n = f.size
+        inst = np.flatnonzero(f != big)
+        fv = f[inst]
+        lo = np.searchsorted(fv, k[:-1])
+        hi = np.searchsorted(fv, k[1:])
+        has = hi > lo
+        a = np.where(has, inst[np.minimum(lo, inst.size - 1)], 0)
+        b = np.where(has, inst[np.maximum(hi - 1, 0)] + 1, 0)
+        pieces[:, j, 0] = a
+        pieces[:, j, 1] = b - a
+        w_of = np.searchsorted(k, np.where(f == big, 0, f), side="right") - 1  # window of each instance
+        rel = np.where(o == NONE32, 0xFFFF, o - k[np.clip(w_of, 0, n_win - 1)][None, :])
+        if n and rel.size and int(rel[o != NONE32].max(initial=0)) >= 0xFFFF:
+            raise ValueError("CSR window too long for 16-bit positions")
+        wpos.append(rel.astype(np.uint16))
+    order = np.argsort(copy_k, kind="stable")
+    ck, ca = np.asarray(copy_k, np.int64)[order], np.asarray(copy_addr, np.int64)[order]
+    copy_off = np.searchsorted(ck, k).astype(np.int64)
+    cw = np.searchsorted(k, ck, side="right") - 1
+    copy_pos = (ck - k[np.clip(cw, 0, max(n_win - 1, 0))]).astype(np.uint16) if ck.size else np.zeros(0, np.uint16)
+    return CsrWindows(k=k, pieces=pieces, wpos=wpos, copy_off=copy_off, copy_src=ca.astype(np.uint32),
+                      copy_pos=copy_pos)
 
 
 def jit_vec(groups, sel) -> int:
@@ -942,7 +1030,8 @@ JIT_MAX_WAVE_GROUPS = 48  # ...unless they share a wave of at most this many gro
 
 def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = None,
                jit: bool | None = None, csr_window: bool | None = None,
-               jit_min_n: int | None = None, relayout: str | bool | None = None) -> DevicePlanArrays:
+               jit_min_n: int | None = None, relayout: str | bool | None = None,
+               jit_compile: bool = True) -> DevicePlanArrays:
     """ExecutionPlan -> device plan.
 
     ``direct_csr``: output groups store their CSR values through output-position
@@ -950,6 +1039,9 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     without a gather pass).  Off by default: on B200 the 8-byte scattered stores
     cost more than the coalesced value-array stores + one u32-indexed gather
     (profiles/r06).
+
+    ``jit_compile=False`` lays out the specialised units without running NVRTC (no cubin: for
+    the CPU emulator of the device plan, tests/device_plan_emu.py).
 
     ``relayout`` (``"auto"`` / ``"all"`` / False): the CSR layout -- big plain
     multi-root groups whose readers gather across roots store instance-major
@@ -962,15 +1054,17 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         direct_csr = os.environ.get("SGB_DIRECT_CSR", "0") == "1"
     if jit is None:  # specialised (compiled) tape units -- see jit.py; SGB_TAPE_JIT=0 keeps the interpreter
         jit = os.environ.get("SGB_TAPE_JIT", "1") != "0"
-    if jit:
+    if jit and jit_compile:
         from . import jit as _jit
 
         jit = _jit.available()
     if jit_min_n is None:
         jit_min_n = int(os.environ.get("SGB_JIT_MIN_N", JIT_MIN_N))
-    if csr_window is None:  # CSR windows of the last wave (specialised units only), see _window_members
-        csr_window = os.environ.get("SGB_CSR_WINDOW", "0") == "1"
-    csr_window = bool(csr_window and jit)
+    window_policy = "force" if csr_window else "off"
+    if csr_window is None:  # CSR windows of the last wave (specialised units only), see _window_members:
+        # by default for plans whose last wave holds a big group and at most JIT_MAX_WAVE_GROUPS members
+        window_policy = {"0": "off", "1": "force"}.get(os.environ.get("SGB_CSR_WINDOW", ""), "auto")
+    csr_window = window_policy != "off" and bool(jit)
     if relayout is None:
         relayout = False
     if relayout is True:
@@ -979,8 +1073,8 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     read_sets = _read_sets(plan)  # which ranges each kernel reads: invariant under the CSR layout
     imajor: set = set()
     if relayout:
-        if direct_csr or csr_window:
-            raise ValueError("the CSR layout does not combine with direct CSR stores or CSR windows")
+        if direct_csr:
+            raise ValueError("the CSR layout does not combine with direct CSR stores")
         cand = [kl.index for kl in lowered if not kl.flags & (FLAG_SELFREF | FLAG_SERIAL)
                 and plan.kernels[kl.index].instances >= jit_min_n
                 and plan.kernels[kl.index].n_roots <= MAX_IMAJOR_ROOTS]
@@ -997,6 +1091,9 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     n_waves = (max(waves) + 1) if waves else 0
     opos, res_k, res_addr = _output_map(plan, lowered, waves)
     window = _window_members(plan, lowered, opos, n_waves) if csr_window and not direct_csr else None
+    if window is not None and window_policy == "auto" and (
+            len(window) > JIT_MAX_WAVE_GROUPS or max(plan.kernels[k].instances for k in window) < jit_min_n):
+        window = None  # small plans: the gather costs nothing, NVRTC time would
     if window is not None:
         # CSR windows: only last-wave members keep output positions; every other output
         # (inputs, duplicates, earlier waves' results) is a copy piece of its window
@@ -1039,15 +1136,21 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                              kl.n_regs, kl.tape, kl.imms, kl.sop, None if in_window else opos[kl.index],
                              kl.index, window_value=in_window))
         if in_window:
-            win_groups.append(_Group(kl.kind, flags | FLAG_CSR_ONLY, n, kp.n_roots, kp.dest_base, kp.p_base,
-                                     kp.c_base, len(kp.const_vars), kl.slot_col, kl.slot_delta, cols, kp.layout,
-                                     kl.wave, kl.n_regs, kl.tape, kl.imms, kl.sop, opos[kl.index], kl.index,
+            win_groups.append(_Group(kl.kind, flags | FLAG_CSR_ONLY | FLAG_WPOS16, n, kp.n_roots, kp.dest_base,
+                                     kp.p_base, kp.c_base, len(kp.const_vars), kl.slot_col, kl.slot_delta, cols,
+                                     kp.layout, kl.wave, kl.n_regs, kl.tape, kl.imms, kl.sop, None, kl.index,
                                      window=True))
+    windows = None
+    if window is not None:
+        # members in kernel order == their order in the window unit (pieces columns)
+        windows = _csr_windows([opos[g.kernel] for g in win_groups], len(plan.outputs), res_k, res_addr)
+        for g, wp in zip(win_groups, windows.wpos):
+            g.wpos = wp
     extra_pos = []
     p_next = int(np.asarray(plan.positions).size)
     copy_waves = []
     for wv, sel in copy_sets:
-        if not np.any(sel):
+        if window is not None or not np.any(sel):  # window units copy these outputs themselves
             continue
         addr, kk = res_addr[sel], res_k[sel]
         ordr = np.argsort(kk, kind="stable")  # CSR order: coalesced stores
@@ -1062,7 +1165,8 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         copy_waves.append(wv)
     needs_zero = _needs_zero(plan, waves, list(zip(waves, read_sets)) +
                              [(g.wave, g.columns[0]) for g in groups + win_groups
-                              if g.flags & FLAG_CSR_ONLY and g.tape is None])
+                              if g.flags & FLAG_CSR_ONLY and g.tape is None] +
+                             ([(last, res_addr)] if window is not None and res_addr.size else []))
     groups = groups + win_groups
     total_waves = max([n_waves] + [w + 1 for w in copy_waves])
 
@@ -1073,9 +1177,6 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     tapes, imms, sops, scol, sdel, cbases, coffs, obases, ooffs, op32 = ([] for _ in range(10))
     n_tape = n_imm = n_sop = n_slot = n_cb = n_co = n_ob = n_oo = n_o32 = 0
     jit_tapes, jit_imms, jit_units = {}, {}, []
-    win_pieces: list = []
-    win_off = [0]
-    win_opos: dict = {}
     window_units: list = []
     n_out_total = len(plan.outputs)
     for w in range(total_waves):
@@ -1086,8 +1187,7 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
             # interpreter would outlast the whole specialised unit it runs beside)
             plain_w = [j for j in members if not groups[j].flags & (FLAG_SELFREF | FLAG_SERIAL)]
             big_wave = any(groups[j].n >= jit_min_n for j in plain_w) and len(plain_w) <= JIT_MAX_WAVE_GROUPS
-            sj = [j for j in plain_w
-                  if groups[j].n >= jit_min_n or big_wave or groups[j].window or groups[j].window_value]
+            sj = [j for j in plain_w if groups[j].n >= jit_min_n or big_wave or groups[j].window]
             for sel, tag in (([j for j in sj if not groups[j].window and not groups[j].window_value], 0),
                              ([j for j in sj if groups[j].window_value], UNIT_VALUE_ONLY),
                              ([j for j in sj if groups[j].window], UNIT_WINDOW)):
@@ -1097,31 +1197,34 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                         vec //= 2
                     plan_units.append((KIND_TAPE, vec, JIT_BLOCK, tag, sel))
             members = [j for j in members if j not in set(sj)]
-        for plain in (True, False):
-            tm = [j for j in members if groups[j].kind == KIND_TAPE and
-                  plain == (not groups[j].flags & (FLAG_SELFREF | FLAG_SERIAL))]
-            if not tm:
-                continue
-            regs = max(groups[j].n_regs for j in tm)
-            bs = block_size_for(regs)
-            if regs * bs * 8 > SMEM_LIMIT:
-                raise ValueError(f"wave {w}: template needs {regs} scratch registers, more than shared memory holds")
-            vec = 1
-            if plain:
-                forced = int(os.environ.get("SGB_TAPE_VEC", "0"))
-                for v in (TAPE_VECS if not forced else (forced,)):
-                    if regs * v * bs * 8 <= VEC_SMEM_BUDGET or v == 1:
-                        vec = v
-                        break
-            plan_units.append((KIND_TAPE, vec, bs, regs, tm))
-        codes: dict[int, list] = {}
-        for j in members:
-            if groups[j].kind == KIND_SOP:
-                codes.setdefault(sop_unit_code(groups[j], compress), []).append(j)
-        for code in sorted(codes):  # one persistent launch per kernel body
-            plan_units.append((KIND_SOP, code, SOP_BLOCK, 0, codes[code]))
-        for kind, variant, bs, regs, ms in plan_units:
-            utag, jit_unit = 0, False
+        hw_units = []  # hand-written units: (kind, variant, block, scratch regs, groups, value-mode only)
+        for twin in (False, True):  # value-only twins of CSR-window members get units of their own
+            sub = [j for j in members if groups[j].window_value == twin]
+            for plain in (True, False):
+                tm = [j for j in sub if groups[j].kind == KIND_TAPE and
+                      plain == (not groups[j].flags & (FLAG_SELFREF | FLAG_SERIAL))]
+                if not tm:
+                    continue
+                regs = max(groups[j].n_regs for j in tm)
+                bs = block_size_for(regs)
+                if regs * bs * 8 > SMEM_LIMIT:
+                    raise ValueError(f"wave {w}: template needs {regs} scratch registers, more than shared memory holds")
+                vec = 1
+                if plain:
+                    for v in TAPE_VECS:
+                        if regs * v * bs * 8 <= VEC_SMEM_BUDGET or v == 1:
+                            vec = v
+                            break
+                hw_units.append((KIND_TAPE, vec, bs, regs, tm, twin))
+            codes: dict[int, list] = {}
+            for j in sub:
+                if groups[j].kind == KIND_SOP:
+                    codes.setdefault(sop_unit_code(groups[j], compress), []).append(j)
+            for code in sorted(codes):  # one persistent launch per kernel body
+                hw_units.append((KIND_SOP, code, SOP_BLOCK, 0, codes[code], twin))
+        plan_units = [u + (False,) for u in plan_units] + hw_units
+        for kind, variant, bs, regs, ms, twin in plan_units:
+            utag, jit_unit = (UNIT_VALUE_ONLY if twin else 0), False
             if kind == KIND_TAPE and bs == JIT_BLOCK and regs in (0, UNIT_VALUE_ONLY, UNIT_WINDOW) \
                     and all(not groups[j].flags & (FLAG_SELFREF | FLAG_SERIAL) for j in ms) and jit:
                 utag, regs, jit_unit = regs, 0, True
@@ -1178,8 +1281,11 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                                 n_cb += cb.size
                                 n_co += co.size
                 # output positions
-                if g.window:
-                    win_opos[gi] = g.opos[0]
+                if g.wpos is not None:  # CSR-window member: positions inside its window
+                    flags |= FLAG_WPOS16
+                    rec["oo_off"] = n_oo
+                    ooffs.append(g.wpos.reshape(-1))
+                    n_oo += g.wpos.size
                 if g.opos is not None:
                     comp = [compress_column(row, allow_none=True) for row in g.opos]
                     if all(c is not None for c in comp):
@@ -1202,13 +1308,13 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                     starts = np.arange(0, g.n, tile, dtype=np.int64)
                 unit_tiles.append(np.stack([np.full(starts.size, gi, np.int64), starts], axis=1))
                 unit_keys.append(_tile_keys(g, starts, tile))
-            if utag == UNIT_WINDOW:  # the unit's tile range is its window range [w0, w1) in win_off
-                w0 = len(win_off) - 1
-                _window_pieces(packed, list(range(g_begin, len(order_groups))), n_out_total, win_pieces, win_off,
-                               win_opos)
-                window_units.append((len(units), w0, len(win_off) - 1))
-                units.append((w, kind, variant, g_begin, len(order_groups), w0, len(win_off) - 1, bs, regs,
-                              UNIT_CSR_ONLY | UNIT_JIT | UNIT_WINDOW))
+            if utag == UNIT_WINDOW:  # the unit's "tiles" are its windows [0, n_win)
+                if window_units or len(order_groups) - g_begin != windows.pieces.shape[1]:
+                    raise AssertionError("one CSR-window unit holding every member")
+                n_win = windows.k.size - 1
+                window_units.append((len(units), 0, n_win))
+                units.append((w, kind, variant, g_begin, len(order_groups), 0, n_win, bs,
+                              8 * int(np.diff(windows.k).max(initial=0)), UNIT_CSR_ONLY | UNIT_JIT | UNIT_WINDOW))
                 jit_units.append(len(units) - 1)
                 continue
             else:
@@ -1279,10 +1385,11 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         exact=exact,
     )
     dp.csr_layout = sorted(imajor)
-    dp.win_pieces = np.asarray(win_pieces, np.int32).reshape(-1, 4)
-    dp.win_off = np.asarray(win_off, np.int64)
+    dp.windows = windows
+    dp.window_members = list(window) if window is not None else []
     dp.window_units = window_units
-    if jit_units:
+    dp.jit_tapes, dp.jit_imms = jit_tapes, jit_imms
+    if jit_units and jit_compile:
         from . import jit as _jit
 
         dp.jit_cubin, dp.jit_source = _jit.specialise(dp, jit_tapes, jit_imms, jit_units)

@@ -80,6 +80,8 @@ def csr_wave_traffic(plan, lowered, batch: int = 1) -> list[LaunchTraffic]:
     outs = np.asarray(plan.outputs, dtype=np.int64)
     uniq = unique_addresses(outs)
     waves = max([lowered.n_waves] + [w + 1 for w, _, _ in lowered.copies])
+    wn = getattr(lowered, "windows", None)
+    members = set(getattr(lowered, "window_members", []) or [])
     out = []
     for w in range(waves):
         idx = con = wr = ops = 0
@@ -92,7 +94,9 @@ def csr_wave_traffic(plan, lowered, batch: int = 1) -> list[LaunchTraffic]:
             con += 8 * len(kp.const_vars) * kp.instances
             ops += kl.ops * kp.instances * batch
             lo, hi = kp.dest_base, kp.dest_base + kp.n_roots * kp.instances
-            if kl.flags & 16:  # FLAG_STREAM: only the outputs are stored
+            if kl.index in members:  # CSR windows: every output is written once, below
+                pass
+            elif kl.flags & 16:  # FLAG_STREAM: only the outputs are stored
                 a, b = np.searchsorted(uniq, [lo, hi])
                 wr += 8 * int(b - a) * batch
             else:
@@ -103,6 +107,12 @@ def csr_wave_traffic(plan, lowered, batch: int = 1) -> list[LaunchTraffic]:
             if cw == w:
                 idx += 4 * src.size
                 wr += 8 * src.size * batch
+                addrs.append(unique_addresses(src))
+        if wn is not None and w == lowered.n_waves - 1:  # the window unit: copies + every output once
+            src = np.asarray(wn.copy_src, np.int64)
+            idx += 4 * src.size
+            wr += 8 * int(outs.size) * batch
+            if src.size:
                 addrs.append(unique_addresses(src))
         reads = int(unique_addresses(np.concatenate(addrs)).size) if addrs else 0
         out.append(LaunchTraffic(f"csr_wave{w}", idx, con, 8 * reads * batch, wr, ops))

@@ -81,8 +81,13 @@ class _Desc(ctypes.Structure):
         ("jit_cubin_size", ctypes.c_int64),
         ("win_pieces", ctypes.c_void_p),
         ("n_win_pieces", ctypes.c_int64),
-        ("win_off", ctypes.c_void_p),
-        ("n_win_off", ctypes.c_int64),
+        ("win_k", ctypes.c_void_p),
+        ("n_win_k", ctypes.c_int64),
+        ("win_copy", ctypes.c_void_p),
+        ("n_win_copy", ctypes.c_int64),
+        ("copy_src", ctypes.c_void_p),
+        ("copy_pos", ctypes.c_void_p),
+        ("n_copy", ctypes.c_int64),
     ]
 
 
@@ -198,9 +203,14 @@ class DevicePlan:
             opos32=np.ascontiguousarray(lw.opos32, np.uint32),
             outs=np.ascontiguousarray(lw.outputs, np.int64),
             cubin=np.frombuffer(lw.jit_cubin, dtype=np.uint8).copy() if lw.jit_cubin else np.zeros(0, np.uint8),
-            wpieces=np.ascontiguousarray(lw.win_pieces if lw.win_pieces is not None else np.zeros((0, 4)),
-                                         np.int32).reshape(-1, 4),
-            woff=np.ascontiguousarray(lw.win_off if lw.win_off is not None else np.zeros(1), np.int64),
+        )
+        wn = getattr(lw, "windows", None)
+        keep.update(
+            wpieces=np.ascontiguousarray(wn.pieces if wn is not None else np.zeros((0, 2)), np.int32).reshape(-1, 2),
+            wk=np.ascontiguousarray(wn.k if wn is not None else np.zeros(0), np.int64),
+            wcopy=np.ascontiguousarray(wn.copy_off if wn is not None else np.zeros(0), np.int64),
+            csrc=np.ascontiguousarray(wn.copy_src if wn is not None else np.zeros(0), np.uint32),
+            cpos=np.ascontiguousarray(wn.copy_pos if wn is not None else np.zeros(0), np.uint16),
         )
         d = _Desc(
             value_array_size=self.value_array_size, input_count=self.input_count,
@@ -218,7 +228,9 @@ class DevicePlan:
             n_opos32=keep["opos32"].size, outputs=_ptr(keep["outs"]), n_outputs=keep["outs"].size,
             jit_cubin=_ptr(keep["cubin"]), jit_cubin_size=keep["cubin"].size,
             win_pieces=_ptr(keep["wpieces"]), n_win_pieces=keep["wpieces"].shape[0],
-            win_off=_ptr(keep["woff"]), n_win_off=keep["woff"].size,
+            win_k=_ptr(keep["wk"]), n_win_k=keep["wk"].size, win_copy=_ptr(keep["wcopy"]),
+            n_win_copy=keep["wcopy"].size, copy_src=_ptr(keep["csrc"]), copy_pos=_ptr(keep["cpos"]),
+            n_copy=keep["csrc"].size,
         )
         torch.cuda.init()
         _check(self._lib.sgb_plan_create(ctypes.byref(d), self.device, ctypes.byref(self._handle)),

@@ -158,6 +158,33 @@ def _tile_instances(dp, unit, gi, g, n):
     return i[i < n]
 
 
+def _run_windows(dp, unit, x, out):
+    """The CSR-window unit (jit.window_source): per window, copies then every member's piece, each
+    result at its FLAG_WPOS16 position; the window is then stored at win_k[w]."""
+    wn = dp.windows
+    g0, g1 = unit["group_begin"], unit["group_end"]
+    for w in range(wn.k.size - 1):
+        k0, k1 = int(wn.k[w]), int(wn.k[w + 1])
+        buf = np.full(k1 - k0, np.nan)
+        c0, c1 = int(wn.copy_off[w]), int(wn.copy_off[w + 1])
+        buf[wn.copy_pos[c0:c1].astype(np.int64)] = x[wn.copy_src[c0:c1].astype(np.int64)]
+        for gi in range(g0, g1):
+            a, cnt = (int(v) for v in wn.pieces[w, gi - g0])
+            if not cnt:
+                continue
+            g = dp.groups[gi]
+            i = np.arange(a, a + cnt, dtype=np.int64)
+            n = int(g["n"])
+
+            def wstore(g_, r, i_, v):
+                o = dp.ooff[int(g_["oo_off"]) + r * n + i_].astype(np.int64)
+                m = o != 0xFFFF
+                buf[o[m]] = np.asarray(v)[m] if np.ndim(v) else v
+
+            _reg_tape(dp, gi, g, x, i, wstore)
+        out[k0:k1] = buf
+
+
 def _run(dp, inputs, csr: bool, by_tiles: bool = False):
     x = np.zeros(dp.value_array_size, np.float64)
     x[: dp.input_count] = inputs
@@ -167,6 +194,11 @@ def _run(dp, inputs, csr: bool, by_tiles: bool = False):
         # groups of one unit are independent; units run in wave order
         unit = dp.unit(u)
         if unit["flags"] & L.UNIT_CSR_ONLY and not csr:
+            continue
+        if unit["flags"] & L.UNIT_VALUE_ONLY and csr:
+            continue
+        if unit["flags"] & L.UNIT_WINDOW:
+            _run_windows(dp, unit, x, out)
             continue
         for gi in range(unit["group_begin"], unit["group_end"]):
             g = dp.groups[gi]
@@ -178,6 +210,9 @@ def _run(dp, inputs, csr: bool, by_tiles: bool = False):
                     _tape(dp, g, x, np.array([i]), store)
                 continue
             i = _tile_instances(dp, unit, gi, g, n) if by_tiles else np.arange(n, dtype=np.int64)
+            if unit["flags"] & L.UNIT_JIT:  # specialised unit: the group's register tape (jit.group_parts)
+                _reg_tape(dp, gi, g, x, i, store)
+                continue
             if g["kind"] == L.KIND_SOP:
                 nt = int(dp.sop[2 * g["sop_off"]])
                 ng = int(dp.sop[2 * g["sop_off"] + 1])
@@ -205,9 +240,9 @@ def run_values(dp, inputs) -> np.ndarray:
 
 
 def run_csr(dp, inputs, by_tiles: bool = False) -> np.ndarray:
-    """CSR mode: direct stores by the producing groups and copy groups, or value mode + gather.
-    ``by_tiles``: evaluate only the instances the tile table covers (output-sharded plans)."""
-    direct = bool(np.any(dp.groups["flags"] & (L.FLAG_OPOS16 | L.FLAG_OPOS32)))
+    """CSR mode: direct stores by the producing groups and copy groups, CSR windows, or value mode +
+    gather.  ``by_tiles``: evaluate only the instances the tile table covers (output-sharded plans)."""
+    direct = bool(np.any(dp.groups["flags"] & (L.FLAG_OPOS16 | L.FLAG_OPOS32 | L.FLAG_WPOS16)))
     if not direct:
         return _run(dp, inputs, csr=False, by_tiles=by_tiles)[0][dp.outputs]
     return _run(dp, inputs, csr=True)[1]
@@ -270,3 +305,56 @@ def _tape(dp, g, x, i, store):
                 else:
                     raise ValueError(f"bad op {op}")
             R[d] = v
+
+
+def _binop(op, A, B, C):
+    if op == L.T_MUL:
+        return A * B
+    if op == L.T_ADD:
+        return A + B
+    if op == L.T_SUB:
+        return A - B
+    if op == L.T_DIV:
+        return A / B
+    if op == L.T_MADD:
+        return (A * B) + C
+    if op == L.T_MSUB:
+        return (A * B) - C
+    if op == L.T_RMSUB:
+        return C - (A * B)
+    raise ValueError(op)
+
+
+def _reg_tape(dp, gi, g, x, i, store):
+    """A specialised unit's group: its register tape (lower.compile_tape), as jit.group_parts unrolls it."""
+    tape = dp.jit_tapes[gi]
+    imms = dp.jit_imms[gi]
+    S, K = int(g["n_slots"]), int(g["n_const"])
+    R = {}
+    for s_, a in enumerate(_decode_addrs(dp, g, i)):
+        R[s_] = x[a].copy()
+    for k in range(K):
+        R[S + k] = _const(dp, g, k, i).copy()
+    slow = {0: math.sin, 1: math.cos, 2: math.exp, 3: math.log}
+    z = np.zeros(len(i))
+    for op, na, nb, dst, a, b, c, aux in tape.tolist():
+        with np.errstate(all="ignore"):
+            if op == L.T_ST:
+                store(g, aux, i, R[a])
+                continue
+            A = -R.get(a, z) if na else R.get(a, z)
+            B = -R.get(b, z) if nb else R.get(b, z)
+            if op == L.T_IMM:
+                v = np.full(len(i), imms[aux])
+            elif op == L.T_NEG:
+                v = -R[a]
+            elif op == L.T_SQRT:
+                v = np.sqrt(R[a])
+            elif op == L.T_SEL:
+                v = np.where(R[a] < 0.0, R[b], R[c])
+            elif op == L.T_SLOW:
+                kind, k = aux >> 16, aux & 0xFFFF
+                v = _dd_powi(R[a], k) if kind == 4 else _vec(slow[kind], R[a])
+            else:
+                v = _binop(op, A, B, R.get(c, z))
+        R[dst] = v

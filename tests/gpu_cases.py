@@ -31,11 +31,22 @@ JIT_CASES = ["lmlt_w7", "lmlt_w12", "prog_energy-hessian_4x4_tag", "transc37", "
 LAYOUT_CASES = ["fem_nh_m1", "fem_nh_m2", "prog_energy-hessian_4x4_tag", "arap_w3", "arap_w5", "prog_cotan_4x4_tag",
                 "lmlt_w7", "transc37", "selfref", "toy256_interleaved"]
 
+# CSR windows forced on (csr_window=True): the fixtures whose last wave qualifies with at most 25
+# members (the default lowering applies windows only to big plans, lower.lower_plan)
+WINDOW_CASES = ["acc1_expr2_s1", "acc9_lpow3_nosimp", "acc9_lpow3_simp", "arap_w3", "arap_w5", "cli_expr2_nosimp",
+                "cli_expr2_simp", "cli_lpow2_simp", "cli_lpow3_simp", "cli_lpow4_nosimp", "cli_lpow4_simp", "coord96",
+                "coord96_baseline", "lmlt_w12", "lmlt_w3", "lmlt_w4", "lmlt_w7", "product_n24_s3_tcompl0",
+                "prog_lpow3_6x6_tag", "select_edge", "spgemm_n2000_k10", "spgemm_n60_k4", "tagged_pair", "toy256",
+                "toy256_interleaved", "transc37", "transc37_nosimp"]
+
 
 def lowering_specs(names: list[str]) -> list[tuple[str, tuple]]:
     specs = [(n, ()) for n in names]
     specs += [(n, (("jit_min_n", 0),)) for n in JIT_CASES]
     specs += [(n, (("jit_min_n", 0), ("relayout", r))) for n in LAYOUT_CASES for r in ("all", "auto")]
+    specs += [(n, (("csr_window", False),)) for n in names]
+    specs += [(n, (("csr_window", True),)) for n in WINDOW_CASES]
+    specs += [(n, (("direct_csr", True),)) for n in names]
     return specs
 
 

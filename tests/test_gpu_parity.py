@@ -17,7 +17,7 @@ import numpy as np
 import pytest
 
 from conftest import bits, device_plan, golden_case, lowered
-from gpu_cases import JIT_CASES, LAYOUT_CASES
+from gpu_cases import JIT_CASES, LAYOUT_CASES, WINDOW_CASES
 
 pytestmark = pytest.mark.gpu
 
@@ -149,12 +149,16 @@ def test_device_resident_run_on_torch(golden):
     assert np.array_equal(bits(out.cpu().numpy()), bits(x.cpu().numpy()[np.asarray(golden.plan.outputs, np.int64)]))
 
 
-@pytest.mark.parametrize("mode", ["gather", "direct", "interpreter"])
+@pytest.mark.parametrize("mode", ["gather", "window", "direct", "interpreter"])
 def test_csr_mode(golden, mode):
-    """sgb_run_csr: value waves + gather; direct scattered stores; the hand-written kernels only."""
+    """sgb_run_csr: value waves + gather; CSR windows (the last wave assembles the CSR array in shared
+    memory, lower._csr_windows); direct scattered stores; the hand-written kernels only."""
     import torch
 
-    kw = {"gather": {}, "direct": dict(direct_csr=True), "interpreter": dict(jit=False)}[mode]
+    if mode == "window" and golden.name not in WINDOW_CASES:
+        pytest.skip("CSR windows forced on: the fixtures of gpu_cases.WINDOW_CASES")
+    kw = {"gather": dict(csr_window=False), "window": dict(csr_window=True), "direct": dict(direct_csr=True),
+          "interpreter": dict(jit=False)}[mode]
     dp = device_plan(golden.name, **kw)
     x = dp.new_values(golden.inputs)
     out = torch.full((len(golden.plan.outputs),), float("nan"), dtype=torch.float64, device=x.device)
@@ -166,6 +170,18 @@ def test_csr_mode(golden, mode):
     cmp = cmp_outputs(golden)
     for got in (first, out.cpu().numpy()):
         assert cmp(got)
+    if mode == "window" and dp.lowered.windows is not None:
+        assert dp.csr_units <= dp.units  # no gather launch
+        assert cmp(dp.run_outputs_host(golden.inputs))
+        if dp.lowered.needs_zero != 2:
+            graph = dp.capture_csr(dp.new_values(golden.inputs), out)
+            out.fill_(float("nan"))
+            graph.replay()
+            torch.cuda.synchronize()
+            assert cmp(out.cpu().numpy())
+        x = dp.new_values(golden.inputs)  # value mode runs the members' value-only twins
+        dp.run_values(x)
+        check(x.cpu().numpy(), golden)
 
 
 @pytest.mark.parametrize("name", JIT_CASES)

@@ -26,6 +26,54 @@ def test_emulated_csr_mode_matches_reference_outputs(golden):
     assert np.array_equal(bits(out), bits(golden.outputs))
 
 
+@pytest.mark.parametrize("jit_min_n", [None, 0])
+def test_emulated_csr_windows_match_reference_outputs(golden, jit_min_n):
+    """CSR windows (lower._csr_windows, jit.window_source): every output lands exactly once, from its
+    member's piece or the window's copy list, bit for bit; plans that do not qualify keep the gather."""
+    dp = lower_plan(golden.plan, csr_window=True, jit_min_n=jit_min_n, jit_compile=False)
+    out = emu.run_csr(dp, golden.inputs)
+    want = golden.outputs
+    if golden.exact:
+        assert np.array_equal(bits(out), bits(want))
+    else:
+        assert np.allclose(out, want, rtol=1e-12, atol=1e-12)
+    if dp.windows is not None:
+        wn = dp.windows
+        assert wn.k[0] == 0 and wn.k[-1] == len(golden.plan.outputs) and np.all(np.diff(wn.k) > 0)
+        assert np.diff(wn.k).max() <= L.WIN_MAX
+        # every position written once: copies + member results partition each window
+        hits = np.zeros(len(golden.plan.outputs), np.int64)
+        u = dp.unit(dp.window_units[0][0])
+        for w in range(wn.k.size - 1):
+            k0 = int(wn.k[w])
+            c0, c1 = wn.copy_off[w], wn.copy_off[w + 1]
+            np.add.at(hits, k0 + wn.copy_pos[c0:c1].astype(np.int64), 1)
+            for gi in range(u["group_begin"], u["group_end"]):
+                a, cnt = (int(v) for v in wn.pieces[w, gi - u["group_begin"]])
+                g = dp.groups[gi]
+                n = int(g["n"])
+                for r in range(int(g["n_roots"])):
+                    o = dp.ooff[int(g["oo_off"]) + r * n + a: int(g["oo_off"]) + r * n + a + cnt].astype(np.int64)
+                    np.add.at(hits, k0 + o[o != 0xFFFF], 1)
+        assert np.all(hits == 1)
+
+
+def test_csr_windows_on_the_c2_builder_plan():
+    """On the mesh builder's L.M.L^T+A plan the windows qualify, hold ~WIN_ROWS rows, and the anchor
+    pieces are one block pass."""
+    from paper_2110_12865_b200.programs.mesh import build_lmlt_plan, lmlt_inputs
+
+    from oracle import oracle
+
+    plan, _, _ = build_lmlt_plan(40)
+    dp = lower_plan(plan, csr_window=True, jit_compile=False)
+    assert dp.windows is not None and len(dp.window_units) == 1
+    cnt = dp.windows.pieces[:, :, 1]
+    assert np.median(cnt.max(axis=1)) <= 256
+    ins = lmlt_inputs(40, seed=3)
+    assert np.array_equal(bits(emu.run_csr(dp, ins)), bits(oracle.run_outputs(plan, ins)))
+
+
 def test_waves_respect_producers(golden):
     plan = golden.plan
     waves = compute_waves(plan)
