@@ -173,6 +173,11 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
              else f"{int(rec['c_off']) + k * n}LL + {i}")
         loads.append(f"const double k{k}{sfx} = {G(f'__ldcs(T.con + {e})', '0.0')};")
         reg[S + k] = f"k{k}{sfx}"
+    if window:  # window positions (FLAG_WPOS16) load with the operands, not after the compute
+        oo_off = int(rec["oo_off"])
+        for r in range(int(rec["n_roots"])):
+            loads.append(f"const u16 wp{r}{sfx} = "
+                         f"{G(f'__ldcs(T.ooff + {oo_off + r * n}LL + {i})', '(u16)0xFFFF')};")
     stream = bool(flags & L.FLAG_STREAM)
     opos = lambda r: _out_pos(rec, r, i)  # noqa: E731
     for j, t in enumerate(tape.tolist()):
@@ -181,8 +186,7 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
         B = ("-" if nb else "") + reg.get(b, "0.0")
         C = reg.get(c, "0.0")
         if op == L.T_ST and window:  # CSR-window member: FLAG_WPOS16 position in the block's window
-            comp.append(f"if (ok{sfx}) {{ const u16 o = __ldcs(T.ooff + {int(rec['oo_off']) + aux * n}LL + {i}); "
-                        f"if (o != 0xFFFF) buf[o] = {reg[a]}; }}")
+            comp.append(f"if (wp{aux}{sfx} != 0xFFFF) buf[wp{aux}{sfx}] = {reg[a]};")
             continue
         if op == L.T_ST and stage is not None:
             comp.append(f"if (ok{sfx}) stage_[({stage}) * {L.stage_stride(int(rec['n_roots']))} + {aux}] = {reg[a]};")
@@ -420,8 +424,8 @@ def compile_cubin(src: str, name: str = "sgb_tape.cu") -> bytes:
     return cubin
 
 
-WINDOW_LOADS = 32  # loads in flight per thread across the members of one chunk of a window kernel
-COPY_UNROLL = 4  # copied outputs per thread in flight
+WINDOW_LOADS = 24  # loads in flight per thread across the members of one chunk of a window kernel
+COPY_UNROLL = 8  # copied outputs per thread in flight
 
 
 def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
@@ -451,7 +455,7 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
     if cur:
         chunks.append(cur)
     B = JIT_BLOCK
-    out = [f'extern "C" __global__ void __launch_bounds__({B}) sgb_window_u{u}(',
+    out = [f'extern "C" __global__ void __launch_bounds__({B}, 3) sgb_window_u{u}(',
            "    Tables T, const int2 *pieces, const i64 *win_k, const i64 *copy_off, const u32 *copy_src,",
            "    const u16 *copy_pos, i64 n_win, const double *x, double *out) {",
            "  extern __shared__ double buf[];",

@@ -3,7 +3,7 @@
 TAG=${1:-win}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
-( time timeout 900 python -m pytest tests -m gpu -q -x --durations=15 -p no:cacheprovider ) > $OUT/pytest_gpu.log 2>&1
+( time timeout 900 python -m pytest tests -m gpu -q --durations=15 -p no:cacheprovider ) > $OUT/pytest_gpu.log 2>&1
 echo "pytest rc=$?" >> $OUT/status.txt
 for W in 1 0; do
   SGB_CSR_WINDOW=$W timeout 600 python bench.py --steps 20 --warmup 5 --e2e-steps 4 --no-cpu-baseline > $OUT/c2_win$W.json 2> $OUT/c2_win$W.err
