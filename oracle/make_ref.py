@@ -3,14 +3,16 @@
 Generates the reference's OWN native evaluator for the bench plans: the C99
 translation unit that ``sparsegen.emit.emit_kernel_source``
 (/root/reference/pkg/src/sparsegen/emit.py:153-195) emits for a plan, written
-to ``oracle/_ref/<key>.c`` together with a fingerprint of the plan it was
+to ``oracle/ref_emitted/<key>.c`` together with a fingerprint of the plan it was
 emitted for.  bench.py compiles it on the GPU box with the reference's flags
 (``cc -O3 -ffp-contract=off -fPIC -shared ... -lm``, emit.py:220, plus
 ``-fopenmp`` for the all-core figure) and times ``sg_run`` as the
 ``cpu_baseline`` (kind "reference").
 
 Runs only where /root/reference exists (this build container);
-``oracle/_ref/`` is git-ignored but travels to the GPU box with gpurun.
+The emitted sources are committed (``oracle/ref_emitted/``, a few hundred KB): they are the
+reference's output for the bench plans, like the golden fixtures, so the reference arm never has
+to fall back to the restated emitter on a box without /root/reference.
 The emitter is used unmodified: it reads only the plan fields
 (codegen.py:56-98), so the template-instancing builder's plans go through it
 as they are.
@@ -30,7 +32,7 @@ import numpy as np
 
 HERE = Path(__file__).resolve().parent
 ROOT = HERE.parent
-REF_DIR = HERE / "_ref"
+REF_DIR = HERE / "ref_emitted"
 REFERENCE_SRC = Path("/root/reference/pkg/src")
 
 
@@ -108,14 +110,13 @@ def main():
             continue
         src = emit_for_plan(load_plan(ROOT / "tests" / "golden" / name), name)
         print(f"wrote {src}")
-    cfgs = [argparse.Namespace(config="c2", w=w) for w in (args.w, 200)]  # C2 and the C5 plan
-    cfgs += [argparse.Namespace(config="c3", m=55), argparse.Namespace(config="c4", w4=708)]
-    for ns in cfgs:
-        key = bench.workload_key(ns)
+    ns = bench.parse_args(["--w", str(args.w)])
+    for cfg in ("c2", "c5", "c3", "c4"):
+        key = bench.workload_key(cfg, ns)
         if args.if_stale and up_to_date(key):
-            print(f"oracle/_ref/{key}.c is up to date")
+            print(f"oracle/ref_emitted/{key}.c is up to date")
             continue
-        key, plan, _, _ = bench.build_workload(ns, 0, 1)
+        key, plan = bench.build_workload(cfg, ns)
         src = emit_for_plan(plan, key)
         print(f"wrote {src} ({src.stat().st_size / 1e6:.1f} MB) for {key}")
 

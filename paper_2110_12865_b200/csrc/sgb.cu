@@ -983,8 +983,12 @@ int sgb_plan_units(const sgb_plan *p, int csr) {
   if (!p) return 0;
   const bool direct = csr && p->direct_csr;
   int k = 0;
-  for (const Unit &u : p->units)
-    if (direct || !(u.flags & UNIT_CSR_ONLY)) ++k;
+  for (const Unit &u : p->units) {
+    if ((u.flags & UNIT_CSR_ONLY) && !direct) continue;  // CSR-only units run in direct CSR mode only
+    if ((u.flags & UNIT_VALUE_ONLY) && direct) continue;  // value-mode twins of CSR-window members
+    if (u.t1 <= u.t0) continue;                           // nothing to launch
+    ++k;
+  }
   return k + (csr && !p->direct_csr && p->n_out > 0 ? 1 : 0);
 }
 
@@ -1413,8 +1417,13 @@ static int launch_wave(sgb_plan *p, int wave, double *x, int64_t ld, int64_t bat
   if (wave < 0 || wave >= (int)p->wave_units.size()) return 0;
   std::vector<const Unit *> us;
   us.reserve(p->wave_units[wave].size());
-  for (int k : p->wave_units[wave])
-    if (csr || !(p->units[k].flags & UNIT_CSR_ONLY)) us.push_back(&p->units[k]);
+  for (int k : p->wave_units[wave]) {
+    const Unit &u = p->units[k];
+    if (!csr && (u.flags & UNIT_CSR_ONLY)) continue;
+    if (csr && !batched && (u.flags & UNIT_VALUE_ONLY)) continue;  // twins of CSR-window members
+    if ((batched ? u.bt1 - u.bt0 : u.t1 - u.t0) <= 0) continue;
+    us.push_back(&u);
+  }
   const int n = (int)us.size();
   if (n == 0) return 0;
   const int k_aux = n - 1 < (int)p->aux.size() ? n - 1 : (int)p->aux.size();

@@ -426,6 +426,7 @@ def compile_cubin(src: str, name: str = "sgb_tape.cu") -> bytes:
 
 WINDOW_LOADS = 24  # loads in flight per thread across the members of one chunk of a window kernel
 COPY_UNROLL = 8  # copied outputs per thread in flight
+WINDOW_MIN_BLOCKS = 3  # resident windows per SM the window kernel's register budget is sized for
 
 
 def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
@@ -455,7 +456,7 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
     if cur:
         chunks.append(cur)
     B = JIT_BLOCK
-    out = [f'extern "C" __global__ void __launch_bounds__({B}, 3) sgb_window_u{u}(',
+    out = [f'extern "C" __global__ void __launch_bounds__({B}, {WINDOW_MIN_BLOCKS}) sgb_window_u{u}(',
            "    Tables T, const int2 *pieces, const i64 *win_k, const i64 *copy_off, const u32 *copy_src,",
            "    const u16 *copy_pos, i64 n_win, const double *x, double *out) {",
            "  extern __shared__ double buf[];",

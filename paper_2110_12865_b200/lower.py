@@ -762,6 +762,7 @@ def _window_members(plan, lowered, opos, n_waves):
 WIN_ROWS = 240  # anchor instances per CSR window (block of JIT_BLOCK threads: 16 lanes of slack)
 WIN_MAX = 7936  # outputs per CSR window (62 KB of shared memory: 3 windows resident per SM)
 WIN_MIN = 1024  # windows are not cut shorter than this unless the anchor forces it
+WIN_MAX_LOADS = 32  # default lowering: windows only when every member loads at most this many slots
 
 
 @dataclass
@@ -1092,8 +1093,11 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     opos, res_k, res_addr = _output_map(plan, lowered, waves)
     window = _window_members(plan, lowered, opos, n_waves) if csr_window and not direct_csr else None
     if window is not None and window_policy == "auto" and (
-            len(window) > JIT_MAX_WAVE_GROUPS or max(plan.kernels[k].instances for k in window) < jit_min_n):
-        window = None  # small plans: the gather costs nothing, NVRTC time would
+            len(window) > JIT_MAX_WAVE_GROUPS or max(plan.kernels[k].instances for k in window) < jit_min_n
+            or max(len(plan.kernels[k].pos_vars) + len(plan.kernels[k].const_vars) for k in window) > WIN_MAX_LOADS):
+        # small plans: the gather costs nothing, NVRTC time would; wide templates (C4's rhs, 38-90
+        # loads per instance) need the register file the window kernel's three resident blocks cannot give
+        window = None
     if window is not None:
         # CSR windows: only last-wave members keep output positions; every other output
         # (inputs, duplicates, earlier waves' results) is a copy piece of its window

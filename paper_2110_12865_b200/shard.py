@@ -82,6 +82,25 @@ def shard_outputs(total: int, world: int, rank: int) -> tuple[int, int]:
     return first, first + count
 
 
+def shard_bounds(lowered, n_out: int, world: int, rank: int) -> tuple[int, int]:
+    """[lo, hi) of ``rank``'s CSR outputs: the even split of ``shard_outputs``, moved to the nearest
+    CSR-window boundary when the plan assembles its outputs in windows (lower._csr_windows), so
+    every window belongs to one rank."""
+    import numpy as np
+
+    wn = getattr(lowered, "windows", None)
+    if wn is None:
+        return shard_outputs(n_out, world, rank)
+    k = np.asarray(wn.k, np.int64)
+
+    def snap(p):
+        j = int(np.argmin(np.abs(k - p)))
+        return int(k[j])
+
+    lo, hi = shard_outputs(n_out, world, rank)
+    return (0 if rank == 0 else snap(lo)), (n_out if rank == world - 1 else snap(hi))
+
+
 def output_cone(plan, lo: int, hi: int):
     """Per plan kernel, the instances the CSR outputs [lo, hi) depend on (bool mask of length N).
 
@@ -129,8 +148,15 @@ def shard_device_plan(plan, lowered, lo: int, hi: int):
         raise ValueError("output sharding needs the reference value-array layout (csr_layout off)")
     if int(lowered.needs_zero) == 2:
         raise ValueError("output sharding needs a plan without reads before writes")
-    if np.any(lowered.groups["flags"] & (L.FLAG_OPOS16 | L.FLAG_OPOS32)) or lowered.window_units:
-        raise ValueError("output sharding supports the gather output mode only")
+    if np.any(lowered.groups["flags"] & (L.FLAG_OPOS16 | L.FLAG_OPOS32)):
+        raise ValueError("output sharding supports the gather and CSR-window output modes only")
+    wn = getattr(lowered, "windows", None)
+    w0 = w1 = 0
+    if wn is not None:  # keep the windows [w0, w1) that make up [lo, hi), re-based to the shard
+        k = np.asarray(wn.k, np.int64)
+        w0, w1 = int(np.searchsorted(k, lo)), int(np.searchsorted(k, hi))
+        if k[w0] != lo or k[w1] != hi:
+            raise ValueError("a CSR-window plan shards at window boundaries (shard_bounds)")
     masks = output_cone(plan, lo, hi)
     by_base = {int(kp.dest_base): k for k, kp in enumerate(plan.kernels) if kp.instances}
     tiles = np.asarray(lowered.tiles).reshape(-1, 2)
@@ -138,6 +164,9 @@ def shard_device_plan(plan, lowered, lo: int, hi: int):
     keep_t, t_cur = [], 0
     for u in range(len(units)):
         ur = lowered.unit(u)
+        if ur["flags"] & L.UNIT_WINDOW:  # its "tiles" are windows
+            units[u, UNIT_TB], units[u, UNIT_TE] = 0, w1 - w0
+            continue
         t = tiles[ur["tile_begin"]: ur["tile_end"]]
         keep = np.zeros(len(t), bool)
         for j, (gi, s) in enumerate(t.tolist()):
@@ -158,8 +187,14 @@ def shard_device_plan(plan, lowered, lo: int, hi: int):
         keep_t.append(kt)
     new_tiles = np.concatenate(keep_t).astype(np.int32) if keep_t else np.zeros((0, 2), np.int32)
     view = _OutputSlice(plan, lo, hi)
+    swn = None
+    if wn is not None:
+        c0, c1 = int(wn.copy_off[w0]), int(wn.copy_off[w1])
+        swn = L.CsrWindows(k=np.asarray(wn.k[w0: w1 + 1], np.int64) - lo, pieces=wn.pieces[w0:w1], wpos=wn.wpos,
+                           copy_off=np.asarray(wn.copy_off[w0: w1 + 1], np.int64) - c0,
+                           copy_src=wn.copy_src[c0:c1], copy_pos=wn.copy_pos[c0:c1])
     lw = dataclasses.replace(lowered, tiles=new_tiles.reshape(-1, 2), units=units,
-                             outputs=np.asarray(lowered.outputs, np.int64)[lo:hi], tiles_alt=None)
+                             outputs=np.asarray(lowered.outputs, np.int64)[lo:hi], tiles_alt=None, windows=swn)
     return view, lw
 
 

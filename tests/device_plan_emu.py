@@ -245,7 +245,7 @@ def run_csr(dp, inputs, by_tiles: bool = False) -> np.ndarray:
     direct = bool(np.any(dp.groups["flags"] & (L.FLAG_OPOS16 | L.FLAG_OPOS32 | L.FLAG_WPOS16)))
     if not direct:
         return _run(dp, inputs, csr=False, by_tiles=by_tiles)[0][dp.outputs]
-    return _run(dp, inputs, csr=True)[1]
+    return _run(dp, inputs, csr=True, by_tiles=by_tiles)[1]
 
 
 def _tape(dp, g, x, i, store):

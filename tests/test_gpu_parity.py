@@ -171,7 +171,7 @@ def test_csr_mode(golden, mode):
     for got in (first, out.cpu().numpy()):
         assert cmp(got)
     if mode == "window" and dp.lowered.windows is not None:
-        assert dp.csr_units <= dp.units  # no gather launch
+        assert dp.csr_launches == dp.launches  # no gather launch
         assert cmp(dp.run_outputs_host(golden.inputs))
         if dp.lowered.needs_zero != 2:
             graph = dp.capture_csr(dp.new_values(golden.inputs), out)
@@ -351,7 +351,7 @@ def test_output_shards_on_device(golden, world):
     """One evaluation with its CSR outputs split (shard.shard_device_plan): each shard's device plan,
     running only the tiles of its producer cone, gives the full evaluation's slice bit for bit."""
     from paper_2110_12865_b200 import DevicePlan
-    from paper_2110_12865_b200.shard import shard_device_plan, shard_outputs
+    from paper_2110_12865_b200.shard import shard_bounds, shard_device_plan
 
     plan = golden.plan
     kw = dict(jit_min_n=0) if golden.name in JIT_CASES else {}
@@ -361,7 +361,7 @@ def test_output_shards_on_device(golden, world):
     full = device_plan(golden.name, **kw).run_outputs_host(golden.inputs)
     n_out = len(plan.outputs)
     for r in range(world):
-        lo, hi = shard_outputs(n_out, world, r)
+        lo, hi = shard_bounds(lw, n_out, world, r)
         if hi == lo:
             continue
         view, slw = shard_device_plan(plan, lw, lo, hi)

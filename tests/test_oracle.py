@@ -70,3 +70,12 @@ def test_reference_emitted_c_matches_fixture_and_port(name, tmp_path):
         assert np.allclose(x, g.values, rtol=1e-12, atol=0, equal_nan=True)
     port = emit_c.compile_plan(g.plan, parallel="pragma", work_dir=tmp_path)(g.inputs)
     assert np.array_equal(bits(port), bits(x))
+
+
+def test_numpy_interpreter_restatement_matches_reference(golden):
+    """oracle/interp_np.py (the timed single-core interpreter leg of bench.py) == interpret_plan, bitwise."""
+    from oracle import interp_np
+
+    x, skipped = interp_np.interpret(golden.plan, golden.inputs)
+    assert skipped == 0
+    assert np.array_equal(bits(x), bits(golden.values))

@@ -85,6 +85,35 @@ def test_gloo_world2_gather_equals_single_process(tmp_path, total):
 # -- one evaluation, output nonzeros partitioned (shard.shard_device_plan) --------------------
 
 
+@pytest.mark.parametrize("name", ["lmlt_w12", "spgemm_n2000_k10", "acc1_expr2_s1"])
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_output_shards_with_csr_windows(name, world):
+    """CSR-window plans shard at window boundaries (shard.shard_bounds): each rank keeps its windows,
+    re-based, and its output cone's tiles; the shards tile the outputs and equal the full evaluation."""
+    from conftest import Golden, bits
+
+    import device_plan_emu as emu
+    from paper_2110_12865_b200 import lower_plan
+    from paper_2110_12865_b200.shard import shard_bounds, shard_device_plan
+
+    g = Golden(name)
+    lw = lower_plan(g.plan, csr_window=True, jit_compile=False)
+    assert lw.windows is not None
+    full = emu.run_csr(lw, g.inputs)
+    n_out = len(g.plan.outputs)
+    covered = []
+    for r in range(world):
+        lo, hi = shard_bounds(lw, n_out, world, r)
+        covered.extend(range(lo, hi))
+        if hi == lo:
+            continue
+        view, slw = shard_device_plan(g.plan, lw, lo, hi)
+        assert slw.windows.k[0] == 0 and slw.windows.k[-1] == hi - lo
+        got = emu.run_csr(slw, g.inputs, by_tiles=True)
+        assert np.array_equal(bits(got), bits(full[lo:hi]))
+    assert covered == list(range(n_out))
+
+
 @pytest.mark.parametrize("name", ["lmlt_w7", "spgemm_n60_k4", "prog_energy-hessian_4x4_tag"])
 @pytest.mark.parametrize("world", [2, 3])
 def test_output_shards_match_full_evaluation(name, world):
