@@ -100,22 +100,31 @@ def _affine(dp, rec, col: int):
     return None
 
 
+def _off(v: int) -> str:
+    """A table offset as a 64-bit literal (the instance index added to it stays u32)."""
+    return f"{int(v)}ull"
+
+
+def _affine_u32(base: int, stride: int, i: str) -> str:
+    return f"({int(base) % 2**32}u + {int(stride) % 2**32}u * {i})"
+
+
 def _column(rec, col: int, i: str = "i", dp=None) -> str:
     """Index expression (u32) of retained column ``col`` for instance ``i``."""
     n = int(rec["n"])
     f = int(rec["flags"])
     aff = _affine(dp, rec, col) if dp is not None else None
-    if aff is not None:
-        return f"(u32)({aff[0]}LL + {aff[1]}LL * {i})"
-    if col == 0 and f & L.FLAG_AFFINE0:
-        return f"(u32)({int(rec['a0_base'])}LL + {int(rec['a0_stride'])}LL * {i})"
+    if aff is None and col == 0 and f & L.FLAG_AFFINE0:
+        aff = int(rec["a0_base"]), int(rec["a0_stride"])
+    if aff is not None:  # modular u32 arithmetic: every decoded address is < 2^32
+        return _affine_u32(aff[0], aff[1], i)
     if f & L.FLAG_W16:
         nch = (n + 31) // 32
-        return (f"(__ldg(T.cbase + {int(rec['cb_off']) + col * nch}LL + ({i} >> 5)) + "
-                f"(u32)__ldcs(T.coff + {int(rec['co_off']) + col * n}LL + {i}))")
+        return (f"(__ldg(T.cbase + {_off(int(rec['cb_off']) + col * nch)} + ({i} >> 5)) + "
+                f"(u32)__ldcs(T.coff + {_off(int(rec['co_off']) + col * n)} + {i}))")
     if f & L.FLAG_INTERLEAVED:
-        return f"__ldcs(T.pos + {int(rec['p_off'])}LL + {i} * {int(rec['n_ret'])} + {col})"
-    return f"__ldcs(T.pos + {int(rec['p_off']) + col * n}LL + {i})"
+        return f"__ldcs(T.pos + {_off(int(rec['p_off']))} + (u64){i} * {int(rec['n_ret'])}u + {col}u)"
+    return f"__ldcs(T.pos + {_off(int(rec['p_off']) + col * n)} + {i})"
 
 
 def _out_pos(rec, r: int, i: str = "i") -> str | None:
@@ -123,10 +132,10 @@ def _out_pos(rec, r: int, i: str = "i") -> str | None:
     f = int(rec["flags"])
     if f & L.FLAG_OPOS16:
         nch = (n + 31) // 32
-        return (f"[&]() {{ const u16 o_ = __ldcs(T.ooff + {int(rec['oo_off']) + r * n}LL + {i}); "
-                f"return o_ == 0xFFFF ? NONE : __ldg(T.obase + {int(rec['ob_off']) + r * nch}LL + ({i} >> 5)) + o_; }}()")
+        return (f"[&]() {{ const u16 o_ = __ldcs(T.ooff + {_off(int(rec['oo_off']) + r * n)} + {i}); "
+                f"return o_ == 0xFFFF ? NONE : __ldg(T.obase + {_off(int(rec['ob_off']) + r * nch)} + ({i} >> 5)) + o_; }}()")
     if f & L.FLAG_OPOS32:
-        return f"__ldcs(T.opos32 + {int(rec['oo_off']) + r * n}LL + {i})"
+        return f"__ldcs(T.opos32 + {_off(int(rec['oo_off']) + r * n)} + {i})"
     return None
 
 
@@ -161,7 +170,7 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
     for s_ in range(S):
         c = int(cols[s_])
         if c < 0:
-            addr = f"idx0{sfx} + (u32)({int(dels[s_])}LL)"
+            addr = f"idx0{sfx} + {int(dels[s_]) % 2**32}u"
         elif c == 0:
             addr = f"idx0{sfx}"
         else:
@@ -169,15 +178,15 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
         loads.append(f"const double s{s_}{sfx} = {G(f'__ldg({X(addr)})', '0.0')};")
         reg[s_] = f"s{s_}{sfx}"
     for k in range(K):
-        e = (f"{int(rec['c_off'])}LL + {i} * {K} + {k}" if flags & L.FLAG_INTERLEAVED
-             else f"{int(rec['c_off']) + k * n}LL + {i}")
+        e = (f"{_off(int(rec['c_off']))} + (u64){i} * {K}u + {k}u" if flags & L.FLAG_INTERLEAVED
+             else f"{_off(int(rec['c_off']) + k * n)} + {i}")
         loads.append(f"const double k{k}{sfx} = {G(f'__ldcs(T.con + {e})', '0.0')};")
         reg[S + k] = f"k{k}{sfx}"
     if window:  # window positions (FLAG_WPOS16) load with the operands, not after the compute
         oo_off = int(rec["oo_off"])
         for r in range(int(rec["n_roots"])):
             loads.append(f"const u16 wp{r}{sfx} = "
-                         f"{G(f'__ldcs(T.ooff + {oo_off + r * n}LL + {i})', '(u16)0xFFFF')};")
+                         f"{G(f'__ldcs(T.ooff + {_off(oo_off + r * n)} + {i})', '(u16)0xFFFF')};")
     stream = bool(flags & L.FLAG_STREAM)
     opos = lambda r: _out_pos(rec, r, i)  # noqa: E731
     for j, t in enumerate(tape.tolist()):
@@ -186,7 +195,7 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
         B = ("-" if nb else "") + reg.get(b, "0.0")
         C = reg.get(c, "0.0")
         if op == L.T_ST and window:  # CSR-window member: FLAG_WPOS16 position in the block's window
-            comp.append(f"if (wp{aux}{sfx} != 0xFFFF) buf[wp{aux}{sfx}] = {reg[a]};")
+            comp.append(f"if (wp{aux}{sfx} != 0xFFFF) bw[wp{aux}{sfx}] = {reg[a]};")
             continue
         if op == L.T_ST and stage is not None:
             comp.append(f"if (ok{sfx}) stage_[({stage}) * {L.stage_stride(int(rec['n_roots']))} + {aux}] = {reg[a]};")
@@ -195,9 +204,9 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
             r = aux
             v = reg[a]
             if flags & L.FLAG_IMAJOR:  # CSR layout (lower._RelaidPlan): instance-major results
-                x_addr = X(f"{int(rec['dest_base']) + r}LL + {i} * {int(rec['n_roots'])}LL")
+                x_addr = X(f"{int(rec['dest_base']) + r}u + {i} * {int(rec['n_roots'])}u")
             else:
-                x_addr = X(f"{int(rec['dest_base']) + r * n}LL + {i}")
+                x_addr = X(f"{int(rec['dest_base']) + r * n}u + {i}")
             store = f"st_stream({x_addr}, {v});" if stream else f"*({x_addr}) = {v};"
             comp.append(f"if (ok{sfx}{' && !csr' if stream else ''}) {store}")
             if _out_pos(rec, r) is not None:
@@ -256,10 +265,10 @@ def group_vec_body(dp, gi, tape, imms, vec: int, base: str, stride: int, batched
     n = int(dp.groups[gi]["n"])
     lines, comps = [], []
     for v in range(vec):
-        lines.append(f"const i64 iv{v} = {base} + {v * stride}LL;")
+        lines.append(f"const u32 iv{v} = {base} + {v * stride}u;")
         extra = f" && ({limit.format(v=v * stride)})" if limit else ""
-        lines.append(f"const bool ok_{v} = iv{v} < {n}LL{extra};")
-        lines.append(f"const i64 ic{v} = ok_{v} ? iv{v} : {n - 1}LL;")
+        lines.append(f"const bool ok_{v} = iv{v} < {n}u{extra};")
+        lines.append(f"const u32 ic{v} = ok_{v} ? iv{v} : {n - 1}u;")
         ld, cp = group_parts(dp, gi, tape, imms, iv=f"ic{v}", sfx=f"_{v}", batched=batched, window=window,
                              stage=f"threadIdx.x + {v * stride}" if stage else None)
         lines += ld
@@ -280,10 +289,10 @@ def _stage_out(rec, vec: int) -> list[str]:
     rp = L.stage_stride(R)
     st = "__stcs(x + base_ + k_, v_)" if rec["flags"] & L.FLAG_STREAM else "x[base_ + k_] = v_"
     return ["__syncthreads();",
-            f"{{ const i64 cnt_ = min((i64){JIT_BLOCK * vec}, {n}LL - (i64)tl.y) * {R};",
-            f"  const i64 base_ = {int(rec['dest_base'])}LL + (i64)tl.y * {R}LL;",
-            f"  for (i64 k_ = threadIdx.x; k_ < cnt_; k_ += {JIT_BLOCK}) {{",
-            f"    const i64 q_ = k_ / {R}; const double v_ = stage_[q_ * {rp} + (k_ - q_ * {R})]; {st}; }} }}",
+            f"{{ const u32 cnt_ = min({JIT_BLOCK * vec}u, {n}u - (u32)tl.y) * {R}u;",
+            f"  const u32 base_ = {int(rec['dest_base'])}u + (u32)tl.y * {R}u;",
+            f"  for (u32 k_ = threadIdx.x; k_ < cnt_; k_ += {JIT_BLOCK}u) {{",
+            f"    const u32 q_ = k_ / {R}u; const double v_ = stage_[q_ * {rp}u + (k_ - q_ * {R}u)]; {st}; }} }}",
             "__syncthreads();"]
 
 
@@ -309,7 +318,7 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
                     "    i64 ld_out, int csr) {",
                     "  for (i64 t = blockIdx.x; t < n_tiles; t += gridDim.x) {",
                     "    const int2 tl = tiles[t];",
-                    "    const i64 i = (i64)tl.y + (threadIdx.x >> 5);",
+                    "    const u32 i = (u32)tl.y + (threadIdx.x >> 5);",
                     f"    for (i64 b = threadIdx.x & 31; b < batch; b += {32 * bvec}) {{",
                     "    switch (tl.x) {"]
         else:
@@ -319,7 +328,7 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
                     "  extern __shared__ double stage_[];",
                     "  for (i64 t = blockIdx.x; t < n_tiles; t += gridDim.x) {",
                     "    const int2 tl = tiles[t];",
-                    "    const i64 i = (i64)tl.y + threadIdx.x;",
+                    "    const u32 i = (u32)tl.y + threadIdx.x;",
                     "    {",
                     "    switch (tl.x) {"]
         out += head
@@ -330,7 +339,7 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
             staged = not batched and bool(rec["flags"] & L.FLAG_IMAJOR)
             out.append(f"    case {gi}: {{")
             if not staged:  # (a staged tile keeps every thread: the block synchronises)
-                out.append(f"      if (i >= {int(rec['n'])}LL) break;")
+                out.append(f"      if (i >= {int(rec['n'])}u) break;")
             if rec["flags"] & L.FLAG_CSR_ONLY:
                 out.append("      if (!csr) break;")
             body = (group_batch_body(dp, gi, tapes[gi], imms[gi], bvec) if batched else
@@ -425,7 +434,7 @@ def compile_cubin(src: str, name: str = "sgb_tape.cu") -> bytes:
 
 
 WINDOW_LOADS = 24  # loads in flight per thread across the members of one chunk of a window kernel
-COPY_UNROLL = 8  # copied outputs per thread in flight
+COPY_UNROLL = 6  # copied outputs per thread in flight
 WINDOW_MIN_BLOCKS = 3  # resident windows per SM the window kernel's register budget is sized for
 
 
@@ -464,17 +473,20 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
            "  const int tid = threadIdx.x;",
            "  for (i64 w = blockIdx.x; w < n_win; w += gridDim.x) {",
            f"    for (int j = tid; j < {J}; j += {B}) sp[j] = __ldg(pieces + w * {J} + j);",
-           "    const i64 k0 = __ldg(win_k + w), len_ = __ldg(win_k + w + 1) - k0;",
+           "    const i64 k0 = __ldg(win_k + w);",
+           "    const u32 len_ = (u32)(__ldg(win_k + w + 1) - k0);",
            "    const i64 c0_ = __ldg(copy_off + w), c1_ = __ldg(copy_off + w + 1);",
+           "    // window position p at bw[p]: out + k0 - head_ is 16-byte aligned, so is buf",
+           "    const u32 head_ = (u32)((reinterpret_cast<u64>(out + k0) >> 3) & 1ull);",
+           "    double *bw = buf + head_;",
            "    __syncthreads();",
-           f"    for (i64 c = c0_ + tid; c < c1_; c += {B * COPY_UNROLL}) {{",
-           f"      double cv_[{COPY_UNROLL}]; u16 cp_[{COPY_UNROLL}];",
-           "#pragma unroll",
-           f"      for (int q = 0; q < {COPY_UNROLL}; ++q) if (c + q * {B} < c1_) {{",
-           f"        cp_[q] = __ldcs(copy_pos + c + q * {B}); cv_[q] = __ldg(x + __ldcs(copy_src + c + q * {B})); }}",
-           "#pragma unroll",
-           f"      for (int q = 0; q < {COPY_UNROLL}; ++q) if (c + q * {B} < c1_) buf[cp_[q]] = cv_[q];",
-           "    }"]
+           f"    for (i64 c = c0_ + tid; c < c1_; c += {B * COPY_UNROLL}) {{"]
+    for q in range(COPY_UNROLL):  # named registers (no local arrays): every copy's loads in flight
+        out.append(f"      const bool cq{q} = c + {q * B} < c1_;")
+        out.append(f"      const u16 cp{q} = cq{q} ? __ldcs(copy_pos + c + {q * B}) : (u16)0;")
+        out.append(f"      const double cv{q} = cq{q} ? __ldg(x + __ldcs(copy_src + c + {q * B})) : 0.0;")
+    out += [f"      if (cq{q}) bw[cp{q}] = cv{q};" for q in range(COPY_UNROLL)]
+    out += ["    }"]
     for chunk in chunks:
         cmax = "0"
         for gi in chunk:
@@ -484,7 +496,7 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
         for gi in chunk:
             j = gi - g0
             out.append(f"      const bool ok_{j} = c0 + tid < sp[{j}].y;")
-            out.append(f"      const i64 i_{j} = ok_{j} ? (i64)sp[{j}].x + c0 + tid : 0;")
+            out.append(f"      const u32 i_{j} = ok_{j} ? (u32)(sp[{j}].x + c0 + tid) : 0u;")
             ld, cp = group_parts(dp, gi, tapes[gi], imms[gi], iv=f"i_{j}", sfx=f"_{j}", window=True,
                                  guard=f"ok_{j}")
             loads += ld
@@ -492,16 +504,15 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
         out += ["      " + ln for ln in loads + comps]
         out.append("    }")
     out += ["    __syncthreads();",
-            "    {",
-            "      double *o_ = out + k0;",
-            "      const i64 head = (i64)((reinterpret_cast<unsigned long long>(o_) >> 3) & 1ull);",
-            "      if (tid == 0 && head && len_ > 0) __stcs(o_, buf[0]);",
-            "      const i64 np_ = (len_ - head) >> 1;",
-            f"      for (i64 q = tid; q < np_; q += {B}) {{",
-            "        double2 v_; v_.x = buf[head + 2 * q]; v_.y = buf[head + 2 * q + 1];",
-            "        __stcs(reinterpret_cast<double2 *>(o_ + head) + q, v_);",
+            "    {  // 16-byte shared loads and streaming stores; the pair straddling k0 writes its second half",
+            "      const u32 tot_ = len_ + head_;",
+            "      double2 *o2 = reinterpret_cast<double2 *>(out + k0 - head_);",
+            "      const double2 *b2 = reinterpret_cast<const double2 *>(buf);",
+            f"      for (u32 q = tid; q < (tot_ >> 1); q += {B}) {{",
+            "        const double2 v_ = b2[q];",
+            "        if (q == 0 && head_) __stcs(out + k0, v_.y); else __stcs(o2 + q, v_);",
             "      }",
-            "      if (tid == 0 && len_ > head && ((len_ - head) & 1)) __stcs(o_ + len_ - 1, buf[len_ - 1]);",
+            "      if (tid == 0 && (tot_ & 1u)) __stcs(out + k0 + len_ - 1, buf[tot_ - 1]);",
             "    }",
             "    __syncthreads();",
             "  }",

@@ -341,6 +341,18 @@ def compile_tape(kp):
         rr, rn = operand(right)
         emit(T_SUB if sub else T_ADD, dst, lr, rr, nega=ln, negb=rn)
 
+    # every root is stored right after it is computed (not at the end), so a multi-root template
+    # (C3's 78-root element Hessian) does not keep all of its roots live until the last one
+    root_idx: dict[int, list[int]] = {}
+    for r_idx, root in enumerate(roots):
+        root_idx.setdefault(root, []).append(r_idx)
+    stored: set = set()
+
+    def store_roots(ref):
+        for r_idx in root_idx.get(ref, ()):
+            emit(T_ST, 0, reg[ref], aux=r_idx)
+        stored.add(ref)
+
     for ref in live:
         op = int(ops[ref])
         a = args[ref]
@@ -360,6 +372,8 @@ def compile_tape(kp):
             d = ra.get()
             emit(T_IMM, d, aux=imm_of[bits])
             reg[ref] = d
+            if ref in root_set:
+                store_roots(ref)
             continue
         d = ra.get()
         if op == OpKind.ADD:
@@ -399,7 +413,9 @@ def compile_tape(kp):
         else:
             raise ValueError(f"{kp.name}: unknown op {op}")
         reg[ref] = d
-        # recycle temporaries after their last use (slot registers stay pinned)
+        if ref in root_set:
+            store_roots(ref)
+        # recycle temporaries after their last use (slot registers stay pinned; roots are stored)
         dead = set()
         stack = list(a)
         while stack:
@@ -409,14 +425,15 @@ def compile_tape(kp):
                 continue
             dead.add(ch)
         for ch in dead:
-            if last_use.get(ch) is not None and last_use[ch] <= order[ref] and ch not in root_set \
+            if last_use.get(ch) is not None and last_use[ch] <= order[ref] and (ch not in root_set or ch in stored) \
                     and ch in reg and reg[ch] >= S + K and int(ops[ch]) != OpKind.VAR and reg[ch] != d:
                 ra.put(reg[ch])
                 reg[ch] = -1 - reg[ch]  # mark released (never released twice)
         if ra.top > REG_MAX:
             raise ValueError(f"{kp.name}: template needs more than {REG_MAX} scratch registers")
-    for r_idx, root in enumerate(roots):
-        emit(T_ST, 0, reg[root] if reg[root] >= 0 else -1 - reg[root], aux=r_idx)
+    for r_idx, root in enumerate(roots):  # roots that are slots (never computed)
+        if root not in stored:
+            emit(T_ST, 0, reg[root] if reg[root] >= 0 else -1 - reg[root], aux=r_idx)
     tape = np.array(recs, dtype=TAPE_DTYPE) if recs else np.zeros(0, TAPE_DTYPE)
     return tape, imms, max(ra.top, 1), fops
 
@@ -1317,8 +1334,8 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                     raise AssertionError("one CSR-window unit holding every member")
                 n_win = windows.k.size - 1
                 window_units.append((len(units), 0, n_win))
-                units.append((w, kind, variant, g_begin, len(order_groups), 0, n_win, bs,
-                              8 * int(np.diff(windows.k).max(initial=0)), UNIT_CSR_ONLY | UNIT_JIT | UNIT_WINDOW))
+                units.append((w, kind, variant, g_begin, len(order_groups), 0, n_win, bs,  # + 1: alignment slot
+                              8 * (int(np.diff(windows.k).max(initial=0)) + 1), UNIT_CSR_ONLY | UNIT_JIT | UNIT_WINDOW))
                 jit_units.append(len(units) - 1)
                 continue
             else:
