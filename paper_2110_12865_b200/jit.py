@@ -75,10 +75,13 @@ __device__ __noinline__ double powi(double x, int k) {  // == csrc powi
 __device__ __forceinline__ void st_stream(double *a, double v) { __stcs(a, v); }
 """
 
+# glibc's log restated for the device (tools/gen_glibc_log.py): the reference's math.log, bit for bit
+_PREAMBLE += (Path(__file__).resolve().parent / "csrc" / "glibc_log.h").read_text()
+
 _BIN = {L.T_MUL: "__dmul_rn({a}, {b})", L.T_ADD: "__dadd_rn({a}, {b})", L.T_SUB: "__dsub_rn({a}, {b})",
         L.T_DIV: "__ddiv_rn({a}, {b})", L.T_MADD: "__dadd_rn(__dmul_rn({a}, {b}), {c})",
         L.T_MSUB: "__dsub_rn(__dmul_rn({a}, {b}), {c})", L.T_RMSUB: "__dsub_rn({c}, __dmul_rn({a}, {b}))"}
-_SLOW = {0: "sin({a})", 1: "cos({a})", 2: "exp({a})", 3: "log({a})"}
+_SLOW = {0: "sin({a})", 1: "cos({a})", 2: "exp({a})", 3: "sgb_log({a})"}
 
 
 def _imm(v: float) -> str:

@@ -36,6 +36,9 @@ import numpy as np
 
 from .plan import EXACT_OPS, OpKind, reachable, slot_addresses, unique_addresses
 
+# ops the device reproduces bit for bit: the reference's _EXACT_OPS (codegen.py:43-53), POW k=2 (x*x,
+# SURVEY F7) and LOG (glibc's log restated, csrc/glibc_log.h)
+DEVICE_EXACT_OPS = frozenset(EXACT_OPS) | {int(OpKind.LOG)}
 KIND_TAPE, KIND_SOP = 0, 1
 FLAG_SELFREF, FLAG_INTERLEAVED, FLAG_SERIAL, FLAG_EXACT, FLAG_STREAM, FLAG_W16 = 1, 2, 4, 8, 16, 32
 FLAG_AFFINE0 = 64  # index column 0 is a0_base + a0_stride * i: no table read
@@ -513,8 +516,8 @@ def recognise_sop(kp):
 def lower_kernel(plan, kp, index: int) -> KernelLowering:
     tmpl = kp.template_arena
     live = reachable(tmpl, kp.template_roots)
-    exact = all(int(tmpl.ops[i]) in EXACT_OPS or (int(tmpl.ops[i]) == OpKind.POW and tmpl.payload[tmpl.args[i][1]] == 2.0)
-                for i in live)
+    exact = all(int(tmpl.ops[i]) in DEVICE_EXACT_OPS
+                or (int(tmpl.ops[i]) == OpKind.POW and tmpl.payload[tmpl.args[i][1]] == 2.0) for i in live)
     flags = (FLAG_SELFREF if kp.self_referencing else 0) | \
             (FLAG_INTERLEAVED if kp.layout == "interleaved" else 0) | (FLAG_EXACT if exact else 0)
     ridx = {s: k for k, s in enumerate(kp.retained)}

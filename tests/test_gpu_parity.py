@@ -369,3 +369,43 @@ def test_output_shards_on_device(golden, world):
         got = dp.run_csr(dp.new_values(golden.inputs)).cpu().numpy()
         assert np.array_equal(bits(got), bits(full[lo:hi]))
         assert np.array_equal(bits(dp.run_outputs_host(golden.inputs)), bits(full[lo:hi]))
+
+
+def _log_plan(n):
+    """One group of n instances, template log(v0) over the inputs (the reference's LOG node)."""
+    from paper_2110_12865_b200.plan import OpKind, Template
+    from paper_2110_12865_b200.programs.planbuild import PlanBuilder
+
+    T = Template()
+    root = T.apply(OpKind.LOG, (T.var(0),))
+    B = PlanBuilder(n)
+    res = B.add_group("log", 0, T, [root], [np.arange(n, dtype=np.int64)])
+    return B.finish(res[0], {"program": "log probe"})
+
+
+@pytest.mark.parametrize("jit", [True, False])
+def test_device_log_matches_glibc_bitwise(jit):
+    """LOG on the device (csrc/glibc_log.h, glibc's algorithm restated) == the reference's math.log
+    (glibc), bit for bit, on 4M values: both of glibc's paths (|x-1| < 2^-4 and the table), the whole
+    exponent range, subnormals, +inf and NaN -- through the specialised and the interpreter kernels."""
+    import math
+
+    from paper_2110_12865_b200 import DevicePlan, lower_plan
+
+    rng = np.random.default_rng(11)
+    q = 1 << 19
+    xs = np.concatenate([
+        rng.uniform(0.5, 2.0, q), rng.uniform(1 - 2 ** -4, 1 + 0.0646, q), np.exp(rng.uniform(-700, 700, q)),
+        rng.uniform(1e-3, 1e3, q),
+        np.frombuffer(rng.integers(1, 0x000FFFFFFFFFFFFF, q, dtype=np.uint64).tobytes(), np.float64),
+        np.frombuffer(rng.integers(0x0010000000000000, 0x7FEFFFFFFFFFFFFF, 3 * q - 3, dtype=np.uint64).tobytes(),
+                      np.float64),
+        np.array([1.0, math.inf, math.nan])])
+    plan = _log_plan(xs.size)
+    dp = DevicePlan(plan, lowered=lower_plan(plan, jit=jit))
+    got = dp.run_outputs_host(xs)
+    want = np.array([math.log(v) for v in xs.tolist()])
+    nan = np.isnan(want)
+    assert np.array_equal(np.isnan(got), nan)
+    bad = np.flatnonzero(bits(got[~nan]) != bits(want[~nan]))
+    assert bad.size == 0, f"{bad.size} of {xs.size} differ, e.g. {xs[~nan][bad[:3]]}"

@@ -79,3 +79,24 @@ def test_numpy_interpreter_restatement_matches_reference(golden):
     x, skipped = interp_np.interpret(golden.plan, golden.inputs)
     assert skipped == 0
     assert np.array_equal(bits(x), bits(golden.values))
+
+
+def test_glibc_log_header_matches_this_libm():
+    """csrc/glibc_log.h holds this image's glibc __log_data, and the restatement it implements equals
+    math.log (the reference's LOG) bit for bit on a random sample (tools/gen_glibc_log.py)."""
+    import math
+    import re
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    sys.path.insert(0, str(root / "tools"))
+    import gen_glibc_log as g
+
+    A, B, T = g.read_log_data(g.libm_path())
+    text = (root / "paper_2110_12865_b200" / "csrc" / "glibc_log.h").read_text()
+    tab = [float.fromhex(v) for v in re.findall(r"(-?0x[0-9a-f.]+p[-+]\d+)", text.split("sgb_log_tab")[1])[: 2 * g.N_TAB]]
+    assert tab == list(T)
+    xs = g.samples(6000, seed=5)
+    for x in xs.tolist():
+        assert np.array(g.restated_log(x, A, B, T)).view(np.uint64) == np.array(math.log(x)).view(np.uint64)
