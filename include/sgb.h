@@ -125,6 +125,7 @@ typedef struct sgb_plan_desc {
   const uint32_t *copy_src;  /* [n_copy] value-array address of each copied output */
   const uint16_t *copy_pos;  /* [n_copy] its position in its window */
   int64_t n_copy;
+  int64_t win_stage;         /* doubles of staged operand streams in front of the window buffer */
 } sgb_plan_desc;
 
 /* Upload a device plan to `device`.  Replaces compile_plan (emit.py:198-245). */

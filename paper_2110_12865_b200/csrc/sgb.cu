@@ -1158,7 +1158,9 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       SGB_CUDA(cudaLibraryGetKernel(&kw, p->jit_lib, nw.c_str()));
       u.jit = (const void *)kw;
       if (u.regs > 48 * 1024) SGB_CUDA(cudaFuncSetAttribute(u.jit, cudaFuncAttributeMaxDynamicSharedMemorySize, u.regs));
-      const int64_t wmax = u.regs / 8 - 1;  // the window buffer (doubles), one alignment slot
+      if (d->win_stage < 0 || 8 * (d->win_stage + 2) > (int64_t)u.regs)
+        return fail(-1, "sgb_plan_create: CSR-window stage does not fit its shared memory");
+      const int64_t wmax = u.regs / 8 - 2 - d->win_stage;  // the window buffer (doubles) after the stage
       if (d->win_k[0] != 0 || d->win_k[n_win] != d->n_outputs || d->win_copy[0] != 0 || d->win_copy[n_win] != d->n_copy)
         return fail(-1, "sgb_plan_create: CSR windows do not cover the outputs / copies");
       for (int g = u.g0; g < u.g1; ++g)

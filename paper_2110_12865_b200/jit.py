@@ -73,6 +73,14 @@ __device__ __noinline__ double powi(double x, int k) {  // == csrc powi
   return isfinite(r) ? r : rh;
 }
 __device__ __forceinline__ void st_stream(double *a, double v) { __stcs(a, v); }
+// asynchronous global -> shared copies (LDGSTS): a staged window's operand streams, no registers held
+__device__ __forceinline__ void cp_async8(double *smem, const double *gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
+               "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
 """
 
 # glibc's log restated for the device (tools/gen_glibc_log.py): the reference's math.log, bit for bit
@@ -144,7 +152,8 @@ def _out_pos(rec, r: int, i: str = "i") -> str | None:
 
 def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: str = "",
                 batched: bool = False, window: bool = False, bv: str = "b",
-                stage: str | None = None, guard: str | None = None) -> tuple[list[str], list[str]]:
+                stage: str | None = None, guard: str | None = None,
+                slot_src: list | None = None) -> tuple[list[str], list[str]]:
     """Straight-line CUDA for instance ``iv`` of packed group ``gi`` (register tape -> SSA).
 
     Returns (load lines, compute + store lines) so several instances' loads can be
@@ -155,7 +164,9 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
     results go to the block's staging buffer at ``stage_[(stage) * RP + r]``
     (``stage`` = the instance's offset in the tile, RP = lower.stage_stride); the
     unit writes the tile out coalesced.  ``guard``: every load is predicated on it
-    (lanes without an instance issue no memory traffic).
+    (lanes without an instance issue no memory traffic).  ``slot_src``: the slots' values
+    are these expressions (a staged window's shared-memory operand streams) and the
+    window positions ``wp<r><sfx>`` are loaded by the caller.
     """
     X = (lambda a: f"x + (u64)({a}) * ld + {bv}") if batched else (lambda a: f"x + ({a})")
     G = (lambda e, z: f"({guard}) ? ({e}) : {z}") if guard else (lambda e, z: e)  # noqa: E731
@@ -168,9 +179,13 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
     reg: dict[int, str] = {}
     i = iv
     col = lambda c: _column(rec, c, i, dp)  # noqa: E731
-    if S:
+    if S and slot_src is None:
         loads.append(f"const u32 idx0{sfx} = {G(col(0), '0u')};")
     for s_ in range(S):
+        if slot_src is not None:
+            loads.append(f"const double s{s_}{sfx} = {slot_src[s_]};")
+            reg[s_] = f"s{s_}{sfx}"
+            continue
         c = int(cols[s_])
         if c < 0:
             addr = f"idx0{sfx} + {int(dels[s_]) % 2**32}u"
@@ -185,7 +200,7 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
              else f"{_off(int(rec['c_off']) + k * n)} + {i}")
         loads.append(f"const double k{k}{sfx} = {G(f'__ldcs(T.con + {e})', '0.0')};")
         reg[S + k] = f"k{k}{sfx}"
-    if window:  # window positions (FLAG_WPOS16) load with the operands, not after the compute
+    if window and slot_src is None:  # window positions (FLAG_WPOS16) load with the operands, not after the compute
         oo_off = int(rec["oo_off"])
         for r in range(int(rec["n_roots"])):
             loads.append(f"const u16 wp{r}{sfx} = "
@@ -455,10 +470,16 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
     unit = dp.unit(u)
     g0, g1 = unit["group_begin"], unit["group_end"]
     J = g1 - g0
+    wn = dp.windows
+    ROWS = int(wn.rows) if wn is not None else 0
+    staged = [g0 + j for j in range(J) if ROWS and wn.aligned[j]]
+    NS = len(wn.streams) if staged else 0
     chunks, cur, width = [], [], 0
     for gi in range(g0, g1):
         rec = dp.groups[gi]
         _check_stores(tapes[gi], int(rec["n_roots"]), gi)
+        if gi in staged:
+            continue
         wdt = max(1, int(rec["n_slots"]) + int(rec["n_const"]))
         if cur and width + wdt > WINDOW_LOADS:
             chunks.append(cur)
@@ -468,22 +489,58 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
     if cur:
         chunks.append(cur)
     B = JIT_BLOCK
-    out = [f'extern "C" __global__ void __launch_bounds__({B}, {WINDOW_MIN_BLOCKS}) sgb_window_u{u}(',
-           "    Tables T, const int2 *pieces, const i64 *win_k, const i64 *copy_off, const u32 *copy_src,",
-           "    const u16 *copy_pos, i64 n_win, const double *x, double *out) {",
-           "  extern __shared__ double buf[];",
-           f"  __shared__ int2 sp[{J}];",
-           "  const int tid = threadIdx.x;",
-           "  for (i64 w = blockIdx.x; w < n_win; w += gridDim.x) {",
-           f"    for (int j = tid; j < {J}; j += {B}) sp[j] = __ldg(pieces + w * {J} + j);",
+    out = []
+    if staged:  # operand streams of the staged members: (base, stride) per stream, u32 modular
+        out.append(f"__constant__ u32 sgb_wsb_u{u}[{NS}] = {{{', '.join(f'{b % 2**32}u' for b, _ in wn.streams)}}};")
+        out.append(f"__constant__ u32 sgb_wss_u{u}[{NS}] = {{{', '.join(f'{t % 2**32}u' for _, t in wn.streams)}}};")
+    out += [f'extern "C" __global__ void __launch_bounds__({B}, {WINDOW_MIN_BLOCKS}) sgb_window_u{u}(',
+            "    Tables T, const int2 *pieces, const i64 *win_k, const i64 *copy_off, const u32 *copy_src,",
+            "    const u16 *copy_pos, i64 n_win, const double *x, double *out) {",
+            "  extern __shared__ __align__(16) double smem_[];",
+            f"  double *const stage_ = smem_;  // [{NS}][{ROWS}] staged operand streams",
+            f"  double *const buf = smem_ + {NS * ROWS};  // the window",
+            f"  __shared__ int2 sp[{J}];",
+            "  const int tid = threadIdx.x;",
+            "  for (i64 w = blockIdx.x; w < n_win; w += gridDim.x) {",
+            f"    for (int j = tid; j < {J}; j += {B}) sp[j] = __ldg(pieces + w * {J} + j);",
            "    const i64 k0 = __ldg(win_k + w);",
            "    const u32 len_ = (u32)(__ldg(win_k + w + 1) - k0);",
            "    const i64 c0_ = __ldg(copy_off + w), c1_ = __ldg(copy_off + w + 1);",
            "    // window position p at bw[p]: out + k0 - head_ is 16-byte aligned, so is buf",
            "    const u32 head_ = (u32)((reinterpret_cast<u64>(out + k0) >> 3) & 1ull);",
            "    double *bw = buf + head_;",
-           "    __syncthreads();",
-           f"    for (i64 c = c0_ + tid; c < c1_; c += {B * COPY_UNROLL}) {{"]
+           "    __syncthreads();"]
+    if staged:
+        n_a = int(dp.groups[staged[0]]["n"])
+        H = B // ROWS  # thread groups of the staged compute: thread tid takes row tid % ROWS
+        out += [f"    const u32 R0 = (u32)w * {ROWS}u, nrow = min({ROWS}u, {n_a}u - R0);",
+                f"    for (u32 e = tid; e < {NS * ROWS}u; e += {B}u) {{  // stage[s][r] = x[base_s + stride_s * (R0 + r)]",
+                f"      const u32 s_ = e / {ROWS}u, r_ = e % {ROWS}u;",
+                f"      if (r_ < nrow) cp_async8(stage_ + e, x + (sgb_wsb_u{u}[s_] + sgb_wss_u{u}[s_] * (R0 + r_)));",
+                "    }",
+                f"    const u32 rr_ = tid % {ROWS}u, hh_ = tid / {ROWS}u;",
+                "    const bool okr_ = rr_ < nrow;",
+                "    const u32 ir_ = R0 + rr_;"]
+        # members of the staged compute, balanced over the H thread groups by tape length
+        load = [0] * H
+        part = [[] for _ in range(H)]
+        for gi in sorted(staged, key=lambda g: -len(tapes[g])):
+            h = load.index(min(load))
+            part[h].append(gi)
+            load[h] += len(tapes[gi]) + 2
+        nwp = max(sum(int(dp.groups[gi]["n_roots"]) for gi in ms) for ms in part)
+        out.append(f"    u16 {', '.join(f'wq{q} = 0xFFFF' for q in range(nwp))};  // window positions of the row")
+        for h, ms in enumerate(part):  # issued now: they arrive while the stage fills
+            q = 0
+            out.append(f"    {'if' if h == 0 else 'else if'} (hh_ == {h}u && okr_) {{")
+            for gi in ms:
+                rec = dp.groups[gi]
+                for r in range(int(rec["n_roots"])):
+                    off = int(rec["oo_off"]) + r * int(rec["n"])
+                    out.append(f"      wq{q} = __ldcs(T.ooff + {_off(off)} + ir_);")
+                    q += 1
+            out.append("    }")
+    out += [f"    for (i64 c = c0_ + tid; c < c1_; c += {B * COPY_UNROLL}) {{"]
     for q in range(COPY_UNROLL):  # named registers (no local arrays): every copy's loads in flight
         out.append(f"      const bool cq{q} = c + {q * B} < c1_;")
         out.append(f"      const u16 cp{q} = cq{q} ? __ldcs(copy_pos + c + {q * B}) : (u16)0;")
@@ -506,6 +563,23 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
             comps += cp
         out += ["      " + ln for ln in loads + comps]
         out.append("    }")
+    if staged:  # the staged members: operands from shared memory, one row per thread
+        out.append("    cp_async_wait_all();")
+        out.append("    __syncthreads();")
+        for h, ms in enumerate(part):
+            out.append(f"    {'if' if h == 0 else 'else if'} (hh_ == {h}u && okr_) {{")
+            q = 0
+            for gi in ms:
+                rec = dp.groups[gi]
+                j = gi - g0
+                src = [f"stage_[{wn.slot_stream[j][s_] * ROWS}u + rr_]" for s_ in range(int(rec["n_slots"]))]
+                sfx = f"_{j}"
+                for r in range(int(rec["n_roots"])):
+                    out.append(f"      const u16 wp{r}{sfx} = wq{q};")
+                    q += 1
+                ld, cp = group_parts(dp, gi, tapes[gi], imms[gi], iv="ir_", sfx=sfx, window=True, slot_src=src)
+                out += ["      " + ln for ln in ld + cp]
+            out.append("    }")
     out += ["    __syncthreads();",
             "    {  // 16-byte shared loads and streaming stores; the pair straddling k0 writes its second half",
             "      const u32 tot_ = len_ + head_;",

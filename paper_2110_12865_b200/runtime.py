@@ -88,6 +88,7 @@ class _Desc(ctypes.Structure):
         ("copy_src", ctypes.c_void_p),
         ("copy_pos", ctypes.c_void_p),
         ("n_copy", ctypes.c_int64),
+        ("win_stage", ctypes.c_int64),
     ]
 
 
@@ -230,7 +231,7 @@ class DevicePlan:
             win_pieces=_ptr(keep["wpieces"]), n_win_pieces=keep["wpieces"].shape[0],
             win_k=_ptr(keep["wk"]), n_win_k=keep["wk"].size, win_copy=_ptr(keep["wcopy"]),
             n_win_copy=keep["wcopy"].size, copy_src=_ptr(keep["csrc"]), copy_pos=_ptr(keep["cpos"]),
-            n_copy=keep["csrc"].size,
+            n_copy=keep["csrc"].size, win_stage=wn.stage_doubles if wn is not None else 0,
         )
         torch.cuda.init()
         _check(self._lib.sgb_plan_create(ctypes.byref(d), self.device, ctypes.byref(self._handle)),
