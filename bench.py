@@ -716,6 +716,53 @@ def measure_batched(args, rank: int, world: int, barrier) -> dict:
     }
 
 
+def measure_emulated(args, rank: int, world: int, barrier) -> dict:
+    """``--emulate``: the N-rank orchestration of ``measure_eval`` on CPU -- gloo, the device-plan
+    emulator (tests/device_plan_emu.py) in place of the GPU -- so the multi-rank path (spawn, CSR
+    window-aligned output shards, max-over-ranks timing, the all-gather of the slices) is testable
+    without GPUs (tests/test_shard.py).  Test infrastructure: never a bench number."""
+    import torch
+    import torch.distributed as dist
+
+    sys.path.insert(0, str(ROOT / "tests"))
+    import device_plan_emu as emu
+
+    from paper_2110_12865_b200 import lower_plan
+    from paper_2110_12865_b200.shard import max_over_ranks, shard_bounds, shard_device_plan
+
+    cfg = args.config
+    key, plan = build_workload(cfg, args, rank, barrier)
+    n_total = len(plan.outputs)
+    lw = lower_plan(plan, jit_compile=False, csr_window=True)
+    lo, hi = shard_bounds(lw, n_total, world, rank)
+    _, slw = shard_device_plan(plan, lw, lo, hi)
+    inputs = workload_inputs(cfg, args, seed=0, plan=plan)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        mine = emu.run_csr(slw, inputs, by_tiles=True)
+    sec = max_over_ranks((time.perf_counter() - t0) / args.steps)
+    width = torch.tensor([hi - lo])
+    dist.all_reduce(width, op=dist.ReduceOp.MAX)
+    send = torch.zeros(int(width.item()), dtype=torch.float64)
+    send[: hi - lo] = torch.from_numpy(mine)
+    parts = [torch.empty_like(send) for _ in range(world)]
+    dist.all_gather(parts, send)
+    bounds = [shard_bounds(lw, n_total, world, r) for r in range(world)]
+    full = torch.cat([parts[r][: b - a] for r, (a, b) in enumerate(bounds)]).numpy()
+    if rank != 0:
+        return {}
+    from oracle import oracle
+
+    ok = bool(np.array_equal(full.view(np.uint64), oracle.run_outputs(plan, inputs).view(np.uint64)))
+    return {"metric": METRIC, "value": n_total / sec, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "emulated": True,
+            "config": dict(config_dict(cfg, args, plan), parity="bitwise" if ok else "MISMATCH",
+                           shards=[list(b) for b in bounds],
+                           parallelism=f"CPU emulation, gloo x{world}: one evaluation, CSR outputs split at window "
+                                       "boundaries, slices all-gathered and compared with the oracle")}
+
+
 def compact(line: dict) -> dict:
     """The other_configs entry of a config's full line."""
     roof = line.get("roofline", {})
@@ -800,6 +847,8 @@ def parse_args(argv=None):
     ap.add_argument("--split-world", type=int, default=0,
                     help="N=1: time one rank's share of an outputs split this many ways")
     ap.add_argument("--split-rank", type=int, default=0)
+    ap.add_argument("--emulate", action="store_true",
+                    help="test infrastructure: the multi-rank path on CPU (gloo + the device-plan emulator)")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
     return args
@@ -809,7 +858,7 @@ def main(argv=None) -> int:
     argv = sys.argv[1:] if argv is None else argv
     args = parse_args(argv)
     rank, world, local = dist_env()
-    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+    if (args.gpus > 1 or args.emulate) and "WORLD_SIZE" not in os.environ:
         return spawn(args, argv)
     if "WORLD_SIZE" in os.environ and world != args.gpus:
         log(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
@@ -819,6 +868,14 @@ def main(argv=None) -> int:
 
     import torch
     import torch.distributed as dist
+
+    if args.emulate:
+        dist.init_process_group("gloo")
+        line = measure_emulated(args, rank, world, dist.barrier)
+        if rank == 0:
+            print(json.dumps(line), flush=True)
+        dist.destroy_process_group()
+        return 0
 
     torch.cuda.set_device(local)
     barrier = None

@@ -28,7 +28,7 @@ def nvcc() -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
-    deps = [SRC, HDR, PKG / "csrc" / "glibc_log.h", Path(__file__)]
+    deps = [SRC, HDR, PKG / "csrc" / "glibc_math.h", Path(__file__)]
     if LIB.exists() and not force and LIB.stat().st_mtime >= max(d.stat().st_mtime for d in deps):
         return LIB
     tmp = LIB.with_name(f"libsgb.{os.getpid()}.so")

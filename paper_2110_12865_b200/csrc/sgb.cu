@@ -42,7 +42,7 @@
 #include <vector>
 
 #include "sgb.h"
-#include "glibc_log.h"  // sgb_log: glibc's log restated (tools/gen_glibc_log.py)
+#include "glibc_math.h"  // sgb_log / sgb_exp / sgb_pow: glibc restated (tools/gen_glibc_math.py)
 
 namespace {
 
@@ -170,35 +170,16 @@ __device__ __forceinline__ void store_root(const Tables &T, const sgb_group &G, 
   }
 }
 
-// ---- double-double integer power (POW k >= 3; k == 2 is an exact x*x) ----------
-__device__ __forceinline__ void dd_mul(double ah, double al, double bh, double bl, double &rh, double &rl) {
-  double p = __dmul_rn(ah, bh);
-  double e = __fma_rn(ah, bh, -p);
-  e = __dadd_rn(e, __dadd_rn(__dmul_rn(ah, bl), __dmul_rn(al, bh)));
-  rh = __dadd_rn(p, e);
-  rl = __dsub_rn(e, __dsub_rn(rh, p));
-}
-
-__device__ __noinline__ double powi(double x, int k) {
-  if (k == 2) return __dmul_rn(x, x);  // glibc pow(x, 2.0) == x*x
-  double rh = 1.0, rl = 0.0, bh = x, bl = 0.0;
-  while (k) {
-    if (k & 1) dd_mul(rh, rl, bh, bl, rh, rl);
-    k >>= 1;
-    if (k) dd_mul(bh, bl, bh, bl, bh, bl);
-  }
-  double r = __dadd_rn(rh, rl);
-  return isfinite(r) ? r : rh;
-}
-
-// Rare ops live out of line so the interpreter loop stays small.
+// Rare ops live out of line so the interpreter loop stays small.  LOG / EXP / POW are glibc's own
+// algorithms (glibc_math.h) -- the reference's math.log / math.exp / math.pow, bit for bit; POW k = 2
+// is x*x (glibc's pow(x, 2.0) == x*x); SIN / COS use CUDA's libm (<= 1e-12 relative).
 __device__ __noinline__ double slow_op(unsigned kind, double a, int k) {
   switch (kind) {
     case 0: return sin(a);
     case 1: return cos(a);
-    case 2: return exp(a);
-    case 3: return sgb_log(a);  // == glibc log == the reference's math.log, bit for bit
-    default: return powi(a, k);
+    case 2: return sgb_exp(a);
+    case 3: return sgb_log(a);
+    default: return k == 2 ? __dmul_rn(a, a) : sgb_pow(a, (double)k);
   }
 }
 

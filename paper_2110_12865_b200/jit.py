@@ -54,24 +54,6 @@ struct Tables {  // == csrc/sgb.cu Tables
 };
 #define NONE 0xFFFFFFFFu
 __device__ __forceinline__ double bits(u64 b) { return __longlong_as_double((long long)b); }
-__device__ __forceinline__ void dd_mul(double ah, double al, double bh, double bl, double &rh, double &rl) {
-  double p = __dmul_rn(ah, bh);
-  double e = __fma_rn(ah, bh, -p);
-  e = __dadd_rn(e, __dadd_rn(__dmul_rn(ah, bl), __dmul_rn(al, bh)));
-  rh = __dadd_rn(p, e);
-  rl = __dsub_rn(e, __dsub_rn(rh, p));
-}
-__device__ __noinline__ double powi(double x, int k) {  // == csrc powi
-  if (k == 2) return __dmul_rn(x, x);
-  double rh = 1.0, rl = 0.0, bh = x, bl = 0.0;
-  while (k) {
-    if (k & 1) dd_mul(rh, rl, bh, bl, rh, rl);
-    k >>= 1;
-    if (k) dd_mul(bh, bl, bh, bl, bh, bl);
-  }
-  double r = __dadd_rn(rh, rl);
-  return isfinite(r) ? r : rh;
-}
 __device__ __forceinline__ void st_stream(double *a, double v) { __stcs(a, v); }
 // asynchronous global -> shared copies (LDGSTS): a staged window's operand streams, no registers held
 __device__ __forceinline__ void cp_async8(double *smem, const double *gmem) {
@@ -83,13 +65,14 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 """
 
-# glibc's log restated for the device (tools/gen_glibc_log.py): the reference's math.log, bit for bit
-_PREAMBLE += (Path(__file__).resolve().parent / "csrc" / "glibc_log.h").read_text()
+# glibc's log / exp / pow restated for the device (tools/gen_glibc_math.py): the reference's math
+# module, bit for bit
+_PREAMBLE += (Path(__file__).resolve().parent / "csrc" / "glibc_math.h").read_text()
 
 _BIN = {L.T_MUL: "__dmul_rn({a}, {b})", L.T_ADD: "__dadd_rn({a}, {b})", L.T_SUB: "__dsub_rn({a}, {b})",
         L.T_DIV: "__ddiv_rn({a}, {b})", L.T_MADD: "__dadd_rn(__dmul_rn({a}, {b}), {c})",
         L.T_MSUB: "__dsub_rn(__dmul_rn({a}, {b}), {c})", L.T_RMSUB: "__dsub_rn({c}, __dmul_rn({a}, {b}))"}
-_SLOW = {0: "sin({a})", 1: "cos({a})", 2: "exp({a})", 3: "sgb_log({a})"}
+_SLOW = {0: "sin({a})", 1: "cos({a})", 2: "sgb_exp({a})", 3: "sgb_log({a})"}
 
 
 def _imm(v: float) -> str:
@@ -243,7 +226,8 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
             expr = f"({reg[a]} < 0.0 ? {reg[b]} : {C})"
         elif op == L.T_SLOW:
             kind, k = aux >> 16, aux & 0xFFFF
-            expr = f"powi({reg[a]}, {k})" if kind == 4 else _SLOW[kind].format(a=reg[a])
+            expr = (f"__dmul_rn({reg[a]}, {reg[a]})" if k == 2 else f"sgb_pow({reg[a]}, {float(k)!r})") \
+                if kind == 4 else _SLOW[kind].format(a=reg[a])
         else:
             raise ValueError(f"unknown tape op {op}")
         comp.append(f"const double t{j}{sfx} = {expr};")

@@ -36,9 +36,9 @@ import numpy as np
 
 from .plan import EXACT_OPS, OpKind, reachable, slot_addresses, unique_addresses
 
-# ops the device reproduces bit for bit: the reference's _EXACT_OPS (codegen.py:43-53), POW k=2 (x*x,
-# SURVEY F7) and LOG (glibc's log restated, csrc/glibc_log.h)
-DEVICE_EXACT_OPS = frozenset(EXACT_OPS) | {int(OpKind.LOG)}
+# ops the device reproduces bit for bit: the reference's _EXACT_OPS (codegen.py:43-53) and LOG / EXP /
+# POW (glibc's algorithms restated, csrc/glibc_math.h); SIN / COS stay on CUDA's libm (1e-12)
+DEVICE_EXACT_OPS = frozenset(EXACT_OPS) | {int(OpKind.LOG), int(OpKind.EXP), int(OpKind.POW)}
 KIND_TAPE, KIND_SOP = 0, 1
 FLAG_SELFREF, FLAG_INTERLEAVED, FLAG_SERIAL, FLAG_EXACT, FLAG_STREAM, FLAG_W16 = 1, 2, 4, 8, 16, 32
 FLAG_AFFINE0 = 64  # index column 0 is a0_base + a0_stride * i: no table read
@@ -516,8 +516,7 @@ def recognise_sop(kp):
 def lower_kernel(plan, kp, index: int) -> KernelLowering:
     tmpl = kp.template_arena
     live = reachable(tmpl, kp.template_roots)
-    exact = all(int(tmpl.ops[i]) in DEVICE_EXACT_OPS
-                or (int(tmpl.ops[i]) == OpKind.POW and tmpl.payload[tmpl.args[i][1]] == 2.0) for i in live)
+    exact = all(int(tmpl.ops[i]) in DEVICE_EXACT_OPS for i in live)
     flags = (FLAG_SELFREF if kp.self_referencing else 0) | \
             (FLAG_INTERLEAVED if kp.layout == "interleaved" else 0) | (FLAG_EXACT if exact else 0)
     ridx = {s: k for k, s in enumerate(kp.retained)}
@@ -805,7 +804,9 @@ class CsrWindows:
         return len(self.streams) * self.rows
 
 
-STAGE_ROWS = (128, 64, 32)  # row-window heights tried, largest first (one 256-thread block: 2 halves)
+# row-window heights tried, largest first (one 256-thread block: 2 halves); SGB_STAGE_ROWS=0 turns the
+# staged windows off (the profiling comparison in tools/gpu_r2d.sh)
+STAGE_ROWS = () if os.environ.get("SGB_STAGE_ROWS") == "0" else (128, 64, 32)
 STAGE_MAX_BYTES = 96 * 1024  # shared memory a staged window may use (operand streams + window buffer)
 
 

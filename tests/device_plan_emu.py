@@ -124,6 +124,16 @@ def _dd_powi(xs, k):
     return out
 
 
+def _glibc_pow(v, k):
+    """math.pow (glibc) with IEEE overflow instead of Python's OverflowError; k == 2 is v * v."""
+    if k == 2:
+        return v * v
+    try:
+        return math.pow(v, float(k))
+    except OverflowError:
+        return math.copysign(math.inf, v) if k % 2 else math.inf
+
+
 def _vec(fn, a):
     return np.array([fn(v) for v in a.tolist()], dtype=np.float64)
 
@@ -301,7 +311,7 @@ def _tape(dp, g, x, i, store):
                     v = np.where(R[a] < 0.0, R[b], R[c])
                 elif op == L.T_SLOW:
                     kind, k = ww >> 16, ww & 0xFFFF
-                    v = _dd_powi(R[a], k) if kind == 4 else _vec(slow[kind], R[a])
+                    v = _vec(lambda v: _glibc_pow(v, k), R[a]) if kind == 4 else _vec(slow[kind], R[a])
                 else:
                     raise ValueError(f"bad op {op}")
             R[d] = v
@@ -354,7 +364,7 @@ def _reg_tape(dp, gi, g, x, i, store):
                 v = np.where(R[a] < 0.0, R[b], R[c])
             elif op == L.T_SLOW:
                 kind, k = aux >> 16, aux & 0xFFFF
-                v = _dd_powi(R[a], k) if kind == 4 else _vec(slow[kind], R[a])
+                v = _vec(lambda v: _glibc_pow(v, k), R[a]) if kind == 4 else _vec(slow[kind], R[a])
             else:
                 v = _binop(op, A, B, R.get(c, z))
         R[dst] = v

@@ -265,6 +265,11 @@ def main(which=None):
             emit(f"product_n24_s{s}", sess, off, 7, {"source": "test_codegen.py:29-36"}, csr=out)
         job(f"product_n24_s{s}", _p)
 
+    def _p21():  # test_emit.py:81-91 (test_compiled_matches_interpreter_bitwise): inputs seed 21
+        sess, out = trace_product_program(24, 3)
+        emit("product_n24_s3_seed21", sess, off, 21, {"source": "test_emit.py:81-91"}, csr=out)
+    job("product_n24_s3_seed21", _p21)
+
     def _p0():
         sess, out = trace_product_program(24, 3)
         emit("product_n24_s3_tcompl0", sess, PlanConfig(simplify_enabled=False, t_compl=0), 9,

@@ -108,3 +108,17 @@ def test_arap_builder_matches_reference_trace(w):
     assert np.array_equal(bits(out), bits(g.oracle))
     x = emu.run_values(lower_plan(plan, jit=False), g.inputs)
     assert np.array_equal(bits(x[np.asarray(plan.outputs)]), bits(g.oracle))
+
+
+@pytest.mark.parametrize("w,m,w4", [(60, 6, 40), (33, 5, 21)])
+def test_builder_patterns_equal_scipy_boolean_products(w, m, w4):
+    """C2 / C3 / C4 CSR patterns from the builders == scipy boolean products of the mesh alone
+    (tools/check_patterns.py; the full BASELINE sizes are checked by `--full`, profiles/r2/patterns_full.json)."""
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tools"))
+    import check_patterns
+
+    res = check_patterns.check(w, m, w4)
+    assert all(r["match"] for r in res.values()), res

@@ -371,40 +371,69 @@ def test_output_shards_on_device(golden, world):
         assert np.array_equal(bits(dp.run_outputs_host(golden.inputs)), bits(full[lo:hi]))
 
 
-def _log_plan(n):
-    """One group of n instances, template log(v0) over the inputs (the reference's LOG node)."""
-    from paper_2110_12865_b200.plan import OpKind, Template
+def _unary_plan(n, op, k=None):
+    """One group of n instances, template op(v0) (POW: v0 ** k) over the inputs."""
+    from paper_2110_12865_b200.plan import Template
     from paper_2110_12865_b200.programs.planbuild import PlanBuilder
 
     T = Template()
-    root = T.apply(OpKind.LOG, (T.var(0),))
+    args = (T.var(0),) if k is None else (T.var(0), T.const(float(k)))
+    root = T.apply(op, args)
     B = PlanBuilder(n)
-    res = B.add_group("log", 0, T, [root], [np.arange(n, dtype=np.int64)])
-    return B.finish(res[0], {"program": "log probe"})
+    res = B.add_group("probe", 0, T, [root], [np.arange(n, dtype=np.int64)])
+    return B.finish(res[0], {"program": "transcendental probe"})
+
+
+def _ref_math(fn, *a):
+    import math
+
+    try:
+        return fn(*a)
+    except OverflowError:
+        return math.inf
+    except ValueError:
+        return math.nan
 
 
 @pytest.mark.parametrize("jit", [True, False])
-def test_device_log_matches_glibc_bitwise(jit):
-    """LOG on the device (csrc/glibc_log.h, glibc's algorithm restated) == the reference's math.log
-    (glibc), bit for bit, on 4M values: both of glibc's paths (|x-1| < 2^-4 and the table), the whole
-    exponent range, subnormals, +inf and NaN -- through the specialised and the interpreter kernels."""
+@pytest.mark.parametrize("op", ["log", "exp", "pow3", "pow4", "pow7"])
+def test_device_transcendentals_match_glibc_bitwise(op, jit):
+    """LOG / EXP / POW on the device (csrc/glibc_math.h, glibc's algorithms restated) == the
+    reference's math.log / math.exp / math.pow (glibc), bit for bit, on ~3M values covering every
+    branch (both log paths, the whole exponent range, subnormals, exp's under/overflow scaling,
+    negative bases of odd and even powers), through the specialised and the interpreter kernels."""
     import math
+    import sys
+    from pathlib import Path
 
     from paper_2110_12865_b200 import DevicePlan, lower_plan
+    from paper_2110_12865_b200.plan import OpKind
 
-    rng = np.random.default_rng(11)
-    q = 1 << 19
-    xs = np.concatenate([
-        rng.uniform(0.5, 2.0, q), rng.uniform(1 - 2 ** -4, 1 + 0.0646, q), np.exp(rng.uniform(-700, 700, q)),
-        rng.uniform(1e-3, 1e3, q),
-        np.frombuffer(rng.integers(1, 0x000FFFFFFFFFFFFF, q, dtype=np.uint64).tobytes(), np.float64),
-        np.frombuffer(rng.integers(0x0010000000000000, 0x7FEFFFFFFFFFFFFF, 3 * q - 3, dtype=np.uint64).tobytes(),
-                      np.float64),
-        np.array([1.0, math.inf, math.nan])])
-    plan = _log_plan(xs.size)
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tools"))
+    import gen_glibc_math as g
+
+    n = 3 << 20
+    if op == "log":
+        xs, kind, k, fn = np.concatenate([g.samples(n, seed=11), [1.0, math.inf, math.nan]]), OpKind.LOG, None, math.log
+    elif op == "exp":
+        xs, kind, k, fn = np.concatenate([g.exp_samples(n, seed=12), [0.0, -math.inf, math.inf, 709.8, -746.0]]), \
+            OpKind.EXP, None, math.exp
+    else:
+        k = int(op[3:])
+        rng = np.random.default_rng(k)
+        xs = np.concatenate([rng.uniform(-3.0, 3.0, n // 2), np.exp(rng.uniform(-200, 200, n // 2)) *
+                             rng.choice([-1.0, 1.0], n // 2), [0.0, -0.0, 1e300, -1e300, 5e-324]])
+        kind = OpKind.POW
+
+        def fn(v, k=k):  # math.pow raises on overflow; glibc returns the signed infinity
+            try:
+                return math.pow(v, float(k))
+            except OverflowError:
+                return -math.inf if v < 0 and k % 2 else math.inf
+    plan = _unary_plan(xs.size, kind, k)
     dp = DevicePlan(plan, lowered=lower_plan(plan, jit=jit))
     got = dp.run_outputs_host(xs)
-    want = np.array([math.log(v) for v in xs.tolist()])
+    want = np.array([_ref_math(fn, v) for v in xs.tolist()])
     nan = np.isnan(want)
     assert np.array_equal(np.isnan(got), nan)
     bad = np.flatnonzero(bits(got[~nan]) != bits(want[~nan]))

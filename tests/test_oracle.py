@@ -81,22 +81,25 @@ def test_numpy_interpreter_restatement_matches_reference(golden):
     assert np.array_equal(bits(x), bits(golden.values))
 
 
-def test_glibc_log_header_matches_this_libm():
-    """csrc/glibc_log.h holds this image's glibc __log_data, and the restatement it implements equals
-    math.log (the reference's LOG) bit for bit on a random sample (tools/gen_glibc_log.py)."""
-    import math
+def test_glibc_math_header_matches_this_libm():
+    """csrc/glibc_math.h holds this image's glibc tables (__log_data, __exp_data, __pow_log_data), and
+    the restatements it implements equal math.log / math.exp / math.pow -- the reference's LOG / EXP /
+    POW -- bit for bit on a random sample (tools/gen_glibc_math.py)."""
     import re
     import sys
     from pathlib import Path
 
     root = Path(__file__).resolve().parent.parent
     sys.path.insert(0, str(root / "tools"))
-    import gen_glibc_log as g
+    import gen_glibc_math as g
 
-    A, B, T = g.read_log_data(g.libm_path())
-    text = (root / "paper_2110_12865_b200" / "csrc" / "glibc_log.h").read_text()
-    tab = [float.fromhex(v) for v in re.findall(r"(-?0x[0-9a-f.]+p[-+]\d+)", text.split("sgb_log_tab")[1])[: 2 * g.N_TAB]]
-    assert tab == list(T)
-    xs = g.samples(6000, seed=5)
-    for x in xs.tolist():
-        assert np.array(g.restated_log(x, A, B, T)).view(np.uint64) == np.array(math.log(x)).view(np.uint64)
+    t = g.read_tables(g.libm_path())
+    text = (root / "paper_2110_12865_b200" / "csrc" / "glibc_math.h").read_text()
+    hexf = r"(-?0x[0-9a-f.]+p[-+]\d+)"
+    tab = [float.fromhex(v) for v in re.findall(hexf, text.split("sgb_log_tab")[1])[: 2 * g.N_TAB]]
+    assert tab == list(t["log_tab"])
+    ptab = [float.fromhex(v) for v in re.findall(hexf, text.split("sgb_pow_tab")[1])[: 3 * g.N_TAB]]
+    assert ptab == [t["pow_tab"][4 * j + q] for j in range(g.N_TAB) for q in (0, 2, 3)]
+    etab = [int(v, 16) for v in re.findall(r"0x([0-9a-f]{16})ull", text.split("sgb_exp_tab")[1])[: 2 * g.N_TAB]]
+    assert etab == list(t["exp_tab"])
+    assert g.verify(t, 3000) == []

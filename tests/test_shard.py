@@ -200,3 +200,23 @@ def test_gloo_world2_output_split_equals_oracle(tmp_path):
 
     g = Golden("lmlt_w7")
     assert np.array_equal(bits(np.load(path)), bits(oracle.run_outputs(g.plan, g.inputs)))
+
+
+def test_bench_emulated_eight_ranks_via_the_bench_entry_point():
+    """`python bench.py --gpus 8 --emulate`: the bench's own spawn (torchrun, 8 ranks, gloo), CSR-window
+    aligned output shards, max-over-ranks timing and the all-gather of the slices; the gathered
+    evaluation equals the oracle bit for bit and the line reports n_gpus = 8."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, SGB_PLAN_CACHE=str(Path(os.environ.get("TMPDIR", "/tmp")) / "sgb_plan_cache_emu"))
+    env.pop("WORLD_SIZE", None)
+    proc = subprocess.run([sys.executable, str(root / "bench.py"), "--gpus", "8", "--emulate", "--w", "14",
+                           "--steps", "1"], capture_output=True, text=True, timeout=600, env=env)
+    assert proc.returncode == 0, proc.stderr[-3000:]
+    line = json.loads([ln for ln in proc.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 8 and line["config"]["parity"] == "bitwise"
+    assert len(line["config"]["shards"]) == 8

@@ -1,0 +1,610 @@
+"""Generate paper_2110_12865_b200/csrc/glibc_math.h: glibc's log, exp and pow restated for the device.
+
+The reference evaluates LOG / EXP / POW nodes with Python's ``math`` module (codegen.py:545-557,
+expr.py:423-484) -- the C library of this image, glibc 2.39.  Its log, exp and pow are the ARM
+optimized-routines algorithms (sysdeps/ieee754/dbl-64/e_log.c, e_exp.c, e_pow.c):
+
+* log: |x - 1| < 2^-4 -> a degree-11 polynomial in r = x - 1 with an exact split of r^2/2;
+  otherwise x = 2^k z, a 128-entry table (1/c, log c), r = fma(z, 1/c, -1), a degree-5 polynomial;
+* exp: x = k ln2/128 + r, 2^(k/128) from a 128-entry table (tail, bits), a degree-4 polynomial,
+  special scaling near overflow / underflow;
+* pow: log(x) to ~2^-68 relative (hi + lo) with its own 128-entry table, y*log(x) split with an
+  fma, then exp of the pair; sign of negative x with integer y, zero / inf / nan / subnormal
+  special cases.
+
+On x86-64 with FMA glibc runs its FMA builds (ifunc), compiled with GCC's default floating-point
+contraction: a product whose value has a single use in an addition is fused -- the Python
+restatements below and the device code mirror exactly where.  The numeric tables (__log_data,
+__exp_data, __pow_log_data) are read out of the installed libm.so.6; every restatement is checked
+against ``math`` bit for bit on a large random sample before the header is written.
+
+    python tools/gen_glibc_math.py [--samples 300000]
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes.util
+import math
+import struct
+import sys
+from fractions import Fraction
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+OUT = ROOT / "paper_2110_12865_b200" / "csrc" / "glibc_math.h"
+N_TAB = 128
+LN2HI = float.fromhex("0x1.62e42fefa3800p-1")
+LN2LO = float.fromhex("0x1.ef35793c76730p-45")
+EXP_INVLN2N = float.fromhex("0x1.71547652b82fep7")
+POW_OFF = 0x3FE6955500000000
+LOG_OFF = 0x3FE6000000000000
+
+
+def libm_path() -> Path:
+    for cand in ("/lib/x86_64-linux-gnu/libm.so.6", "/usr/lib/x86_64-linux-gnu/libm.so.6", ctypes.util.find_library("m")):
+        if cand and Path(cand).exists():
+            return Path(cand)
+    raise SystemExit("libm.so.6 not found")
+
+
+def _find(data: bytes, head: bytes, ok) -> int:
+    start = 0
+    while True:
+        off = data.find(head, start)
+        if off < 0:
+            raise SystemExit("glibc math table not found in libm")
+        if ok(off):
+            return off
+        start = off + 1
+
+
+def read_tables(path: Path) -> dict:
+    """__log_data, __pow_log_data (both start ln2hi, ln2lo) and __exp_data (starts invln2N, shift)."""
+    data = path.read_bytes()
+    d = lambda off, n: struct.unpack_from(f"<{n}d", data, off)  # noqa: E731
+    head = struct.pack("<dd", LN2HI, LN2LO)
+    # __log_data: poly[5] (poly[0] ~ -0.5), poly1[11] (poly1[0] == -0.5), tab[128] (invc, logc)
+    lo = _find(data, head, lambda o: d(o, 18)[7] == -0.5 and abs(d(o, 18)[2] + 0.5) < 1e-15)
+    v = d(lo, 2 + 5 + 11 + 2 * N_TAB)
+    # __pow_log_data: poly[7] (poly[0] == -0.5), tab[128] (invc, pad, logc, logctail)
+    po = _find(data, head, lambda o: d(o, 9)[2] == -0.5 and d(o, 10)[9] > 1.0)
+    pv = d(po, 2 + 7 + 4 * N_TAB)
+    # __exp_data: invln2N, shift, negln2hiN, negln2loN, poly[4], ..., tab[256] u64 at (0, 2^0 bits)
+    eo = _find(data, struct.pack("<dd", EXP_INVLN2N, float.fromhex("0x1.8p52")), lambda o: True)
+    k = next(k for k in range(8, 64) if struct.unpack_from("<QQ", data, eo + 8 * k) == (0, 0x3FF0000000000000))
+    ev = d(eo, 8)
+    etab = struct.unpack_from(f"<{2 * N_TAB}Q", data, eo + 8 * k)
+    return {"log_poly": v[2:7], "log_poly1": v[7:18], "log_tab": v[18:18 + 2 * N_TAB],
+            "pow_poly": pv[2:9], "pow_tab": pv[9:9 + 4 * N_TAB],
+            "exp_shift": ev[1], "exp_negln2hiN": ev[2], "exp_negln2loN": ev[3], "exp_poly": ev[4:8],
+            "exp_tab": etab}
+
+
+# -- Python restatements (the oracle for the header) -------------------------------------------
+
+
+def _fma(a, b, c):
+    if not (math.isfinite(a) and math.isfinite(b) and math.isfinite(c)):
+        return a * b + c
+    r = Fraction(a) * Fraction(b) + Fraction(c)
+    try:
+        return float(r)
+    except OverflowError:
+        return math.inf if r > 0 else -math.inf
+
+
+def _u64(x):
+    return struct.unpack("<Q", struct.pack("<d", x))[0]
+
+
+def _f64(u):
+    return struct.unpack("<d", struct.pack("<Q", u & 0xFFFFFFFFFFFFFFFF))[0]
+
+
+def _top12(x):
+    return _u64(x) >> 52
+
+
+def restated_log(x, t):
+    A, B, T = t["log_poly"], t["log_poly1"], t["log_tab"]
+    lo_b, hi_b = _u64(1.0 - 2.0 ** -4), _u64(1.0 + float.fromhex("0x1.09p-4"))
+    ix = _u64(x)
+    if (ix - lo_b) % 2 ** 64 < hi_b - lo_b:
+        if ix == _u64(1.0):
+            return 0.0
+        r = x - 1.0
+        r2 = r * r
+        r3 = r * r2
+        p3 = _fma(r3, B[10], _fma(r2, B[9], _fma(r, B[8], B[7])))
+        p2 = _fma(r3, p3, _fma(r2, B[6], _fma(r, B[5], B[4])))
+        p1 = _fma(r3, p2, _fma(r2, B[3], _fma(r, B[2], B[1])))
+        w = r * 2.0 ** 27
+        rhi = r + w - w
+        rlo = r - rhi
+        w = rhi * rhi * B[0]
+        hi = r + w
+        lo = r - hi + w
+        lo = _fma(B[0] * rlo, rhi + r, lo)
+        return _fma(r3, p1, lo) + hi
+    top = ix >> 48
+    if (top - 0x0010) % 2 ** 32 >= 0x7FF0 - 0x0010:
+        if (ix * 2) % 2 ** 64 == 0:
+            return -math.inf
+        if ix == _u64(math.inf):
+            return x
+        if (top & 0x8000) or (top & 0x7FF0) == 0x7FF0:
+            return math.nan
+        ix = _u64(x * 2.0 ** 52) - (52 << 52)
+    tmp = (ix - LOG_OFF) % 2 ** 64
+    i = (tmp >> (52 - 7)) % N_TAB
+    k = (tmp - 2 ** 64 if tmp >= 2 ** 63 else tmp) >> 52
+    z = _f64(ix - (tmp & (0xFFF << 52)))
+    invc, logc = T[2 * i], T[2 * i + 1]
+    r = _fma(z, invc, -1.0)
+    kd = float(k)
+    w = _fma(kd, LN2HI, logc)
+    hi = w + r
+    lo = _fma(kd, LN2LO, w - hi + r)
+    r2 = r * r
+    p = _fma(r2, _fma(r, A[4], A[3]), _fma(r, A[2], A[1]))
+    return _fma(r * r2, p, _fma(r2, A[0], lo)) + hi
+
+
+def _exp_special(tmp, sbits, ki, signed):
+    if (ki & 0x80000000) == 0:
+        scale = _f64((sbits - (1009 << 52)) % 2 ** 64)
+        return 2.0 ** 1009 * _fma(scale, tmp, scale)
+    sbits = (sbits + (1022 << 52)) % 2 ** 64
+    scale = _f64(sbits)
+    y = scale + scale * tmp  # scale * tmp has two uses: not fused
+    if (abs(y) if signed else y) < 1.0:
+        one = -1.0 if signed and y < 0.0 else 1.0
+        lo = scale - y + scale * tmp
+        hi = one + y
+        lo = one - hi + y + lo
+        y = (hi + lo) - one
+        if y == 0.0:
+            y = _f64(sbits & 0x8000000000000000) if signed else 0.0
+    return 2.0 ** -1022 * y
+
+
+def _exp_core(x, xtail, sign_bias, t, signed):
+    """exp (xtail None, exp.c) or pow's exp_inline (pow.c)."""
+    C2, C3, C4, C5 = t["exp_poly"]
+    T = t["exp_tab"]
+    abstop = _top12(x) & 0x7FF
+    if (abstop - _top12(2.0 ** -54)) % 2 ** 32 >= _top12(512.0) - _top12(2.0 ** -54):
+        if (abstop - _top12(2.0 ** -54)) % 2 ** 32 >= 0x80000000:
+            one = 1.0 + x
+            return -one if sign_bias else one
+        if abstop >= _top12(1024.0):
+            if xtail is None:
+                if x == -math.inf:
+                    return 0.0
+                if abstop >= _top12(math.inf):
+                    return 1.0 + x
+            if _u64(x) >> 63:
+                return -0.0 if sign_bias else 0.0
+            return -math.inf if sign_bias else math.inf
+        abstop = 0
+    kd = _fma(EXP_INVLN2N, x, t["exp_shift"])
+    ki = _u64(kd)
+    kd -= t["exp_shift"]
+    r = _fma(kd, t["exp_negln2loN"], _fma(kd, t["exp_negln2hiN"], x))
+    if xtail is not None:
+        r += xtail
+    idx = 2 * (ki % N_TAB)
+    top = ((ki + sign_bias) << (52 - 7)) % 2 ** 64
+    tail = _f64(T[idx])
+    sbits = (T[idx + 1] + top) % 2 ** 64
+    r2 = r * r
+    tmp = _fma(r2 * r2, _fma(r, C5, C4), _fma(r2, _fma(r, C3, C2), tail + r))
+    if abstop == 0:
+        return _exp_special(tmp, sbits, ki, signed)
+    scale = _f64(sbits)
+    return _fma(scale, tmp, scale)
+
+
+def restated_exp(x, t):
+    return _exp_core(x, None, 0, t, signed=False)
+
+
+def _checkint(iy):
+    e = iy >> 52 & 0x7FF
+    if e < 0x3FF:
+        return 0
+    if e > 0x3FF + 52:
+        return 2
+    if iy & ((1 << (0x3FF + 52 - e)) - 1):
+        return 0
+    if iy & (1 << (0x3FF + 52 - e)):
+        return 1
+    return 2
+
+
+def _zeroinfnan(i):
+    return (2 * i - 1) % 2 ** 64 >= 2 * _u64(math.inf) - 1
+
+
+def _pow_log(ix, t):
+    A, T = t["pow_poly"], t["pow_tab"]
+    tmp = (ix - POW_OFF) % 2 ** 64
+    i = (tmp >> (52 - 7)) % N_TAB
+    k = (tmp - 2 ** 64 if tmp >= 2 ** 63 else tmp) >> 52
+    z = _f64(ix - (tmp & (0xFFF << 52)))
+    kd = float(k)
+    invc, logc, logctail = T[4 * i], T[4 * i + 2], T[4 * i + 3]
+    r = _fma(z, invc, -1.0)
+    t1 = _fma(kd, LN2HI, logc)
+    t2 = t1 + r
+    lo1 = _fma(kd, LN2LO, logctail)
+    lo2 = t1 - t2 + r
+    ar = A[0] * r
+    ar2 = r * ar
+    ar3 = r * ar2
+    hi = t2 + ar2
+    lo3 = _fma(ar, r, -ar2)
+    lo4 = t2 - hi + ar2
+    p = ar3 * _fma(ar2, _fma(ar2, _fma(r, A[6], A[5]), _fma(r, A[4], A[3])), _fma(r, A[2], A[1]))
+    lo = lo1 + lo2 + lo3 + lo4 + p
+    y = hi + lo
+    return y, hi - y + lo
+
+
+def restated_pow(x, y, t):
+    sign_bias = 0
+    ix, iy = _u64(x), _u64(y)
+    topx, topy = ix >> 52, iy >> 52
+    if (topx - 1) % 2 ** 32 >= 0x7FF - 1 or ((topy & 0x7FF) - 0x3BE) % 2 ** 32 >= 0x43E - 0x3BE:
+        if _zeroinfnan(iy):
+            if (2 * iy) % 2 ** 64 == 0:
+                return 1.0
+            if ix == _u64(1.0):
+                return 1.0
+            if (2 * ix) % 2 ** 64 > 2 * _u64(math.inf) or (2 * iy) % 2 ** 64 > 2 * _u64(math.inf):
+                return x + y
+            if (2 * ix) % 2 ** 64 == 2 * _u64(1.0):
+                return 1.0
+            if ((2 * ix) % 2 ** 64 < 2 * _u64(1.0)) == (not (iy >> 63)):
+                return 0.0
+            return y * y
+        if _zeroinfnan(ix):
+            x2 = x * x
+            if ix >> 63 and _checkint(iy) == 1:
+                x2 = -x2
+            return (1 / x2 if x2 != 0 else math.copysign(math.inf, x2)) if iy >> 63 else x2
+        if ix >> 63:
+            yint = _checkint(iy)
+            if yint == 0:
+                return math.nan
+            if yint == 1:
+                sign_bias = 0x800 << 7
+            ix &= 0x7FFFFFFFFFFFFFFF
+            topx &= 0x7FF
+        if ((topy & 0x7FF) - 0x3BE) % 2 ** 32 >= 0x43E - 0x3BE:
+            if ix == _u64(1.0):
+                return 1.0
+            if (topy & 0x7FF) < 0x3BE:
+                return 1.0 + y if ix > _u64(1.0) else 1.0 - y
+            return math.inf if (ix > _u64(1.0)) == (topy < 0x800) else 0.0
+        if topx == 0:
+            ix = (_u64(_f64(ix) * 2.0 ** 52) & 0x7FFFFFFFFFFFFFFF) - (52 << 52)
+    hi, lo = _pow_log(ix, t)
+    ehi = y * hi
+    elo = _fma(y, lo, _fma(y, hi, -ehi))
+    return _exp_core(ehi, elo, sign_bias, t, signed=True)
+
+
+# -- verification ----------------------------------------------------------------------------------
+
+
+def _bits(v):
+    return np.array(v, np.float64).view(np.uint64)
+
+
+def _same(a, b):
+    return (math.isnan(a) and math.isnan(b)) or _bits(a) == _bits(b)
+
+
+def samples(n: int, seed: int = 0) -> np.ndarray:
+    """Positive doubles over every range the algorithms split on (subnormals included)."""
+    rng = np.random.default_rng(seed)
+    q = n // 6
+    parts = [rng.uniform(0.5, 2.0, q), rng.uniform(1 - 2 ** -4, 1 + 0.0646, q), np.exp(rng.uniform(-700, 700, q)),
+             rng.uniform(1e-3, 1e3, q),
+             np.frombuffer(rng.integers(1, 0x000FFFFFFFFFFFFF, q, dtype=np.uint64).tobytes(), np.float64),
+             np.frombuffer(rng.integers(0x0010000000000000, 0x7FEFFFFFFFFFFFFF, n - 5 * q,
+                                        dtype=np.uint64).tobytes(), np.float64)]
+    return np.concatenate(parts)
+
+
+def exp_samples(n: int, seed: int = 1) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    q = n // 5
+    return np.concatenate([rng.uniform(-5, 5, q), rng.uniform(-745.2, 709.8, q), rng.uniform(-1e-3, 1e-3, q),
+                           rng.uniform(-745.2, -700, q), rng.uniform(-2 ** -40, 2 ** -40, n - 4 * q)])
+
+
+def pow_samples(n: int, seed: int = 2):
+    """(x, k) with integer k >= 2 (the reference's POW nodes: Sym.__pow__, expr.py:835-845) and
+    general (x, y) pairs, negative bases included."""
+    rng = np.random.default_rng(seed)
+    h = n // 2
+    xs = np.concatenate([rng.uniform(-3.0, 3.0, h // 2), rng.uniform(0.5, 2.0, h // 2)])
+    ks = rng.integers(2, 12, xs.size).astype(np.float64)
+    gx = rng.uniform(1e-3, 100, n - h)
+    gy = rng.uniform(-30, 30, n - h)
+    return np.concatenate([xs, gx]), np.concatenate([ks, gy])
+
+
+def verify(t: dict, n: int) -> list[str]:
+    bad = []
+    for x in samples(n).tolist():
+        if not _same(restated_log(x, t), math.log(x)):
+            bad.append(f"log({x!r})")
+    for x in exp_samples(n).tolist():
+        try:
+            want = math.exp(x)
+        except OverflowError:
+            want = math.inf
+        if not _same(restated_exp(x, t), want):
+            bad.append(f"exp({x!r})")
+    for x, y in zip(*[a.tolist() for a in pow_samples(n)]):
+        try:
+            want = math.pow(x, y)
+        except (OverflowError, ValueError):
+            continue
+        if not _same(restated_pow(x, y, t), want):
+            bad.append(f"pow({x!r}, {y!r})")
+    return bad
+
+
+# -- the header ------------------------------------------------------------------------------------
+
+
+def _lit(v) -> str:
+    return float(v).hex()
+
+
+def _arr(vals) -> str:
+    return ", ".join(_lit(v) for v in vals)
+
+
+def header(t: dict, source: str) -> str:
+    log_rows = ",\n".join(f"    {_lit(t['log_tab'][2 * j])}, {_lit(t['log_tab'][2 * j + 1])}" for j in range(N_TAB))
+    pow_rows = ",\n".join(f"    {_lit(t['pow_tab'][4 * j])}, {_lit(t['pow_tab'][4 * j + 2])}, "
+                          f"{_lit(t['pow_tab'][4 * j + 3])}" for j in range(N_TAB))
+    exp_rows = ",\n".join(f"    0x{t['exp_tab'][2 * j]:016x}ull, 0x{t['exp_tab'][2 * j + 1]:016x}ull"
+                          for j in range(N_TAB))
+    return f"""// GENERATED by tools/gen_glibc_math.py from {source} -- do not edit.
+//
+// sgb_log / sgb_exp / sgb_pow: glibc 2.39's log, exp and pow (the ARM optimized-routines algorithms,
+// sysdeps/ieee754/dbl-64/e_log.c, e_exp.c, e_pow.c) restated for the device, FMA build (x86-64 glibc
+// selects it by ifunc; GCC fuses every product whose value has a single use in an addition).  The
+// reference evaluates LOG / EXP / POW with Python's math module, i.e. these functions
+// (codegen.py:545-557), so such templates are bit-exact on the device.  The tables are glibc's
+// __log_data, __exp_data and __pow_log_data, read from the installed libm; the generator checks its
+// Python restatement of every function against math bit for bit before writing this file.
+#ifndef SGB_GLIBC_MATH_H
+#define SGB_GLIBC_MATH_H
+
+#define SGB_LN2HI {_lit(LN2HI)}
+#define SGB_LN2LO {_lit(LN2LO)}
+__device__ const double sgb_log_poly[5] = {{{_arr(t['log_poly'])}}};
+__device__ const double sgb_log_poly1[11] = {{{_arr(t['log_poly1'])}}};
+__device__ const double sgb_log_tab[{2 * N_TAB}] = {{  // (1/c, log c) per subinterval
+{log_rows}}};
+__device__ const double sgb_pow_poly[7] = {{{_arr(t['pow_poly'])}}};
+__device__ const double sgb_pow_tab[{3 * N_TAB}] = {{  // (1/c, log c, log c tail) per subinterval
+{pow_rows}}};
+__device__ const double sgb_exp_poly[4] = {{{_arr(t['exp_poly'])}}};
+__device__ const unsigned long long sgb_exp_tab[{2 * N_TAB}] = {{  // (tail, bits of 2^(j/128))
+{exp_rows}}};
+#define SGB_EXP_INVLN2N {_lit(EXP_INVLN2N)}
+#define SGB_EXP_SHIFT {_lit(t['exp_shift'])}
+#define SGB_EXP_NEGLN2HIN {_lit(t['exp_negln2hiN'])}
+#define SGB_EXP_NEGLN2LON {_lit(t['exp_negln2loN'])}
+
+__device__ __forceinline__ double sgb_as_double(unsigned long long u) {{ return __longlong_as_double((long long)u); }}
+__device__ __forceinline__ unsigned long long sgb_as_u64(double x) {{ return (unsigned long long)__double_as_longlong(x); }}
+
+__device__ __noinline__ double sgb_log(double x) {{
+  unsigned long long ix = sgb_as_u64(x);
+  const unsigned long long lo_b = 0x3fee000000000000ull, hi_b = 0x3ff1090000000000ull;  // 1 -/+ 2^-4, 1.0646
+  if (ix - lo_b < hi_b - lo_b) {{  // |x - 1| small: polynomial in r = x - 1, exact split of r*r/2
+    if (ix == 0x3ff0000000000000ull) return 0.0;
+    const double *B = sgb_log_poly1;
+    const double r = __dsub_rn(x, 1.0), r2 = __dmul_rn(r, r), r3 = __dmul_rn(r, r2);
+    const double p3 = __fma_rn(r3, B[10], __fma_rn(r2, B[9], __fma_rn(r, B[8], B[7])));
+    const double p2 = __fma_rn(r3, p3, __fma_rn(r2, B[6], __fma_rn(r, B[5], B[4])));
+    const double p1 = __fma_rn(r3, p2, __fma_rn(r2, B[3], __fma_rn(r, B[2], B[1])));
+    double w = __dmul_rn(r, 0x1p27);
+    const double rhi = __dsub_rn(__dadd_rn(r, w), w);
+    const double rlo = __dsub_rn(r, rhi);
+    w = __dmul_rn(__dmul_rn(rhi, rhi), B[0]);
+    const double hi = __dadd_rn(r, w);
+    double lo = __dadd_rn(__dsub_rn(r, hi), w);
+    lo = __fma_rn(__dmul_rn(B[0], rlo), __dadd_rn(rhi, r), lo);
+    return __dadd_rn(__fma_rn(r3, p1, lo), hi);
+  }}
+  const unsigned top = (unsigned)(ix >> 48);
+  if (top - 0x0010u >= 0x7ff0u - 0x0010u) {{
+    if ((ix << 1) == 0) return sgb_as_double(0xfff0000000000000ull);  // log(+-0) = -inf
+    if (ix == 0x7ff0000000000000ull) return x;                        // log(inf) = inf
+    if ((top & 0x8000u) || (top & 0x7ff0u) == 0x7ff0u)                // x < 0 or NaN
+      return isnan(x) ? sgb_as_double(ix | 0x0008000000000000ull) : sgb_as_double(0xfff8000000000000ull);
+    ix = sgb_as_u64(__dmul_rn(x, 0x1p52)) - (52ull << 52);  // subnormal
+  }}
+  const unsigned long long tmp = ix - {LOG_OFF:#x}ull;
+  const int i = (int)((tmp >> (52 - 7)) % {N_TAB});
+  const long long k = (long long)tmp >> 52;
+  const double z = sgb_as_double(ix - (tmp & (0xfffull << 52)));
+  const double invc = sgb_log_tab[2 * i], logc = sgb_log_tab[2 * i + 1];
+  const double r = __fma_rn(z, invc, -1.0);
+  const double kd = (double)k;
+  const double w = __fma_rn(kd, SGB_LN2HI, logc);
+  const double hi = __dadd_rn(w, r);
+  const double lo = __fma_rn(kd, SGB_LN2LO, __dadd_rn(__dsub_rn(w, hi), r));
+  const double *A = sgb_log_poly;
+  const double r2 = __dmul_rn(r, r);
+  const double p = __fma_rn(r2, __fma_rn(r, A[4], A[3]), __fma_rn(r, A[2], A[1]));
+  return __dadd_rn(__fma_rn(__dmul_rn(r, r2), p, __fma_rn(r2, A[0], lo)), hi);
+}}
+
+// exp's and pow's scaling near the ends of the range (k = round(x * 128 / ln2) out of [-1022, 1023] * 128)
+__device__ __forceinline__ double sgb_exp_special(double tmp, unsigned long long sbits, unsigned long long ki, bool sgn) {{
+  if ((ki & 0x80000000ull) == 0) {{
+    const double scale = sgb_as_double(sbits - (1009ull << 52));
+    return __dmul_rn(0x1p1009, __fma_rn(scale, tmp, scale));
+  }}
+  sbits += 1022ull << 52;
+  const double scale = sgb_as_double(sbits);
+  const double st = __dmul_rn(scale, tmp);  // two uses: not fused
+  double y = __dadd_rn(scale, st);
+  if ((sgn ? fabs(y) : y) < 1.0) {{
+    const double one = (sgn && y < 0.0) ? -1.0 : 1.0;
+    double lo = __dadd_rn(__dsub_rn(scale, y), st);
+    const double hi = __dadd_rn(one, y);
+    lo = __dadd_rn(__dadd_rn(__dsub_rn(one, hi), y), lo);
+    y = __dsub_rn(__dadd_rn(hi, lo), one);
+    if (y == 0.0) y = sgn ? sgb_as_double(sbits & 0x8000000000000000ull) : 0.0;
+  }}
+  return __dmul_rn(0x1p-1022, y);
+}}
+
+// exp (xtail unused, pow == false) and pow's exp_inline (x + xtail, sign_bias)
+__device__ __forceinline__ double sgb_exp_core(double x, double xtail, unsigned sign_bias, bool pow_) {{
+  unsigned abstop = (unsigned)(sgb_as_u64(x) >> 52) & 0x7ffu;
+  if (abstop - 0x3c9u >= 0x408u - 0x3c9u) {{  // |x| < 2^-54 or |x| >= 512 (or inf / nan)
+    if (abstop - 0x3c9u >= 0x80000000u) {{
+      const double one = __dadd_rn(1.0, x);
+      return sign_bias ? -one : one;
+    }}
+    if (abstop >= 0x409u) {{
+      if (!pow_) {{
+        if (sgb_as_u64(x) == 0xfff0000000000000ull) return 0.0;
+        if (abstop >= 0x7ffu) return __dadd_rn(1.0, x);
+      }}
+      if (sgb_as_u64(x) >> 63) return sign_bias ? -0.0 : 0.0;
+      return sign_bias ? sgb_as_double(0xfff0000000000000ull) : sgb_as_double(0x7ff0000000000000ull);
+    }}
+    abstop = 0;  // large |x|: scaled below
+  }}
+  double kd = __fma_rn(SGB_EXP_INVLN2N, x, SGB_EXP_SHIFT);
+  const unsigned long long ki = sgb_as_u64(kd);
+  kd = __dsub_rn(kd, SGB_EXP_SHIFT);
+  double r = __fma_rn(kd, SGB_EXP_NEGLN2LON, __fma_rn(kd, SGB_EXP_NEGLN2HIN, x));
+  if (pow_) r = __dadd_rn(r, xtail);
+  const unsigned idx = 2u * (unsigned)(ki % {N_TAB});
+  const unsigned long long top = (ki + sign_bias) << (52 - 7);
+  const double tail = sgb_as_double(sgb_exp_tab[idx]);
+  const unsigned long long sbits = sgb_exp_tab[idx + 1] + top;
+  const double *C = sgb_exp_poly;
+  const double r2 = __dmul_rn(r, r);
+  const double tmp = __fma_rn(__dmul_rn(r2, r2), __fma_rn(r, C[3], C[2]),
+                              __fma_rn(r2, __fma_rn(r, C[1], C[0]), __dadd_rn(tail, r)));
+  if (abstop == 0) return sgb_exp_special(tmp, sbits, ki, pow_);
+  const double scale = sgb_as_double(sbits);
+  return __fma_rn(scale, tmp, scale);
+}}
+
+__device__ __noinline__ double sgb_exp(double x) {{ return sgb_exp_core(x, 0.0, 0u, false); }}
+
+// 0: y not an integer, 1: odd integer, 2: even integer (y non-zero finite)
+__device__ __forceinline__ int sgb_checkint(unsigned long long iy) {{
+  const int e = (int)(iy >> 52 & 0x7ff);
+  if (e < 0x3ff) return 0;
+  if (e > 0x3ff + 52) return 2;
+  if (iy & ((1ull << (0x3ff + 52 - e)) - 1)) return 0;
+  if (iy & (1ull << (0x3ff + 52 - e))) return 1;
+  return 2;
+}}
+
+__device__ __forceinline__ bool sgb_zeroinfnan(unsigned long long i) {{
+  return 2 * i - 1 >= 2 * 0x7ff0000000000000ull - 1;
+}}
+
+__device__ __noinline__ double sgb_pow(double x, double y) {{
+  unsigned sign_bias = 0;
+  unsigned long long ix = sgb_as_u64(x);
+  const unsigned long long iy = sgb_as_u64(y);
+  unsigned topx = (unsigned)(ix >> 52);
+  const unsigned topy = (unsigned)(iy >> 52);
+  if (topx - 0x001u >= 0x7ffu - 0x001u || (topy & 0x7ffu) - 0x3beu >= 0x43eu - 0x3beu) {{
+    if (sgb_zeroinfnan(iy)) {{
+      if (2 * iy == 0) return 1.0;
+      if (ix == 0x3ff0000000000000ull) return 1.0;
+      if (2 * ix > 2 * 0x7ff0000000000000ull || 2 * iy > 2 * 0x7ff0000000000000ull) return __dadd_rn(x, y);
+      if (2 * ix == 2 * 0x3ff0000000000000ull) return 1.0;
+      if ((2 * ix < 2 * 0x3ff0000000000000ull) == !(iy >> 63)) return 0.0;
+      return __dmul_rn(y, y);
+    }}
+    if (sgb_zeroinfnan(ix)) {{
+      double x2 = __dmul_rn(x, x);
+      if ((ix >> 63) && sgb_checkint(iy) == 1) x2 = -x2;
+      return (iy >> 63) ? __ddiv_rn(1.0, x2) : x2;
+    }}
+    if (ix >> 63) {{  // finite x < 0
+      const int yint = sgb_checkint(iy);
+      if (yint == 0) return sgb_as_double(0xfff8000000000000ull);  // x86 default NaN
+      if (yint == 1) sign_bias = 0x800u << 7;
+      ix &= 0x7fffffffffffffffull;
+      topx &= 0x7ffu;
+    }}
+    if ((topy & 0x7ffu) - 0x3beu >= 0x43eu - 0x3beu) {{
+      if (ix == 0x3ff0000000000000ull) return 1.0;
+      if ((topy & 0x7ffu) < 0x3beu) return ix > 0x3ff0000000000000ull ? __dadd_rn(1.0, y) : __dsub_rn(1.0, y);
+      return (ix > 0x3ff0000000000000ull) == (topy < 0x800u) ? sgb_as_double(0x7ff0000000000000ull) : 0.0;
+    }}
+    if (topx == 0) ix = (sgb_as_u64(__dmul_rn(sgb_as_double(ix), 0x1p52)) & 0x7fffffffffffffffull) - (52ull << 52);
+  }}
+  // log(x) as hi + lo (pow.c log_inline)
+  const unsigned long long tmp = ix - {POW_OFF:#x}ull;
+  const int i = (int)((tmp >> (52 - 7)) % {N_TAB});
+  const long long k = (long long)tmp >> 52;
+  const double z = sgb_as_double(ix - (tmp & (0xfffull << 52)));
+  const double kd = (double)k;
+  const double invc = sgb_pow_tab[3 * i], logc = sgb_pow_tab[3 * i + 1], logctail = sgb_pow_tab[3 * i + 2];
+  const double r = __fma_rn(z, invc, -1.0);
+  const double t1 = __fma_rn(kd, SGB_LN2HI, logc);
+  const double t2 = __dadd_rn(t1, r);
+  const double lo1 = __fma_rn(kd, SGB_LN2LO, logctail);
+  const double lo2 = __dadd_rn(__dsub_rn(t1, t2), r);
+  const double *A = sgb_pow_poly;
+  const double ar = __dmul_rn(A[0], r), ar2 = __dmul_rn(r, ar), ar3 = __dmul_rn(r, ar2);
+  const double hi = __dadd_rn(t2, ar2);
+  const double lo3 = __fma_rn(ar, r, -ar2);
+  const double lo4 = __dadd_rn(__dsub_rn(t2, hi), ar2);
+  const double p = __dmul_rn(ar3, __fma_rn(ar2, __fma_rn(ar2, __fma_rn(r, A[6], A[5]), __fma_rn(r, A[4], A[3])),
+                                          __fma_rn(r, A[2], A[1])));
+  const double lo = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(lo1, lo2), lo3), lo4), p);
+  const double lhi = __dadd_rn(hi, lo);
+  const double llo = __dadd_rn(__dsub_rn(hi, lhi), lo);
+  // y * log(x) as ehi + elo, then exp
+  const double ehi = __dmul_rn(y, lhi);
+  const double elo = __fma_rn(y, llo, __fma_rn(y, lhi, -ehi));
+  return sgb_exp_core(ehi, elo, sign_bias, true);
+}}
+
+#endif  // SGB_GLIBC_MATH_H
+"""
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--samples", type=int, default=300000)
+    args = ap.parse_args()
+    path = libm_path()
+    t = read_tables(path)
+    bad = verify(t, args.samples)
+    if bad:
+        raise SystemExit(f"restatement differs from math on {len(bad)} samples, e.g. {bad[:5]}")
+    OUT.write_text(header(t, str(path)))
+    print(f"wrote {OUT} (log / exp / pow restatements bit-identical to math on {args.samples} samples each)")
+
+
+if __name__ == "__main__":
+    sys.exit(main())
