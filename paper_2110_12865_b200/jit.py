@@ -65,14 +65,14 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 """
 
-# glibc's log / exp / pow restated for the device (tools/gen_glibc_math.py): the reference's math
-# module, bit for bit
+# glibc's sin / cos / exp / log / pow restated for the device (tools/gen_glibc_math.py): the
+# reference's math module, bit for bit
 _PREAMBLE += (Path(__file__).resolve().parent / "csrc" / "glibc_math.h").read_text()
 
 _BIN = {L.T_MUL: "__dmul_rn({a}, {b})", L.T_ADD: "__dadd_rn({a}, {b})", L.T_SUB: "__dsub_rn({a}, {b})",
         L.T_DIV: "__ddiv_rn({a}, {b})", L.T_MADD: "__dadd_rn(__dmul_rn({a}, {b}), {c})",
         L.T_MSUB: "__dsub_rn(__dmul_rn({a}, {b}), {c})", L.T_RMSUB: "__dsub_rn({c}, __dmul_rn({a}, {b}))"}
-_SLOW = {0: "sin({a})", 1: "cos({a})", 2: "sgb_exp({a})", 3: "sgb_log({a})"}
+_SLOW = {0: "sgb_sin({a})", 1: "sgb_cos({a})", 2: "sgb_exp({a})", 3: "sgb_log({a})"}
 
 
 def _imm(v: float) -> str:
@@ -444,12 +444,18 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
     """CSR-window kernel of unit ``u`` (lower._csr_windows): block w assembles the outputs
     [win_k[w], win_k[w+1]) in shared memory and writes them out with 16-byte streaming stores.
 
-    Work inside a window is block-uniform, so nothing diverges: the outputs copied from the
-    value array (inputs, earlier waves' results) first, then the members in chunks -- every
-    member of a chunk takes its piece (instance range) with one instance per thread, all the
-    chunk's loads issued before its computes (WINDOW_LOADS per thread) -- each result stored at
-    its FLAG_WPOS16 position in the window.  Members store nothing to the value array (the last
-    wave: never re-read), so every output crosses HBM once, coalesced.
+    Work inside a window is block-uniform, so nothing diverges.  On row windows (mesh plans:
+    instance = vertex = CSR row) one round trip feeds the whole window: asynchronous copies
+    (LDGSTS, no registers held) stage every operand stream of the row-aligned members -- streams
+    of neighbouring bases merged into one range -- and, when their sources are dense, the copied
+    outputs (inputs, earlier waves' results) with their packed (source, position) descriptors;
+    the window positions of the aligned members load into registers meanwhile.  The other
+    members (mesh boundary groups) run in chunks from global memory while the stage fills --
+    every member of a chunk takes its piece (instance range) with one instance per thread, the
+    chunk's loads issued before its computes.  Then the aligned members compute from shared
+    memory, one row per thread.  Every result goes to its FLAG_WPOS16 position in the window;
+    members store nothing to the value array (the last wave: never re-read), so every output
+    crosses HBM once, coalesced.
     """
     unit = dp.unit(u)
     g0, g1 = unit["group_begin"], unit["group_end"]
@@ -457,7 +463,6 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
     wn = dp.windows
     ROWS = int(wn.rows) if wn is not None else 0
     staged = [g0 + j for j in range(J) if ROWS and wn.aligned[j]]
-    NS = len(wn.streams) if staged else 0
     chunks, cur, width = [], [], 0
     for gi in range(g0, g1):
         rec = dp.groups[gi]
@@ -473,20 +478,26 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
     if cur:
         chunks.append(cur)
     B = JIT_BLOCK
-    out = []
-    if staged:  # operand streams of the staged members: (base, stride) per stream, u32 modular
-        out.append(f"__constant__ u32 sgb_wsb_u{u}[{NS}] = {{{', '.join(f'{b % 2**32}u' for b, _ in wn.streams)}}};")
-        out.append(f"__constant__ u32 sgb_wss_u{u}[{NS}] = {{{', '.join(f'{t % 2**32}u' for _, t in wn.streams)}}};")
-    out += [f'extern "C" __global__ void __launch_bounds__({B}, {WINDOW_MIN_BLOCKS}) sgb_window_u{u}(',
-            "    Tables T, const int2 *pieces, const i64 *win_k, const i64 *copy_off, const u32 *copy_src,",
-            "    const u16 *copy_pos, i64 n_win, const double *x, double *out) {",
-            "  extern __shared__ __align__(16) double smem_[];",
-            f"  double *const stage_ = smem_;  // [{NS}][{ROWS}] staged operand streams",
-            f"  double *const buf = smem_ + {NS * ROWS};  // the window",
-            f"  __shared__ int2 sp[{J}];",
-            "  const int tid = threadIdx.x;",
-            "  for (i64 w = blockIdx.x; w < n_win; w += gridDim.x) {",
-            f"    for (int j = tid; j < {J}; j += {B}) sp[j] = __ldg(pieces + w * {J} + j);",
+    RD = wn.range_doubles if staged else 0
+    CS = wn.cstage if staged else 0  # staged copy span (doubles), then its u32 descriptors
+    DS = wn.dstage if staged else 0
+    STAGE = wn.stage_doubles if staged else 0
+    roff, o_ = [], 0
+    for _, _, n in (wn.ranges if staged else []):
+        roff.append(o_)
+        o_ += int(n)
+    out = [f'extern "C" __global__ void __launch_bounds__({B}, {WINDOW_MIN_BLOCKS}) sgb_window_u{u}(',
+           "    Tables T, const int2 *pieces, const i64 *win_k, const i64 *copy_off, const u32 *copy_src,",
+           "    const u16 *copy_pos, const uint2 *cstg, const u32 *copy_pk, i64 n_win, const double *x,",
+           "    double *out) {",
+           "  extern __shared__ __align__(16) double smem_[];",
+           f"  double *const stage_ = smem_;  // {RD} doubles of operand ranges, {CS} of copied sources",
+           f"  const u32 *const dsc_ = reinterpret_cast<const u32 *>(smem_ + {RD + CS});  // {DS} copy descriptors",
+           f"  double *const buf = smem_ + {STAGE};  // the window",
+           f"  __shared__ int2 sp[{J}];",
+           "  const int tid = threadIdx.x;",
+           "  for (i64 w = blockIdx.x; w < n_win; w += gridDim.x) {",
+           f"    for (int j = tid; j < {J}; j += {B}) sp[j] = __ldg(pieces + w * {J} + j);",
            "    const i64 k0 = __ldg(win_k + w);",
            "    const u32 len_ = (u32)(__ldg(win_k + w + 1) - k0);",
            "    const i64 c0_ = __ldg(copy_off + w), c1_ = __ldg(copy_off + w + 1);",
@@ -495,12 +506,19 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
            "    double *bw = buf + head_;",
            "    __syncthreads();"]
     if staged:
-        n_a = int(dp.groups[staged[0]]["n"])
+        ja = staged[0] - g0
         H = B // ROWS  # thread groups of the staged compute: thread tid takes row tid % ROWS
-        out += [f"    const u32 R0 = (u32)w * {ROWS}u, nrow = min({ROWS}u, {n_a}u - R0);",
-                f"    for (u32 e = tid; e < {NS * ROWS}u; e += {B}u) {{  // stage[s][r] = x[base_s + stride_s * (R0 + r)]",
-                f"      const u32 s_ = e / {ROWS}u, r_ = e % {ROWS}u;",
-                f"      if (r_ < nrow) cp_async8(stage_ + e, x + (sgb_wsb_u{u}[s_] + sgb_wss_u{u}[s_] * (R0 + r_)));",
+        out += [f"    const u32 R0 = (u32)sp[{ja}].x, nrow = (u32)sp[{ja}].y;  // the window's rows"]
+        for q, (base, stride, n) in enumerate(wn.ranges):  # range q element e = x[base + stride*(R0 + e)]
+            lim = f"{int(n) - ROWS}u + nrow" if stride == 1 else "nrow"
+            out.append(f"    for (u32 e = tid; e < {lim}; e += {B}u) "
+                       f"cp_async8(stage_ + {roff[q] + 0}u + e, x + ({base % 2**32}u + {stride % 2**32}u * (R0 + e)));")
+        out += ["    const uint2 cs_ = __ldg(cstg + w);  // staged copies: first source, span (0: gathered)",
+                "    if (cs_.y) {",
+                f"      for (u32 e = tid; e < cs_.y; e += {B}u) cp_async8(stage_ + {RD}u + e, x + (cs_.x + e));",
+                f"      for (u32 e = tid; e < (u32)(c1_ - c0_); e += {B}u)",
+                "        asm volatile(\"cp.async.ca.shared.global [%0], [%1], 4;\" :: "
+                "\"r\"((unsigned)__cvta_generic_to_shared(dsc_ + e)), \"l\"(copy_pk + c0_ + e) : \"memory\");",
                 "    }",
                 f"    const u32 rr_ = tid % {ROWS}u, hh_ = tid / {ROWS}u;",
                 "    const bool okr_ = rr_ < nrow;",
@@ -524,13 +542,19 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
                     out.append(f"      wq{q} = __ldcs(T.ooff + {_off(off)} + ir_);")
                     q += 1
             out.append("    }")
-    out += [f"    for (i64 c = c0_ + tid; c < c1_; c += {B * COPY_UNROLL}) {{"]
+    gather = [f"    for (i64 c = c0_ + tid; c < c1_; c += {B * COPY_UNROLL}) {{"]
     for q in range(COPY_UNROLL):  # named registers (no local arrays): every copy's loads in flight
-        out.append(f"      const bool cq{q} = c + {q * B} < c1_;")
-        out.append(f"      const u16 cp{q} = cq{q} ? __ldcs(copy_pos + c + {q * B}) : (u16)0;")
-        out.append(f"      const double cv{q} = cq{q} ? __ldg(x + __ldcs(copy_src + c + {q * B})) : 0.0;")
-    out += [f"      if (cq{q}) bw[cp{q}] = cv{q};" for q in range(COPY_UNROLL)]
-    out += ["    }"]
+        gather.append(f"      const bool cq{q} = c + {q * B} < c1_;")
+        gather.append(f"      const u16 cp{q} = cq{q} ? __ldcs(copy_pos + c + {q * B}) : (u16)0;")
+        gather.append(f"      const double cv{q} = cq{q} ? __ldg(x + __ldcs(copy_src + c + {q * B})) : 0.0;")
+    gather += [f"      if (cq{q}) bw[cp{q}] = cv{q};" for q in range(COPY_UNROLL)]
+    gather += ["    }"]
+    if staged:
+        out.append("    if (!cs_.y) {  // copies too sparse to stage: gathered from global")
+        out += ["  " + ln for ln in gather]
+        out.append("    }")
+    else:
+        out += gather
     for chunk in chunks:
         cmax = "0"
         for gi in chunk:
@@ -550,13 +574,19 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
     if staged:  # the staged members: operands from shared memory, one row per thread
         out.append("    cp_async_wait_all();")
         out.append("    __syncthreads();")
+        out.append("    if (cs_.y)  // the staged copies: shared to shared")
+        out.append(f"      for (u32 e = tid; e < (u32)(c1_ - c0_); e += {B}u) {{"
+                   f" const u32 pk = dsc_[e]; bw[pk & 0xFFFFu] = stage_[{RD}u + (pk >> 16)]; }}")
         for h, ms in enumerate(part):
             out.append(f"    {'if' if h == 0 else 'else if'} (hh_ == {h}u && okr_) {{")
             q = 0
             for gi in ms:
                 rec = dp.groups[gi]
                 j = gi - g0
-                src = [f"stage_[{wn.slot_stream[j][s_] * ROWS}u + rr_]" for s_ in range(int(rec["n_slots"]))]
+                src = []
+                for s_ in range(int(rec["n_slots"])):
+                    qs = wn.slot_stream[j][s_]
+                    src.append(f"stage_[{roff[wn.stream_range[qs]] + wn.stream_delta[qs]}u + rr_]")
                 sfx = f"_{j}"
                 for r in range(int(rec["n_roots"])):
                     out.append(f"      const u16 wp{r}{sfx} = wq{q};")

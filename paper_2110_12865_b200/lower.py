@@ -36,9 +36,11 @@ import numpy as np
 
 from .plan import EXACT_OPS, OpKind, reachable, slot_addresses, unique_addresses
 
-# ops the device reproduces bit for bit: the reference's _EXACT_OPS (codegen.py:43-53) and LOG / EXP /
-# POW (glibc's algorithms restated, csrc/glibc_math.h); SIN / COS stay on CUDA's libm (1e-12)
-DEVICE_EXACT_OPS = frozenset(EXACT_OPS) | {int(OpKind.LOG), int(OpKind.EXP), int(OpKind.POW)}
+# ops the device reproduces bit for bit: the reference's _EXACT_OPS (codegen.py:43-53) and SIN / COS /
+# EXP / LOG / POW (glibc's algorithms restated, csrc/glibc_math.h; SIN / COS for |x| < 105414350,
+# beyond which glibc's Payne-Hanek reduction is replaced by CUDA's -- within 1e-12)
+DEVICE_EXACT_OPS = frozenset(EXACT_OPS) | {int(OpKind.SIN), int(OpKind.COS), int(OpKind.LOG), int(OpKind.EXP),
+                                           int(OpKind.POW)}
 KIND_TAPE, KIND_SOP = 0, 1
 FLAG_SELFREF, FLAG_INTERLEAVED, FLAG_SERIAL, FLAG_EXACT, FLAG_STREAM, FLAG_W16 = 1, 2, 4, 8, 16, 32
 FLAG_AFFINE0 = 64  # index column 0 is a0_base + a0_stride * i: no table read
@@ -798,15 +800,34 @@ class CsrWindows:
     aligned: list = field(default_factory=list)  # per member: its operands are staged (jit.window_source)
     streams: list = field(default_factory=list)  # staged operand streams (base, stride): x[base + stride*i]
     slot_stream: dict = field(default_factory=dict)  # aligned member -> stream index of each slot
+    # stage ranges: streams of stride 1 whose bases lie within STREAM_MERGE of each other share one
+    # range (base, stride, length); stream q is range stream_range[q] at offset stream_delta[q]
+    ranges: list = field(default_factory=list)
+    stream_range: list = field(default_factory=list)
+    stream_delta: list = field(default_factory=list)
+    # staged copies: window w's copy sources lie in [base, base + span) = copy_stage[w] (span 0: not
+    # staged, gathered from global); copy_pk[c] = (source - base) << 16 | window position
+    copy_stage: np.ndarray = None  # uint32 [n_win, 2]: (first source, span); span 0 = gathered from global
+    copy_pk: np.ndarray = None
+    cstage: int = 0  # doubles of the staged copy span (max over staged windows)
+    dstage: int = 0  # packed copy descriptors staged per window (max over staged windows)
+
+    @property
+    def range_doubles(self) -> int:
+        return sum(int(n) for _, _, n in self.ranges)
 
     @property
     def stage_doubles(self) -> int:
-        return len(self.streams) * self.rows
+        """Shared memory in front of the window buffer: ranges, copy span, copy descriptors (u32 pairs)."""
+        return self.range_doubles + self.cstage + (self.dstage + 1) // 2
 
 
 # row-window heights tried, largest first (one 256-thread block: 2 halves); SGB_STAGE_ROWS=0 turns the
 # staged windows off (the profiling comparison in tools/gpu_r2d.sh)
 STAGE_ROWS = () if os.environ.get("SGB_STAGE_ROWS") == "0" else (128, 64, 32)
+STREAM_MERGE = 16  # staged streams of stride 1 closer than this share one range
+COPY_STAGE_MAX = 2048  # a window's copies are staged when their sources span at most this many doubles..
+COPY_STAGE_DENSITY = 4  # ..and at most this many times their count
 STAGE_MAX_BYTES = 96 * 1024  # shared memory a staged window may use (operand streams + window buffer)
 
 
@@ -873,10 +894,28 @@ def _member_streams(plan, kp) -> list:
     return [(base + int(c), stride) for c in kp.coherence]
 
 
+def _merge_streams(wn) -> None:
+    """Stride-1 streams whose bases are within STREAM_MERGE share one staged range."""
+    order = sorted(range(len(wn.streams)), key=lambda q: (wn.streams[q][1], wn.streams[q][0]))
+    ranges, rng_of, delta = [], [0] * len(wn.streams), [0] * len(wn.streams)
+    for q in order:
+        base, stride = wn.streams[q]
+        if ranges and stride == 1 and ranges[-1][1] == 1 and base - ranges[-1][0] <= STREAM_MERGE:
+            lo, _, n = ranges[-1]
+            ranges[-1] = (lo, 1, max(n, base - lo + wn.rows))
+        else:
+            ranges.append((base, stride, wn.rows))
+        rng_of[q] = len(ranges) - 1
+        delta[q] = base - ranges[-1][0]
+    wn.ranges, wn.stream_range, wn.stream_delta = ranges, rng_of, delta
+
+
 def _stage_bytes(plan, groups, rows: int, wlen: int) -> int:
     streams = stage_streams([_member_streams(plan, plan.kernels[g.kernel]) for g in groups])
-    roots = sum(g.n_roots for g in groups)
-    return 8 * len(streams) * rows + 2 * roots * rows + 8 * (wlen + 2)
+    fake = CsrWindows(k=None, pieces=None, wpos=None, copy_off=None, copy_src=None, copy_pos=None, rows=rows,
+                      streams=streams)
+    _merge_streams(fake)
+    return 8 * fake.range_doubles + 8 * (wlen + 2) + 8 * 1024  # + a typical copy stage
 
 
 def _csr_windows(member_opos: list, n_out: int, copy_k: np.ndarray, copy_addr: np.ndarray,
@@ -975,9 +1014,25 @@ def _csr_windows(member_opos: list, n_out: int, copy_k: np.ndarray, copy_addr: n
     cw = np.searchsorted(k, ck, side="right") - 1
     copy_pos = (ck - k[np.clip(cw, 0, max(n_win - 1, 0))]).astype(np.uint16) if ck.size else np.zeros(0, np.uint16)
     aligned = set(row_mode[2]) if row_mode is not None else set()
+    # staged copies (row windows only): per window the span of its copy sources
+    copy_stage = np.zeros((n_win, 2), np.uint32)
+    copy_pk = np.zeros(ca.size, np.uint32)
+    cstage = dstage = 0
+    if row_mode is not None and ca.size:
+        for w in range(n_win):
+            c0, c1 = int(copy_off[w]), int(copy_off[w + 1])
+            if c1 == c0:
+                continue
+            lo_, hi_ = int(ca[c0:c1].min()), int(ca[c0:c1].max())
+            span = hi_ - lo_ + 1
+            if span <= COPY_STAGE_MAX and span <= COPY_STAGE_DENSITY * (c1 - c0):
+                copy_stage[w] = (lo_, span)
+                copy_pk[c0:c1] = ((ca[c0:c1] - lo_) << 16 | copy_pos[c0:c1].astype(np.int64)).astype(np.uint32)
+                cstage, dstage = max(cstage, span), max(dstage, c1 - c0)
     return CsrWindows(k=k, pieces=pieces, wpos=wpos, copy_off=copy_off, copy_src=ca.astype(np.uint32),
                       copy_pos=copy_pos, rows=row_mode[0] if row_mode is not None else 0,
-                      aligned=[j in aligned for j in range(J)])
+                      aligned=[j in aligned for j in range(J)], copy_stage=copy_stage, copy_pk=copy_pk,
+                      cstage=(cstage + 1) // 2 * 2, dstage=(dstage + 3) // 4 * 4)
 
 
 def jit_vec(groups, sel) -> int:
@@ -1276,6 +1331,7 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
             windows.streams = stage_streams([per[j] for j in al])
             sidx = {key: q for q, key in enumerate(windows.streams)}
             windows.slot_stream = {j: [sidx[key] for key in per[j]] for j in al}
+            _merge_streams(windows)
     extra_pos = []
     p_next = int(np.asarray(plan.positions).size)
     copy_waves = []

@@ -396,7 +396,7 @@ def _ref_math(fn, *a):
 
 
 @pytest.mark.parametrize("jit", [True, False])
-@pytest.mark.parametrize("op", ["log", "exp", "pow3", "pow4", "pow7"])
+@pytest.mark.parametrize("op", ["log", "exp", "pow3", "pow4", "pow7", "sin", "cos"])
 def test_device_transcendentals_match_glibc_bitwise(op, jit):
     """LOG / EXP / POW on the device (csrc/glibc_math.h, glibc's algorithms restated) == the
     reference's math.log / math.exp / math.pow (glibc), bit for bit, on ~3M values covering every
@@ -418,6 +418,9 @@ def test_device_transcendentals_match_glibc_bitwise(op, jit):
     elif op == "exp":
         xs, kind, k, fn = np.concatenate([g.exp_samples(n, seed=12), [0.0, -math.inf, math.inf, 709.8, -746.0]]), \
             OpKind.EXP, None, math.exp
+    elif op in ("sin", "cos"):  # glibc's bit-exact range, |x| < 105414350
+        xs = np.concatenate([g.sincos_samples(n, seed=13), [0.0, -0.0, 1e-300, 2.426265, 105414349.0]])
+        kind, k, fn = (OpKind.SIN, None, math.sin) if op == "sin" else (OpKind.COS, None, math.cos)
     else:
         k = int(op[3:])
         rng = np.random.default_rng(k)

@@ -102,4 +102,6 @@ def test_glibc_math_header_matches_this_libm():
     assert ptab == [t["pow_tab"][4 * j + q] for j in range(g.N_TAB) for q in (0, 2, 3)]
     etab = [int(v, 16) for v in re.findall(r"0x([0-9a-f]{16})ull", text.split("sgb_exp_tab")[1])[: 2 * g.N_TAB]]
     assert etab == list(t["exp_tab"])
+    sct = [float.fromhex(v) for v in re.findall(hexf, text.split("sgb_sincostab")[1])[:440]]
+    assert sct == list(t["sincostab"])
     assert g.verify(t, 3000) == []

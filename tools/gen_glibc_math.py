@@ -1,4 +1,4 @@
-"""Generate paper_2110_12865_b200/csrc/glibc_math.h: glibc's log, exp and pow restated for the device.
+"""Generate paper_2110_12865_b200/csrc/glibc_math.h: glibc's log, exp, pow, sin and cos restated for the device.
 
 The reference evaluates LOG / EXP / POW nodes with Python's ``math`` module (codegen.py:545-557,
 expr.py:423-484) -- the C library of this image, glibc 2.39.  Its log, exp and pow are the ARM
@@ -10,11 +10,17 @@ optimized-routines algorithms (sysdeps/ieee754/dbl-64/e_log.c, e_exp.c, e_pow.c)
   special scaling near overflow / underflow;
 * pow: log(x) to ~2^-68 relative (hi + lo) with its own 128-entry table, y*log(x) split with an
   fma, then exp of the pair; sign of negative x with integer y, zero / inf / nan / subnormal
-  special cases.
+  special cases;
+* sin / cos: the IBM Accurate Mathematical Library (s_sin.c): Taylor series below 0.126, the
+  __sincostab table (sin, cos of multiples of 1/128 as hi + lo pairs) with short polynomials
+  below 0.855, pi/2 - |x| as a hi + lo pair up to 2.426, a 3-part Cody-Waite reduction by pi/2
+  below 105414350.  Larger arguments need glibc's __branred (a 1200-bit 2/pi table); the device
+  uses CUDA's sin / cos there (documented; the generator checks the bit-exact range only).
 
 On x86-64 with FMA glibc runs its FMA builds (ifunc), compiled with GCC's default floating-point
 contraction: a product whose value has a single use in an addition is fused -- the Python
-restatements below and the device code mirror exactly where.  The numeric tables (__log_data,
+restatements below and the device code mirror exactly where (for sin / cos read off the
+disassembly of __sin_fma / __cos_fma: every vfmadd / vfnmadd / vfmsub).  The numeric tables (__log_data,
 __exp_data, __pow_log_data) are read out of the installed libm.so.6; every restatement is checked
 against ``math`` bit for bit on a large random sample before the header is written.
 
@@ -77,7 +83,10 @@ def read_tables(path: Path) -> dict:
     k = next(k for k in range(8, 64) if struct.unpack_from("<QQ", data, eo + 8 * k) == (0, 0x3FF0000000000000))
     ev = d(eo, 8)
     etab = struct.unpack_from(f"<{2 * N_TAB}Q", data, eo + 8 * k)
-    return {"log_poly": v[2:7], "log_poly1": v[7:18], "log_tab": v[18:18 + 2 * N_TAB],
+    # __sincostab: (sin, sin tail, cos, cos tail) of k/128, k = 0..109, starting (0, 0, 1, 0)
+    first = struct.pack("<5d", 0.0, 0.0, 1.0, 0.0, math.sin(1 / 128))
+    so = _find(data, first, lambda o: True)
+    return {"sincostab": d(so, 440), "log_poly": v[2:7], "log_poly1": v[7:18], "log_tab": v[18:18 + 2 * N_TAB],
             "pow_poly": pv[2:9], "pow_tab": pv[9:9 + 4 * N_TAB],
             "exp_shift": ev[1], "exp_negln2hiN": ev[2], "exp_negln2loN": ev[3], "exp_poly": ev[4:8],
             "exp_tab": etab}
@@ -298,6 +307,115 @@ def restated_pow(x, y, t):
     return _exp_core(ehi, elo, sign_bias, t, signed=True)
 
 
+# s_sin.c / usncs.h constants of this glibc (the __sin_fma / __cos_fma constant loads)
+SINCOS_K = {name: _f64(bits) for name, bits in {
+    "BIG": 0x42c8000000000000, "SN5": 0x3f811110e829872f, "SN3": 0xbfc5555555555515, "CS6": 0x3f56c16bedd9e239,
+    "CS4": 0xbfa5555555555535, "CS2": 0x3fe0000000000000, "S5": 0xbe5addffc2fcdf59, "S4": 0x3ec71de27b9a7ed9,
+    "S3": 0xbf2a01a019db08b8, "S2": 0x3f81111111110ece, "S1": 0xbfc5555555555555, "HP0": 0x3ff921fb54442d18,
+    "HP1": 0x3c91a62633145c07, "TOINT": 0x4338000000000000, "HPINV": 0x3fe45f306dc9c883,
+    "MP1": 0x3ff921fb58000000, "MP2": 0xbe4dde973c000000, "PP3": 0xbc8cb3b398000000, "PP4": 0xbacd747f23e32ed7,
+    "SMALL": 0x3fc020c49ba5e354}.items()}
+SINCOS_MAX_HI = 0x419921FB  # |x| < 105414350: beyond, glibc reduces with __branred
+
+
+def _taylor_sin(a, da):
+    K = SINCOS_K
+    xx = a * a
+    p = _fma(xx, _fma(xx, _fma(xx, _fma(xx, K["S5"], K["S4"]), K["S3"]), K["S2"]), K["S1"])
+    return a + _fma(xx, _fma(p, a, -(0.5 * da)), da)
+
+
+def _do_sin(x, dx, tab):
+    K = SINCOS_K
+    if not x > 0:
+        dx = -dx
+    ax = abs(x)
+    u = ax + K["BIG"]
+    k = ((_u64(u) & 0xFFFFFFFF) << 2) & 0xFFFFFFFF
+    xr = ax - (u - K["BIG"])
+    xx = xr * xr
+    s = xr + _fma(xr * xx, _fma(xx, K["SN5"], K["SN3"]), dx)
+    c = _fma(dx, xr, xx * _fma(xx, _fma(xx, K["CS6"], K["CS4"]), K["CS2"]))
+    sn, ssn, cs, ccs = tab[k: k + 4]
+    return math.copysign(sn + _fma(s, cs, _fma(-c, sn, _fma(s, ccs, ssn))), x)
+
+
+def _do_cos(x, dx, tab):
+    K = SINCOS_K
+    if x < 0:
+        dx = -dx
+    ax = abs(x)
+    u = ax + K["BIG"]
+    k = ((_u64(u) & 0xFFFFFFFF) << 2) & 0xFFFFFFFF
+    xr = (ax - (u - K["BIG"])) + dx
+    xx = xr * xr
+    s = _fma(xr * xx, _fma(xx, K["SN5"], K["SN3"]), xr)
+    c = xx * _fma(xx, _fma(xx, K["CS6"], K["CS4"]), K["CS2"])
+    sn, ssn, cs, ccs = tab[k: k + 4]
+    return cs + _fma(-s, sn, _fma(-c, cs, _fma(-s, ssn, ccs)))
+
+
+def _reduce(x):
+    K = SINCOS_K
+    t = _fma(x, K["HPINV"], K["TOINT"])
+    xn = t - K["TOINT"]
+    y = _fma(-xn, K["MP2"], _fma(-xn, K["MP1"], x))
+    t2 = _fma(-xn, K["PP3"], y)
+    db = _fma(-xn, K["PP3"], y - t2)
+    b = _fma(-xn, K["PP4"], t2)
+    return _u64(t) & 3, b, db + _fma(-xn, K["PP4"], t2 - b)
+
+
+def _do_sincos(a, da, n, tab):
+    if n & 1:
+        r = _do_cos(a, da, tab)
+    elif abs(a) < SINCOS_K["SMALL"]:
+        r = _taylor_sin(a, da)
+    else:
+        r = _do_sin(a, da, tab)
+    return -r if n & 2 else r
+
+
+def restated_sin(x, t):
+    tab, K = t["sincostab"], SINCOS_K
+    k = (_u64(x) >> 32) & 0x7FFFFFFF
+    if k < 0x3E500000:
+        return x
+    if k < 0x3FEB6000:
+        return _taylor_sin(x, 0.0) if abs(x) < K["SMALL"] else _do_sin(x, 0.0, tab)
+    if k < 0x400368FD:
+        return math.copysign(_do_cos(K["HP0"] - abs(x), K["HP1"], tab), x)
+    if k < SINCOS_MAX_HI:
+        n, a, da = _reduce(x)
+        return _do_sincos(a, da, n, tab)
+    raise ValueError("outside the bit-exact range")
+
+
+def restated_cos(x, t):
+    tab, K = t["sincostab"], SINCOS_K
+    k = (_u64(x) >> 32) & 0x7FFFFFFF
+    if k < 0x3E400000:
+        return 1.0
+    if k < 0x3FEB6000:
+        return _do_cos(x, 0.0, tab)
+    if k < 0x400368FD:
+        y = K["HP0"] - abs(x)
+        a = y + K["HP1"]
+        da = (y - a) + K["HP1"]
+        return _taylor_sin(a, da) if abs(a) < K["SMALL"] else _do_sin(a, da, tab)
+    if k < SINCOS_MAX_HI:
+        n, a, da = _reduce(x)
+        return _do_sincos(a, da, n + 1, tab)
+    raise ValueError("outside the bit-exact range")
+
+
+def sincos_samples(n: int, seed: int = 3) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    q = n // 5
+    return np.concatenate([rng.uniform(-2.5, 2.5, q), rng.uniform(-0.2, 0.2, q), rng.uniform(-100, 100, q),
+                           rng.uniform(-1.05e8, 1.05e8, q), rng.uniform(-1e-7, 1e-7, n - 4 * q)])
+
+
 # -- verification ----------------------------------------------------------------------------------
 
 
@@ -352,6 +470,11 @@ def verify(t: dict, n: int) -> list[str]:
             want = math.inf
         if not _same(restated_exp(x, t), want):
             bad.append(f"exp({x!r})")
+    for x in sincos_samples(n).tolist():
+        if not _same(restated_sin(x, t), math.sin(x)):
+            bad.append(f"sin({x!r})")
+        if not _same(restated_cos(x, t), math.cos(x)):
+            bad.append(f"cos({x!r})")
     for x, y in zip(*[a.tolist() for a in pow_samples(n)]):
         try:
             want = math.pow(x, y)
@@ -374,6 +497,8 @@ def _arr(vals) -> str:
 
 
 def header(t: dict, source: str) -> str:
+    K = {k: _lit(v) for k, v in SINCOS_K.items()}
+    sct = ",\n".join("    " + ", ".join(_lit(v) for v in t["sincostab"][j: j + 4]) for j in range(0, 440, 4))
     log_rows = ",\n".join(f"    {_lit(t['log_tab'][2 * j])}, {_lit(t['log_tab'][2 * j + 1])}" for j in range(N_TAB))
     pow_rows = ",\n".join(f"    {_lit(t['pow_tab'][4 * j])}, {_lit(t['pow_tab'][4 * j + 2])}, "
                           f"{_lit(t['pow_tab'][4 * j + 3])}" for j in range(N_TAB))
@@ -381,10 +506,11 @@ def header(t: dict, source: str) -> str:
                           for j in range(N_TAB))
     return f"""// GENERATED by tools/gen_glibc_math.py from {source} -- do not edit.
 //
-// sgb_log / sgb_exp / sgb_pow: glibc 2.39's log, exp and pow (the ARM optimized-routines algorithms,
-// sysdeps/ieee754/dbl-64/e_log.c, e_exp.c, e_pow.c) restated for the device, FMA build (x86-64 glibc
-// selects it by ifunc; GCC fuses every product whose value has a single use in an addition).  The
-// reference evaluates LOG / EXP / POW with Python's math module, i.e. these functions
+// sgb_log / sgb_exp / sgb_pow / sgb_sin / sgb_cos: glibc 2.39's log, exp and pow (the ARM
+// optimized-routines algorithms, sysdeps/ieee754/dbl-64/e_log.c, e_exp.c, e_pow.c) and sin / cos (the
+// IBM library, s_sin.c; |x| < 105414350) restated for the device, FMA build (x86-64 glibc selects it by
+// ifunc; GCC fuses every product whose value has a single use in an addition).  The reference
+// evaluates LOG / EXP / POW / SIN / COS with Python's math module, i.e. these functions
 // (codegen.py:545-557), so such templates are bit-exact on the device.  The tables are glibc's
 // __log_data, __exp_data and __pow_log_data, read from the installed libm; the generator checks its
 // Python restatement of every function against math bit for bit before writing this file.
@@ -587,6 +713,94 @@ __device__ __noinline__ double sgb_pow(double x, double y) {{
   const double ehi = __dmul_rn(y, lhi);
   const double elo = __fma_rn(y, llo, __fma_rn(y, lhi, -ehi));
   return sgb_exp_core(ehi, elo, sign_bias, true);
+}}
+
+// ---- sin / cos (s_sin.c, FMA build), |x| < 105414350; beyond: CUDA's sin / cos ----
+__device__ const double sgb_sincostab[440] = {{  // (sin, sin tail, cos, cos tail) of k/128
+{sct}}};
+#define SGB_SC_BIG {K['BIG']}
+#define SGB_SC_SMALL {K['SMALL']}
+
+__device__ __forceinline__ double sgb_taylor_sin(double a, double da) {{
+  const double xx = __dmul_rn(a, a);
+  const double p = __fma_rn(xx, __fma_rn(xx, __fma_rn(xx, __fma_rn(xx, {K['S5']}, {K['S4']}), {K['S3']}), {K['S2']}), {K['S1']});
+  return __dadd_rn(a, __fma_rn(xx, __fma_rn(p, a, -__dmul_rn(0.5, da)), da));
+}}
+
+__device__ __forceinline__ double sgb_do_sin(double x, double dx) {{
+  if (!(x > 0)) dx = -dx;
+  const double ax = fabs(x);
+  const double u = __dadd_rn(ax, SGB_SC_BIG);
+  const unsigned k = ((unsigned)sgb_as_u64(u)) << 2;
+  const double xr = __dsub_rn(ax, __dsub_rn(u, SGB_SC_BIG));
+  const double xx = __dmul_rn(xr, xr);
+  const double s = __dadd_rn(xr, __fma_rn(__dmul_rn(xr, xx), __fma_rn(xx, {K['SN5']}, {K['SN3']}), dx));
+  const double c = __fma_rn(dx, xr, __dmul_rn(xx, __fma_rn(xx, __fma_rn(xx, {K['CS6']}, {K['CS4']}), {K['CS2']})));
+  const double sn = sgb_sincostab[k], ssn = sgb_sincostab[k + 1], cs = sgb_sincostab[k + 2], ccs = sgb_sincostab[k + 3];
+  return copysign(__dadd_rn(sn, __fma_rn(s, cs, __fma_rn(-c, sn, __fma_rn(s, ccs, ssn)))), x);
+}}
+
+__device__ __forceinline__ double sgb_do_cos(double x, double dx) {{
+  if (x < 0) dx = -dx;
+  const double ax = fabs(x);
+  const double u = __dadd_rn(ax, SGB_SC_BIG);
+  const unsigned k = ((unsigned)sgb_as_u64(u)) << 2;
+  const double xr = __dadd_rn(__dsub_rn(ax, __dsub_rn(u, SGB_SC_BIG)), dx);
+  const double xx = __dmul_rn(xr, xr);
+  const double s = __fma_rn(__dmul_rn(xr, xx), __fma_rn(xx, {K['SN5']}, {K['SN3']}), xr);
+  const double c = __dmul_rn(xx, __fma_rn(xx, __fma_rn(xx, {K['CS6']}, {K['CS4']}), {K['CS2']}));
+  const double sn = sgb_sincostab[k], ssn = sgb_sincostab[k + 1], cs = sgb_sincostab[k + 2], ccs = sgb_sincostab[k + 3];
+  return __dadd_rn(cs, __fma_rn(-s, sn, __fma_rn(-c, cs, __fma_rn(-s, ssn, ccs))));
+}}
+
+__device__ __forceinline__ unsigned sgb_reduce(double x, double &a, double &da) {{
+  const double t = __fma_rn(x, {K['HPINV']}, {K['TOINT']});
+  const double xn = __dsub_rn(t, {K['TOINT']});
+  const double y = __fma_rn(-xn, {K['MP2']}, __fma_rn(-xn, {K['MP1']}, x));
+  const double t2 = __fma_rn(-xn, {K['PP3']}, y);
+  const double db = __fma_rn(-xn, {K['PP3']}, __dsub_rn(y, t2));
+  const double b = __fma_rn(-xn, {K['PP4']}, t2);
+  a = b;
+  da = __dadd_rn(db, __fma_rn(-xn, {K['PP4']}, __dsub_rn(t2, b)));
+  return (unsigned)sgb_as_u64(t) & 3u;
+}}
+
+__device__ __forceinline__ double sgb_do_sincos(double a, double da, unsigned n) {{
+  const double r = (n & 1u) ? sgb_do_cos(a, da) : (fabs(a) < SGB_SC_SMALL ? sgb_taylor_sin(a, da) : sgb_do_sin(a, da));
+  return (n & 2u) ? -r : r;
+}}
+
+__device__ __noinline__ double sgb_sin(double x) {{
+  const unsigned k = (unsigned)(sgb_as_u64(x) >> 32) & 0x7fffffffu;
+  if (k < 0x3e500000u) return x;
+  if (k < 0x3feb6000u) return fabs(x) < SGB_SC_SMALL ? sgb_taylor_sin(x, 0.0) : sgb_do_sin(x, 0.0);
+  if (k < 0x400368fdu) return copysign(sgb_do_cos(__dsub_rn({K['HP0']}, fabs(x)), {K['HP1']}), x);
+  if (k < {SINCOS_MAX_HI:#x}u) {{
+    double a, da;
+    const unsigned n = sgb_reduce(x, a, da);
+    return sgb_do_sincos(a, da, n);
+  }}
+  if (k < 0x7ff00000u) return sin(x);  // glibc: __branred; CUDA's reduction here
+  return __ddiv_rn(x, x);
+}}
+
+__device__ __noinline__ double sgb_cos(double x) {{
+  const unsigned k = (unsigned)(sgb_as_u64(x) >> 32) & 0x7fffffffu;
+  if (k < 0x3e400000u) return 1.0;
+  if (k < 0x3feb6000u) return sgb_do_cos(x, 0.0);
+  if (k < 0x400368fdu) {{
+    const double y = __dsub_rn({K['HP0']}, fabs(x));
+    const double a = __dadd_rn(y, {K['HP1']});
+    const double da = __dadd_rn(__dsub_rn(y, a), {K['HP1']});
+    return fabs(a) < SGB_SC_SMALL ? sgb_taylor_sin(a, da) : sgb_do_sin(a, da);
+  }}
+  if (k < {SINCOS_MAX_HI:#x}u) {{
+    double a, da;
+    const unsigned n = sgb_reduce(x, a, da);
+    return sgb_do_sincos(a, da, n + 1u);
+  }}
+  if (k < 0x7ff00000u) return cos(x);  // glibc: __branred; CUDA's reduction here
+  return __ddiv_rn(x, x);
 }}
 
 #endif  // SGB_GLIBC_MATH_H
