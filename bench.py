@@ -414,17 +414,17 @@ def measure_eval(cfg: str, args, rank: int, world: int, barrier, split=None) -> 
     cfgd = config_dict(cfg, args, plan)
     split_info = None
     lo, hi = 0, n_total
-    if split is not None:  # one evaluation, CSR outputs split: this rank computes its slice's producer cone
-        from paper_2110_12865_b200.shard import shard_bounds, shard_device_plan
+    if split is not None:  # one evaluation, CSR outputs split: this rank's own plan shard (its producer cone)
+        from paper_2110_12865_b200.shard import shard_outputs, shard_plan
 
         s_world, s_rank = split
-        lw_full = lower_plan(plan, relayout=False)
-        lo, hi = shard_bounds(lw_full, n_total, s_world, s_rank)
-        view, lw_s = shard_device_plan(plan, lw_full, lo, hi)
-        split_info = {"world": s_world, "rank": s_rank, "outputs": [lo, hi], "tiles_kept": int(len(lw_s.tiles)),
-                      "tiles_full": int(len(lw_full.tiles))}
-        dp = DevicePlan(view, device=local, lowered=lw_s)
-        plan = view
+        lo, hi = shard_outputs(n_total, s_world, s_rank)
+        plan = shard_plan(full_plan, lo, hi)
+        split_info = {"world": s_world, "rank": s_rank, "outputs": [lo, hi],
+                      "index_entries_kept": int(plan.positions.size),
+                      "index_entries_full": int(np.asarray(full_plan.positions).size),
+                      "kernels_kept": len(plan.kernels)}
+        dp = DevicePlan(plan, device=local, csr_layout=True)
         inputs = workload_inputs(cfg, args, seed=0, plan=full_plan)
     else:
         inputs = workload_inputs(cfg, args, seed=rank, plan=plan)
@@ -525,25 +525,20 @@ def measure_eval(cfg: str, args, rank: int, world: int, barrier, split=None) -> 
         return {}
 
     direct = bool(np.any(dp.lowered.groups["flags"] & (384 | 4096)))
-    traffic = csr_wave_traffic(full_plan, dp.lowered) if direct else wave_traffic(full_plan, dp.lowered)
+    traffic = csr_wave_traffic(plan, dp.lowered) if direct else wave_traffic(plan, dp.lowered)
     traffic = traffic[:n_w]
-    if split_info:  # full-plan bytes scaled by this shard's share of the outputs (approximate)
-        f = (hi - lo) / max(n_total, 1)
-        traffic = [dataclasses.replace(t, index_bytes=int(t.index_bytes * f), const_bytes=int(t.const_bytes * f),
-                                       read_bytes=int(t.read_bytes * f), write_bytes=int(t.write_bytes * f))
-                   for t in traffic]
     dom = int(np.argmax(per_launch))
     peak, peak_src = peak_gbs()
     achieved = traffic[dom].bytes / (per_launch[dom] * 1e-3) / 1e9
-    balg = plan_balg(full_plan) * ((hi - lo) / n_total if split_info else 1)
+    balg = plan_balg(plan)
     whole = balg / (ms * 1e-3) / 1e9
     cpu = None
     if world == 1 and not split_info and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, args, full_plan, key, inputs, gpu_out=out.cpu().numpy())
     if split_info:
-        par = (f"one evaluation, CSR outputs split {split_info['world']} ways (shard.shard_device_plan): rank 0 "
-               f"computes outputs {split_info['outputs']} from its producer cone ({split_info['tiles_kept']} of "
-               f"{split_info['tiles_full']} tiles); no collective in the step")
+        par = (f"one evaluation, CSR outputs split {split_info['world']} ways (shard.shard_plan): each rank holds its "
+               f"own plan shard -- rank 0 outputs {split_info['outputs']}, {split_info['index_entries_kept']} of "
+               f"{split_info['index_entries_full']} index entries; no collective in the step")
     else:
         par = "single GPU" if world == 1 else f"replicas x{world}: one full evaluation per GPU per step"
     cfgd.update({
@@ -728,18 +723,17 @@ def measure_emulated(args, rank: int, world: int, barrier) -> dict:
     import device_plan_emu as emu
 
     from paper_2110_12865_b200 import lower_plan
-    from paper_2110_12865_b200.shard import max_over_ranks, shard_bounds, shard_device_plan
+    from paper_2110_12865_b200.shard import max_over_ranks, shard_outputs, shard_plan
 
     cfg = args.config
     key, plan = build_workload(cfg, args, rank, barrier)
     n_total = len(plan.outputs)
-    lw = lower_plan(plan, jit_compile=False, csr_window=True)
-    lo, hi = shard_bounds(lw, n_total, world, rank)
-    _, slw = shard_device_plan(plan, lw, lo, hi)
+    lo, hi = shard_outputs(n_total, world, rank)
+    slw = lower_plan(shard_plan(plan, lo, hi), jit_compile=False, csr_window=True)
     inputs = workload_inputs(cfg, args, seed=0, plan=plan)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        mine = emu.run_csr(slw, inputs, by_tiles=True)
+        mine = emu.run_csr(slw, inputs)
     sec = max_over_ranks((time.perf_counter() - t0) / args.steps)
     width = torch.tensor([hi - lo])
     dist.all_reduce(width, op=dist.ReduceOp.MAX)
@@ -747,7 +741,7 @@ def measure_emulated(args, rank: int, world: int, barrier) -> dict:
     send[: hi - lo] = torch.from_numpy(mine)
     parts = [torch.empty_like(send) for _ in range(world)]
     dist.all_gather(parts, send)
-    bounds = [shard_bounds(lw, n_total, world, r) for r in range(world)]
+    bounds = [shard_outputs(n_total, world, r) for r in range(world)]
     full = torch.cat([parts[r][: b - a] for r, (a, b) in enumerate(bounds)]).numpy()
     if rank != 0:
         return {}
@@ -759,8 +753,8 @@ def measure_emulated(args, rank: int, world: int, barrier) -> dict:
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "emulated": True,
             "config": dict(config_dict(cfg, args, plan), parity="bitwise" if ok else "MISMATCH",
                            shards=[list(b) for b in bounds],
-                           parallelism=f"CPU emulation, gloo x{world}: one evaluation, CSR outputs split at window "
-                                       "boundaries, slices all-gathered and compared with the oracle")}
+                           parallelism=f"CPU emulation, gloo x{world}: one evaluation, each rank its own plan shard "
+                                       "(shard.shard_plan), slices all-gathered and compared with the oracle")}
 
 
 def compact(line: dict) -> dict:

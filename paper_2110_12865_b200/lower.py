@@ -819,7 +819,8 @@ class CsrWindows:
     @property
     def stage_doubles(self) -> int:
         """Shared memory in front of the window buffer: ranges, copy span, copy descriptors (u32 pairs)."""
-        return self.range_doubles + self.cstage + (self.dstage + 1) // 2
+        n = self.range_doubles + self.cstage + (self.dstage + 1) // 2
+        return n + (n & 1)  # the window buffer after it stays 16-byte aligned (double2 write-out)
 
 
 # row-window heights tried, largest first (one 256-thread block: 2 halves); SGB_STAGE_ROWS=0 turns the

@@ -201,3 +201,57 @@ def shard_device_plan(plan, lowered, lo: int, hi: int):
 
 
 UNIT_TB, UNIT_TE = 5, 6  # lower.UNIT_FIELDS tile_begin / tile_end
+
+
+def shard_plan(plan, lo: int, hi: int):
+    """The plan shard of the CSR outputs [lo, hi): an ExecutionPlan of its own (codegen.py:88-98
+    fields), every kernel cut to the instance range its outputs' producer cone needs.
+
+    A kernel outside the cone is dropped; a single-root kernel keeps instances [a, b) -- the first
+    to the last needed -- with ``dest_base + a``, so its results stay at the full plan's addresses
+    (``dest_base + i``, codegen.py:265) and its position / constant columns are sliced to [a, b);
+    multi-root and self-referencing kernels are kept whole (their result stride is N).  Value-array
+    addresses are unchanged, so the shard lowers and runs like any plan and its CSR values equal
+    the full evaluation's [lo, hi) bit for bit -- while the rank uploads only its share of the
+    index tables ("each GPU holds its own plan shard").
+    """
+    import dataclasses
+
+    import numpy as np
+
+    from .plan import ExecutionPlan
+
+    masks = output_cone(plan, lo, hi)
+    positions = np.asarray(plan.positions)
+    constants = np.asarray(plan.constants)
+    kernels, pos, con = [], [], []
+    p_next = c_next = 0
+    for k, kp in enumerate(plan.kernels):
+        m = masks[k]
+        n = kp.instances
+        if n == 0 or not m.any():
+            continue
+        need = np.flatnonzero(m)
+        a, b = int(need[0]), int(need[-1]) + 1
+        if kp.n_roots != 1 or kp.self_referencing:
+            a, b = 0, n
+        r, c = len(kp.retained), len(kp.const_vars)
+        seg = positions[kp.p_base: kp.p_base + r * n]
+        cols = seg.reshape(r, n) if kp.layout == "coalesced" else seg.reshape(n, r).T
+        cseg = constants[kp.c_base: kp.c_base + c * n]
+        ccols = cseg.reshape(c, n) if kp.layout == "coalesced" else cseg.reshape(n, c).T
+        cut = cols[:, a:b]
+        ccut = ccols[:, a:b]
+        pos.append((cut if kp.layout == "coalesced" else cut.T).reshape(-1))
+        con.append((ccut if kp.layout == "coalesced" else ccut.T).reshape(-1))
+        kernels.append(dataclasses.replace(kp, instances=b - a, dest_base=kp.dest_base + a, p_base=p_next,
+                                           c_base=c_next))
+        p_next += cut.size
+        c_next += ccut.size
+    return ExecutionPlan(
+        value_array_size=int(plan.value_array_size), input_count=int(plan.input_count),
+        vector_width=int(plan.vector_width), outputs=np.asarray(plan.outputs, np.int64)[lo:hi],
+        kernels=kernels,
+        positions=np.concatenate(pos).astype(np.uint32) if pos else np.zeros(0, np.uint32),
+        constants=np.concatenate(con).astype(np.float64) if con else np.zeros(0, np.float64),
+        metadata=dict(getattr(plan, "metadata", {}) or {}, shard=[int(lo), int(hi)]))

@@ -17,7 +17,7 @@ import numpy as np
 import pytest
 
 from conftest import bits, device_plan, golden_case, lowered
-from gpu_cases import JIT_CASES, LAYOUT_CASES, WINDOW_CASES
+from gpu_cases import BUILDER_CASES, JIT_CASES, LAYOUT_CASES, WINDOW_CASES, builder_plan
 
 pytestmark = pytest.mark.gpu
 
@@ -53,6 +53,34 @@ def test_compile_plan_values(golden):
     # the native library that ran is the in-tree one
     assert run.library_path.name == "libsgb.so"
     assert np.array_equal(bits(run.outputs(golden.inputs)), bits(x[np.asarray(golden.plan.outputs, np.int64)]))
+
+
+@pytest.mark.parametrize("name", sorted(BUILDER_CASES))
+@pytest.mark.parametrize("relayout", [False, "auto"])
+def test_builder_plans_default_lowering(name, relayout):
+    """The config builders' plans at small sizes through the default lowering (CSR windows with staged
+    operand streams and copies on the mesh plans, the CSR layout on the FEM plan): run_csr, the captured
+    graph and the host path == the oracle, bit for bit."""
+    import torch
+
+    from oracle import oracle
+    from paper_2110_12865_b200 import DevicePlan, lower_plan
+
+    plan, inputs = builder_plan(name)
+    dp = DevicePlan(plan, lowered=lower_plan(plan, relayout=relayout))
+    want = oracle.run_outputs(plan, inputs)
+    x = dp.new_values(inputs)
+    out = dp.run_csr(x)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(out.cpu().numpy()), bits(want))
+    assert np.array_equal(bits(dp.run_outputs_host(inputs)), bits(want))
+    graph = dp.capture_csr(dp.new_values(inputs), out)
+    out.fill_(float("nan"))
+    graph.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(out.cpu().numpy()), bits(want))
+    if name.startswith("lmlt"):
+        assert dp.lowered.windows is not None and dp.lowered.windows.rows > 0  # staged windows ran
 
 
 @pytest.mark.parametrize("name", LAYOUT_CASES)
