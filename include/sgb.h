@@ -125,11 +125,6 @@ typedef struct sgb_plan_desc {
   const uint32_t *copy_src;  /* [n_copy] value-array address of each copied output */
   const uint16_t *copy_pos;  /* [n_copy] its position in its window */
   int64_t n_copy;
-  int64_t win_stage;         /* doubles of shared memory staged in front of the window buffer */
-  const uint32_t *win_cstg;  /* [n_windows][2]: staged copies -- first source, span (0: gathered) */
-  const uint32_t *copy_pk;   /* [n_copy] staged copies: (source - first source) << 16 | window position */
-  int64_t win_cstage;        /* largest staged span (doubles) the window kernel holds */
-  int64_t win_dstage;        /* most staged copies per window the window kernel holds */
 } sgb_plan_desc;
 
 /* Upload a device plan to `device`.  Replaces compile_plan (emit.py:198-245). */

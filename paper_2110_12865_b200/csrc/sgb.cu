@@ -803,9 +803,8 @@ struct sgb_plan {
   cudaLibrary_t jit_lib = nullptr;
   int2 *d_wpieces = nullptr;  // CSR windows: [n_win][J] first instance, count
   int64_t *d_wk = nullptr, *d_wcopy = nullptr;
-  uint32_t *d_csrc = nullptr, *d_cpk = nullptr;
+  uint32_t *d_csrc = nullptr;
   uint16_t *d_cpos = nullptr;
-  uint2 *d_cstg = nullptr;
   uint32_t *d_fbase = nullptr;
   // workspace for the host-buffer entry points
   std::mutex ws_mu;
@@ -864,13 +863,12 @@ void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_
   if (u.flags & UNIT_WINDOW) {  // CSR windows (jit.py window_source): one block per window
     const int2 *pieces = p->d_wpieces;
     const int64_t *wk = p->d_wk, *wc = p->d_wcopy;
-    const uint32_t *csrc = p->d_csrc, *cpk = p->d_cpk;
+    const uint32_t *csrc = p->d_csrc;
     const uint16_t *cpos = p->d_cpos;
-    const uint2 *cstg = p->d_cstg;
     int64_t n = u.t1 - u.t0;
     Tables T = p->T;
     const double *xc = x;
-    void *args[] = {&T, &pieces, &wk, &wc, &csrc, &cpos, &cstg, &cpk, &n, &xc, &out};
+    void *args[] = {&T, &pieces, &wk, &wc, &csrc, &cpos, &n, &xc, &out};
     cudaLaunchKernel(u.jit, dim3((unsigned)u.grid), dim3(JIT_BLOCK), args, (size_t)u.regs, s);
     return;
   }
@@ -982,7 +980,7 @@ void sgb_plan_destroy(sgb_plan *p) {
   void *bufs[] = {p->d_groups, p->d_tiles, p->d_btiles, p->d_outputs, p->d_tape, p->d_imm, p->d_con,
                   p->d_sop, p->d_scol, p->d_sdel, p->d_pos, p->d_x, p->d_out, p->d_cbase, p->d_coff,
                   p->d_obase, p->d_ooff, p->d_opos32, p->d_sopd, p->d_fbase, p->d_outputs32,
-                  p->d_wpieces, p->d_wk, p->d_wcopy, p->d_csrc, p->d_cpos, p->d_cpk, p->d_cstg, p->d_x2, p->d_out2};
+                  p->d_wpieces, p->d_wk, p->d_wcopy, p->d_csrc, p->d_cpos, p->d_x2, p->d_out2};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (p->ws_stream) cudaStreamDestroy(p->ws_stream);
@@ -1141,11 +1139,7 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       SGB_CUDA(cudaLibraryGetKernel(&kw, p->jit_lib, nw.c_str()));
       u.jit = (const void *)kw;
       if (u.regs > 48 * 1024) SGB_CUDA(cudaFuncSetAttribute(u.jit, cudaFuncAttributeMaxDynamicSharedMemorySize, u.regs));
-      if (!d->win_cstg || (d->n_copy && !d->copy_pk) || d->win_cstage < 0 || d->win_dstage < 0)
-        return fail(-1, "sgb_plan_create: CSR-window copy staging tables missing");
-      if (d->win_stage < 0 || 8 * (d->win_stage + 2) > (int64_t)u.regs)
-        return fail(-1, "sgb_plan_create: CSR-window stage does not fit its shared memory");
-      const int64_t wmax = u.regs / 8 - 2 - d->win_stage;  // the window buffer (doubles) after the stage
+      const int64_t wmax = u.regs / 8 - 2;  // the window buffer (doubles), alignment slots
       if (d->win_k[0] != 0 || d->win_k[n_win] != d->n_outputs || d->win_copy[0] != 0 || d->win_copy[n_win] != d->n_copy)
         return fail(-1, "sgb_plan_create: CSR windows do not cover the outputs / copies");
       for (int g = u.g0; g < u.g1; ++g)
@@ -1158,15 +1152,6 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
         for (int64_t c = d->win_copy[w]; c < d->win_copy[w + 1]; ++c)
           if ((int64_t)d->copy_src[c] >= d->value_array_size || (int64_t)d->copy_pos[c] >= len)
             return fail(-1, "sgb_plan_create: bad CSR-window copy");
-        const uint32_t cbase = d->win_cstg[2 * w], cspan = d->win_cstg[2 * w + 1];
-        if (cspan) {  // staged copies: span and descriptors fit the kernel's regions, stay inside x and the window
-          const int64_t nc = d->win_copy[w + 1] - d->win_copy[w];
-          if ((int64_t)cspan > d->win_cstage || nc > d->win_dstage || (int64_t)cbase + cspan > d->value_array_size)
-            return fail(-1, "sgb_plan_create: staged CSR-window copies exceed their region");
-          for (int64_t c = d->win_copy[w]; c < d->win_copy[w + 1]; ++c)
-            if ((d->copy_pk[c] >> 16) >= cspan || (int64_t)(d->copy_pk[c] & 0xFFFFu) >= len)
-              return fail(-1, "sgb_plan_create: bad staged CSR-window copy");
-        }
         for (int64_t j = 0; j < J; ++j) {  // every staged position of every piece stays inside its window
           const int32_t a = d->win_pieces[2 * (w * J + j)], cnt = d->win_pieces[2 * (w * J + j) + 1];
           const sgb_group &G = d->groups[u.g0 + j];
@@ -1386,9 +1371,6 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       (rc = upload(&p->d_wpieces, reinterpret_cast<const int2 *>(d->win_pieces), d->n_win_pieces)) ||
       (rc = upload(&p->d_wk, d->win_k, d->n_win_k)) || (rc = upload(&p->d_wcopy, d->win_copy, d->n_win_copy)) ||
       (rc = upload(&p->d_csrc, d->copy_src, d->n_copy)) || (rc = upload(&p->d_cpos, d->copy_pos, d->n_copy)) ||
-      (rc = upload(&p->d_cpk, d->copy_pk, d->copy_pk ? d->n_copy : 0)) ||
-      (rc = upload(&p->d_cstg, reinterpret_cast<const uint2 *>(d->win_cstg),
-                   d->win_cstg && d->n_win_k > 0 ? d->n_win_k - 1 : 0)) ||
       (rc = upload(&p->d_fbase, fbase.data(), (int64_t)fbase.size())))
     return rc;
   p->T = Tables{p->d_groups, p->d_tape, p->d_imm, p->d_sop, p->d_scol, p->d_sdel, p->d_pos,

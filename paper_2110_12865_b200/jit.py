@@ -55,14 +55,6 @@ struct Tables {  // == csrc/sgb.cu Tables
 #define NONE 0xFFFFFFFFu
 __device__ __forceinline__ double bits(u64 b) { return __longlong_as_double((long long)b); }
 __device__ __forceinline__ void st_stream(double *a, double v) { __stcs(a, v); }
-// asynchronous global -> shared copies (LDGSTS): a staged window's operand streams, no registers held
-__device__ __forceinline__ void cp_async8(double *smem, const double *gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(smem)),
-               "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
-}
 """
 
 # glibc's sin / cos / exp / log / pow restated for the device (tools/gen_glibc_math.py): the
@@ -135,8 +127,7 @@ def _out_pos(rec, r: int, i: str = "i") -> str | None:
 
 def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: str = "",
                 batched: bool = False, window: bool = False, bv: str = "b",
-                stage: str | None = None, guard: str | None = None,
-                slot_src: list | None = None) -> tuple[list[str], list[str]]:
+                stage: str | None = None, guard: str | None = None) -> tuple[list[str], list[str]]:
     """Straight-line CUDA for instance ``iv`` of packed group ``gi`` (register tape -> SSA).
 
     Returns (load lines, compute + store lines) so several instances' loads can be
@@ -147,9 +138,7 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
     results go to the block's staging buffer at ``stage_[(stage) * RP + r]``
     (``stage`` = the instance's offset in the tile, RP = lower.stage_stride); the
     unit writes the tile out coalesced.  ``guard``: every load is predicated on it
-    (lanes without an instance issue no memory traffic).  ``slot_src``: the slots' values
-    are these expressions (a staged window's shared-memory operand streams) and the
-    window positions ``wp<r><sfx>`` are loaded by the caller.
+    (lanes without an instance issue no memory traffic).
     """
     X = (lambda a: f"x + (u64)({a}) * ld + {bv}") if batched else (lambda a: f"x + ({a})")
     G = (lambda e, z: f"({guard}) ? ({e}) : {z}") if guard else (lambda e, z: e)  # noqa: E731
@@ -162,13 +151,9 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
     reg: dict[int, str] = {}
     i = iv
     col = lambda c: _column(rec, c, i, dp)  # noqa: E731
-    if S and slot_src is None:
+    if S:
         loads.append(f"const u32 idx0{sfx} = {G(col(0), '0u')};")
     for s_ in range(S):
-        if slot_src is not None:
-            loads.append(f"const double s{s_}{sfx} = {slot_src[s_]};")
-            reg[s_] = f"s{s_}{sfx}"
-            continue
         c = int(cols[s_])
         if c < 0:
             addr = f"idx0{sfx} + {int(dels[s_]) % 2**32}u"
@@ -183,7 +168,7 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
              else f"{_off(int(rec['c_off']) + k * n)} + {i}")
         loads.append(f"const double k{k}{sfx} = {G(f'__ldcs(T.con + {e})', '0.0')};")
         reg[S + k] = f"k{k}{sfx}"
-    if window and slot_src is None:  # window positions (FLAG_WPOS16) load with the operands, not after the compute
+    if window:  # window positions (FLAG_WPOS16) load with the operands, not after the compute
         oo_off = int(rec["oo_off"])
         for r in range(int(rec["n_roots"])):
             loads.append(f"const u16 wp{r}{sfx} = "
@@ -444,31 +429,22 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
     """CSR-window kernel of unit ``u`` (lower._csr_windows): block w assembles the outputs
     [win_k[w], win_k[w+1]) in shared memory and writes them out with 16-byte streaming stores.
 
-    Work inside a window is block-uniform, so nothing diverges.  On row windows (mesh plans:
-    instance = vertex = CSR row) one round trip feeds the whole window: asynchronous copies
-    (LDGSTS, no registers held) stage every operand stream of the row-aligned members -- streams
-    of neighbouring bases merged into one range -- and, when their sources are dense, the copied
-    outputs (inputs, earlier waves' results) with their packed (source, position) descriptors;
-    the window positions of the aligned members load into registers meanwhile.  The other
-    members (mesh boundary groups) run in chunks from global memory while the stage fills --
-    every member of a chunk takes its piece (instance range) with one instance per thread, the
-    chunk's loads issued before its computes.  Then the aligned members compute from shared
-    memory, one row per thread.  Every result goes to its FLAG_WPOS16 position in the window;
-    members store nothing to the value array (the last wave: never re-read), so every output
-    crosses HBM once, coalesced.
+    Work inside a window is block-uniform, so nothing diverges: the outputs copied from the
+    value array (inputs, earlier waves' results) first, then the members in chunks -- every
+    member of a chunk takes its piece (instance range) with one instance per thread, all the
+    chunk's loads (operands and window positions) issued before its computes (WINDOW_LOADS per
+    thread) -- each result stored at its FLAG_WPOS16 position in the window.  Members store
+    nothing to the value array (the last wave: never re-read), so every output crosses HBM
+    once, coalesced.  (Staging the row-aligned members' operand streams and the copies in shared
+    memory with cp.async -- one round trip per window -- measured 14-19 % slower on C2, r2e/r2f.)
     """
     unit = dp.unit(u)
     g0, g1 = unit["group_begin"], unit["group_end"]
     J = g1 - g0
-    wn = dp.windows
-    ROWS = int(wn.rows) if wn is not None else 0
-    staged = [g0 + j for j in range(J) if ROWS and wn.aligned[j]]
     chunks, cur, width = [], [], 0
     for gi in range(g0, g1):
         rec = dp.groups[gi]
         _check_stores(tapes[gi], int(rec["n_roots"]), gi)
-        if gi in staged:
-            continue
         wdt = max(1, int(rec["n_slots"]) + int(rec["n_const"]))
         if cur and width + wdt > WINDOW_LOADS:
             chunks.append(cur)
@@ -478,22 +454,10 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
     if cur:
         chunks.append(cur)
     B = JIT_BLOCK
-    RD = wn.range_doubles if staged else 0
-    CS = wn.cstage if staged else 0  # staged copy span (doubles), then its u32 descriptors
-    DS = wn.dstage if staged else 0
-    STAGE = wn.stage_doubles if staged else 0
-    roff, o_ = [], 0
-    for _, _, n in (wn.ranges if staged else []):
-        roff.append(o_)
-        o_ += int(n)
     out = [f'extern "C" __global__ void __launch_bounds__({B}, {WINDOW_MIN_BLOCKS}) sgb_window_u{u}(',
            "    Tables T, const int2 *pieces, const i64 *win_k, const i64 *copy_off, const u32 *copy_src,",
-           "    const u16 *copy_pos, const uint2 *cstg, const u32 *copy_pk, i64 n_win, const double *x,",
-           "    double *out) {",
-           "  extern __shared__ __align__(16) double smem_[];",
-           f"  double *const stage_ = smem_;  // {RD} doubles of operand ranges, {CS} of copied sources",
-           f"  const u32 *const dsc_ = reinterpret_cast<const u32 *>(smem_ + {RD + CS});  // {DS} copy descriptors",
-           f"  double *const buf = smem_ + {STAGE};  // the window",
+           "    const u16 *copy_pos, i64 n_win, const double *x, double *out) {",
+           "  extern __shared__ __align__(16) double buf[];",
            f"  __shared__ int2 sp[{J}];",
            "  const int tid = threadIdx.x;",
            "  for (i64 w = blockIdx.x; w < n_win; w += gridDim.x) {",
@@ -504,57 +468,14 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
            "    // window position p at bw[p]: out + k0 - head_ is 16-byte aligned, so is buf",
            "    const u32 head_ = (u32)((reinterpret_cast<u64>(out + k0) >> 3) & 1ull);",
            "    double *bw = buf + head_;",
-           "    __syncthreads();"]
-    if staged:
-        ja = staged[0] - g0
-        H = B // ROWS  # thread groups of the staged compute: thread tid takes row tid % ROWS
-        out += [f"    const u32 R0 = (u32)sp[{ja}].x, nrow = (u32)sp[{ja}].y;  // the window's rows"]
-        for q, (base, stride, n) in enumerate(wn.ranges):  # range q element e = x[base + stride*(R0 + e)]
-            lim = f"{int(n) - ROWS}u + nrow" if stride == 1 else "nrow"
-            out.append(f"    for (u32 e = tid; e < {lim}; e += {B}u) "
-                       f"cp_async8(stage_ + {roff[q] + 0}u + e, x + ({base % 2**32}u + {stride % 2**32}u * (R0 + e)));")
-        out += ["    const uint2 cs_ = __ldg(cstg + w);  // staged copies: first source, span (0: gathered)",
-                "    if (cs_.y) {",
-                f"      for (u32 e = tid; e < cs_.y; e += {B}u) cp_async8(stage_ + {RD}u + e, x + (cs_.x + e));",
-                f"      for (u32 e = tid; e < (u32)(c1_ - c0_); e += {B}u)",
-                "        asm volatile(\"cp.async.ca.shared.global [%0], [%1], 4;\" :: "
-                "\"r\"((unsigned)__cvta_generic_to_shared(dsc_ + e)), \"l\"(copy_pk + c0_ + e) : \"memory\");",
-                "    }",
-                f"    const u32 rr_ = tid % {ROWS}u, hh_ = tid / {ROWS}u;",
-                "    const bool okr_ = rr_ < nrow;",
-                "    const u32 ir_ = R0 + rr_;"]
-        # members of the staged compute, balanced over the H thread groups by tape length
-        load = [0] * H
-        part = [[] for _ in range(H)]
-        for gi in sorted(staged, key=lambda g: -len(tapes[g])):
-            h = load.index(min(load))
-            part[h].append(gi)
-            load[h] += len(tapes[gi]) + 2
-        nwp = max(sum(int(dp.groups[gi]["n_roots"]) for gi in ms) for ms in part)
-        out.append(f"    u16 {', '.join(f'wq{q} = 0xFFFF' for q in range(nwp))};  // window positions of the row")
-        for h, ms in enumerate(part):  # issued now: they arrive while the stage fills
-            q = 0
-            out.append(f"    {'if' if h == 0 else 'else if'} (hh_ == {h}u && okr_) {{")
-            for gi in ms:
-                rec = dp.groups[gi]
-                for r in range(int(rec["n_roots"])):
-                    off = int(rec["oo_off"]) + r * int(rec["n"])
-                    out.append(f"      wq{q} = __ldcs(T.ooff + {_off(off)} + ir_);")
-                    q += 1
-            out.append("    }")
-    gather = [f"    for (i64 c = c0_ + tid; c < c1_; c += {B * COPY_UNROLL}) {{"]
+           "    __syncthreads();",
+           f"    for (i64 c = c0_ + tid; c < c1_; c += {B * COPY_UNROLL}) {{"]
     for q in range(COPY_UNROLL):  # named registers (no local arrays): every copy's loads in flight
-        gather.append(f"      const bool cq{q} = c + {q * B} < c1_;")
-        gather.append(f"      const u16 cp{q} = cq{q} ? __ldcs(copy_pos + c + {q * B}) : (u16)0;")
-        gather.append(f"      const double cv{q} = cq{q} ? __ldg(x + __ldcs(copy_src + c + {q * B})) : 0.0;")
-    gather += [f"      if (cq{q}) bw[cp{q}] = cv{q};" for q in range(COPY_UNROLL)]
-    gather += ["    }"]
-    if staged:
-        out.append("    if (!cs_.y) {  // copies too sparse to stage: gathered from global")
-        out += ["  " + ln for ln in gather]
-        out.append("    }")
-    else:
-        out += gather
+        out.append(f"      const bool cq{q} = c + {q * B} < c1_;")
+        out.append(f"      const u16 cp{q} = cq{q} ? __ldcs(copy_pos + c + {q * B}) : (u16)0;")
+        out.append(f"      const double cv{q} = cq{q} ? __ldg(x + __ldcs(copy_src + c + {q * B})) : 0.0;")
+    out += [f"      if (cq{q}) bw[cp{q}] = cv{q};" for q in range(COPY_UNROLL)]
+    out += ["    }"]
     for chunk in chunks:
         cmax = "0"
         for gi in chunk:
@@ -571,29 +492,6 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
             comps += cp
         out += ["      " + ln for ln in loads + comps]
         out.append("    }")
-    if staged:  # the staged members: operands from shared memory, one row per thread
-        out.append("    cp_async_wait_all();")
-        out.append("    __syncthreads();")
-        out.append("    if (cs_.y)  // the staged copies: shared to shared")
-        out.append(f"      for (u32 e = tid; e < (u32)(c1_ - c0_); e += {B}u) {{"
-                   f" const u32 pk = dsc_[e]; bw[pk & 0xFFFFu] = stage_[{RD}u + (pk >> 16)]; }}")
-        for h, ms in enumerate(part):
-            out.append(f"    {'if' if h == 0 else 'else if'} (hh_ == {h}u && okr_) {{")
-            q = 0
-            for gi in ms:
-                rec = dp.groups[gi]
-                j = gi - g0
-                src = []
-                for s_ in range(int(rec["n_slots"])):
-                    qs = wn.slot_stream[j][s_]
-                    src.append(f"stage_[{roff[wn.stream_range[qs]] + wn.stream_delta[qs]}u + rr_]")
-                sfx = f"_{j}"
-                for r in range(int(rec["n_roots"])):
-                    out.append(f"      const u16 wp{r}{sfx} = wq{q};")
-                    q += 1
-                ld, cp = group_parts(dp, gi, tapes[gi], imms[gi], iv="ir_", sfx=sfx, window=True, slot_src=src)
-                out += ["      " + ln for ln in ld + cp]
-            out.append("    }")
     out += ["    __syncthreads();",
             "    {  // 16-byte shared loads and streaming stores; the pair straddling k0 writes its second half",
             "      const u32 tot_ = len_ + head_;",

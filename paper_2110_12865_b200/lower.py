@@ -796,132 +796,11 @@ class CsrWindows:
     copy_off: np.ndarray  # int64 [n_win + 1]: copies of window w are [copy_off[w], copy_off[w+1])
     copy_src: np.ndarray  # uint32: value-array address of each copied output (CSR order)
     copy_pos: np.ndarray  # uint16: its position in its window
-    rows: int = 0  # row windows: window w = rows [w*rows, (w+1)*rows) of the aligned members (0: none)
-    aligned: list = field(default_factory=list)  # per member: its operands are staged (jit.window_source)
-    streams: list = field(default_factory=list)  # staged operand streams (base, stride): x[base + stride*i]
-    slot_stream: dict = field(default_factory=dict)  # aligned member -> stream index of each slot
-    # stage ranges: streams of stride 1 whose bases lie within STREAM_MERGE of each other share one
-    # range (base, stride, length); stream q is range stream_range[q] at offset stream_delta[q]
-    ranges: list = field(default_factory=list)
-    stream_range: list = field(default_factory=list)
-    stream_delta: list = field(default_factory=list)
-    # staged copies: window w's copy sources lie in [base, base + span) = copy_stage[w] (span 0: not
-    # staged, gathered from global); copy_pk[c] = (source - base) << 16 | window position
-    copy_stage: np.ndarray = None  # uint32 [n_win, 2]: (first source, span); span 0 = gathered from global
-    copy_pk: np.ndarray = None
-    cstage: int = 0  # doubles of the staged copy span (max over staged windows)
-    dstage: int = 0  # packed copy descriptors staged per window (max over staged windows)
 
-    @property
-    def range_doubles(self) -> int:
-        return sum(int(n) for _, _, n in self.ranges)
-
-    @property
-    def stage_doubles(self) -> int:
-        """Shared memory in front of the window buffer: ranges, copy span, copy descriptors (u32 pairs)."""
-        n = self.range_doubles + self.cstage + (self.dstage + 1) // 2
-        return n + (n & 1)  # the window buffer after it stays 16-byte aligned (double2 write-out)
-
-
-# row-window heights tried, largest first (one 256-thread block: 2 halves); SGB_STAGE_ROWS=0 turns the
-# staged windows off (the profiling comparison in tools/gpu_r2d.sh)
-STAGE_ROWS = () if os.environ.get("SGB_STAGE_ROWS") == "0" else (128, 64, 32)
-STREAM_MERGE = 16  # staged streams of stride 1 closer than this share one range
-COPY_STAGE_MAX = 2048  # a window's copies are staged when their sources span at most this many doubles..
-COPY_STAGE_DENSITY = 4  # ..and at most this many times their count
-STAGE_MAX_BYTES = 96 * 1024  # shared memory a staged window may use (operand streams + window buffer)
-
-
-def _row_windows(firsts, lasts, cand, n_out: int, blocked, rows: int, wmax: int):
-    """Row windows: window w starts at the first output of the aligned members' instances
-    [w*rows, (w+1)*rows) -- on mesh plans instance = vertex = CSR row, so a window is ``rows``
-    consecutive CSR rows and every aligned member's piece is exactly those instances.  Members
-    whose outputs do not follow (CSR row-major per instance) drop out of the aligned set.
-    Returns (k, aligned member indices) or None."""
-    big = np.iinfo(np.int64).max
-    if not cand:
-        return None
-    N = max((firsts[j].size for j in cand), key=lambda n: sum(firsts[j].size == n for j in cand))
-    aligned = {j for j in cand if firsts[j].size == N}
-    n_win = (N + rows - 1) // rows
-    while aligned:
-        F = np.full(N, big, np.int64)
-        for j in aligned:
-            F = np.minimum(F, firsts[j])
-        K = np.minimum.reduceat(F, np.arange(0, N, rows))
-        K[0] = 0
-        K = np.append(K, n_out)
-        for w in range(n_win - 1, 0, -1):  # windows without aligned outputs start where the next one does
-            if K[w] == big:
-                K[w] = K[w + 1]
-        if np.any(np.diff(K) < 0):
-            return None
-        bad = []
-        for j in aligned:
-            i = np.flatnonzero(firsts[j] != big)
-            w = i // rows
-            if not np.all((firsts[j][i] >= K[w]) & (lasts[j][i] < K[w + 1])):
-                bad.append(j)
-        if bad:
-            aligned -= set(bad)
-            continue
-        if np.any(blocked[K[1:-1]]) or int(np.diff(K).max(initial=0)) > wmax:
-            return None
-        return K, sorted(aligned)
-    return None
-
-
-def _stage_candidate(plan, kp) -> bool:
-    """A window member whose operands can be staged by rows: every slot is ``base + stride * i``
-    (affine column 0, all other slots offset-coherent), no constants."""
-    if kp.const_vars or not kp.pos_vars or len(kp.retained) != 1 or kp.layout != "coalesced" or kp.instances < 2:
-        return False
-    col0 = np.asarray(plan.positions[kp.p_base: kp.p_base + kp.instances], dtype=np.int64)
-    return affine_column0(col0) is not None
-
-
-def stage_streams(members) -> list:
-    """Distinct operand streams (base, stride) of the staged members, in first-use order."""
-    seen = {}
-    for g in members:
-        for key in g:
-            seen.setdefault(key, len(seen))
-    return list(seen)
-
-
-def _member_streams(plan, kp) -> list:
-    col0 = np.asarray(plan.positions[kp.p_base: kp.p_base + kp.instances], dtype=np.int64)
-    base, stride = affine_column0(col0)
-    return [(base + int(c), stride) for c in kp.coherence]
-
-
-def _merge_streams(wn) -> None:
-    """Stride-1 streams whose bases are within STREAM_MERGE share one staged range."""
-    order = sorted(range(len(wn.streams)), key=lambda q: (wn.streams[q][1], wn.streams[q][0]))
-    ranges, rng_of, delta = [], [0] * len(wn.streams), [0] * len(wn.streams)
-    for q in order:
-        base, stride = wn.streams[q]
-        if ranges and stride == 1 and ranges[-1][1] == 1 and base - ranges[-1][0] <= STREAM_MERGE:
-            lo, _, n = ranges[-1]
-            ranges[-1] = (lo, 1, max(n, base - lo + wn.rows))
-        else:
-            ranges.append((base, stride, wn.rows))
-        rng_of[q] = len(ranges) - 1
-        delta[q] = base - ranges[-1][0]
-    wn.ranges, wn.stream_range, wn.stream_delta = ranges, rng_of, delta
-
-
-def _stage_bytes(plan, groups, rows: int, wlen: int) -> int:
-    streams = stage_streams([_member_streams(plan, plan.kernels[g.kernel]) for g in groups])
-    fake = CsrWindows(k=None, pieces=None, wpos=None, copy_off=None, copy_src=None, copy_pos=None, rows=rows,
-                      streams=streams)
-    _merge_streams(fake)
-    return 8 * fake.range_doubles + 8 * (wlen + 2) + 8 * 1024  # + a typical copy stage
 
 
 def _csr_windows(member_opos: list, n_out: int, copy_k: np.ndarray, copy_addr: np.ndarray,
-                 rows: int = WIN_ROWS, wmax: int = WIN_MAX, stage_cand: list | None = None,
-                 stage_bytes=None) -> CsrWindows:
+                 rows: int = WIN_ROWS, wmax: int = WIN_MAX) -> CsrWindows:
     """Cut the CSR value array into windows for the window unit (jit.window_source).
 
     ``member_opos``: per member group its (R, N) CSR positions (NONE32 = not an output), first
@@ -949,13 +828,6 @@ def _csr_windows(member_opos: list, n_out: int, copy_k: np.ndarray, copy_addr: n
     allowed = allowed[(allowed > 0) & (allowed <= n_out)]
     if not allowed.size or allowed[-1] != n_out:
         allowed = np.append(allowed, n_out)
-    row_mode = None
-    for r_ in STAGE_ROWS if stage_cand and any(stage_cand) else ():
-        got = _row_windows(firsts, lasts, [j for j, c in enumerate(stage_cand) if c], n_out, blocked, r_, wmax)
-        if got is not None and (stage_bytes is None or stage_bytes(got[1], r_, int(np.diff(got[0]).max())) <=
-                                STAGE_MAX_BYTES):
-            row_mode = (r_,) + got
-            break
     counts = [int((f != big).sum()) for f in firsts]
     anchor = int(np.argmax(counts)) if counts else -1
     # preferred cuts: the first output of every ``rows``-th anchor instance (snapped to an allowed cut)
@@ -967,7 +839,7 @@ def _csr_windows(member_opos: list, n_out: int, copy_k: np.ndarray, copy_addr: n
         starts = fa[valid[q[q < valid.size]]]
         j = np.searchsorted(allowed, starts, side="right") - 1
         pref = np.unique(allowed[j[j >= 0]])
-    k = [0] if row_mode is None else list(row_mode[1])
+    k = [0]
     while k[-1] < n_out:
         cur = k[-1]
         lim = cur + wmax
@@ -1000,10 +872,6 @@ def _csr_windows(member_opos: list, n_out: int, copy_k: np.ndarray, copy_addr: n
         b = np.where(has, inst[np.maximum(hi - 1, 0)] + 1, 0)
         pieces[:, j, 0] = a
         pieces[:, j, 1] = b - a
-        if row_mode is not None and j in row_mode[2]:  # aligned: the window's rows, padding included
-            r0 = np.arange(n_win, dtype=np.int64) * row_mode[0]
-            pieces[:, j, 0] = r0
-            pieces[:, j, 1] = np.minimum(row_mode[0], n - r0)
         w_of = np.searchsorted(k, np.where(f == big, 0, f), side="right") - 1  # window of each instance
         rel = np.where(o == NONE32, 0xFFFF, o - k[np.clip(w_of, 0, n_win - 1)][None, :])
         if n and rel.size and int(rel[o != NONE32].max(initial=0)) >= 0xFFFF:
@@ -1014,26 +882,8 @@ def _csr_windows(member_opos: list, n_out: int, copy_k: np.ndarray, copy_addr: n
     copy_off = np.searchsorted(ck, k).astype(np.int64)
     cw = np.searchsorted(k, ck, side="right") - 1
     copy_pos = (ck - k[np.clip(cw, 0, max(n_win - 1, 0))]).astype(np.uint16) if ck.size else np.zeros(0, np.uint16)
-    aligned = set(row_mode[2]) if row_mode is not None else set()
-    # staged copies (row windows only): per window the span of its copy sources
-    copy_stage = np.zeros((n_win, 2), np.uint32)
-    copy_pk = np.zeros(ca.size, np.uint32)
-    cstage = dstage = 0
-    if row_mode is not None and ca.size:
-        for w in range(n_win):
-            c0, c1 = int(copy_off[w]), int(copy_off[w + 1])
-            if c1 == c0:
-                continue
-            lo_, hi_ = int(ca[c0:c1].min()), int(ca[c0:c1].max())
-            span = hi_ - lo_ + 1
-            if span <= COPY_STAGE_MAX and span <= COPY_STAGE_DENSITY * (c1 - c0):
-                copy_stage[w] = (lo_, span)
-                copy_pk[c0:c1] = ((ca[c0:c1] - lo_) << 16 | copy_pos[c0:c1].astype(np.int64)).astype(np.uint32)
-                cstage, dstage = max(cstage, span), max(dstage, c1 - c0)
     return CsrWindows(k=k, pieces=pieces, wpos=wpos, copy_off=copy_off, copy_src=ca.astype(np.uint32),
-                      copy_pos=copy_pos, rows=row_mode[0] if row_mode is not None else 0,
-                      aligned=[j in aligned for j in range(J)], copy_stage=copy_stage, copy_pk=copy_pk,
-                      cstage=(cstage + 1) // 2 * 2, dstage=(dstage + 3) // 4 * 4)
+                      copy_pos=copy_pos)
 
 
 def jit_vec(groups, sel) -> int:
@@ -1319,20 +1169,9 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     windows = None
     if window is not None:
         # members in kernel order == their order in the window unit (pieces columns)
-        cand = [_stage_candidate(plan, plan.kernels[g.kernel]) and g.kernel not in imajor for g in win_groups]
-        windows = _csr_windows([opos[g.kernel] for g in win_groups], len(plan.outputs), res_k, res_addr,
-                               stage_cand=cand,
-                               stage_bytes=lambda al, rows, wlen: _stage_bytes(plan, [win_groups[j] for j in al],
-                                                                              rows, wlen))
+        windows = _csr_windows([opos[g.kernel] for g in win_groups], len(plan.outputs), res_k, res_addr)
         for g, wp in zip(win_groups, windows.wpos):
             g.wpos = wp
-        if windows.rows:  # staged members: their slots as operand streams
-            al = [j for j, a in enumerate(windows.aligned) if a]
-            per = {j: _member_streams(plan, plan.kernels[win_groups[j].kernel]) for j in al}
-            windows.streams = stage_streams([per[j] for j in al])
-            sidx = {key: q for q, key in enumerate(windows.streams)}
-            windows.slot_stream = {j: [sidx[key] for key in per[j]] for j in al}
-            _merge_streams(windows)
     extra_pos = []
     p_next = int(np.asarray(plan.positions).size)
     copy_waves = []
@@ -1500,7 +1339,7 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                     raise AssertionError("one CSR-window unit holding every member")
                 n_win = windows.k.size - 1
                 window_units.append((len(units), 0, n_win))
-                smem = 8 * (windows.stage_doubles + int(np.diff(windows.k).max(initial=0)) + 2)  # + alignment
+                smem = 8 * (int(np.diff(windows.k).max(initial=0)) + 2)  # + alignment slots
                 units.append((w, kind, variant, g_begin, len(order_groups), 0, n_win, bs, smem,
                               UNIT_CSR_ONLY | UNIT_JIT | UNIT_WINDOW))
                 jit_units.append(len(units) - 1)

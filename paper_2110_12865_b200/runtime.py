@@ -88,11 +88,6 @@ class _Desc(ctypes.Structure):
         ("copy_src", ctypes.c_void_p),
         ("copy_pos", ctypes.c_void_p),
         ("n_copy", ctypes.c_int64),
-        ("win_stage", ctypes.c_int64),
-        ("win_cstg", ctypes.c_void_p),
-        ("copy_pk", ctypes.c_void_p),
-        ("win_cstage", ctypes.c_int64),
-        ("win_dstage", ctypes.c_int64),
     ]
 
 
@@ -216,10 +211,6 @@ class DevicePlan:
             wcopy=np.ascontiguousarray(wn.copy_off if wn is not None else np.zeros(0), np.int64),
             csrc=np.ascontiguousarray(wn.copy_src if wn is not None else np.zeros(0), np.uint32),
             cpos=np.ascontiguousarray(wn.copy_pos if wn is not None else np.zeros(0), np.uint16),
-            cstg=np.ascontiguousarray(wn.copy_stage if wn is not None and wn.copy_stage is not None
-                                      else np.zeros((0, 2)), np.uint32).reshape(-1, 2),
-            cpk=np.ascontiguousarray(wn.copy_pk if wn is not None and wn.copy_pk is not None else np.zeros(0),
-                                     np.uint32),
         )
         d = _Desc(
             value_array_size=self.value_array_size, input_count=self.input_count,
@@ -239,9 +230,7 @@ class DevicePlan:
             win_pieces=_ptr(keep["wpieces"]), n_win_pieces=keep["wpieces"].shape[0],
             win_k=_ptr(keep["wk"]), n_win_k=keep["wk"].size, win_copy=_ptr(keep["wcopy"]),
             n_win_copy=keep["wcopy"].size, copy_src=_ptr(keep["csrc"]), copy_pos=_ptr(keep["cpos"]),
-            n_copy=keep["csrc"].size, win_stage=wn.stage_doubles if wn is not None else 0,
-            win_cstg=_ptr(keep["cstg"]), copy_pk=_ptr(keep["cpk"]),
-            win_cstage=wn.cstage if wn is not None else 0, win_dstage=wn.dstage if wn is not None else 0,
+            n_copy=keep["csrc"].size,
         )
         torch.cuda.init()
         _check(self._lib.sgb_plan_create(ctypes.byref(d), self.device, ctypes.byref(self._handle)),

@@ -192,9 +192,7 @@ def shard_device_plan(plan, lowered, lo: int, hi: int):
         c0, c1 = int(wn.copy_off[w0]), int(wn.copy_off[w1])
         swn = dataclasses.replace(wn, k=np.asarray(wn.k[w0: w1 + 1], np.int64) - lo, pieces=wn.pieces[w0:w1],
                                   copy_off=np.asarray(wn.copy_off[w0: w1 + 1], np.int64) - c0,
-                                  copy_src=wn.copy_src[c0:c1], copy_pos=wn.copy_pos[c0:c1],
-                                  copy_stage=None if wn.copy_stage is None else wn.copy_stage[w0:w1],
-                                  copy_pk=None if wn.copy_pk is None else wn.copy_pk[c0:c1])
+                                  copy_src=wn.copy_src[c0:c1], copy_pos=wn.copy_pos[c0:c1])
     lw = dataclasses.replace(lowered, tiles=new_tiles.reshape(-1, 2), units=units,
                              outputs=np.asarray(lowered.outputs, np.int64)[lo:hi], tiles_alt=None, windows=swn)
     return view, lw

@@ -51,8 +51,8 @@ def lowering_specs(names: list[str]) -> list[tuple[str, tuple]]:
     return specs
 
 
-# builder plans the GPU suite runs beyond the fixtures: C2 (staged CSR windows, odd stage sizes),
-# C3 (CSR layout), C4 (gather) at small sizes
+# builder plans the GPU suite runs beyond the fixtures: C2 (CSR windows), C3 (CSR layout), C4 (gather)
+# at small sizes
 BUILDER_CASES = {"lmlt_w70": ("mesh", 70), "lmlt_w65": ("mesh", 65), "fem_m9": ("fem", 9), "arap_w70": ("arap", 70)}
 
 

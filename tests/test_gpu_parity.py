@@ -58,9 +58,9 @@ def test_compile_plan_values(golden):
 @pytest.mark.parametrize("name", sorted(BUILDER_CASES))
 @pytest.mark.parametrize("relayout", [False, "auto"])
 def test_builder_plans_default_lowering(name, relayout):
-    """The config builders' plans at small sizes through the default lowering (CSR windows with staged
-    operand streams and copies on the mesh plans, the CSR layout on the FEM plan): run_csr, the captured
-    graph and the host path == the oracle, bit for bit."""
+    """The config builders' plans at small sizes through the default lowering (CSR windows on the mesh
+    plans, the CSR layout on the FEM plan): run_csr, the captured graph and the host path == the oracle,
+    bit for bit."""
     import torch
 
     from oracle import oracle
@@ -80,7 +80,7 @@ def test_builder_plans_default_lowering(name, relayout):
     torch.cuda.synchronize()
     assert np.array_equal(bits(out.cpu().numpy()), bits(want))
     if name.startswith("lmlt"):
-        assert dp.lowered.windows is not None and dp.lowered.windows.rows > 0  # staged windows ran
+        assert dp.lowered.windows is not None  # the CSR windows ran
 
 
 @pytest.mark.parametrize("name", LAYOUT_CASES)

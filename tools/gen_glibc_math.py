@@ -537,7 +537,7 @@ __device__ const unsigned long long sgb_exp_tab[{2 * N_TAB}] = {{  // (tail, bit
 __device__ __forceinline__ double sgb_as_double(unsigned long long u) {{ return __longlong_as_double((long long)u); }}
 __device__ __forceinline__ unsigned long long sgb_as_u64(double x) {{ return (unsigned long long)__double_as_longlong(x); }}
 
-__device__ __noinline__ double sgb_log(double x) {{
+__device__ __forceinline__ double sgb_log(double x) {{
   unsigned long long ix = sgb_as_u64(x);
   const unsigned long long lo_b = 0x3fee000000000000ull, hi_b = 0x3ff1090000000000ull;  // 1 -/+ 2^-4, 1.0646
   if (ix - lo_b < hi_b - lo_b) {{  // |x - 1| small: polynomial in r = x - 1, exact split of r*r/2
@@ -637,7 +637,7 @@ __device__ __forceinline__ double sgb_exp_core(double x, double xtail, unsigned 
   return __fma_rn(scale, tmp, scale);
 }}
 
-__device__ __noinline__ double sgb_exp(double x) {{ return sgb_exp_core(x, 0.0, 0u, false); }}
+__device__ __forceinline__ double sgb_exp(double x) {{ return sgb_exp_core(x, 0.0, 0u, false); }}
 
 // 0: y not an integer, 1: odd integer, 2: even integer (y non-zero finite)
 __device__ __forceinline__ int sgb_checkint(unsigned long long iy) {{
@@ -653,7 +653,7 @@ __device__ __forceinline__ bool sgb_zeroinfnan(unsigned long long i) {{
   return 2 * i - 1 >= 2 * 0x7ff0000000000000ull - 1;
 }}
 
-__device__ __noinline__ double sgb_pow(double x, double y) {{
+__device__ __forceinline__ double sgb_pow(double x, double y) {{
   unsigned sign_bias = 0;
   unsigned long long ix = sgb_as_u64(x);
   const unsigned long long iy = sgb_as_u64(y);
@@ -770,7 +770,7 @@ __device__ __forceinline__ double sgb_do_sincos(double a, double da, unsigned n)
   return (n & 2u) ? -r : r;
 }}
 
-__device__ __noinline__ double sgb_sin(double x) {{
+__device__ __forceinline__ double sgb_sin(double x) {{
   const unsigned k = (unsigned)(sgb_as_u64(x) >> 32) & 0x7fffffffu;
   if (k < 0x3e500000u) return x;
   if (k < 0x3feb6000u) return fabs(x) < SGB_SC_SMALL ? sgb_taylor_sin(x, 0.0) : sgb_do_sin(x, 0.0);
@@ -784,7 +784,7 @@ __device__ __noinline__ double sgb_sin(double x) {{
   return __ddiv_rn(x, x);
 }}
 
-__device__ __noinline__ double sgb_cos(double x) {{
+__device__ __forceinline__ double sgb_cos(double x) {{
   const unsigned k = (unsigned)(sgb_as_u64(x) >> 32) & 0x7fffffffu;
   if (k < 0x3e400000u) return 1.0;
   if (k < 0x3feb6000u) return sgb_do_cos(x, 0.0);
@@ -817,7 +817,7 @@ def main():
     if bad:
         raise SystemExit(f"restatement differs from math on {len(bad)} samples, e.g. {bad[:5]}")
     OUT.write_text(header(t, str(path)))
-    print(f"wrote {OUT} (log / exp / pow restatements bit-identical to math on {args.samples} samples each)")
+    print(f"wrote {OUT} (sin / cos / exp / log / pow restatements bit-identical to math on {args.samples} samples each)")
 
 
 if __name__ == "__main__":
