@@ -712,26 +712,6 @@ __global__ void __launch_bounds__(256) gather_outputs(const double *__restrict__
     st_stream(out + k, __ldg(x + __ldg(outs + k)), pol);
 }
 
-// Four outputs per thread, one block per 1024 outputs (in-order dispatch): one 16-byte index load,
-// four independent gathered loads in flight, two 16-byte streaming stores.
-__device__ __forceinline__ void st_stream2(double *a, double v0, double v1, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(a), "d"(v0), "d"(v1), "l"(pol) : "memory");
-}
-
-__global__ void __launch_bounds__(256) gather_outputs4(const double *__restrict__ x, const uint32_t *__restrict__ outs,
-                                                       int64_t n, double *__restrict__ out) {
-  const uint64_t pol = evict_first_policy();
-  const int64_t k = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  if (k + 3 < n) {
-    const uint4 ix = __ldcs(reinterpret_cast<const uint4 *>(outs + k));
-    const double a = __ldg(x + ix.x), b = __ldg(x + ix.y), c = __ldg(x + ix.z), d = __ldg(x + ix.w);
-    st_stream2(out + k, a, b, pol);
-    st_stream2(out + k + 2, c, d, pol);
-  } else {
-    for (int64_t j = k; j < n; ++j) st_stream(out + j, __ldg(x + __ldg(outs + j)), pol);
-  }
-}
-
 // Batched outputs: one output per warp, lanes over value sets, 4 value sets per lane
 // per iteration with all loads issued first.
 __global__ void gather_outputs_batch(const double *__restrict__ X, int64_t ld, int64_t batch,
@@ -882,12 +862,8 @@ void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_
       int64_t ld_ = ld, batch_ = batch, ldo = ld_out;
       void *args[] = {&T, &tiles, &n, &x, &ld_, &batch_, &out, &ldo, &c};
       // the batched kernels run a persistent grid of their own occupancy (the per-wave grid choice is
-      // tuned single-set); SGB_BATCH_GRID=tiles launches one block per batched tile instead
-      static const bool batch_tiles = [] {
-        const char *e = getenv("SGB_BATCH_GRID");
-        return e && !strcmp(e, "tiles");
-      }();
-      const int64_t cap = batch_tiles ? blocks : (u.grid_b > 0 ? u.grid_b : u.grid);
+      // tuned single-set; one block per batched tile measured slower, profiles/r44)
+      const int64_t cap = u.grid_b > 0 ? u.grid_b : u.grid;
       const int64_t grid = blocks < cap ? blocks : cap;
       cudaLaunchKernel(u.jitb, dim3((unsigned)grid), dim3(JIT_BLOCK), args, 0, s);
     } else {
@@ -1294,14 +1270,11 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
     // specialised units have two grids: the persistent one (resident capacity, tiles grid-strided)
     // and one block per tile, the hardware dispatching blocks in tile order as SMs free up --
     // persistent blocks drift apart over a long sweep and widen its L2 working set.
-    // sgb_plan_set_wave_grid picks per wave (runtime autotune); SGB_JIT_GRID=tiles sets the default.
-    const char *jg = getenv("SGB_JIT_GRID");
-    const bool tiles_default = jg && !strcmp(jg, "tiles");
+    // sgb_plan_set_wave_grid picks per wave (runtime autotune); the default is persistent.
     for (Unit &u : p->units)
       if ((u.flags & UNIT_JIT) && !(u.flags & UNIT_WINDOW)) {
         u.grid_p = u.grid;
         u.grid_t = u.t1 - u.t0 < 0x7fffffffLL ? u.t1 - u.t0 : 0x7fffffffLL;
-        if (tiles_default && u.grid_t > 0) u.grid = u.grid_t;
       }
     p->wave_units.assign(max_wave + 1, {});
     for (int k = 0; k < (int)p->units.size(); ++k) p->wave_units[p->units[k].wave].push_back(k);
@@ -1498,21 +1471,9 @@ static int launch_gather(sgb_plan *p, const double *x, int64_t ld, int64_t batch
     gather_outputs_batch<<<(unsigned)blocks, 256, 0, s>>>(x, ld, batch, p->d_outputs, p->n_out, out, ld_out);
   } else {
     int64_t blocks = (p->n_out + 255) / 256;
-    // SGB_GATHER_GRID=tiles: one block per 256 outputs (in-order dispatch) instead of a capped grid
-    static const bool gather_tiles = [] {
-      const char *e = getenv("SGB_GATHER_GRID");
-      return e && !strcmp(e, "tiles");
-    }();
-    static const bool gather_v4 = [] {
-      const char *e = getenv("SGB_GATHER");
-      return e && !strcmp(e, "v4");
-    }();
-    if (gather_v4 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
-      const int64_t b4 = (p->n_out + 1023) / 1024;
-      gather_outputs4<<<(unsigned)b4, 256, 0, s>>>(x, p->d_outputs32, p->n_out, out);
-      return 0;
-    }
-    if (!gather_tiles && blocks > 148 * 32) blocks = 148 * 32;
+    // a capped grid-stride grid: one block per 256 outputs and four outputs per thread with 16-byte
+    // index loads both measured slower (profiles/r42)
+    if (blocks > 148 * 32) blocks = 148 * 32;
     if (blocks > 0x7fffffffLL) blocks = 0x7fffffffLL;
     gather_outputs<<<(unsigned)blocks, 256, 0, s>>>(x, p->d_outputs32, p->n_out, out);
   }

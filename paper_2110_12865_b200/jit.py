@@ -293,8 +293,6 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
     unit = dp.unit(u)
     out = []
     big = max(len(tapes[gi]) for gi in range(unit["group_begin"], unit["group_end"]))
-    # register cap (blocks per SM): huge templates run best uncapped -- spills cost more than occupancy
-    min_blocks = int(os.environ.get("SGB_JIT_MINBLOCKS", "0"))  # 2 measured 2.7x slower on C3 (r24)
     # batched value sets per lane: 8 for small templates (C5: 2.90 -> 2.47 ms, r45); big templates keep
     # 4 (their register file is full already, and the body is compiled once per value set)
     bvec = BATCH_VEC if big <= BATCH_VEC_SMALL_TAPE else min(BATCH_VEC, 4)
@@ -309,7 +307,9 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
                     f"    for (i64 b = threadIdx.x & 31; b < batch; b += {32 * bvec}) {{",
                     "    switch (tl.x) {"]
         else:
-            bounds = f"{JIT_BLOCK}, {min_blocks}" if min_blocks > 1 else f"{JIT_BLOCK}"
+            # no register cap: huge templates run best uncapped -- a 2-block cap spilled and measured
+            # 2.7x slower on C3 (r24)
+            bounds = f"{JIT_BLOCK}"
             head = [f'extern "C" __global__ void __launch_bounds__({bounds}) sgb_tape_u{u}(',
                     "    Tables T, const int2 *tiles, i64 n_tiles, double *x, double *out, int csr) {",
                     "  extern __shared__ double stage_[];",

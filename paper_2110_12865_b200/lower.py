@@ -51,6 +51,7 @@ FLAG_COHERENT = 1024  # one retained column: every slot is column 0 + delta
 FLAG_IMAJOR = 2048  # CSR layout: result r of instance i at dest_base + i * n_roots + r (specialised units only)
 FLAG_WPOS16 = 4096  # CSR-window member: root r of instance i goes to its window's position ooff[oo_off + r*n + i]
 UNIT_CSR_ONLY = 1
+STORE_ROOTS_EARLY = True  # roots stored as soon as computed (False: all at the end of the tape)
 UNIT_JIT = 2  # tape unit compiled to straight-line code (jit.py), one instance per thread
 UNIT_VALUE_ONLY = 4  # value-mode twin of a CSR-window unit (skipped by sgb_run_csr)
 UNIT_WINDOW = 8  # CSR windows: each block assembles one window of consecutive outputs in shared memory
@@ -354,6 +355,8 @@ def compile_tape(kp):
     stored: set = set()
 
     def store_roots(ref):
+        if not STORE_ROOTS_EARLY:
+            return
         for r_idx in root_idx.get(ref, ()):
             emit(T_ST, 0, reg[ref], aux=r_idx)
         stored.add(ref)

@@ -30,8 +30,7 @@ def main():
     ins = bench.workload_inputs("c2", ns, 0)
     ref = DevicePlan(plan, lowered=lower_plan(plan, csr_window=False))
     want = ref.run_csr(ref.new_values(ins)).cpu().numpy()
-    variants = [dict(loads=l_, blocks=b_, rows=r_) for l_, b_, r_ in itertools.product((16, 24, 32), (3, 4), (240,))]
-    variants += [dict(loads=24, blocks=3, rows=112), dict(loads=24, blocks=4, rows=112)]
+    variants = [dict(loads=l_, blocks=3, rows=240) for l_ in (24, 32, 40, 48)] * 2
     for v in variants:
         jit.WINDOW_LOADS, jit.WINDOW_MIN_BLOCKS, lower.WIN_ROWS = v["loads"], v["blocks"], v["rows"]
         t0 = time.perf_counter()
