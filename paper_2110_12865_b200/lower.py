@@ -51,7 +51,7 @@ FLAG_COHERENT = 1024  # one retained column: every slot is column 0 + delta
 FLAG_IMAJOR = 2048  # CSR layout: result r of instance i at dest_base + i * n_roots + r (specialised units only)
 FLAG_WPOS16 = 4096  # CSR-window member: root r of instance i goes to its window's position ooff[oo_off + r*n + i]
 UNIT_CSR_ONLY = 1
-STORE_ROOTS_EARLY = True  # roots stored as soon as computed (False: all at the end of the tape)
+STORE_ROOTS_EARLY = False  # roots stored as soon as computed (True) or at the end: C3 element kernel 0.318 vs 0.291 ms (c3v)
 UNIT_JIT = 2  # tape unit compiled to straight-line code (jit.py), one instance per thread
 UNIT_VALUE_ONLY = 4  # value-mode twin of a CSR-window unit (skipped by sgb_run_csr)
 UNIT_WINDOW = 8  # CSR windows: each block assembles one window of consecutive outputs in shared memory
@@ -347,8 +347,9 @@ def compile_tape(kp):
         rr, rn = operand(right)
         emit(T_SUB if sub else T_ADD, dst, lr, rr, nega=ln, negb=rn)
 
-    # every root is stored right after it is computed (not at the end), so a multi-root template
-    # (C3's 78-root element Hessian) does not keep all of its roots live until the last one
+    # STORE_ROOTS_EARLY: every root is stored right after it is computed, so a multi-root template
+    # does not keep all of its roots live until the last one (fewer registers; measured slower on C3's
+    # 78-root element Hessian, whose stores then interleave with the computes)
     root_idx: dict[int, list[int]] = {}
     for r_idx, root in enumerate(roots):
         root_idx.setdefault(root, []).append(r_idx)

@@ -33,7 +33,7 @@ def main():
     key, plan = bench.build_workload("c3", ns)
     ins = bench.workload_inputs("c3", ns, 0)
     want = None
-    for early, log in itertools.product((True, False), ("sgb_log", "log")):
+    for early, log in itertools.product((True, False), ("sgb_log({a})", "log({a})")):
         lower.STORE_ROOTS_EARLY = early
         jit._SLOW[3] = log
         t0 = time.perf_counter()
