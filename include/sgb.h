@@ -23,9 +23,12 @@
  *
  * Conventions: every call returns 0 on success and a negative code on
  * failure (no exceptions cross the ABI); sgb_last_error() describes the last
- * failure of the calling thread.  A plan is immutable after create and may be
- * run concurrently on distinct x buffers; device calls are stream-ordered
- * with no host synchronisation inside.  `stream` is a cudaStream_t (NULL =
+ * failure of the calling thread.  A plan's tables and kernels are fixed at
+ * create; only its launch configuration changes afterwards (sgb_plan_set_tiles,
+ * sgb_plan_set_wave_grid: same tiles, other order / grid, same results).  Calls
+ * on one plan serialise their launch sequences (the wave fork/join streams are
+ * per plan); distinct x buffers may be in flight at once.  Device calls are
+ * stream-ordered with no host synchronisation inside.  `stream` is a cudaStream_t (NULL =
  * legacy default stream).  Only sm_100a (B200) is supported; there is no CPU
  * fallback.
  */
@@ -125,6 +128,23 @@ typedef struct sgb_plan_desc {
   const uint32_t *copy_src;  /* [n_copy] value-array address of each copied output */
   const uint16_t *copy_pos;  /* [n_copy] its position in its window */
   int64_t n_copy;
+  /* Bulk feed of the CSR-window unit (units flag 16 on the window unit, lower.WindowBulk): a
+     persistent block of block_size threads (consumers + one producer warp) walks windows
+     blockIdx.x, blockIdx.x + gridDim.x, ...; per window its producer thread copies the consumer
+     blob win_meta[win_meta_off[w] .. win_meta_off[w+1]) and the value-array intervals
+     win_iv[win_iv_off[w] .. win_iv_off[w+1]) (first element, element count; both even) with
+     cp.async.bulk into a ring slot of win_slot_meta + win_slot_x bytes (win_ring slots after a
+     win_bw-byte window buffer); win_bulk[j] = 1 marks the members fed from the ring.  A plan with
+     such a unit reads value-array slot value_array_size (padding) when that size is odd: see
+     sgb_plan_value_slots. */
+  const uint8_t *win_meta;
+  int64_t n_win_meta;
+  const int64_t *win_meta_off; /* [n_windows + 1] when n_win_meta > 0 */
+  const uint32_t *win_iv;      /* [n_win_iv][2] */
+  int64_t n_win_iv;
+  const int64_t *win_iv_off;   /* [n_windows + 1] */
+  const int32_t *win_bulk;     /* [J] */
+  int64_t win_ring, win_slot_meta, win_slot_x, win_bw;
 } sgb_plan_desc;
 
 /* Upload a device plan to `device`.  Replaces compile_plan (emit.py:198-245). */
@@ -136,7 +156,8 @@ void sgb_plan_destroy(sgb_plan *plan);
 int sgb_run_values(sgb_plan *plan, double *x_dev, void *stream);
 
 /* inputs -> CSR values: out_dev[k] == x[outputs[k]] after sg_run (codegen.py:445).
- * x_dev holds the inputs and serves as scratch for intermediates.  With CSR
+ * x_dev holds the inputs and serves as scratch for intermediates; it must be
+ * 16-byte aligned and readable for sgb_plan_value_slots(plan) doubles.  With CSR
  * windows (the default lowering when the last wave qualifies) the last wave
  * assembles the CSR array window by window in shared memory and writes it
  * coalesced -- no separate gather; otherwise the value waves run and one
@@ -199,6 +220,11 @@ int sgb_plan_waves(const sgb_plan *plan, int csr);
 
 /* Kernel launches one evaluation issues in value / CSR mode. */
 int sgb_plan_units(const sgb_plan *plan, int csr);
+
+/* Doubles a CSR-mode value-array workspace must span: value_array_size, rounded up to even
+ * when the plan has a bulk-fed CSR-window unit (its 16-byte bulk copies may read the padding
+ * slot; its value is never used). */
+int64_t sgb_plan_value_slots(const sgb_plan *plan);
 
 const char *sgb_last_error(void);
 

@@ -36,6 +36,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <cstring>
+
 #include <algorithm>
 #include <mutex>
 #include <string>
@@ -61,7 +63,7 @@ enum : int {
 enum : int {
   U_WAVE = 0, U_KIND, U_VARIANT, U_G0, U_G1, U_T0, U_T1, U_BS, U_REGS, U_FLAGS, U_COUNT
 };
-enum : int { UNIT_CSR_ONLY = 1, UNIT_JIT = 2, UNIT_VALUE_ONLY = 4, UNIT_WINDOW = 8 };
+enum : int { UNIT_CSR_ONLY = 1, UNIT_JIT = 2, UNIT_VALUE_ONLY = 4, UNIT_WINDOW = 8, UNIT_BULK = 16 };
 constexpr int JIT_BLOCK = 256;  // jit.py JIT_BLOCK
 constexpr int PRE = 8;        // slot loads kept in flight by the tape prologue
 constexpr int SOP_BS = 256;   // sum-of-products block
@@ -786,6 +788,12 @@ struct sgb_plan {
   uint32_t *d_csrc = nullptr;
   uint16_t *d_cpos = nullptr;
   uint32_t *d_fbase = nullptr;
+  // bulk feed of the CSR-window unit (UNIT_BULK): consumer blobs + value-array intervals per window
+  uint8_t *d_wmeta = nullptr;
+  int64_t *d_wmeta_off = nullptr, *d_wiv_off = nullptr;
+  uint2 *d_wiv = nullptr;
+  int64_t wb_ring = 0, wb_meta = 0, wb_x = 0, wb_bw = 0;
+  int64_t vas_slots = 0;  // value-array doubles a CSR workspace spans (vas, even with a bulk unit)
   // workspace for the host-buffer entry points
   std::mutex ws_mu;
   double *d_x = nullptr, *d_out = nullptr;
@@ -840,6 +848,17 @@ void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_
   const int64_t blocks = batched ? u.bt1 - u.bt0 : u.t1 - u.t0;
   if (blocks <= 0) return;
   if (!batched && csr && (u.flags & UNIT_VALUE_ONLY)) return;
+  if (u.flags & UNIT_BULK) {  // bulk-fed CSR windows (jit.py wbulk_source): persistent blocks, smem ring
+    const uint8_t *meta = p->d_wmeta;
+    const int64_t *moff = p->d_wmeta_off, *ivoff = p->d_wiv_off;
+    const uint2 *iv = p->d_wiv;
+    int64_t n = u.t1 - u.t0, ring = p->wb_ring, sm = p->wb_meta, sx = p->wb_x, bw = p->wb_bw;
+    Tables T = p->T;
+    const double *xc = x;
+    void *args[] = {&T, &meta, &moff, &iv, &ivoff, &n, &xc, &out, &ring, &sm, &sx, &bw};
+    cudaLaunchKernel(u.jit, dim3((unsigned)u.grid), dim3(u.bs), args, (size_t)u.regs, s);
+    return;
+  }
   if (u.flags & UNIT_WINDOW) {  // CSR windows (jit.py window_source): one block per window
     const int2 *pieces = p->d_wpieces;
     const int64_t *wk = p->d_wk, *wc = p->d_wcopy;
@@ -937,6 +956,8 @@ int sgb_plan_waves(const sgb_plan *p, int csr) {
   return p->direct_csr ? p->csr_waves : p->n_waves + (p->n_out > 0 ? 1 : 0);  // + the gather
 }
 
+int64_t sgb_plan_value_slots(const sgb_plan *p) { return p ? p->vas_slots : 0; }
+
 int sgb_plan_units(const sgb_plan *p, int csr) {
   if (!p) return 0;
   const bool direct = csr && p->direct_csr;
@@ -956,7 +977,8 @@ void sgb_plan_destroy(sgb_plan *p) {
   void *bufs[] = {p->d_groups, p->d_tiles, p->d_btiles, p->d_outputs, p->d_tape, p->d_imm, p->d_con,
                   p->d_sop, p->d_scol, p->d_sdel, p->d_pos, p->d_x, p->d_out, p->d_cbase, p->d_coff,
                   p->d_obase, p->d_ooff, p->d_opos32, p->d_sopd, p->d_fbase, p->d_outputs32,
-                  p->d_wpieces, p->d_wk, p->d_wcopy, p->d_csrc, p->d_cpos, p->d_x2, p->d_out2};
+                  p->d_wpieces, p->d_wk, p->d_wcopy, p->d_csrc, p->d_cpos, p->d_x2, p->d_out2,
+                  p->d_wmeta, p->d_wmeta_off, p->d_wiv_off, p->d_wiv};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (p->ws_stream) cudaStreamDestroy(p->ws_stream);
@@ -967,6 +989,89 @@ void sgb_plan_destroy(sgb_plan *p) {
   for (cudaEvent_t e : p->ev_join) cudaEventDestroy(e);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   delete p;
+}
+
+static int64_t a16(int64_t v) { return (v + 15) & ~(int64_t)15; }
+
+// The bulk feed of the CSR-window unit (lower.WindowBulk): every blob, interval and offset the
+// kernel dereferences stays inside its window's ring slot, window buffer and value array.
+static int check_window_bulk(const sgb_plan_desc *d, const Unit &u, int64_t n_win, int64_t J, int64_t smem_max) {
+  auto bad = [](const std::string &what) { return fail(-1, "sgb_plan_create: bad bulk CSR-window feed: " + what); };
+  if (!d->win_meta || d->n_win_meta <= 0 || !d->win_meta_off || !d->win_iv_off || !d->win_bulk ||
+      (d->n_win_iv > 0 && !d->win_iv) || d->n_win_iv < 0)
+    return bad("missing tables");
+  if (d->win_ring < 1 || d->win_ring > 8 || d->win_slot_meta <= 0 || d->win_slot_meta % 128 || d->win_slot_x <= 0 ||
+      d->win_slot_x % 128 || d->win_bw < 128 || d->win_bw % 128 || u.bs != JIT_BLOCK + 32 ||
+      (int64_t)u.regs != d->win_bw + d->win_ring * (d->win_slot_meta + d->win_slot_x) || u.regs > smem_max)
+    return bad("ring / block geometry");
+  const int64_t vas_even = d->value_array_size + (d->value_array_size & 1);
+  int64_t NR = 0, NW = 0;
+  for (int64_t j = 0; j < J; ++j) {
+    if (!d->win_bulk[j]) continue;
+    const sgb_group &G = d->groups[u.g0 + j];
+    if ((G.flags & FLAG_INTERLEAVED) || G.n_const || G.n_slots < 1) return bad("member " + std::to_string(j));
+    NR += G.n_slots;
+    NW += G.n_roots;
+  }
+  const int64_t roff_at = 32 + 8 * J, woff_at = roff_at + 2 * NR, wpos_at = a16(woff_at + 2 * NW);
+  if (d->win_meta_off[0] != 0 || d->win_meta_off[n_win] != d->n_win_meta || d->win_iv_off[0] != 0 ||
+      d->win_iv_off[n_win] != d->n_win_iv)
+    return bad("offsets do not cover the tables");
+  const int64_t wmax = d->win_bw / 8 - 2;
+  for (int64_t w = 0; w < n_win; ++w) {
+    const int64_t m0 = d->win_meta_off[w], m1 = d->win_meta_off[w + 1];
+    if (m1 <= m0 || m0 % 16 || (m1 - m0) % 16 || m1 - m0 > d->win_slot_meta || m1 - m0 < wpos_at)
+      return bad("blob " + std::to_string(w));
+    const uint8_t *b = d->win_meta + m0;
+    uint32_t h[4];
+    int64_t k0;
+    uint32_t h2[2];
+    std::memcpy(h, b, 16);
+    std::memcpy(&k0, b + 16, 8);
+    std::memcpy(h2, b + 24, 8);
+    const int64_t nc = h[0], csrc_at = h[1], cpos_at = h[2], len = h[3], nwp = h2[0], xl = h2[1];
+    if (k0 != d->win_k[w] || len != d->win_k[w + 1] - d->win_k[w] || len > wmax ||
+        nc != d->win_copy[w + 1] - d->win_copy[w] || csrc_at != a16(wpos_at + 2 * nwp) ||
+        cpos_at != a16(csrc_at + 4 * nc) || a16(cpos_at + 2 * nc) != m1 - m0 || 8 * xl > d->win_slot_x)
+      return bad("header of window " + std::to_string(w));
+    int64_t sum = 0;
+    for (int64_t v = d->win_iv_off[w]; v < d->win_iv_off[w + 1]; ++v) {
+      const int64_t src = d->win_iv[2 * v], cnt = d->win_iv[2 * v + 1];
+      if ((src & 1) || (cnt & 1) || cnt <= 0 || src + cnt > vas_even) return bad("interval " + std::to_string(v));
+      sum += cnt;
+    }
+    if (sum != xl) return bad("x area of window " + std::to_string(w));
+    if (std::memcmp(b + 32, d->win_pieces + 2 * w * J, 8 * J)) return bad("pieces of window " + std::to_string(w));
+    int64_t ri = 0, wi = 0;
+    for (int64_t j = 0; j < J; ++j) {
+      if (!d->win_bulk[j]) continue;
+      const sgb_group &G = d->groups[u.g0 + j];
+      const int64_t cnt = d->win_pieces[2 * (w * J + j) + 1];
+      for (int s2 = 0; s2 < G.n_slots; ++s2, ++ri) {
+        uint16_t ro;
+        std::memcpy(&ro, b + roff_at + 2 * ri, 2);
+        if (cnt && ro + cnt > xl) return bad("run offset of window " + std::to_string(w));
+      }
+      for (int r2 = 0; r2 < G.n_roots; ++r2, ++wi) {
+        uint16_t wo;
+        std::memcpy(&wo, b + woff_at + 2 * wi, 2);
+        if (cnt && wo + cnt > nwp) return bad("position offset of window " + std::to_string(w));
+      }
+    }
+    for (int64_t q = 0; q < nwp; ++q) {
+      uint16_t o;
+      std::memcpy(&o, b + wpos_at + 2 * q, 2);
+      if (o != 0xFFFFu && o >= len) return bad("window position of window " + std::to_string(w));
+    }
+    for (int64_t c = 0; c < nc; ++c) {
+      uint32_t cs;
+      uint16_t cp;
+      std::memcpy(&cs, b + csrc_at + 4 * c, 4);
+      std::memcpy(&cp, b + cpos_at + 2 * c, 2);
+      if ((int64_t)cs >= d->value_array_size || cp >= len) return bad("copy of window " + std::to_string(w));
+    }
+  }
+  return 0;
 }
 
 static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
@@ -1086,7 +1191,7 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
   }
   std::vector<int2> btiles;
   int max_wave = -1;
-  bool has_window = false;
+  bool has_window = false, has_bulk = false;
   for (int k = 0; k < d->n_units; ++k) {
     const int64_t *r = d->units + (int64_t)k * U_COUNT;
     Unit u;
@@ -1110,12 +1215,20 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
           d->n_win_pieces != n_win * J || d->n_win_copy != d->n_win_k || u.regs < 8 || has_window)
         return fail(-1, "sgb_plan_create: bad CSR-window unit " + std::to_string(k));
       has_window = true;
+      const bool bulk = u.flags & UNIT_BULK;
+      has_bulk = bulk;
       cudaKernel_t kw;
-      const std::string nw = "sgb_window_u" + std::to_string(k);
+      const std::string nw = (bulk ? "sgb_wbulk_u" : "sgb_window_u") + std::to_string(k);
       SGB_CUDA(cudaLibraryGetKernel(&kw, p->jit_lib, nw.c_str()));
       u.jit = (const void *)kw;
       if (u.regs > 48 * 1024) SGB_CUDA(cudaFuncSetAttribute(u.jit, cudaFuncAttributeMaxDynamicSharedMemorySize, u.regs));
-      const int64_t wmax = u.regs / 8 - 2;  // the window buffer (doubles), alignment slots
+      const int64_t wmax = (bulk ? d->win_bw : u.regs) / 8 - 2;  // the window buffer (doubles), alignment slots
+      if (bulk) {
+        const int rc = check_window_bulk(d, u, n_win, J, (int64_t)smem_max);
+        if (rc) return rc;
+      } else if (u.bs != JIT_BLOCK) {
+        return fail(-1, "sgb_plan_create: bad CSR-window block size");
+      }
       if (d->win_k[0] != 0 || d->win_k[n_win] != d->n_outputs || d->win_copy[0] != 0 || d->win_copy[n_win] != d->n_copy)
         return fail(-1, "sgb_plan_create: CSR windows do not cover the outputs / copies");
       for (int g = u.g0; g < u.g1; ++g)
@@ -1164,7 +1277,11 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
     max_wave = u.wave > max_wave ? u.wave : max_wave;
     {  // persistent grid: resident capacity of the chip, at most one block (warp for SOP) per tile
       int nb = 0;
-      if (window) {
+      if (window && (u.flags & UNIT_BULK)) {  // persistent: each block walks its windows through its ring
+        SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, u.jit, u.bs, (size_t)u.regs));
+        u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
+        if (u.grid > u.t1 - u.t0) u.grid = u.t1 - u.t0;
+      } else if (window) {
         u.grid = u.t1 - u.t0;  // one block per window, dispatched in CSR order
       } else if (jit) {
         SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, u.jit, JIT_BLOCK, (size_t)u.regs));
@@ -1346,6 +1463,18 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       (rc = upload(&p->d_csrc, d->copy_src, d->n_copy)) || (rc = upload(&p->d_cpos, d->copy_pos, d->n_copy)) ||
       (rc = upload(&p->d_fbase, fbase.data(), (int64_t)fbase.size())))
     return rc;
+  if (has_bulk) {
+    if ((rc = upload(&p->d_wmeta, d->win_meta, d->n_win_meta)) ||
+        (rc = upload(&p->d_wmeta_off, d->win_meta_off, d->n_win_k)) ||
+        (rc = upload(&p->d_wiv, reinterpret_cast<const uint2 *>(d->win_iv), d->n_win_iv)) ||
+        (rc = upload(&p->d_wiv_off, d->win_iv_off, d->n_win_k)))
+      return rc;
+    p->wb_ring = d->win_ring;
+    p->wb_meta = d->win_slot_meta;
+    p->wb_x = d->win_slot_x;
+    p->wb_bw = d->win_bw;
+  }
+  p->vas_slots = has_bulk ? d->value_array_size + (d->value_array_size & 1) : d->value_array_size;
   p->T = Tables{p->d_groups, p->d_tape, p->d_imm, p->d_sop, p->d_scol, p->d_sdel, p->d_pos,
                 p->d_con, p->d_cbase, p->d_coff, p->d_obase, p->d_ooff, p->d_opos32, p->d_fbase};
   return 0;
@@ -1423,6 +1552,8 @@ int sgb_run_wave(sgb_plan *p, double *x, double *out, int wave, void *stream) {
   if (!csr && p->csr_layout) return fail(-2, "sgb_run_wave: plan uses the CSR layout (value mode unavailable)");
   if (wave < 0 || wave >= sgb_plan_waves(p, csr)) return fail(-1, "sgb_run_wave: wave out of range");
   if (csr && p->n_out == 0) return 0;
+  if (csr && p->wb_ring && (reinterpret_cast<uintptr_t>(x) & 15))
+    return fail(-1, "sgb_run_wave: the bulk CSR-window feed needs a 16-byte aligned value array");
   std::lock_guard<std::mutex> lk(p->run_mu);
   if (csr && !p->direct_csr && wave == p->n_waves) {  // the output gather
     int rc = launch_gather(p, x, 1, 1, false, out, 1, (cudaStream_t)stream);
@@ -1445,6 +1576,8 @@ int sgb_run_values(sgb_plan *p, double *x, void *stream) {
 int sgb_run_csr(sgb_plan *p, double *x, double *out, void *stream) {
   if (!p || (!x && p->vas) || (!out && p->n_out)) return fail(-1, "sgb_run_csr: null argument");
   if (!p->n_out) return 0;
+  if (p->wb_ring && (reinterpret_cast<uintptr_t>(x) & 15))
+    return fail(-1, "sgb_run_csr: the bulk CSR-window feed needs a 16-byte aligned value array");
   return launch_all(p, x, 1, 1, false, out, 1, true, (cudaStream_t)stream);
 }
 
@@ -1509,7 +1642,7 @@ static int ensure_ws(sgb_plan *p) {
   SGB_CUDA(cudaSetDevice(p->device));
   if (!p->ws_stream) SGB_CUDA(cudaStreamCreateWithFlags(&p->ws_stream, cudaStreamNonBlocking));
   if (!p->d_x && p->vas) {
-    SGB_CUDA(cudaMalloc((void **)&p->d_x, sizeof(double) * (size_t)p->vas));
+    SGB_CUDA(cudaMalloc((void **)&p->d_x, sizeof(double) * (size_t)p->vas_slots));
     // never-written slots (padding, reads before writes) read as zero (codegen.py:419)
     SGB_CUDA(cudaMemset(p->d_x, 0, sizeof(double) * (size_t)p->vas));
     SGB_CUDA(cudaDeviceSynchronize());  // the non-blocking ws_stream does not order after the legacy stream
@@ -1571,7 +1704,7 @@ int sgb_run_outputs_host_many(sgb_plan *p, int64_t n_sets, const double *inputs,
   if (!p->h2d_stream) SGB_CUDA(cudaStreamCreateWithFlags(&p->h2d_stream, cudaStreamNonBlocking));
   if (!p->d2h_stream) SGB_CUDA(cudaStreamCreateWithFlags(&p->d2h_stream, cudaStreamNonBlocking));
   if (n_sets > 1 && !p->d_x2 && p->vas) {
-    SGB_CUDA(cudaMalloc((void **)&p->d_x2, sizeof(double) * (size_t)p->vas));
+    SGB_CUDA(cudaMalloc((void **)&p->d_x2, sizeof(double) * (size_t)p->vas_slots));
     // zeroed on the evaluation stream, so ordered before set 1 evaluates (codegen.py:419); only
     // [n_in, vas): set 1's inputs land in [0, n_in) on the H2D stream, unordered with this memset
     if (p->vas > p->n_in)

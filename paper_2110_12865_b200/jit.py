@@ -510,11 +510,207 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
     return "\n".join(out)
 
 
+_WBULK_HELPERS = r"""
+#ifndef SGB_WBULK_HELPERS
+#define SGB_WBULK_HELPERS
+__device__ __forceinline__ u32 sgb_smem(const void *p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void sgb_mbar_init(u64 *b, u32 n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sgb_smem(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void sgb_mbar_expect(u64 *b, u32 bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sgb_smem(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void sgb_mbar_arrive(u64 *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sgb_smem(b)) : "memory");
+}
+__device__ __forceinline__ void sgb_mbar_wait(u64 *b, u32 parity) {
+  asm volatile("{\n .reg .pred P1;\n LAB_WAIT:\n mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+               " @P1 bra DONE;\n bra LAB_WAIT;\n DONE:\n }" ::"r"(sgb_smem(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void sgb_bulk_g2s(void *dst, const void *src, u32 bytes, u64 *b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(sgb_smem(dst)), "l"(src), "r"(bytes), "r"(sgb_smem(b)) : "memory");
+}
+__device__ __forceinline__ void sgb_bar_consumers(u32 n) { asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory"); }
+#endif
+"""
+
+
+def _window_chunks(dp, g0: int, members: list, tapes: dict, imms: dict, threads: int) -> list[str]:
+    """Members evaluated from the value array (global loads), chunked so every thread has at
+    most WINDOW_LOADS loads in flight: a chunk's loads (operands + window positions) are all
+    issued before its computes.  Member j's piece is ``sp[j]``; results go to ``bw[wpos]``."""
+    chunks, cur, width = [], [], 0
+    for gi in members:
+        rec = dp.groups[gi]
+        _check_stores(tapes[gi], int(rec["n_roots"]), gi)
+        wdt = max(1, int(rec["n_slots"]) + int(rec["n_const"]))
+        if cur and width + wdt > WINDOW_LOADS:
+            chunks.append(cur)
+            cur, width = [], 0
+        cur.append(gi)
+        width += wdt
+    if cur:
+        chunks.append(cur)
+    out = []
+    for chunk in chunks:
+        cmax = "0"
+        for gi in chunk:
+            cmax = f"max({cmax}, sp[{gi - g0}].y)"
+        out.append(f"    for (int c0 = 0, cmax_ = {cmax}; c0 < cmax_; c0 += {threads}) {{")
+        loads, comps = [], []
+        for gi in chunk:
+            j = gi - g0
+            out.append(f"      const bool ok_{j} = c0 + tid < sp[{j}].y;")
+            out.append(f"      const u32 i_{j} = ok_{j} ? (u32)(sp[{j}].x + c0 + tid) : 0u;")
+            ld, cp = group_parts(dp, gi, tapes[gi], imms[gi], iv=f"i_{j}", sfx=f"_{j}", window=True,
+                                 guard=f"ok_{j}")
+            loads += ld
+            comps += cp
+        out += ["      " + ln for ln in loads + comps]
+        out.append("    }")
+    return out
+
+
+def _window_writeout(threads: int) -> list[str]:
+    """The assembled window buf[head_ ..] -> out[k0 ..]: 16-byte shared loads and streaming stores
+    (out + k0 - head_ is 16-byte aligned; the pair straddling k0 writes its second half)."""
+    return ["    {",
+            "      const u32 tot_ = len_ + head_;",
+            "      double2 *o2 = reinterpret_cast<double2 *>(out + k0 - head_);",
+            "      const double2 *b2 = reinterpret_cast<const double2 *>(buf);",
+            f"      for (u32 q = tid; q < (tot_ >> 1); q += {threads}) {{",
+            "        const double2 v_ = b2[q];",
+            "        if (q == 0 && head_) __stcs(out + k0, v_.y); else __stcs(o2 + q, v_);",
+            "      }",
+            "      if (tid == 0 && (tot_ & 1u)) __stcs(out + k0 + len_ - 1, buf[tot_ - 1]);",
+            "    }"]
+
+
+def wbulk_source(dp, u: int, tapes: dict, imms: dict) -> str:
+    """Bulk-fed CSR-window kernel of unit ``u`` (lower.WindowBulk): persistent blocks of
+    WBULK_CONSUMERS consumer threads + one producer warp; block b walks windows b, b + grid, ...
+
+    The producer thread copies each window's consumer blob and its merged value-array intervals
+    into the next slot of a shared-memory ring with ``cp.async.bulk`` (TMA engine, completion
+    counted on the slot's ``full`` mbarrier) as soon as the consumers have released that slot
+    (``empty`` mbarrier), so the copies of the next windows run while the consumers evaluate this
+    one.  The consumers issue the window's copy gathers first, evaluate the bulk members from the
+    ring (operands ``X[run offset + t]``, window positions from the blob), the other members from
+    the value array (chunked loads, as window_source), store the copies, release the slot and
+    write the window out with 16-byte streaming stores.  Same arithmetic as every other path.
+    """
+    wb = dp.wbulk
+    unit = dp.unit(u)
+    g0, g1 = unit["group_begin"], unit["group_end"]
+    CT = L.WBULK_CONSUMERS
+    bulk = set(wb.members)
+    out = [_WBULK_HELPERS,
+           f'extern "C" __global__ void __launch_bounds__({CT + 32}, 1) sgb_wbulk_u{u}(',
+           "    Tables T, const unsigned char *meta, const i64 *meta_off, const uint2 *iv, const i64 *iv_off,",
+           "    i64 n_win, const double *x, double *out, i64 ring, i64 slot_meta, i64 slot_x, i64 bwb) {",
+           "  extern __shared__ __align__(128) unsigned char smem_[];",
+           "  __shared__ __align__(8) u64 full_[8], empty_[8];",
+           "  const int tid = threadIdx.x;",
+           "  double *buf = reinterpret_cast<double *>(smem_);",
+           "  unsigned char *ring_ = smem_ + bwb;",
+           "  const i64 slot = slot_meta + slot_x;",
+           "  const u32 R = (u32)ring;",
+           "  if (tid == 0) {",
+           "    for (u32 r = 0; r < R; ++r) { sgb_mbar_init(&full_[r], 1); sgb_mbar_init(&empty_[r], 1); }",
+           '    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");',
+           "  }",
+           "  __syncthreads();",
+           f"  if (tid >= {CT}) {{  // producer warp: one thread issues the bulk copies",
+           f"    if (tid == {CT}) {{",
+           "      u32 q = 0;",
+           "      for (i64 w = blockIdx.x; w < n_win; w += gridDim.x, ++q) {",
+           "        const u32 s = q % R;",
+           "        if (q >= R) sgb_mbar_wait(&empty_[s], ((q / R) - 1u) & 1u);",
+           "        const i64 m0 = __ldg(meta_off + w), m1 = __ldg(meta_off + w + 1);",
+           "        const i64 v0 = __ldg(iv_off + w), v1 = __ldg(iv_off + w + 1);",
+           "        const u32 xl = __ldg(reinterpret_cast<const u32 *>(meta + m0) + 7);",
+           "        unsigned char *sm = ring_ + (i64)s * slot;",
+           "        sgb_mbar_expect(&full_[s], (u32)(m1 - m0) + 8u * xl);",
+           "        sgb_bulk_g2s(sm, meta + m0, (u32)(m1 - m0), &full_[s]);",
+           "        u32 dst = 0;",
+           "        for (i64 v = v0; v < v1; ++v) {",
+           "          const uint2 e = __ldg(iv + v);",
+           "          sgb_bulk_g2s(sm + slot_meta + 8u * dst, x + e.x, 8u * e.y, &full_[s]);",
+           "          dst += e.y;",
+           "        }",
+           "      }",
+           "    }",
+           "    return;",
+           "  }",
+           "  u32 q = 0;",
+           "  for (i64 w = blockIdx.x; w < n_win; w += gridDim.x, ++q) {",
+           "    const u32 s = q % R;",
+           "    const unsigned char *sm = ring_ + (i64)s * slot;",
+           "    sgb_mbar_wait(&full_[s], (q / R) & 1u);",
+           "    const u32 *hd_ = reinterpret_cast<const u32 *>(sm);",
+           "    const u32 nc_ = hd_[0], len_ = hd_[3];",
+           "    const i64 k0 = *reinterpret_cast<const i64 *>(sm + 16);",
+           "    const int2 *sp = reinterpret_cast<const int2 *>(sm + 32);",
+           f"    const u16 *roff = reinterpret_cast<const u16 *>(sm + {wb.roff_at});",
+           f"    const u16 *woff = reinterpret_cast<const u16 *>(sm + {wb.woff_at});",
+           f"    const u16 *wps = reinterpret_cast<const u16 *>(sm + {wb.wpos_at});",
+           "    const u32 *csrc = reinterpret_cast<const u32 *>(sm + hd_[1]);",
+           "    const u16 *cpos = reinterpret_cast<const u16 *>(sm + hd_[2]);",
+           "    const double *X = reinterpret_cast<const double *>(sm + slot_meta);",
+           "    const u32 head_ = (u32)((reinterpret_cast<u64>(out + k0) >> 3) & 1ull);",
+           "    double *bw = buf + head_;"]
+    U = COPY_UNROLL
+    for q in range(U):  # first batch of copies: gathers in flight while the members evaluate
+        out.append(f"    const bool cq{q} = tid + {q * CT}u < nc_;")
+        out.append(f"    const u16 cp{q} = cq{q} ? cpos[tid + {q * CT}u] : (u16)0;")
+        out.append(f"    const double cv{q} = cq{q} ? __ldg(x + csrc[tid + {q * CT}u]) : 0.0;")
+    ro = wo = 0
+    for j in range(g1 - g0):
+        gi = g0 + j
+        if j not in bulk:
+            continue
+        rec = dp.groups[gi]
+        S, R_ = int(rec["n_slots"]), int(rec["n_roots"])
+        _check_stores(tapes[gi], R_, gi)
+        _, comps = group_parts(dp, gi, tapes[gi], imms[gi], iv="t_", sfx=f"_{j}", window=True)
+        out.append(f"    for (int c0 = 0, n_ = sp[{j}].y; c0 < n_; c0 += {CT}) {{  // bulk member {j}")
+        out.append("      const int t_ = c0 + tid;")
+        out.append("      const bool ok_ = t_ < n_;")
+        for s_ in range(S):
+            out.append(f"      const double s{s_}_{j} = ok_ ? X[roff[{ro + s_}] + t_] : 0.0;")
+        for r_ in range(R_):
+            out.append(f"      const u16 wp{r_}_{j} = ok_ ? wps[woff[{wo + r_}] + t_] : (u16)0xFFFF;")
+        out += ["      " + ln for ln in comps]
+        out.append("    }")
+        ro += S
+        wo += R_
+    out += _window_chunks(dp, g0, [g0 + j for j in range(g1 - g0) if j not in bulk], tapes, imms, CT)
+    out += [f"    if (cq{q}) bw[cp{q}] = cv{q};" for q in range(U)]
+    out += [f"    for (u32 c = tid + {U * CT}u; c < nc_; c += {U * CT}u) {{"]
+    for q in range(U):
+        out.append(f"      const bool dq{q} = c + {q * CT}u < nc_;")
+        out.append(f"      const u16 dp{q} = dq{q} ? cpos[c + {q * CT}u] : (u16)0;")
+        out.append(f"      const double dv{q} = dq{q} ? __ldg(x + csrc[c + {q * CT}u]) : 0.0;")
+    out += [f"      if (dq{q}) bw[dp{q}] = dv{q};" for q in range(U)]
+    out += ["    }",
+            f"    sgb_bar_consumers({CT});",
+            "    if (tid == 0) sgb_mbar_arrive(&empty_[s]);  // every read of the slot is done"]
+    out += _window_writeout(CT)
+    out += [f"    sgb_bar_consumers({CT});  // the window buffer is free again",
+            "  }",
+            "}",
+            ""]
+    return "\n".join(out)
+
+
 def specialise(dp, tapes: dict, imms: dict, units: list[int]) -> tuple[bytes, str]:
     """Compile the given tape units of a lowered plan; returns (cubin, source)."""
     parts = []
     for u in units:
-        if dp.unit(u)["flags"] & L.UNIT_WINDOW:
+        if dp.unit(u)["flags"] & L.UNIT_BULK:
+            parts.append(wbulk_source(dp, u, tapes, imms))
+        elif dp.unit(u)["flags"] & L.UNIT_WINDOW:
             parts.append(window_source(dp, u, tapes, imms))
         else:
             parts.append(unit_source(dp, u, tapes, imms))

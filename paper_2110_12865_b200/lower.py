@@ -55,6 +55,7 @@ STORE_ROOTS_EARLY = False  # roots stored as soon as computed (True) or at the e
 UNIT_JIT = 2  # tape unit compiled to straight-line code (jit.py), one instance per thread
 UNIT_VALUE_ONLY = 4  # value-mode twin of a CSR-window unit (skipped by sgb_run_csr)
 UNIT_WINDOW = 8  # CSR windows: each block assembles one window of consecutive outputs in shared memory
+UNIT_BULK = 16  # CSR-window unit fed by bulk copies into a shared-memory ring (WindowBulk, jit.wbulk_source)
 JIT_BLOCK = 256
 CHUNK = 32  # instances per compressed-index chunk (one warp in single-set mode)
 NONE32 = 0xFFFFFFFF
@@ -125,6 +126,7 @@ class DevicePlanArrays:
     jit_cubin: bytes = b""  # specialised tape units (UNIT_JIT): kernels sgb_tape_u<unit>, see jit.py
     jit_source: str = ""
     windows: "CsrWindows" = None  # CSR windows of the last wave (the window unit's pieces and copies)
+    wbulk: "WindowBulk" = None  # bulk-copy feed of the window unit (UNIT_BULK), see window_bulk
     window_members: list = field(default_factory=list)  # plan kernels the window unit evaluates
     window_units: list = field(default_factory=list)
     jit_tapes: dict = field(default_factory=dict)  # packed group -> register tape of specialised units
@@ -890,6 +892,194 @@ def _csr_windows(member_opos: list, n_out: int, copy_k: np.ndarray, copy_addr: n
                       copy_pos=copy_pos)
 
 
+WBULK_GAP = 16  # value-array runs closer than this many doubles merge into one bulk copy
+WBULK_SMEM = 227 * 1024  # dynamic shared memory of one window block (one block per SM)
+WBULK_RING = (2, 4)  # ring depth range (windows in flight per block)
+WBULK_CONSUMERS = 256  # consumer threads of a bulk window block (one instance each per pass)
+WBULK_THREADS = WBULK_CONSUMERS + 32  # + one producer warp
+
+
+@dataclass
+class WindowBulk:
+    """Bulk-copy feed of a CSR-window unit (jit.wbulk_source).
+
+    A member whose every slot reads a stride-1 stream of the value array (``x[base_s + i]``:
+    affine column 0 plus coherent deltas or affine columns, no constants) is *bulk*: in window
+    w its piece [i0, i0 + n) reads the runs ``x[base_s + i0 : base_s + i0 + n)``.  Per window
+    the runs of all bulk members are merged into intervals (``iv``: first element, element
+    count, both even, so every copy is 16-byte aligned and a multiple of 16 bytes) that one
+    producer thread copies with ``cp.async.bulk`` into the x area of a ring slot, together with
+    the window's consumer blob (``meta``); the consumer threads evaluate the bulk members from
+    shared memory.  Blob layout (byte offsets, 16-byte aligned sections)::
+
+        0   u32 n_copy, u32 copy_src offset, u32 copy_pos offset, u32 window length,
+            i64 first output k0, u32 window positions, u32 x-area elements
+        32  int2 pieces[J]                       (first instance, count) of every member
+        roff_at  u16 run offset[NR]              x-area element of x[base_s + i0], bulk (member, slot)
+        woff_at  u16 wpos offset[NW]             first window position of each bulk (member, root)
+        wpos_at  u16 wpos[...]                   window positions of the bulk pieces
+        copy_src u32[n_copy], copy_pos u16[n_copy]
+    """
+
+    members: list  # member indices j (group group_begin + j) fed from the ring
+    bases: list  # per bulk member: value-array base of each slot's stream
+    meta: np.ndarray  # uint8: the consumer blobs of all windows
+    meta_off: np.ndarray  # int64 [n_win + 1]
+    iv: np.ndarray  # uint32 [n_iv, 2]
+    iv_off: np.ndarray  # int64 [n_win + 1]
+    ring: int  # ring slots (windows in flight per block)
+    slot_meta: int  # bytes of a slot's blob area (128-byte multiple)
+    slot_x: int  # bytes of a slot's x area (128-byte multiple)
+    bw: int  # bytes of the window buffer (128-byte multiple)
+    roff_at: int
+    woff_at: int
+    wpos_at: int
+
+    @property
+    def smem(self) -> int:
+        return self.bw + self.ring * (self.slot_meta + self.slot_x)
+
+
+def _a16(v: int) -> int:
+    return (int(v) + 15) & ~15
+
+
+def _a128(v: int) -> int:
+    return (int(v) + 127) & ~127
+
+
+def window_bulk(dp, u: int, windows: "CsrWindows", gap: int | None = None) -> WindowBulk | None:
+    """The bulk feed of window unit ``u`` of a lowered plan, or None (no bulk member, or the
+    ring does not fit in shared memory)."""
+    from . import jit as _jit
+
+    gap = WBULK_GAP if gap is None else gap
+
+    r = dp.unit(u)
+    g0, g1 = r["group_begin"], r["group_end"]
+    J = g1 - g0
+    vas = int(dp.value_array_size)  # intervals end at most at vas rounded up to even (value_slots)
+    members, bases = [], []
+    for j in range(J):
+        rec = dp.groups[g0 + j]
+        f = int(rec["flags"])
+        S, K = int(rec["n_slots"]), int(rec["n_const"])
+        if f & FLAG_INTERLEAVED or K or not S or not f & FLAG_WPOS16:
+            continue
+        a0 = _jit._affine(dp, rec, 0)
+        if a0 is None or a0[1] != 1:
+            continue
+        cols = dp.slot_col[rec["slot_off"]: rec["slot_off"] + S]
+        dels = dp.slot_delta[rec["slot_off"]: rec["slot_off"] + S]
+        bs = []
+        for s_ in range(S):
+            c = int(cols[s_])
+            if c < 0:
+                bs.append(a0[0] + int(dels[s_]))
+            elif c == 0:
+                bs.append(a0[0])
+            else:
+                a = _jit._affine(dp, rec, c)
+                if a is None or a[1] != 1:
+                    bs = None
+                    break
+                bs.append(a[0])
+        if bs is not None:
+            members.append(j)
+            bases.append(bs)
+    if not members:
+        return None
+    P = windows.pieces.astype(np.int64)
+    n_win = P.shape[0]
+    NR = sum(len(b) for b in bases)
+    NW = sum(int(dp.groups[g0 + j]["n_roots"]) for j in members)
+    # every (window, bulk member, slot) run, merged per window into aligned intervals
+    W, ST, LN, RID = [], [], [], []
+    rid = 0
+    for j, bs in zip(members, bases):
+        for b in bs:
+            W.append(np.arange(n_win, dtype=np.int64))
+            ST.append(b + P[:, j, 0])
+            LN.append(P[:, j, 1])
+            RID.append(np.full(n_win, rid, np.int64))
+            rid += 1
+    W, ST, LN, RID = (np.concatenate(a) for a in (W, ST, LN, RID))
+    keep = LN > 0
+    W, ST, LN, RID = W[keep], ST[keep], LN[keep], RID[keep]
+    if ST.size and (ST.min() < 0 or (ST + LN).max() > vas):
+        raise AssertionError("window_bulk: a run leaves the value array")
+    order = np.lexsort((ST, W))
+    W, ST, LN, RID = W[order], ST[order], LN[order], RID[order]
+    big = vas + 4 * gap + 4
+    en = ST + LN
+    cm = np.maximum.accumulate(en + W * big) if ST.size else en
+    new = np.ones(ST.size, bool)
+    new[1:] = ST[1:] + W[1:] * big > cm[:-1] + gap
+    ivid = np.cumsum(new) - 1
+    heads = np.flatnonzero(new)
+    iv_w = W[heads]
+    iv_s = ST[heads] & ~1
+    iv_e = (np.maximum.reduceat(en, heads) + 1) & ~1 if heads.size else np.zeros(0, np.int64)
+    iv_n = iv_e - iv_s
+    iv_off = np.searchsorted(iv_w, np.arange(n_win + 1)).astype(np.int64)
+    excl = np.cumsum(iv_n) - iv_n
+    dst = excl - excl[np.minimum(iv_off[iv_w], max(excl.size - 1, 0))] if excl.size else excl
+    xlen = np.bincount(iv_w, weights=iv_n, minlength=n_win).astype(np.int64)
+    roff = np.zeros((n_win, NR), np.int64)
+    roff[W, RID] = dst[ivid] + (ST - iv_s[ivid])
+    if roff.size and int(roff.max()) > 0xFFFF or (xlen.size and int(xlen.max()) > 0xFFFF):
+        return None
+    # per window consumer blobs
+    roff_at = 32 + 8 * J
+    woff_at = roff_at + 2 * NR
+    wpos_at = _a16(woff_at + 2 * NW)
+    k = windows.k
+    blobs, offs = [], [0]
+    for w in range(n_win):
+        wp_parts, woff = [], []
+        pos = 0
+        for j in members:
+            i0, n = int(P[w, j, 0]), int(P[w, j, 1])
+            wpj = windows.wpos[j]
+            for r_ in range(wpj.shape[0]):
+                woff.append(pos)
+                if n:
+                    wp_parts.append(wpj[r_, i0:i0 + n])
+                    pos += n
+        c0, c1 = int(windows.copy_off[w]), int(windows.copy_off[w + 1])
+        nc = c1 - c0
+        csrc_at = _a16(wpos_at + 2 * pos)
+        cpos_at = _a16(csrc_at + 4 * nc)
+        size = _a16(cpos_at + 2 * nc)
+        b = np.zeros(size, np.uint8)
+        b[0:16].view(np.uint32)[:] = (nc, csrc_at, cpos_at, int(k[w + 1] - k[w]))
+        b[16:24].view(np.int64)[0] = int(k[w])
+        b[24:32].view(np.uint32)[:] = (pos, int(xlen[w]))
+        b[32:32 + 8 * J].view(np.int32)[:] = windows.pieces[w].reshape(-1)
+        b[roff_at:woff_at].view(np.uint16)[:] = roff[w]
+        if NW:
+            b[woff_at:woff_at + 2 * NW].view(np.uint16)[:] = np.asarray(woff, np.uint16)
+        if pos:
+            b[wpos_at:wpos_at + 2 * pos].view(np.uint16)[:] = np.concatenate(wp_parts)
+        if nc:
+            b[csrc_at:csrc_at + 4 * nc].view(np.uint32)[:] = windows.copy_src[c0:c1]
+            b[cpos_at:cpos_at + 2 * nc].view(np.uint16)[:] = windows.copy_pos[c0:c1]
+        blobs.append(b)
+        offs.append(offs[-1] + size)
+    meta = np.concatenate(blobs) if blobs else np.zeros(0, np.uint8)
+    slot_meta = _a128(max((b.size for b in blobs), default=16))
+    slot_x = _a128(8 * max(int(xlen.max(initial=0)), 2))
+    bw = _a128(8 * (int(np.diff(k).max(initial=0)) + 2))
+    ring = (WBULK_SMEM - bw) // (slot_meta + slot_x)
+    if ring < WBULK_RING[0]:
+        return None
+    ring = min(ring, WBULK_RING[1])
+    iv = np.stack([iv_s, iv_n], axis=1).astype(np.uint32) if iv_s.size else np.zeros((0, 2), np.uint32)
+    return WindowBulk(members=members, bases=bases, meta=meta, meta_off=np.asarray(offs, np.int64), iv=iv,
+                      iv_off=iv_off, ring=int(ring), slot_meta=slot_meta, slot_x=slot_x, bw=bw,
+                      roff_at=roff_at, woff_at=woff_at, wpos_at=wpos_at)
+
+
 def jit_vec(groups, sel) -> int:
     """Instances per thread of a specialised unit: all of them keep their loads in flight
     together, so small templates take 4, mid-size 2, big element templates 1."""
@@ -1058,7 +1248,7 @@ JIT_MAX_WAVE_GROUPS = 48  # ...unless they share a wave of at most this many gro
 def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = None,
                jit: bool | None = None, csr_window: bool | None = None,
                jit_min_n: int | None = None, relayout: str | bool | None = None,
-               jit_compile: bool = True) -> DevicePlanArrays:
+               jit_compile: bool = True, wbulk: bool | None = None) -> DevicePlanArrays:
     """ExecutionPlan -> device plan.
 
     ``direct_csr``: output groups store their CSR values through output-position
@@ -1420,6 +1610,17 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     dp.window_members = list(window) if window is not None else []
     dp.window_units = window_units
     dp.jit_tapes, dp.jit_imms = jit_tapes, jit_imms
+    dp.wbulk = None
+    if wbulk is None:
+        wbulk = os.environ.get("SGB_WBULK", "1") != "0"
+    if windows is not None and window_units and wbulk:  # feed the window unit with bulk copies
+        uw = window_units[0][0]
+        wb = window_bulk(dp, uw, windows)
+        if wb is not None:
+            dp.wbulk = wb
+            dp.units[uw, UNIT_FIELDS.index("flags")] |= UNIT_BULK
+            dp.units[uw, UNIT_FIELDS.index("block_size")] = WBULK_THREADS
+            dp.units[uw, UNIT_FIELDS.index("smem_regs")] = wb.smem
     if jit_units and jit_compile:
         from . import jit as _jit
 

@@ -88,6 +88,17 @@ class _Desc(ctypes.Structure):
         ("copy_src", ctypes.c_void_p),
         ("copy_pos", ctypes.c_void_p),
         ("n_copy", ctypes.c_int64),
+        ("win_meta", ctypes.c_void_p),
+        ("n_win_meta", ctypes.c_int64),
+        ("win_meta_off", ctypes.c_void_p),
+        ("win_iv", ctypes.c_void_p),
+        ("n_win_iv", ctypes.c_int64),
+        ("win_iv_off", ctypes.c_void_p),
+        ("win_bulk", ctypes.c_void_p),
+        ("win_ring", ctypes.c_int64),
+        ("win_slot_meta", ctypes.c_int64),
+        ("win_slot_x", ctypes.c_int64),
+        ("win_bw", ctypes.c_int64),
     ]
 
 
@@ -95,7 +106,7 @@ SYMBOLS = (
     "sgb_plan_create", "sgb_plan_destroy", "sgb_run_values", "sgb_run_csr", "sgb_gather_outputs",
     "sgb_sg_run", "sgb_run_outputs_host", "sgb_run_outputs_host_many", "sgb_run_batch", "sgb_run_batch_csr", "sgb_gather_outputs_batch",
     "sgb_plan_waves", "sgb_last_error", "sgb_run_wave", "sgb_plan_units", "sgb_plan_set_tiles",
-    "sgb_plan_set_wave_grid",
+    "sgb_plan_set_wave_grid", "sgb_plan_value_slots",
 )
 
 
@@ -128,6 +139,7 @@ def load_library(path: Path | str | None = None):
             "sgb_plan_units": (i32, [vp, i32]),
             "sgb_plan_set_tiles": (i32, [vp, vp, i64]),
             "sgb_plan_set_wave_grid": (i32, [vp, i32, i32]),
+            "sgb_plan_value_slots": (i64, [vp]),
             "sgb_last_error": (ctypes.c_char_p, []),
         }
         for name, (res, args) in sig.items():
@@ -212,6 +224,17 @@ class DevicePlan:
             csrc=np.ascontiguousarray(wn.copy_src if wn is not None else np.zeros(0), np.uint32),
             cpos=np.ascontiguousarray(wn.copy_pos if wn is not None else np.zeros(0), np.uint16),
         )
+        wb = getattr(lw, "wbulk", None)
+        bulk_flags = np.zeros(wn.pieces.shape[1] if wn is not None else 0, np.int32)
+        if wb is not None:
+            bulk_flags[wb.members] = 1
+        keep.update(
+            wmeta=np.ascontiguousarray(wb.meta if wb is not None else np.zeros(0), np.uint8),
+            wmeta_off=np.ascontiguousarray(wb.meta_off if wb is not None else np.zeros(0), np.int64),
+            wiv=np.ascontiguousarray(wb.iv if wb is not None else np.zeros((0, 2)), np.uint32).reshape(-1, 2),
+            wiv_off=np.ascontiguousarray(wb.iv_off if wb is not None else np.zeros(0), np.int64),
+            wbulk=bulk_flags,
+        )
         d = _Desc(
             value_array_size=self.value_array_size, input_count=self.input_count,
             n_groups=len(keep["groups"]), n_waves=lw.n_waves, n_units=len(keep["units"]),
@@ -231,6 +254,11 @@ class DevicePlan:
             win_k=_ptr(keep["wk"]), n_win_k=keep["wk"].size, win_copy=_ptr(keep["wcopy"]),
             n_win_copy=keep["wcopy"].size, copy_src=_ptr(keep["csrc"]), copy_pos=_ptr(keep["cpos"]),
             n_copy=keep["csrc"].size,
+            win_meta=_ptr(keep["wmeta"]), n_win_meta=keep["wmeta"].size, win_meta_off=_ptr(keep["wmeta_off"]),
+            win_iv=_ptr(keep["wiv"]), n_win_iv=keep["wiv"].shape[0], win_iv_off=_ptr(keep["wiv_off"]),
+            win_bulk=_ptr(keep["wbulk"]),
+            win_ring=wb.ring if wb is not None else 0, win_slot_meta=wb.slot_meta if wb is not None else 0,
+            win_slot_x=wb.slot_x if wb is not None else 0, win_bw=wb.bw if wb is not None else 0,
         )
         torch.cuda.init()
         _check(self._lib.sgb_plan_create(ctypes.byref(d), self.device, ctypes.byref(self._handle)),
@@ -238,6 +266,7 @@ class DevicePlan:
         self.launches = int(self._lib.sgb_plan_waves(self._handle, 0))  # value-mode waves
         self.csr_launches = int(self._lib.sgb_plan_waves(self._handle, 1))  # CSR-mode waves
         self.units = int(self._lib.sgb_plan_units(self._handle, 0))  # kernel launches per evaluation
+        self.value_slots = int(self._lib.sgb_plan_value_slots(self._handle))  # CSR workspace doubles
         self.csr_units = int(self._lib.sgb_plan_units(self._handle, 1))
         self.tile_order = {}  # wave -> (schedule, grid) kept by autotune
         if os.environ.get("SGB_AUTOTUNE", "1") != "0":
@@ -344,11 +373,21 @@ class DevicePlan:
         if not t.is_contiguous() or t.shape[0] != rows:
             raise ValueError(f"{name} must be contiguous with {rows} rows, got {tuple(t.shape)}")
 
+    def _check_workspace(self, x):
+        """CSR-mode value arrays of a plan with a bulk-fed window unit must span value_slots doubles
+        (the 16-byte bulk copies may read one padding slot; DevicePlan.new_values allocates it)."""
+        if self.value_slots > self.value_array_size:
+            span = x.untyped_storage().nbytes() // 8 - x.storage_offset()
+            if span < self.value_slots:
+                raise ValueError(f"x must span {self.value_slots} doubles (sgb_plan_value_slots), got {span}: "
+                                 "allocate it with DevicePlan.new_values")
+
     def new_values(self, inputs=None):
         """Zeroed device value array with ``inputs`` placed at [0, input_count)."""
         import torch
 
-        x = torch.zeros(self.value_array_size, dtype=torch.float64, device=f"cuda:{self.device}")
+        # a bulk-fed window unit may read one padding slot past the value array (sgb_plan_value_slots)
+        x = torch.zeros(self.value_slots, dtype=torch.float64, device=f"cuda:{self.device}")[: self.value_array_size]
         if inputs is not None:
             x[: self.input_count] = torch.as_tensor(inputs, dtype=torch.float64).to(x.device)
         return x
@@ -365,6 +404,7 @@ class DevicePlan:
         import torch
 
         self._check_tensor(x, self.value_array_size, "x")
+        self._check_workspace(x)
         if out is None:
             out = torch.empty(self.n_outputs, dtype=torch.float64, device=x.device)
         self._check_tensor(out, self.n_outputs, "out")
@@ -400,6 +440,8 @@ class DevicePlan:
 
     def run_wave(self, x, wave: int, out=None, stream=None):
         """One dependency wave (profiling / per-launch timing); ``out`` given = CSR mode."""
+        if out is not None:
+            self._check_workspace(x)
         _check(self._lib.sgb_run_wave(self._handle, ctypes.c_void_p(x.data_ptr()),
                                       ctypes.c_void_p(out.data_ptr() if out is not None else 0), int(wave),
                                       _stream_handle(stream)), "sgb_run_wave")

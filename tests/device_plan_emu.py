@@ -195,6 +195,69 @@ def _run_windows(dp, unit, x, out):
         out[k0:k1] = buf
 
 
+def _run_windows_bulk(dp, unit, x, out):
+    """The bulk-fed CSR-window unit (jit.wbulk_source) from its own tables: per window the ring slot
+    is rebuilt from the consumer blob and the value-array intervals (lower.WindowBulk), the bulk
+    members read their operands and window positions from it, the others from the value array."""
+    wb, wn = dp.wbulk, dp.windows
+    g0, g1 = unit["group_begin"], unit["group_end"]
+    J = g1 - g0
+    bulk = set(wb.members)
+    NR = sum(int(dp.groups[g0 + j]["n_slots"]) for j in wb.members)
+    NW = sum(int(dp.groups[g0 + j]["n_roots"]) for j in wb.members)
+    xp = np.concatenate([x, [np.nan]]) if x.size % 2 else x  # the padding slot (sgb_plan_value_slots)
+    for w in range(wn.k.size - 1):
+        blob = wb.meta[int(wb.meta_off[w]): int(wb.meta_off[w + 1])]
+        assert blob.size <= wb.slot_meta
+        nc, csrc_at, cpos_at, ln = (int(v) for v in blob[:16].view(np.uint32))
+        k0 = int(blob[16:24].view(np.int64)[0])
+        nwp, xl = (int(v) for v in blob[24:32].view(np.uint32))
+        assert k0 == int(wn.k[w]) and ln == int(wn.k[w + 1]) - k0
+        sp = blob[32:32 + 8 * J].view(np.int32).reshape(J, 2)
+        ivs = wb.iv[int(wb.iv_off[w]): int(wb.iv_off[w + 1])].astype(np.int64)
+        X = np.concatenate([xp[s_: s_ + n_] for s_, n_ in ivs]) if len(ivs) else np.zeros(0)
+        assert X.size == xl and 8 * xl <= wb.slot_x
+        roff = blob[wb.roff_at: wb.roff_at + 2 * NR].view(np.uint16).astype(np.int64)
+        woff = blob[wb.woff_at: wb.woff_at + 2 * NW].view(np.uint16).astype(np.int64)
+        wps = blob[wb.wpos_at: wb.wpos_at + 2 * nwp].view(np.uint16).astype(np.int64)
+        csrc = blob[csrc_at: csrc_at + 4 * nc].view(np.uint32).astype(np.int64)
+        cpos = blob[cpos_at: cpos_at + 2 * nc].view(np.uint16).astype(np.int64)
+        buf = np.full(ln, np.nan)
+        ro = wo = 0
+        for j in range(J):
+            gi = g0 + j
+            g = dp.groups[gi]
+            a, cnt = int(sp[j, 0]), int(sp[j, 1])
+            S, R = int(g["n_slots"]), int(g["n_roots"])
+            if j in bulk:
+                if cnt:
+                    t = np.arange(cnt)
+                    slots = [X[roff[ro + s_] + t] for s_ in range(S)]
+                    wposs = [wps[woff[wo + r] + t] for r in range(R)]
+
+                    def bstore(g_, r, i_, v, wposs=wposs):
+                        o = wposs[r]
+                        m = o != 0xFFFF
+                        buf[o[m]] = np.asarray(v)[m] if np.ndim(v) else v
+
+                    _reg_tape(dp, gi, g, x, np.arange(a, a + cnt, dtype=np.int64), bstore, slots=slots)
+                ro += S
+                wo += R
+                continue
+            if not cnt:
+                continue
+            n = int(g["n"])
+
+            def wstore(g_, r, i_, v, n=n):
+                o = dp.ooff[int(g_["oo_off"]) + r * n + i_].astype(np.int64)
+                m = o != 0xFFFF
+                buf[o[m]] = np.asarray(v)[m] if np.ndim(v) else v
+
+            _reg_tape(dp, gi, g, x, np.arange(a, a + cnt, dtype=np.int64), wstore)
+        buf[cpos] = x[csrc]
+        out[k0:k0 + ln] = buf
+
+
 def _run(dp, inputs, csr: bool, by_tiles: bool = False):
     x = np.zeros(dp.value_array_size, np.float64)
     x[: dp.input_count] = inputs
@@ -206,6 +269,9 @@ def _run(dp, inputs, csr: bool, by_tiles: bool = False):
         if unit["flags"] & L.UNIT_CSR_ONLY and not csr:
             continue
         if unit["flags"] & L.UNIT_VALUE_ONLY and csr:
+            continue
+        if unit["flags"] & L.UNIT_BULK:
+            _run_windows_bulk(dp, unit, x, out)
             continue
         if unit["flags"] & L.UNIT_WINDOW:
             _run_windows(dp, unit, x, out)
@@ -335,14 +401,15 @@ def _binop(op, A, B, C):
     raise ValueError(op)
 
 
-def _reg_tape(dp, gi, g, x, i, store):
-    """A specialised unit's group: its register tape (lower.compile_tape), as jit.group_parts unrolls it."""
+def _reg_tape(dp, gi, g, x, i, store, slots=None):
+    """A specialised unit's group: its register tape (lower.compile_tape), as jit.group_parts unrolls it.
+    ``slots``: the operand values (a bulk-fed window member reads them from its ring slot)."""
     tape = dp.jit_tapes[gi]
     imms = dp.jit_imms[gi]
     S, K = int(g["n_slots"]), int(g["n_const"])
     R = {}
-    for s_, a in enumerate(_decode_addrs(dp, g, i)):
-        R[s_] = x[a].copy()
+    for s_, a in enumerate(_decode_addrs(dp, g, i) if slots is None else slots):
+        R[s_] = x[a].copy() if slots is None else np.asarray(a, np.float64)
     for k in range(K):
         R[S + k] = _const(dp, g, k, i).copy()
     slow = {0: math.sin, 1: math.cos, 2: math.exp, 3: math.log}

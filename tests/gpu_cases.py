@@ -47,7 +47,8 @@ def lowering_specs(names: list[str]) -> list[tuple[str, tuple]]:
     specs += [(n, (("csr_window", False),)) for n in names]
     specs += [(n, (("csr_window", True),)) for n in WINDOW_CASES]
     specs += [(n, (("direct_csr", True),)) for n in names]
-    specs += [(n, ()) for n in BUILDER_CASES] + [(n, (("relayout", "auto"),)) for n in BUILDER_CASES]
+    specs += [(n, (("relayout", r), ("wbulk", b))) for n in BUILDER_CASES for r in (False, "auto")
+              for b in (True, False)]
     return specs
 
 

@@ -14,7 +14,7 @@ HDR = Path(__file__).resolve().parent.parent / "include" / "sgb.h"
 
 def declared_functions():
     text = HDR.read_text()
-    return sorted(set(re.findall(r"^\s*(?:int|void|const char \*)\s*\*?\s*(sgb_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int|int64_t|void|const char \*)\s*\*?\s*(sgb_\w+)\s*\(", text, re.M)))
 
 
 def test_header_declares_the_runtime_symbols():

@@ -57,23 +57,33 @@ def test_compile_plan_values(golden):
 
 @pytest.mark.parametrize("name", sorted(BUILDER_CASES))
 @pytest.mark.parametrize("relayout", [False, "auto"])
-def test_builder_plans_default_lowering(name, relayout):
+@pytest.mark.parametrize("wbulk", [True, False])
+def test_builder_plans_default_lowering(name, relayout, wbulk):
     """The config builders' plans at small sizes through the default lowering (CSR windows on the mesh
-    plans, the CSR layout on the FEM plan): run_csr, the captured graph and the host path == the oracle,
-    bit for bit."""
+    plans -- bulk-fed through the shared-memory ring or not --, the CSR layout on the FEM plan):
+    run_csr, every wave one at a time, the captured graph and the host path == the oracle, bit for bit."""
     import torch
 
     from oracle import oracle
     from paper_2110_12865_b200 import DevicePlan, lower_plan
 
     plan, inputs = builder_plan(name)
-    dp = DevicePlan(plan, lowered=lower_plan(plan, relayout=relayout))
+    dp = DevicePlan(plan, lowered=lower_plan(plan, relayout=relayout, wbulk=wbulk))
+    if name.startswith("lmlt"):
+        assert (dp.lowered.wbulk is not None) == wbulk
+        assert dp.value_slots == dp.value_array_size + (dp.value_array_size % 2 if wbulk else 0)
     want = oracle.run_outputs(plan, inputs)
     x = dp.new_values(inputs)
     out = dp.run_csr(x)
     torch.cuda.synchronize()
     assert np.array_equal(bits(out.cpu().numpy()), bits(want))
     assert np.array_equal(bits(dp.run_outputs_host(inputs)), bits(want))
+    out.fill_(float("nan"))
+    x = dp.new_values(inputs)
+    for w in range(dp.csr_launches):
+        dp.run_wave(x, w, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(out.cpu().numpy()), bits(want))
     graph = dp.capture_csr(dp.new_values(inputs), out)
     out.fill_(float("nan"))
     graph.replay()

@@ -26,11 +26,15 @@ def test_emulated_csr_mode_matches_reference_outputs(golden):
     assert np.array_equal(bits(out), bits(golden.outputs))
 
 
+@pytest.mark.parametrize("wbulk", [False, True])
 @pytest.mark.parametrize("jit_min_n", [None, 0])
-def test_emulated_csr_windows_match_reference_outputs(golden, jit_min_n):
-    """CSR windows (lower._csr_windows, jit.window_source): every output lands exactly once, from its
-    member's piece or the window's copy list, bit for bit; plans that do not qualify keep the gather."""
-    dp = lower_plan(golden.plan, csr_window=True, jit_min_n=jit_min_n, jit_compile=False)
+def test_emulated_csr_windows_match_reference_outputs(golden, jit_min_n, wbulk):
+    """CSR windows (lower._csr_windows, jit.window_source / wbulk_source): every output lands exactly
+    once, from its member's piece or the window's copy list, bit for bit; with the bulk feed the
+    emulator rebuilds every ring slot from the blobs and intervals (lower.WindowBulk); plans that do
+    not qualify keep the gather."""
+    dp = lower_plan(golden.plan, csr_window=True, jit_min_n=jit_min_n, jit_compile=False, wbulk=wbulk)
+    assert (dp.wbulk is not None) <= wbulk
     out = emu.run_csr(dp, golden.inputs)
     want = golden.outputs
     if golden.exact:
@@ -66,12 +70,19 @@ def test_csr_windows_on_the_c2_builder_plan():
     from oracle import oracle
 
     plan, _, _ = build_lmlt_plan(40)
-    dp = lower_plan(plan, csr_window=True, jit_compile=False)
-    assert dp.windows is not None and len(dp.window_units) == 1
-    cnt = dp.windows.pieces[:, :, 1]
-    assert np.median(cnt.max(axis=1)) <= 256
     ins = lmlt_inputs(40, seed=3)
-    assert np.array_equal(bits(emu.run_csr(dp, ins)), bits(oracle.run_outputs(plan, ins)))
+    want = bits(oracle.run_outputs(plan, ins))
+    for wbulk in (False, True):
+        dp = lower_plan(plan, csr_window=True, jit_compile=False, wbulk=wbulk)
+        assert dp.windows is not None and len(dp.window_units) == 1
+        cnt = dp.windows.pieces[:, :, 1]
+        assert np.median(cnt.max(axis=1)) <= 256
+        assert np.array_equal(bits(emu.run_csr(dp, ins)), want)
+        if wbulk:  # every bulk member's runs are merged into aligned intervals of the value array
+            wb = dp.wbulk
+            assert wb is not None and len(wb.members) >= 10
+            assert np.all(wb.iv % 2 == 0) and np.all(wb.iv[:, 1] > 0)
+            assert np.all(wb.meta_off % 16 == 0) and wb.smem <= L.WBULK_SMEM
 
 
 def test_waves_respect_producers(golden):

@@ -30,11 +30,19 @@ def main():
     ins = bench.workload_inputs("c2", ns, 0)
     ref = DevicePlan(plan, lowered=lower_plan(plan, csr_window=False))
     want = ref.run_csr(ref.new_values(ins)).cpu().numpy()
-    variants = [dict(loads=l_, blocks=3, rows=240) for l_ in (24, 32, 40, 48)] * 2
+    variants = [dict(wbulk=False, rows=240, ct=256, smem=227), dict(wbulk=True, rows=240, ct=256, smem=227),
+                dict(wbulk=True, rows=120, ct=128, smem=227), dict(wbulk=True, rows=120, ct=128, smem=113),
+                dict(wbulk=True, rows=240, ct=256, smem=227, gap=64)] * 2
     for v in variants:
-        jit.WINDOW_LOADS, jit.WINDOW_MIN_BLOCKS, lower.WIN_ROWS = v["loads"], v["blocks"], v["rows"]
+        lower.WIN_ROWS = v["rows"]
+        lower.WBULK_CONSUMERS, lower.WBULK_THREADS = v["ct"], v["ct"] + 32
+        lower.WBULK_SMEM = v["smem"] * 1024
+        lower.WBULK_GAP = v.get("gap", 16)
         t0 = time.perf_counter()
-        lw = lower_plan(plan, csr_window=True)
+        lw = lower_plan(plan, csr_window=True, wbulk=v["wbulk"])
+        if lw.wbulk is not None:
+            wb = lw.wbulk
+            v = dict(v, ring=wb.ring, smem_kb=round(wb.smem / 1024, 1), iv=int(wb.iv.shape[0]))
         t_low = time.perf_counter() - t0
         import os
         os.environ["SGB_AUTOTUNE"] = "0"
