@@ -1001,7 +1001,7 @@ static int check_window_bulk(const sgb_plan_desc *d, const Unit &u, int64_t n_wi
       (d->n_win_iv > 0 && !d->win_iv) || d->n_win_iv < 0)
     return bad("missing tables");
   if (d->win_ring < 1 || d->win_ring > 8 || d->win_slot_meta <= 0 || d->win_slot_meta % 128 || d->win_slot_x <= 0 ||
-      d->win_slot_x % 128 || d->win_bw < 128 || d->win_bw % 128 || u.bs != JIT_BLOCK + 32 ||
+      d->win_slot_x % 128 || d->win_bw < 128 || d->win_bw % 128 || u.bs % 32 || u.bs < 64 || u.bs > 1024 ||
       (int64_t)u.regs != d->win_bw + d->win_ring * (d->win_slot_meta + d->win_slot_x) || u.regs > smem_max)
     return bad("ring / block geometry");
   const int64_t vas_even = d->value_array_size + (d->value_array_size & 1);

@@ -520,6 +520,9 @@ __device__ __forceinline__ void sgb_mbar_init(u64 *b, u32 n) {
 __device__ __forceinline__ void sgb_mbar_expect(u64 *b, u32 bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sgb_smem(b)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void sgb_mbar_expect_only(u64 *b, u32 bytes) {
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(sgb_smem(b)), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void sgb_mbar_arrive(u64 *b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sgb_smem(b)) : "memory");
 }
@@ -621,25 +624,34 @@ def wbulk_source(dp, u: int, tapes: dict, imms: dict) -> str:
            '    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");',
            "  }",
            "  __syncthreads();",
-           f"  if (tid >= {CT}) {{  // producer warp: one thread issues the bulk copies",
-           f"    if (tid == {CT}) {{",
-           "      u32 q = 0;",
-           "      for (i64 w = blockIdx.x; w < n_win; w += gridDim.x, ++q) {",
-           "        const u32 s = q % R;",
-           "        if (q >= R) sgb_mbar_wait(&empty_[s], ((q / R) - 1u) & 1u);",
-           "        const i64 m0 = __ldg(meta_off + w), m1 = __ldg(meta_off + w + 1);",
-           "        const i64 v0 = __ldg(iv_off + w), v1 = __ldg(iv_off + w + 1);",
-           "        const u32 xl = __ldg(reinterpret_cast<const u32 *>(meta + m0) + 7);",
-           "        unsigned char *sm = ring_ + (i64)s * slot;",
-           "        sgb_mbar_expect(&full_[s], (u32)(m1 - m0) + 8u * xl);",
-           "        sgb_bulk_g2s(sm, meta + m0, (u32)(m1 - m0), &full_[s]);",
-           "        u32 dst = 0;",
-           "        for (i64 v = v0; v < v1; ++v) {",
-           "          const uint2 e = __ldg(iv + v);",
-           "          sgb_bulk_g2s(sm + slot_meta + 8u * dst, x + e.x, 8u * e.y, &full_[s]);",
-           "          dst += e.y;",
-           "        }",
+           f"  if (tid >= {CT}) {{  // producer warp: lane l issues the bulk copies of intervals l, l + 32, ...",
+           f"    const u32 lane = tid - {CT};",
+           "    u32 q = 0;",
+           "    for (i64 w = blockIdx.x; w < n_win; w += gridDim.x, ++q) {",
+           "      const u32 s = q % R;",
+           "      const i64 m0 = __ldg(meta_off + w), m1 = __ldg(meta_off + w + 1);",
+           "      const i64 v0 = __ldg(iv_off + w), v1 = __ldg(iv_off + w + 1);",
+           "      uint2 e = make_uint2(0u, 0u);",
+           "      if (v0 + lane < v1) e = __ldg(iv + v0 + lane);  // the first 32 intervals: loads before the wait",
+           "      if (q >= R) sgb_mbar_wait(&empty_[s], ((q / R) - 1u) & 1u);",
+           "      unsigned char *sm = ring_ + (i64)s * slot;",
+           "      u32 off = 0;",
+           "      for (i64 b = v0; b < v1; b += 32) {",
+           "        if (b != v0) { e = make_uint2(0u, 0u); if (b + lane < v1) e = __ldg(iv + b + lane); }",
+           "        const u32 by = 8u * e.y;",
+           "        u32 inc = by;  // inclusive prefix sum of the lanes' bytes",
+           "        for (int d = 1; d < 32; d <<= 1) { const u32 t = __shfl_up_sync(0xffffffffu, inc, d); if ((int)lane >= d) inc += t; }",
+           "        const u32 tot = __shfl_sync(0xffffffffu, inc, 31);",
+           "        if (lane == 0) sgb_mbar_expect_only(&full_[s], tot);  // expected before any of them lands",
+           "        __syncwarp();",
+           "        if (by) sgb_bulk_g2s(sm + slot_meta + off + inc - by, x + e.x, by, &full_[s]);",
+           "        off += tot;",
            "      }",
+           "      if (lane == 0) {",
+           "        sgb_mbar_expect(&full_[s], (u32)(m1 - m0));  // the blob; the arrival closes the phase",
+           "        sgb_bulk_g2s(sm, meta + m0, (u32)(m1 - m0), &full_[s]);",
+           "      }",
+           "      __syncwarp();",
            "    }",
            "    return;",
            "  }",
