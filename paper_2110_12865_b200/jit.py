@@ -560,6 +560,7 @@ def _window_chunks(dp, g0: int, members: list, tapes: dict, imms: dict, threads:
         cmax = "0"
         for gi in chunk:
             cmax = f"max({cmax}, sp[{gi - g0}].y)"
+        out.append("    #pragma unroll 1")
         out.append(f"    for (int c0 = 0, cmax_ = {cmax}; c0 < cmax_; c0 += {threads}) {{")
         loads, comps = [], []
         for gi in chunk:
@@ -677,26 +678,56 @@ def wbulk_source(dp, u: int, tapes: dict, imms: dict) -> str:
         out.append(f"    const bool cq{q} = tid + {q * CT}u < nc_;")
         out.append(f"    const u16 cp{q} = cq{q} ? cpos[tid + {q * CT}u] : (u16)0;")
         out.append(f"    const double cv{q} = cq{q} ? __ldg(x + csrc[tid + {q * CT}u]) : 0.0;")
-    ro = wo = 0
+    # bulk members in chunks of at most WINDOW_LOADS shared-memory loads per thread: a chunk's run /
+    # position offsets go to registers once per window, then per pass every operand and position of
+    # the chunk is loaded (indices clamped into the piece, no branches) before any result is stored
+    info, ro, wo = [], 0, 0
     for j in range(g1 - g0):
-        gi = g0 + j
         if j not in bulk:
             continue
-        rec = dp.groups[gi]
+        rec = dp.groups[g0 + j]
         S, R_ = int(rec["n_slots"]), int(rec["n_roots"])
-        _check_stores(tapes[gi], R_, gi)
-        _, comps = group_parts(dp, gi, tapes[gi], imms[gi], iv="t_", sfx=f"_{j}", window=True)
-        out.append(f"    for (int c0 = 0, n_ = sp[{j}].y; c0 < n_; c0 += {CT}) {{  // bulk member {j}")
-        out.append("      const int t_ = c0 + tid;")
-        out.append("      const bool ok_ = t_ < n_;")
-        for s_ in range(S):
-            out.append(f"      const double s{s_}_{j} = ok_ ? X[roff[{ro + s_}] + t_] : 0.0;")
-        for r_ in range(R_):
-            out.append(f"      const u16 wp{r_}_{j} = ok_ ? wps[woff[{wo + r_}] + t_] : (u16)0xFFFF;")
-        out += ["      " + ln for ln in comps]
-        out.append("    }")
+        _check_stores(tapes[g0 + j], R_, g0 + j)
+        info.append((j, S, R_, ro, wo))
         ro += S
         wo += R_
+    chunks, cur, width = [], [], 0
+    for it in info:
+        wdt = it[1] + it[2]
+        if cur and width + wdt > WINDOW_LOADS:
+            chunks.append(cur)
+            cur, width = [], 0
+        cur.append(it)
+        width += wdt
+    if cur:
+        chunks.append(cur)
+    for chunk in chunks:
+        out.append("    {")
+        cmax = "0"
+        for j, S, R_, ro_, wo_ in chunk:
+            out.append(f"      const int n_{j} = sp[{j}].y;")
+            for s_ in range(S):
+                out.append(f"      const u32 ra{s_}_{j} = roff[{ro_ + s_}];")
+            for r_ in range(R_):
+                out.append(f"      const u32 wa{r_}_{j} = woff[{wo_ + r_}];")
+            cmax = f"max({cmax}, n_{j})"
+        out.append("      #pragma unroll 1")
+        out.append(f"      for (int c0 = 0, cmax_ = {cmax}; c0 < cmax_; c0 += {CT}) {{")
+        loads, comps = [], []
+        for j, S, R_, ro_, wo_ in chunk:
+            gi = g0 + j
+            loads.append(f"const bool ok_{j} = c0 + tid < n_{j};")
+            loads.append(f"const u32 t_{j} = ok_{j} ? (u32)(c0 + tid) : 0u;")
+            for s_ in range(S):
+                loads.append(f"const double s{s_}_{j} = X[ra{s_}_{j} + t_{j}];")
+            for r_ in range(R_):
+                loads.append(f"const u16 wv{r_}_{j} = wps[wa{r_}_{j} + t_{j}];")
+                loads.append(f"const u16 wp{r_}_{j} = ok_{j} ? wv{r_}_{j} : (u16)0xFFFF;")
+            _, cp = group_parts(dp, gi, tapes[gi], imms[gi], iv=f"t_{j}", sfx=f"_{j}", window=True)
+            comps += cp
+        out += ["        " + ln for ln in loads + comps]
+        out.append("      }")
+        out.append("    }")
     out += _window_chunks(dp, g0, [g0 + j for j in range(g1 - g0) if j not in bulk], tapes, imms, CT)
     out += [f"    if (cq{q}) bw[cp{q}] = cv{q};" for q in range(U)]
     out += [f"    for (u32 c = tid + {U * CT}u; c < nc_; c += {U * CT}u) {{"]

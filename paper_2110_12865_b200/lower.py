@@ -806,7 +806,7 @@ class CsrWindows:
 
 
 def _csr_windows(member_opos: list, n_out: int, copy_k: np.ndarray, copy_addr: np.ndarray,
-                 rows: int = WIN_ROWS, wmax: int = WIN_MAX) -> CsrWindows:
+                 rows: int | None = None, wmax: int | None = None) -> CsrWindows:
     """Cut the CSR value array into windows for the window unit (jit.window_source).
 
     ``member_opos``: per member group its (R, N) CSR positions (NONE32 = not an output), first
@@ -817,6 +817,8 @@ def _csr_windows(member_opos: list, n_out: int, copy_k: np.ndarray, copy_addr: n
     pass of a 256-thread block.  ``copy_k`` / ``copy_addr``: the outputs the members do not
     produce (CSR positions, value-array sources).
     """
+    rows = WIN_ROWS if rows is None else rows
+    wmax = WIN_MAX if wmax is None else wmax
     big = np.iinfo(np.int64).max
     firsts, lasts = [], []
     for o in member_opos:

@@ -32,7 +32,7 @@ def main():
     want = ref.run_csr(ref.new_values(ins)).cpu().numpy()
     variants = [dict(wbulk=False, rows=240, ct=256, smem=227), dict(wbulk=True, rows=240, ct=256, smem=227),
                 dict(wbulk=True, rows=120, ct=128, smem=227), dict(wbulk=True, rows=120, ct=128, smem=113),
-                dict(wbulk=True, rows=60, ct=64, smem=75), dict(wbulk=True, rows=120, ct=256, smem=113)]
+                dict(wbulk=True, rows=120, ct=256, smem=113), dict(wbulk=True, rows=80, ct=96, smem=75)]
     for v in variants:
         lower.WIN_ROWS = v["rows"]
         lower.WBULK_CONSUMERS, lower.WBULK_THREADS = v["ct"], v["ct"] + 32
