@@ -278,6 +278,7 @@ def _stage_out(rec, vec: int) -> list[str]:
     return ["__syncthreads();",
             f"{{ const u32 cnt_ = min({JIT_BLOCK * vec}u, {n}u - (u32)tl.y) * {R}u;",
             f"  const u32 base_ = {int(rec['dest_base'])}u + (u32)tl.y * {R}u;",
+            "  #pragma unroll 8",  # shared loads of the write-out in flight together (C3: 78 per thread)
             f"  for (u32 k_ = threadIdx.x; k_ < cnt_; k_ += {JIT_BLOCK}u) {{",
             f"    const u32 q_ = k_ / {R}u; const double v_ = stage_[q_ * {rp}u + (k_ - q_ * {R}u)]; {st}; }} }}",
             "__syncthreads();"]
@@ -423,6 +424,7 @@ def compile_cubin(src: str, name: str = "sgb_tape.cu") -> bytes:
 WINDOW_LOADS = 32  # loads in flight per thread per chunk of a window kernel (C2: 24 0.134 ms, 32 0.128, 40 0.144, r2h)
 COPY_UNROLL = 6  # copied outputs per thread in flight
 WINDOW_MIN_BLOCKS = 3  # resident windows per SM the window kernel's register budget is sized for
+WBULK_LOADS = 16  # bulk-fed window kernel: shared-memory loads per thread per member chunk
 
 
 def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
@@ -539,41 +541,48 @@ __device__ __forceinline__ void sgb_bar_consumers(u32 n) { asm volatile("bar.syn
 """
 
 
-def _window_chunks(dp, g0: int, members: list, tapes: dict, imms: dict, threads: int) -> list[str]:
+def _window_chunks(dp, g0: int, members: list, tapes: dict, imms: dict, threads: int,
+                   lane: str = "tid", split: bool = False, loads: int | None = None) -> list:
     """Members evaluated from the value array (global loads), chunked so every thread has at
     most WINDOW_LOADS loads in flight: a chunk's loads (operands + window positions) are all
-    issued before its computes.  Member j's piece is ``sp[j]``; results go to ``bw[wpos]``."""
+    issued before its computes.  Member j's piece is ``sp[j]``; results go to ``bw[wpos]``;
+    instance c0 + ``lane`` per thread.  ``split``: a list of (loads, lines) per chunk."""
+    cap = WINDOW_LOADS if loads is None else loads
     chunks, cur, width = [], [], 0
     for gi in members:
         rec = dp.groups[gi]
         _check_stores(tapes[gi], int(rec["n_roots"]), gi)
         wdt = max(1, int(rec["n_slots"]) + int(rec["n_const"]))
-        if cur and width + wdt > WINDOW_LOADS:
+        if cur and width + wdt > cap:
             chunks.append(cur)
             cur, width = [], 0
         cur.append(gi)
         width += wdt
     if cur:
         chunks.append(cur)
-    out = []
+    out, parts = [], []
     for chunk in chunks:
+        lines = []
         cmax = "0"
         for gi in chunk:
             cmax = f"max({cmax}, sp[{gi - g0}].y)"
-        out.append("    #pragma unroll 1")
-        out.append(f"    for (int c0 = 0, cmax_ = {cmax}; c0 < cmax_; c0 += {threads}) {{")
+        lines.append("    #pragma unroll 1")
+        lines.append(f"    for (int c0 = 0, cmax_ = {cmax}; c0 < cmax_; c0 += {threads}) {{")
         loads, comps = [], []
         for gi in chunk:
             j = gi - g0
-            out.append(f"      const bool ok_{j} = c0 + tid < sp[{j}].y;")
-            out.append(f"      const u32 i_{j} = ok_{j} ? (u32)(sp[{j}].x + c0 + tid) : 0u;")
+            lines.append(f"      const bool ok_{j} = c0 + {lane} < sp[{j}].y;")
+            lines.append(f"      const u32 i_{j} = ok_{j} ? (u32)(sp[{j}].x + c0 + {lane}) : 0u;")
             ld, cp = group_parts(dp, gi, tapes[gi], imms[gi], iv=f"i_{j}", sfx=f"_{j}", window=True,
                                  guard=f"ok_{j}")
             loads += ld
             comps += cp
-        out += ["      " + ln for ln in loads + comps]
-        out.append("    }")
-    return out
+        lines += ["      " + ln for ln in loads + comps]
+        lines.append("    }")
+        out += lines
+        parts.append((sum(max(1, int(dp.groups[gi]["n_slots"]) + int(dp.groups[gi]["n_const"])) for gi in chunk),
+                      lines))
+    return parts if split else out
 
 
 def _window_writeout(threads: int) -> list[str]:
@@ -607,10 +616,12 @@ def wbulk_source(dp, u: int, tapes: dict, imms: dict) -> str:
     wb = dp.wbulk
     unit = dp.unit(u)
     g0, g1 = unit["group_begin"], unit["group_end"]
-    CT = L.WBULK_CONSUMERS
+    CT = L.WBULK_CONSUMERS  # threads per member group (one instance each per pass)
+    H = L.WBULK_GROUPS  # member groups: chunks of members spread over H x CT consumer threads
+    NC = H * CT
     bulk = set(wb.members)
     out = [_WBULK_HELPERS,
-           f'extern "C" __global__ void __launch_bounds__({CT + 32}, 1) sgb_wbulk_u{u}(',
+           f'extern "C" __global__ void __launch_bounds__({NC + 32}, 1) sgb_wbulk_u{u}(',
            "    Tables T, const unsigned char *meta, const i64 *meta_off, const uint2 *iv, const i64 *iv_off,",
            "    i64 n_win, const double *x, double *out, i64 ring, i64 slot_meta, i64 slot_x, i64 bwb) {",
            "  extern __shared__ __align__(128) unsigned char smem_[];",
@@ -625,8 +636,8 @@ def wbulk_source(dp, u: int, tapes: dict, imms: dict) -> str:
            '    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");',
            "  }",
            "  __syncthreads();",
-           f"  if (tid >= {CT}) {{  // producer warp: lane l issues the bulk copies of intervals l, l + 32, ...",
-           f"    const u32 lane = tid - {CT};",
+           f"  if (tid >= {NC}) {{  // producer warp: lane l issues the bulk copies of intervals l, l + 32, ...",
+           f"    const u32 lane = tid - {NC};",
            "    u32 q = 0;",
            "    for (i64 w = blockIdx.x; w < n_win; w += gridDim.x, ++q) {",
            "      const u32 s = q % R;",
@@ -656,6 +667,7 @@ def wbulk_source(dp, u: int, tapes: dict, imms: dict) -> str:
            "    }",
            "    return;",
            "  }",
+           f"  const int grp_ = tid / {CT}, tl_ = tid % {CT};  // member group, instance lane",
            "  u32 q = 0;",
            "  for (i64 w = blockIdx.x; w < n_win; w += gridDim.x, ++q) {",
            "    const u32 s = q % R;",
@@ -675,9 +687,9 @@ def wbulk_source(dp, u: int, tapes: dict, imms: dict) -> str:
            "    double *bw = buf + head_;"]
     U = COPY_UNROLL
     for q in range(U):  # first batch of copies: gathers in flight while the members evaluate
-        out.append(f"    const bool cq{q} = tid + {q * CT}u < nc_;")
-        out.append(f"    const u16 cp{q} = cq{q} ? cpos[tid + {q * CT}u] : (u16)0;")
-        out.append(f"    const double cv{q} = cq{q} ? __ldg(x + csrc[tid + {q * CT}u]) : 0.0;")
+        out.append(f"    const bool cq{q} = tid + {q * NC}u < nc_;")
+        out.append(f"    const u16 cp{q} = cq{q} ? cpos[tid + {q * NC}u] : (u16)0;")
+        out.append(f"    const double cv{q} = cq{q} ? __ldg(x + csrc[tid + {q * NC}u]) : 0.0;")
     # bulk members in chunks of at most WINDOW_LOADS shared-memory loads per thread: a chunk's run /
     # position offsets go to registers once per window, then per pass every operand and position of
     # the chunk is loaded (indices clamped into the piece, no branches) before any result is stored
@@ -694,14 +706,17 @@ def wbulk_source(dp, u: int, tapes: dict, imms: dict) -> str:
     chunks, cur, width = [], [], 0
     for it in info:
         wdt = it[1] + it[2]
-        if cur and width + wdt > WINDOW_LOADS:
+        if cur and width + wdt > WBULK_LOADS:
             chunks.append(cur)
             cur, width = [], 0
         cur.append(it)
         width += wdt
     if cur:
         chunks.append(cur)
+    blocks = []  # (load weight, lines) per chunk, spread over the member groups below
     for chunk in chunks:
+        out_c = out
+        out = []
         out.append("    {")
         cmax = "0"
         for j, S, R_, ro_, wo_ in chunk:
@@ -716,8 +731,8 @@ def wbulk_source(dp, u: int, tapes: dict, imms: dict) -> str:
         loads, comps = [], []
         for j, S, R_, ro_, wo_ in chunk:
             gi = g0 + j
-            loads.append(f"const bool ok_{j} = c0 + tid < n_{j};")
-            loads.append(f"const u32 t_{j} = ok_{j} ? (u32)(c0 + tid) : 0u;")
+            loads.append(f"const bool ok_{j} = c0 + tl_ < n_{j};")
+            loads.append(f"const u32 t_{j} = ok_{j} ? (u32)(c0 + tl_) : 0u;")
             for s_ in range(S):
                 loads.append(f"const double s{s_}_{j} = X[ra{s_}_{j} + t_{j}];")
             for r_ in range(R_):
@@ -728,19 +743,34 @@ def wbulk_source(dp, u: int, tapes: dict, imms: dict) -> str:
         out += ["        " + ln for ln in loads + comps]
         out.append("      }")
         out.append("    }")
-    out += _window_chunks(dp, g0, [g0 + j for j in range(g1 - g0) if j not in bulk], tapes, imms, CT)
+        blocks.append((sum(c[1] + c[2] for c in chunk), out))
+        out = out_c
+    blocks += _window_chunks(dp, g0, [g0 + j for j in range(g1 - g0) if j not in bulk], tapes, imms, CT,
+                             lane="tl_", split=True, loads=WBULK_LOADS)
+    load = [0] * H
+    per = [[] for _ in range(H)]
+    for wgt, lines in sorted(blocks, key=lambda b: -b[0]):  # heaviest first onto the lightest group
+        h = load.index(min(load))
+        load[h] += wgt
+        per[h].append(lines)
+    for h in range(H):
+        if per[h]:
+            out.append(f"    if (grp_ == {h}) {{")
+            for lines in per[h]:
+                out += lines
+            out.append("    }")
     out += [f"    if (cq{q}) bw[cp{q}] = cv{q};" for q in range(U)]
-    out += [f"    for (u32 c = tid + {U * CT}u; c < nc_; c += {U * CT}u) {{"]
+    out += [f"    for (u32 c = tid + {U * NC}u; c < nc_; c += {U * NC}u) {{"]
     for q in range(U):
-        out.append(f"      const bool dq{q} = c + {q * CT}u < nc_;")
-        out.append(f"      const u16 dp{q} = dq{q} ? cpos[c + {q * CT}u] : (u16)0;")
-        out.append(f"      const double dv{q} = dq{q} ? __ldg(x + csrc[c + {q * CT}u]) : 0.0;")
+        out.append(f"      const bool dq{q} = c + {q * NC}u < nc_;")
+        out.append(f"      const u16 dp{q} = dq{q} ? cpos[c + {q * NC}u] : (u16)0;")
+        out.append(f"      const double dv{q} = dq{q} ? __ldg(x + csrc[c + {q * NC}u]) : 0.0;")
     out += [f"      if (dq{q}) bw[dp{q}] = dv{q};" for q in range(U)]
     out += ["    }",
-            f"    sgb_bar_consumers({CT});",
+            f"    sgb_bar_consumers({NC});",
             "    if (tid == 0) sgb_mbar_arrive(&empty_[s]);  // every read of the slot is done"]
-    out += _window_writeout(CT)
-    out += [f"    sgb_bar_consumers({CT});  // the window buffer is free again",
+    out += _window_writeout(NC)
+    out += [f"    sgb_bar_consumers({NC});  // the window buffer is free again",
             "  }",
             "}",
             ""]

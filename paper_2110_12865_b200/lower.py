@@ -897,8 +897,9 @@ def _csr_windows(member_opos: list, n_out: int, copy_k: np.ndarray, copy_addr: n
 WBULK_GAP = 16  # value-array runs closer than this many doubles merge into one bulk copy
 WBULK_SMEM = 227 * 1024  # dynamic shared memory of one window block (one block per SM)
 WBULK_RING = (2, 4)  # ring depth range (windows in flight per block)
-WBULK_CONSUMERS = 256  # consumer threads of a bulk window block (one instance each per pass)
-WBULK_THREADS = WBULK_CONSUMERS + 32  # + one producer warp
+WBULK_CONSUMERS = 256  # consumer threads per member group of a bulk window block (one instance each per pass)
+WBULK_GROUPS = 2  # member groups per block (chunks of members evaluated side by side)
+WBULK_THREADS = WBULK_GROUPS * WBULK_CONSUMERS + 32  # + one producer warp
 
 
 @dataclass

@@ -30,14 +30,16 @@ def main():
     ins = bench.workload_inputs("c2", ns, 0)
     ref = DevicePlan(plan, lowered=lower_plan(plan, csr_window=False))
     want = ref.run_csr(ref.new_values(ins)).cpu().numpy()
-    variants = [dict(wbulk=False, rows=240, ct=256, smem=227), dict(wbulk=True, rows=240, ct=256, smem=227),
-                dict(wbulk=True, rows=120, ct=128, smem=227), dict(wbulk=True, rows=120, ct=128, smem=113),
-                dict(wbulk=True, rows=120, ct=256, smem=113), dict(wbulk=True, rows=80, ct=96, smem=75)]
+    variants = [dict(wbulk=False, rows=240, ct=256, h=1, smem=227)]
+    variants += [dict(wbulk=True, rows=240, ct=256, h=h, smem=227) for h in (1, 2, 3)]
+    variants += [dict(wbulk=True, rows=240, ct=256, h=2, smem=227, loads=lo) for lo in (8, 24)]
     for v in variants:
         lower.WIN_ROWS = v["rows"]
-        lower.WBULK_CONSUMERS, lower.WBULK_THREADS = v["ct"], v["ct"] + 32
+        lower.WBULK_CONSUMERS, lower.WBULK_GROUPS = v["ct"], v["h"]
+        lower.WBULK_THREADS = v["ct"] * v["h"] + 32
         lower.WBULK_SMEM = v["smem"] * 1024
         lower.WBULK_GAP = v.get("gap", 16)
+        jit.WBULK_LOADS = v.get("loads", 16)
         t0 = time.perf_counter()
         lw = lower_plan(plan, csr_window=True, wbulk=v["wbulk"])
         if lw.wbulk is not None:
