@@ -1615,7 +1615,7 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     dp.jit_tapes, dp.jit_imms = jit_tapes, jit_imms
     dp.wbulk = None
     if wbulk is None:
-        wbulk = os.environ.get("SGB_WBULK", "1") != "0"
+        wbulk = os.environ.get("SGB_WBULK", "0") == "1"  # measured slower than the register-pipelined windows (r2m)
     if windows is not None and window_units and wbulk:  # feed the window unit with bulk copies
         uw = window_units[0][0]
         wb = window_bulk(dp, uw, windows)

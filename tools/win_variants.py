@@ -30,16 +30,15 @@ def main():
     ins = bench.workload_inputs("c2", ns, 0)
     ref = DevicePlan(plan, lowered=lower_plan(plan, csr_window=False))
     want = ref.run_csr(ref.new_values(ins)).cpu().numpy()
-    variants = [dict(wbulk=False, rows=240, ct=256, h=1, smem=227)]
-    variants += [dict(wbulk=True, rows=240, ct=256, h=h, smem=227) for h in (1, 2, 3)]
-    variants += [dict(wbulk=True, rows=240, ct=256, h=2, smem=227, loads=lo) for lo in (8, 24)]
+    variants = [dict(wbulk=False, loads=32, blocks=3, winmax=7936), dict(wbulk=False, loads=32, blocks=3, winmax=6144),
+                dict(wbulk=False, loads=24, blocks=4, winmax=6144), dict(wbulk=False, loads=28, blocks=4, winmax=6144),
+                dict(wbulk=False, loads=16, blocks=5, winmax=4800), dict(wbulk=True, h=2, winmax=6144),
+                dict(wbulk=True, h=2, winmax=7936)]
     for v in variants:
-        lower.WIN_ROWS = v["rows"]
-        lower.WBULK_CONSUMERS, lower.WBULK_GROUPS = v["ct"], v["h"]
-        lower.WBULK_THREADS = v["ct"] * v["h"] + 32
-        lower.WBULK_SMEM = v["smem"] * 1024
-        lower.WBULK_GAP = v.get("gap", 16)
-        jit.WBULK_LOADS = v.get("loads", 16)
+        lower.WIN_MAX = v["winmax"]
+        jit.WINDOW_LOADS, jit.WINDOW_MIN_BLOCKS = v.get("loads", 32), v.get("blocks", 3)
+        lower.WBULK_GROUPS = v.get("h", 2)
+        lower.WBULK_THREADS = 256 * lower.WBULK_GROUPS + 32
         t0 = time.perf_counter()
         lw = lower_plan(plan, csr_window=True, wbulk=v["wbulk"])
         if lw.wbulk is not None:
