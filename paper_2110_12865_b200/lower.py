@@ -787,7 +787,7 @@ def _window_members(plan, lowered, opos, n_waves):
 
 
 WIN_ROWS = 240  # anchor instances per CSR window (block of JIT_BLOCK threads: 16 lanes of slack)
-WIN_MAX = 7936  # outputs per CSR window (62 KB of shared memory: 3 windows resident per SM)
+WIN_MAX = 6144  # outputs per CSR window (48 KB of shared memory; 7936 measured 3 % slower on C2, r2o)
 WIN_MIN = 1024  # windows are not cut shorter than this unless the anchor forces it
 WIN_MAX_LOADS = 32  # default lowering: windows only when every member loads at most this many slots
 
