@@ -887,7 +887,7 @@ void launch_unit(const sgb_plan *p, const Unit &u, double *x, int64_t ld, int64_
       cudaLaunchKernel(u.jitb, dim3((unsigned)grid), dim3(JIT_BLOCK), args, 0, s);
     } else {
       void *args[] = {&T, &tiles, &n, &x, &out, &c};
-      cudaLaunchKernel(u.jit, dim3((unsigned)u.grid), dim3(JIT_BLOCK), args, (size_t)u.regs, s);
+      cudaLaunchKernel(u.jit, dim3((unsigned)u.grid), dim3(u.bs), args, (size_t)u.regs, s);
     }
     return;
   }
@@ -1253,7 +1253,10 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
         }
       }
     } else if (jit) {
-      if (u.kind != KIND_TAPE || u.bs != JIT_BLOCK || (u.variant != 1 && u.variant != 2 && u.variant != 4) ||
+      // block: JIT_BLOCK threads, or k x JIT_BLOCK for a single-group unit whose root set is split k ways
+      // (jit.py: part p = threadIdx.x / JIT_BLOCK evaluates its roots' cone for the tile's instances)
+      if (u.kind != KIND_TAPE || u.bs % JIT_BLOCK || u.bs < JIT_BLOCK || u.bs > 4 * JIT_BLOCK ||
+          (u.bs != JIT_BLOCK && u.g1 - u.g0 != 1) || (u.variant != 1 && u.variant != 2 && u.variant != 4) ||
           !p->jit_lib)
         return fail(-1, "sgb_plan_create: specialised unit " + std::to_string(k) + " without its kernels");
       cudaKernel_t kf, kb;
@@ -1284,7 +1287,7 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       } else if (window) {
         u.grid = u.t1 - u.t0;  // one block per window, dispatched in CSR order
       } else if (jit) {
-        SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, u.jit, JIT_BLOCK, (size_t)u.regs));
+        SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, u.jit, u.bs, (size_t)u.regs));
         u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
         if (u.grid > u.t1 - u.t0) u.grid = u.t1 - u.t0;
       } else if (u.kind == KIND_TAPE) {

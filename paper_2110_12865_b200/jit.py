@@ -139,7 +139,8 @@ def _out_pos(rec, r: int, i: str = "i") -> str | None:
 
 def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: str = "",
                 batched: bool = False, window: bool = False, bv: str = "b",
-                stage: str | None = None, guard: str | None = None) -> tuple[list[str], list[str]]:
+                stage: str | None = None, guard: str | None = None,
+                keep: set | None = None) -> tuple[list[str], list[str]]:
     """Straight-line CUDA for instance ``iv`` of packed group ``gi`` (register tape -> SSA).
 
     Returns (load lines, compute + store lines) so several instances' loads can be
@@ -150,7 +151,8 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
     results go to the block's staging buffer at ``stage_[(stage) * RP + r]``
     (``stage`` = the instance's offset in the tile, RP = lower.stage_stride); the
     unit writes the tile out coalesced.  ``guard``: every load is predicated on it
-    (lanes without an instance issue no memory traffic).
+    (lanes without an instance issue no memory traffic).  ``keep``: evaluate only these tape
+    records (one part of a split root set, lower.split_roots; unused loads are dead code).
     """
     X = (lambda a: f"x + (u64)({a}) * ld + {bv}") if batched else (lambda a: f"x + ({a})")
     G = (lambda e, z: f"({guard}) ? ({e}) : {z}") if guard else (lambda e, z: e)  # noqa: E731
@@ -189,6 +191,8 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
     stream = bool(flags & L.FLAG_STREAM)
     opos = lambda r: _out_pos(rec, r, i)  # noqa: E731
     for j, t in enumerate(tape.tolist()):
+        if keep is not None and j not in keep:
+            continue
         op, na, nb, dst, a, b, c, aux = t
         A = ("-" if na else "") + reg.get(a, "0.0")
         B = ("-" if nb else "") + reg.get(b, "0.0")
@@ -257,10 +261,13 @@ def group_batch_body(dp, gi, tape, imms, vec: int) -> list[str]:
 
 
 def group_vec_body(dp, gi, tape, imms, vec: int, base: str, stride: int, batched=False, window=False,
-                   limit: str | None = None, stage: bool = False):
+                   limit: str | None = None, stage: bool = False, keep: set | None = None,
+                   lane: str = "threadIdx.x"):
     """VEC instances base + v*stride: every instance's loads first, then the computes.
 
     ``limit``: instance v is valid only if ``limit`` (with ``{v}`` = v * stride) holds too.
+    ``keep``: the tape records of one part of a split root set; ``lane``: the thread's instance
+    lane inside the tile (stage position).
     """
     n = int(dp.groups[gi]["n"])
     lines, comps = [], []
@@ -270,7 +277,7 @@ def group_vec_body(dp, gi, tape, imms, vec: int, base: str, stride: int, batched
         lines.append(f"const bool ok_{v} = iv{v} < {n}u{extra};")
         lines.append(f"const u32 ic{v} = ok_{v} ? iv{v} : {n - 1}u;")
         ld, cp = group_parts(dp, gi, tape, imms, iv=f"ic{v}", sfx=f"_{v}", batched=batched, window=window,
-                             stage=f"threadIdx.x + {v * stride}" if stage else None)
+                             stage=f"{lane} + {v * stride}" if stage else None, keep=keep)
         lines += ld
         comps += cp
     return lines + comps
@@ -282,7 +289,7 @@ def _check_stores(tape, n_roots: int, gi: int):
         raise ValueError(f"group {gi}: tape stores roots {roots}, expected 0..{n_roots - 1}")
 
 
-def _stage_out(rec, vec: int) -> list[str]:
+def _stage_out(rec, vec: int, threads: int = JIT_BLOCK) -> list[str]:
     """Write a staged tile of an instance-major group: its instances' results are one contiguous
     run ``dest_base + tile_start * R ...`` of the value array, stored by consecutive threads."""
     n, R = int(rec["n"]), int(rec["n_roots"])
@@ -292,7 +299,7 @@ def _stage_out(rec, vec: int) -> list[str]:
             f"{{ const u32 cnt_ = min({JIT_BLOCK * vec}u, {n}u - (u32)tl.y) * {R}u;",
             f"  const u32 base_ = {int(rec['dest_base'])}u + (u32)tl.y * {R}u;",
             "  #pragma unroll 8",  # shared loads of the write-out in flight together (C3: 78 per thread)
-            f"  for (u32 k_ = threadIdx.x; k_ < cnt_; k_ += {JIT_BLOCK}u) {{",
+            f"  for (u32 k_ = threadIdx.x; k_ < cnt_; k_ += {threads}u) {{",
             f"    const u32 q_ = k_ / {R}u; const double v_ = stage_[q_ * {rp}u + (k_ - q_ * {R}u)]; {st}; }} }}",
             "__syncthreads();"]
 
@@ -306,6 +313,9 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
     """
     unit = dp.unit(u)
     out = []
+    split = getattr(dp, "jit_split", {}).get(unit["group_begin"]) if unit["group_end"] - unit["group_begin"] == 1 \
+        else None
+    nthreads = JIT_BLOCK * (len(split) if split else 1)
     big = max(len(tapes[gi]) for gi in range(unit["group_begin"], unit["group_end"]))
     # batched value sets per lane: 8 for small templates (C5: 2.90 -> 2.47 ms, r45); big templates keep
     # 4 (their register file is full already, and the body is compiled once per value set)
@@ -323,13 +333,15 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
         else:
             # no register cap: huge templates run best uncapped -- a 2-block cap spilled and measured
             # 2.7x slower on C3 (r24)
-            bounds = f"{JIT_BLOCK}"
+            bounds = f"{nthreads}"
+            lane = f"(threadIdx.x % {JIT_BLOCK}u)" if split else "threadIdx.x"
             head = [f'extern "C" __global__ void __launch_bounds__({bounds}) sgb_tape_u{u}(',
                     "    Tables T, const int2 *tiles, i64 n_tiles, double *x, double *out, int csr) {",
                     "  extern __shared__ double stage_[];",
                     "  for (i64 t = blockIdx.x; t < n_tiles; t += gridDim.x) {",
                     "    const int2 tl = tiles[t];",
-                    "    const u32 i = (u32)tl.y + threadIdx.x;",
+                    f"    const u32 i = (u32)tl.y + {lane};",
+                    f"    const u32 part_ = threadIdx.x / {JIT_BLOCK}u;  // root-set part (lower.split_roots)",
                     "    {",
                     "    switch (tl.x) {"]
         out += head
@@ -343,11 +355,20 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
                 out.append(f"      if (i >= {int(rec['n'])}u) break;")
             if rec["flags"] & L.FLAG_CSR_ONLY:
                 out.append("      if (!csr) break;")
-            body = (group_batch_body(dp, gi, tapes[gi], imms[gi], bvec) if batched else
-                    group_vec_body(dp, gi, tapes[gi], imms[gi], vec, "i", JIT_BLOCK, stage=staged))
+            if batched or not split:
+                body = (group_batch_body(dp, gi, tapes[gi], imms[gi], bvec) if batched else
+                        group_vec_body(dp, gi, tapes[gi], imms[gi], vec, "i", JIT_BLOCK, stage=staged))
+            else:  # part p of the split root set: its roots' cone, the same tile of instances
+                body = []
+                for p, keep in enumerate(split):
+                    body.append(f"if (part_ == {p}u) {{")
+                    body += ["  " + ln for ln in group_vec_body(dp, gi, tapes[gi], imms[gi], vec, "i", JIT_BLOCK,
+                                                                 stage=staged, keep=keep,
+                                                                 lane=f"(threadIdx.x % {JIT_BLOCK}u)")]
+                    body.append("}")
             out += ["      " + ln for ln in body]
             if staged:
-                out += ["      " + ln for ln in _stage_out(rec, vec)]
+                out += ["      " + ln for ln in _stage_out(rec, vec, nthreads)]
             out.append("    } break;")
         out += ["    default: break;", "    }", "    }", "  }", "}", ""]
     return "\n".join(out)

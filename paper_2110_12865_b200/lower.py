@@ -127,6 +127,7 @@ class DevicePlanArrays:
     jit_source: str = ""
     windows: "CsrWindows" = None  # CSR windows of the last wave (the window unit's pieces and copies)
     wbulk: "WindowBulk" = None  # bulk-copy feed of the window unit (UNIT_BULK), see window_bulk
+    jit_split: dict = field(default_factory=dict)  # group -> per part the tape records it evaluates
     window_members: list = field(default_factory=list)  # plan kernels the window unit evaluates
     window_units: list = field(default_factory=list)
     jit_tapes: dict = field(default_factory=dict)  # packed group -> register tape of specialised units
@@ -1083,6 +1084,78 @@ def window_bulk(dp, u: int, windows: "CsrWindows", gap: int | None = None) -> Wi
                       roff_at=roff_at, woff_at=woff_at, wpos_at=wpos_at)
 
 
+JIT_SPLIT = 1  # single-group specialised units with a big multi-root template: root set split this many ways
+JIT_SPLIT_MIN_TAPE = 600  # tape records from which a template is split (C3's element Hessian: 955)
+
+
+def _tape_reads(t) -> tuple:
+    op = int(t[0])
+    if op == T_IMM:
+        return ()
+    if op in (T_NEG, T_SQRT, T_SLOW, T_ST):
+        return (int(t[4]),)
+    if op in (T_SEL, T_MADD, T_MSUB, T_RMSUB):
+        return (int(t[4]), int(t[5]), int(t[6]))
+    return (int(t[4]), int(t[5]))
+
+
+def split_roots(tape: np.ndarray, n_roots: int, k: int, seed: int = 0, rounds: int = 4) -> list:
+    """Partition a register tape's roots into ``k`` equal-count parts with small cones.
+
+    Returns per part the set of tape records it evaluates (the union of its roots' cones, their
+    stores included).  A part's records are a sub-DAG of the tape evaluated in the same order,
+    so every root keeps its exact op sequence (bit-identical results); records shared by
+    several parts are evaluated by each of them.  Balanced swap local search on bitmask cones."""
+    last: dict[int, int] = {}
+    cone: list[int] = []
+    store_of: dict[int, int] = {}
+    for j, t in enumerate(tape.tolist()):
+        m = 1 << j
+        for r in _tape_reads(t):
+            if r in last:
+                m |= cone[last[r]]
+        cone.append(m)
+        if int(t[0]) == T_ST:
+            store_of.setdefault(int(t[7]), j)
+        else:
+            last[int(t[3])] = j
+    roots = sorted(store_of)
+    cm = [cone[store_of[r]] for r in roots]
+    rng = np.random.default_rng(seed)
+    order = list(rng.permutation(len(roots)))
+    parts = [order[i::k] for i in range(k)]
+
+    def size(p):
+        u = 0
+        for q in p:
+            u |= cm[q]
+        return u.bit_count()
+
+    sizes = [size(p) for p in parts]
+    for _ in range(rounds):
+        better = False
+        for a in range(k):
+            for b in range(a + 1, k):
+                for ia in range(len(parts[a])):
+                    for ib in range(len(parts[b])):
+                        parts[a][ia], parts[b][ib] = parts[b][ib], parts[a][ia]
+                        na, nb = size(parts[a]), size(parts[b])
+                        if na + nb < sizes[a] + sizes[b] and max(na, nb) <= max(sizes[a], sizes[b]):
+                            sizes[a], sizes[b] = na, nb
+                            better = True
+                        else:
+                            parts[a][ia], parts[b][ib] = parts[b][ib], parts[a][ia]
+        if not better:
+            break
+    keeps = []
+    for p in parts:
+        u = 0
+        for q in p:
+            u |= cm[q]
+        keeps.append({j for j in range(len(tape)) if (u >> j) & 1})
+    return keeps
+
+
 def jit_vec(groups, sel) -> int:
     """Instances per thread of a specialised unit: all of them keep their loads in flight
     together, so small templates take 4, mid-size 2, big element templates 1."""
@@ -1613,6 +1686,21 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     dp.window_members = list(window) if window is not None else []
     dp.window_units = window_units
     dp.jit_tapes, dp.jit_imms = jit_tapes, jit_imms
+    # split the root set of a big multi-root template over k x JIT_BLOCK threads (jit.py: part p =
+    # threadIdx.x / JIT_BLOCK evaluates its roots' cone): fewer live registers per thread
+    dp.jit_split = {}
+    if JIT_SPLIT > 1:
+        fu, fb = UNIT_FIELDS.index("flags"), UNIT_FIELDS.index("block_size")
+        for uu in range(len(dp.units)):
+            r = dp.unit(uu)
+            if not r["flags"] & UNIT_JIT or r["flags"] & UNIT_WINDOW or r["group_end"] - r["group_begin"] != 1:
+                continue
+            gi = r["group_begin"]
+            tp = jit_tapes.get(gi)
+            if tp is None or len(tp) < JIT_SPLIT_MIN_TAPE or int(dp.groups[gi]["n_roots"]) < 4 * JIT_SPLIT:
+                continue
+            dp.jit_split[gi] = split_roots(tp, int(dp.groups[gi]["n_roots"]), JIT_SPLIT)
+            dp.units[uu, fb] = r["block_size"] * JIT_SPLIT
     dp.wbulk = None
     if wbulk is None:
         wbulk = os.environ.get("SGB_WBULK", "0") == "1"  # measured slower than the register-pipelined windows (r2m)

@@ -2,12 +2,10 @@
 
     python tools/c3_variants.py [--m 55]
 
-Knobs: lower.STORE_ROOTS_EARLY (roots stored as computed vs at the end of the tape) and the LOG
-restatement (jit._SLOW[3]: the glibc restatement ``sgb_log`` vs CUDA's ``log``, timing only --
-CUDA's log is not bit-exact).  Autotune on, as in bench.py.
+Knob: lower.JIT_SPLIT (the element template's root set split over k x 256 threads per tile).
+Autotune on, as in bench.py.
 """
 import argparse
-import itertools
 import sys
 import time
 from pathlib import Path
@@ -33,9 +31,8 @@ def main():
     key, plan = bench.build_workload("c3", ns)
     ins = bench.workload_inputs("c3", ns, 0)
     want = None
-    for early, log in itertools.product((True, False), ("sgb_log({a})", "log({a})")):
-        lower.STORE_ROOTS_EARLY = early
-        jit._SLOW[3] = log
+    for split in (1, 2, 3, 1):
+        lower.JIT_SPLIT = split
         t0 = time.perf_counter()
         lw = lower_plan(plan, relayout="auto")
         t_low = time.perf_counter() - t0
@@ -58,7 +55,7 @@ def main():
             torch.cuda.synchronize()
             tw = sorted(e0.elapsed_time(e1) for e0, e1 in evs)
             per.append(round(tw[len(tw) // 2], 4))
-        print(f"early={early} log={log} same_bits_as_first={ok} waves {per} tiles {dp.tile_order} "
+        print(f"split={split} same_bits_as_first={ok} waves {per} tiles {dp.tile_order} "
               f"(lower {t_low:.0f}s)", flush=True)
         del dp
 
