@@ -97,17 +97,17 @@ def _off(v: int) -> str:
 INDEX64 = True
 
 
-def _idx_t() -> str:
-    return "u64" if INDEX64 else "u32"
+def _idx_t(wide: bool = True) -> str:
+    return "u64" if INDEX64 and wide else "u32"
 
 
-def _affine_u32(base: int, stride: int, i: str) -> str:
-    if INDEX64:
+def _affine_u32(base: int, stride: int, i: str, wide: bool = True) -> str:
+    if INDEX64 and wide:
         return f"({int(base) % 2**64}ull + {int(stride) % 2**64}ull * (u64)({i}))"
     return f"({int(base) % 2**32}u + {int(stride) % 2**32}u * {i})"
 
 
-def _column(rec, col: int, i: str = "i", dp=None) -> str:
+def _column(rec, col: int, i: str = "i", dp=None, wide: bool = True) -> str:
     """Index expression (u32) of retained column ``col`` for instance ``i``."""
     n = int(rec["n"])
     f = int(rec["flags"])
@@ -115,7 +115,7 @@ def _column(rec, col: int, i: str = "i", dp=None) -> str:
     if aff is None and col == 0 and f & L.FLAG_AFFINE0:
         aff = int(rec["a0_base"]), int(rec["a0_stride"])
     if aff is not None:  # modular u32 arithmetic: every decoded address is < 2^32
-        return _affine_u32(aff[0], aff[1], i)
+        return _affine_u32(aff[0], aff[1], i, wide)
     if f & L.FLAG_W16:
         nch = (n + 31) // 32
         return (f"(__ldg(T.cbase + {_off(int(rec['cb_off']) + col * nch)} + ({i} >> 5)) + "
@@ -164,13 +164,17 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
     loads, comp = [], []
     reg: dict[int, str] = {}
     i = iv
-    col = lambda c: _column(rec, c, i, dp)  # noqa: E731
+    # batched addresses are scaled by ld (x + addr * ld + b): u32 keeps that a 32 x 32 -> 64 multiply
+    # (64-bit addresses there measured 2.48 -> 2.95 ms on C5, r2q)
+    wide = not batched
+    col = lambda c: _column(rec, c, i, dp, wide)  # noqa: E731
+    it = _idx_t(wide)
     if S:
-        loads.append(f"const {_idx_t()} idx0{sfx} = {G(f'({_idx_t()})({col(0)})', '0u')};")
+        loads.append(f"const {it} idx0{sfx} = {G(f'({it})({col(0)})', '0u')};")
     for s_ in range(S):
         c = int(cols[s_])
         if c < 0:
-            addr = (f"idx0{sfx} + {int(dels[s_]) % 2**64}ull" if INDEX64
+            addr = (f"idx0{sfx} + {int(dels[s_]) % 2**64}ull" if INDEX64 and wide
                     else f"idx0{sfx} + {int(dels[s_]) % 2**32}u")
         elif c == 0:
             addr = f"idx0{sfx}"
@@ -249,9 +253,9 @@ def group_batch_body(dp, gi, tape, imms, vec: int) -> list[str]:
         ld, cp = group_parts(dp, gi, tape, imms, iv="i", sfx=f"_{v}", batched=True, bv=f"bc{v}")
         # the index decode (idx0 / column loads) is the same for every value set: emit it once
         if shared is None:
-            shared = [ln for ln in ld if ln.startswith(f"const {_idx_t()} idx0")]
+            shared = [ln for ln in ld if ln.startswith(f"const {_idx_t(False)} idx0")]
             lines = shared[:1] + lines if shared else lines
-        ld = [ln.replace(f"idx0_{v}", "idx0_0") for ln in ld if not ln.startswith(f"const {_idx_t()} idx0")]
+        ld = [ln.replace(f"idx0_{v}", "idx0_0") for ln in ld if not ln.startswith(f"const {_idx_t(False)} idx0")]
         cp = [ln.replace(f"idx0_{v}", "idx0_0") for ln in cp]
         lines += ld
         comps += cp
@@ -600,7 +604,8 @@ def _window_chunks(dp, g0: int, members: list, tapes: dict, imms: dict, threads:
         cmax = "0"
         for gi in chunk:
             cmax = f"max({cmax}, sp[{gi - g0}].y)"
-        lines.append("    #pragma unroll 1")
+        if split:  # (the bulk kernel's code size matters more than overlapping passes)
+            lines.append("    #pragma unroll 1")
         lines.append(f"    for (int c0 = 0, cmax_ = {cmax}; c0 < cmax_; c0 += {threads}) {{")
         loads, comps = [], []
         for gi in chunk:

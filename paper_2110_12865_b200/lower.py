@@ -1163,6 +1163,12 @@ def jit_vec(groups, sel) -> int:
         return int(os.environ["SGB_JIT_VEC"])
     width = max(len(groups[j].slot_col) + groups[j].n_const + (len(groups[j].tape) if groups[j].tape is not None
                                                                else 1) // 4 for j in sel)
+    # long-latency ops (DIV / SQRT / transcendentals): one instance per thread -- more resident warps
+    # hide them better than a second instance's loads (C2 faces 0.025 -> 0.023 ms, C4 rotations, r2q)
+    slow = any(groups[j].tape is not None and np.isin(groups[j].tape["op"], (T_DIV, T_SQRT, T_SLOW)).any()
+               for j in sel)
+    if slow:
+        return 1
     return 4 if width <= 24 else (2 if width <= 64 else 1)
 
 
