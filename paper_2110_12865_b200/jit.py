@@ -462,6 +462,8 @@ def compile_cubin(src: str, name: str = "sgb_tape.cu") -> bytes:
 WINDOW_LOADS = 32  # loads in flight per thread per chunk of a window kernel (C2: 24 0.134 ms, 32 0.128, 40 0.144, r2h)
 COPY_UNROLL = 6  # copied outputs per thread in flight
 WINDOW_MIN_BLOCKS = 3  # resident windows per SM the window kernel's register budget is sized for
+WINDOW_COPY_OVERLAP = False  # first copy batch in flight with the first member chunk
+COPY_OVERLAP_LOADS = 9  # registers (in doubles) the first copy batch takes from the first chunk
 WBULK_LOADS = 16  # bulk-fed window kernel: shared-memory loads per thread per member chunk
 
 
@@ -486,7 +488,9 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
         rec = dp.groups[gi]
         _check_stores(tapes[gi], int(rec["n_roots"]), gi)
         wdt = max(1, int(rec["n_slots"]) + int(rec["n_const"]))
-        if cur and width + wdt > WINDOW_LOADS:
+        # the first chunk shares the register budget with the first batch of copies in flight
+        cap = WINDOW_LOADS - (COPY_OVERLAP_LOADS if WINDOW_COPY_OVERLAP and not chunks else 0)
+        if cur and width + wdt > cap:
             chunks.append(cur)
             cur, width = [], 0
         cur.append(gi)
@@ -508,15 +512,29 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
            "    // window position p at bw[p]: out + k0 - head_ is 16-byte aligned, so is buf",
            "    const u32 head_ = (u32)((reinterpret_cast<u64>(out + k0) >> 3) & 1ull);",
            "    double *bw = buf + head_;",
-           "    __syncthreads();",
-           f"    for (i64 c = c0_ + tid; c < c1_; c += {B * COPY_UNROLL}) {{"]
-    for q in range(COPY_UNROLL):  # named registers (no local arrays): every copy's loads in flight
-        out.append(f"      const bool cq{q} = c + {q * B} < c1_;")
-        out.append(f"      const u16 cp{q} = cq{q} ? __ldcs(copy_pos + c + {q * B}) : (u16)0;")
-        out.append(f"      const double cv{q} = cq{q} ? __ldg(x + __ldcs(copy_src + c + {q * B})) : 0.0;")
-    out += [f"      if (cq{q}) bw[cp{q}] = cv{q};" for q in range(COPY_UNROLL)]
-    out += ["    }"]
-    for chunk in chunks:
+           "    __syncthreads();"]
+
+    def copy_loop(first: str, pre: str) -> list:
+        lines = [f"    for (i64 c = {first}; c < c1_; c += {B * COPY_UNROLL}) {{"]
+        for q in range(COPY_UNROLL):  # named registers (no local arrays): every copy's loads in flight
+            lines.append(f"      const bool {pre}q{q} = c + {q * B} < c1_;")
+            lines.append(f"      const u16 {pre}p{q} = {pre}q{q} ? __ldcs(copy_pos + c + {q * B}) : (u16)0;")
+            lines.append(f"      const double {pre}v{q} = {pre}q{q} ? __ldg(x + __ldcs(copy_src + c + {q * B})) : 0.0;")
+        lines += [f"      if ({pre}q{q}) bw[{pre}p{q}] = {pre}v{q};" for q in range(COPY_UNROLL)]
+        return lines + ["    }"]
+
+    if WINDOW_COPY_OVERLAP:  # the first copy batch's loads in flight with the first member chunk's
+        out.append("    const i64 cb_ = c0_ + tid;")
+        for q in range(COPY_UNROLL):
+            out.append(f"    const bool cq{q} = cb_ + {q * B} < c1_;")
+            out.append(f"    const u16 cp{q} = cq{q} ? __ldcs(copy_pos + cb_ + {q * B}) : (u16)0;")
+            out.append(f"    const double cv{q} = cq{q} ? __ldg(x + __ldcs(copy_src + cb_ + {q * B})) : 0.0;")
+    else:
+        out += copy_loop("c0_ + tid", "c")
+    for k_, chunk in enumerate(chunks):
+        if WINDOW_COPY_OVERLAP and k_ == 1:
+            out += [f"    if (cq{q}) bw[cp{q}] = cv{q};" for q in range(COPY_UNROLL)]
+            out += copy_loop(f"cb_ + {B * COPY_UNROLL}", "d")
         cmax = "0"
         for gi in chunk:
             cmax = f"max({cmax}, sp[{gi - g0}].y)"
@@ -532,6 +550,9 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
             comps += cp
         out += ["      " + ln for ln in loads + comps]
         out.append("    }")
+    if WINDOW_COPY_OVERLAP and len(chunks) < 2:
+        out += [f"    if (cq{q}) bw[cp{q}] = cv{q};" for q in range(COPY_UNROLL)]
+        out += copy_loop(f"cb_ + {B * COPY_UNROLL}", "d")
     out += ["    __syncthreads();",
             "    {  // 16-byte shared loads and streaming stores; the pair straddling k0 writes its second half",
             "      const u32 tot_ = len_ + head_;",

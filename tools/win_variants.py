@@ -30,15 +30,11 @@ def main():
     ins = bench.workload_inputs("c2", ns, 0)
     ref = DevicePlan(plan, lowered=lower_plan(plan, csr_window=False))
     want = ref.run_csr(ref.new_values(ins)).cpu().numpy()
-    variants = [dict(wbulk=False, loads=32, blocks=3, winmax=7936), dict(wbulk=False, loads=32, blocks=3, winmax=6144),
-                dict(wbulk=False, loads=24, blocks=4, winmax=6144), dict(wbulk=False, loads=28, blocks=4, winmax=6144),
-                dict(wbulk=False, loads=16, blocks=5, winmax=4800), dict(wbulk=True, h=2, winmax=6144),
-                dict(wbulk=True, h=2, winmax=7936)]
+    variants = [dict(ovl=o, loads=l_, ovl_loads=ol) for o, l_, ol in
+                ((False, 32, 9), (True, 32, 9), (True, 32, 3), (True, 28, 6), (False, 32, 9), (True, 32, 9))]
     for v in variants:
-        lower.WIN_MAX = v["winmax"]
-        jit.WINDOW_LOADS, jit.WINDOW_MIN_BLOCKS = v.get("loads", 32), v.get("blocks", 3)
-        lower.WBULK_GROUPS = v.get("h", 2)
-        lower.WBULK_THREADS = 256 * lower.WBULK_GROUPS + 32
+        jit.WINDOW_COPY_OVERLAP, jit.WINDOW_LOADS, jit.COPY_OVERLAP_LOADS = v["ovl"], v["loads"], v["ovl_loads"]
+        v["wbulk"] = False
         t0 = time.perf_counter()
         lw = lower_plan(plan, csr_window=True, wbulk=v["wbulk"])
         if lw.wbulk is not None:
