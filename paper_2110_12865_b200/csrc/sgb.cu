@@ -734,6 +734,26 @@ __global__ void gather_outputs_batch(const double *__restrict__ X, int64_t ld, i
   }
 }
 
+// Batched outputs that are plain value-array entries of a CSR-window plan (the window members'
+// value-mode twins store theirs directly): out[copy_k[c] * ld_out + b] = X[copy_src[c] * ld + b].
+__global__ void gather_copies_batch(const double *__restrict__ X, int64_t ld, int64_t batch,
+                                    const uint32_t *__restrict__ copy_k, const uint32_t *__restrict__ copy_src,
+                                    int64_t n, double *__restrict__ out, int64_t ld_out) {
+  const int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= n) return;
+  const double *src = X + (int64_t)__ldg(copy_src + c) * ld;
+  double *dst = out + (int64_t)__ldg(copy_k + c) * ld_out;
+  for (int64_t b = threadIdx.x & 31; b < batch; b += 128) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (b + 32 * u < batch) v[u] = __ldg(src + b + 32 * u);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (b + 32 * u < batch) __stcs(dst + b + 32 * u, v[u]);
+  }
+}
+
 template <class T>
 int upload(T **dst, const T *src, int64_t n) {
   *dst = nullptr;
@@ -787,6 +807,9 @@ struct sgb_plan {
   int64_t *d_wk = nullptr, *d_wcopy = nullptr;
   uint32_t *d_csrc = nullptr;
   uint16_t *d_cpos = nullptr;
+  uint32_t *d_copy_k = nullptr;  // CSR position of every copy (win_k[w] + copy_pos[c]): batched CSR mode
+  bool batch_direct = false;     // batched CSR: window-member twins store their outputs, copies gathered
+  int64_t n_copy_k = 0;
   uint32_t *d_fbase = nullptr;
   // bulk feed of the CSR-window unit (UNIT_BULK): consumer blobs + value-array intervals per window
   uint8_t *d_wmeta = nullptr;
@@ -978,7 +1001,7 @@ void sgb_plan_destroy(sgb_plan *p) {
                   p->d_sop, p->d_scol, p->d_sdel, p->d_pos, p->d_x, p->d_out, p->d_cbase, p->d_coff,
                   p->d_obase, p->d_ooff, p->d_opos32, p->d_sopd, p->d_fbase, p->d_outputs32,
                   p->d_wpieces, p->d_wk, p->d_wcopy, p->d_csrc, p->d_cpos, p->d_x2, p->d_out2,
-                  p->d_wmeta, p->d_wmeta_off, p->d_wiv_off, p->d_wiv};
+                  p->d_wmeta, p->d_wmeta_off, p->d_wiv_off, p->d_wiv, p->d_copy_k};
   for (void *b : bufs)
     if (b) cudaFree(b);
   if (p->ws_stream) cudaStreamDestroy(p->ws_stream);
@@ -1478,6 +1501,46 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
     p->wb_bw = d->win_bw;
   }
   p->vas_slots = has_bulk ? d->value_array_size + (d->value_array_size & 1) : d->value_array_size;
+  if (has_window && d->n_outputs > 0) {
+    // batched CSR of a window plan: every output must come from exactly one value-mode twin
+    // position (FLAG_OPOS*) or one copy; otherwise batched CSR keeps the full gather
+    std::vector<uint8_t> hit((size_t)d->n_outputs, 0);
+    bool ok = true;
+    std::vector<uint32_t> copy_k((size_t)d->n_copy);
+    const int64_t n_win = d->n_win_k - 1;
+    for (int64_t w = 0; w < n_win && ok; ++w)
+      for (int64_t c = d->win_copy[w]; c < d->win_copy[w + 1]; ++c) {
+        const int64_t k = d->win_k[w] + d->copy_pos[c];
+        copy_k[(size_t)c] = (uint32_t)k;
+        ok = ok && k < d->n_outputs && ++hit[(size_t)k] == 1;
+      }
+    for (const Unit &u : p->units) {
+      if (!(u.flags & UNIT_VALUE_ONLY) || !ok) continue;
+      for (int g = u.g0; g < u.g1 && ok; ++g) {
+        const sgb_group &G = d->groups[g];
+        if (!(G.flags & (FLAG_OPOS16 | FLAG_OPOS32))) { ok = false; break; }
+        const int64_t nch = (G.n + 31) >> 5;
+        for (int r = 0; r < G.n_roots && ok; ++r)
+          for (int64_t i = 0; i < G.n; ++i) {
+            uint32_t o = NONE;
+            if (G.flags & FLAG_OPOS16) {
+              const uint16_t off = d->ooff[G.oo_off + (int64_t)r * G.n + i];
+              if (off != 0xFFFFu) o = d->obase[G.ob_off + (int64_t)r * nch + (i >> 5)] + off;
+            } else {
+              o = d->opos32[G.oo_off + (int64_t)r * G.n + i];
+            }
+            if (o == NONE) continue;
+            if ((int64_t)o >= d->n_outputs || ++hit[o] != 1) { ok = false; break; }
+          }
+      }
+    }
+    for (int64_t k = 0; k < d->n_outputs && ok; ++k) ok = hit[(size_t)k] == 1;
+    if (ok) {
+      if ((rc = upload(&p->d_copy_k, copy_k.data(), (int64_t)copy_k.size()))) return rc;
+      p->n_copy_k = (int64_t)copy_k.size();
+      p->batch_direct = true;
+    }
+  }
   p->T = Tables{p->d_groups, p->d_tape, p->d_imm, p->d_sop, p->d_scol, p->d_sdel, p->d_pos,
                 p->d_con, p->d_cbase, p->d_coff, p->d_obase, p->d_ooff, p->d_opos32, p->d_fbase};
   return 0;
@@ -1507,6 +1570,7 @@ static int launch_wave(sgb_plan *p, int wave, double *x, int64_t ld, int64_t bat
   for (int k : p->wave_units[wave]) {
     const Unit &u = p->units[k];
     if (!csr && (u.flags & UNIT_CSR_ONLY)) continue;
+    if (batched && (u.flags & UNIT_CSR_ONLY)) continue;            // single-set only (windows, copy groups)
     if (csr && !batched && (u.flags & UNIT_VALUE_ONLY)) continue;  // twins of CSR-window members
     if ((batched ? u.bt1 - u.bt0 : u.t1 - u.t0) <= 0) continue;
     us.push_back(&u);
@@ -1536,12 +1600,21 @@ static int launch_all(sgb_plan *p, double *x, int64_t ld, int64_t batch, bool ba
                       bool csr, cudaStream_t s) {
   std::lock_guard<std::mutex> lk(p->run_mu);
   const bool direct = csr && p->direct_csr && !batched;  // batched CSR: batched values + gather
+  // batched CSR of a CSR-window plan: the members' value-mode twins store their outputs directly
+  // (out[pos * ld_out + b], one warp per instance: coalesced), the other outputs are gathered
+  const bool bdirect = csr && batched && p->batch_direct;
   const int waves = direct ? p->csr_waves : p->n_waves;
   for (int w = 0; w < waves; ++w) {
-    int rc = launch_wave(p, w, x, ld, batch, batched, out, ld_out, direct, s);
+    int rc = launch_wave(p, w, x, ld, batch, batched, out, ld_out, direct || bdirect, s);
     if (rc) return rc;
   }
-  if (csr && !direct) {
+  if (bdirect) {
+    if (p->n_copy_k > 0) {
+      const int64_t blocks = (p->n_copy_k + 7) / 8;
+      gather_copies_batch<<<(unsigned)blocks, 256, 0, s>>>(x, ld, batch, p->d_copy_k, p->d_csrc, p->n_copy_k, out,
+                                                           ld_out);
+    }
+  } else if (csr && !direct) {
     int rc = launch_gather(p, x, ld, batch, batched, out, ld_out, s);
     if (rc) return rc;
   }

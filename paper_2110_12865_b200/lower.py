@@ -1435,8 +1435,8 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         in_window = window is not None and kl.index in window
         groups.append(_Group(kl.kind, flags, n, kp.n_roots, kp.dest_base, kp.p_base, kp.c_base,
                              len(kp.const_vars), kl.slot_col, kl.slot_delta, cols, kp.layout, kl.wave,
-                             kl.n_regs, kl.tape, kl.imms, kl.sop, None if in_window else opos[kl.index],
-                             kl.index, window_value=in_window))
+                             kl.n_regs, kl.tape, kl.imms, kl.sop, opos[kl.index],  # (twins: batched CSR
+                             kl.index, window_value=in_window))                    # stores them directly)
         if in_window:
             win_groups.append(_Group(kl.kind, flags | FLAG_CSR_ONLY | FLAG_WPOS16, n, kp.n_roots, kp.dest_base,
                                      kp.p_base, kp.c_base, len(kp.const_vars), kl.slot_col, kl.slot_delta, cols,

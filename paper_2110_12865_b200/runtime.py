@@ -469,7 +469,9 @@ class DevicePlan:
         return X
 
     def run_batch_csr(self, X, out=None, stream=None):
-        """Batched CSR mode: out[k, b] = value of output k in value set b (no gather pass)."""
+        """Batched CSR mode: out[k, b] = value of output k in value set b (CSR-window plans: the members'
+        value-mode twins store their outputs directly, only the copied outputs are gathered; otherwise
+        batched values + one gather)."""
         import torch
 
         self._check_tensor(X, self.value_array_size, "X")

@@ -148,8 +148,18 @@ def shard_device_plan(plan, lowered, lo: int, hi: int):
         raise ValueError("output sharding needs the reference value-array layout (csr_layout off)")
     if int(lowered.needs_zero) == 2:
         raise ValueError("output sharding needs a plan without reads before writes")
-    if np.any(lowered.groups["flags"] & (L.FLAG_OPOS16 | L.FLAG_OPOS32)):
+    # the value-mode twins of CSR-window members carry output positions for batched CSR only (not a
+    # mode of the shard): the view drops them
+    twins = np.zeros(len(lowered.groups), bool)
+    for u in range(len(lowered.units)):
+        ur = lowered.unit(u)
+        if ur["flags"] & L.UNIT_VALUE_ONLY:
+            twins[ur["group_begin"]: ur["group_end"]] = True
+    opos_flags = L.FLAG_OPOS16 | L.FLAG_OPOS32
+    if np.any((lowered.groups["flags"] & opos_flags) & ~twins):
         raise ValueError("output sharding supports the gather and CSR-window output modes only")
+    groups = np.array(lowered.groups, copy=True)
+    groups["flags"] = np.where(twins, groups["flags"] & ~opos_flags, groups["flags"])
     wn = getattr(lowered, "windows", None)
     w0 = w1 = 0
     if wn is not None:  # keep the windows [w0, w1) that make up [lo, hi), re-based to the shard
@@ -193,7 +203,7 @@ def shard_device_plan(plan, lowered, lo: int, hi: int):
         swn = dataclasses.replace(wn, k=np.asarray(wn.k[w0: w1 + 1], np.int64) - lo, pieces=wn.pieces[w0:w1],
                                   copy_off=np.asarray(wn.copy_off[w0: w1 + 1], np.int64) - c0,
                                   copy_src=wn.copy_src[c0:c1], copy_pos=wn.copy_pos[c0:c1])
-    lw = dataclasses.replace(lowered, tiles=new_tiles.reshape(-1, 2), units=units,
+    lw = dataclasses.replace(lowered, tiles=new_tiles.reshape(-1, 2), units=units, groups=groups,
                              outputs=np.asarray(lowered.outputs, np.int64)[lo:hi], tiles_alt=None, windows=swn)
     return view, lw
 

@@ -89,6 +89,15 @@ def test_builder_plans_default_lowering(name, relayout, wbulk):
     graph.replay()
     torch.cuda.synchronize()
     assert np.array_equal(bits(out.cpu().numpy()), bits(want))
+    # batched CSR (window plans: the members' value-mode twins store their outputs, copies gathered)
+    rng = np.random.default_rng(5)
+    sets = [inputs] + [inputs * rng.uniform(0.9, 1.1, inputs.size) for _ in range(2)]
+    X = torch.zeros((dp.value_array_size, 3), dtype=torch.float64, device="cuda")
+    X[: dp.input_count] = torch.from_numpy(np.stack(sets, axis=1)).cuda()
+    outb = dp.run_batch_csr(X)
+    torch.cuda.synchronize()
+    for j, ins in enumerate(sets):
+        assert np.array_equal(bits(outb[:, j].cpu().numpy()), bits(oracle.run_outputs(plan, ins)))
     if name.startswith("lmlt"):
         assert dp.lowered.windows is not None  # the CSR windows ran
 
