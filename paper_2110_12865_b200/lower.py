@@ -791,6 +791,9 @@ WIN_ROWS = 240  # anchor instances per CSR window (block of JIT_BLOCK threads: 1
 WIN_MAX = 6144  # outputs per CSR window (48 KB of shared memory; 7936 measured 3 % slower on C2, r2o)
 WIN_MIN = 1024  # windows are not cut shorter than this unless the anchor forces it
 WIN_MAX_LOADS = 32  # default lowering: windows only when every member loads at most this many slots
+# batched CSR of a window plan: the members' value-mode twins store their outputs directly (they get
+# output positions; sgb.cu batch_direct) instead of batched values + one gather
+BATCH_DIRECT = False
 
 
 @dataclass
@@ -1435,8 +1438,9 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         in_window = window is not None and kl.index in window
         groups.append(_Group(kl.kind, flags, n, kp.n_roots, kp.dest_base, kp.p_base, kp.c_base,
                              len(kp.const_vars), kl.slot_col, kl.slot_delta, cols, kp.layout, kl.wave,
-                             kl.n_regs, kl.tape, kl.imms, kl.sop, opos[kl.index],  # (twins: batched CSR
-                             kl.index, window_value=in_window))                    # stores them directly)
+                             kl.n_regs, kl.tape, kl.imms, kl.sop,
+                             opos[kl.index] if not in_window or BATCH_DIRECT else None,
+                             kl.index, window_value=in_window))
         if in_window:
             win_groups.append(_Group(kl.kind, flags | FLAG_CSR_ONLY | FLAG_WPOS16, n, kp.n_roots, kp.dest_base,
                                      kp.p_base, kp.c_base, len(kp.const_vars), kl.slot_col, kl.slot_delta, cols,
