@@ -28,6 +28,7 @@ from __future__ import annotations
 import ctypes
 import hashlib
 import os
+import re
 import struct
 from pathlib import Path
 
@@ -130,8 +131,10 @@ def _out_pos(rec, r: int, i: str = "i") -> str | None:
     f = int(rec["flags"])
     if f & L.FLAG_OPOS16:
         nch = (n + 31) // 32
+        # both loads issued together (the base does not depend on the offset)
         return (f"[&]() {{ const u16 o_ = __ldcs(T.ooff + {_off(int(rec['oo_off']) + r * n)} + {i}); "
-                f"return o_ == 0xFFFF ? NONE : __ldg(T.obase + {_off(int(rec['ob_off']) + r * nch)} + ({i} >> 5)) + o_; }}()")
+                f"const u32 b_ = __ldg(T.obase + {_off(int(rec['ob_off']) + r * nch)} + ({i} >> 5)); "
+                f"return o_ == 0xFFFF ? NONE : b_ + o_; }}()")
     if f & L.FLAG_OPOS32:
         return f"__ldcs(T.opos32 + {_off(int(rec['oo_off']) + r * n)} + {i})"
     return None
@@ -194,6 +197,11 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
                          f"{G(f'__ldcs(T.ooff + {_off(oo_off + r * n)} + {i})', '(u16)0xFFFF')};")
     stream = bool(flags & L.FLAG_STREAM)
     opos = lambda r: _out_pos(rec, r, i)  # noqa: E731
+    if not window:  # output positions (direct CSR stores) load with the operands, not after the compute
+        for r in range(int(rec["n_roots"])):
+            if _out_pos(rec, r) is not None and (keep is None or any(
+                    t[0] == L.T_ST and t[7] == r and j in keep for j, t in enumerate(tape.tolist()))):
+                loads.append(f"const u32 op{r}{sfx} = ({guard or 'true'}) && csr ? {opos(r)} : NONE;")
     for j, t in enumerate(tape.tolist()):
         if keep is not None and j not in keep:
             continue
@@ -217,8 +225,8 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
             store = f"st_stream({x_addr}, {v});" if stream else f"*({x_addr}) = {v};"
             comp.append(f"if (ok{sfx}{' && !csr' if stream else ''}) {store}")
             if _out_pos(rec, r) is not None:
-                dst_o = f"out[(u64)o * ld_out + {bv}]" if batched else "out[o]"
-                comp.append(f"if (ok{sfx} && csr) {{ const u32 o = {opos(r)}; if (o != NONE) {dst_o} = {v}; }}")
+                dst_o = f"out[(u64)op{r}{sfx} * ld_out + {bv}]" if batched else f"out[op{r}{sfx}]"
+                comp.append(f"if (ok{sfx} && op{r}{sfx} != NONE) {dst_o} = {v};")
             continue
         if op == L.T_IMM:
             expr = _imm(imms[aux])
@@ -255,8 +263,12 @@ def group_batch_body(dp, gi, tape, imms, vec: int) -> list[str]:
         if shared is None:
             shared = [ln for ln in ld if ln.startswith(f"const {_idx_t(False)} idx0")]
             lines = shared[:1] + lines if shared else lines
-        ld = [ln.replace(f"idx0_{v}", "idx0_0") for ln in ld if not ln.startswith(f"const {_idx_t(False)} idx0")]
+            opl = [ln for ln in ld if ln.startswith("const u32 op")]  # output positions: per instance
+            lines = opl + lines
+        ld = [ln.replace(f"idx0_{v}", "idx0_0") for ln in ld
+              if not ln.startswith(f"const {_idx_t(False)} idx0") and not ln.startswith("const u32 op")]
         cp = [ln.replace(f"idx0_{v}", "idx0_0") for ln in cp]
+        cp = [re.sub(rf"\bop(\d+)_{v}\b", r"op\1_0", ln) for ln in cp]
         lines += ld
         comps += cp
     if shared:

@@ -790,6 +790,8 @@ def _window_members(plan, lowered, opos, n_waves):
 WIN_ROWS = 240  # anchor instances per CSR window (block of JIT_BLOCK threads: 16 lanes of slack)
 WIN_MAX = 6144  # outputs per CSR window (48 KB of shared memory; 7936 measured 3 % slower on C2, r2o)
 WIN_MIN = 1024  # windows are not cut shorter than this unless the anchor forces it
+WIN_SLOTS = 148 * 3  # windows resident at once (B200 SMs x the window kernel's blocks per SM)
+WIN_BALANCE = True  # cut whole rounds of resident windows (lower_plan)
 WIN_MAX_LOADS = 32  # default lowering: windows only when every member loads at most this many slots
 # batched CSR of a window plan: the members' value-mode twins store their outputs directly (they get
 # output positions; sgb.cu batch_direct) instead of batched values + one gather
@@ -1449,7 +1451,28 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     windows = None
     if window is not None:
         # members in kernel order == their order in the window unit (pieces columns)
-        windows = _csr_windows([opos[g.kernel] for g in win_groups], len(plan.outputs), res_k, res_addr)
+        mo = [opos[g.kernel] for g in win_groups]
+        windows = _csr_windows(mo, len(plan.outputs), res_k, res_addr)
+        # whole rounds of resident windows: one block per window, WIN_SLOTS resident at once -- a last
+        # round of a few windows would leave the chip idle for a whole window's time
+        n_win = windows.k.size - 1
+        if WIN_BALANCE and n_win > WIN_SLOTS and n_win % WIN_SLOTS:
+            rounds, rem = divmod(n_win, WIN_SLOTS)
+            targets = ([rounds * WIN_SLOTS] if rem < WIN_SLOTS // 2 else []) + [(rounds + 1) * WIN_SLOTS]
+            done = False
+            for target in targets:
+                rows = max(8, int(WIN_ROWS * n_win / target))
+                for _ in range(6):  # the count falls with rows (cuts snap): step rows until it lands
+                    cand = _csr_windows(mo, len(plan.outputs), res_k, res_addr, rows=rows)
+                    n_cur = cand.k.size - 1
+                    if target - WIN_SLOTS // 8 <= n_cur <= target:
+                        windows, done = cand, True
+                        break
+                    if n_cur > n_win and target < n_win:  # bigger windows hit WIN_MAX: not reachable
+                        break
+                    rows += 1 if n_cur > target else -1
+                if done:
+                    break
         for g, wp in zip(win_groups, windows.wpos):
             g.wpos = wp
     extra_pos = []
