@@ -791,11 +791,11 @@ WIN_ROWS = 240  # anchor instances per CSR window (block of JIT_BLOCK threads: 1
 WIN_MAX = 6144  # outputs per CSR window (48 KB of shared memory; 7936 measured 3 % slower on C2, r2o)
 WIN_MIN = 1024  # windows are not cut shorter than this unless the anchor forces it
 WIN_SLOTS = 148 * 3  # windows resident at once (B200 SMs x the window kernel's blocks per SM)
-WIN_BALANCE = True  # cut whole rounds of resident windows (lower_plan)
+WIN_BALANCE = False  # cut whole rounds of resident windows (lower_plan): C2 window 0.1275 -> 0.1292 ms, off (r2v)
 WIN_MAX_LOADS = 32  # default lowering: windows only when every member loads at most this many slots
 # batched CSR of a window plan: the members' value-mode twins store their outputs directly (they get
 # output positions; sgb.cu batch_direct) instead of batched values + one gather
-BATCH_DIRECT = False
+BATCH_DIRECT = True  # C5: 2.46 -> 2.12 ms (r2v)
 
 
 @dataclass
@@ -1421,8 +1421,12 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
     avail = _owner_waves(plan, waves, res_addr) + 1  # first wave that may read the source
     last = max(n_waves - 1, 0)
     copy_sets = [(min(last, n_waves), avail <= last), (n_waves, avail > last)]
-    # stream flags: results no later kernel (or copy group) reads
+    # stream flags: results no later kernel (or copy group) reads -- nor the output gather: its
+    # reads should hit L2, not follow evict-first streaming stores (gather mode: no windows, no
+    # direct positions)
     reads = [r for r in read_sets if r.size] + ([res_addr] if res_addr.size else [])
+    if window is None and not direct_csr and len(plan.outputs):
+        reads.append(np.asarray(plan.outputs, np.int64))
     allr = unique_addresses(np.concatenate(reads)) if reads else np.zeros(0, np.int64)
     groups: list[_Group] = []
     win_groups: list[_Group] = []  # window members (CSR-only records; value-mode twins stay in `groups`)
