@@ -31,8 +31,8 @@ def main():
     key, plan = bench.build_workload("c3", ns)
     ins = bench.workload_inputs("c3", ns, 0)
     want = None
-    for split in (1, 2, 3, 1):
-        lower.JIT_SPLIT = split
+    for split, early in ((1, False), (1, True), (2, True), (1, False)):
+        lower.JIT_SPLIT, lower.STORE_ROOTS_EARLY = split, early
         t0 = time.perf_counter()
         lw = lower_plan(plan, relayout="auto")
         t_low = time.perf_counter() - t0
@@ -55,7 +55,7 @@ def main():
             torch.cuda.synchronize()
             tw = sorted(e0.elapsed_time(e1) for e0, e1 in evs)
             per.append(round(tw[len(tw) // 2], 4))
-        print(f"split={split} same_bits_as_first={ok} waves {per} tiles {dp.tile_order} "
+        print(f"split={split} early={early} same_bits_as_first={ok} waves {per} tiles {dp.tile_order} "
               f"(lower {t_low:.0f}s)", flush=True)
         del dp
 
