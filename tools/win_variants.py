@@ -30,10 +30,9 @@ def main():
     ins = bench.workload_inputs("c2", ns, 0)
     ref = DevicePlan(plan, lowered=lower_plan(plan, csr_window=False))
     want = ref.run_csr(ref.new_values(ins)).cpu().numpy()
-    variants = [dict(ovl=o, loads=l_, ovl_loads=ol) for o, l_, ol in
-                ((False, 32, 9), (True, 32, 9), (True, 32, 3), (True, 28, 6), (False, 32, 9), (True, 32, 9))]
+    variants = [dict(persistent=p_) for p_ in (False, True, False, True)]
     for v in variants:
-        jit.WINDOW_COPY_OVERLAP, jit.WINDOW_LOADS, jit.COPY_OVERLAP_LOADS = v["ovl"], v["loads"], v["ovl_loads"]
+        lower.WIN_PERSISTENT = v["persistent"]
         v["wbulk"] = False
         t0 = time.perf_counter()
         lw = lower_plan(plan, csr_window=True, wbulk=v["wbulk"])
