@@ -791,7 +791,7 @@ WIN_ROWS = 240  # anchor instances per CSR window (block of JIT_BLOCK threads: 1
 WIN_MAX = 6144  # outputs per CSR window (48 KB of shared memory; 7936 measured 3 % slower on C2, r2o)
 WIN_MIN = 1024  # windows are not cut shorter than this unless the anchor forces it
 WIN_SLOTS = 148 * 3  # windows resident at once (B200 SMs x the window kernel's blocks per SM)
-WIN_PERSISTENT = False  # window unit on a persistent grid (sgb.cu), the next window's header prefetched
+WIN_PERSISTENT = False  # persistent window grid + next-header prefetch: 0.1274 -> 0.1725 ms on C2 (concurrent windows drift apart in L2, r2x)
 WIN_BALANCE = False  # cut whole rounds of resident windows (lower_plan): C2 window 0.1275 -> 0.1292 ms, off (r2v)
 WIN_MAX_LOADS = 32  # default lowering: windows only when every member loads at most this many slots
 # batched CSR of a window plan: the members' value-mode twins store their outputs directly (they get
