@@ -813,7 +813,7 @@ class CsrWindows:
 
 
 def _csr_windows(member_opos: list, n_out: int, copy_k: np.ndarray, copy_addr: np.ndarray,
-                 rows: int | None = None, wmax: int | None = None) -> CsrWindows:
+                 rows: int | None = None, wmax: int | None = None, wmin: int | None = None) -> CsrWindows:
     """Cut the CSR value array into windows for the window unit (jit.window_source).
 
     ``member_opos``: per member group its (R, N) CSR positions (NONE32 = not an output), first
@@ -826,6 +826,8 @@ def _csr_windows(member_opos: list, n_out: int, copy_k: np.ndarray, copy_addr: n
     """
     rows = WIN_ROWS if rows is None else rows
     wmax = WIN_MAX if wmax is None else wmax
+    # small plans: windows down to n_out / WIN_SLOTS outputs, so every resident slot gets one
+    wmin = min(WIN_MIN, max(128, n_out // WIN_SLOTS)) if wmin is None else wmin
     big = np.iinfo(np.int64).max
     firsts, lasts = [], []
     for o in member_opos:
@@ -861,9 +863,9 @@ def _csr_windows(member_opos: list, n_out: int, copy_k: np.ndarray, copy_addr: n
         # the next preferred cut, if the window stays within wmax; else the last allowed cut in reach
         j = np.searchsorted(pref, cur, side="right")
         nxt = int(pref[j]) if j < pref.size and pref[j] <= lim else None
-        if nxt is not None and nxt - cur < WIN_MIN and j + 1 < pref.size and pref[j + 1] <= lim:
-            # tiny windows (anchor sparse here): merge preferred steps up to WIN_MIN
-            jj = np.searchsorted(pref, min(lim, cur + WIN_MIN), side="right") - 1
+        if nxt is not None and nxt - cur < wmin and j + 1 < pref.size and pref[j + 1] <= lim:
+            # tiny windows (anchor sparse here): merge preferred steps up to wmin
+            jj = np.searchsorted(pref, min(lim, cur + wmin), side="right") - 1
             nxt = int(pref[max(jj, j)])
         if nxt is None:
             jj = np.searchsorted(allowed, lim, side="right") - 1
