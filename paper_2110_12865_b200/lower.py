@@ -792,6 +792,7 @@ WIN_MAX = 6144  # outputs per CSR window (48 KB of shared memory; 7936 measured 
 WIN_MIN = 1024  # windows are not cut shorter than this unless the anchor forces it
 WIN_SLOTS = 148 * 3  # windows resident at once (B200 SMs x the window kernel's blocks per SM)
 WIN_PERSISTENT = False  # persistent window grid + next-header prefetch: 0.1274 -> 0.1725 ms on C2 (concurrent windows drift apart in L2, r2x)
+WIN_BALANCE_ROUNDS = 4  # ... always below this many rounds (plan shards, small plans: a partial round is a big tail)
 WIN_BALANCE = False  # cut whole rounds of resident windows (lower_plan): C2 window 0.1275 -> 0.1292 ms, off (r2v)
 WIN_MAX_LOADS = 32  # default lowering: windows only when every member loads at most this many slots
 # batched CSR of a window plan: the members' value-mode twins store their outputs directly (they get
@@ -1463,22 +1464,21 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
         # whole rounds of resident windows: one block per window, WIN_SLOTS resident at once -- a last
         # round of a few windows would leave the chip idle for a whole window's time
         n_win = windows.k.size - 1
-        if WIN_BALANCE and n_win > WIN_SLOTS and n_win % WIN_SLOTS:
+        if n_win % WIN_SLOTS and (WIN_BALANCE or n_win < WIN_BALANCE_ROUNDS * WIN_SLOTS):
             rounds, rem = divmod(n_win, WIN_SLOTS)
-            targets = ([rounds * WIN_SLOTS] if rem < WIN_SLOTS // 2 else []) + [(rounds + 1) * WIN_SLOTS]
-            done = False
-            for target in targets:
-                rows = max(8, int(WIN_ROWS * n_win / target))
-                for _ in range(6):  # the count falls with rows (cuts snap): step rows until it lands
-                    cand = _csr_windows(mo, len(plan.outputs), res_k, res_addr, rows=rows)
+            targets = ([rounds * WIN_SLOTS] if rounds and rem < WIN_SLOTS // 2 else []) + [(rounds + 1) * WIN_SLOTS]
+            for target in targets:  # the count falls with rows: bisect rows (no small-window merging)
+                lo_r, hi_r, best = 8, 4 * WIN_ROWS, None
+                while lo_r <= hi_r:
+                    mid = (lo_r + hi_r) // 2
+                    cand = _csr_windows(mo, len(plan.outputs), res_k, res_addr, rows=mid, wmin=0)
                     n_cur = cand.k.size - 1
-                    if target - WIN_SLOTS // 8 <= n_cur <= target:
-                        windows, done = cand, True
-                        break
-                    if n_cur > n_win and target < n_win:  # bigger windows hit WIN_MAX: not reachable
-                        break
-                    rows += 1 if n_cur > target else -1
-                if done:
+                    if n_cur <= target:
+                        best, hi_r = (cand, n_cur), mid - 1
+                    else:
+                        lo_r = mid + 1
+                if best is not None and best[1] >= target - WIN_SLOTS // 8:
+                    windows = best[0]
                     break
         for g, wp in zip(win_groups, windows.wpos):
             g.wpos = wp
