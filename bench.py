@@ -424,7 +424,10 @@ def measure_eval(cfg: str, args, rank: int, world: int, barrier, split=None) -> 
                       "index_entries_kept": int(plan.positions.size),
                       "index_entries_full": int(np.asarray(full_plan.positions).size),
                       "kernels_kept": len(plan.kernels)}
-        dp = DevicePlan(plan, device=local, csr_layout=True)
+        from paper_2110_12865_b200.shard import shard_device
+
+        view, lw = shard_device(plan, relayout=os.environ.get("SGB_RELAYOUT", "auto"))
+        dp = DevicePlan(view, device=local, lowered=lw)
         inputs = workload_inputs(cfg, args, seed=0, plan=full_plan)
     else:
         inputs = workload_inputs(cfg, args, seed=rank, plan=plan)

@@ -211,6 +211,20 @@ def shard_device_plan(plan, lowered, lo: int, hi: int):
 UNIT_TB, UNIT_TE = 5, 6  # lower.UNIT_FIELDS tile_begin / tile_end
 
 
+def shard_device(shard, relayout="auto", **lower_kw):
+    """(plan, lowered) one rank runs for a plan shard (``shard_plan``): the shard's own lowering and,
+    where it keeps the reference value-array layout, its launch tiles filtered to the instances its
+    outputs need -- shard_plan keeps multi-root and self-referencing kernels whole (their result
+    stride is N), the tile filter (``shard_device_plan`` over all of the shard's outputs) then skips
+    their unneeded instances (C2's face kernel: every rank evaluated all 2M faces)."""
+    from .lower import lower_plan
+
+    lw = lower_plan(shard, relayout=relayout, **lower_kw)
+    if getattr(lw, "csr_layout", None) or int(lw.needs_zero) == 2:
+        return shard, lw
+    return shard_device_plan(shard, lw, 0, len(shard.outputs))
+
+
 def shard_plan(plan, lo: int, hi: int):
     """The plan shard of the CSR outputs [lo, hi): an ExecutionPlan of its own (codegen.py:88-98
     fields), every kernel cut to the instance range its outputs' producer cone needs.

@@ -488,3 +488,25 @@ def test_device_transcendentals_match_glibc_bitwise(op, jit):
     assert np.array_equal(np.isnan(got), nan)
     bad = np.flatnonzero(bits(got[~nan]) != bits(want[~nan]))
     assert bad.size == 0, f"{bad.size} of {xs.size} differ, e.g. {xs[~nan][bad[:3]]}"
+
+
+@pytest.mark.parametrize("world", [4])
+def test_plan_shards_on_device(world):
+    """bench.py's --split outputs path: each rank's own plan (shard.shard_plan) lowered with its
+    whole-kept kernels' tiles filtered (shard.shard_device), on the device == the full evaluation's
+    CSR slice, bit for bit."""
+    import torch
+
+    from oracle import oracle
+    from paper_2110_12865_b200 import DevicePlan
+    from paper_2110_12865_b200.shard import shard_device, shard_outputs, shard_plan
+
+    plan, inputs = builder_plan("lmlt_w70")
+    full = oracle.run_outputs(plan, inputs)
+    for r in (0, world - 1):
+        lo, hi = shard_outputs(len(plan.outputs), world, r)
+        view, lw = shard_device(shard_plan(plan, lo, hi), relayout=False)
+        dp = DevicePlan(view, lowered=lw)
+        out = dp.run_csr(dp.new_values(inputs))
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(out.cpu().numpy()), bits(full[lo:hi]))

@@ -251,6 +251,31 @@ def test_plan_shards_are_plans_of_their_own(name, world):
                 assert np.allclose(got, full[lo:hi], rtol=1e-12, atol=1e-12)
 
 
+@pytest.mark.parametrize("world", [2, 8])
+def test_shard_device_filters_the_kernels_kept_whole(world):
+    """shard.shard_device: a rank's shard lowered and its whole-kept (multi-root) kernels' tiles cut to
+    the instances its outputs need -- fewer tiles than the shard's own lowering, the same CSR slice
+    bit for bit (emulated over the filtered tiles)."""
+    from conftest import bits
+
+    import device_plan_emu as emu
+    from oracle import oracle
+    from paper_2110_12865_b200 import lower_plan
+    from paper_2110_12865_b200.programs.mesh import build_lmlt_plan, lmlt_inputs
+    from paper_2110_12865_b200.shard import shard_device, shard_outputs, shard_plan
+
+    plan = build_lmlt_plan(48)[0]
+    ins = lmlt_inputs(48, seed=2)
+    full = oracle.run_outputs(plan, ins)
+    for r in (0, world - 1):
+        lo, hi = shard_outputs(len(plan.outputs), world, r)
+        sp = shard_plan(plan, lo, hi)
+        view, lw = shard_device(sp, relayout=False, jit_compile=False)
+        assert np.asarray(lw.tiles).shape[0] < np.asarray(lower_plan(sp, relayout=False, jit_compile=False).tiles).shape[0]
+        got = emu.run_csr(lw, ins, by_tiles=True)
+        assert np.array_equal(bits(got), bits(full[lo:hi]))
+
+
 def test_plan_shards_hold_their_share_of_the_tables():
     """On a mesh plan 8 shards together hold about one copy of the index tables (the cone overlap
     is a few grid rows per boundary, multi-root kernels whole), not 8."""
