@@ -220,8 +220,10 @@ def shard_device(shard, relayout="auto", **lower_kw):
     from .lower import lower_plan
 
     lw = lower_plan(shard, relayout=relayout, **lower_kw)
-    if getattr(lw, "csr_layout", None) or int(lw.needs_zero) == 2:
+    if int(lw.needs_zero) == 2:
         return shard, lw
+    if getattr(lw, "csr_layout", None):  # the tile filter needs the reference layout; whole multi-root
+        lw = lower_plan(shard, relayout=False, **lower_kw)  # kernels per rank would cost more (C3)
     return shard_device_plan(shard, lw, 0, len(shard.outputs))
 
 
