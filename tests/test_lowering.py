@@ -213,3 +213,25 @@ def test_relaid_plan_remap_is_a_bijection():
         kp = plan.kernels[k]
         r, i = 1, kp.instances - 1
         assert b[kp.dest_base + r * kp.instances + i] == kp.dest_base + i * kp.n_roots + r
+
+
+def test_window_rounds_are_balanced(monkeypatch):
+    """Between one and WIN_BALANCE_ROUNDS rounds of resident windows the lowering re-chooses the rows
+    per window for whole rounds; the windows still cover every output once, bit for bit."""
+    from paper_2110_12865_b200.programs.mesh import build_lmlt_plan, lmlt_inputs
+
+    from oracle import oracle
+
+    plan, _, _ = build_lmlt_plan(40)
+    monkeypatch.setattr(L, "WIN_ROWS", 64)
+    monkeypatch.setattr(L, "WIN_BALANCE_ROUNDS", 1000)
+    base = lower_plan(plan, csr_window=True, jit_compile=False)
+    n0 = base.windows.k.size - 1
+    slots = max(2, n0 // 3 + 1)  # a partial last round
+    monkeypatch.setattr(L, "WIN_SLOTS", slots)
+    dp = lower_plan(plan, csr_window=True, jit_compile=False)
+    n = dp.windows.k.size - 1
+    assert n % slots == 0 or n >= (n // slots) * slots + slots - slots // 8, (n0, n, slots)
+    assert np.all(np.diff(dp.windows.k) > 0) and np.diff(dp.windows.k).max() <= L.WIN_MAX
+    ins = lmlt_inputs(40, seed=5)
+    assert np.array_equal(bits(emu.run_csr(dp, ins)), bits(oracle.run_outputs(plan, ins)))
