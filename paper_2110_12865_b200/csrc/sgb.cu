@@ -1307,10 +1307,6 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
         SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, u.jit, u.bs, (size_t)u.regs));
         u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
         if (u.grid > u.t1 - u.t0) u.grid = u.t1 - u.t0;
-      } else if (window && u.variant == 2) {  // persistent: blocks walk windows, prefetching the next header
-        SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, u.jit, u.bs, (size_t)u.regs));
-        u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
-        if (u.grid > u.t1 - u.t0) u.grid = u.t1 - u.t0;
       } else if (window) {
         u.grid = u.t1 - u.t0;  // one block per window, dispatched in CSR order
       } else if (jit) {

@@ -495,8 +495,6 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
     unit = dp.unit(u)
     g0, g1 = unit["group_begin"], unit["group_end"]
     J = g1 - g0
-    if J > JIT_BLOCK:
-        raise ValueError(f"CSR-window unit {u}: {J} members exceed the block's {JIT_BLOCK} threads")
     chunks, cur, width = [], [], 0
     for gi in range(g0, g1):
         rec = dp.groups[gi]
@@ -518,25 +516,11 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
            "  extern __shared__ __align__(16) double buf[];",
            f"  __shared__ int2 sp[{J}];",
            "  const int tid = threadIdx.x;",
-           # the window header (pieces, output and copy ranges); a persistent grid (unit variant 2)
-           # loads the next window's header while this one runs
-           "  i64 w = blockIdx.x;",
-           f"  int2 hp_ = (w < n_win && tid < {J}) ? __ldg(pieces + w * {J} + tid) : make_int2(0, 0);",
-           "  i64 hk0_ = w < n_win ? __ldg(win_k + w) : 0, hk1_ = w < n_win ? __ldg(win_k + w + 1) : 0;",
-           "  i64 hc0_ = w < n_win ? __ldg(copy_off + w) : 0, hc1_ = w < n_win ? __ldg(copy_off + w + 1) : 0;",
-           "  for (; w < n_win; w += gridDim.x) {",
-           f"    if (tid < {J}) sp[tid] = hp_;",
-           "    const i64 k0 = hk0_;",
-           "    const u32 len_ = (u32)(hk1_ - k0);",
-           "    const i64 c0_ = hc0_, c1_ = hc1_;",
-           "    {  // prefetch the next window's header (registers; stored to sp after this window)",
-           "      const i64 wn = w + gridDim.x;",
-           "      if (wn < n_win) {",
-           f"        if (tid < {J}) hp_ = __ldg(pieces + wn * {J} + tid);",
-           "        hk0_ = __ldg(win_k + wn); hk1_ = __ldg(win_k + wn + 1);",
-           "        hc0_ = __ldg(copy_off + wn); hc1_ = __ldg(copy_off + wn + 1);",
-           "      }",
-           "    }",
+           "  for (i64 w = blockIdx.x; w < n_win; w += gridDim.x) {",
+           f"    for (int j = tid; j < {J}; j += {B}) sp[j] = __ldg(pieces + w * {J} + j);",
+           "    const i64 k0 = __ldg(win_k + w);",
+           "    const u32 len_ = (u32)(__ldg(win_k + w + 1) - k0);",
+           "    const i64 c0_ = __ldg(copy_off + w), c1_ = __ldg(copy_off + w + 1);",
            "    // window position p at bw[p]: out + k0 - head_ is 16-byte aligned, so is buf",
            "    const u32 head_ = (u32)((reinterpret_cast<u64>(out + k0) >> 3) & 1ull);",
            "    double *bw = buf + head_;",

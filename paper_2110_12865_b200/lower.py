@@ -791,7 +791,6 @@ WIN_ROWS = 240  # anchor instances per CSR window (block of JIT_BLOCK threads: 1
 WIN_MAX = 6144  # outputs per CSR window (48 KB of shared memory; 7936 measured 3 % slower on C2, r2o)
 WIN_MIN = 1024  # windows are not cut shorter than this unless the anchor forces it
 WIN_SLOTS = 148 * 3  # windows resident at once (B200 SMs x the window kernel's blocks per SM)
-WIN_PERSISTENT = False  # persistent window grid + next-header prefetch: 0.1274 -> 0.1725 ms on C2 (concurrent windows drift apart in L2, r2x)
 WIN_BALANCE_ROUNDS = 4  # ... always below this many rounds (plan shards, small plans: a partial round is a big tail)
 WIN_BALANCE = False  # cut whole rounds of resident windows (lower_plan): C2 window 0.1275 -> 0.1292 ms, off (r2v)
 WIN_MAX_LOADS = 32  # default lowering: windows only when every member loads at most this many slots
@@ -1651,9 +1650,10 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                 n_win = windows.k.size - 1
                 window_units.append((len(units), 0, n_win))
                 smem = 8 * (int(np.diff(windows.k).max(initial=0)) + 2)  # + alignment slots
-                # variant 2: a persistent grid (each block walks windows, prefetching the next one's
-                # header); 1: one block per window
-                units.append((w, kind, 2 if WIN_PERSISTENT else 1, g_begin, len(order_groups), 0, n_win, bs, smem,
+                # one block per window, dispatched in CSR order (a persistent grid prefetching the next
+                # window's header measured 0.1274 -> 0.1725 ms on C2: concurrently running windows drift
+                # apart and stop sharing the L2-resident intermediates, r2x)
+                units.append((w, kind, variant, g_begin, len(order_groups), 0, n_win, bs, smem,
                               UNIT_CSR_ONLY | UNIT_JIT | UNIT_WINDOW))
                 jit_units.append(len(units) - 1)
                 continue
