@@ -164,6 +164,11 @@ int sgb_run_values(sgb_plan *plan, double *x_dev, void *stream);
  * u32-indexed gather copies the outputs. */
 int sgb_run_csr(sgb_plan *plan, double *x_dev, double *out_dev, void *stream);
 
+/* inputs -> CSR values on device buffers: inputs_dev[input_count] -> out_dev[n_outputs] (SURVEY.md
+ * §8(b)), through the plan's own value-array workspace; stream-ordered, no host synchronisation.
+ * Calls sharing a plan serialise on that workspace (one evaluation in flight per plan). */
+int sgb_run_inputs_csr(sgb_plan *plan, const double *inputs_dev, double *out_dev, void *stream);
+
 /* One dependency wave (waves in order 0..sgb_plan_waves(plan, csr)-1); out_dev
  * NULL = value mode (sgb_run_values), else CSR mode (sgb_run_csr).  For
  * per-launch timing and profiling. */

@@ -828,6 +828,7 @@ struct sgb_plan {
   std::vector<cudaStream_t> aux;
   std::vector<cudaEvent_t> ev_join;
   cudaEvent_t ev_fork = nullptr;
+  cudaEvent_t ws_event = nullptr;  // last device-side use of the workspace by sgb_run_inputs_csr
   std::mutex run_mu;  // the aux streams / events are per plan: one launch sequence at a time
 };
 
@@ -1011,6 +1012,7 @@ void sgb_plan_destroy(sgb_plan *p) {
   for (cudaStream_t a : p->aux) cudaStreamDestroy(a);
   for (cudaEvent_t e : p->ev_join) cudaEventDestroy(e);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ws_event) cudaEventDestroy(p->ws_event);
   delete p;
 }
 
@@ -1724,6 +1726,29 @@ static int ensure_ws(sgb_plan *p) {
     SGB_CUDA(cudaDeviceSynchronize());  // the non-blocking ws_stream does not order after the legacy stream
   }
   if (!p->d_out && p->n_out) SGB_CUDA(cudaMalloc((void **)&p->d_out, sizeof(double) * (size_t)p->n_out));
+  // a workspace use enqueued by sgb_run_inputs_csr on another stream must finish first
+  if (p->ws_event) SGB_CUDA(cudaStreamWaitEvent(p->ws_stream, p->ws_event, 0));
+  return 0;
+}
+
+// Device inputs -> device CSR values (the inputs -> CSR shape), through the
+// plan's own value-array workspace: stream-ordered, no host synchronisation.
+int sgb_run_inputs_csr(sgb_plan *p, const double *inputs, double *out, void *stream) {
+  if (!p || (!inputs && p->n_in) || (!out && p->n_out)) return fail(-1, "sgb_run_inputs_csr: null argument");
+  if (!p->n_out) return 0;
+  std::lock_guard<std::mutex> lk(p->ws_mu);
+  int rc = ensure_ws(p);
+  if (rc) return rc;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (p->ws_event) SGB_CUDA(cudaStreamWaitEvent(s, p->ws_event, 0));
+  if ((p->needs_zero == 2 || (p->needs_zero == 1 && p->ws_dirty)) && p->vas > p->n_in)
+    SGB_CUDA(cudaMemsetAsync(p->d_x + p->n_in, 0, sizeof(double) * (size_t)(p->vas - p->n_in), s));
+  p->ws_dirty = false;
+  if (p->n_in)
+    SGB_CUDA(cudaMemcpyAsync(p->d_x, inputs, sizeof(double) * (size_t)p->n_in, cudaMemcpyDeviceToDevice, s));
+  if ((rc = sgb_run_csr(p, p->d_x, out, s))) return rc;
+  if (!p->ws_event) SGB_CUDA(cudaEventCreateWithFlags(&p->ws_event, cudaEventDisableTiming));
+  SGB_CUDA(cudaEventRecord(p->ws_event, s));
   return 0;
 }
 

@@ -106,7 +106,7 @@ SYMBOLS = (
     "sgb_plan_create", "sgb_plan_destroy", "sgb_run_values", "sgb_run_csr", "sgb_gather_outputs",
     "sgb_sg_run", "sgb_run_outputs_host", "sgb_run_outputs_host_many", "sgb_run_batch", "sgb_run_batch_csr", "sgb_gather_outputs_batch",
     "sgb_plan_waves", "sgb_last_error", "sgb_run_wave", "sgb_plan_units", "sgb_plan_set_tiles",
-    "sgb_plan_set_wave_grid", "sgb_plan_value_slots",
+    "sgb_plan_set_wave_grid", "sgb_plan_value_slots", "sgb_run_inputs_csr",
 )
 
 
@@ -140,6 +140,7 @@ def load_library(path: Path | str | None = None):
             "sgb_plan_set_tiles": (i32, [vp, vp, i64]),
             "sgb_plan_set_wave_grid": (i32, [vp, i32, i32]),
             "sgb_plan_value_slots": (i64, [vp]),
+            "sgb_run_inputs_csr": (i32, [vp, vp, vp, vp]),
             "sgb_last_error": (ctypes.c_char_p, []),
         }
         for name, (res, args) in sig.items():
@@ -410,6 +411,22 @@ class DevicePlan:
         self._check_tensor(out, self.n_outputs, "out")
         _check(self._lib.sgb_run_csr(self._handle, ctypes.c_void_p(x.data_ptr()), ctypes.c_void_p(out.data_ptr()),
                                      _stream_handle(stream)), "sgb_run_csr")
+        return out
+
+    def run_inputs_csr(self, inputs, out=None, stream=None):
+        """Device inputs [input_count] -> CSR values [n_outputs] through the plan's own workspace
+        (sgb_run_inputs_csr; no value array on the caller's side)."""
+        import torch
+
+        if not isinstance(inputs, torch.Tensor) or inputs.dtype != torch.float64 or not inputs.is_cuda \
+                or not inputs.is_contiguous() or inputs.numel() != self.input_count:
+            raise ValueError(f"inputs must be a contiguous float64 CUDA tensor of {self.input_count} values")
+        if out is None:
+            out = torch.empty(self.n_outputs, dtype=torch.float64, device=inputs.device)
+        self._check_tensor(out, self.n_outputs, "out")
+        _check(self._lib.sgb_run_inputs_csr(self._handle, ctypes.c_void_p(inputs.data_ptr()),
+                                            ctypes.c_void_p(out.data_ptr()), _stream_handle(stream)),
+               "sgb_run_inputs_csr")
         return out
 
     def capture_csr(self, x, out, batch: bool = False):

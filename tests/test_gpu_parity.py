@@ -172,6 +172,14 @@ def test_outputs_host_many(golden):
     dp.run_batch_outputs_host(hin, hout)
     for k in range(6):
         assert np.array_equal(bits(hout[k // 2, :, k % 2].numpy()), bits(dp.run_outputs_host(sets[k])))
+    # device inputs -> device CSR values through the plan's own workspace (sgb_run_inputs_csr), on a
+    # side stream, interleaved with the host-buffer path that shares the workspace
+    s = torch.cuda.Stream()
+    for k in (1, 3, 0):
+        with torch.cuda.stream(s):
+            o = dp.run_inputs_csr(torch.from_numpy(ins[k]).cuda(), stream=s)
+        s.synchronize()
+        assert np.array_equal(bits(o.cpu().numpy()), bits(dp.run_outputs_host(ins[k])))
 
 
 def test_interpret_plan_outputs(golden):
