@@ -564,7 +564,8 @@ def measure_eval(cfg: str, args, rank: int, world: int, barrier, split=None) -> 
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None, "kernel": traffic[dom].name, "algorithmic_bytes": traffic[dom].bytes,
                      "avg_launch_ms": float(per_launch[dom]), "peak_source": peak_src,
-                     "traffic_note": "ncu dram bytes per launch are in profiles/ (not measurable in a timed run)",
+                     "traffic_note": ("not measurable in a timed run: ncu --set full DRAM bytes per launch of "
+                                      "this kernel are in profiles/r2/ncu_full_*.txt"),
                      "whole_evaluation": {"balg_bytes": int(balg), "achieved": whole, "frac": whole / peak,
                                           "definition": "SURVEY 8(d) single-pass B_alg of the plan / ms_per_step"}},
         "launches": [{"name": t.name, "ms": float(m), "alg_bytes": t.bytes,
