@@ -787,8 +787,8 @@ def _window_members(plan, lowered, opos, n_waves):
     return members
 
 
-WIN_ROWS = 240  # anchor instances per CSR window (block of JIT_BLOCK threads: 16 lanes of slack)
-WIN_MAX = 6144  # outputs per CSR window (48 KB of shared memory; 7936 measured 3 % slower on C2, r2o)
+WIN_ROWS = 256  # anchor instances per CSR window = JIT_BLOCK: one pass, no idle lanes (240: 0.1253 ms, 256: 0.1212, r3e)
+WIN_MAX = 6656  # outputs per CSR window (52 KB of shared memory: 3 windows per SM; sized for 256 rows of C2, r3e)
 WIN_MIN = 1024  # windows are not cut shorter than this unless the anchor forces it
 WIN_SLOTS = 148 * 3  # windows resident at once (B200 SMs x the window kernel's blocks per SM)
 WIN_BALANCE_ROUNDS = 4  # ... always below this many rounds (plan shards, small plans: a partial round is a big tail)

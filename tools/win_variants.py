@@ -30,10 +30,9 @@ def main():
     ins = bench.workload_inputs("c2", ns, 0)
     ref = DevicePlan(plan, lowered=lower_plan(plan, csr_window=False))
     want = ref.run_csr(ref.new_values(ins)).cpu().numpy()
-    variants = [dict(rows=r_, winmax=m_, wbulk=False) for r_, m_ in
-                ((240, 6144), (256, 6656), (248, 6400), (272, 7040), (240, 6144), (256, 6656))]
+    variants = [dict(loads=lo, wbulk=False) for lo in (32, 28, 36, 32)]
     for v in variants:
-        lower.WIN_ROWS, lower.WIN_MAX = v["rows"], v["winmax"]
+        jit.WINDOW_LOADS = v["loads"]
         t0 = time.perf_counter()
         lw = lower_plan(plan, csr_window=True, wbulk=v["wbulk"])
         if lw.wbulk is not None:
