@@ -37,8 +37,8 @@ import numpy as np
 from .plan import EXACT_OPS, OpKind, reachable, slot_addresses, unique_addresses
 
 # ops the device reproduces bit for bit: the reference's _EXACT_OPS (codegen.py:43-53) and SIN / COS /
-# EXP / LOG / POW (glibc's algorithms restated, csrc/glibc_math.h; SIN / COS for |x| < 105414350,
-# beyond which glibc's Payne-Hanek reduction is replaced by CUDA's -- within 1e-12)
+# EXP / LOG / POW (glibc's algorithms restated, csrc/glibc_math.h, __branred's large-argument
+# reduction included)
 DEVICE_EXACT_OPS = frozenset(EXACT_OPS) | {int(OpKind.SIN), int(OpKind.COS), int(OpKind.LOG), int(OpKind.EXP),
                                            int(OpKind.POW)}
 KIND_TAPE, KIND_SOP = 0, 1

@@ -473,8 +473,9 @@ def test_device_transcendentals_match_glibc_bitwise(op, jit):
     elif op == "exp":
         xs, kind, k, fn = np.concatenate([g.exp_samples(n, seed=12), [0.0, -math.inf, math.inf, 709.8, -746.0]]), \
             OpKind.EXP, None, math.exp
-    elif op in ("sin", "cos"):  # glibc's bit-exact range, |x| < 105414350
-        xs = np.concatenate([g.sincos_samples(n, seed=13), [0.0, -0.0, 1e-300, 2.426265, 105414349.0]])
+    elif op in ("sin", "cos"):  # the whole finite range (glibc's __branred beyond 105414350)
+        xs = np.concatenate([g.sincos_samples(n, seed=13), [0.0, -0.0, 1e-300, 2.426265, 105414349.0,
+                                                             105414350.0, -1e22, 1.7976931348623157e308]])
         kind, k, fn = (OpKind.SIN, None, math.sin) if op == "sin" else (OpKind.COS, None, math.cos)
     else:
         k = int(op[3:])

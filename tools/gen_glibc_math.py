@@ -14,8 +14,8 @@ optimized-routines algorithms (sysdeps/ieee754/dbl-64/e_log.c, e_exp.c, e_pow.c)
 * sin / cos: the IBM Accurate Mathematical Library (s_sin.c): Taylor series below 0.126, the
   __sincostab table (sin, cos of multiples of 1/128 as hi + lo pairs) with short polynomials
   below 0.855, pi/2 - |x| as a hi + lo pair up to 2.426, a 3-part Cody-Waite reduction by pi/2
-  below 105414350.  Larger arguments need glibc's __branred (a 1200-bit 2/pi table); the device
-  uses CUDA's sin / cos there (documented; the generator checks the bit-exact range only).
+  below 105414350, glibc's __branred beyond (branred.c: x split in two 27-bit halves, each
+  multiplied by six 24-bit chunks of 2/pi from the toverp table, compiled without FMA).
 
 On x86-64 with FMA glibc runs its FMA builds (ifunc), compiled with GCC's default floating-point
 contraction: a product whose value has a single use in an addition is fused -- the Python
@@ -86,7 +86,9 @@ def read_tables(path: Path) -> dict:
     # __sincostab: (sin, sin tail, cos, cos tail) of k/128, k = 0..109, starting (0, 0, 1, 0)
     first = struct.pack("<5d", 0.0, 0.0, 1.0, 0.0, math.sin(1 / 128))
     so = _find(data, first, lambda o: True)
-    return {"sincostab": d(so, 440), "log_poly": v[2:7], "log_poly1": v[7:18], "log_tab": v[18:18 + 2 * N_TAB],
+    # __branred's toverp[75]: 2/pi in 24-bit chunks as doubles (0xA2F983, 0x6E4E44, 0x1529FC, ...)
+    to = _find(data, struct.pack("<3d", 10680707.0, 7228996.0, 1387004.0), lambda o: True)
+    return {"toverp": d(to, 75), "sincostab": d(so, 440), "log_poly": v[2:7], "log_poly1": v[7:18], "log_tab": v[18:18 + 2 * N_TAB],
             "pow_poly": pv[2:9], "pow_tab": pv[9:9 + 4 * N_TAB],
             "exp_shift": ev[1], "exp_negln2hiN": ev[2], "exp_negln2loN": ev[3], "exp_poly": ev[4:8],
             "exp_tab": etab}
@@ -388,7 +390,75 @@ def restated_sin(x, t):
     if k < SINCOS_MAX_HI:
         n, a, da = _reduce(x)
         return _do_sincos(a, da, n, tab)
-    raise ValueError("outside the bit-exact range")
+    if k < 0x7FF00000:
+        n, a, da = _branred(x, t)
+        return _do_sincos(a, da, n, tab)
+    return x / x if x == x else x
+
+
+# branred.h constants (the reduction of s_sin.c for |x| >= 105414350; compiled without FMA)
+BRANRED_K = {k: float.fromhex(v) for k, v in {
+    "TM600": "0x1p-600", "TM24": "0x1p-24", "T576": "0x1p576", "BIG": "0x1.8p52", "BIG1": "0x1.8p54",
+    "SPLIT": "0x1.0000002p27", "HP0": "0x1.921fb54442d18p0", "HP1": "0x1.1a62633145c07p-54",
+    "MP1": "0x1.921fb58000000p0", "MP2": "-0x1.dde9740000000p-27"}.items()}
+
+
+def _branred_half(xh, toverp):
+    K = BRANRED_K
+    k = (_u64(xh) >> 52) & 2047
+    k = max((k - 450) // 24 if k >= 450 else 0, 0)  # C division truncates toward zero; k < 0 -> 0
+    gor = _f64(_u64(K["T576"]) - ((k * 24) << 52))
+    r = []
+    for i in range(6):
+        r.append((xh * toverp[k + i]) * gor)
+        gor *= K["TM24"]
+    sm = 0.0
+    for i in range(3):
+        s_ = (r[i] + K["BIG"]) - K["BIG"]
+        sm += s_
+        r[i] -= s_
+    t_ = 0.0
+    for i in range(6):
+        t_ += r[5 - i]
+    bb = (((((r[0] - t_) + r[1]) + r[2]) + r[3]) + r[4]) + r[5]
+    s_ = (t_ + K["BIG"]) - K["BIG"]
+    sm += s_
+    t_ -= s_
+    b = t_ + bb
+    bb = (t_ - b) + bb
+    s_ = (sm + K["BIG1"]) - K["BIG1"]
+    sm -= s_
+    return b, bb, sm
+
+
+def _branred(x, t):
+    """glibc's __branred (branred.c): x mod pi/2 as a + aa and the quadrant, for |x| >= 105414350."""
+    K = BRANRED_K
+    x *= K["TM600"]
+    tt = x * K["SPLIT"]
+    x1 = tt - (tt - x)
+    x2 = x - x1
+    b1, bb1, sum1 = _branred_half(x1, t["toverp"])
+    b2, bb2, sum2 = _branred_half(x2, t["toverp"])
+    sm = sum1 + sum2
+    b = b1 + b2
+    bb = (b1 - b) + b2 if abs(b1) > abs(b2) else (b2 - b) + b1
+    if b > 0.5:
+        b -= 1.0
+        sm += 1.0
+    elif b < -0.5:
+        b += 1.0
+        sm -= 1.0
+    s_ = b + (bb + bb1 + bb2)
+    tt = ((b - s_) + bb) + (bb1 + bb2)
+    b = s_ * K["SPLIT"]
+    t1 = b - (b - s_)
+    t2 = s_ - t1
+    b = s_ * K["HP0"]
+    bb = (((t1 * K["MP1"] - b) + t1 * K["MP2"]) + t2 * K["MP1"]) + (t2 * K["MP2"] + s_ * K["HP1"] + tt * K["HP0"])
+    s_ = b + bb
+    tt = (b - s_) + bb
+    return int(sm) & 3, s_, tt
 
 
 def restated_cos(x, t):
@@ -406,14 +476,19 @@ def restated_cos(x, t):
     if k < SINCOS_MAX_HI:
         n, a, da = _reduce(x)
         return _do_sincos(a, da, n + 1, tab)
-    raise ValueError("outside the bit-exact range")
+    if k < 0x7FF00000:
+        n, a, da = _branred(x, t)
+        return _do_sincos(a, da, n + 1, tab)
+    return x / x if x == x else x
 
 
 def sincos_samples(n: int, seed: int = 3) -> np.ndarray:
     rng = np.random.default_rng(seed)
     q = n // 5
+    r = n - 4 * q
+    big = np.sign(rng.uniform(-1, 1, r // 2)) * 10 ** rng.uniform(8.03, 308.2, r // 2)  # __branred's range
     return np.concatenate([rng.uniform(-2.5, 2.5, q), rng.uniform(-0.2, 0.2, q), rng.uniform(-100, 100, q),
-                           rng.uniform(-1.05e8, 1.05e8, q), rng.uniform(-1e-7, 1e-7, n - 4 * q)])
+                           rng.uniform(-1.05e8, 1.05e8, q), rng.uniform(-1e-7, 1e-7, r - r // 2), big])
 
 
 # -- verification ----------------------------------------------------------------------------------
@@ -498,6 +573,8 @@ def _arr(vals) -> str:
 
 def header(t: dict, source: str) -> str:
     K = {k: _lit(v) for k, v in SINCOS_K.items()}
+    BR = {k: _lit(v) for k, v in BRANRED_K.items()}
+    toverp = ",\n".join("    " + ", ".join(_lit(v) for v in t["toverp"][j: j + 5]) for j in range(0, 75, 5))
     sct = ",\n".join("    " + ", ".join(_lit(v) for v in t["sincostab"][j: j + 4]) for j in range(0, 440, 4))
     log_rows = ",\n".join(f"    {_lit(t['log_tab'][2 * j])}, {_lit(t['log_tab'][2 * j + 1])}" for j in range(N_TAB))
     pow_rows = ",\n".join(f"    {_lit(t['pow_tab'][4 * j])}, {_lit(t['pow_tab'][4 * j + 2])}, "
@@ -508,7 +585,7 @@ def header(t: dict, source: str) -> str:
 //
 // sgb_log / sgb_exp / sgb_pow / sgb_sin / sgb_cos: glibc 2.39's log, exp and pow (the ARM
 // optimized-routines algorithms, sysdeps/ieee754/dbl-64/e_log.c, e_exp.c, e_pow.c) and sin / cos (the
-// IBM library, s_sin.c; |x| < 105414350) restated for the device, FMA build (x86-64 glibc selects it by
+// IBM library, s_sin.c, with __branred) restated for the device, FMA build (x86-64 glibc selects it by
 // ifunc; GCC fuses every product whose value has a single use in an addition).  The reference
 // evaluates LOG / EXP / POW / SIN / COS with Python's math module, i.e. these functions
 // (codegen.py:545-557), so such templates are bit-exact on the device.  The tables are glibc's
@@ -715,7 +792,7 @@ __device__ __forceinline__ double sgb_pow(double x, double y) {{
   return sgb_exp_core(ehi, elo, sign_bias, true);
 }}
 
-// ---- sin / cos (s_sin.c, FMA build), |x| < 105414350; beyond: CUDA's sin / cos ----
+// ---- sin / cos (s_sin.c, FMA build; __branred for |x| >= 105414350) ----
 __device__ const double sgb_sincostab[440] = {{  // (sin, sin tail, cos, cos tail) of k/128
 {sct}}};
 #define SGB_SC_BIG {K['BIG']}
@@ -765,6 +842,76 @@ __device__ __forceinline__ unsigned sgb_reduce(double x, double &a, double &da) 
   return (unsigned)sgb_as_u64(t) & 3u;
 }}
 
+// __branred (branred.c, no FMA): |x| >= 105414350 reduced by pi/2 with 2/pi in 24-bit chunks
+__device__ const double sgb_toverp[75] = {{
+{toverp}}};
+
+__device__ __noinline__ void sgb_branred_half(double xh, double &b_, double &bb_, double &sm_) {{
+  const unsigned e = (unsigned)(sgb_as_u64(xh) >> 52) & 2047u;
+  const int k = e >= 450u ? (int)((e - 450u) / 24u) : 0;
+  double gor = sgb_as_double(sgb_as_u64({BR['T576']}) - ((unsigned long long)(k * 24) << 52));
+  double r[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) {{
+    r[i] = __dmul_rn(__dmul_rn(xh, sgb_toverp[k + i]), gor);
+    gor = __dmul_rn(gor, {BR['TM24']});
+  }}
+  double sm = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {{
+    const double s = __dsub_rn(__dadd_rn(r[i], {BR['BIG']}), {BR['BIG']});
+    sm = __dadd_rn(sm, s);
+    r[i] = __dsub_rn(r[i], s);
+  }}
+  double t = 0.0;
+#pragma unroll
+  for (int i = 0; i < 6; ++i) t = __dadd_rn(t, r[5 - i]);
+  double bb = __dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dadd_rn(__dsub_rn(r[0], t), r[1]), r[2]), r[3]), r[4]), r[5]);
+  double s = __dsub_rn(__dadd_rn(t, {BR['BIG']}), {BR['BIG']});
+  sm = __dadd_rn(sm, s);
+  t = __dsub_rn(t, s);
+  const double b = __dadd_rn(t, bb);
+  bb = __dadd_rn(__dsub_rn(t, b), bb);
+  s = __dsub_rn(__dadd_rn(sm, {BR['BIG1']}), {BR['BIG1']});
+  b_ = b;
+  bb_ = bb;
+  sm_ = __dsub_rn(sm, s);
+}}
+
+__device__ __noinline__ unsigned sgb_branred(double x, double &a, double &da) {{
+  x = __dmul_rn(x, {BR['TM600']});
+  const double tt = __dmul_rn(x, {BR['SPLIT']});
+  const double x1 = __dsub_rn(tt, __dsub_rn(tt, x));
+  const double x2 = __dsub_rn(x, x1);
+  double b1, bb1, s1, b2, bb2, s2;
+  sgb_branred_half(x1, b1, bb1, s1);
+  sgb_branred_half(x2, b2, bb2, s2);
+  double sm = __dadd_rn(s1, s2);
+  double b = __dadd_rn(b1, b2);
+  double bb = fabs(b1) > fabs(b2) ? __dadd_rn(__dsub_rn(b1, b), b2) : __dadd_rn(__dsub_rn(b2, b), b1);
+  if (b > 0.5) {{
+    b = __dsub_rn(b, 1.0);
+    sm = __dadd_rn(sm, 1.0);
+  }} else if (b < -0.5) {{
+    b = __dadd_rn(b, 1.0);
+    sm = __dsub_rn(sm, 1.0);
+  }}
+  double s = __dadd_rn(b, __dadd_rn(__dadd_rn(bb, bb1), bb2));
+  double t = __dadd_rn(__dadd_rn(__dsub_rn(b, s), bb), __dadd_rn(bb1, bb2));
+  b = __dmul_rn(s, {BR['SPLIT']});
+  const double t1 = __dsub_rn(b, __dsub_rn(b, s));
+  const double t2 = __dsub_rn(s, t1);
+  b = __dmul_rn(s, {BR['HP0']});
+  bb = __dadd_rn(__dadd_rn(__dadd_rn(__dsub_rn(__dmul_rn(t1, {BR['MP1']}), b), __dmul_rn(t1, {BR['MP2']})),
+                           __dmul_rn(t2, {BR['MP1']})),
+                 __dadd_rn(__dadd_rn(__dmul_rn(t2, {BR['MP2']}), __dmul_rn(s, {BR['HP1']})), __dmul_rn(t, {BR['HP0']})));
+  s = __dadd_rn(b, bb);
+  t = __dadd_rn(__dsub_rn(b, s), bb);
+  a = s;
+  da = t;
+  return (unsigned)(int)sm & 3u;
+}}
+
 __device__ __forceinline__ double sgb_do_sincos(double a, double da, unsigned n) {{
   const double r = (n & 1u) ? sgb_do_cos(a, da) : (fabs(a) < SGB_SC_SMALL ? sgb_taylor_sin(a, da) : sgb_do_sin(a, da));
   return (n & 2u) ? -r : r;
@@ -780,7 +927,11 @@ __device__ __forceinline__ double sgb_sin(double x) {{
     const unsigned n = sgb_reduce(x, a, da);
     return sgb_do_sincos(a, da, n);
   }}
-  if (k < 0x7ff00000u) return sin(x);  // glibc: __branred; CUDA's reduction here
+  if (k < 0x7ff00000u) {{
+    double a, da;
+    const unsigned n = sgb_branred(x, a, da);
+    return sgb_do_sincos(a, da, n);
+  }}
   return __ddiv_rn(x, x);
 }}
 
@@ -799,7 +950,11 @@ __device__ __forceinline__ double sgb_cos(double x) {{
     const unsigned n = sgb_reduce(x, a, da);
     return sgb_do_sincos(a, da, n + 1u);
   }}
-  if (k < 0x7ff00000u) return cos(x);  // glibc: __branred; CUDA's reduction here
+  if (k < 0x7ff00000u) {{
+    double a, da;
+    const unsigned n = sgb_branred(x, a, da);
+    return sgb_do_sincos(a, da, n + 1u);
+  }}
   return __ddiv_rn(x, x);
 }}
 
