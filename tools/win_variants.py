@@ -30,9 +30,9 @@ def main():
     ins = bench.workload_inputs("c2", ns, 0)
     ref = DevicePlan(plan, lowered=lower_plan(plan, csr_window=False))
     want = ref.run_csr(ref.new_values(ins)).cpu().numpy()
-    variants = [dict(loads=lo, wbulk=False) for lo in (32, 28, 36, 32)]
+    variants = [dict(order=o, wbulk=False) for o in ("kernel", "shared", "kernel", "shared")]
     for v in variants:
-        jit.WINDOW_LOADS = v["loads"]
+        lower.WIN_MEMBER_ORDER = v["order"]
         t0 = time.perf_counter()
         lw = lower_plan(plan, csr_window=True, wbulk=v["wbulk"])
         if lw.wbulk is not None:
