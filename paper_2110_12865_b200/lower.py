@@ -791,7 +791,6 @@ WIN_ROWS = 256  # anchor instances per CSR window = JIT_BLOCK: one pass, no idle
 WIN_MAX = 6656  # outputs per CSR window (52 KB of shared memory: 3 windows per SM; sized for 256 rows of C2, r3e)
 WIN_MIN = 1024  # windows are not cut shorter than this unless the anchor forces it
 WIN_SLOTS = 148 * 3  # windows resident at once (B200 SMs x the window kernel's blocks per SM)
-WIN_MEMBER_ORDER = "kernel"  # "shared": members grouped into chunks by the value-array lines they share
 WIN_BALANCE_ROUNDS = 4  # ... always below this many rounds (plan shards, small plans: a partial round is a big tail)
 WIN_BALANCE = False  # cut whole rounds of resident windows (lower_plan): C2 window 0.1275 -> 0.1292 ms, off (r2v)
 WIN_MAX_LOADS = 32  # default lowering: windows only when every member loads at most this many slots
@@ -1166,44 +1165,6 @@ def split_roots(tape: np.ndarray, n_roots: int, k: int, seed: int = 0, rounds: i
     return keeps
 
 
-def _first_addresses(g) -> set:
-    """Value-array addresses instance 0 of a group loads, at cache-line (8 doubles) granularity."""
-    if not g.n or not g.columns:
-        return set()
-    out = set()
-    for c, d in zip(g.slot_col.tolist(), g.slot_delta.tolist()):
-        a = int(g.columns[0][0]) + int(d) if c < 0 else int(g.columns[c][0])
-        out.add(a >> 3)
-    return out
-
-
-def _shared_stream_order(members: list) -> list:
-    """CSR-window members reordered so each chunk of the window kernel (WINDOW_LOADS loads per thread,
-    jit.window_source) groups members that read the same value-array lines: greedy, seeded by the
-    widest remaining member, then the member sharing the most lines with the chunk so far."""
-    from . import jit as _jit
-
-    lines = [_first_addresses(g) for g in members]
-    width = [max(1, len(g.slot_col) + g.n_const) for g in members]
-    left = list(range(len(members)))
-    order = []
-    while left:
-        seed = max(left, key=lambda j: (width[j], -j))
-        chunk, used, w = [seed], set(lines[seed]), width[seed]
-        left.remove(seed)
-        while True:
-            fit = [j for j in left if w + width[j] <= _jit.WINDOW_LOADS]
-            if not fit:
-                break
-            j = max(fit, key=lambda j: (len(lines[j] & used), -j))
-            chunk.append(j)
-            used |= lines[j]
-            w += width[j]
-            left.remove(j)
-        order += chunk
-    return [members[j] for j in order]
-
-
 def jit_vec(groups, sel) -> int:
     """Instances per thread of a specialised unit: all of them keep their loads in flight
     together, so small templates take 4, mid-size 2, big element templates 1."""
@@ -1497,8 +1458,6 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                                      window=True))
     windows = None
     if window is not None:
-        if WIN_MEMBER_ORDER == "shared" and len(win_groups) > 2:
-            win_groups = _shared_stream_order(win_groups)
         # members in list order == their order in the window unit (pieces columns)
         mo = [opos[g.kernel] for g in win_groups]
         windows = _csr_windows(mo, len(plan.outputs), res_k, res_addr)

@@ -11,7 +11,7 @@ def main():
     from paper_2110_12865_b200 import jit
 
     args = bench.parse_args(["--config", "c5", "--only", "--no-cpu-baseline", "--steps", "5"])
-    for bvec in (8, 16, 8, 16):
+    for bvec in (8, 4, 2, 16):
         jit.BATCH_VEC = bvec
         line = bench.measure_batched(args, 0, 1, None)
         print(f"batch_vec={bvec} ms {line['ms_per_step']:.4f} parity {line['config'].get('parity')}", flush=True)

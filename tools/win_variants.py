@@ -30,9 +30,9 @@ def main():
     ins = bench.workload_inputs("c2", ns, 0)
     ref = DevicePlan(plan, lowered=lower_plan(plan, csr_window=False))
     want = ref.run_csr(ref.new_values(ins)).cpu().numpy()
-    variants = [dict(order=o, wbulk=False) for o in ("kernel", "shared", "kernel", "shared")]
+    variants = [dict(loads=lo, wbulk=b) for lo, b in ((32, False), (24, False), (32, True))]
     for v in variants:
-        lower.WIN_MEMBER_ORDER = v["order"]
+        jit.WINDOW_LOADS = v["loads"]
         t0 = time.perf_counter()
         lw = lower_plan(plan, csr_window=True, wbulk=v["wbulk"])
         if lw.wbulk is not None:
