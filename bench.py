@@ -727,17 +727,17 @@ def measure_emulated(args, rank: int, world: int, barrier) -> dict:
     import device_plan_emu as emu
 
     from paper_2110_12865_b200 import lower_plan
-    from paper_2110_12865_b200.shard import max_over_ranks, shard_outputs, shard_plan
+    from paper_2110_12865_b200.shard import max_over_ranks, shard_device, shard_outputs, shard_plan
 
     cfg = args.config
     key, plan = build_workload(cfg, args, rank, barrier)
     n_total = len(plan.outputs)
     lo, hi = shard_outputs(n_total, world, rank)
-    slw = lower_plan(shard_plan(plan, lo, hi), jit_compile=False, csr_window=True)
+    _, slw = shard_device(shard_plan(plan, lo, hi), relayout=False, jit_compile=False, csr_window=True)
     inputs = workload_inputs(cfg, args, seed=0, plan=plan)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        mine = emu.run_csr(slw, inputs)
+        mine = emu.run_csr(slw, inputs, by_tiles=True)  # the same tile-filtered shard the GPU path runs
     sec = max_over_ranks((time.perf_counter() - t0) / args.steps)
     width = torch.tensor([hi - lo])
     dist.all_reduce(width, op=dist.ReduceOp.MAX)
