@@ -34,7 +34,6 @@ from __future__ import annotations
 
 import argparse
 import ctypes
-import dataclasses
 import json
 import os
 import pickle
@@ -404,7 +403,7 @@ def measure_eval(cfg: str, args, rank: int, world: int, barrier, split=None) -> 
     import torch
     import torch.distributed as dist
 
-    from paper_2110_12865_b200 import DevicePlan, lower_plan
+    from paper_2110_12865_b200 import DevicePlan
     from paper_2110_12865_b200.metrics import csr_wave_traffic, plan_balg, wave_traffic
 
     local = torch.cuda.current_device()
@@ -726,7 +725,6 @@ def measure_emulated(args, rank: int, world: int, barrier) -> dict:
     sys.path.insert(0, str(ROOT / "tests"))
     import device_plan_emu as emu
 
-    from paper_2110_12865_b200 import lower_plan
     from paper_2110_12865_b200.shard import max_over_ranks, shard_device, shard_outputs, shard_plan
 
     cfg = args.config
