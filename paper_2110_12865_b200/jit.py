@@ -222,7 +222,8 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
                 x_addr = X(f"{int(rec['dest_base']) + r}u + {i} * {int(rec['n_roots'])}u")
             else:
                 x_addr = X(f"{int(rec['dest_base']) + r * n}u + {i}")
-            store = f"st_stream({x_addr}, {v});" if stream else f"*({x_addr}) = {v};"
+            store = (f"st_stream({x_addr}, {v});" if stream else
+                     f"st_keep({x_addr}, {v});" if flags & L.FLAG_KEEP else f"*({x_addr}) = {v};")
             comp.append(f"if (ok{sfx}{' && !csr' if stream else ''}) {store}")
             if _out_pos(rec, r) is not None:
                 dst_o = f"out[(u64)op{r}{sfx} * ld_out + {bv}]" if batched else f"out[op{r}{sfx}]"
@@ -320,6 +321,18 @@ def _stage_out(rec, vec: int, threads: int = JIT_BLOCK) -> list[str]:
             "__syncthreads();"]
 
 
+_KEEP_HELPER = r"""
+#ifndef SGB_KEEP_HELPER
+#define SGB_KEEP_HELPER
+__device__ __forceinline__ void st_keep(double *a, double v) {  // store, L2 evict_last
+  u64 pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+#endif
+"""
+
+
 def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
     """Persistent kernels for tape unit ``u``: a case per group.
 
@@ -329,6 +342,8 @@ def unit_source(dp, u: int, tapes: dict, imms: dict) -> str:
     """
     unit = dp.unit(u)
     out = []
+    if any(int(dp.groups[g]["flags"]) & L.FLAG_KEEP for g in range(unit["group_begin"], unit["group_end"])):
+        out.append(_KEEP_HELPER)
     split = getattr(dp, "jit_split", {}).get(unit["group_begin"]) if unit["group_end"] - unit["group_begin"] == 1 \
         else None
     nthreads = JIT_BLOCK * (len(split) if split else 1)

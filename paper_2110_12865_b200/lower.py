@@ -50,6 +50,7 @@ FLAG_CSR_ONLY = 512  # synthetic copy group: runs in CSR mode only
 FLAG_COHERENT = 1024  # one retained column: every slot is column 0 + delta
 FLAG_IMAJOR = 2048  # CSR layout: result r of instance i at dest_base + i * n_roots + r (specialised units only)
 FLAG_WPOS16 = 4096  # CSR-window member: root r of instance i goes to its window's position ooff[oo_off + r*n + i]
+FLAG_KEEP = 8192  # specialised kernels store its results with an L2 evict_last hint (read soon by the window unit)
 UNIT_CSR_ONLY = 1
 STORE_ROOTS_EARLY = False  # roots stored as soon as computed (True) or at the end: C3 element kernel 0.318 vs 0.291 ms (c3v)
 UNIT_JIT = 2  # tape unit compiled to straight-line code (jit.py), one instance per thread
@@ -791,6 +792,7 @@ WIN_ROWS = 256  # anchor instances per CSR window = JIT_BLOCK: one pass, no idle
 WIN_MAX = 6656  # outputs per CSR window (52 KB of shared memory: 3 windows per SM; sized for 256 rows of C2, r3e)
 WIN_MIN = 1024  # windows are not cut shorter than this unless the anchor forces it
 WIN_SLOTS = 148 * 3  # windows resident at once (B200 SMs x the window kernel's blocks per SM)
+KEEP_BEFORE_WINDOW = False  # results of the wave before the window unit stored with an L2 evict_last hint
 WIN_BALANCE_ROUNDS = 4  # ... always below this many rounds (plan shards, small plans: a partial round is a big tail)
 WIN_BALANCE = False  # cut whole rounds of resident windows (lower_plan): C2 window 0.1275 -> 0.1292 ms, off (r2v)
 WIN_MAX_LOADS = 32  # default lowering: windows only when every member loads at most this many slots
@@ -1744,6 +1746,15 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                 continue
             dp.jit_split[gi] = split_roots(tp, int(dp.groups[gi]["n_roots"]), JIT_SPLIT)
             dp.units[uu, fb] = r["block_size"] * JIT_SPLIT
+    if KEEP_BEFORE_WINDOW and window_units:  # the window unit's operands: keep them in L2
+        fw = UNIT_FIELDS.index("wave")
+        w_win = int(dp.units[window_units[0][0], fw])
+        for uu in range(len(dp.units)):
+            r = dp.unit(uu)
+            if r["wave"] == w_win - 1 and r["flags"] & UNIT_JIT and not r["flags"] & UNIT_WINDOW:
+                for g in range(r["group_begin"], r["group_end"]):
+                    if not dp.groups[g]["flags"] & FLAG_STREAM:
+                        dp.groups[g]["flags"] |= FLAG_KEEP
     dp.wbulk = None
     if wbulk is None:
         wbulk = os.environ.get("SGB_WBULK", "0") == "1"  # measured slower than the register-pipelined windows (r2m)

@@ -30,9 +30,9 @@ def main():
     ins = bench.workload_inputs("c2", ns, 0)
     ref = DevicePlan(plan, lowered=lower_plan(plan, csr_window=False))
     want = ref.run_csr(ref.new_values(ins)).cpu().numpy()
-    variants = [dict(loads=lo, wbulk=b) for lo, b in ((32, False), (24, False), (32, True))]
+    variants = [dict(keep=k_, wbulk=False) for k_ in (False, True, False, True)]
     for v in variants:
-        jit.WINDOW_LOADS = v["loads"]
+        lower.KEEP_BEFORE_WINDOW = v["keep"]
         t0 = time.perf_counter()
         lw = lower_plan(plan, csr_window=True, wbulk=v["wbulk"])
         if lw.wbulk is not None:
