@@ -60,7 +60,8 @@ typedef struct sgb_group {
   int64_t ob_off;    /* output positions (flags & 128): first chunk base in obase */
   int64_t oo_off;    /*   first offset in ooff (flags & 128) or entry in opos32 (flags & 256) */
   int32_t n_roots, n_slots, n_ret, n_const;
-  int32_t tape_len, n_regs, kind, flags;
+  int32_t tape_len, n_regs, kind, flags; /* flags: lower.FLAG_* (8192: the specialised kernel stores with an
+                                             L2 evict_last hint -- code generation only) */
   int32_t slot_off, sop_off, sop_len, unit;
   int32_t variant; /* sum-of-products width class (factors <= 2, 4, 8, 16, 32) */
   int32_t shape;   /* sum-of-products shape: 0 generic, 1 plain sum, 2 two-factor products (+ single tail) */
