@@ -792,6 +792,7 @@ WIN_ROWS = 256  # anchor instances per CSR window = JIT_BLOCK: one pass, no idle
 WIN_MAX = 6656  # outputs per CSR window (52 KB of shared memory: 3 windows per SM; sized for 256 rows of C2, r3e)
 WIN_MIN = 1024  # windows are not cut shorter than this unless the anchor forces it
 WIN_SLOTS = 148 * 3  # windows resident at once (B200 SMs x the window kernel's blocks per SM)
+KEEP_BEFORE_GATHER = False  # gather mode: the last wave's output results stored with an L2 evict_last hint
 KEEP_BEFORE_WINDOW = True  # results of the wave before the window unit stored with an L2 evict_last hint (C2: window 0.1212 -> 0.1183 ms, step -0.6 %, r3m)
 WIN_BALANCE_ROUNDS = 4  # ... always below this many rounds (plan shards, small plans: a partial round is a big tail)
 WIN_BALANCE = False  # cut whole rounds of resident windows (lower_plan): C2 window 0.1275 -> 0.1292 ms, off (r2v)
@@ -1746,6 +1747,21 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                 continue
             dp.jit_split[gi] = split_roots(tp, int(dp.groups[gi]["n_roots"]), JIT_SPLIT)
             dp.units[uu, fb] = r["block_size"] * JIT_SPLIT
+    if KEEP_BEFORE_GATHER and not window_units and not direct_csr and len(plan.outputs):
+        # gather mode: the last wave's output groups' results are what the gather reads next
+        outs_sorted = np.sort(np.asarray(plan.outputs, np.int64))
+        last_w = n_waves - 1
+        for uu in range(len(dp.units)):
+            r = dp.unit(uu)
+            if r["wave"] != last_w or not r["flags"] & UNIT_JIT:
+                continue
+            for g in range(r["group_begin"], r["group_end"]):
+                rec = dp.groups[g]
+                lo = int(rec["dest_base"])
+                hi = lo + int(rec["n_roots"]) * int(rec["n"])
+                a, b = np.searchsorted(outs_sorted, [lo, hi])
+                if b > a and not rec["flags"] & FLAG_STREAM:
+                    dp.groups[g]["flags"] |= FLAG_KEEP
     if KEEP_BEFORE_WINDOW and window_units:  # the window unit's operands: keep them in L2
         fw = UNIT_FIELDS.index("wave")
         w_win = int(dp.units[window_units[0][0], fw])
