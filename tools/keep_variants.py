@@ -12,8 +12,8 @@ def main():
     from paper_2110_12865_b200 import lower
 
     args = bench.parse_args(["--only", "--no-cpu-baseline", "--steps", "20"])
-    for keep in (False, True, False, True):
-        lower.KEEP_BEFORE_WINDOW = keep
+    for keep in (1, 2, 3, 1):
+        lower.KEEP_WAVES = keep
         line = bench.measure_eval("c2", args, 0, 1, None)
         print(f"keep={keep} ms {line['ms_per_step']:.4f} launches "
               f"{[(l_['name'], round(l_['ms'], 4)) for l_ in line['launches']]} parity {line['config'].get('parity')}",
