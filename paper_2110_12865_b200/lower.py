@@ -793,7 +793,7 @@ WIN_MAX = 6656  # outputs per CSR window (52 KB of shared memory: 3 windows per 
 WIN_MIN = 1024  # windows are not cut shorter than this unless the anchor forces it
 WIN_SLOTS = 148 * 3  # windows resident at once (B200 SMs x the window kernel's blocks per SM)
 KEEP_BEFORE_GATHER = True  # gather mode: the last wave's output results stored with an L2 evict_last hint (C3 -0.8 %, C4 -2.8 %, r3o)
-KEEP_WAVES = 1  # how many waves before the window unit keep their results (2: C2 see r3p)
+KEEP_WAVES = 2  # waves before the window unit that keep their results in L2 (C2: 1 0.1777-0.1784, 2 0.1768, 3 0.1788 ms, r3p)
 KEEP_BEFORE_WINDOW = True  # results of the wave before the window unit stored with an L2 evict_last hint (C2: window 0.1212 -> 0.1183 ms, step -0.6 %, r3m)
 WIN_BALANCE_ROUNDS = 4  # ... always below this many rounds (plan shards, small plans: a partial round is a big tail)
 WIN_BALANCE = False  # cut whole rounds of resident windows (lower_plan): C2 window 0.1275 -> 0.1292 ms, off (r2v)
