@@ -222,8 +222,9 @@ def group_parts(dp, gi: int, tape: np.ndarray, imms: list, iv: str = "i", sfx: s
                 x_addr = X(f"{int(rec['dest_base']) + r}u + {i} * {int(rec['n_roots'])}u")
             else:
                 x_addr = X(f"{int(rec['dest_base']) + r * n}u + {i}")
+            # (L2 keep hints for one value set only: a batched wave is hundreds of MB)
             store = (f"st_stream({x_addr}, {v});" if stream else
-                     f"st_keep({x_addr}, {v});" if flags & L.FLAG_KEEP else f"*({x_addr}) = {v};")
+                     f"st_keep({x_addr}, {v});" if flags & L.FLAG_KEEP and not batched else f"*({x_addr}) = {v};")
             comp.append(f"if (ok{sfx}{' && !csr' if stream else ''}) {store}")
             if _out_pos(rec, r) is not None:
                 dst_o = f"out[(u64)op{r}{sfx} * ld_out + {bv}]" if batched else f"out[op{r}{sfx}]"
