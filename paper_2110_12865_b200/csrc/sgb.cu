@@ -1406,8 +1406,10 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       for (const Unit &u : p->units) n += u.wave == w;
       max_units = n > max_units ? n : max_units;
       if (n < 2) continue;
-      for (Unit &u : p->units)  // leave one block per SM to the co-running units
-        if (u.wave == w && u.grid > prop.multiProcessorCount) {
+      // leave one block per SM to the co-running units (not window units: one block per window, and
+      // they run in CSR mode only while their wave's value-mode twins do not)
+      for (Unit &u : p->units)
+        if (u.wave == w && !(u.flags & UNIT_WINDOW) && u.grid > prop.multiProcessorCount) {
           const int64_t cap = u.grid - prop.multiProcessorCount;
           if (cap >= prop.multiProcessorCount) u.grid = cap;
         }
