@@ -1423,6 +1423,9 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
         u.grid_p = u.grid;
         u.grid_t = u.t1 - u.t0 < 0x7fffffffLL ? u.t1 - u.t0 : 0x7fffffffLL;
       }
+    for (const Unit &u : p->units)  // jit.window_source: exactly one block per window, no grid-stride loop
+      if ((u.flags & UNIT_WINDOW) && !(u.flags & UNIT_BULK) && u.grid != u.t1 - u.t0)
+        return fail(-1, "sgb_plan_create: CSR-window grid differs from the window count");
     p->wave_units.assign(max_wave + 1, {});
     for (int k = 0; k < (int)p->units.size(); ++k) p->wave_units[p->units[k].wave].push_back(k);
     const int n_aux = max_units - 1 < 8 ? max_units - 1 : 8;
