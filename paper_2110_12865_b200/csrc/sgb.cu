@@ -1298,7 +1298,8 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
         (!(u.flags & UNIT_WINDOW) && u.t1 > d->n_tiles) ||
         u.t0 > u.t1 || (u.kind != KIND_TAPE && u.kind != KIND_SOP) ||
         (u.kind == KIND_TAPE && !jit && (u.bs != 32 && u.bs != 64 && u.bs != 128)) ||
-        (u.kind == KIND_TAPE && (u.variant != 1 && u.variant != 2 && u.variant != 4)) ||
+        (u.kind == KIND_TAPE && !window && (u.variant != 1 && u.variant != 2 && u.variant != 4)) ||
+        (window && (u.variant < 0 || u.variant > 64)) ||
         (jit ? (int64_t)u.regs : (int64_t)u.regs * (u.kind == KIND_TAPE ? u.bs * u.variant : 0) * 8) > smem_max ||
         u.regs < 0)
       return fail(-1, "sgb_plan_create: bad launch unit " + std::to_string(k));
@@ -1310,7 +1311,12 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
         u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
         if (u.grid > u.t1 - u.t0) u.grid = u.t1 - u.t0;
       } else if (window) {
-        u.grid = u.t1 - u.t0;  // one block per window, dispatched in CSR order
+        // one block per window, dispatched in CSR order, minus `variant` rounds of one block per SM: the
+        // first blocks then take a second window each (grid-stride) -- the last windows start early and
+        // the final round is short (C2: 3757 windows, 0.1273 ms with 3757 blocks, 0.1188 with 3609)
+        u.grid = u.t1 - u.t0;
+        const int64_t cut = (int64_t)u.variant * prop.multiProcessorCount;
+        if (u.grid - cut >= prop.multiProcessorCount) u.grid -= cut;
       } else if (jit) {
         SGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, u.jit, u.bs, (size_t)u.regs));
         u.grid = (int64_t)(nb > 0 ? nb : 1) * prop.multiProcessorCount;
@@ -1406,8 +1412,8 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
       for (const Unit &u : p->units) n += u.wave == w;
       max_units = n > max_units ? n : max_units;
       if (n < 2) continue;
-      // leave one block per SM to the co-running units (not window units: one block per window, and
-      // they run in CSR mode only while their wave's value-mode twins do not)
+      // leave one block per SM to the co-running units (not window units: they run in CSR mode only
+      // while their wave's value-mode twins do not; their grid is chosen above)
       for (Unit &u : p->units)
         if (u.wave == w && !(u.flags & UNIT_WINDOW) && u.grid > prop.multiProcessorCount) {
           const int64_t cap = u.grid - prop.multiProcessorCount;
@@ -1423,9 +1429,6 @@ static int create_impl(const sgb_plan_desc *d, int device, sgb_plan *p) {
         u.grid_p = u.grid;
         u.grid_t = u.t1 - u.t0 < 0x7fffffffLL ? u.t1 - u.t0 : 0x7fffffffLL;
       }
-    for (const Unit &u : p->units)  // jit.window_source: exactly one block per window, no grid-stride loop
-      if ((u.flags & UNIT_WINDOW) && !(u.flags & UNIT_BULK) && u.grid != u.t1 - u.t0)
-        return fail(-1, "sgb_plan_create: CSR-window grid differs from the window count");
     p->wave_units.assign(max_wave + 1, {});
     for (int k = 0; k < (int)p->units.size(); ++k) p->wave_units[p->units[k].wave].push_back(k);
     const int n_aux = max_units - 1 < 8 ? max_units - 1 : 8;

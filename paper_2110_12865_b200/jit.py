@@ -532,9 +532,7 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
            "  extern __shared__ __align__(16) double buf[];",
            f"  __shared__ int2 sp[{J}];",
            "  const int tid = threadIdx.x;",
-           "  {  // one block per window (grid = n_win): no loop, no trailing barrier",
-           "    const i64 w = blockIdx.x;",
-           "    if (w >= n_win) return;",
+           "  for (i64 w = blockIdx.x; w < n_win; w += gridDim.x) {",
            f"    for (int j = tid; j < {J}; j += {B}) sp[j] = __ldg(pieces + w * {J} + j);",
            "    const i64 k0 = __ldg(win_k + w);",
            "    const u32 len_ = (u32)(__ldg(win_k + w + 1) - k0);",
@@ -594,6 +592,7 @@ def window_source(dp, u: int, tapes: dict, imms: dict) -> str:
             "      }",
             "      if (tid == 0 && (tot_ & 1u)) __stcs(out + k0 + len_ - 1, buf[tot_ - 1]);",
             "    }",
+            "    if (w + gridDim.x < n_win) __syncthreads();  // the window buffer is reused (uniform)",
             "  }",
             "}",
             ""]

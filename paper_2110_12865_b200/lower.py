@@ -792,6 +792,7 @@ WIN_ROWS = 256  # anchor instances per CSR window = JIT_BLOCK: one pass, no idle
 WIN_MAX = 6656  # outputs per CSR window (52 KB of shared memory: 3 windows per SM; sized for 256 rows of C2, r3e)
 WIN_MIN = 1024  # windows are not cut shorter than this unless the anchor forces it
 WIN_SLOTS = 148 * 3  # windows resident at once (B200 SMs x the window kernel's blocks per SM)
+WIN_GRID_CUT = 1  # window unit grid = n_win - WIN_GRID_CUT x 148 blocks (sgb.cu)
 KEEP_BEFORE_GATHER = True  # gather mode: the last wave's output results stored with an L2 evict_last hint (C3 -0.8 %, C4 -2.8 %, r3o)
 KEEP_WAVES = 2  # waves before the window unit that keep their results in L2 (C2: 1 0.1777-0.1784, 2 0.1768, 3 0.1788 ms, r3p)
 KEEP_BEFORE_WINDOW = True  # results of the wave before the window unit stored with an L2 evict_last hint (C2: window 0.1212 -> 0.1183 ms, step -0.6 %, r3m)
@@ -1654,10 +1655,11 @@ def lower_plan(plan, compress: bool | None = None, direct_csr: bool | None = Non
                 n_win = windows.k.size - 1
                 window_units.append((len(units), 0, n_win))
                 smem = 8 * (int(np.diff(windows.k).max(initial=0)) + 2)  # + alignment slots
-                # one block per window, dispatched in CSR order (a persistent grid prefetching the next
-                # window's header measured 0.1274 -> 0.1725 ms on C2: concurrently running windows drift
-                # apart and stop sharing the L2-resident intermediates, r2x)
-                units.append((w, kind, variant, g_begin, len(order_groups), 0, n_win, bs, smem,
+                # about one block per window, dispatched in CSR order: variant = rounds of one block per
+                # SM cut from the grid (sgb.cu; the first blocks take a second window).  (A persistent grid
+                # prefetching the next window's header measured 0.1274 -> 0.1725 ms on C2: concurrently
+                # running windows drift apart and stop sharing the L2-resident intermediates, r2x)
+                units.append((w, kind, WIN_GRID_CUT, g_begin, len(order_groups), 0, n_win, bs, smem,
                               UNIT_CSR_ONLY | UNIT_JIT | UNIT_WINDOW))
                 jit_units.append(len(units) - 1)
                 continue

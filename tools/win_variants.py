@@ -30,9 +30,9 @@ def main():
     ins = bench.workload_inputs("c2", ns, 0)
     ref = DevicePlan(plan, lowered=lower_plan(plan, csr_window=False))
     want = ref.run_csr(ref.new_values(ins)).cpu().numpy()
-    variants = [dict(keep=k_, wbulk=False) for k_ in (False, True, False, True)]
+    variants = [dict(cut=c_, wbulk=False) for c_ in (1, 0, 2, 4, 8, 1)]
     for v in variants:
-        lower.KEEP_BEFORE_WINDOW = v["keep"]
+        lower.WIN_GRID_CUT = v["cut"]
         t0 = time.perf_counter()
         lw = lower_plan(plan, csr_window=True, wbulk=v["wbulk"])
         if lw.wbulk is not None:
